@@ -1,0 +1,331 @@
+#!/usr/bin/env python3
+"""Benchmark: 20-iteration Jacobi-CG solve on a constant-coefficient Laplacian.
+
+Metric (BASELINE.json): "20-iter Jacobi-CG solve time, achieved HBM GB/s vs
+peak, host syncs/iter".  One STEP = one full solve (setup residual + 20 CG
+iterations, PAPER.md:46-65 timing loop; assembly and the Jacobi setup are
+outside, as in the reference's KSPSolve timing).  Headline workload: 3D
+7-point 256^3 (BASELINE.json north_star target) on one B200.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 7pt256]
+  python bench.py --impl reference ...   # the reference CPU solver (oracle/_ref)
+
+Prints ONE JSON line on rank 0.  Diagnostics go to stderr.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (dim, points, grid, description)
+    "5pt1024": (2, 5, (1024, 1024), "2D 5-point Laplacian 1024x1024"),
+    "9pt4096": (2, 9, (4096, 4096), "2D 9-point Laplacian 4096x4096"),
+    "7pt256": (3, 7, (256, 256, 256), "3D 7-point Laplacian 256^3"),
+    "27pt256": (3, 27, (256, 256, 256), "3D 27-point Laplacian 256^3"),
+    "7pt768": (3, 7, (768, 768, 768), "3D 7-point Laplacian 768^3"),
+    "5pt64": (2, 5, (64, 64), "2D 5-point Laplacian 64x64 (latency sweep)"),
+    "5pt128": (2, 5, (128, 128), "2D 5-point Laplacian 128x128 (latency sweep)"),
+    "5pt256": (2, 5, (256, 256), "2D 5-point Laplacian 256x256 (latency sweep)"),
+    "5pt512": (2, 5, (512, 512), "2D 5-point Laplacian 512x512 (latency sweep)"),
+}
+METRIC = "20-iter Jacobi-CG solve time, achieved HBM GB/s vs peak, host syncs/iter"
+MAX_IT = 20
+L2_BYTES = 126 * 2 ** 20
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy kernel)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def bytes_model(n: int, nnz: int):
+    """Algorithmic HBM bytes.  All FP64 + int64 offsets + int32 cols."""
+    k1 = 12 * nnz + 8 * (n + 1) + 32 * n        # off, cols, vals, z, p_old -> p_new, w
+    k2 = 64 * n                                  # x, p, r, w, dinv -> x, r, z
+    b_min = k1 + k2                              # = 12 nnz + 8 (n+1) + 96 n
+    b_ref = 12 * nnz + 8 * (n + 1) + 152 * n     # reference's unfused sequence
+    setup = 64 * n
+    return {"k1": k1, "k2": k2, "b_min_iter": b_min, "b_ref_iter": b_ref,
+            "b_min_solve": MAX_IT * b_min + setup, "b_ref_solve": MAX_IT * b_ref + setup,
+            "flops_iter": 2 * nnz + 13 * n}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.p = None
+        self.path = os.path.join("/tmp", f"rvk_clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        try:
+            self.f = open(self.path, "w")
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
+        except Exception:
+            self.p = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.p:
+            time.sleep(0.2)
+            self.p.terminate()
+            self.p.wait()
+            self.f.close()
+
+    def summary(self):
+        if not self.p or not os.path.exists(self.path):
+            return None
+        rows = [r.split(",") for r in open(self.path).read().strip().splitlines() if r.strip()]
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                sm.append(float(r[1]))
+                smax = float(r[2])
+                for name, v in zip(names, r[5:9]):
+                    if v.strip() == "Active":
+                        reasons.add(name)
+            except (ValueError, IndexError):
+                continue
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def ncu_traffic(config: str):
+    """DRAM bytes per K1 launch from the committed `ncu --set full` summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        d = json.load(f)
+    k = d.get(config, {}).get("k1")
+    return k.get("dram_bytes") if k else None
+
+
+def cpu_baseline(dim, pts, grid, steps=1):
+    """The reference's own kernels (oracle/_ref, kernels_scalar.cpp via dispatch)
+    running the restated PCG, 1 host thread (the kernels are single-threaded).
+    Sample = `steps` full 20-iteration solves of the SAME workload."""
+    import oracle as O
+    kind = "reference" if O.ref_available() else "port"
+    A = O.build_laplacian(dim, pts, grid)
+    b = O.rhs(A.n_rows)
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        if kind == "reference":
+            O.ref_cg_solve(A, b, max_it=MAX_IT, backend=2)   # reference auto dispatch
+        else:
+            O.cg_solve(A, b, max_it=MAX_IT)
+        times.append((time.perf_counter() - t0) * 1e3)
+    return kind, times, A
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    dim, pts, grid, desc = cfg
+    t_all = time.perf_counter()
+    import oracle as O
+    kind = "reference" if O.ref_available() else "port"
+    A = O.build_laplacian(dim, pts, grid)
+    b = O.rhs(A.n_rows)
+    solve = (lambda: O.ref_cg_solve(A, b, max_it=MAX_IT, backend=2)) if kind == "reference" \
+        else (lambda: O.cg_solve(A, b, max_it=MAX_IT))
+    for _ in range(args.warmup):
+        solve()
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        solve()
+        times.append((time.perf_counter() - t0) * 1e3)
+    ms = statistics.mean(times)
+    bm = bytes_model(A.n_rows, A.nnz)
+    out = {
+        "metric": METRIC, "impl": "reference", "value": round(ms, 3), "unit": "ms/solve",
+        "n_gpus": 0, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
+        "min_ms": round(min(times), 3), "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{desc}, Jacobi-CG {MAX_IT} iterations", "n": A.n_rows,
+                   "nnz": A.nnz},
+        "cpu_baseline": {"value": round(ms, 3), "unit": "ms/solve", "cores": 1, "kind": kind,
+                         "sample": f"{args.steps} full {MAX_IT}-iteration solves of {desc} "
+                                   "(reference kernels_*.cpp, auto AVX2/scalar dispatch, "
+                                   "single-threaded like the reference's kernels)"},
+        "e2e": {"value": round(ms, 3), "unit": "ms/solve", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "achieved_gbs_bref": round(bm["b_ref_solve"] / (ms * 1e-3) / 1e9, 2),
+        "host_syncs_per_iter": 0,
+    }
+    log(f"reference CPU: {ms:.1f} ms/solve (min {min(times):.1f}); total {time.perf_counter()-t_all:.0f}s")
+    print(json.dumps(out), flush=True)
+
+
+def run_gpu(args, cfg):
+    import torch
+    from paper_2306_17801_b200 import rvk
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        log(f"warning: WORLD_SIZE={world} but --gpus {args.gpus}")
+    if world > 1:
+        from paper_2306_17801_b200 import sharded
+        return sharded.bench_main(args, cfg)
+    torch.cuda.set_device(local)
+    dim, pts, grid, desc = cfg
+    stream = torch.cuda.Stream()
+    ctx = rvk.Ctx(stream.cuda_stream)
+    A = rvk.DeviceCsr.laplacian(ctx, dim, pts, grid)
+    n, nnz = A.n_rows, A.nnz
+    b = rvk.DeviceArray(n)
+    x = rvk.DeviceArray(n)
+    rvk.check(rvk.lib().rvk_fill_rhs(ctx.h, 0x9E3779B97F4A7C15, n, b.ptr))
+    plan = rvk.CgPlan(ctx, A, max_it=MAX_IT, mode=args.mode, use_graph=not args.no_graph)
+    plan.set_profiling(True)
+    bm = bytes_model(n, nnz)
+    hbm_peak, peak_src = peaks()
+    ws_bytes = 20 * nnz + 8 * (n + 1) + 9 * 8 * n
+    log(f"{desc}: n={n} nnz={nnz} working set {ws_bytes/1e9:.2f} GB (L2 {L2_BYTES/1e6:.0f} MB)")
+
+    for _ in range(args.warmup):
+        plan.solve_dev(b, x)
+    res = plan.result()
+    assert res.iterations == MAX_IT, res
+
+    syncs0 = rvk.host_syncs()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        with torch.cuda.stream(stream):
+            ev[0].record(stream)
+            for k in range(args.steps):
+                plan.solve_dev(b, x)
+                ev[k + 1].record(stream)
+        stream.synchronize()
+        torch.cuda.synchronize()
+    syncs = rvk.host_syncs() - syncs0
+    step_ms = [ev[k].elapsed_time(ev[k + 1]) for k in range(args.steps)]
+    total_ms = ev[0].elapsed_time(ev[-1])
+    ms = total_ms / args.steps
+    k1_ms, k2_ms, launches = plan.kernel_times()   # last timed solve, 20 launches each
+    res = plan.result()
+    assert res.iterations == MAX_IT
+
+    k1_avg = k1_ms / MAX_IT
+    k2_avg = k2_ms / MAX_IT
+    k1_gbs = bm["k1"] / (k1_avg * 1e-3) / 1e9
+    k2_gbs = bm["k2"] / (k2_avg * 1e-3) / 1e9
+    solve_gbs = bm["b_min_solve"] / (ms * 1e-3) / 1e9
+    traffic = ncu_traffic(args.config)
+
+    # ---- e2e through the C-ABI with host buffers (pinned) ----------------------
+    bh = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    xh = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    bh.numpy()[:] = b.download(ctx)
+    hist = np.empty(MAX_IT + 1)
+    plan.set_profiling(False)
+    for _ in range(max(1, args.warmup)):
+        plan.solve_host(bh.numpy(), xh.numpy(), hist)
+    e2e = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        _, r = plan.solve_host(bh.numpy(), xh.numpy(), hist)
+        e2e.append((time.perf_counter() - t0) * 1e3)
+    e2e_ms = statistics.mean(e2e)
+
+    cpu = None
+    if not args.no_cpu_baseline:
+        kind, ctimes, _ = cpu_baseline(dim, pts, grid, steps=1)
+        cpu = {"value": round(statistics.mean(ctimes), 1), "unit": "ms/solve", "cores": 1,
+               "kind": kind,
+               "sample": f"1 full {MAX_IT}-iteration solve of {desc} on the GPU box host "
+                         "(reference kernels_*.cpp from oracle/_ref, auto dispatch, 1 thread)"}
+
+    out = {
+        "metric": METRIC, "value": round(ms, 4), "unit": "ms/solve", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+        "min_ms": round(min(step_ms), 4), "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{desc}, Jacobi-CG {MAX_IT} iterations, x0=0, splitmix64 RHS",
+                   "n": n, "nnz": nnz, "mode": args.mode, "graph": not args.no_graph,
+                   "l2": f"no flush: working set {ws_bytes/1e9:.2f} GB >> 126 MB L2 "
+                         "(every operand streams from HBM each step)"},
+        "roofline": {"bound": "hbm", "kernel": "k_spmv_tma<CgSpmvOp> (SpMV + on-the-fly AYPX + p.w)",
+                     "achieved": round(k1_gbs, 1), "peak": hbm_peak, "unit": "GB/s",
+                     "frac": round(k1_gbs / hbm_peak, 4), "traffic": traffic,
+                     "alg_bytes_per_launch": bm["k1"], "avg_launch_ms": round(k1_avg, 5),
+                     "peak_source": peak_src},
+        "solve_roofline": {"alg_bytes_per_solve": bm["b_min_solve"],
+                           "achieved": round(solve_gbs, 1), "frac": round(solve_gbs / hbm_peak, 4),
+                           "update_kernel_gbs": round(k2_gbs, 1),
+                           "b_ref_gbs": round(bm["b_ref_solve"] / (ms * 1e-3) / 1e9, 1)},
+        "host_syncs_per_iter": syncs / (args.steps * MAX_IT),
+        "e2e": {"value": round(e2e_ms, 4), "unit": "ms/solve", "h2d_bytes_per_step": 8 * n,
+                "d2h_bytes_per_step": 8 * n + 8 * (MAX_IT + 1) + 64},
+        "gpu_launches": launches * args.steps,
+        "cpu_baseline": cpu,
+        "clocks": clk.summary(),
+    }
+    log(f"solve {ms:.3f} ms (min {min(step_ms):.3f}); K1 {k1_avg*1e3:.1f} us = {k1_gbs:.0f} GB/s; "
+        f"K2 {k2_avg*1e3:.1f} us = {k2_gbs:.0f} GB/s; solve {solve_gbs:.0f} GB/s "
+        f"({solve_gbs/hbm_peak:.1%}); e2e {e2e_ms:.2f} ms; syncs {syncs}")
+    print(json.dumps(out), flush=True)
+    plan.close()
+    ctx.close()
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawTextHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["rvk", "reference"], default="rvk")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="7pt256")
+    ap.add_argument("--mode", choices=["fused", "unfused"], default="fused")
+    ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "rvk":
+        log("note: raising --warmup to 3 (timing rule)")
+        args.warmup = 3
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_gpu(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

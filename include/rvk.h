@@ -1,0 +1,210 @@
+/*
+ * rvk.h -- C ABI of the B200-native Jacobi-CG path (librvk.so).
+ *
+ * This is the drop-in boundary between the reference's C++ Vec/Mat/KSP-style
+ * API (include/rivulet/ headers here, mirroring /root/reference/proj/include/
+ * rivulet/linalg.hpp:48-78) and hand-written sm_100a kernels.  Plain C types
+ * only: pointers, sizes, an opaque context handle.  No torch types.
+ *
+ * Conventions
+ *  - Every entry point returns an rvk_status (0 = RVK_OK).  On failure the
+ *    thread-local message is available from rvk_last_error().
+ *  - Pointers named *_dev are device pointers owned by the caller; *_host are
+ *    host pointers (pinned or pageable).
+ *  - Every compute entry point is ASYNCHRONOUS and stream-ordered on the
+ *    rvk_ctx's CUDA stream: it never blocks the host.  The only host
+ *    synchronisations are the explicitly named ones (rvk_ctx_synchronize,
+ *    rvk_scalar_read, rvk_cg_result, rvk_cg_solve_host, rvk_*_plan_create);
+ *    each is counted in rvk_host_sync_count(), mirroring trace::host_sync
+ *    (reference trace.hpp:40-41, managed.cpp:74-84).
+ *  - Reductions write their result to DEVICE memory (the paper's fix for the
+ *    "scalar problem"), in a fixed order, so results are
+ *    bit-reproducible run to run.
+ *  - Elementwise ops and SpMV compute every element with IEEE mul-then-add
+ *    (no FMA), in the reference's operand order, so they are bit-identical to
+ *    rivulet::kernels::scalar (kernels_scalar.cpp:24-63).
+ */
+#ifndef RVK_H
+#define RVK_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RVK_ABI_VERSION 1
+
+typedef enum {
+    RVK_OK             = 0,
+    RVK_ERR_INVALID    = 1, /* bad argument / invalid spec                     */
+    RVK_ERR_DIM        = 2, /* dimension mismatch    */
+    RVK_ERR_CUDA       = 3, /* CUDA runtime error                              */
+    RVK_ERR_ALLOC      = 4, /* device / pinned allocation failed               */
+    RVK_ERR_BREAKDOWN  = 5, /* Krylov breakdown (common.hpp:33-43)             */
+    RVK_ERR_COMM       = 6, /* NCCL / communicator error                       */
+    RVK_ERR_UNSUPPORTED = 7
+} rvk_status;
+
+/* Thread-local description of the last failure on this thread. */
+const char* rvk_last_error(void);
+int         rvk_abi_version(void);
+/* Number of SMs / name of device 0 as seen by the library (setup helper). */
+int         rvk_device_info(int* sm_count, char* name, int name_len);
+
+/* ---- context: a CUDA stream + reduction scratch (PetscDeviceContext) -----
+ * Replaces rivulet::Context's agent-thread queue (context.hpp:75-114;
+ * context.cpp:151-232).  A ctx created with cuda_stream == NULL owns a new
+ * non-blocking stream; otherwise it wraps the caller's stream. */
+typedef struct rvk_ctx_s* rvk_ctx;
+rvk_status rvk_ctx_create(void* cuda_stream, rvk_ctx* out);
+rvk_status rvk_ctx_destroy(rvk_ctx ctx);                 /* drains first */
+void*      rvk_ctx_stream(rvk_ctx ctx);                  /* the cudaStream_t          */
+rvk_status rvk_ctx_synchronize(rvk_ctx ctx);             /* context.hpp:96-99; counted */
+rvk_status rvk_ctx_query_idle(rvk_ctx ctx, int* idle);   /* context.hpp:92; no block   */
+/* wait_for (context.hpp:88-90): future work on `waiter` starts after all
+ * work enqueued on `waitee` so far.  Self-wait is a no-op. */
+rvk_status rvk_ctx_wait_for(rvk_ctx waiter, rvk_ctx waitee);
+
+/* ---- host-sync accounting (trace.hpp:40-41 HostSync events) ------------- */
+uint64_t rvk_host_sync_count(void);
+void     rvk_host_sync_reset(void);
+
+/* ---- device memory (plumbing) -------------------------------------------- */
+rvk_status rvk_malloc(void** dev, size_t bytes);
+rvk_status rvk_free(void* dev);
+rvk_status rvk_host_alloc(void** host, size_t bytes);    /* pinned */
+rvk_status rvk_host_free(void* host);
+rvk_status rvk_memcpy_h2d(rvk_ctx ctx, void* dst_dev, const void* src_host, size_t bytes);
+rvk_status rvk_memcpy_d2h(rvk_ctx ctx, void* dst_host, const void* src_dev, size_t bytes);
+rvk_status rvk_memcpy_d2d(rvk_ctx ctx, void* dst_dev, const void* src_dev, size_t bytes);
+
+/* ---- scalar arguments: detail::ScalarArg (linalg.hpp:17-38) --------------
+ * A constant, a device scalar, its negation, or a ratio of two device
+ * scalars: exactly the expression shapes the CG listing passes to a
+ * consuming kernel.  Evaluated inside the kernel;
+ * the value never visits the host. */
+typedef enum {
+    RVK_SCALAR_CONST       = 0, /* c                                   */
+    RVK_SCALAR_PTR         = 1, /* *p0                                 */
+    RVK_SCALAR_NEG_PTR     = 2, /* -(*p0)                              */
+    RVK_SCALAR_DIV_PTR_PTR = 3, /* (*p0) / (*p1)                       */
+    RVK_SCALAR_SQRT_PTR    = 4, /* sqrt(*p0)                           */
+    RVK_SCALAR_RECIP_PTR   = 5  /* 1.0 / (*p0)  (normalize) */
+} rvk_scalar_kind;
+
+typedef struct {
+    int           kind;
+    double        c;
+    const double* p0;
+    const double* p1;
+} rvk_scalar;
+
+/* out_dev = value of `s` (Eval(expr, ctx).execute(out), expr.cpp:314-386,
+ * restricted to the scalar shapes above). */
+rvk_status rvk_scalar_eval(rvk_ctx ctx, rvk_scalar s, double* out_dev);
+/* Host read of a device scalar: Managed::front() (managed.cpp:86-91).
+ * Synchronises the context; counted as one host sync. */
+rvk_status rvk_scalar_read(rvk_ctx ctx, const double* s_dev, double* out_host);
+
+/* ---- Vec kernels (linalg.hpp:48-66; kernels.hpp:38-48) ------------------ */
+rvk_status rvk_dot(rvk_ctx ctx, int64_t n, const double* x, const double* y, double* out_dev);
+rvk_status rvk_nrm2(rvk_ctx ctx, int64_t n, const double* x, double* out_dev);
+/* fused pair: zz = z.z, zr = z.r in one pass */
+rvk_status rvk_dot2(rvk_ctx ctx, int64_t n, const double* z, const double* r,
+                    double* zz_dev, double* zr_dev);
+rvk_status rvk_axpy(rvk_ctx ctx, int64_t n, rvk_scalar a, const double* x, double* y);  /* y += a*x   */
+rvk_status rvk_aypx(rvk_ctx ctx, int64_t n, rvk_scalar b, const double* x, double* y);  /* y = x + b*y */
+rvk_status rvk_waxpy(rvk_ctx ctx, int64_t n, rvk_scalar a, const double* x, const double* y,
+                     double* w);                                                      /* w = a*x + y */
+rvk_status rvk_scale(rvk_ctx ctx, int64_t n, rvk_scalar a, double* x);                  /* x *= a     */
+rvk_status rvk_pointwise_mult(rvk_ctx ctx, int64_t n, const double* a, const double* b,
+                              double* out);                                           /* out = a.*b */
+rvk_status rvk_copy(rvk_ctx ctx, int64_t n, const double* src, double* dst);
+rvk_status rvk_set(rvk_ctx ctx, int64_t n, double value, double* x);
+
+/* ---- Mat: CSR (csr.hpp:19-85) -------------------------------------------
+ * int64 row offsets, int32 column indices, double values, all on device.
+ * Columns strictly increasing within a row (csr.hpp:51-53). */
+typedef struct {
+    int64_t        n_rows;
+    int64_t        n_cols;
+    int64_t        nnz;
+    const int64_t* row_offsets;
+    const int32_t* col_indices;
+    const double*  values;
+} rvk_csr;
+
+/* y = A x (mat_mult, linalg.hpp:68-69; kernels_scalar.cpp:53-63): per-row
+ * left-to-right sum from 0.0, mul-then-add => bit-identical to the reference. */
+rvk_status rvk_csr_spmv(rvk_ctx ctx, const rvk_csr* A, const double* x, double* y);
+/* diag = diagonal() (csr.hpp:76-77; zero where absent); dinv = 1/diag. */
+rvk_status rvk_csr_diagonal(rvk_ctx ctx, const rvk_csr* A, double* diag);
+rvk_status rvk_csr_diagonal_inverse(rvk_ctx ctx, const rvk_csr* A, double* dinv);
+/* Structural validation (csr.hpp:46-53 contract).  Synchronises (setup).
+ * Also returns the maximum row length. */
+rvk_status rvk_csr_validate(rvk_ctx ctx, const rvk_csr* A, int64_t* max_row_len);
+
+/* ---- stencil assembly on device --- */
+rvk_status rvk_laplacian_size(int dim, int points, int64_t nx, int64_t ny, int64_t nz,
+                              int64_t* n_rows, int64_t* nnz);
+/* Fills caller-allocated device arrays off[n+1], cols[nnz], vals[nnz];
+ * bit-identical to the CPU builder (lexicographic, x fastest, ascending
+ * columns, Dirichlet by truncation, centre = points-1, neighbours -1). */
+rvk_status rvk_build_laplacian(rvk_ctx ctx, int dim, int points, int64_t nx, int64_t ny,
+                               int64_t nz, int64_t* off_dev, int32_t* cols_dev,
+                               double* vals_dev);
+/* Synthetic RHS b_i = (splitmix64(seed+i)>>11)*2^-52 - 1. */
+rvk_status rvk_fill_rhs(rvk_ctx ctx, uint64_t seed, int64_t n, double* b_dev);
+
+/* ---- KSP: Jacobi-preconditioned CG --- */
+typedef enum { RVK_PC_NONE = 0, RVK_PC_JACOBI = 1 } rvk_pc;
+typedef enum {
+    RVK_CG_MODE_FUSED   = 0, /* 3 kernels/iteration-pair, device tails (default) */
+    RVK_CG_MODE_UNFUSED = 1  /* the reference's op-per-kernel sequence         */
+} rvk_cg_mode;
+typedef enum { RVK_CG_RUNNING = 0, RVK_CG_CONVERGED = 1, RVK_CG_BREAKDOWN = 2 } rvk_cg_state;
+
+typedef struct {
+    int    max_it;    /* SPEC.md:444 default 20                                  */
+    int    pc;        /* rvk_pc                                                  */
+    double rtol;      /* converged if dp <= max(rtol*dp0, atol); 0,0 => only 0   */
+    double atol;
+    int    mode;      /* rvk_cg_mode                                             */
+    int    use_graph; /* capture the whole solve as one CUDA graph (replayed)    */
+} rvk_cg_config;
+
+typedef struct {
+    int state;          /* rvk_cg_state: RUNNING here means "ran max_it"     */
+    int iterations;     /* completed iterations: hist[0..iterations] valid   */
+    int breakdown_iter; /* iteration index of breakdown, -1 if none          */
+} rvk_cg_info;
+
+typedef struct rvk_cg_plan_s* rvk_cg_plan;
+
+/* KSPSetUp analogue: validates A (one sync), computes dinv on device, sizes
+ * the SpMV tiles, allocates the work vectors r, z, p0, p1, w. */
+rvk_status rvk_cg_plan_create(rvk_ctx ctx, const rvk_csr* A_dev, rvk_cg_config cfg,
+                              rvk_cg_plan* out);
+rvk_status rvk_cg_plan_destroy(rvk_cg_plan plan);
+/* Enqueue one full solve (x0 = 0, r0 = b; max_it iterations or device-side
+ * convergence/breakdown exit).  ZERO host synchronisations. */
+rvk_status rvk_cg_solve_dev(rvk_cg_plan plan, const double* b_dev, double* x_dev);
+/* Device pointer to the residual history hist[0..max_it] (||z_k||_2). */
+const double* rvk_cg_history_dev(rvk_cg_plan plan);
+/* Synchronise and read hist (max_it+1 doubles, may be NULL) and info;
+ * returns RVK_ERR_BREAKDOWN if the solve broke down.  One counted sync. */
+rvk_status rvk_cg_result(rvk_cg_plan plan, double* hist_host, rvk_cg_info* info);
+/* End-to-end: copy b from host, solve, copy x and hist back, one sync. */
+rvk_status rvk_cg_solve_host(rvk_cg_plan plan, const double* b_host, double* x_host,
+                             double* hist_host, rvk_cg_info* info);
+/* Per-kernel event timing of the last solve's dominant kernels (bench): */
+rvk_status rvk_cg_set_profiling(rvk_cg_plan plan, int on);
+rvk_status rvk_cg_kernel_times(rvk_cg_plan plan, float* spmv_ms, float* update_ms,
+                               int* launches);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,806 @@
+// rvk_cg.cu -- Jacobi-preconditioned CG on sm_100a with zero host syncs per
+// iteration.
+//
+// Reference path: cg_solve running the PETSc
+// KSPCG loop of PAPER.md:104-150:
+//   setup:  r = b, z = B r, dp = ||z|| -> hist[0], beta = z.r
+//   iter i: b = beta/betaold (i>=1); p = z + b p (i==0: p = z); w = A p
+//           a = beta/(p.w); betaold = beta; x += a p; r += (-a) w; z = B r
+//           dp = ||z|| -> hist[i+1]; converged?; beta = z.r
+//
+// FUSED mode (default) -- per iteration two kernels, all scalars on device:
+//   K1 = k_spmv_tma<CgSpmvOp>: p_new = z + b p_old evaluated on the fly for
+//        every gathered column (b = beta/betaold read from device memory),
+//        w = A p_new, p.w partials; last block: alpha = beta/pAp, breakdown
+//        check, betaold = beta.  p ping-pongs between two buffers because
+//        neighbouring tiles still gather p_old while p_new is written.
+//   K2 = k_cg_update: x += a p; r += (-a) w; z = dinv .* r; z.z and z.r
+//        partials; last block: dp = sqrt(z.z) -> hist, convergence, beta.
+//   K0 = k_cg_setup once per solve (r = b, x = 0, z = B r, dp0, beta).
+// Every per-element result uses the reference's rounding sequence, so p, w,
+// x, r, z differ from the CPU oracle only through the reduction order of the
+// three scalars (tolerance 1e-10, BASELINE.json north_star).
+//
+// UNFUSED mode issues the reference's one-kernel-per-op sequence
+// through the same Vec/SpMV kernels with device-scalar arguments; it exists
+// for the fusion A/B and as the literal drop-in for the listing.
+//
+// Early exit (converged / breakdown) is decided on device: the tails set a
+// `done` flag and every later kernel of the solve returns immediately, so
+// the whole solve is one CUDA graph replayed with no host involvement.
+#include "rvk_common.cuh"
+#include "rvk_context.hpp"
+#include "rvk_internal.hpp"
+#include "rvk_spmv.cuh"
+
+#include <cmath>
+#include <vector>
+
+namespace rvk {
+
+struct CgState {
+    double beta, betaold, alpha, pAp, dp0, dp;
+    int    done, state, iterations, breakdown_iter;
+};
+
+constexpr int kUpdThreads = 256;
+
+__device__ __forceinline__ bool cg_converged(double dp, double dp0, double rtol, double atol)
+{
+    return dp <= fmax(rtol * dp0, atol);
+}
+
+// ---------------------------------------------------------------------------
+// K0: setup.  r = b; x = 0; z = B r; partials z.z, z.r.
+// ---------------------------------------------------------------------------
+template <bool VEC, bool JACOBI>
+__global__ void __launch_bounds__(kUpdThreads)
+    k_cg_setup(int64_t n, const double* __restrict__ b, const double* __restrict__ dinv,
+               double* __restrict__ x, double* __restrict__ r, double* __restrict__ z,
+               CgState* st, double* hist, double rtol, double atol, double* partials,
+               unsigned int* ticket)
+{
+    __shared__ double smem[64];
+    __shared__ int    flag;
+    double            acc[2] = {0.0, 0.0};
+    const int64_t     stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t     t0     = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (VEC) {
+        const int64_t n2 = n >> 1;
+        for (int64_t i = t0; i < n2; i += stride) {
+            const double2 bi = ld_stream(reinterpret_cast<const double2*>(b) + i);
+            double2       zi = bi;
+            if (JACOBI) {
+                const double2 d = ld_stream(reinterpret_cast<const double2*>(dinv) + i);
+                zi.x = mul(d.x, bi.x);
+                zi.y = mul(d.y, bi.y);
+            }
+            reinterpret_cast<double2*>(r)[i] = bi;
+            reinterpret_cast<double2*>(z)[i] = zi;
+            st_stream(reinterpret_cast<double2*>(x) + i, make_double2(0.0, 0.0));
+            acc[0] = add(acc[0], mul(zi.x, zi.x));
+            acc[0] = add(acc[0], mul(zi.y, zi.y));
+            acc[1] = add(acc[1], mul(zi.x, bi.x));
+            acc[1] = add(acc[1], mul(zi.y, bi.y));
+        }
+    }
+    for (int64_t i = (VEC ? (n & ~int64_t(1)) : 0) + t0; i < n; i += stride) {
+        const double bi = b[i];
+        const double zi = JACOBI ? mul(dinv[i], bi) : bi;
+        r[i] = bi;
+        z[i] = zi;
+        x[i] = 0.0;
+        acc[0] = add(acc[0], mul(zi, zi));
+        acc[1] = add(acc[1], mul(zi, bi));
+    }
+    const int tid = threadIdx.x;
+    block_sum<2>(acc, smem, tid, blockDim.x, 1);
+    if (tid == 0) {
+        partials[2 * blockIdx.x]     = acc[0];
+        partials[2 * blockIdx.x + 1] = acc[1];
+    }
+    if (!last_block(ticket, tid, &flag, blockDim.x, 1)) return;
+    fold_partials<2>(partials, gridDim.x, acc, smem, tid, blockDim.x, 1);
+    if (tid == 0) {
+        const double dp0 = sqrt(acc[0]);
+        hist[0]            = dp0;
+        st->dp0            = dp0;
+        st->dp             = dp0;
+        st->beta           = acc[1];
+        st->betaold        = 0.0;
+        st->alpha          = 0.0;
+        st->pAp            = 0.0;
+        st->iterations     = 0;
+        st->breakdown_iter = -1;
+        const bool conv    = cg_converged(dp0, dp0, rtol, atol);
+        st->state          = conv ? RVK_CG_CONVERGED : RVK_CG_RUNNING;
+        st->done           = conv ? 1 : 0;
+        *ticket            = 0u;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K1 op: p_new = z + b p_old on the fly; w = A p_new; tail alpha.
+// ---------------------------------------------------------------------------
+template <bool FIRST>
+struct CgSpmvOp {
+    static constexpr bool kHasTail = true;
+    const double* __restrict__ z;
+    const double* __restrict__ p_old;
+    double* __restrict__ p_new;
+    double* __restrict__ w;
+    CgState* st;
+    int      it;
+    double   b; // set by init()
+
+    __device__ __forceinline__ bool init()
+    {
+        if (st->done) return false;
+        if (!FIRST) {
+            const double bo = st->betaold;
+            if (bo == 0.0) { // breakdown in beta/betaold
+                if (blockIdx.x == 0 && threadIdx.x == 0) {
+                    st->state          = RVK_CG_BREAKDOWN;
+                    st->breakdown_iter = it;
+                    st->done           = 1;
+                }
+                return false;
+            }
+            b = st->beta / bo;
+        }
+        return true;
+    }
+    __device__ __forceinline__ double src(int32_t j) const
+    {
+        if (FIRST) return __ldg(z + j);
+        return aypx1(b, __ldg(z + j), __ldg(p_old + j)); // z + b*p  (kernels_scalar.cpp:33)
+    }
+    __device__ __forceinline__ double row(int64_t i, double sum, double acc) const
+    {
+        const double p = src((int32_t)i);
+        p_new[i]       = p;
+        w[i]           = sum;
+        return add(acc, mul(p, sum));
+    }
+    __device__ __forceinline__ void tail(double pAp) const
+    {
+        const double a = st->beta / pAp;
+        st->pAp        = pAp;
+        if (pAp == 0.0 || !isfinite(a)) {
+            st->state          = RVK_CG_BREAKDOWN;
+            st->breakdown_iter = it;
+            st->done           = 1;
+        } else {
+            st->alpha   = a;
+            st->betaold = st->beta;
+        }
+    }
+};
+
+// ---------------------------------------------------------------------------
+// K2: x += a p; r += (-a) w; z = B r; partials z.z, z.r; tail dp/hist/beta.
+// ---------------------------------------------------------------------------
+template <bool VEC, bool JACOBI>
+__global__ void __launch_bounds__(kUpdThreads)
+    k_cg_update(int64_t n, const double* __restrict__ p, const double* __restrict__ w,
+                const double* __restrict__ dinv, double* __restrict__ x, double* __restrict__ r,
+                double* __restrict__ z, CgState* st, double* hist, int it, double rtol,
+                double atol, double* partials, unsigned int* ticket)
+{
+    if (st->done) return;
+    __shared__ double smem[64];
+    __shared__ int    flag;
+    const double      a      = st->alpha;
+    const double      na     = -a;
+    double            acc[2] = {0.0, 0.0};
+    const int64_t     stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t     t0     = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (VEC) {
+        const int64_t n2 = n >> 1;
+        for (int64_t i = t0; i < n2; i += stride) {
+            const double2 pi = ld_stream(reinterpret_cast<const double2*>(p) + i);
+            const double2 wi = ld_stream(reinterpret_cast<const double2*>(w) + i);
+            double2       xi = ld_stream(reinterpret_cast<const double2*>(x) + i);
+            double2       ri = ld_stream(reinterpret_cast<const double2*>(r) + i);
+            xi.x = axpy1(a, pi.x, xi.x);
+            xi.y = axpy1(a, pi.y, xi.y);
+            ri.x = axpy1(na, wi.x, ri.x);
+            ri.y = axpy1(na, wi.y, ri.y);
+            double2 zi = ri;
+            if (JACOBI) {
+                const double2 d = ld_stream(reinterpret_cast<const double2*>(dinv) + i);
+                zi.x = mul(d.x, ri.x);
+                zi.y = mul(d.y, ri.y);
+            }
+            st_stream(reinterpret_cast<double2*>(x) + i, xi);
+            reinterpret_cast<double2*>(r)[i] = ri;
+            reinterpret_cast<double2*>(z)[i] = zi;
+            acc[0] = add(acc[0], mul(zi.x, zi.x));
+            acc[0] = add(acc[0], mul(zi.y, zi.y));
+            acc[1] = add(acc[1], mul(zi.x, ri.x));
+            acc[1] = add(acc[1], mul(zi.y, ri.y));
+        }
+    }
+    for (int64_t i = (VEC ? (n & ~int64_t(1)) : 0) + t0; i < n; i += stride) {
+        x[i]            = axpy1(a, p[i], x[i]);
+        const double ri = axpy1(na, w[i], r[i]);
+        const double zi = JACOBI ? mul(dinv[i], ri) : ri;
+        r[i]            = ri;
+        z[i]            = zi;
+        acc[0]          = add(acc[0], mul(zi, zi));
+        acc[1]          = add(acc[1], mul(zi, ri));
+    }
+    const int tid = threadIdx.x;
+    block_sum<2>(acc, smem, tid, blockDim.x, 1);
+    if (tid == 0) {
+        partials[2 * blockIdx.x]     = acc[0];
+        partials[2 * blockIdx.x + 1] = acc[1];
+    }
+    if (!last_block(ticket, tid, &flag, blockDim.x, 1)) return;
+    fold_partials<2>(partials, gridDim.x, acc, smem, tid, blockDim.x, 1);
+    if (tid == 0) {
+        const double dp = sqrt(acc[0]);
+        hist[it + 1]    = dp;
+        st->dp          = dp;
+        st->iterations  = it + 1;
+        if (cg_converged(dp, st->dp0, rtol, atol)) {
+            st->state = RVK_CG_CONVERGED;
+            st->done  = 1;
+        } else {
+            st->beta = acc[1];
+        }
+        *ticket = 0u;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Unfused-mode scalar tails (one thread each): the Eval() steps of the
+// listing plus state bookkeeping.
+// ---------------------------------------------------------------------------
+__global__ void k_unfused_tail0(CgState* st, double* hist, const double* dp, double rtol,
+                                double atol)
+{
+    const double dp0   = *dp;
+    hist[0]            = dp0;
+    st->dp0            = dp0;
+    st->dp             = dp0;
+    st->betaold        = 0.0;
+    st->iterations     = 0;
+    st->breakdown_iter = -1;
+    const bool conv    = cg_converged(dp0, dp0, rtol, atol);
+    st->state          = conv ? RVK_CG_CONVERGED : RVK_CG_RUNNING;
+    st->done           = conv ? 1 : 0;
+}
+
+__global__ void k_unfused_pre(CgState* st, int it) // b = beta/betaold guard
+{
+    if (st->done) return;
+    if (st->betaold == 0.0) {
+        st->state          = RVK_CG_BREAKDOWN;
+        st->breakdown_iter = it;
+        st->done           = 1;
+    }
+}
+
+__global__ void k_unfused_alpha(CgState* st, int it) // a = beta/a; betaold = beta
+{
+    if (st->done) return;
+    const double pAp = st->pAp;
+    const double a   = st->beta / pAp;
+    if (pAp == 0.0 || !isfinite(a)) {
+        st->state          = RVK_CG_BREAKDOWN;
+        st->breakdown_iter = it;
+        st->done           = 1;
+    } else {
+        st->alpha   = a;
+        st->betaold = st->beta;
+    }
+}
+
+__global__ void k_unfused_hist(CgState* st, double* hist, int it, double rtol, double atol)
+{
+    if (st->done) return;
+    hist[it + 1]   = st->dp;
+    st->iterations = it + 1;
+    if (cg_converged(st->dp, st->dp0, rtol, atol)) {
+        st->state = RVK_CG_CONVERGED;
+        st->done  = 1;
+    }
+}
+
+// guarded copy p = z (iteration 0 of the unfused sequence)
+__global__ void k_guarded_copy(int64_t n, const double* __restrict__ src, double* __restrict__ dst,
+                               const int* guard)
+{
+    if (*guard) return;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+        dst[i] = src[i];
+}
+
+// Guarded plain SpMV op for the unfused sequence.
+struct SpmvGuardedOp : SpmvPlainOp {
+    const int* guard;
+    __device__ __forceinline__ bool init() { return *guard == 0; }
+};
+
+// diag / dinv (csr.hpp:76-77): zero where absent; dinv = 1/diag.
+template <bool INV>
+__global__ void k_diagonal(int64_t n, const int64_t* __restrict__ off,
+                           const int32_t* __restrict__ cols, const double* __restrict__ vals,
+                           double* __restrict__ out)
+{
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += stride) {
+        double d = 0.0;
+        for (int64_t k = off[r]; k < off[r + 1]; ++k)
+            if (cols[k] == r) d = vals[k];
+        out[r] = INV ? 1.0 / d : d;
+    }
+}
+
+// Structural checks + max row length (csr.hpp:46-53).  err bits:
+// 1 off[0]!=0, 2 decreasing offsets, 4 off[n]!=nnz, 8 col out of range,
+// 16 columns not strictly increasing.
+__global__ void k_validate(int64_t n, int64_t n_cols, int64_t nnz, const int64_t* __restrict__ off,
+                           const int32_t* __restrict__ cols, unsigned int* err,
+                           unsigned long long* maxlen)
+{
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    unsigned int  e      = 0;
+    unsigned long long ml = 0;
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += stride) {
+        const int64_t a = off[r], b = off[r + 1];
+        if (r == 0 && a != 0) e |= 1u;
+        if (b < a) { e |= 2u; continue; }
+        if (r == n - 1 && b != nnz) e |= 4u;
+        if (a < 0 || b > nnz) { e |= 4u; continue; }
+        if ((unsigned long long)(b - a) > ml) ml = (unsigned long long)(b - a);
+        int64_t prev = -1;
+        for (int64_t k = a; k < b; ++k) {
+            const int64_t c = cols[k];
+            if (c < 0 || c >= n_cols) e |= 8u;
+            if (c <= prev) e |= 16u;
+            prev = c;
+        }
+    }
+    if (e) atomicOr(err, e);
+    if (ml) atomicMax(maxlen, ml);
+}
+
+int update_grid(int64_t n)
+{
+    const int64_t want = (n / 2 + kUpdThreads - 1) / kUpdThreads;
+    const int64_t cap  = (int64_t)sm_count() * 4;
+    return (int)(want < 1 ? 1 : (want > cap ? cap : want));
+}
+
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+} // namespace rvk
+
+using namespace rvk;
+
+struct rvk_cg_plan_s {
+    rvk_ctx       ctx = nullptr;
+    rvk_csr       A{};
+    rvk_cg_config cfg{};
+    int           R = 0, spmv_grid = 0, upd_grid = 0;
+    double*       dinv = nullptr;
+    double*       r = nullptr;
+    double*       z = nullptr;
+    double*       p[2] = {nullptr, nullptr};
+    double*       w    = nullptr;
+    double*       hist = nullptr;
+    CgState*      st   = nullptr;
+    double*       partials = nullptr;     // plan-owned reduction scratch
+    unsigned int* tickets  = nullptr;
+    double*       tmp      = nullptr;     // unfused: dp scratch
+    double*       b_buf    = nullptr;     // host e2e staging
+    double*       x_buf    = nullptr;
+    // graph cache
+    cudaGraphExec_t graph   = nullptr;
+    const double*   g_b     = nullptr;
+    double*         g_x     = nullptr;
+    bool            g_prof  = false;
+    // profiling
+    bool                     profiling = false;
+    std::vector<cudaEvent_t> ev;          // 4 per iteration: K1 begin/end, K2 begin/end
+    int                      launches  = 0;
+};
+
+namespace {
+
+rvk_status enqueue_fused(rvk_cg_plan P, const double* b, double* x)
+{
+    const int64_t n     = P->A.n_rows;
+    cudaStream_t  s     = P->ctx->stream;
+    const bool    jac   = P->cfg.pc == RVK_PC_JACOBI;
+    const bool    vec   = aligned16(b) && aligned16(x) && aligned16(P->dinv);
+    const int     ug    = P->upd_grid;
+    const double  rtol  = P->cfg.rtol, atol = P->cfg.atol;
+    unsigned int* tk0   = P->tickets;
+    unsigned int* tk1   = P->tickets + 1;
+    double*       part0 = P->partials;
+    double*       part1 = P->partials + 2 * kMaxReduceBlocks;
+    P->launches         = 0;
+
+#define RVK_SETUP(V, J)                                                                        \
+    k_cg_setup<V, J><<<ug, kUpdThreads, 0, s>>>(n, b, P->dinv, x, P->r, P->z, P->st, P->hist,  \
+                                                rtol, atol, part0, tk0)
+    if (vec) { if (jac) RVK_SETUP(true, true); else RVK_SETUP(true, false); }
+    else { if (jac) RVK_SETUP(false, true); else RVK_SETUP(false, false); }
+#undef RVK_SETUP
+    RVK_CHECK_LAUNCH("k_cg_setup");
+    ++P->launches;
+
+    const SpmvArgs sa = make_spmv_args(P->A, P->R);
+    const TailArgs ta{part1, tk1};
+    for (int it = 0; it < P->cfg.max_it; ++it) {
+        const double* p_old = P->p[it & 1];
+        double*       p_new = P->p[(it + 1) & 1];
+        if (P->profiling) RVK_CUDA(cudaEventRecord(P->ev[4 * it + 0], s));
+        rvk_status rc;
+        if (it == 0) {
+            CgSpmvOp<true> op{P->z, p_old, p_new, P->w, P->st, it, 0.0};
+            rc = launch_spmv(s, sa, op, ta, P->spmv_grid);
+        } else {
+            CgSpmvOp<false> op{P->z, p_old, p_new, P->w, P->st, it, 0.0};
+            rc = launch_spmv(s, sa, op, ta, P->spmv_grid);
+        }
+        if (rc != RVK_OK) return rc;
+        ++P->launches;
+        if (P->profiling) {
+            RVK_CUDA(cudaEventRecord(P->ev[4 * it + 1], s));
+            RVK_CUDA(cudaEventRecord(P->ev[4 * it + 2], s));
+        }
+#define RVK_UPD(V, J)                                                                          \
+    k_cg_update<V, J><<<ug, kUpdThreads, 0, s>>>(n, p_new, P->w, P->dinv, x, P->r, P->z, P->st, \
+                                                 P->hist, it, rtol, atol, part0, tk0)
+        if (vec) { if (jac) RVK_UPD(true, true); else RVK_UPD(true, false); }
+        else { if (jac) RVK_UPD(false, true); else RVK_UPD(false, false); }
+#undef RVK_UPD
+        RVK_CHECK_LAUNCH("k_cg_update");
+        ++P->launches;
+        if (P->profiling) RVK_CUDA(cudaEventRecord(P->ev[4 * it + 3], s));
+    }
+    return RVK_OK;
+}
+
+#define RVK_TRY(x)                                                                             \
+    do {                                                                                       \
+        rvk_status rc_ = (x);                                                                  \
+        if (rc_ != RVK_OK) return rc_;                                                         \
+    } while (0)
+
+// The reference's op-per-kernel sequence, every scalar a
+// device pointer: identical arithmetic to the fused path.
+rvk_status enqueue_unfused(rvk_cg_plan P, const double* b, double* x)
+{
+    const int64_t n   = P->A.n_rows;
+    cudaStream_t  s   = P->ctx->stream;
+    const bool    jac = P->cfg.pc == RVK_PC_JACOBI;
+    Scratch       sc{P->partials, P->tickets};
+    CgState*      st  = P->st;
+    const int*    g   = &st->done;
+    double*       dp  = P->tmp;
+    auto ptr = [](const double* p) { return rvk_scalar{RVK_SCALAR_PTR, 0.0, p, nullptr}; };
+    P->launches = 0;
+
+    RVK_CUDA(cudaMemcpyAsync(P->r, b, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    RVK_CUDA(cudaMemsetAsync(x, 0, n * sizeof(double), s));
+    if (jac) RVK_TRY(vec_ew(s, EW_PMULT, n, const_scalar(0), P->dinv, P->r, P->z, nullptr));
+    else RVK_CUDA(cudaMemcpyAsync(P->z, P->r, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    RVK_TRY(vec_reduce(s, sc, RED_NRM2, n, P->z, nullptr, dp, nullptr, nullptr));
+    RVK_TRY(vec_reduce(s, sc, RED_DOT, n, P->z, P->r, &st->beta, nullptr, nullptr));
+    k_unfused_tail0<<<1, 1, 0, s>>>(st, P->hist, dp, P->cfg.rtol, P->cfg.atol);
+    RVK_CHECK_LAUNCH("k_unfused_tail0");
+    P->launches += 5;
+
+    double*        p  = P->p[0];
+    const SpmvArgs sa = make_spmv_args(P->A, P->R);
+    for (int it = 0; it < P->cfg.max_it; ++it) {
+        if (it == 0) {
+            k_guarded_copy<<<update_grid(n), kUpdThreads, 0, s>>>(n, P->z, p, g);
+            RVK_CHECK_LAUNCH("k_guarded_copy");
+        } else {
+            k_unfused_pre<<<1, 1, 0, s>>>(st, it);
+            RVK_CHECK_LAUNCH("k_unfused_pre");
+            const rvk_scalar bb{RVK_SCALAR_DIV_PTR_PTR, 0.0, &st->beta, &st->betaold};
+            RVK_TRY(vec_ew(s, EW_AYPX, n, bb, P->z, p, p, g));             // p = z + b p
+            ++P->launches;
+        }
+        if (P->profiling) RVK_CUDA(cudaEventRecord(P->ev[4 * it + 0], s));
+        SpmvGuardedOp op;
+        op.x     = p;
+        op.y     = P->w;
+        op.guard = g;
+        RVK_TRY(launch_spmv(s, sa, op, TailArgs{nullptr, nullptr}, P->spmv_grid)); // w = A p
+        if (P->profiling) {
+            RVK_CUDA(cudaEventRecord(P->ev[4 * it + 1], s));
+            RVK_CUDA(cudaEventRecord(P->ev[4 * it + 2], s));
+        }
+        RVK_TRY(vec_reduce(s, sc, RED_DOT, n, p, P->w, &st->pAp, nullptr, g));       // a = p.w
+        k_unfused_alpha<<<1, 1, 0, s>>>(st, it);                                    // a = beta/a
+        RVK_CHECK_LAUNCH("k_unfused_alpha");
+        RVK_TRY(vec_ew(s, EW_AXPY, n, ptr(&st->alpha), p, x, x, g));                // x += a p
+        const rvk_scalar na{RVK_SCALAR_NEG_PTR, 0.0, &st->alpha, nullptr};
+        RVK_TRY(vec_ew(s, EW_AXPY, n, na, P->w, P->r, P->r, g));                    // r += -a w
+        if (jac) RVK_TRY(vec_ew(s, EW_PMULT, n, const_scalar(0), P->dinv, P->r, P->z, g));
+        else k_guarded_copy<<<update_grid(n), kUpdThreads, 0, s>>>(n, P->r, P->z, g);
+        RVK_TRY(vec_reduce(s, sc, RED_NRM2, n, P->z, nullptr, &st->dp, nullptr, g)); // dp = ||z||
+        k_unfused_hist<<<1, 1, 0, s>>>(st, P->hist, it, P->cfg.rtol, P->cfg.atol);
+        RVK_CHECK_LAUNCH("k_unfused_hist");
+        RVK_TRY(vec_reduce(s, sc, RED_DOT, n, P->z, P->r, &st->beta, nullptr, g));  // beta = z.r
+        if (P->profiling) RVK_CUDA(cudaEventRecord(P->ev[4 * it + 3], s));
+        P->launches += 10;
+    }
+    return RVK_OK;
+}
+
+rvk_status enqueue_solve(rvk_cg_plan P, const double* b, double* x)
+{
+    return P->cfg.mode == RVK_CG_MODE_UNFUSED ? enqueue_unfused(P, b, x) : enqueue_fused(P, b, x);
+}
+
+rvk_status destroy_graph(rvk_cg_plan P)
+{
+    if (P->graph) {
+        cudaGraphExecDestroy(P->graph);
+        P->graph = nullptr;
+    }
+    return RVK_OK;
+}
+
+} // namespace
+
+extern "C" {
+
+rvk_status rvk_csr_validate(rvk_ctx ctx, const rvk_csr* A, int64_t* max_row_len)
+{
+    if (!ctx || !A) return set_error(RVK_ERR_INVALID, "csr_validate: null argument");
+    if (A->n_rows < 0 || A->n_cols < 0 || A->nnz < 0)
+        return set_error(RVK_ERR_INVALID, "csr_validate: negative size");
+    if (A->n_cols > INT32_MAX) return set_error(RVK_ERR_INVALID, "n_cols exceeds int32 indices");
+    if (A->n_rows > 0 && !A->row_offsets) return set_error(RVK_ERR_INVALID, "null row_offsets");
+    if (A->nnz > 0 && (!A->col_indices || !A->values))
+        return set_error(RVK_ERR_INVALID, "null col_indices/values");
+    unsigned int*       err = nullptr;
+    unsigned long long* ml  = nullptr;
+    RVK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&err), 16, ctx->stream));
+    ml = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(err) + 8);
+    RVK_CUDA(cudaMemsetAsync(err, 0, 16, ctx->stream));
+    if (A->n_rows > 0) {
+        const int g = (int)std::min<int64_t>((A->n_rows + 255) / 256, (int64_t)sm_count() * 8);
+        k_validate<<<g, 256, 0, ctx->stream>>>(A->n_rows, A->n_cols, A->nnz, A->row_offsets,
+                                               A->col_indices, err, ml);
+        RVK_CHECK_LAUNCH("k_validate");
+    }
+    unsigned long long host[2] = {0, 0};
+    RVK_CUDA(cudaMemcpyAsync(host, err, 16, cudaMemcpyDeviceToHost, ctx->stream));
+    RVK_CUDA(cudaFreeAsync(err, ctx->stream));
+    note_host_sync();
+    RVK_CUDA(cudaStreamSynchronize(ctx->stream));
+    const unsigned int e = (unsigned int)host[0];
+    if (max_row_len) *max_row_len = (int64_t)host[1];
+    if (A->n_rows == 0 && A->nnz != 0) return set_error(RVK_ERR_INVALID, "CsrMatrix: nnz != 0 with no rows");
+    if (e & 1u) return set_error(RVK_ERR_INVALID, "CsrMatrix: row_offsets[0] != 0");
+    if (e & 2u) return set_error(RVK_ERR_INVALID, "CsrMatrix: row_offsets decreasing");
+    if (e & 4u) return set_error(RVK_ERR_INVALID, "CsrMatrix: row_offsets[n_rows] != nnz");
+    if (e & 8u) return set_error(RVK_ERR_INVALID, "CsrMatrix: column index out of range");
+    if (e & 16u)
+        return set_error(RVK_ERR_INVALID, "CsrMatrix: columns not strictly increasing in a row");
+    return RVK_OK;
+}
+
+rvk_status rvk_csr_spmv(rvk_ctx ctx, const rvk_csr* A, const double* x, double* y)
+{
+    if (!ctx || !A) return set_error(RVK_ERR_INVALID, "csr_spmv: null argument");
+    if (A->n_rows == 0) return RVK_OK;
+    if (!x || !y) return set_error(RVK_ERR_INVALID, "csr_spmv: null vector");
+    // Tile height from the mean row length (no host sync on this path);
+    // tiles that overflow a stage fall back to direct global reads.
+    const int64_t avg = (A->nnz + A->n_rows - 1) / A->n_rows;
+    SpmvPlainOp   op;
+    op.x = x;
+    op.y = y;
+    return launch_spmv(ctx->stream, make_spmv_args(*A, spmv_rows_per_tile(avg)), op,
+                       TailArgs{nullptr, nullptr}, sm_count());
+}
+
+rvk_status rvk_csr_diagonal(rvk_ctx ctx, const rvk_csr* A, double* diag)
+{
+    if (!ctx || !A || (A->n_rows > 0 && !diag)) return set_error(RVK_ERR_INVALID, "null argument");
+    if (A->n_rows == 0) return RVK_OK;
+    k_diagonal<false><<<update_grid(2 * A->n_rows), kUpdThreads, 0, ctx->stream>>>(
+        A->n_rows, A->row_offsets, A->col_indices, A->values, diag);
+    RVK_CHECK_LAUNCH("k_diagonal");
+    return RVK_OK;
+}
+
+rvk_status rvk_csr_diagonal_inverse(rvk_ctx ctx, const rvk_csr* A, double* dinv)
+{
+    if (!ctx || !A || (A->n_rows > 0 && !dinv)) return set_error(RVK_ERR_INVALID, "null argument");
+    if (A->n_rows == 0) return RVK_OK;
+    k_diagonal<true><<<update_grid(2 * A->n_rows), kUpdThreads, 0, ctx->stream>>>(
+        A->n_rows, A->row_offsets, A->col_indices, A->values, dinv);
+    RVK_CHECK_LAUNCH("k_diagonal");
+    return RVK_OK;
+}
+
+rvk_status rvk_cg_plan_create(rvk_ctx ctx, const rvk_csr* A, rvk_cg_config cfg, rvk_cg_plan* out)
+{
+    if (!ctx || !A || !out) return set_error(RVK_ERR_INVALID, "cg_plan_create: null argument");
+    *out = nullptr;
+    if (A->n_rows != A->n_cols) return set_error(RVK_ERR_DIM, "cg_solve: matrix is not square");
+    if (A->n_rows < 1) return set_error(RVK_ERR_DIM, "cg_solve: empty system");
+    if (cfg.max_it < 1) return set_error(RVK_ERR_INVALID, "cg_solve: max_it must be >= 1");
+    if (cfg.pc != RVK_PC_NONE && cfg.pc != RVK_PC_JACOBI)
+        return set_error(RVK_ERR_INVALID, "cg_solve: unknown preconditioner %d", cfg.pc);
+    if (cfg.mode != RVK_CG_MODE_FUSED && cfg.mode != RVK_CG_MODE_UNFUSED)
+        return set_error(RVK_ERR_INVALID, "cg_solve: unknown mode %d", cfg.mode);
+    int64_t maxlen = 0;
+    RVK_TRY(rvk_csr_validate(ctx, A, &maxlen));
+
+    auto P       = new rvk_cg_plan_s();
+    P->ctx       = ctx;
+    P->A         = *A;
+    P->cfg       = cfg;
+    P->R         = spmv_rows_per_tile(maxlen);
+    P->spmv_grid = sm_count();
+    P->upd_grid  = update_grid(A->n_rows);
+    const size_t vb = (size_t)A->n_rows * sizeof(double);
+    cudaError_t  e  = cudaSuccess;
+    auto alloc = [&](void** p, size_t bytes) {
+        if (e == cudaSuccess) e = cudaMalloc(p, bytes);
+    };
+    alloc(reinterpret_cast<void**>(&P->dinv), vb);
+    alloc(reinterpret_cast<void**>(&P->r), vb);
+    alloc(reinterpret_cast<void**>(&P->z), vb);
+    alloc(reinterpret_cast<void**>(&P->p[0]), vb);
+    alloc(reinterpret_cast<void**>(&P->p[1]), vb);
+    alloc(reinterpret_cast<void**>(&P->w), vb);
+    alloc(reinterpret_cast<void**>(&P->hist), sizeof(double) * (cfg.max_it + 1));
+    alloc(reinterpret_cast<void**>(&P->st), sizeof(CgState));
+    alloc(reinterpret_cast<void**>(&P->partials), sizeof(double) * 4 * kMaxReduceBlocks);
+    alloc(reinterpret_cast<void**>(&P->tickets), 16 * sizeof(unsigned int));
+    alloc(reinterpret_cast<void**>(&P->tmp), 16 * sizeof(double));
+    if (e != cudaSuccess) {
+        rvk_cg_plan_destroy(P);
+        return cuda_error(e, "rvk_cg_plan_create: allocation");
+    }
+    cudaStream_t s = ctx->stream;
+    e              = cudaMemsetAsync(P->tickets, 0, 16 * sizeof(unsigned int), s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(P->p[0], 0, vb, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(P->p[1], 0, vb, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(P->st, 0, sizeof(CgState), s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(P->hist, 0, sizeof(double) * (cfg.max_it + 1), s);
+    if (e != cudaSuccess) {
+        rvk_cg_plan_destroy(P);
+        return cuda_error(e, "rvk_cg_plan_create: init");
+    }
+    rvk_status rc = RVK_OK;
+    if (cfg.pc == RVK_PC_JACOBI) rc = rvk_csr_diagonal_inverse(ctx, A, P->dinv);
+    else rc = rvk_set(ctx, A->n_rows, 1.0, P->dinv);
+    if (rc != RVK_OK) {
+        rvk_cg_plan_destroy(P);
+        return rc;
+    }
+    *out = P;
+    return RVK_OK;
+}
+
+rvk_status rvk_cg_plan_destroy(rvk_cg_plan P)
+{
+    if (!P) return RVK_OK;
+    if (P->ctx) cudaStreamSynchronize(P->ctx->stream);
+    destroy_graph(P);
+    for (auto ev : P->ev) cudaEventDestroy(ev);
+    void* bufs[] = {P->dinv, P->r, P->z, P->p[0], P->p[1], P->w, P->hist, P->st,
+                    P->partials, P->tickets, P->tmp, P->b_buf, P->x_buf};
+    for (void* b : bufs)
+        if (b) cudaFree(b);
+    delete P;
+    return RVK_OK;
+}
+
+rvk_status rvk_cg_set_profiling(rvk_cg_plan P, int on)
+{
+    if (!P) return set_error(RVK_ERR_INVALID, "null plan");
+    P->profiling = on != 0;
+    if (P->profiling && P->ev.empty()) {
+        P->ev.resize(4 * (size_t)P->cfg.max_it);
+        for (auto& ev : P->ev) RVK_CUDA(cudaEventCreate(&ev));
+    }
+    return RVK_OK;
+}
+
+rvk_status rvk_cg_solve_dev(rvk_cg_plan P, const double* b, double* x)
+{
+    if (!P) return set_error(RVK_ERR_INVALID, "null plan");
+    if (!b || !x) return set_error(RVK_ERR_INVALID, "cg_solve: null vector");
+    if (b == x) return set_error(RVK_ERR_INVALID, "cg_solve: b and x must not alias");
+    cudaStream_t s = P->ctx->stream;
+    if (!P->cfg.use_graph) return enqueue_solve(P, b, x);
+    if (!P->graph || P->g_b != b || P->g_x != x || P->g_prof != P->profiling) {
+        destroy_graph(P);
+        cudaGraph_t g = nullptr;
+        // Global capture mode: ANY synchronous CUDA call made while the solve
+        // is being enqueued invalidates the capture -- a structural proof
+        // that the solve performs zero host synchronisations.
+        RVK_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeGlobal));
+        rvk_status rc = enqueue_solve(P, b, x);
+        cudaError_t e = cudaStreamEndCapture(s, &g);
+        if (rc != RVK_OK) {
+            if (g) cudaGraphDestroy(g);
+            return rc;
+        }
+        if (e != cudaSuccess) return cuda_error(e, "cudaStreamEndCapture (solve not capturable)");
+        e = cudaGraphInstantiate(&P->graph, g, 0);
+        cudaGraphDestroy(g);
+        if (e != cudaSuccess) return cuda_error(e, "cudaGraphInstantiate");
+        P->g_b    = b;
+        P->g_x    = x;
+        P->g_prof = P->profiling;
+    }
+    RVK_CUDA(cudaGraphLaunch(P->graph, s));
+    return RVK_OK;
+}
+
+const double* rvk_cg_history_dev(rvk_cg_plan P) { return P ? P->hist : nullptr; }
+
+rvk_status rvk_cg_result(rvk_cg_plan P, double* hist_host, rvk_cg_info* info)
+{
+    if (!P) return set_error(RVK_ERR_INVALID, "null plan");
+    CgState      h{};
+    cudaStream_t s = P->ctx->stream;
+    RVK_CUDA(cudaMemcpyAsync(&h, P->st, sizeof(CgState), cudaMemcpyDeviceToHost, s));
+    if (hist_host)
+        RVK_CUDA(cudaMemcpyAsync(hist_host, P->hist, sizeof(double) * (P->cfg.max_it + 1),
+                                 cudaMemcpyDeviceToHost, s));
+    note_host_sync();
+    RVK_CUDA(cudaStreamSynchronize(s));
+    if (info) {
+        info->state          = h.state;
+        info->iterations     = h.iterations;
+        info->breakdown_iter = h.breakdown_iter;
+    }
+    if (h.state == RVK_CG_BREAKDOWN)
+        return set_error(RVK_ERR_BREAKDOWN, "cg_solve: breakdown at iteration %d",
+                         h.breakdown_iter);
+    return RVK_OK;
+}
+
+rvk_status rvk_cg_solve_host(rvk_cg_plan P, const double* b_host, double* x_host,
+                             double* hist_host, rvk_cg_info* info)
+{
+    if (!P || !b_host || !x_host) return set_error(RVK_ERR_INVALID, "null argument");
+    const size_t vb = (size_t)P->A.n_rows * sizeof(double);
+    if (!P->b_buf) RVK_CUDA(cudaMalloc(&P->b_buf, vb));
+    if (!P->x_buf) RVK_CUDA(cudaMalloc(&P->x_buf, vb));
+    cudaStream_t s = P->ctx->stream;
+    RVK_CUDA(cudaMemcpyAsync(P->b_buf, b_host, vb, cudaMemcpyHostToDevice, s));
+    RVK_TRY(rvk_cg_solve_dev(P, P->b_buf, P->x_buf));
+    RVK_CUDA(cudaMemcpyAsync(x_host, P->x_buf, vb, cudaMemcpyDeviceToHost, s));
+    return rvk_cg_result(P, hist_host, info);
+}
+
+rvk_status rvk_cg_kernel_times(rvk_cg_plan P, float* spmv_ms, float* update_ms, int* launches)
+{
+    if (!P) return set_error(RVK_ERR_INVALID, "null plan");
+    if (launches) *launches = P->launches;
+    if (!P->profiling || P->ev.empty()) return set_error(RVK_ERR_INVALID, "profiling is off");
+    float a = 0.f, b = 0.f;
+    for (int it = 0; it < P->cfg.max_it; ++it) {
+        float t1 = 0.f, t2 = 0.f;
+        RVK_CUDA(cudaEventElapsedTime(&t1, P->ev[4 * it + 0], P->ev[4 * it + 1]));
+        RVK_CUDA(cudaEventElapsedTime(&t2, P->ev[4 * it + 2], P->ev[4 * it + 3]));
+        a += t1;
+        b += t2;
+    }
+    if (spmv_ms) *spmv_ms = a;
+    if (update_ms) *update_ms = b;
+    return RVK_OK;
+}
+
+} // extern "C"

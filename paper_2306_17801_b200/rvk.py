@@ -1,0 +1,361 @@
+"""ctypes binding of librvk.so (include/rvk.h) -- the sm_100a Jacobi-CG path.
+
+This is a thin host-side mirror of the C ABI used by the tests and bench.py;
+it has NO compute fallback: if librvk.so is missing or no CUDA device is
+present, every call fails loudly.  The C++ drop-in API for the reference's
+rivulet::linalg / cg_solve surface lives in include/rivulet/ + csrc/api/.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "lib", "librvk.so")
+
+RVK_OK = 0
+RVK_ERR_BREAKDOWN = 5
+SCALAR_CONST, SCALAR_PTR, SCALAR_NEG_PTR, SCALAR_DIV, SCALAR_SQRT, SCALAR_RECIP = range(6)
+PC_NONE, PC_JACOBI = 0, 1
+MODE_FUSED, MODE_UNFUSED = 0, 1
+CG_RUNNING, CG_CONVERGED, CG_BREAKDOWN = 0, 1, 2
+
+# every symbol include/rvk.h declares (checked by tests/test_abi.py)
+EXPORTS = [
+    "rvk_last_error", "rvk_abi_version", "rvk_device_info",
+    "rvk_ctx_create", "rvk_ctx_destroy", "rvk_ctx_stream", "rvk_ctx_synchronize",
+    "rvk_ctx_query_idle", "rvk_ctx_wait_for", "rvk_host_sync_count", "rvk_host_sync_reset",
+    "rvk_malloc", "rvk_free", "rvk_host_alloc", "rvk_host_free", "rvk_memcpy_h2d",
+    "rvk_memcpy_d2h", "rvk_memcpy_d2d", "rvk_scalar_eval", "rvk_scalar_read",
+    "rvk_dot", "rvk_nrm2", "rvk_dot2", "rvk_axpy", "rvk_aypx", "rvk_waxpy", "rvk_scale",
+    "rvk_pointwise_mult", "rvk_copy", "rvk_set", "rvk_csr_spmv", "rvk_csr_diagonal",
+    "rvk_csr_diagonal_inverse", "rvk_csr_validate", "rvk_laplacian_size",
+    "rvk_build_laplacian", "rvk_fill_rhs", "rvk_cg_plan_create", "rvk_cg_plan_destroy",
+    "rvk_cg_solve_dev", "rvk_cg_history_dev", "rvk_cg_result", "rvk_cg_solve_host",
+    "rvk_cg_set_profiling", "rvk_cg_kernel_times",
+]
+
+
+class RvkError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"rvk status {status}: {msg}")
+        self.status = status
+
+
+class BreakdownError(RvkError):
+    """common.hpp:33-43 BreakdownError(iteration)."""
+
+    def __init__(self, status, msg, iteration):
+        super().__init__(status, msg)
+        self.iteration = iteration
+
+
+class Scalar(C.Structure):
+    _fields_ = [("kind", C.c_int), ("c", C.c_double), ("p0", C.c_void_p), ("p1", C.c_void_p)]
+
+
+class Csr(C.Structure):
+    _fields_ = [("n_rows", C.c_int64), ("n_cols", C.c_int64), ("nnz", C.c_int64),
+                ("row_offsets", C.c_void_p), ("col_indices", C.c_void_p), ("values", C.c_void_p)]
+
+
+class CgConfig(C.Structure):
+    _fields_ = [("max_it", C.c_int), ("pc", C.c_int), ("rtol", C.c_double),
+                ("atol", C.c_double), ("mode", C.c_int), ("use_graph", C.c_int)]
+
+
+class CgInfo(C.Structure):
+    _fields_ = [("state", C.c_int), ("iterations", C.c_int), ("breakdown_iter", C.c_int)]
+
+
+_lib = None
+
+
+def lib():
+    """Load librvk.so (raises if it was not built -- there is no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} missing: run __graft_entry__.build() "
+                          "(make -C paper_2306_17801_b200)")
+    L = C.CDLL(LIB_PATH)
+    vp, i64, d, i = C.c_void_p, C.c_int64, C.c_double, C.c_int
+    sig = {
+        "rvk_last_error": (C.c_char_p, []),
+        "rvk_abi_version": (i, []),
+        "rvk_device_info": (i, [C.POINTER(C.c_int), C.c_char_p, i]),
+        "rvk_ctx_create": (i, [vp, C.POINTER(vp)]),
+        "rvk_ctx_destroy": (i, [vp]),
+        "rvk_ctx_stream": (vp, [vp]),
+        "rvk_ctx_synchronize": (i, [vp]),
+        "rvk_ctx_query_idle": (i, [vp, C.POINTER(C.c_int)]),
+        "rvk_ctx_wait_for": (i, [vp, vp]),
+        "rvk_host_sync_count": (C.c_uint64, []),
+        "rvk_host_sync_reset": (None, []),
+        "rvk_malloc": (i, [C.POINTER(vp), C.c_size_t]),
+        "rvk_free": (i, [vp]),
+        "rvk_host_alloc": (i, [C.POINTER(vp), C.c_size_t]),
+        "rvk_host_free": (i, [vp]),
+        "rvk_memcpy_h2d": (i, [vp, vp, vp, C.c_size_t]),
+        "rvk_memcpy_d2h": (i, [vp, vp, vp, C.c_size_t]),
+        "rvk_memcpy_d2d": (i, [vp, vp, vp, C.c_size_t]),
+        "rvk_scalar_eval": (i, [vp, Scalar, vp]),
+        "rvk_scalar_read": (i, [vp, vp, C.POINTER(d)]),
+        "rvk_dot": (i, [vp, i64, vp, vp, vp]),
+        "rvk_nrm2": (i, [vp, i64, vp, vp]),
+        "rvk_dot2": (i, [vp, i64, vp, vp, vp, vp]),
+        "rvk_axpy": (i, [vp, i64, Scalar, vp, vp]),
+        "rvk_aypx": (i, [vp, i64, Scalar, vp, vp]),
+        "rvk_waxpy": (i, [vp, i64, Scalar, vp, vp, vp]),
+        "rvk_scale": (i, [vp, i64, Scalar, vp]),
+        "rvk_pointwise_mult": (i, [vp, i64, vp, vp, vp]),
+        "rvk_copy": (i, [vp, i64, vp, vp]),
+        "rvk_set": (i, [vp, i64, d, vp]),
+        "rvk_csr_spmv": (i, [vp, C.POINTER(Csr), vp, vp]),
+        "rvk_csr_diagonal": (i, [vp, C.POINTER(Csr), vp]),
+        "rvk_csr_diagonal_inverse": (i, [vp, C.POINTER(Csr), vp]),
+        "rvk_csr_validate": (i, [vp, C.POINTER(Csr), C.POINTER(i64)]),
+        "rvk_laplacian_size": (i, [i, i, i64, i64, i64, C.POINTER(i64), C.POINTER(i64)]),
+        "rvk_build_laplacian": (i, [vp, i, i, i64, i64, i64, vp, vp, vp]),
+        "rvk_fill_rhs": (i, [vp, C.c_uint64, i64, vp]),
+        "rvk_cg_plan_create": (i, [vp, C.POINTER(Csr), CgConfig, C.POINTER(vp)]),
+        "rvk_cg_plan_destroy": (i, [vp]),
+        "rvk_cg_solve_dev": (i, [vp, vp, vp]),
+        "rvk_cg_history_dev": (vp, [vp]),
+        "rvk_cg_result": (i, [vp, vp, C.POINTER(CgInfo)]),
+        "rvk_cg_solve_host": (i, [vp, vp, vp, vp, C.POINTER(CgInfo)]),
+        "rvk_cg_set_profiling": (i, [vp, i]),
+        "rvk_cg_kernel_times": (i, [vp, C.POINTER(C.c_float), C.POINTER(C.c_float),
+                                    C.POINTER(C.c_int)]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = L
+    return L
+
+
+def check(status: int) -> None:
+    if status != RVK_OK:
+        msg = lib().rvk_last_error().decode(errors="replace")
+        raise RvkError(status, msg)
+
+
+def host_syncs() -> int:
+    return int(lib().rvk_host_sync_count())
+
+
+def device_info():
+    n = C.c_int(0)
+    name = C.create_string_buffer(128)
+    check(lib().rvk_device_info(C.byref(n), name, 128))
+    return n.value, name.value.decode()
+
+
+def _ptr(a: np.ndarray) -> int:
+    assert a.flags["C_CONTIGUOUS"]
+    return a.ctypes.data
+
+
+class Ctx:
+    """rvk_ctx: one CUDA stream + reduction scratch (PetscDeviceContext)."""
+
+    def __init__(self, stream: int | None = None):
+        h = C.c_void_p()
+        check(lib().rvk_ctx_create(stream, C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if self.h:
+            lib().rvk_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def stream(self) -> int:
+        return lib().rvk_ctx_stream(self.h)
+
+    def synchronize(self):
+        check(lib().rvk_ctx_synchronize(self.h))
+
+    def idle(self) -> bool:
+        v = C.c_int(0)
+        check(lib().rvk_ctx_query_idle(self.h, C.byref(v)))
+        return bool(v.value)
+
+    def wait_for(self, other: "Ctx"):
+        check(lib().rvk_ctx_wait_for(self.h, other.h))
+
+
+class DeviceArray:
+    """Owning device buffer (plumbing for tests/bench)."""
+
+    def __init__(self, n: int, dtype=np.float64):
+        self.n = int(n)
+        self.dtype = np.dtype(dtype)
+        p = C.c_void_p()
+        check(lib().rvk_malloc(C.byref(p), max(self.n, 1) * self.dtype.itemsize))
+        self.ptr = p.value
+
+    @classmethod
+    def from_host(cls, ctx: Ctx, a: np.ndarray):
+        a = np.ascontiguousarray(a)
+        d = cls(a.shape[0], a.dtype)
+        d.upload(ctx, a)
+        return d
+
+    @property
+    def nbytes(self) -> int:
+        return self.n * self.dtype.itemsize
+
+    def upload(self, ctx: Ctx, a: np.ndarray):
+        a = np.ascontiguousarray(a, self.dtype)
+        assert a.shape[0] == self.n
+        check(lib().rvk_memcpy_h2d(ctx.h, self.ptr, _ptr(a), self.nbytes))
+        ctx.synchronize()
+
+    def download(self, ctx: Ctx) -> np.ndarray:
+        out = np.empty(self.n, self.dtype)
+        check(lib().rvk_memcpy_d2h(ctx.h, _ptr(out), self.ptr, self.nbytes))
+        ctx.synchronize()
+        return out
+
+    def free(self):
+        if self.ptr:
+            lib().rvk_free(self.ptr)
+            self.ptr = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def scalar_const(c: float) -> Scalar:
+    return Scalar(SCALAR_CONST, c, None, None)
+
+
+def scalar_ptr(p: int, kind: int = SCALAR_PTR, p1: int | None = None) -> Scalar:
+    return Scalar(kind, 0.0, p, p1)
+
+
+class DeviceCsr:
+    """CSR on device (int64 offsets, int32 columns, float64 values)."""
+
+    def __init__(self, n_rows, n_cols, off: DeviceArray, cols: DeviceArray, vals: DeviceArray):
+        self.n_rows, self.n_cols = int(n_rows), int(n_cols)
+        self.off, self.cols, self.vals = off, cols, vals
+        self.nnz = cols.n
+        self.c = Csr(self.n_rows, self.n_cols, self.nnz, off.ptr, cols.ptr, vals.ptr)
+
+    @classmethod
+    def from_host(cls, ctx: Ctx, n_rows, n_cols, off, cols, vals):
+        return cls(n_rows, n_cols, DeviceArray.from_host(ctx, np.asarray(off, np.int64)),
+                   DeviceArray.from_host(ctx, np.asarray(cols, np.int32)),
+                   DeviceArray.from_host(ctx, np.asarray(vals, np.float64)))
+
+    @classmethod
+    def laplacian(cls, ctx: Ctx, dim: int, points: int, grid):
+        """Device-side assembly (rvk_build_laplacian)."""
+        nx, ny, nz = (list(grid) + [1, 1])[:3]
+        n, nnz = C.c_int64(), C.c_int64()
+        check(lib().rvk_laplacian_size(dim, points, nx, ny, nz, C.byref(n), C.byref(nnz)))
+        off = DeviceArray(n.value + 1, np.int64)
+        cols = DeviceArray(nnz.value, np.int32)
+        vals = DeviceArray(nnz.value, np.float64)
+        check(lib().rvk_build_laplacian(ctx.h, dim, points, nx, ny, nz, off.ptr, cols.ptr,
+                                        vals.ptr))
+        return cls(n.value, n.value, off, cols, vals)
+
+    def validate(self, ctx: Ctx) -> int:
+        ml = C.c_int64()
+        check(lib().rvk_csr_validate(ctx.h, C.byref(self.c), C.byref(ml)))
+        return ml.value
+
+    def spmv(self, ctx: Ctx, x: DeviceArray, y: DeviceArray):
+        check(lib().rvk_csr_spmv(ctx.h, C.byref(self.c), x.ptr, y.ptr))
+
+
+@dataclass
+class CgResult:
+    hist: np.ndarray
+    state: int
+    iterations: int
+    breakdown_iter: int
+
+
+class CgPlan:
+    """KSPSetUp + KSPSolve for Jacobi-PCG (rvk_cg_plan_*)."""
+
+    def __init__(self, ctx: Ctx, A: DeviceCsr, max_it: int = 20, pc: str = "jacobi",
+                 rtol: float = 0.0, atol: float = 0.0, mode: str = "fused",
+                 use_graph: bool = True):
+        self.ctx, self.A = ctx, A
+        self.max_it = max_it
+        cfg = CgConfig(max_it, PC_JACOBI if pc == "jacobi" else PC_NONE, rtol, atol,
+                       MODE_FUSED if mode == "fused" else MODE_UNFUSED, 1 if use_graph else 0)
+        h = C.c_void_p()
+        check(lib().rvk_cg_plan_create(ctx.h, C.byref(A.c), cfg, C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if self.h:
+            lib().rvk_cg_plan_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def solve_dev(self, b: DeviceArray, x: DeviceArray):
+        check(lib().rvk_cg_solve_dev(self.h, b.ptr, x.ptr))
+
+    def result(self, raise_breakdown: bool = True) -> CgResult:
+        hist = np.full(self.max_it + 1, np.nan)
+        info = CgInfo()
+        st = lib().rvk_cg_result(self.h, _ptr(hist), C.byref(info))
+        res = CgResult(hist[: info.iterations + 1].copy(), info.state, info.iterations,
+                       info.breakdown_iter)
+        if st == RVK_ERR_BREAKDOWN:
+            if raise_breakdown:
+                raise BreakdownError(st, lib().rvk_last_error().decode(), info.breakdown_iter)
+            return res
+        check(st)
+        return res
+
+    def solve_host(self, b: np.ndarray, x_out: np.ndarray | None = None, hist_out=None):
+        b = np.ascontiguousarray(b, np.float64)
+        x = x_out if x_out is not None else np.empty_like(b)
+        hist = hist_out if hist_out is not None else np.full(self.max_it + 1, np.nan)
+        info = CgInfo()
+        st = lib().rvk_cg_solve_host(self.h, _ptr(b), _ptr(x), _ptr(hist), C.byref(info))
+        if st not in (RVK_OK, RVK_ERR_BREAKDOWN):
+            check(st)
+        return x, CgResult(hist[: info.iterations + 1].copy(), info.state, info.iterations,
+                           info.breakdown_iter)
+
+    def set_profiling(self, on: bool):
+        check(lib().rvk_cg_set_profiling(self.h, 1 if on else 0))
+
+    def kernel_times(self):
+        a, b, n = C.c_float(), C.c_float(), C.c_int()
+        check(lib().rvk_cg_kernel_times(self.h, C.byref(a), C.byref(b), C.byref(n)))
+        return a.value, b.value, n.value
+
+    def launches(self) -> int:
+        n = C.c_int()
+        lib().rvk_cg_kernel_times(self.h, None, None, C.byref(n))
+        return n.value
