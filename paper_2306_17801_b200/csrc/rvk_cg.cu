@@ -130,6 +130,7 @@ struct CgSpmvOp {
     double* __restrict__ p_new;
     double* __restrict__ w;
     CgState* st;
+    int64_t  n;
     int      it;
     double   b; // set by init()
 
@@ -150,14 +151,25 @@ struct CgSpmvOp {
         }
         return true;
     }
-    __device__ __forceinline__ double src(int32_t j) const
+    __device__ __forceinline__ int64_t n_src() const { return n; } // square: n_cols == n_rows
+    struct Fetch {
+        double z, p;
+    };
+    __device__ __forceinline__ Fetch fetch(int32_t j) const
     {
-        if (FIRST) return __ldg(z + j);
-        return aypx1(b, __ldg(z + j), __ldg(p_old + j)); // z + b*p  (kernels_scalar.cpp:33)
+        return Fetch{__ldg(z + j), FIRST ? 0.0 : __ldg(p_old + j)};
     }
-    __device__ __forceinline__ double row(int64_t i, double sum, double acc) const
+    __device__ __forceinline__ double value(const Fetch& f) const
     {
-        const double p = src((int32_t)i);
+        return FIRST ? f.z : aypx1(b, f.z, f.p); // z + b*p  (kernels_scalar.cpp:33)
+    }
+    __device__ __forceinline__ double src(int32_t j) const { return value(fetch(j)); }
+    // own = SRC(i) when the row holds its diagonal (always, for the
+    // stencils): reuse the gathered value instead of reloading z[i], p[i].
+    __device__ __forceinline__ double row(int64_t i, double sum, double acc, double own,
+                                          bool have_own) const
+    {
+        const double p = have_own ? own : src((int32_t)i);
         p_new[i]       = p;
         w[i]           = sum;
         return add(acc, mul(p, sum));
@@ -439,20 +451,20 @@ rvk_status enqueue_fused(rvk_cg_plan P, const double* b, double* x)
     for (int it = 0; it < P->cfg.max_it; ++it) {
         const double* p_old = P->p[it & 1];
         double*       p_new = P->p[(it + 1) & 1];
-        if (P->profiling) RVK_CUDA(cudaEventRecord(P->ev[4 * it + 0], s));
+        if (P->profiling) RVK_CUDA(cudaEventRecordWithFlags(P->ev[4 * it + 0], s, cudaEventRecordExternal));
         rvk_status rc;
         if (it == 0) {
-            CgSpmvOp<true> op{P->z, p_old, p_new, P->w, P->st, it, 0.0};
+            CgSpmvOp<true> op{P->z, p_old, p_new, P->w, P->st, n, it, 0.0};
             rc = launch_spmv(s, sa, op, ta, P->spmv_grid);
         } else {
-            CgSpmvOp<false> op{P->z, p_old, p_new, P->w, P->st, it, 0.0};
+            CgSpmvOp<false> op{P->z, p_old, p_new, P->w, P->st, n, it, 0.0};
             rc = launch_spmv(s, sa, op, ta, P->spmv_grid);
         }
         if (rc != RVK_OK) return rc;
         ++P->launches;
         if (P->profiling) {
-            RVK_CUDA(cudaEventRecord(P->ev[4 * it + 1], s));
-            RVK_CUDA(cudaEventRecord(P->ev[4 * it + 2], s));
+            RVK_CUDA(cudaEventRecordWithFlags(P->ev[4 * it + 1], s, cudaEventRecordExternal));
+            RVK_CUDA(cudaEventRecordWithFlags(P->ev[4 * it + 2], s, cudaEventRecordExternal));
         }
 #define RVK_UPD(V, J)                                                                          \
     k_cg_update<V, J><<<ug, kUpdThreads, 0, s>>>(n, p_new, P->w, P->dinv, x, P->r, P->z, P->st, \
@@ -462,7 +474,7 @@ rvk_status enqueue_fused(rvk_cg_plan P, const double* b, double* x)
 #undef RVK_UPD
         RVK_CHECK_LAUNCH("k_cg_update");
         ++P->launches;
-        if (P->profiling) RVK_CUDA(cudaEventRecord(P->ev[4 * it + 3], s));
+        if (P->profiling) RVK_CUDA(cudaEventRecordWithFlags(P->ev[4 * it + 3], s, cudaEventRecordExternal));
     }
     return RVK_OK;
 }
@@ -510,15 +522,16 @@ rvk_status enqueue_unfused(rvk_cg_plan P, const double* b, double* x)
             RVK_TRY(vec_ew(s, EW_AYPX, n, bb, P->z, p, p, g));             // p = z + b p
             ++P->launches;
         }
-        if (P->profiling) RVK_CUDA(cudaEventRecord(P->ev[4 * it + 0], s));
+        if (P->profiling) RVK_CUDA(cudaEventRecordWithFlags(P->ev[4 * it + 0], s, cudaEventRecordExternal));
         SpmvGuardedOp op;
         op.x     = p;
         op.y     = P->w;
+        op.ncols = P->A.n_cols;
         op.guard = g;
         RVK_TRY(launch_spmv(s, sa, op, TailArgs{nullptr, nullptr}, P->spmv_grid)); // w = A p
         if (P->profiling) {
-            RVK_CUDA(cudaEventRecord(P->ev[4 * it + 1], s));
-            RVK_CUDA(cudaEventRecord(P->ev[4 * it + 2], s));
+            RVK_CUDA(cudaEventRecordWithFlags(P->ev[4 * it + 1], s, cudaEventRecordExternal));
+            RVK_CUDA(cudaEventRecordWithFlags(P->ev[4 * it + 2], s, cudaEventRecordExternal));
         }
         RVK_TRY(vec_reduce(s, sc, RED_DOT, n, p, P->w, &st->pAp, nullptr, g));       // a = p.w
         k_unfused_alpha<<<1, 1, 0, s>>>(st, it);                                    // a = beta/a
@@ -532,7 +545,7 @@ rvk_status enqueue_unfused(rvk_cg_plan P, const double* b, double* x)
         k_unfused_hist<<<1, 1, 0, s>>>(st, P->hist, it, P->cfg.rtol, P->cfg.atol);
         RVK_CHECK_LAUNCH("k_unfused_hist");
         RVK_TRY(vec_reduce(s, sc, RED_DOT, n, P->z, P->r, &st->beta, nullptr, g));  // beta = z.r
-        if (P->profiling) RVK_CUDA(cudaEventRecord(P->ev[4 * it + 3], s));
+        if (P->profiling) RVK_CUDA(cudaEventRecordWithFlags(P->ev[4 * it + 3], s, cudaEventRecordExternal));
         P->launches += 10;
     }
     return RVK_OK;
@@ -598,12 +611,14 @@ rvk_status rvk_csr_spmv(rvk_ctx ctx, const rvk_csr* A, const double* x, double* 
     if (!ctx || !A) return set_error(RVK_ERR_INVALID, "csr_spmv: null argument");
     if (A->n_rows == 0) return RVK_OK;
     if (!x || !y) return set_error(RVK_ERR_INVALID, "csr_spmv: null vector");
+    if (A->nnz == 0) return rvk_set(ctx, A->n_rows, 0.0, y); // every row empty: y = 0
     // Tile height from the mean row length (no host sync on this path);
     // tiles that overflow a stage fall back to direct global reads.
     const int64_t avg = (A->nnz + A->n_rows - 1) / A->n_rows;
     SpmvPlainOp   op;
-    op.x = x;
-    op.y = y;
+    op.x     = x;
+    op.y     = y;
+    op.ncols = A->n_cols;
     return launch_spmv(ctx->stream, make_spmv_args(*A, spmv_rows_per_tile(avg)), op,
                        TailArgs{nullptr, nullptr}, sm_count());
 }

@@ -73,6 +73,94 @@ struct TailArgs {
     unsigned int* ticket;
 };
 
+// Rows processed concurrently per consumer thread, and columns per batch.
+// Each pass a thread owns G rows (lr, lr+256, ...); for every batch of 8
+// columns it first reads all G*8 (col, val) pairs (LDS from the stage, or
+// LDG for direct tiles), then issues all G*8 gathers, then folds them into
+// the per-row sums strictly left to right -- so the memory-level
+// parallelism is G*8 gathers per thread while each row's sum keeps the
+// reference's sequential order.
+constexpr int kSpmvRowGroup = 2;
+constexpr int kSpmvBatch    = 8;
+
+template <int G, typename IDX, class Op>
+__device__ __forceinline__ double spmv_rows(const Op& op, double acc, int ctid, int rows,
+                                            int64_t r0, const int64_t* __restrict__ O,
+                                            int64_t kbase, const int32_t* __restrict__ Cc,
+                                            const double* __restrict__ V)
+{
+    // IDX = int for staged tiles (indices local to the stage: value k lives at
+    // V[k - kbase], its column at Cc[k - kbase]), int64_t for direct tiles.
+    for (int base = ctid; base < rows; base += G * kSpmvConsumers) {
+        IDX     kb[G], ke[G], last[G];
+        int32_t safe[G];
+        int     len = 0;
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            const int  lr = base + g * kSpmvConsumers;
+            const bool in = lr < rows;
+            kb[g]         = in ? (IDX)(O[lr] - kbase) : (IDX)0;
+            ke[g]         = in ? (IDX)(O[lr + 1] - kbase) : (IDX)0;
+            len           = max(len, (int)(ke[g] - kb[g]));
+            // dead slots re-read a valid entry (nnz >= 1 is guaranteed by the
+            // host) and gather a valid index; they never reach the sum
+            last[g] = ke[g] > kb[g] ? ke[g] - 1 : (kb[g] > 0 ? kb[g] - 1 : (IDX)0);
+            const int64_t row = r0 + lr;
+            safe[g]           = (int32_t)(in && row < op.n_src() ? row : 0);
+        }
+        double sum[G], own[G];
+        bool   have_own[G];
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            sum[g]      = 0.0;
+            own[g]      = 0.0;
+            have_own[g] = false;
+        }
+        for (int k = 0; k < len; k += kSpmvBatch) {
+            // Branch-free batch: (1) all column/value reads, (2) all gathers,
+            // (3) the per-row sums strictly left to right (dead slots dropped
+            // by a select), so every load of the batch is in flight together.
+            int32_t c[G][kSpmvBatch];
+            double  v[G][kSpmvBatch];
+            bool    ok[G][kSpmvBatch];
+#pragma unroll
+            for (int g = 0; g < G; ++g)
+#pragma unroll
+                for (int u = 0; u < kSpmvBatch; ++u) {
+                    const IDX kk = kb[g] + (IDX)(k + u);
+                    ok[g][u]     = kk < ke[g];
+                    const IDX ks = ok[g][u] ? kk : last[g];
+                    c[g][u]      = ok[g][u] ? Cc[ks] : safe[g];
+                    v[g][u]      = V[ks];
+                }
+            typename Op::Fetch f[G][kSpmvBatch];
+#pragma unroll
+            for (int g = 0; g < G; ++g)
+#pragma unroll
+                for (int u = 0; u < kSpmvBatch; ++u) f[g][u] = op.fetch(c[g][u]);
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                const int32_t row = (int32_t)(r0 + base + g * kSpmvConsumers);
+#pragma unroll
+                for (int u = 0; u < kSpmvBatch; ++u) {
+                    const double x = op.value(f[g][u]);
+                    const double t = add(sum[g], mul(v[g][u], x));
+                    sum[g]         = ok[g][u] ? t : sum[g];
+                    const bool d   = ok[g][u] && c[g][u] == row;
+                    own[g]         = d ? x : own[g];
+                    have_own[g]    = have_own[g] || d;
+                }
+            }
+        }
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            const int lr = base + g * kSpmvConsumers;
+            if (lr < rows) acc = op.row(r0 + lr, sum[g], acc, own[g], have_own[g]);
+        }
+    }
+    return acc;
+}
+
 template <class Op>
 __global__ void __launch_bounds__(kSpmvThreads, 1) k_spmv_tma(SpmvArgs A, Op op_in, TailArgs tail)
 {
@@ -160,35 +248,18 @@ __global__ void __launch_bounds__(kSpmvThreads, 1) k_spmv_tma(SpmvArgs A, Op op_
         mbar_wait(&full[s], (j / kSpmvStages) & 1);
         const int64_t r0   = t * A.R;
         const int     rows = (int)min((int64_t)A.R, A.n_rows - r0);
-        const bool    direct = meta[s].direct != 0;
-        unsigned char* st = stage0 + (size_t)s * sbytes;
-        const int64_t* O  = direct ? A.off + r0 : reinterpret_cast<const int64_t*>(st);
-        const double*  V  = direct ? A.vals
-                                   : reinterpret_cast<const double*>(st + obytes) - meta[s].kv0;
-        const int32_t* Cc = direct ? A.cols
-                                   : reinterpret_cast<const int32_t*>(st + obytes +
-                                                                      SpmvLayout::val_bytes()) -
-                                         meta[s].kc0;
-        for (int lr = ctid; lr < rows; lr += kSpmvConsumers) {
-            const int64_t kb = O[lr], ke = O[lr + 1];
-            double        sum = 0.0;
-            for (int64_t k = kb; k < ke; k += 8) {
-                double  v[8];
-                int32_t c[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const bool ok = k + u < ke;
-                    c[u] = ok ? Cc[k + u] : 0;
-                    v[u] = ok ? V[k + u] : 0.0;
-                }
-                double xv[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) xv[u] = (k + u < ke) ? op.src(c[u]) : 0.0;
-#pragma unroll
-                for (int u = 0; u < 8; ++u)
-                    if (k + u < ke) sum = add(sum, mul(v[u], xv[u]));
-            }
-            acc = op.row(r0 + lr, sum, acc);
+        if (meta[s].direct) {
+            acc = spmv_rows<kSpmvRowGroup, int64_t>(op, acc, ctid, rows, r0, A.off + r0, 0,
+                                                    A.cols, A.vals);
+        } else {
+            unsigned char* st  = stage0 + (size_t)s * sbytes;
+            const int64_t  kv0 = meta[s].kv0;
+            // columns were copied from kc0 <= kv0: shift so both share kv0-local indices
+            const int32_t* cs = reinterpret_cast<const int32_t*>(st + obytes + SpmvLayout::val_bytes()) +
+                                (kv0 - meta[s].kc0);
+            acc = spmv_rows<kSpmvRowGroup, int>(op, acc, ctid, rows, r0,
+                                                reinterpret_cast<const int64_t*>(st), kv0, cs,
+                                                reinterpret_cast<const double*>(st + obytes));
         }
         __syncwarp();
         if ((ctid & 31) == 0) mbar_arrive(&empty[s]);
@@ -212,9 +283,15 @@ struct SpmvPlainOp {
     static constexpr bool kHasTail = false;
     const double* __restrict__ x;
     double* __restrict__ y;
-    __device__ __forceinline__ bool   init() { return true; }
-    __device__ __forceinline__ double src(int32_t j) const { return __ldg(x + j); }
-    __device__ __forceinline__ double row(int64_t i, double sum, double acc) const
+    int64_t ncols;
+    __device__ __forceinline__ bool    init() { return true; }
+    __device__ __forceinline__ int64_t n_src() const { return ncols; }
+    struct Fetch {
+        double x;
+    };
+    __device__ __forceinline__ Fetch  fetch(int32_t j) const { return Fetch{__ldg(x + j)}; }
+    __device__ __forceinline__ double value(const Fetch& f) const { return f.x; }
+    __device__ __forceinline__ double row(int64_t i, double sum, double acc, double, bool) const
     {
         y[i] = sum;
         return acc;
