@@ -151,7 +151,6 @@ struct CgSpmvOp {
         }
         return true;
     }
-    __device__ __forceinline__ int64_t n_src() const { return n; } // square: n_cols == n_rows
     struct Fetch {
         double z, p;
     };
@@ -164,12 +163,11 @@ struct CgSpmvOp {
         return FIRST ? f.z : aypx1(b, f.z, f.p); // z + b*p  (kernels_scalar.cpp:33)
     }
     __device__ __forceinline__ double src(int32_t j) const { return value(fetch(j)); }
-    // own = SRC(i) when the row holds its diagonal (always, for the
-    // stencils): reuse the gathered value instead of reloading z[i], p[i].
-    __device__ __forceinline__ double row(int64_t i, double sum, double acc, double own,
-                                          bool have_own) const
+    using Own = Fetch;
+    __device__ __forceinline__ Own own_fetch(int64_t i) const { return fetch((int32_t)i); }
+    __device__ __forceinline__ double row(int64_t i, double sum, double acc, const Own& o) const
     {
-        const double p = have_own ? own : src((int32_t)i);
+        const double p = value(o); // p_new[i] = z[i] + b p_old[i]
         p_new[i]       = p;
         w[i]           = sum;
         return add(acc, mul(p, sum));
@@ -208,29 +206,52 @@ __global__ void __launch_bounds__(kUpdThreads)
     const int64_t     stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t     t0     = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (VEC) {
-        const int64_t n2 = n >> 1;
-        for (int64_t i = t0; i < n2; i += stride) {
-            const double2 pi = ld_stream(reinterpret_cast<const double2*>(p) + i);
-            const double2 wi = ld_stream(reinterpret_cast<const double2*>(w) + i);
-            double2       xi = ld_stream(reinterpret_cast<const double2*>(x) + i);
-            double2       ri = ld_stream(reinterpret_cast<const double2*>(r) + i);
+        // two double2 per thread per trip: 10 independent 16-B loads in flight
+        const int64_t  n2 = n >> 1;
+        const double2* p2 = reinterpret_cast<const double2*>(p);
+        const double2* w2 = reinterpret_cast<const double2*>(w);
+        const double2* d2 = reinterpret_cast<const double2*>(dinv);
+        double2*       x2 = reinterpret_cast<double2*>(x);
+        double2*       r2 = reinterpret_cast<double2*>(r);
+        double2*       z2 = reinterpret_cast<double2*>(z);
+        auto step = [&](const double2& pi, const double2& wi, double2 xi, double2 ri,
+                        const double2& d, int64_t i) {
             xi.x = axpy1(a, pi.x, xi.x);
             xi.y = axpy1(a, pi.y, xi.y);
             ri.x = axpy1(na, wi.x, ri.x);
             ri.y = axpy1(na, wi.y, ri.y);
             double2 zi = ri;
             if (JACOBI) {
-                const double2 d = ld_stream(reinterpret_cast<const double2*>(dinv) + i);
                 zi.x = mul(d.x, ri.x);
                 zi.y = mul(d.y, ri.y);
             }
-            st_stream(reinterpret_cast<double2*>(x) + i, xi);
-            reinterpret_cast<double2*>(r)[i] = ri;
-            reinterpret_cast<double2*>(z)[i] = zi;
+            st_stream(x2 + i, xi);
+            r2[i] = ri;
+            z2[i] = zi;
             acc[0] = add(acc[0], mul(zi.x, zi.x));
             acc[0] = add(acc[0], mul(zi.y, zi.y));
             acc[1] = add(acc[1], mul(zi.x, ri.x));
             acc[1] = add(acc[1], mul(zi.y, ri.y));
+        };
+        int64_t i = t0;
+        for (; i + stride < n2; i += 2 * stride) {
+            const int64_t j  = i + stride;
+            const double2 pa = ld_stream(p2 + i), pb = ld_stream(p2 + j);
+            const double2 wa = ld_stream(w2 + i), wb = ld_stream(w2 + j);
+            const double2 xa = ld_stream(x2 + i), xb = ld_stream(x2 + j);
+            const double2 ra = ld_stream(r2 + i), rb = ld_stream(r2 + j);
+            double2 da = make_double2(0, 0), db = make_double2(0, 0);
+            if (JACOBI) {
+                da = ld_stream(d2 + i);
+                db = ld_stream(d2 + j);
+            }
+            step(pa, wa, xa, ra, da, i);
+            step(pb, wb, xb, rb, db, j);
+        }
+        if (i < n2) {
+            double2 d = make_double2(0, 0);
+            if (JACOBI) d = ld_stream(d2 + i);
+            step(ld_stream(p2 + i), ld_stream(w2 + i), ld_stream(x2 + i), ld_stream(r2 + i), d, i);
         }
     }
     for (int64_t i = (VEC ? (n & ~int64_t(1)) : 0) + t0; i < n; i += stride) {
@@ -380,6 +401,21 @@ __global__ void k_validate(int64_t n, int64_t n_cols, int64_t nnz, const int64_t
     if (ml) atomicMax(maxlen, ml);
 }
 
+// Largest grid that is fully resident (one wave): blocks/SM from the
+// occupancy calculator times the SM count.  Grid-stride kernels launched with
+// more blocks than this run a second, equally long wave.
+template <class K>
+int resident_grid(K kernel, int threads, int64_t n_items)
+{
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, 0) != cudaSuccess ||
+        per_sm < 1)
+        per_sm = 1;
+    const int64_t want = (n_items + threads - 1) / threads;
+    const int64_t cap  = (int64_t)sm_count() * per_sm;
+    return (int)(want < 1 ? 1 : (want > cap ? cap : want));
+}
+
 int update_grid(int64_t n)
 {
     const int64_t want = (n / 2 + kUpdThreads - 1) / kUpdThreads;
@@ -397,7 +433,8 @@ struct rvk_cg_plan_s {
     rvk_ctx       ctx = nullptr;
     rvk_csr       A{};
     rvk_cg_config cfg{};
-    int           R = 0, spmv_grid = 0, upd_grid = 0;
+    SpmvArgs      sa{};
+    int           spmv_grid = 0, upd_grid = 0, setup_grid = 0;
     double*       dinv = nullptr;
     double*       r = nullptr;
     double*       z = nullptr;
@@ -438,7 +475,7 @@ rvk_status enqueue_fused(rvk_cg_plan P, const double* b, double* x)
     P->launches         = 0;
 
 #define RVK_SETUP(V, J)                                                                        \
-    k_cg_setup<V, J><<<ug, kUpdThreads, 0, s>>>(n, b, P->dinv, x, P->r, P->z, P->st, P->hist,  \
+    k_cg_setup<V, J><<<P->setup_grid, kUpdThreads, 0, s>>>(n, b, P->dinv, x, P->r, P->z, P->st, P->hist,  \
                                                 rtol, atol, part0, tk0)
     if (vec) { if (jac) RVK_SETUP(true, true); else RVK_SETUP(true, false); }
     else { if (jac) RVK_SETUP(false, true); else RVK_SETUP(false, false); }
@@ -446,7 +483,7 @@ rvk_status enqueue_fused(rvk_cg_plan P, const double* b, double* x)
     RVK_CHECK_LAUNCH("k_cg_setup");
     ++P->launches;
 
-    const SpmvArgs sa = make_spmv_args(P->A, P->R);
+    const SpmvArgs& sa = P->sa;
     const TailArgs ta{part1, tk1};
     for (int it = 0; it < P->cfg.max_it; ++it) {
         const double* p_old = P->p[it & 1];
@@ -510,7 +547,7 @@ rvk_status enqueue_unfused(rvk_cg_plan P, const double* b, double* x)
     P->launches += 5;
 
     double*        p  = P->p[0];
-    const SpmvArgs sa = make_spmv_args(P->A, P->R);
+    const SpmvArgs& sa = P->sa;
     for (int it = 0; it < P->cfg.max_it; ++it) {
         if (it == 0) {
             k_guarded_copy<<<update_grid(n), kUpdThreads, 0, s>>>(n, P->z, p, g);
@@ -526,7 +563,6 @@ rvk_status enqueue_unfused(rvk_cg_plan P, const double* b, double* x)
         SpmvGuardedOp op;
         op.x     = p;
         op.y     = P->w;
-        op.ncols = P->A.n_cols;
         op.guard = g;
         RVK_TRY(launch_spmv(s, sa, op, TailArgs{nullptr, nullptr}, P->spmv_grid)); // w = A p
         if (P->profiling) {
@@ -616,10 +652,9 @@ rvk_status rvk_csr_spmv(rvk_ctx ctx, const rvk_csr* A, const double* x, double* 
     // tiles that overflow a stage fall back to direct global reads.
     const int64_t avg = (A->nnz + A->n_rows - 1) / A->n_rows;
     SpmvPlainOp   op;
-    op.x     = x;
-    op.y     = y;
-    op.ncols = A->n_cols;
-    return launch_spmv(ctx->stream, make_spmv_args(*A, spmv_rows_per_tile(avg)), op,
+    op.x = x;
+    op.y = y;
+    return launch_spmv(ctx->stream, make_spmv_args(*A, avg + avg / 4 + 1), op,
                        TailArgs{nullptr, nullptr}, sm_count());
 }
 
@@ -661,9 +696,11 @@ rvk_status rvk_cg_plan_create(rvk_ctx ctx, const rvk_csr* A, rvk_cg_config cfg, 
     P->ctx       = ctx;
     P->A         = *A;
     P->cfg       = cfg;
-    P->R         = spmv_rows_per_tile(maxlen);
+    P->sa        = make_spmv_args(*A, maxlen);
     P->spmv_grid = sm_count();
-    P->upd_grid  = update_grid(A->n_rows);
+    // one resident wave each (the vectorised loops take 2 elements per thread)
+    P->upd_grid   = resident_grid(k_cg_update<true, true>, kUpdThreads, (A->n_rows + 1) / 2);
+    P->setup_grid = resident_grid(k_cg_setup<true, true>, kUpdThreads, (A->n_rows + 1) / 2);
     const size_t vb = (size_t)A->n_rows * sizeof(double);
     cudaError_t  e  = cudaSuccess;
     auto alloc = [&](void** p, size_t bytes) {

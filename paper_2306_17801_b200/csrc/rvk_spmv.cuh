@@ -5,35 +5,46 @@
 // 0.0, left to right, each product rounded before it is added), so the result
 // is bit-identical to rivulet::kernels::scalar::csr_spmv when SRC(j) = x[j].
 //
-// Design (B200-first, HBM-bound: ~12 B/nnz of streamed CSR + gathers):
-//  * persistent grid, one CTA per SM (148 on B200), tiles of R consecutive
-//    rows assigned round-robin (deterministic, and it keeps the rows in
-//    flight chip-wide inside a narrow window so the x-gather reuses L2);
-//  * warp-specialised: warp 0 is the producer -- one elected lane issues
+// Design (B200-first; HBM-bound: 12 B/nnz of streamed CSR + gathers):
+//  * persistent grid, one CTA per SM (148 on B200); tiles of R consecutive
+//    rows assigned round-robin, so the rows in flight chip-wide stay inside a
+//    narrow window and the x-gather is served by L2;
+//  * warp-specialised: warp 0 is the producer -- one lane issues
 //    cp.async.bulk (TMA bulk copies, UBLKCP in SASS) of the tile's row
-//    offsets, values and column indices into a STAGES-deep shared-memory
-//    ring, with mbarrier full/empty handshakes and an L2 evict_first policy
-//    for the streamed-once CSR bytes;
-//  * warps 1..8 (256 consumer threads) each own rows tid, tid+256, ... of the
-//    tile and walk them sequentially out of shared memory (row stride of an
-//    odd nnz/row => conflict-free 64-bit LDS), gathering SRC(j) through L1/L2;
-//  * tiles that do not fit a stage (long rows) and the very last tile (whose
-//    16-byte-rounded bulk range could run past the arrays) are marked
-//    "direct": consumers read them straight from global memory instead.
-//  * Op supplies SRC(j), the per-row epilogue and the reduction tail, so the
-//    same mainloop serves mat_mult and the fused CG kernel
-//    (p = z + b p on the fly; w = A p; p.w partial; alpha tail).
+//    offsets, values and column indices into an S-deep shared-memory ring
+//    (S, R and the stage capacity are sized per matrix at plan time), with
+//    mbarrier full/empty handshakes and an L2 evict_first policy on the
+//    streamed-once CSR bytes;
+//  * warps 1..16 consume: lane-per-row (consecutive lanes own consecutive
+//    rows, so for banded/stencil matrices every gather instruction of a warp
+//    hits one contiguous run -- perfectly coalesced), reading (col, val) from
+//    the stage with LDS; per batch of 8 nonzeros a thread first reads all
+//    8 pairs, then issues all 8 gathers, then adds the rounded products
+//    strictly left to right (the reference's order => bit-exact).  When a
+//    tile is shorter than the 512 consumer threads (long rows, e.g. 27-point:
+//    R = 128) the consumers split into NG groups that work on NG different
+//    ring stages at once, so no thread idles;
+//  * tiles that do not fit a stage (very long rows) and the last tile (whose
+//    16-byte-rounded bulk range could run past the arrays) are "direct":
+//    consumers read them from global memory thread-per-row;
+//  * Op supplies SRC(j) (split into raw fetch + arithmetic so every gather is
+//    issued before any is consumed), the per-row epilogue and the reduction
+//    tail, so the same mainloop serves mat_mult and the fused CG kernel
+//    (p = z + b p on the fly; w = A p; p.w partials; alpha tail).
 #pragma once
 
 #include "rvk_common.cuh"
 
 namespace rvk {
 
-constexpr int kSpmvConsumers = 256;               // 8 consumer warps
-constexpr int kSpmvThreads   = kSpmvConsumers + 32; // + producer warp
-constexpr int kSpmvStages    = 3;
-constexpr int kSpmvCapNnz    = 5120;              // per-stage nnz capacity
-constexpr int kSpmvMaxRows   = 1024;              // per-tile row cap
+constexpr int    kSpmvConsumerWarps = 16;
+constexpr int    kSpmvConsumers     = kSpmvConsumerWarps * 32;
+constexpr int    kSpmvThreads       = kSpmvConsumers + 32; // + producer warp
+constexpr int    kSpmvMaxStages     = 4;
+constexpr int    kSpmvChunkRows     = 32;
+constexpr int    kSpmvUnroll        = 8;                   // nonzeros per lane per sweep step
+constexpr size_t kSpmvHeaderBytes   = 1024;                // barriers, meta, reduction scratch
+constexpr size_t kSpmvStageBudget   = 200 * 1024;          // dynamic smem for the ring
 
 struct SpmvStageMeta {
     int64_t kv0;    // first value index held in the stage (16-B aligned)
@@ -42,29 +53,19 @@ struct SpmvStageMeta {
     int     pad;
 };
 
-// Shared-memory layout of one stage.
-struct SpmvLayout {
-    int rows_per_tile;
-    __host__ __device__ static constexpr size_t off_bytes(int R) { return (size_t)(R + 2) * 8; }
-    __host__ __device__ static constexpr size_t val_bytes() { return (size_t)kSpmvCapNnz * 8; }
-    __host__ __device__ static constexpr size_t col_bytes() { return (size_t)kSpmvCapNnz * 4; }
-    __host__ __device__ static constexpr size_t stage_bytes(int R)
-    {
-        return ((off_bytes(R) + 15) & ~size_t(15)) + val_bytes() + col_bytes();
-    }
-    __host__ __device__ static constexpr size_t smem_bytes(int R)
-    {
-        return 1024 /* barriers + meta */ + kSpmvStages * stage_bytes(R);
-    }
-};
-
 struct SpmvArgs {
     int64_t        n_rows;
     int64_t        n_tiles;
-    int            R;    // rows per tile (even, multiple of 32)
+    int            R;        // rows per tile (multiple of 32)
+    int            stages;   // ring depth (<= kSpmvMaxStages)
+    int            groups;   // consumer groups working on distinct stages (divides stages)
+    int            cap;      // nonzeros per stage
+    int            off_bytes, val_bytes, stage_bytes; // stage layout: [off | vals | cols]
     const int64_t* off;
     const int32_t* cols;
     const double*  vals;
+
+    size_t smem_bytes() const { return kSpmvHeaderBytes + (size_t)stages * stage_bytes; }
 };
 
 // Shared reduction workspace used by Ops with a tail.
@@ -73,90 +74,130 @@ struct TailArgs {
     unsigned int* ticket;
 };
 
-// Rows processed concurrently per consumer thread, and columns per batch.
-// Each pass a thread owns G rows (lr, lr+256, ...); for every batch of 8
-// columns it first reads all G*8 (col, val) pairs (LDS from the stage, or
-// LDG for direct tiles), then issues all G*8 gathers, then folds them into
-// the per-row sums strictly left to right -- so the memory-level
-// parallelism is G*8 gathers per thread while each row's sum keeps the
-// reference's sequential order.
-constexpr int kSpmvRowGroup = 2;
-constexpr int kSpmvBatch    = 8;
+__host__ __device__ inline int align16(int64_t b) { return (int)((b + 15) & ~int64_t(15)); }
 
-template <int G, typename IDX, class Op>
-__device__ __forceinline__ double spmv_rows(const Op& op, double acc, int ctid, int rows,
-                                            int64_t r0, const int64_t* __restrict__ O,
-                                            int64_t kbase, const int32_t* __restrict__ Cc,
-                                            const double* __restrict__ V)
+// Tile geometry for a matrix whose longest row has max_row_len nonzeros: the
+// largest R (multiple of 32, <= 1024) whose worst-case slab fits a stage with
+// at least 3 stages in the ring, else 2.  Rows too long for any stage still
+// work (direct tiles).
+inline SpmvArgs make_spmv_args(const rvk_csr& A, int64_t max_row_len)
 {
-    // IDX = int for staged tiles (indices local to the stage: value k lives at
-    // V[k - kbase], its column at Cc[k - kbase]), int64_t for direct tiles.
-    for (int base = ctid; base < rows; base += G * kSpmvConsumers) {
-        IDX     kb[G], ke[G], last[G];
-        int32_t safe[G];
-        int     len = 0;
+    if (max_row_len < 1) max_row_len = 1;
+    SpmvArgs a{};
+    a.n_rows = A.n_rows;
+    a.off    = A.row_offsets;
+    a.cols   = A.col_indices;
+    a.vals   = A.values;
+    auto fit = [&](int R, int min_stages) {
+        const int64_t cap = ((R * max_row_len + 8) + 3) & ~int64_t(3);
+        const int64_t ob = align16((int64_t)(R + 2) * 8), vb = cap * 8, cb = align16(cap * 4);
+        const int64_t sb = ob + vb + cb;
+        const int64_t st = std::min<int64_t>(kSpmvMaxStages, (int64_t)kSpmvStageBudget / sb);
+        if (st < min_stages) return false;
+        a.R = R;
+        a.stages = (int)st;
+        a.cap = (int)cap;
+        a.off_bytes = (int)ob;
+        a.val_bytes = (int)vb;
+        a.stage_bytes = (int)sb;
+        return true;
+    };
+    bool ok = false;
+    for (int need = 3; need >= 2 && !ok; --need)
+        for (int R = 1024; R >= 32 && !ok; R /= 2) ok = fit(R, need);
+    if (!ok) { // rows longer than a stage: every tile direct, small ring
+        a.R = 32;
+        a.stages = 4;
+        a.off_bytes = align16(34 * 8);
+        a.cap = (int)(((kSpmvStageBudget / 4 - a.off_bytes) / 12) & ~size_t(3));
+        a.val_bytes = a.cap * 8;
+        a.stage_bytes = a.off_bytes + a.val_bytes + align16((int64_t)a.cap * 4);
+    }
+    a.n_tiles = (A.n_rows + a.R - 1) / a.R;
+    // enough groups that every consumer thread owns a row of some tile
+    a.groups = 1;
+    while (a.groups * 2 <= a.stages && a.stages % (a.groups * 2) == 0 &&
+           a.R * a.groups * 2 <= kSpmvConsumers)
+        a.groups *= 2;
+    return a;
+}
+
+// ---------------------------------------------------------------------------
+// Direct tiles: thread-per-row straight from global memory (rare path).
+// ---------------------------------------------------------------------------
+template <class Op>
+__device__ __forceinline__ double spmv_rows_direct(const Op& op, double acc, int gtid, int gsize,
+                                                   int rows, int64_t r0,
+                                                   const int64_t* __restrict__ O,
+                                                   const int32_t* __restrict__ Cc,
+                                                   const double* __restrict__ V)
+{
+    for (int lr = gtid; lr < rows; lr += gsize) {
+        const int64_t kb = O[lr], ke = O[lr + 1];
+        double        sum = 0.0;
+        for (int64_t k = kb; k < ke; k += kSpmvUnroll) {
+            int32_t c[kSpmvUnroll];
+            double  v[kSpmvUnroll];
+            bool    ok[kSpmvUnroll];
 #pragma unroll
-        for (int g = 0; g < G; ++g) {
-            const int  lr = base + g * kSpmvConsumers;
-            const bool in = lr < rows;
-            kb[g]         = in ? (IDX)(O[lr] - kbase) : (IDX)0;
-            ke[g]         = in ? (IDX)(O[lr + 1] - kbase) : (IDX)0;
-            len           = max(len, (int)(ke[g] - kb[g]));
-            // dead slots re-read a valid entry (nnz >= 1 is guaranteed by the
-            // host) and gather a valid index; they never reach the sum
-            last[g] = ke[g] > kb[g] ? ke[g] - 1 : (kb[g] > 0 ? kb[g] - 1 : (IDX)0);
-            const int64_t row = r0 + lr;
-            safe[g]           = (int32_t)(in && row < op.n_src() ? row : 0);
-        }
-        double sum[G], own[G];
-        bool   have_own[G];
+            for (int u = 0; u < kSpmvUnroll; ++u) {
+                ok[u]            = k + u < ke;
+                const int64_t ks = ok[u] ? k + u : ke - 1;
+                c[u]             = __ldg(Cc + ks);
+                v[u]             = __ldg(V + ks);
+            }
+            typename Op::Fetch f[kSpmvUnroll];
 #pragma unroll
-        for (int g = 0; g < G; ++g) {
-            sum[g]      = 0.0;
-            own[g]      = 0.0;
-            have_own[g] = false;
-        }
-        for (int k = 0; k < len; k += kSpmvBatch) {
-            // Branch-free batch: (1) all column/value reads, (2) all gathers,
-            // (3) the per-row sums strictly left to right (dead slots dropped
-            // by a select), so every load of the batch is in flight together.
-            int32_t c[G][kSpmvBatch];
-            double  v[G][kSpmvBatch];
-            bool    ok[G][kSpmvBatch];
+            for (int u = 0; u < kSpmvUnroll; ++u) f[u] = op.fetch(c[u]);
 #pragma unroll
-            for (int g = 0; g < G; ++g)
-#pragma unroll
-                for (int u = 0; u < kSpmvBatch; ++u) {
-                    const IDX kk = kb[g] + (IDX)(k + u);
-                    ok[g][u]     = kk < ke[g];
-                    const IDX ks = ok[g][u] ? kk : last[g];
-                    c[g][u]      = ok[g][u] ? Cc[ks] : safe[g];
-                    v[g][u]      = V[ks];
-                }
-            typename Op::Fetch f[G][kSpmvBatch];
-#pragma unroll
-            for (int g = 0; g < G; ++g)
-#pragma unroll
-                for (int u = 0; u < kSpmvBatch; ++u) f[g][u] = op.fetch(c[g][u]);
-#pragma unroll
-            for (int g = 0; g < G; ++g) {
-                const int32_t row = (int32_t)(r0 + base + g * kSpmvConsumers);
-#pragma unroll
-                for (int u = 0; u < kSpmvBatch; ++u) {
-                    const double x = op.value(f[g][u]);
-                    const double t = add(sum[g], mul(v[g][u], x));
-                    sum[g]         = ok[g][u] ? t : sum[g];
-                    const bool d   = ok[g][u] && c[g][u] == row;
-                    own[g]         = d ? x : own[g];
-                    have_own[g]    = have_own[g] || d;
-                }
+            for (int u = 0; u < kSpmvUnroll; ++u) {
+                const double t = add(sum, mul(v[u], op.value(f[u])));
+                sum            = ok[u] ? t : sum;
             }
         }
+        acc = op.row(r0 + lr, sum, acc, op.own_fetch(r0 + lr));
+    }
+    return acc;
+}
+
+// ---------------------------------------------------------------------------
+// Staged tiles: lane-per-row out of the shared-memory stage.
+//   O  : the tile's row offsets in shared memory (global nnz indices)
+//   V  : stage values, V[k - kv0];  Cc : stage columns, Cc[k - kv0]
+// Stage-local 32-bit indices keep the address arithmetic cheap.
+// ---------------------------------------------------------------------------
+template <class Op>
+__device__ __forceinline__ double spmv_rows_staged(const Op& op, double acc, int gtid, int gsize,
+                                                   int rows, int64_t r0, const int64_t* O,
+                                                   int64_t kv0, const int32_t* Cc,
+                                                   const double* V)
+{
+    for (int lr = gtid; lr < rows; lr += gsize) {
+        const auto own = op.own_fetch(r0 + lr); // epilogue operands, in flight early
+        const int  kb  = (int)(O[lr] - kv0);
+        const int  ke  = (int)(O[lr + 1] - kv0);
+        double     sum = 0.0;
+        for (int k = kb; k < ke; k += kSpmvUnroll) {
+            int32_t c[kSpmvUnroll];
+            double  v[kSpmvUnroll];
+            bool    ok[kSpmvUnroll];
 #pragma unroll
-        for (int g = 0; g < G; ++g) {
-            const int lr = base + g * kSpmvConsumers;
-            if (lr < rows) acc = op.row(r0 + lr, sum[g], acc, own[g], have_own[g]);
+            for (int u = 0; u < kSpmvUnroll; ++u) {
+                ok[u]        = k + u < ke;
+                const int ks = ok[u] ? k + u : k; // k < ke: a valid entry
+                c[u]         = Cc[ks];
+                v[u]         = V[ks];
+            }
+            typename Op::Fetch f[kSpmvUnroll];
+#pragma unroll
+            for (int u = 0; u < kSpmvUnroll; ++u) f[u] = op.fetch(c[u]);
+#pragma unroll
+            for (int u = 0; u < kSpmvUnroll; ++u) {
+                const double t = add(sum, mul(v[u], op.value(f[u])));
+                sum            = ok[u] ? t : sum;
+            }
         }
+        acc = op.row(r0 + lr, sum, acc, own);
     }
     return acc;
 }
@@ -165,23 +206,21 @@ template <class Op>
 __global__ void __launch_bounds__(kSpmvThreads, 1) k_spmv_tma(SpmvArgs A, Op op_in, TailArgs tail)
 {
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    uint64_t*      full  = reinterpret_cast<uint64_t*>(smem_raw);
-    uint64_t*      empty = full + kSpmvStages;
-    SpmvStageMeta* meta  = reinterpret_cast<SpmvStageMeta*>(smem_raw + 128);
-    double*        red   = reinterpret_cast<double*>(smem_raw + 512);  // 32 doubles
-    int*           flag  = reinterpret_cast<int*>(smem_raw + 512 + 256);
-    unsigned char* stage0 = smem_raw + 1024;
-    const size_t   sbytes = SpmvLayout::stage_bytes(A.R);
-    const size_t   obytes = (SpmvLayout::off_bytes(A.R) + 15) & ~size_t(15);
+    uint64_t*      full   = reinterpret_cast<uint64_t*>(smem_raw);
+    uint64_t*      empty  = full + kSpmvMaxStages;
+    SpmvStageMeta* meta   = reinterpret_cast<SpmvStageMeta*>(smem_raw + 128);
+    double*        red    = reinterpret_cast<double*>(smem_raw + 512); // 32 doubles
+    int*           flag   = reinterpret_cast<int*>(smem_raw + 512 + 256);
+    unsigned char* stage0 = smem_raw + kSpmvHeaderBytes;
 
     Op op = op_in;
     if (!op.init()) return; // device-side early exit (converged / breakdown)
 
     const int tid = threadIdx.x;
     if (tid == 0) {
-        for (int s = 0; s < kSpmvStages; ++s) {
+        for (int s = 0; s < A.stages; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], kSpmvConsumers / 32);
+            mbar_init(&empty[s], kSpmvConsumerWarps / A.groups);
         }
         fence_mbar_init();
     }
@@ -191,75 +230,72 @@ __global__ void __launch_bounds__(kSpmvThreads, 1) k_spmv_tma(SpmvArgs A, Op op_
         // ===================== producer warp =====================
         if (tid == 0) {
             const uint64_t pol = policy_evict_first();
-            int64_t t = blockIdx.x;
-            // prefetch the first tile's slab bounds
-            int64_t k0 = 0, k1 = 0;
+            int64_t        t   = blockIdx.x;
+            int64_t        k0 = 0, k1 = 0; // slab bounds, prefetched one tile ahead
             if (t < A.n_tiles) {
-                const int64_t r0 = t * A.R;
-                const int64_t r1 = min(r0 + A.R, A.n_rows);
-                k0 = __ldg(A.off + r0);
-                k1 = __ldg(A.off + r1);
+                k0 = __ldg(A.off + t * A.R);
+                k1 = __ldg(A.off + min(t * A.R + A.R, A.n_rows));
             }
             for (int j = 0; t < A.n_tiles; ++j, t += gridDim.x) {
-                const int s = j % kSpmvStages;
-                if (j >= kSpmvStages) mbar_wait(&empty[s], ((j / kSpmvStages) - 1) & 1);
+                const int s = j % A.stages;
+                if (j >= A.stages) mbar_wait(&empty[s], ((j / A.stages) - 1) & 1);
                 const int64_t r0 = t * A.R;
                 const int64_t r1 = min(r0 + A.R, A.n_rows);
                 const int64_t ck0 = k0, ck1 = k1;
-                // prefetch the next tile's bounds (overlaps this tile's copies)
-                const int64_t tn = t + gridDim.x;
+                const int64_t tn  = t + gridDim.x;
                 if (tn < A.n_tiles) {
-                    const int64_t q0 = tn * A.R;
-                    const int64_t q1 = min(q0 + A.R, A.n_rows);
-                    k0 = __ldg(A.off + q0);
-                    k1 = __ldg(A.off + q1);
+                    k0 = __ldg(A.off + tn * A.R);
+                    k1 = __ldg(A.off + min(tn * A.R + A.R, A.n_rows));
                 }
                 const int64_t kv0 = ck0 & ~int64_t(1), kv1 = (ck1 + 1) & ~int64_t(1);
                 const int64_t kc0 = ck0 & ~int64_t(3), kc1 = (ck1 + 3) & ~int64_t(3);
-                const bool last   = r1 >= A.n_rows;
-                const bool direct = last || (kv1 - kv0) > kSpmvCapNnz || (kc1 - kc0) > kSpmvCapNnz;
-                meta[s].kv0    = kv0;
-                meta[s].kc0    = kc0;
-                meta[s].direct = direct ? 1 : 0;
+                const bool    last   = r1 >= A.n_rows;
+                const bool    direct = last || (kv1 - kv0) > A.cap || (kc1 - kc0) > A.cap;
+                meta[s].kv0          = kv0;
+                meta[s].kc0          = kc0;
+                meta[s].direct       = direct ? 1 : 0;
                 if (direct) {
                     mbar_arrive(&full[s]);
                 } else {
-                    unsigned char* st = stage0 + (size_t)s * sbytes;
+                    unsigned char* st = stage0 + (size_t)s * A.stage_bytes;
                     const uint32_t ob = (uint32_t)((A.R + 2) * 8);
                     const uint32_t vb = (uint32_t)((kv1 - kv0) * 8);
                     const uint32_t cb = (uint32_t)((kc1 - kc0) * 4);
                     mbar_arrive_expect_tx(&full[s], ob + vb + cb);
                     bulk_g2s(st, A.off + r0, ob, &full[s], pol);
-                    if (vb) bulk_g2s(st + obytes, A.vals + kv0, vb, &full[s], pol);
-                    if (cb) bulk_g2s(st + obytes + SpmvLayout::val_bytes(), A.cols + kc0, cb,
-                                     &full[s], pol);
+                    if (vb) bulk_g2s(st + A.off_bytes, A.vals + kv0, vb, &full[s], pol);
+                    if (cb)
+                        bulk_g2s(st + A.off_bytes + A.val_bytes, A.cols + kc0, cb, &full[s], pol);
                 }
             }
         }
-        return; // producer warp does not take part in the consumer reduction
+        return; // the producer warp takes no part in the consumer reduction
     }
 
     // ===================== consumer warps =====================
-    const int ctid = tid - 32;
-    double    acc  = 0.0;
-    int64_t   t    = blockIdx.x;
-    for (int j = 0; t < A.n_tiles; ++j, t += gridDim.x) {
-        const int s = j % kSpmvStages;
-        mbar_wait(&full[s], (j / kSpmvStages) & 1);
+    // NG groups of GS threads; group q takes the tiles j with j % NG == q
+    // (NG divides the ring depth, so a group always owns the same stages).
+    const int ctid  = tid - 32;
+    const int gs    = kSpmvConsumers / A.groups;
+    const int group = ctid / gs, gtid = ctid % gs;
+    double    acc   = 0.0;
+    int64_t   t     = blockIdx.x + (int64_t)group * gridDim.x;
+    for (int j = group; t < A.n_tiles; j += A.groups, t += (int64_t)A.groups * gridDim.x) {
+        const int s = j % A.stages;
+        mbar_wait(&full[s], (j / A.stages) & 1);
         const int64_t r0   = t * A.R;
         const int     rows = (int)min((int64_t)A.R, A.n_rows - r0);
         if (meta[s].direct) {
-            acc = spmv_rows<kSpmvRowGroup, int64_t>(op, acc, ctid, rows, r0, A.off + r0, 0,
-                                                    A.cols, A.vals);
+            acc = spmv_rows_direct(op, acc, gtid, gs, rows, r0, A.off + r0, A.cols, A.vals);
         } else {
-            unsigned char* st  = stage0 + (size_t)s * sbytes;
+            unsigned char* st  = stage0 + (size_t)s * A.stage_bytes;
             const int64_t  kv0 = meta[s].kv0;
-            // columns were copied from kc0 <= kv0: shift so both share kv0-local indices
-            const int32_t* cs = reinterpret_cast<const int32_t*>(st + obytes + SpmvLayout::val_bytes()) +
+            // columns were copied from kc0 <= kv0: shift so both use kv0-local indices
+            const int32_t* Cc = reinterpret_cast<const int32_t*>(st + A.off_bytes + A.val_bytes) +
                                 (kv0 - meta[s].kc0);
-            acc = spmv_rows<kSpmvRowGroup, int>(op, acc, ctid, rows, r0,
-                                                reinterpret_cast<const int64_t*>(st), kv0, cs,
-                                                reinterpret_cast<const double*>(st + obytes));
+            acc = spmv_rows_staged(op, acc, gtid, gs, rows, r0,
+                                   reinterpret_cast<const int64_t*>(st), kv0, Cc,
+                                   reinterpret_cast<const double*>(st + A.off_bytes));
         }
         __syncwarp();
         if ((ctid & 31) == 0) mbar_arrive(&empty[s]);
@@ -283,15 +319,15 @@ struct SpmvPlainOp {
     static constexpr bool kHasTail = false;
     const double* __restrict__ x;
     double* __restrict__ y;
-    int64_t ncols;
-    __device__ __forceinline__ bool    init() { return true; }
-    __device__ __forceinline__ int64_t n_src() const { return ncols; }
     struct Fetch {
         double x;
     };
+    __device__ __forceinline__ bool   init() { return true; }
     __device__ __forceinline__ Fetch  fetch(int32_t j) const { return Fetch{__ldg(x + j)}; }
     __device__ __forceinline__ double value(const Fetch& f) const { return f.x; }
-    __device__ __forceinline__ double row(int64_t i, double sum, double acc, double, bool) const
+    struct Own {};
+    __device__ __forceinline__ Own    own_fetch(int64_t) const { return Own{}; }
+    __device__ __forceinline__ double row(int64_t i, double sum, double acc, Own) const
     {
         y[i] = sum;
         return acc;
@@ -299,43 +335,17 @@ struct SpmvPlainOp {
     __device__ __forceinline__ void tail(double) const {}
 };
 
-// Rows per tile for a matrix whose longest row has `max_row_len` entries:
-// the largest multiple of 32 (<= kSpmvMaxRows) whose worst-case 16-B-rounded
-// slab fits one stage.  Rows longer than a stage still work (direct tiles).
-inline int spmv_rows_per_tile(int64_t max_row_len)
-{
-    if (max_row_len < 1) max_row_len = 1;
-    int64_t r = (kSpmvCapNnz - 8) / max_row_len;
-    r         = (r / 32) * 32;
-    if (r < 32) r = 32;
-    if (r > kSpmvMaxRows) r = kSpmvMaxRows;
-    return (int)r;
-}
-
-inline SpmvArgs make_spmv_args(const rvk_csr& A, int R)
-{
-    SpmvArgs a;
-    a.n_rows  = A.n_rows;
-    a.R       = R;
-    a.n_tiles = (A.n_rows + R - 1) / R;
-    a.off     = A.row_offsets;
-    a.cols    = A.col_indices;
-    a.vals    = A.values;
-    return a;
-}
-
 template <class Op>
 rvk_status launch_spmv(cudaStream_t stream, const SpmvArgs& a, const Op& op, TailArgs tail,
                        int grid)
 {
-    const size_t smem = SpmvLayout::smem_bytes(kSpmvMaxRows);
-    static bool  configured = false; // per instantiation
+    static bool configured = false; // per instantiation; before any graph capture
     if (!configured) {
         RVK_CUDA(cudaFuncSetAttribute(k_spmv_tma<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)smem));
+                                      (int)(kSpmvHeaderBytes + kSpmvStageBudget)));
         configured = true;
     }
-    k_spmv_tma<Op><<<grid, kSpmvThreads, SpmvLayout::smem_bytes(a.R), stream>>>(a, op, tail);
+    k_spmv_tma<Op><<<grid, kSpmvThreads, a.smem_bytes(), stream>>>(a, op, tail);
     RVK_CHECK_LAUNCH("k_spmv_tma");
     return RVK_OK;
 }
