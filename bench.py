@@ -57,10 +57,15 @@ def peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def bytes_model(n: int, nnz: int):
-    """Algorithmic HBM bytes.  All FP64 + int64 offsets + int32 cols."""
-    k1 = 12 * nnz + 8 * (n + 1) + 32 * n        # off, cols, vals, z, p_old -> p_new, w
-    k2 = 64 * n                                  # x, p, r, w, dinv -> x, r, z
+def bytes_model(n: int, nnz: int, mode: str = "fused"):
+    """Algorithmic HBM bytes.  All FP64 + int64 offsets + int32 cols.
+    k1 = the SpMV launch (fused: + on-the-fly AYPX), k2 = the rest of an iteration."""
+    if mode == "fused":
+        k1 = 12 * nnz + 8 * (n + 1) + 32 * n    # off, cols, vals, z, p_old -> p_new, w
+        k2 = 64 * n                              # x, p, r, w, dinv -> x, r, z
+    else:
+        k1 = 12 * nnz + 8 * (n + 1) + 16 * n    # off, cols, vals, p -> w
+        k2 = 136 * n                             # aypx 24, dot 16, 2 axpy 48, jacobi 24, norm 8, dot 16
     b_min = k1 + k2                              # = 12 nnz + 8 (n+1) + 96 n
     b_ref = 12 * nnz + 8 * (n + 1) + 152 * n     # reference's unfused sequence
     setup = 64 * n
@@ -213,8 +218,7 @@ def run_gpu(args, cfg):
     x = rvk.DeviceArray(n)
     rvk.check(rvk.lib().rvk_fill_rhs(ctx.h, 0x9E3779B97F4A7C15, n, b.ptr))
     plan = rvk.CgPlan(ctx, A, max_it=MAX_IT, mode=args.mode, use_graph=not args.no_graph)
-    plan.set_profiling(True)
-    bm = bytes_model(n, nnz)
+    bm = bytes_model(n, nnz, args.mode)
     hbm_peak, peak_src = peaks()
     ws_bytes = 20 * nnz + 8 * (n + 1) + 9 * 8 * n
     log(f"{desc}: n={n} nnz={nnz} working set {ws_bytes/1e9:.2f} GB (L2 {L2_BYTES/1e6:.0f} MB)")
@@ -224,38 +228,60 @@ def run_gpu(args, cfg):
     res = plan.result()
     assert res.iterations == MAX_IT, res
 
+    # ---- timed region: K solves, CUDA events on the solve stream --------------
+    # Working sets above 2x L2 stream from HBM anyway; smaller ones get an L2
+    # flush (a 512 MiB write on the same stream) between steps, outside the
+    # per-step event pairs.
+    flush = None
+    if ws_bytes < 2 * L2_BYTES:
+        flush = torch.empty(512 * 2 ** 20, dtype=torch.uint8, device=f"cuda:{local}")
     syncs0 = rvk.host_syncs()
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
         with torch.cuda.stream(stream):
-            ev[0].record(stream)
             for k in range(args.steps):
+                if flush is not None:
+                    flush.fill_(k & 0xFF)
+                ev0[k].record(stream)
                 plan.solve_dev(b, x)
-                ev[k + 1].record(stream)
+                ev1[k].record(stream)
         stream.synchronize()
-        torch.cuda.synchronize()
     syncs = rvk.host_syncs() - syncs0
-    step_ms = [ev[k].elapsed_time(ev[k + 1]) for k in range(args.steps)]
-    total_ms = ev[0].elapsed_time(ev[-1])
-    ms = total_ms / args.steps
-    k1_ms, k2_ms, launches = plan.kernel_times()   # last timed solve, 20 launches each
+    step_ms = [ev0[k].elapsed_time(ev1[k]) for k in range(args.steps)]
+    ms = sum(step_ms) / args.steps
     res = plan.result()
     assert res.iterations == MAX_IT
+    launches = plan.launches()
 
+    # ---- per-kernel durations: the same solves with event pairs captured in the
+    # graph around every K1 (SpMV) and K2 (update) launch, same stream ---------
+    plan.set_profiling(True)
+    plan.solve_dev(b, x)                      # (re)capture the profiled graph
+    plan.result()
+    k1_ms = k2_ms = 0.0
+    for _ in range(args.steps):
+        plan.solve_dev(b, x)
+        plan.result()
+        a1, a2, _ = plan.kernel_times()
+        k1_ms += a1
+        k2_ms += a2
+    k1_ms /= args.steps
+    k2_ms /= args.steps
+    plan.set_profiling(False)
     k1_avg = k1_ms / MAX_IT
     k2_avg = k2_ms / MAX_IT
     k1_gbs = bm["k1"] / (k1_avg * 1e-3) / 1e9
     k2_gbs = bm["k2"] / (k2_avg * 1e-3) / 1e9
     solve_gbs = bm["b_min_solve"] / (ms * 1e-3) / 1e9
-    traffic = ncu_traffic(args.config)
+    traffic = ncu_traffic(args.config) if args.mode == "fused" else None
 
     # ---- e2e through the C-ABI with host buffers (pinned) ----------------------
     bh = torch.empty(n, dtype=torch.float64, pin_memory=True)
     xh = torch.empty(n, dtype=torch.float64, pin_memory=True)
     bh.numpy()[:] = b.download(ctx)
     hist = np.empty(MAX_IT + 1)
-    plan.set_profiling(False)
     for _ in range(max(1, args.warmup)):
         plan.solve_host(bh.numpy(), xh.numpy(), hist)
     e2e = []
@@ -280,9 +306,13 @@ def run_gpu(args, cfg):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{desc}, Jacobi-CG {MAX_IT} iterations, x0=0, splitmix64 RHS",
                    "n": n, "nnz": nnz, "mode": args.mode, "graph": not args.no_graph,
-                   "l2": f"no flush: working set {ws_bytes/1e9:.2f} GB >> 126 MB L2 "
-                         "(every operand streams from HBM each step)"},
-        "roofline": {"bound": "hbm", "kernel": "k_spmv_tma<CgSpmvOp> (SpMV + on-the-fly AYPX + p.w)",
+                   "l2": (f"no flush: working set {ws_bytes/1e9:.2f} GB >> 126 MB L2 "
+                          "(every operand streams from HBM each step)") if flush is None else
+                         (f"L2 flushed between steps (512 MiB write); working set "
+                          f"{ws_bytes/1e6:.1f} MB")},
+        "roofline": {"bound": "hbm",
+                     "kernel": ("k_spmv_tma<CgSpmvOp> (SpMV + on-the-fly AYPX + p.w)"
+                                if args.mode == "fused" else "k_spmv_tma<SpmvGuardedOp> (SpMV)"),
                      "achieved": round(k1_gbs, 1), "peak": hbm_peak, "unit": "GB/s",
                      "frac": round(k1_gbs / hbm_peak, 4), "traffic": traffic,
                      "alg_bytes_per_launch": bm["k1"], "avg_launch_ms": round(k1_avg, 5),

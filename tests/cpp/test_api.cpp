@@ -1,0 +1,365 @@
+// test_api.cpp -- the C++ drop-in API (include/rivulet/) against SPEC.md's
+// examples and the CPU oracle (oracle/rvk_oracle.h, test infrastructure).
+// Run by tests/test_gpu_api.py on a B200; prints PASS/FAIL per case.
+#include "rivulet/context.hpp"
+#include "rivulet/csr.hpp"
+#include "rivulet/expr.hpp"
+#include "rivulet/linalg.hpp"
+#include "rivulet/managed.hpp"
+#include "rivulet/runtime.hpp"
+#include "rivulet/solvers.hpp"
+#include "rivulet/stencil.hpp"
+#include "rivulet/vector.hpp"
+
+extern "C" {
+#include "../../oracle/rvk_oracle.h"
+}
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <string>
+#include <vector>
+
+using namespace rivulet;
+
+static int g_fail = 0;
+#define EXPECT(c)                                                                                \
+    do {                                                                                         \
+        if (!(c)) {                                                                              \
+            std::printf("  expectation failed: %s (%s:%d)\n", #c, __FILE__, __LINE__);           \
+            throw std::runtime_error("expectation");                                             \
+        }                                                                                        \
+    } while (0)
+
+static void run(const char* name, const std::function<void()>& f)
+{
+    try {
+        f();
+        std::printf("PASS %s\n", name);
+    } catch (const std::exception& e) {
+        ++g_fail;
+        std::printf("FAIL %s: %s\n", name, e.what());
+    }
+    std::fflush(stdout);
+}
+
+static double rel(double a, double b) { return std::fabs(a - b) / std::max(std::fabs(b), 1e-300); }
+
+struct HostCsr {
+    std::size_t n;
+    std::vector<int64_t> off;
+    std::vector<int32_t> cols;
+    std::vector<double> vals;
+};
+
+static HostCsr oracle_laplacian(int dim, int pts, int64_t nx, int64_t ny, int64_t nz)
+{
+    HostCsr h;
+    h.n = (std::size_t)ro_laplacian_rows(dim, nx, ny, nz);
+    const int64_t nnz = ro_laplacian_nnz(dim, pts, nx, ny, nz);
+    h.off.resize(h.n + 1);
+    h.cols.resize(nnz);
+    h.vals.resize(nnz);
+    ro_build_laplacian(dim, pts, nx, ny, nz, h.off.data(), h.cols.data(), h.vals.data());
+    return h;
+}
+
+int main()
+{
+    // ---- Vec known answers ---------------------------------------
+    run("vec_norm [3,4] = 5", [] {
+        Context     ctx;
+        DenseVector v(std::vector<double>{3, 4});
+        Managed     out;
+        vec_norm_async(v, NormType::Norm2, out, ctx);
+        EXPECT(out.validity() == Managed::Validity::PendingOnContext);
+        EXPECT(out.front() == 5.0);
+        EXPECT(out.validity() == Managed::Validity::HostValid);
+        DenseVector z(100);
+        vec_norm_async(z, NormType::Norm2, out, ctx);
+        EXPECT(out.front() == 0.0);
+    });
+    run("vec_dot / axpy / waxpy / scale", [] {
+        Context     ctx;
+        DenseVector x(std::vector<double>{1, 1, 1}), y(std::vector<double>{1, 1, 1});
+        Managed     d;
+        vec_dot_async(x, y, d, ctx);
+        EXPECT(d.front() == 3.0);
+        DenseVector yy(std::vector<double>{1, 1}), xx(std::vector<double>{3, 4});
+        vec_axpy_async(yy, 2.0, xx, ctx);
+        auto h = yy.to_host();
+        EXPECT(h[0] == 7.0 && h[1] == 9.0);
+        DenseVector w(2);
+        vec_waxpy_async(w, 2.0, xx, yy, ctx);  // 2*[3,4] + [7,9]
+        h = w.to_host();
+        EXPECT(h[0] == 13.0 && h[1] == 17.0);
+        vec_scale_async(w, 0.0, ctx);
+        h = w.to_host();
+        EXPECT(h[0] == 0.0 && h[1] == 0.0);
+        bool threw = false;
+        try {
+            DenseVector a(3), b(4);
+            vec_dot_async(a, b, d, ctx);
+        } catch (const Error&) {
+            threw = true;
+        }
+        EXPECT(threw);
+    });
+    run("normalize motif: norm -> 1/norm -> scale, zero host syncs (acceptance #4)", [] {
+        for (std::size_t n : {10ul, 1000ul, 1000000ul}) {
+            std::vector<double> hv(n);
+            ro_rhs(7 + n, (int64_t)n, hv.data());
+            Context     ctx;
+            DenseVector v(hv);
+            Managed     alpha;
+            const auto  s0 = runtime::host_syncs();
+            vec_norm_async(v, NormType::Norm2, alpha, ctx);
+            alpha = Eval(1.0 / alpha, ctx);
+            vec_scale_async(v, alpha, ctx);
+            EXPECT(runtime::host_syncs() == s0);
+            auto   h = v.to_host();
+            double s = 0;
+            for (double e : h) s += e * e;
+            EXPECT(std::fabs(std::sqrt(s) - 1.0) < 1e-12);
+        }
+    });
+    // ---- Mat ----------------------------------------------------------------------------
+    run("mat_mult identity and 1D 3-point (SPEC.md:408-409)", [] {
+        Context     ctx;
+        auto        I = CsrMatrix::identity(5);
+        DenseVector x(std::vector<double>{1, -2, 3.5, 0, 7}), y(5);
+        mat_mult(I, x, y, ctx);
+        EXPECT(y.to_host() == x.to_host());
+        CsrMatrix   T(3, 3, {0, 2, 5, 7}, {0, 1, 0, 1, 2, 1, 2}, {2, -1, -1, 2, -1, -1, 2});
+        DenseVector ones(std::vector<double>{1, 1, 1}), out(3);
+        mat_mult(T, ones, out); // synchronous form
+        auto h = out.to_host();
+        EXPECT(h[0] == 1 && h[1] == 0 && h[2] == 1);
+    });
+    run("CsrMatrix validation", [] {
+        int thrown = 0;
+        try { CsrMatrix(2, 2, {0, 1, 2}, {1, 0}, {1, 1}); } catch (const Error&) { ++thrown; }     // ok actually
+        try { CsrMatrix(2, 2, {1, 1, 2}, {0, 1}, {1, 1}); } catch (const Error&) { ++thrown; }     // off[0] != 0
+        try { CsrMatrix(1, 2, {0, 2}, {1, 0}, {1, 1}); } catch (const Error&) { ++thrown; }       // not increasing
+        try { CsrMatrix(1, 2, {0, 1}, {5}, {1}); } catch (const Error&) { ++thrown; }             // out of range
+        try { CsrMatrix(1, 2, {0, 2}, {0}, {1}); } catch (const Error&) { ++thrown; }             // off[n] != nnz
+        EXPECT(thrown == 4);
+    });
+    run("build_laplacian bit-identical to the CPU builder (4 stencils)", [] {
+        struct S { int dim, pts; int64_t nx, ny, nz; };
+        for (S s : {S{2, 5, 13, 7, 1}, S{2, 9, 9, 11, 1}, S{3, 7, 5, 6, 4}, S{3, 27, 4, 5, 6}}) {
+            StencilSpec sp{s.dim, s.pts, s.dim == 2 ? std::vector<int64_t>{s.nx, s.ny}
+                                                    : std::vector<int64_t>{s.nx, s.ny, s.nz}};
+            auto A = build_laplacian(sp);
+            auto h = oracle_laplacian(s.dim, s.pts, s.nx, s.ny, s.nz);
+            EXPECT(A.rows() == h.n && A.nnz() == h.cols.size());
+            EXPECT(std::equal(h.off.begin(), h.off.end(), A.row_offsets().begin()));
+            EXPECT(std::equal(h.cols.begin(), h.cols.end(), A.col_indices().begin()));
+            EXPECT(std::memcmp(h.vals.data(), A.values().data(), h.vals.size() * 8) == 0);
+            auto d  = A.diagonal().to_host();
+            auto sc = stencil_coefficients(s.dim, s.pts);
+            for (double e : d) EXPECT(e == sc.centre);
+        }
+    });
+    // ---- Managed / Eval (SPEC.md expr & managed examples) ------------------------------------
+    run("Eval / execute / CSE / folding", [] {
+        Context ctx;
+        Managed x(1.0, "x"), y(2.0, "y"), z(4.0, "z");
+        Managed r = Eval(x + y, ctx);
+        EXPECT(r.front() == 3.0);
+        Managed s = x + y; // no Eval: synchronous, host-valid immediately after
+        EXPECT(s.front() == 3.0);
+        auto e1 = Eval((x + y) / z, ctx);
+        Managed t(e1);
+        EXPECT(t.front() == 0.75);
+        EXPECT(Eval(Expr(2.0) * 3.0 + 1.0, ctx).op_count() == 0);
+        auto sum = x + y;
+        EXPECT(Eval(sum + sum, ctx).op_count() == 2);              // shared subtree once
+        EXPECT(Eval((x + y) + (x + y), ctx).op_count() == 2);      // structural CSE
+        Managed u(Eval(sin(((x + y) / z) * z) + 15, ctx));
+        EXPECT(rel(u.front(), std::sin(3.0) + 15.0) < 1e-14);
+        Managed w, v2;
+        e1.execute(w);
+        e1.execute(v2);
+        EXPECT(w.front() == v2.front());
+        Managed copy = r;     // synchronous snapshot
+        r = Eval(x * z, ctx); // later change of the source
+        EXPECT(copy.front() == 3.0 && r.front() == 4.0);
+        Managed betaold = Eval(r, ctx); // copy of a pending value, no host sync
+        EXPECT(betaold.front() == 4.0);
+    });
+    run("cross-context ordering: RAW edge installed, read-read free", [] {
+        Context a, b;
+        const std::size_t n = 4000000;
+        DenseVector v(n), w(n);
+        vec_set_async(v, 1.0, a);
+        for (int i = 0; i < 10; ++i) vec_axpy_async(v, 1.0, v, a); // v = 1024 after 10 doublings
+        Managed d1, d2;
+        vec_norm_async(v, NormType::Norm2, d1, b);  // RAW across contexts
+        EXPECT(rel(d1.front(), 1024.0 * std::sqrt((double)n)) < 1e-13);
+        Context c;
+        vec_dot_async(v, v, d2, c);                 // read after read on another ctx
+        vec_copy_async(v, w, b);                    // read-read: no ordering needed
+        EXPECT(rel(d2.front(), 1024.0 * 1024.0 * n) < 1e-13);
+        vec_set_async(v, 0.0, c);                   // WAR: waits for b's and c's readers
+        auto hw = w.to_host();
+        EXPECT(hw[0] == 1024.0 && hw[n - 1] == 1024.0);
+        auto hv = v.to_host();
+        EXPECT(hv[0] == 0.0);
+    });
+    run("deferred release: handles die while values are in flight", [] {
+        Context ctx;
+        DenseVector big(8000000);
+        vec_set_async(big, 2.0, ctx);
+        for (int i = 0; i < 50; ++i) {
+            Managed tmp;
+            vec_dot_async(big, big, tmp, ctx); // tmp destroyed while pending
+        }
+        Managed last;
+        vec_dot_async(big, big, last, ctx);
+        EXPECT(last.front() == 4.0 * 8000000);
+    });
+    // ---- CG (acceptance #5/#6) --------------------------------------------------
+    struct Case { int dim, pts; int64_t nx, ny, nz; };
+    for (Case cs : {Case{2, 5, 16, 16, 1}, Case{2, 9, 32, 32, 1}, Case{3, 7, 8, 8, 8}, Case{3, 27, 8, 8, 8}}) {
+        const std::string nm = "cg_solve modes vs oracle " + std::to_string(cs.pts) + "-pt";
+        run(nm.c_str(), [cs] {
+            auto h = oracle_laplacian(cs.dim, cs.pts, cs.nx, cs.ny, cs.nz);
+            std::vector<double> bh(h.n), xo(h.n), hist(21), work(5 * h.n);
+            ro_rhs(0x9E3779B97F4A7C15ull, (int64_t)h.n, bh.data());
+            ro_cg_config cfg{20, RO_PC_JACOBI, 0.0, 0.0};
+            ro_cg_result rr = ro_cg_solve((int64_t)h.n, h.off.data(), h.cols.data(), h.vals.data(),
+                                          bh.data(), xo.data(), hist.data(), cfg, work.data());
+            EXPECT(rr.iterations == 20);
+            CsrMatrix   A(h.n, h.n, h.off, h.cols, h.vals);
+            DenseVector b(bh);
+            for (SolverMode m : {SolverMode::Fused, SolverMode::Async, SolverMode::SyncBaseline}) {
+                DenseVector  x(h.n);
+                SolverConfig c;
+                c.mode     = m;
+                const auto census0 = runtime::census();
+                auto res   = cg_solve(A, b, x, c);
+                const auto d = runtime::census() - census0;
+                EXPECT(res.iterations == 20 && res.history.size() == 21);
+                for (int k = 0; k <= 20; ++k)
+                    if (!(rel(res.history[k], hist[k]) < 1e-10)) {
+                        std::printf("  mode %d k %d got %.17g want %.17g\n", (int)m, k, res.history[k], hist[k]);
+                        EXPECT(false);
+                    }
+                auto xh = x.to_host();
+                double num = 0, den = 0;
+                for (std::size_t i = 0; i < h.n; ++i) {
+                    num += (xh[i] - xo[i]) * (xh[i] - xo[i]);
+                    den += xo[i] * xo[i];
+                }
+                EXPECT(std::sqrt(num / den) < 1e-10);
+                // census: 1 matmult + 3 reductions + 3 updates per iteration
+                EXPECT(d.kernels_of(runtime::KernelKind::MatMult) == 20);
+                EXPECT(d.reductions() == 2 + 3 * 20); // setup norm + dot, then 3 per iteration
+                EXPECT(d.kernels_of(runtime::KernelKind::Axpy) == 40);
+                EXPECT(d.kernels_of(runtime::KernelKind::Aypx) == 19);
+                // FlopLog = sum over iterations of 2 nnz + 12 n + c  (exact integer)
+                const uint64_t n = h.n, nnz = h.cols.size();
+                const uint64_t body = 20 * (2 * nnz + 8 * n) + 40 * 2 * n - 2 * n; // aypx only i>=1
+                EXPECT(res.flops.matmult == 20 * 2 * nnz);
+                EXPECT(res.flops.axpy == 40 * 2 * n && res.flops.aypx == 19 * 2 * n);
+                (void)body;
+            }
+        });
+    }
+    run("cg Async: host syncs independent of iteration count (0 per iteration)", [] {
+        auto h = oracle_laplacian(2, 5, 64, 64, 1);
+        CsrMatrix   A(h.n, h.n, h.off, h.cols, h.vals);
+        std::vector<double> bh(h.n);
+        ro_rhs(1, (int64_t)h.n, bh.data());
+        DenseVector b(bh), x(h.n);
+        uint64_t syncs[2];
+        int      its[2] = {5, 20};
+        for (int k = 0; k < 2; ++k) {
+            SolverConfig c;
+            c.mode   = SolverMode::Async;
+            c.max_it = its[k];
+            cg_solve(A, b, x, c); // warm
+            const auto s0 = runtime::host_syncs();
+            cg_solve(A, b, x, c);
+            syncs[k] = runtime::host_syncs() - s0;
+        }
+        EXPECT(syncs[0] == syncs[1]);
+        SolverConfig f;
+        cg_solve(A, b, x, f); // first call also sets the plan up (one validation sync)
+        const auto   s0 = runtime::host_syncs();
+        cg_solve(A, b, x, f); // fused: exactly the one result read
+        std::printf("  syncs: async(5)=%llu async(20)=%llu fused=%llu\n", (unsigned long long)syncs[0],
+                    (unsigned long long)syncs[1], (unsigned long long)(runtime::host_syncs() - s0));
+        EXPECT(runtime::host_syncs() - s0 == 1);
+    });
+    run("cg breakdown reported with iteration (all modes)", [] {
+        CsrMatrix   A(2, 2, {0, 1, 2}, {0, 1}, {1.0, -1.0});
+        DenseVector b(std::vector<double>{1, 1});
+        for (SolverMode m : {SolverMode::Fused, SolverMode::Async, SolverMode::SyncBaseline}) {
+            DenseVector  x(2);
+            SolverConfig c;
+            c.mode = m;
+            c.pc   = PcType::None;
+            bool got = false;
+            try {
+                cg_solve(A, b, x, c);
+            } catch (const BreakdownError& e) {
+                got = e.iteration() == 0;
+            }
+            EXPECT(got);
+        }
+    });
+    run("cg identity converges in one iteration (SPEC.md:464)", [] {
+        auto        I = CsrMatrix::identity(100);
+        std::vector<double> bh(100);
+        ro_rhs(3, 100, bh.data());
+        DenseVector b(bh);
+        for (SolverMode m : {SolverMode::Fused, SolverMode::Async, SolverMode::SyncBaseline}) {
+            DenseVector  x(100);
+            SolverConfig c;
+            c.mode = m;
+            c.pc   = PcType::None;
+            c.rtol = 1e-14;
+            auto r = cg_solve(I, b, x, c);
+            EXPECT(r.converged && r.iterations == 1);
+            auto xh = x.to_host();
+            for (int i = 0; i < 100; ++i) EXPECT(std::fabs(xh[i] - bh[i]) <= 1e-15);
+        }
+    });
+    run("convergence callback: early exit, sync only if it reads dp", [] {
+        auto h = oracle_laplacian(2, 5, 32, 32, 1);
+        CsrMatrix   A(h.n, h.n, h.off, h.cols, h.vals);
+        std::vector<double> bh(h.n), xo(h.n), hist(501), work(5 * h.n);
+        ro_rhs(5, (int64_t)h.n, bh.data());
+        ro_cg_config oc{500, RO_PC_JACOBI, 0.0, 1e-8};
+        auto rr = ro_cg_solve((int64_t)h.n, h.off.data(), h.cols.data(), h.vals.data(), bh.data(),
+                              xo.data(), hist.data(), oc, work.data());
+        EXPECT(rr.status == RO_CONVERGED);
+        DenseVector  b(bh), x(h.n);
+        SolverConfig c;
+        c.mode                 = SolverMode::Async;
+        c.max_it               = 500;
+        c.convergence_callback = [](Managed& dp, int) { return dp.front() <= 1e-8; };
+        auto r = cg_solve(A, b, x, c);
+        EXPECT(r.converged && r.iterations == rr.iterations);
+        int calls = 0;
+        c.max_it  = 20;
+        c.convergence_callback = [&](Managed&, int) { ++calls; return false; }; // ignores dp
+        const auto s0 = runtime::host_syncs();
+        auto r2 = cg_solve(A, b, x, c);
+        EXPECT(calls == 20 && r2.iterations == 20);
+        // a callback that never reads dp adds no sync: only the end-of-solve
+        // reads remain (history + the three context drains), whatever max_it
+        EXPECT(runtime::host_syncs() - s0 <= 4);
+        calls = 0;
+        c.convergence_callback = [&](Managed& dp, int) { ++calls; return dp.front() < 0.0; };
+        const auto s1 = runtime::host_syncs();
+        cg_solve(A, b, x, c);
+        EXPECT(runtime::host_syncs() - s1 >= 20); // reading dp syncs every iteration
+    });
+    std::printf("%s: %d failure(s)\n", g_fail ? "FAILED" : "OK", g_fail);
+    return g_fail ? 1 : 0;
+}
