@@ -204,6 +204,45 @@ rvk_status rvk_cg_set_profiling(rvk_cg_plan plan, int on);
 rvk_status rvk_cg_kernel_times(rvk_cg_plan plan, float* spmv_ms, float* update_ms,
                                int* launches);
 
+/* ---- row sharding across GPUs -----------------------------
+ * The global grid is split into contiguous slabs of planes; shard `rank`
+ * owns n_own rows and keeps one halo plane (halo_lo / halo_hi rows, 0 at the
+ * outer boundary) on each interior side of the gathered vectors.  Its local
+ * CSR has n_own rows and halo_lo + n_own + halo_hi columns. */
+typedef struct rvk_comm_s*     rvk_comm;
+typedef struct rvk_dcg_plan_s* rvk_dcg_plan;
+typedef struct {
+    int64_t n_own, halo_lo, halo_hi;
+    int     rank, nranks;
+} rvk_shard;
+
+/* Rows [row_begin, row_end) of the stencil operator, offsets rebased to 0,
+ * columns shifted by -col_shift (device arrays, caller-allocated). */
+rvk_status rvk_laplacian_rows_nnz(int dim, int points, int64_t nx, int64_t ny, int64_t nz,
+                                  int64_t row_begin, int64_t row_end, int64_t* nnz);
+rvk_status rvk_build_laplacian_rows(rvk_ctx ctx, int dim, int points, int64_t nx, int64_t ny,
+                                    int64_t nz, int64_t row_begin, int64_t row_end,
+                                    int64_t col_shift, int64_t* off_dev, int32_t* cols_dev,
+                                    double* vals_dev);
+/* NCCL communicator (libnccl.so.2 resolved at run time).  The 128-byte
+ * unique id is produced on rank 0 and broadcast by the caller. */
+rvk_status rvk_comm_unique_id(void* id_out, int id_bytes);
+rvk_status rvk_comm_init(const void* id, int nranks, int rank, rvk_comm* out);
+rvk_status rvk_comm_destroy(rvk_comm comm);
+/* comm == NULL with nranks > 1: LOOPBACK shard (all shards on one device,
+ * sharing `shared_gather`, 4*nranks doubles, solved by
+ * rvk_dcg_loopback_solve).  Otherwise shared_gather must be NULL. */
+rvk_status rvk_dcg_plan_create(rvk_ctx ctx, const rvk_csr* A_local, rvk_shard shard,
+                               rvk_cg_config cfg, rvk_comm comm, double* shared_gather,
+                               rvk_dcg_plan* out);
+rvk_status rvk_dcg_plan_destroy(rvk_dcg_plan plan);
+/* One shard per process: halo exchange (ncclSend/Recv) + partial-sum
+ * allgather, all stream-ordered -- zero host syncs. */
+rvk_status rvk_dcg_solve_dev(rvk_dcg_plan plan, const double* b_own, double* x_own);
+rvk_status rvk_dcg_loopback_solve(rvk_dcg_plan* plans, int nplans, const double* const* b_own,
+                                  double* const* x_own);
+rvk_status rvk_dcg_result(rvk_dcg_plan plan, double* hist_host, rvk_cg_info* info);
+
 #ifdef __cplusplus
 }
 #endif

@@ -31,6 +31,7 @@
 #include "rvk_common.cuh"
 #include "rvk_context.hpp"
 #include "rvk_internal.hpp"
+#include "rvk_cg.cuh"
 #include "rvk_spmv.cuh"
 
 #include <cmath>
@@ -38,17 +39,7 @@
 
 namespace rvk {
 
-struct CgState {
-    double beta, betaold, alpha, pAp, dp0, dp;
-    int    done, state, iterations, breakdown_iter;
-};
-
-constexpr int kUpdThreads = 256;
-
-__device__ __forceinline__ bool cg_converged(double dp, double dp0, double rtol, double atol)
-{
-    return dp <= fmax(rtol * dp0, atol);
-}
+// CgState, kUpdThreads, cg_converged, resident_grid: rvk_cg.cuh
 
 // ---------------------------------------------------------------------------
 // K0: setup.  r = b; x = 0; z = B r; partials z.z, z.r.
@@ -358,16 +349,17 @@ struct SpmvGuardedOp : SpmvPlainOp {
 };
 
 // diag / dinv (csr.hpp:76-77): zero where absent; dinv = 1/diag.
+// col_off: column of row r's diagonal is r + col_off (0, or a shard's lo halo).
 template <bool INV>
 __global__ void k_diagonal(int64_t n, const int64_t* __restrict__ off,
                            const int32_t* __restrict__ cols, const double* __restrict__ vals,
-                           double* __restrict__ out)
+                           double* __restrict__ out, int64_t col_off)
 {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += stride) {
         double d = 0.0;
         for (int64_t k = off[r]; k < off[r + 1]; ++k)
-            if (cols[k] == r) d = vals[k];
+            if (cols[k] == r + col_off) d = vals[k];
         out[r] = INV ? 1.0 / d : d;
     }
 }
@@ -401,21 +393,6 @@ __global__ void k_validate(int64_t n, int64_t n_cols, int64_t nnz, const int64_t
     if (ml) atomicMax(maxlen, ml);
 }
 
-// Largest grid that is fully resident (one wave): blocks/SM from the
-// occupancy calculator times the SM count.  Grid-stride kernels launched with
-// more blocks than this run a second, equally long wave.
-template <class K>
-int resident_grid(K kernel, int threads, int64_t n_items)
-{
-    int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, 0) != cudaSuccess ||
-        per_sm < 1)
-        per_sm = 1;
-    const int64_t want = (n_items + threads - 1) / threads;
-    const int64_t cap  = (int64_t)sm_count() * per_sm;
-    return (int)(want < 1 ? 1 : (want > cap ? cap : want));
-}
-
 int update_grid(int64_t n)
 {
     const int64_t want = (n / 2 + kUpdThreads - 1) / kUpdThreads;
@@ -424,6 +401,15 @@ int update_grid(int64_t n)
 }
 
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+rvk_status diag_inverse(cudaStream_t s, const rvk_csr& A, int64_t col_off, double* dinv)
+{
+    if (A.n_rows == 0) return RVK_OK;
+    k_diagonal<true><<<update_grid(2 * A.n_rows), kUpdThreads, 0, s>>>(
+        A.n_rows, A.row_offsets, A.col_indices, A.values, dinv, col_off);
+    RVK_CHECK_LAUNCH("k_diagonal");
+    return RVK_OK;
+}
 
 } // namespace rvk
 
@@ -663,7 +649,7 @@ rvk_status rvk_csr_diagonal(rvk_ctx ctx, const rvk_csr* A, double* diag)
     if (!ctx || !A || (A->n_rows > 0 && !diag)) return set_error(RVK_ERR_INVALID, "null argument");
     if (A->n_rows == 0) return RVK_OK;
     k_diagonal<false><<<update_grid(2 * A->n_rows), kUpdThreads, 0, ctx->stream>>>(
-        A->n_rows, A->row_offsets, A->col_indices, A->values, diag);
+        A->n_rows, A->row_offsets, A->col_indices, A->values, diag, 0);
     RVK_CHECK_LAUNCH("k_diagonal");
     return RVK_OK;
 }
@@ -673,7 +659,7 @@ rvk_status rvk_csr_diagonal_inverse(rvk_ctx ctx, const rvk_csr* A, double* dinv)
     if (!ctx || !A || (A->n_rows > 0 && !dinv)) return set_error(RVK_ERR_INVALID, "null argument");
     if (A->n_rows == 0) return RVK_OK;
     k_diagonal<true><<<update_grid(2 * A->n_rows), kUpdThreads, 0, ctx->stream>>>(
-        A->n_rows, A->row_offsets, A->col_indices, A->values, dinv);
+        A->n_rows, A->row_offsets, A->col_indices, A->values, dinv, 0);
     RVK_CHECK_LAUNCH("k_diagonal");
     return RVK_OK;
 }

@@ -52,18 +52,30 @@ __host__ __device__ __forceinline__ int64_t row_offset(const Grid3& g, int64_t x
     return planes + lines + cells;
 }
 
-__global__ void k_build_laplacian(Grid3 g, int64_t n, int64_t* __restrict__ off,
-                                  int32_t* __restrict__ cols, double* __restrict__ vals)
+__host__ __device__ __forceinline__ int64_t row_offset_lin(const Grid3& g, int64_t row)
+{
+    const int64_t t = row / g.nx;
+    return row_offset(g, row % g.nx, t % g.ny, t / g.ny); // row == n gives nnz
+}
+
+// Rows [r_begin, r_end) of the global operator; offsets rebased to 0 and
+// columns shifted by -col_shift (a shard's local CSR for row sharding).
+__global__ void k_build_laplacian(Grid3 g, int64_t r_begin, int64_t r_end, int64_t col_shift,
+                                  int64_t* __restrict__ off, int32_t* __restrict__ cols,
+                                  double* __restrict__ vals)
 {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < n; row += stride) {
+    const int64_t n      = r_end - r_begin;
+    const int64_t k_base = row_offset_lin(g, r_begin);
+    for (int64_t lr = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; lr < n; lr += stride) {
+        const int64_t row = r_begin + lr;
         const int64_t x = row % g.nx;
         const int64_t t = row / g.nx;
         const int64_t y = t % g.ny;
         const int64_t z = t / g.ny;
-        int64_t       k = row_offset(g, x, y, z);
-        off[row]        = k;
-        if (row == n - 1) off[n] = row_offset(g, 0, 0, g.nz); // == nnz
+        int64_t       k = row_offset(g, x, y, z) - k_base;
+        off[lr]         = k;
+        if (lr == n - 1) off[n] = row_offset_lin(g, r_end) - k_base;
         for (int dz = -g.zr; dz <= g.zr; ++dz)
             for (int dy = -1; dy <= 1; ++dy)
                 for (int dx = -1; dx <= 1; ++dx) {
@@ -71,7 +83,7 @@ __global__ void k_build_laplacian(Grid3 g, int64_t n, int64_t* __restrict__ off,
                     const int64_t xx = x + dx, yy = y + dy, zz = z + dz;
                     if (xx < 0 || xx >= g.nx || yy < 0 || yy >= g.ny || zz < 0 || zz >= g.nz)
                         continue;
-                    cols[k] = (int32_t)(xx + g.nx * (yy + g.ny * zz));
+                    cols[k] = (int32_t)(xx + g.nx * (yy + g.ny * zz) - col_shift);
                     vals[k] = (dx == 0 && dy == 0 && dz == 0) ? g.centre : -1.0;
                     ++k;
                 }
@@ -142,7 +154,40 @@ rvk_status rvk_build_laplacian(rvk_ctx ctx, int dim, int points, int64_t nx, int
     if (rc != RVK_OK) return rc;
     Grid3 g{nx, ny, nz, (points == 9 || points == 27) ? 1 : 0, dim == 3 ? 1 : 0,
             (double)(points - 1)};
-    k_build_laplacian<<<grid_for(n), 256, 0, ctx->stream>>>(g, n, off, cols, vals);
+    k_build_laplacian<<<grid_for(n), 256, 0, ctx->stream>>>(g, 0, n, 0, off, cols, vals);
+    RVK_CHECK_LAUNCH("k_build_laplacian");
+    return RVK_OK;
+}
+
+rvk_status rvk_laplacian_rows_nnz(int dim, int points, int64_t nx, int64_t ny, int64_t nz,
+                                  int64_t row_begin, int64_t row_end, int64_t* nnz)
+{
+    if (dim == 2) nz = 1;
+    int64_t n = 0;
+    rvk_status rc = rvk_laplacian_size(dim, points, nx, ny, nz, &n, nullptr);
+    if (rc != RVK_OK) return rc;
+    if (row_begin < 0 || row_end > n || row_begin >= row_end)
+        return set_error(RVK_ERR_INVALID, "invalid row range [%lld, %lld) of %lld rows",
+                         (long long)row_begin, (long long)row_end, (long long)n);
+    Grid3 g{nx, ny, nz, (points == 9 || points == 27) ? 1 : 0, dim == 3 ? 1 : 0,
+            (double)(points - 1)};
+    if (nnz) *nnz = row_offset_lin(g, row_end) - row_offset_lin(g, row_begin);
+    return RVK_OK;
+}
+
+rvk_status rvk_build_laplacian_rows(rvk_ctx ctx, int dim, int points, int64_t nx, int64_t ny,
+                                    int64_t nz, int64_t row_begin, int64_t row_end,
+                                    int64_t col_shift, int64_t* off, int32_t* cols, double* vals)
+{
+    if (!ctx || !off || !cols || !vals) return set_error(RVK_ERR_INVALID, "null argument");
+    if (dim == 2) nz = 1;
+    int64_t    nnz = 0;
+    rvk_status rc  = rvk_laplacian_rows_nnz(dim, points, nx, ny, nz, row_begin, row_end, &nnz);
+    if (rc != RVK_OK) return rc;
+    Grid3 g{nx, ny, nz, (points == 9 || points == 27) ? 1 : 0, dim == 3 ? 1 : 0,
+            (double)(points - 1)};
+    k_build_laplacian<<<grid_for(row_end - row_begin), 256, 0, ctx->stream>>>(
+        g, row_begin, row_end, col_shift, off, cols, vals);
     RVK_CHECK_LAUNCH("k_build_laplacian");
     return RVK_OK;
 }

@@ -36,6 +36,9 @@ EXPORTS = [
     "rvk_build_laplacian", "rvk_fill_rhs", "rvk_cg_plan_create", "rvk_cg_plan_destroy",
     "rvk_cg_solve_dev", "rvk_cg_history_dev", "rvk_cg_result", "rvk_cg_solve_host",
     "rvk_cg_set_profiling", "rvk_cg_kernel_times",
+    "rvk_laplacian_rows_nnz", "rvk_build_laplacian_rows", "rvk_comm_unique_id", "rvk_comm_init",
+    "rvk_comm_destroy", "rvk_dcg_plan_create", "rvk_dcg_plan_destroy", "rvk_dcg_solve_dev",
+    "rvk_dcg_loopback_solve", "rvk_dcg_result",
 ]
 
 
@@ -65,6 +68,11 @@ class Csr(C.Structure):
 class CgConfig(C.Structure):
     _fields_ = [("max_it", C.c_int), ("pc", C.c_int), ("rtol", C.c_double),
                 ("atol", C.c_double), ("mode", C.c_int), ("use_graph", C.c_int)]
+
+
+class Shard(C.Structure):
+    _fields_ = [("n_own", C.c_int64), ("halo_lo", C.c_int64), ("halo_hi", C.c_int64),
+                ("rank", C.c_int), ("nranks", C.c_int)]
 
 
 class CgInfo(C.Structure):
@@ -131,6 +139,16 @@ def lib():
         "rvk_cg_set_profiling": (i, [vp, i]),
         "rvk_cg_kernel_times": (i, [vp, C.POINTER(C.c_float), C.POINTER(C.c_float),
                                     C.POINTER(C.c_int)]),
+        "rvk_laplacian_rows_nnz": (i, [i, i, i64, i64, i64, i64, i64, C.POINTER(i64)]),
+        "rvk_build_laplacian_rows": (i, [vp, i, i, i64, i64, i64, i64, i64, i64, vp, vp, vp]),
+        "rvk_comm_unique_id": (i, [vp, i]),
+        "rvk_comm_init": (i, [vp, i, i, C.POINTER(vp)]),
+        "rvk_comm_destroy": (i, [vp]),
+        "rvk_dcg_plan_create": (i, [vp, C.POINTER(Csr), Shard, CgConfig, vp, vp, C.POINTER(vp)]),
+        "rvk_dcg_plan_destroy": (i, [vp]),
+        "rvk_dcg_solve_dev": (i, [vp, vp, vp]),
+        "rvk_dcg_loopback_solve": (i, [C.POINTER(vp), i, C.POINTER(vp), C.POINTER(vp)]),
+        "rvk_dcg_result": (i, [vp, vp, C.POINTER(CgInfo)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
