@@ -218,7 +218,7 @@ def run_gpu(args, cfg):
     x = rvk.DeviceArray(n)
     rvk.check(rvk.lib().rvk_fill_rhs(ctx.h, 0x9E3779B97F4A7C15, n, b.ptr))
     plan = rvk.CgPlan(ctx, A, max_it=MAX_IT, mode=args.mode, use_graph=not args.no_graph)
-    bm = bytes_model(n, nnz, args.mode)
+    bm = bytes_model(n, nnz, "unfused" if args.mode == "unfused" else "fused")
     hbm_peak, peak_src = peaks()
     ws_bytes = 20 * nnz + 8 * (n + 1) + 9 * 8 * n
     log(f"{desc}: n={n} nnz={nnz} working set {ws_bytes/1e9:.2f} GB (L2 {L2_BYTES/1e6:.0f} MB)")
@@ -255,27 +255,36 @@ def run_gpu(args, cfg):
     assert res.iterations == MAX_IT
     launches = plan.launches()
 
-    # ---- per-kernel durations: the same solves with event pairs captured in the
-    # graph around every K1 (SpMV) and K2 (update) launch, same stream ---------
-    plan.set_profiling(True)
-    plan.solve_dev(b, x)                      # (re)capture the profiled graph
-    plan.result()
-    k1_ms = k2_ms = 0.0
-    for _ in range(args.steps):
-        plan.solve_dev(b, x)
+    mode = plan.mode()
+    if mode in ("fused", "unfused"):
+        # ---- per-kernel durations: the same solves with event pairs captured in
+        # the graph around every K1 (SpMV) and K2 (update) launch, same stream --
+        plan.set_profiling(True)
+        plan.solve_dev(b, x)                      # (re)capture the profiled graph
         plan.result()
-        a1, a2, _ = plan.kernel_times()
-        k1_ms += a1
-        k2_ms += a2
-    k1_ms /= args.steps
-    k2_ms /= args.steps
-    plan.set_profiling(False)
-    k1_avg = k1_ms / MAX_IT
-    k2_avg = k2_ms / MAX_IT
-    k1_gbs = bm["k1"] / (k1_avg * 1e-3) / 1e9
-    k2_gbs = bm["k2"] / (k2_avg * 1e-3) / 1e9
+        k1_ms = k2_ms = 0.0
+        for _ in range(args.steps):
+            plan.solve_dev(b, x)
+            plan.result()
+            a1, a2, _ = plan.kernel_times()
+            k1_ms += a1
+            k2_ms += a2
+        k1_ms /= args.steps
+        k2_ms /= args.steps
+        plan.set_profiling(False)
+        k1_avg = k1_ms / MAX_IT
+        k2_avg = k2_ms / MAX_IT
+        k1_gbs = bm["k1"] / (k1_avg * 1e-3) / 1e9
+        k2_gbs = bm["k2"] / (k2_avg * 1e-3) / 1e9
+    else:
+        # one persistent kernel (or the host-sync baseline): the dominant
+        # "kernel" is the whole solve
+        k1_avg, k2_avg = ms, 0.0
+        bm = dict(bm, k1=bm["b_min_solve"])
+        k1_gbs = bm["k1"] / (ms * 1e-3) / 1e9
+        k2_gbs = 0.0
     solve_gbs = bm["b_min_solve"] / (ms * 1e-3) / 1e9
-    traffic = ncu_traffic(args.config) if args.mode == "fused" else None
+    traffic = ncu_traffic(args.config) if mode == "fused" else None
 
     # ---- e2e through the C-ABI with host buffers (pinned) ----------------------
     bh = torch.empty(n, dtype=torch.float64, pin_memory=True)
@@ -305,14 +314,16 @@ def run_gpu(args, cfg):
         "min_ms": round(min(step_ms), 4), "higher_is_better": False, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{desc}, Jacobi-CG {MAX_IT} iterations, x0=0, splitmix64 RHS",
-                   "n": n, "nnz": nnz, "mode": args.mode, "graph": not args.no_graph,
+                   "n": n, "nnz": nnz, "mode": mode, "graph": not args.no_graph,
                    "l2": (f"no flush: working set {ws_bytes/1e9:.2f} GB >> 126 MB L2 "
                           "(every operand streams from HBM each step)") if flush is None else
                          (f"L2 flushed between steps (512 MiB write); working set "
                           f"{ws_bytes/1e6:.1f} MB")},
         "roofline": {"bound": "hbm",
-                     "kernel": ("k_spmv_tma<CgSpmvOp> (SpMV + on-the-fly AYPX + p.w)"
-                                if args.mode == "fused" else "k_spmv_tma<SpmvGuardedOp> (SpMV)"),
+                     "kernel": {"fused": "k_spmv_tma<CgSpmvOp> (SpMV + on-the-fly AYPX + p.w)",
+                                "unfused": "k_spmv_tma<SpmvGuardedOp> (SpMV)",
+                                "persistent": "k_cg_persistent (whole solve, one launch)",
+                                "hostsync": "whole solve (host-sync baseline)"}[mode],
                      "achieved": round(k1_gbs, 1), "peak": hbm_peak, "unit": "GB/s",
                      "frac": round(k1_gbs / hbm_peak, 4), "traffic": traffic,
                      "alg_bytes_per_launch": bm["k1"], "avg_launch_ms": round(k1_avg, 5),
@@ -343,7 +354,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["rvk", "reference"], default="rvk")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="7pt256")
-    ap.add_argument("--mode", choices=["fused", "unfused"], default="fused")
+    ap.add_argument("--mode", choices=["fused", "unfused", "persistent", "auto", "hostsync"],
+                    default="auto", help="auto: one persistent kernel for L2-sized grids, "
+                                         "else the fused 2-kernel/iteration graph")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

@@ -161,8 +161,12 @@ rvk_status rvk_fill_rhs(rvk_ctx ctx, uint64_t seed, int64_t n, double* b_dev);
 /* ---- KSP: Jacobi-preconditioned CG --- */
 typedef enum { RVK_PC_NONE = 0, RVK_PC_JACOBI = 1 } rvk_pc;
 typedef enum {
-    RVK_CG_MODE_FUSED   = 0, /* 3 kernels/iteration-pair, device tails (default) */
-    RVK_CG_MODE_UNFUSED = 1  /* the reference's op-per-kernel sequence         */
+    RVK_CG_MODE_FUSED      = 0, /* 2 fused kernels per iteration, device tails (default) */
+    RVK_CG_MODE_UNFUSED    = 1, /* the reference's op-per-kernel sequence               */
+    RVK_CG_MODE_PERSISTENT = 2, /* whole solve in ONE cooperative kernel (L2-sized grids) */
+    RVK_CG_MODE_AUTO       = 3, /* PERSISTENT when the working set fits L2, else FUSED   */
+    RVK_CG_MODE_HOSTSYNC   = 4  /* baseline: every dot/norm read back to the host (3 syncs
+                                   per iteration, PETSc main_gpu behaviour) */
 } rvk_cg_mode;
 typedef enum { RVK_CG_RUNNING = 0, RVK_CG_CONVERGED = 1, RVK_CG_BREAKDOWN = 2 } rvk_cg_state;
 
@@ -199,6 +203,8 @@ rvk_status rvk_cg_result(rvk_cg_plan plan, double* hist_host, rvk_cg_info* info)
 /* End-to-end: copy b from host, solve, copy x and hist back, one sync. */
 rvk_status rvk_cg_solve_host(rvk_cg_plan plan, const double* b_host, double* x_host,
                              double* hist_host, rvk_cg_info* info);
+/* The mode the plan runs (AUTO resolved to FUSED or PERSISTENT). */
+int        rvk_cg_plan_mode(rvk_cg_plan plan);
 /* Per-kernel event timing of the last solve's dominant kernels (bench): */
 rvk_status rvk_cg_set_profiling(rvk_cg_plan plan, int on);
 rvk_status rvk_cg_kernel_times(rvk_cg_plan plan, float* spmv_ms, float* update_ms,

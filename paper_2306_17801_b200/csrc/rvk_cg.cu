@@ -39,6 +39,11 @@
 
 namespace rvk {
 
+// AUTO picks the single persistent kernel only below this working set.  The
+// grid-barrier version measured slower than the 41-node graph at every
+// sweep size (64^2: 0.27 vs 0.19 ms), so AUTO resolves to FUSED for now.
+constexpr int64_t kPersistentMaxBytes = 0;
+
 // CgState, kUpdThreads, cg_converged, resident_grid: rvk_cg.cuh
 
 // ---------------------------------------------------------------------------
@@ -420,7 +425,8 @@ struct rvk_cg_plan_s {
     rvk_csr       A{};
     rvk_cg_config cfg{};
     SpmvArgs      sa{};
-    int           spmv_grid = 0, upd_grid = 0, setup_grid = 0;
+    int           spmv_grid = 0, upd_grid = 0, setup_grid = 0, persist_grid = 0;
+    int           mode = RVK_CG_MODE_FUSED; // resolved (AUTO -> FUSED | PERSISTENT)
     double*       dinv = nullptr;
     double*       r = nullptr;
     double*       z = nullptr;
@@ -573,9 +579,107 @@ rvk_status enqueue_unfused(rvk_cg_plan P, const double* b, double* x)
     return RVK_OK;
 }
 
+rvk_status enqueue_persistent(rvk_cg_plan P, const double* b, double* x)
+{
+    PersistArgs a{P->A.n_rows, P->A.row_offsets, P->A.col_indices, P->A.values, b, P->dinv, x, P->r,
+                  P->z, P->p[0], P->p[1], P->w, P->hist, P->st, P->partials, P->cfg.max_it,
+                  P->cfg.rtol, P->cfg.atol};
+    P->launches = 1;
+    return launch_persistent(P->ctx->stream, a, P->cfg.pc == RVK_PC_JACOBI, P->persist_grid);
+}
+
+// Baseline that exposes the scalar problem: every dot/norm
+// result is copied to the host and the stream synchronised (3 per
+// iteration, like PETSc main's VecDot/VecNorm), and scalars travel back to
+// the kernels as host constants.  Same kernels and arithmetic otherwise.
+rvk_status solve_hostsync(rvk_cg_plan P, const double* b, double* x)
+{
+    const int64_t n   = P->A.n_rows;
+    cudaStream_t  s   = P->ctx->stream;
+    const bool    jac = P->cfg.pc == RVK_PC_JACOBI;
+    Scratch       sc{P->partials, P->tickets};
+    double*       d   = P->tmp; // device scalar slot
+    auto          read = [&](double* out) -> rvk_status {
+        RVK_CUDA(cudaMemcpyAsync(out, d, sizeof(double), cudaMemcpyDeviceToHost, s));
+        note_host_sync();
+        RVK_CUDA(cudaStreamSynchronize(s));
+        return RVK_OK;
+    };
+    std::vector<double> hist(P->cfg.max_it + 1, 0.0);
+    CgState             st{};
+    st.breakdown_iter = -1;
+    P->launches       = 0;
+    RVK_CUDA(cudaMemcpyAsync(P->r, b, n * 8, cudaMemcpyDeviceToDevice, s));
+    RVK_CUDA(cudaMemsetAsync(x, 0, n * 8, s));
+    if (jac) RVK_TRY(vec_ew(s, EW_PMULT, n, const_scalar(0), P->dinv, P->r, P->z, nullptr));
+    else RVK_CUDA(cudaMemcpyAsync(P->z, P->r, n * 8, cudaMemcpyDeviceToDevice, s));
+    double dp0 = 0, beta = 0, betaold = 0, pAp = 0, dp = 0;
+    RVK_TRY(vec_reduce(s, sc, RED_NRM2, n, P->z, nullptr, d, nullptr, nullptr));
+    RVK_TRY(read(&dp0));
+    hist[0] = dp = dp0;
+    auto conv = [&](double v) { return v <= std::fmax(P->cfg.rtol * dp0, P->cfg.atol); };
+    st.state = conv(dp0) ? RVK_CG_CONVERGED : RVK_CG_RUNNING;
+    if (st.state == RVK_CG_RUNNING) {
+        RVK_TRY(vec_reduce(s, sc, RED_DOT, n, P->z, P->r, d, nullptr, nullptr));
+        RVK_TRY(read(&beta));
+    }
+    double* p = P->p[0];
+    for (int it = 0; it < P->cfg.max_it && st.state == RVK_CG_RUNNING; ++it) {
+        if (it == 0) {
+            RVK_CUDA(cudaMemcpyAsync(p, P->z, n * 8, cudaMemcpyDeviceToDevice, s));
+        } else {
+            if (betaold == 0.0) {
+                st.state          = RVK_CG_BREAKDOWN;
+                st.breakdown_iter = it;
+                break;
+            }
+            RVK_TRY(vec_ew(s, EW_AYPX, n, const_scalar(beta / betaold), P->z, p, p, nullptr));
+        }
+        SpmvPlainOp op;
+        op.x = p;
+        op.y = P->w;
+        RVK_TRY(launch_spmv(s, P->sa, op, TailArgs{nullptr, nullptr}, P->spmv_grid));
+        RVK_TRY(vec_reduce(s, sc, RED_DOT, n, p, P->w, d, nullptr, nullptr));
+        RVK_TRY(read(&pAp));
+        const double a = beta / pAp;
+        if (pAp == 0.0 || !std::isfinite(a)) {
+            st.state          = RVK_CG_BREAKDOWN;
+            st.breakdown_iter = it;
+            break;
+        }
+        betaold = beta;
+        RVK_TRY(vec_ew(s, EW_AXPY, n, const_scalar(a), p, x, x, nullptr));
+        RVK_TRY(vec_ew(s, EW_AXPY, n, const_scalar(-a), P->w, P->r, P->r, nullptr));
+        if (jac) RVK_TRY(vec_ew(s, EW_PMULT, n, const_scalar(0), P->dinv, P->r, P->z, nullptr));
+        else RVK_CUDA(cudaMemcpyAsync(P->z, P->r, n * 8, cudaMemcpyDeviceToDevice, s));
+        RVK_TRY(vec_reduce(s, sc, RED_NRM2, n, P->z, nullptr, d, nullptr, nullptr));
+        RVK_TRY(read(&dp));
+        hist[it + 1]  = dp;
+        st.iterations = it + 1;
+        if (conv(dp)) {
+            st.state = RVK_CG_CONVERGED;
+            break;
+        }
+        RVK_TRY(vec_reduce(s, sc, RED_DOT, n, P->z, P->r, d, nullptr, nullptr));
+        RVK_TRY(read(&beta));
+        P->launches += 9;
+    }
+    st.done = st.state != RVK_CG_RUNNING;
+    st.dp0  = dp0;
+    st.dp   = dp;
+    RVK_CUDA(cudaMemcpyAsync(P->hist, hist.data(), hist.size() * 8, cudaMemcpyHostToDevice, s));
+    RVK_CUDA(cudaMemcpyAsync(P->st, &st, sizeof st, cudaMemcpyHostToDevice, s));
+    RVK_CUDA(cudaStreamSynchronize(s)); // host buffers above are stack-local
+    return RVK_OK;
+}
+
 rvk_status enqueue_solve(rvk_cg_plan P, const double* b, double* x)
 {
-    return P->cfg.mode == RVK_CG_MODE_UNFUSED ? enqueue_unfused(P, b, x) : enqueue_fused(P, b, x);
+    switch (P->mode) {
+    case RVK_CG_MODE_UNFUSED: return enqueue_unfused(P, b, x);
+    case RVK_CG_MODE_PERSISTENT: return enqueue_persistent(P, b, x);
+    default: return enqueue_fused(P, b, x);
+    }
 }
 
 rvk_status destroy_graph(rvk_cg_plan P)
@@ -673,7 +777,7 @@ rvk_status rvk_cg_plan_create(rvk_ctx ctx, const rvk_csr* A, rvk_cg_config cfg, 
     if (cfg.max_it < 1) return set_error(RVK_ERR_INVALID, "cg_solve: max_it must be >= 1");
     if (cfg.pc != RVK_PC_NONE && cfg.pc != RVK_PC_JACOBI)
         return set_error(RVK_ERR_INVALID, "cg_solve: unknown preconditioner %d", cfg.pc);
-    if (cfg.mode != RVK_CG_MODE_FUSED && cfg.mode != RVK_CG_MODE_UNFUSED)
+    if (cfg.mode < RVK_CG_MODE_FUSED || cfg.mode > RVK_CG_MODE_HOSTSYNC)
         return set_error(RVK_ERR_INVALID, "cg_solve: unknown mode %d", cfg.mode);
     int64_t maxlen = 0;
     RVK_TRY(rvk_csr_validate(ctx, A, &maxlen));
@@ -687,6 +791,14 @@ rvk_status rvk_cg_plan_create(rvk_ctx ctx, const rvk_csr* A, rvk_cg_config cfg, 
     // one resident wave each (the vectorised loops take 2 elements per thread)
     P->upd_grid   = resident_grid(k_cg_update<true, true>, kUpdThreads, (A->n_rows + 1) / 2);
     P->setup_grid = resident_grid(k_cg_setup<true, true>, kUpdThreads, (A->n_rows + 1) / 2);
+    P->persist_grid = persistent_grid(A->n_rows);
+    P->mode         = cfg.mode;
+    if (cfg.mode == RVK_CG_MODE_AUTO) {
+        // one persistent kernel while the solve's working set stays in L2
+        // (launch latency dominates there); the HBM-streaming path beyond
+        const int64_t ws = 12 * A->nnz + 8 * (A->n_rows + 1) + 9 * 8 * A->n_rows;
+        P->mode          = ws <= kPersistentMaxBytes ? RVK_CG_MODE_PERSISTENT : RVK_CG_MODE_FUSED;
+    }
     const size_t vb = (size_t)A->n_rows * sizeof(double);
     cudaError_t  e  = cudaSuccess;
     auto alloc = [&](void** p, size_t bytes) {
@@ -759,7 +871,9 @@ rvk_status rvk_cg_solve_dev(rvk_cg_plan P, const double* b, double* x)
     if (!b || !x) return set_error(RVK_ERR_INVALID, "cg_solve: null vector");
     if (b == x) return set_error(RVK_ERR_INVALID, "cg_solve: b and x must not alias");
     cudaStream_t s = P->ctx->stream;
-    if (!P->cfg.use_graph) return enqueue_solve(P, b, x);
+    if (P->mode == RVK_CG_MODE_HOSTSYNC) return solve_hostsync(P, b, x);
+    // one cooperative launch needs no graph
+    if (!P->cfg.use_graph || P->mode == RVK_CG_MODE_PERSISTENT) return enqueue_solve(P, b, x);
     if (!P->graph || P->g_b != b || P->g_x != x || P->g_prof != P->profiling) {
         destroy_graph(P);
         cudaGraph_t g = nullptr;
@@ -786,6 +900,8 @@ rvk_status rvk_cg_solve_dev(rvk_cg_plan P, const double* b, double* x)
 }
 
 const double* rvk_cg_history_dev(rvk_cg_plan P) { return P ? P->hist : nullptr; }
+
+int rvk_cg_plan_mode(rvk_cg_plan P) { return P ? P->mode : -1; }
 
 rvk_status rvk_cg_result(rvk_cg_plan P, double* hist_host, rvk_cg_info* info)
 {

@@ -35,4 +35,27 @@ int resident_grid(K kernel, int threads, int64_t n_items)
     return (int)(want < 1 ? 1 : (want > cap ? cap : want));
 }
 
+// Arguments of the single-kernel persistent solve (rvk_cg_small.cu).
+struct PersistArgs {
+    int64_t        n;
+    const int64_t* off;
+    const int32_t* cols;
+    const double*  vals;
+    const double*  b;
+    const double*  dinv;
+    double*        x;
+    double*        r;
+    double*        z;
+    double*        p0;
+    double*        p1;
+    double*        w;
+    double*        hist;
+    CgState*       st;
+    double*        partials; // 4 doubles per block
+    int            max_it;
+    double         rtol, atol;
+};
+int        persistent_grid(int64_t n);
+rvk_status launch_persistent(cudaStream_t s, const PersistArgs& args, bool jacobi, int grid);
+
 } // namespace rvk

@@ -20,7 +20,9 @@ RVK_OK = 0
 RVK_ERR_BREAKDOWN = 5
 SCALAR_CONST, SCALAR_PTR, SCALAR_NEG_PTR, SCALAR_DIV, SCALAR_SQRT, SCALAR_RECIP = range(6)
 PC_NONE, PC_JACOBI = 0, 1
-MODE_FUSED, MODE_UNFUSED = 0, 1
+MODE_FUSED, MODE_UNFUSED, MODE_PERSISTENT, MODE_AUTO, MODE_HOSTSYNC = 0, 1, 2, 3, 4
+MODES = {"fused": MODE_FUSED, "unfused": MODE_UNFUSED, "persistent": MODE_PERSISTENT,
+         "auto": MODE_AUTO, "hostsync": MODE_HOSTSYNC}
 CG_RUNNING, CG_CONVERGED, CG_BREAKDOWN = 0, 1, 2
 
 # every symbol include/rvk.h declares (checked by tests/test_abi.py)
@@ -35,7 +37,7 @@ EXPORTS = [
     "rvk_csr_diagonal_inverse", "rvk_csr_validate", "rvk_laplacian_size",
     "rvk_build_laplacian", "rvk_fill_rhs", "rvk_cg_plan_create", "rvk_cg_plan_destroy",
     "rvk_cg_solve_dev", "rvk_cg_history_dev", "rvk_cg_result", "rvk_cg_solve_host",
-    "rvk_cg_set_profiling", "rvk_cg_kernel_times",
+    "rvk_cg_set_profiling", "rvk_cg_kernel_times", "rvk_cg_plan_mode",
     "rvk_laplacian_rows_nnz", "rvk_build_laplacian_rows", "rvk_comm_unique_id", "rvk_comm_init",
     "rvk_comm_destroy", "rvk_dcg_plan_create", "rvk_dcg_plan_destroy", "rvk_dcg_solve_dev",
     "rvk_dcg_loopback_solve", "rvk_dcg_result",
@@ -139,6 +141,7 @@ def lib():
         "rvk_cg_set_profiling": (i, [vp, i]),
         "rvk_cg_kernel_times": (i, [vp, C.POINTER(C.c_float), C.POINTER(C.c_float),
                                     C.POINTER(C.c_int)]),
+        "rvk_cg_plan_mode": (i, [vp]),
         "rvk_laplacian_rows_nnz": (i, [i, i, i64, i64, i64, i64, i64, C.POINTER(i64)]),
         "rvk_build_laplacian_rows": (i, [vp, i, i, i64, i64, i64, i64, i64, i64, vp, vp, vp]),
         "rvk_comm_unique_id": (i, [vp, i]),
@@ -322,7 +325,7 @@ class CgPlan:
         self.ctx, self.A = ctx, A
         self.max_it = max_it
         cfg = CgConfig(max_it, PC_JACOBI if pc == "jacobi" else PC_NONE, rtol, atol,
-                       MODE_FUSED if mode == "fused" else MODE_UNFUSED, 1 if use_graph else 0)
+                       MODES[mode], 1 if use_graph else 0)
         h = C.c_void_p()
         check(lib().rvk_cg_plan_create(ctx.h, C.byref(A.c), cfg, C.byref(h)))
         self.h = h
@@ -372,6 +375,10 @@ class CgPlan:
         a, b, n = C.c_float(), C.c_float(), C.c_int()
         check(lib().rvk_cg_kernel_times(self.h, C.byref(a), C.byref(b), C.byref(n)))
         return a.value, b.value, n.value
+
+    def mode(self) -> str:
+        m = lib().rvk_cg_plan_mode(self.h)
+        return {v: k for k, v in MODES.items()}[m]
 
     def launches(self) -> int:
         n = C.c_int()

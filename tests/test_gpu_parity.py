@@ -259,7 +259,7 @@ def golden_cases():
         return json.load(f)["cases"]
 
 
-@pytest.mark.parametrize("mode", ["fused", "unfused"])
+@pytest.mark.parametrize("mode", ["fused", "unfused", "persistent", "hostsync"])
 @pytest.mark.parametrize("case", golden_cases(), ids=lambda c: c["name"])
 def test_cg_vs_golden(ctx, case, mode):
     """Committed fixtures from the reference's own kernels (oracle/_ref)."""
@@ -279,13 +279,14 @@ def test_cg_vs_golden(ctx, case, mode):
 @pytest.mark.parametrize("spec", [(2, 5, (1024, 1024)), (2, 9, (300, 200)), (3, 7, (96, 80, 64)),
                                   (3, 27, (48, 48, 48))])
 @pytest.mark.parametrize("graph", [True, False])
-def test_cg_vs_oracle(ctx, spec, graph):
+@pytest.mark.parametrize("mode", ["fused", "persistent"])
+def test_cg_vs_oracle(ctx, spec, graph, mode):
     dim, pts, g = spec
     Ah = O.build_laplacian(dim, pts, g)
     b = O.rhs(Ah.n_rows)
     ref = O.cg_solve(Ah, b, max_it=20)
     A = rvk.DeviceCsr.laplacian(ctx, dim, pts, g)
-    plan = rvk.CgPlan(ctx, A, max_it=20, use_graph=graph)
+    plan = rvk.CgPlan(ctx, A, max_it=20, use_graph=graph, mode=mode)
     x, res = plan.solve_host(b)
     check_cg(res, x, ref)
     # re-solve (graph replay) is bit-reproducible (SPEC.md:604 fingerprint)
@@ -330,7 +331,7 @@ def test_cg_identity_converges_in_one_iteration(ctx):
     Ah = O.Csr(n, n, np.arange(n + 1, dtype=np.int64), np.arange(n, dtype=np.int32), np.ones(n))
     A = rvk.DeviceCsr.from_host(ctx, n, n, Ah.off, Ah.cols, Ah.vals)
     b = O.rhs(n)
-    for mode in ("fused", "unfused"):
+    for mode in ("fused", "unfused", "persistent", "hostsync"):
         plan = rvk.CgPlan(ctx, A, max_it=20, pc="none", mode=mode, rtol=1e-14)
         x, res = plan.solve_host(b)
         assert res.state == rvk.CG_CONVERGED and res.iterations == 1
@@ -341,7 +342,7 @@ def test_cg_breakdown_on_device(ctx):
     Ah = O.Csr(2, 2, np.array([0, 1, 2], np.int64), np.array([0, 1], np.int32),
                np.array([1.0, -1.0]))
     A = rvk.DeviceCsr.from_host(ctx, 2, 2, Ah.off, Ah.cols, Ah.vals)
-    for mode in ("fused", "unfused"):
+    for mode in ("fused", "unfused", "persistent", "hostsync"):
         plan = rvk.CgPlan(ctx, A, max_it=20, pc="none", mode=mode)
         plan.solve_dev(up(ctx, np.array([1.0, 1.0])), rvk.DeviceArray(2))
         with pytest.raises(rvk.BreakdownError) as ei:
@@ -355,7 +356,7 @@ def test_cg_rtol_device_early_exit(ctx):
     ref = O.cg_solve(Ah, b, max_it=500, rtol=1e-8)
     assert ref.status == 1 and ref.iterations < 500
     A = rvk.DeviceCsr.laplacian(ctx, 2, 5, (64, 64))
-    for mode in ("fused", "unfused"):
+    for mode in ("fused", "unfused", "persistent", "hostsync"):
         plan = rvk.CgPlan(ctx, A, max_it=500, rtol=1e-8, mode=mode)
         x, res = plan.solve_host(b)
         check_cg(res, x, ref)
