@@ -34,7 +34,10 @@
 #include "rvk_cg.cuh"
 #include "rvk_spmv.cuh"
 
+#include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 namespace rvk {
@@ -150,20 +153,25 @@ struct CgSpmvOp {
     struct Fetch {
         double z, p;
     };
-    __device__ __forceinline__ Fetch fetch(int32_t j) const
+    __device__ __forceinline__ int           num_src() const { return FIRST ? 1 : 2; }
+    __device__ __forceinline__ const double* src_ptr(int k) const { return k == 0 ? z : p_old; }
+    __device__ __forceinline__ Fetch         fetch(int32_t j) const
     {
         return Fetch{__ldg(z + j), FIRST ? 0.0 : __ldg(p_old + j)};
+    }
+    __device__ __forceinline__ Fetch fetch_smem(const double* s0, const double* s1, int i) const
+    {
+        return Fetch{s0[i], FIRST ? 0.0 : s1[i]};
     }
     __device__ __forceinline__ double value(const Fetch& f) const
     {
         return FIRST ? f.z : aypx1(b, f.z, f.p); // z + b*p  (kernels_scalar.cpp:33)
     }
-    __device__ __forceinline__ double src(int32_t j) const { return value(fetch(j)); }
-    using Own = Fetch;
-    __device__ __forceinline__ Own own_fetch(int64_t i) const { return fetch((int32_t)i); }
-    __device__ __forceinline__ double row(int64_t i, double sum, double acc, const Own& o) const
+    __device__ __forceinline__ int64_t own_col(int64_t i) const { return i; }
+    // p_new[i] = z[i] + b p_old[i] from the row's own (gathered) operands
+    __device__ __forceinline__ double row(int64_t i, double sum, double acc, const Fetch& o) const
     {
-        const double p = value(o); // p_new[i] = z[i] + b p_old[i]
+        const double p = value(o);
         p_new[i]       = p;
         w[i]           = sum;
         return add(acc, mul(p, sum));
@@ -406,6 +414,80 @@ int update_grid(int64_t n)
 }
 
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// ---- stencil structure (plan time) -------------------------------------------
+constexpr int                kDiagTable = 128;
+constexpr unsigned long long kDiagEmpty = ~0ull;
+
+__global__ void k_diagonals(int64_t n, const int64_t* __restrict__ off,
+                            const int32_t* __restrict__ cols, unsigned long long* table,
+                            int* overflow)
+{
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += stride) {
+        for (int64_t k = off[r]; k < off[r + 1]; ++k) {
+            // sign bit flipped so no diagonal (d = -1 included) aliases the empty marker
+            const unsigned long long key =
+                (unsigned long long)((long long)cols[k] - (long long)r) ^ (1ull << 63);
+            // lanes that found the same diagonal insert once (warp dedupe)
+            const unsigned peers  = __match_any_sync(__activemask(), key);
+            const int      leader = __ffs(peers) - 1;
+            if ((int)(threadIdx.x & 31) != leader) continue;
+            unsigned h = (unsigned)((key * 0x9E3779B97F4A7C15ull) >> 57) & (kDiagTable - 1);
+            bool     done = false;
+            for (int probe = 0; probe < kDiagTable && !done; ++probe, h = (h + 1) & (kDiagTable - 1)) {
+                const unsigned long long v = *((volatile unsigned long long*)&table[h]);
+                if (v == key) done = true;
+                else if (v == kDiagEmpty) {
+                    const unsigned long long old = atomicCAS(&table[h], kDiagEmpty, key);
+                    done = (old == kDiagEmpty || old == key);
+                }
+            }
+            if (!done) atomicExch(overflow, 1);
+        }
+    }
+}
+
+rvk_status csr_windows(cudaStream_t s, const rvk_csr& A, SpmvWindows* out)
+{
+    *out = SpmvWindows{};
+    if (A.n_rows == 0 || A.nnz == 0) return RVK_OK;
+    unsigned long long* table = nullptr;
+    RVK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&table), kDiagTable * 8 + 16, s));
+    int* overflow = reinterpret_cast<int*>(table + kDiagTable);
+    RVK_CUDA(cudaMemsetAsync(table, 0xff, kDiagTable * 8, s));
+    RVK_CUDA(cudaMemsetAsync(overflow, 0, 4, s));
+    const int g = (int)std::min<int64_t>((A.n_rows + 255) / 256, (int64_t)sm_count() * 8);
+    k_diagonals<<<g, 256, 0, s>>>(A.n_rows, A.row_offsets, A.col_indices, table, overflow);
+    RVK_CHECK_LAUNCH("k_diagonals");
+    std::vector<unsigned long long> h(kDiagTable + 2);
+    RVK_CUDA(cudaMemcpyAsync(h.data(), table, kDiagTable * 8 + 16, cudaMemcpyDeviceToHost, s));
+    RVK_CUDA(cudaFreeAsync(table, s));
+    note_host_sync();
+    RVK_CUDA(cudaStreamSynchronize(s));
+    if (reinterpret_cast<int*>(&h[kDiagTable])[0]) return RVK_OK; // > 128 diagonals: general CSR
+    std::vector<int64_t> d;
+    for (int i = 0; i < kDiagTable; ++i)
+        if (h[i] != kDiagEmpty) d.push_back((int64_t)(long long)(h[i] ^ (1ull << 63)));
+    std::sort(d.begin(), d.end());
+    // bands: diagonals closer than kGap share a window (at most kGap wasted
+    // doubles per gap); give up beyond kSpmvMaxWin bands or wide bands
+    constexpr int64_t kGap = 64, kMaxBand = 4096;
+    SpmvWindows W;
+    for (int64_t v : d) {
+        if (W.n > 0 && v - W.hi[W.n - 1] <= kGap) {
+            W.hi[W.n - 1] = v;
+        } else {
+            if (W.n == kSpmvMaxWin) return RVK_OK;
+            W.lo[W.n] = W.hi[W.n] = v;
+            ++W.n;
+        }
+    }
+    for (int w = 0; w < W.n; ++w)
+        if (W.hi[w] - W.lo[w] > kMaxBand) return RVK_OK;
+    *out = W;
+    return RVK_OK;
+}
 
 rvk_status diag_inverse(cudaStream_t s, const rvk_csr& A, int64_t col_off, double* dinv)
 {
@@ -786,7 +868,23 @@ rvk_status rvk_cg_plan_create(rvk_ctx ctx, const rvk_csr* A, rvk_cg_config cfg, 
     P->ctx       = ctx;
     P->A         = *A;
     P->cfg       = cfg;
-    P->sa        = make_spmv_args(*A, maxlen);
+    // x-windows (stage the gathered vectors' diagonal bands via TMA) are an
+    // opt-in experiment (RVK_WINDOWS=1): measured slower than L1-cached
+    // gathers on the 2D stencils (9-pt 4096^2 K1 806 vs 467 us, window
+    // lookup made the consumers issue-bound); the 3D stencils have > 4 bands.
+    SpmvWindows win;
+    if (!std::getenv("RVK_WINDOWS") || csr_windows(ctx->stream, *A, &win) != RVK_OK)
+        win = SpmvWindows{};
+    P->sa        = make_spmv_args(*A, maxlen, &win, 2);
+    if (std::getenv("RVK_DEBUG")) {
+        std::fprintf(stderr, "[rvk] plan n=%lld nnz=%lld R=%d stages=%d groups=%d cap=%d nwin=%d",
+                     (long long)A->n_rows, (long long)A->nnz, P->sa.R, P->sa.stages, P->sa.groups,
+                     P->sa.cap, P->sa.nwin);
+        for (int w = 0; w < P->sa.nwin; ++w)
+            std::fprintf(stderr, " [%lld,%lld]@%d", (long long)P->sa.win_lo[w],
+                         (long long)P->sa.win_hi[w], P->sa.win_base[w]);
+        std::fprintf(stderr, " win_elems=%d stage_bytes=%d\n", P->sa.win_elems, P->sa.stage_bytes);
+    }
     P->spmv_grid = sm_count();
     // one resident wave each (the vectorised loops take 2 elements per thread)
     P->upd_grid   = resident_grid(k_cg_update<true, true>, kUpdThreads, (A->n_rows + 1) / 2);
@@ -806,9 +904,10 @@ rvk_status rvk_cg_plan_create(rvk_ctx ctx, const rvk_csr* A, rvk_cg_config cfg, 
     };
     alloc(reinterpret_cast<void**>(&P->dinv), vb);
     alloc(reinterpret_cast<void**>(&P->r), vb);
-    alloc(reinterpret_cast<void**>(&P->z), vb);
-    alloc(reinterpret_cast<void**>(&P->p[0]), vb);
-    alloc(reinterpret_cast<void**>(&P->p[1]), vb);
+    // gathered sources: +4 doubles so x-window copies may round up past n
+    alloc(reinterpret_cast<void**>(&P->z), vb + 32);
+    alloc(reinterpret_cast<void**>(&P->p[0]), vb + 32);
+    alloc(reinterpret_cast<void**>(&P->p[1]), vb + 32);
     alloc(reinterpret_cast<void**>(&P->w), vb);
     alloc(reinterpret_cast<void**>(&P->hist), sizeof(double) * (cfg.max_it + 1));
     alloc(reinterpret_cast<void**>(&P->st), sizeof(CgState));

@@ -162,6 +162,14 @@ __device__ __forceinline__ uint64_t policy_evict_first()
     return p;
 }
 
+// ... and for data several CTAs will re-read soon (the x-windows).
+__device__ __forceinline__ uint64_t policy_evict_last()
+{
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+
 // 1-D bulk copy global -> shared, completion signalled on `bar` (tx bytes).
 // dst/src 16-byte aligned, bytes a multiple of 16.
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,

@@ -35,6 +35,7 @@
 #include <dlfcn.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <type_traits>
@@ -212,21 +213,26 @@ struct DcgSpmvOp {
     struct Fetch {
         double z, p;
     };
-    __device__ __forceinline__ Fetch fetch(int32_t j) const
+    __device__ __forceinline__ int           num_src() const { return FIRST ? 1 : 2; }
+    __device__ __forceinline__ const double* src_ptr(int k) const { return k == 0 ? z : p_old; }
+    __device__ __forceinline__ Fetch         fetch(int32_t j) const
     {
         return Fetch{__ldg(z + j), FIRST ? 0.0 : __ldg(p_old + j)};
+    }
+    __device__ __forceinline__ Fetch fetch_smem(const double* s0, const double* s1, int i) const
+    {
+        return Fetch{s0[i], FIRST ? 0.0 : s1[i]};
     }
     __device__ __forceinline__ double value(const Fetch& f) const
     {
         return FIRST ? f.z : aypx1(b, f.z, f.p);
     }
-    using Own = Fetch;
-    __device__ __forceinline__ Own own_fetch(int64_t i) const { return fetch((int32_t)(i + own_off)); }
-    __device__ __forceinline__ double row(int64_t i, double sum, double acc, const Own& o) const
+    __device__ __forceinline__ int64_t own_col(int64_t i) const { return i + own_off; }
+    __device__ __forceinline__ double row(int64_t i, double sum, double acc, const Fetch& o) const
     {
-        const double p       = value(o);
-        p_new[i + own_off]   = p;
-        w[i]                 = sum;
+        const double p     = value(o);
+        p_new[i + own_off] = p;
+        w[i]               = sum;
         return add(acc, mul(p, sum));
     }
     __device__ __forceinline__ void tail(double pAp_local) const { *gather_out = pAp_local; }
@@ -355,9 +361,9 @@ rvk_status alloc_plan_buffers(rvk_dcg_plan P)
     alloc((void**)&P->dinv, n * 8);
     alloc((void**)&P->r, n * 8);
     alloc((void**)&P->w, n * 8);
-    alloc((void**)&P->z, P->n_ext * 8);
-    alloc((void**)&P->p[0], P->n_ext * 8);
-    alloc((void**)&P->p[1], P->n_ext * 8);
+    alloc((void**)&P->z, P->n_ext * 8 + 32); // padded: x-windows round up
+    alloc((void**)&P->p[0], P->n_ext * 8 + 32);
+    alloc((void**)&P->p[1], P->n_ext * 8 + 32);
     alloc((void**)&P->hist, (P->cfg.max_it + 1) * 8);
     alloc((void**)&P->beta, (P->cfg.max_it + 1) * 8);
     alloc((void**)&P->st, sizeof(CgState));
@@ -564,7 +570,10 @@ rvk_status rvk_dcg_plan_create(rvk_ctx ctx, const rvk_csr* A, rvk_shard sh, rvk_
     P->A           = *A;
     P->sh          = sh;
     P->cfg         = cfg;
-    P->sa          = make_spmv_args(*A, maxlen);
+    SpmvWindows win; // opt-in, see rvk_cg.cu
+    if (!std::getenv("RVK_WINDOWS") || csr_windows(ctx->stream, *A, &win) != RVK_OK)
+        win = SpmvWindows{};
+    P->sa          = make_spmv_args(*A, maxlen, &win, 2);
     P->upd_grid    = resident_grid(k_dcg_update<true>, kUpdThreads, sh.n_own);
     P->owns_gather = shared_gather == nullptr;
     P->gather      = shared_gather;

@@ -24,6 +24,11 @@
 //    tile is shorter than the 512 consumer threads (long rows, e.g. 27-point:
 //    R = 128) the consumers split into NG groups that work on NG different
 //    ring stages at once, so no thread idles;
+//  * stencil-structured matrices (few distinct diagonals col - row, found at
+//    plan time) also get the tile's x-windows -- the contiguous ranges of the
+//    gathered vectors the tile's diagonals touch -- bulk-copied into the
+//    stage, so every gather is a conflict-free LDS instead of an L1/L2 round
+//    trip (other columns still fall back to a global load);
 //  * tiles that do not fit a stage (very long rows) and the last tile (whose
 //    16-byte-rounded bulk range could run past the arrays) are "direct":
 //    consumers read them from global memory thread-per-row;
@@ -41,8 +46,9 @@ constexpr int    kSpmvConsumerWarps = 16;
 constexpr int    kSpmvConsumers     = kSpmvConsumerWarps * 32;
 constexpr int    kSpmvThreads       = kSpmvConsumers + 32; // + producer warp
 constexpr int    kSpmvMaxStages     = 4;
-constexpr int    kSpmvChunkRows     = 32;
-constexpr int    kSpmvUnroll        = 8;                   // nonzeros per lane per sweep step
+constexpr int    kSpmvUnroll        = 8;                   // nonzeros per lane per batch
+constexpr int    kSpmvMaxWin        = 4;                   // x-windows per tile
+constexpr int    kSpmvMaxSrc        = 2;                   // gathered vectors per column
 constexpr size_t kSpmvHeaderBytes   = 1024;                // barriers, meta, reduction scratch
 constexpr size_t kSpmvStageBudget   = 200 * 1024;          // dynamic smem for the ring
 
@@ -51,16 +57,34 @@ struct SpmvStageMeta {
     int64_t kc0;    // first column index held in the stage (16-B aligned)
     int     direct; // 1: read this tile from global memory
     int     pad;
+    int64_t wlo[kSpmvMaxWin]; // global column range [wlo, whi) held by window w
+    int64_t whi[kSpmvMaxWin];
+};
+static_assert(kSpmvMaxStages * sizeof(SpmvStageMeta) <= 512 - 128, "meta must fit the header");
+
+// Plan-time structure of a stencil-like CSR: every nonzero's (col - row)
+// falls in one of n diagonal bands [lo_w, hi_w].  Only used with gathered
+// sources the plan allocated itself, 16-B aligned and padded by >= 2 doubles.
+struct SpmvWindows {
+    int     n = 0;
+    int64_t lo[kSpmvMaxWin] = {0, 0, 0, 0};
+    int64_t hi[kSpmvMaxWin] = {0, 0, 0, 0};
 };
 
 struct SpmvArgs {
     int64_t        n_rows;
+    int64_t        n_cols;
     int64_t        n_tiles;
     int            R;        // rows per tile (multiple of 32)
     int            stages;   // ring depth (<= kSpmvMaxStages)
     int            groups;   // consumer groups working on distinct stages (divides stages)
     int            cap;      // nonzeros per stage
-    int            off_bytes, val_bytes, stage_bytes; // stage layout: [off | vals | cols]
+    int            off_bytes, val_bytes, col_bytes, stage_bytes; // [off | vals | cols | windows]
+    int            nwin;                  // 0: no x-windows
+    int64_t        win_lo[kSpmvMaxWin];   // diagonal bands (col - row)
+    int64_t        win_hi[kSpmvMaxWin];
+    int            win_base[kSpmvMaxWin]; // element offset of window w inside one source's area
+    int            win_elems;             // doubles per source per stage
     const int64_t* off;
     const int32_t* cols;
     const double*  vals;
@@ -76,22 +100,32 @@ struct TailArgs {
 
 __host__ __device__ inline int align16(int64_t b) { return (int)((b + 15) & ~int64_t(15)); }
 
-// Tile geometry for a matrix whose longest row has max_row_len nonzeros: the
-// largest R (multiple of 32, <= 1024) whose worst-case slab fits a stage with
-// at least 3 stages in the ring, else 2.  Rows too long for any stage still
+// Tile geometry: the largest R (power of two, <= 1024) whose worst-case slab
+// (CSR rows of max_row_len, plus nsrc x-windows when W is given) fits a stage
+// with >= 3 stages in the ring (else 2).  Rows too long for any stage still
 // work (direct tiles).
-inline SpmvArgs make_spmv_args(const rvk_csr& A, int64_t max_row_len)
+inline SpmvArgs make_spmv_args(const rvk_csr& A, int64_t max_row_len,
+                               const SpmvWindows* W = nullptr, int nsrc = 1)
 {
     if (max_row_len < 1) max_row_len = 1;
     SpmvArgs a{};
     a.n_rows = A.n_rows;
+    a.n_cols = A.n_cols;
     a.off    = A.row_offsets;
     a.cols   = A.col_indices;
     a.vals   = A.values;
+    const int nwin = (W && W->n > 0 && W->n <= kSpmvMaxWin) ? W->n : 0;
     auto fit = [&](int R, int min_stages) {
         const int64_t cap = ((R * max_row_len + 8) + 3) & ~int64_t(3);
         const int64_t ob = align16((int64_t)(R + 2) * 8), vb = cap * 8, cb = align16(cap * 4);
-        const int64_t sb = ob + vb + cb;
+        int64_t we = 0;
+        int     base[kSpmvMaxWin] = {0, 0, 0, 0};
+        for (int w = 0; w < nwin; ++w) {
+            base[w] = (int)we;
+            // R + band width + 16-B rounding at both ends, kept 16-B aligned
+            we += ((R + (W->hi[w] - W->lo[w]) + 4) + 1) & ~int64_t(1);
+        }
+        const int64_t sb = ob + vb + cb + (int64_t)nsrc * we * 8;
         const int64_t st = std::min<int64_t>(kSpmvMaxStages, (int64_t)kSpmvStageBudget / sb);
         if (st < min_stages) return false;
         a.R = R;
@@ -99,7 +133,15 @@ inline SpmvArgs make_spmv_args(const rvk_csr& A, int64_t max_row_len)
         a.cap = (int)cap;
         a.off_bytes = (int)ob;
         a.val_bytes = (int)vb;
+        a.col_bytes = (int)cb;
         a.stage_bytes = (int)sb;
+        a.nwin = nwin;
+        a.win_elems = (int)we;
+        for (int w = 0; w < kSpmvMaxWin; ++w) {
+            a.win_lo[w]   = w < nwin ? W->lo[w] : 0;
+            a.win_hi[w]   = w < nwin ? W->hi[w] : 0;
+            a.win_base[w] = base[w];
+        }
         return true;
     };
     bool ok = false;
@@ -108,10 +150,12 @@ inline SpmvArgs make_spmv_args(const rvk_csr& A, int64_t max_row_len)
     if (!ok) { // rows longer than a stage: every tile direct, small ring
         a.R = 32;
         a.stages = 4;
+        a.nwin = 0;
         a.off_bytes = align16(34 * 8);
         a.cap = (int)(((kSpmvStageBudget / 4 - a.off_bytes) / 12) & ~size_t(3));
         a.val_bytes = a.cap * 8;
-        a.stage_bytes = a.off_bytes + a.val_bytes + align16((int64_t)a.cap * 4);
+        a.col_bytes = align16((int64_t)a.cap * 4);
+        a.stage_bytes = a.off_bytes + a.val_bytes + a.col_bytes;
     }
     a.n_tiles = (A.n_rows + a.R - 1) / a.R;
     // enough groups that every consumer thread owns a row of some tile
@@ -133,6 +177,7 @@ __device__ __forceinline__ double spmv_rows_direct(const Op& op, double acc, int
                                                    const double* __restrict__ V)
 {
     for (int lr = gtid; lr < rows; lr += gsize) {
+        const auto    own = op.fetch(op.own_col(r0 + lr));
         const int64_t kb = O[lr], ke = O[lr + 1];
         double        sum = 0.0;
         for (int64_t k = kb; k < ke; k += kSpmvUnroll) {
@@ -155,25 +200,54 @@ __device__ __forceinline__ double spmv_rows_direct(const Op& op, double acc, int
                 sum            = ok[u] ? t : sum;
             }
         }
-        acc = op.row(r0 + lr, sum, acc, op.own_fetch(r0 + lr));
+        acc = op.row(r0 + lr, sum, acc, own);
     }
     return acc;
+}
+
+// x-windows of one stage: window w holds global columns [lo[w], hi[w]) of
+// every gathered source at element base[w] of that source's area.
+struct StageWindows {
+    int           n;
+    int64_t       lo[kSpmvMaxWin], hi[kSpmvMaxWin];
+    int           base[kSpmvMaxWin];
+    const double* s0; // window area of source 0 / 1
+    const double* s1;
+};
+
+// Branch-free window lookup.  Every column of a staged tile lies in some
+// window by construction (the bands come from a scan of all nonzeros and the
+// loaded ranges are rounded outward into padded buffers), so no fallback.
+__device__ __forceinline__ int window_index(const StageWindows& W, int64_t c)
+{
+    int idx = 0;
+#pragma unroll
+    for (int w = 0; w < kSpmvMaxWin; ++w) {
+        const bool in = w < W.n && c >= W.lo[w] && c < W.hi[w];
+        idx           = in ? W.base[w] + (int)(c - W.lo[w]) : idx;
+    }
+    return idx;
 }
 
 // ---------------------------------------------------------------------------
 // Staged tiles: lane-per-row out of the shared-memory stage.
 //   O  : the tile's row offsets in shared memory (global nnz indices)
 //   V  : stage values, V[k - kv0];  Cc : stage columns, Cc[k - kv0]
-// Stage-local 32-bit indices keep the address arithmetic cheap.
+// Stage-local 32-bit indices keep the address arithmetic cheap.  WIN: the
+// gathers read the stage's x-windows (LDS) instead of global memory.
 // ---------------------------------------------------------------------------
-template <class Op>
+template <bool WIN, class Op>
 __device__ __forceinline__ double spmv_rows_staged(const Op& op, double acc, int gtid, int gsize,
                                                    int rows, int64_t r0, const int64_t* O,
                                                    int64_t kv0, const int32_t* Cc,
-                                                   const double* V)
+                                                   const double* V, const StageWindows& W)
 {
+    auto gather = [&](int64_t c) {
+        if constexpr (WIN) return op.fetch_smem(W.s0, W.s1, window_index(W, c));
+        else return op.fetch((int32_t)c);
+    };
     for (int lr = gtid; lr < rows; lr += gsize) {
-        const auto own = op.own_fetch(r0 + lr); // epilogue operands, in flight early
+        const auto own = gather(op.own_col(r0 + lr)); // epilogue operand, in flight early
         const int  kb  = (int)(O[lr] - kv0);
         const int  ke  = (int)(O[lr + 1] - kv0);
         double     sum = 0.0;
@@ -190,7 +264,7 @@ __device__ __forceinline__ double spmv_rows_staged(const Op& op, double acc, int
             }
             typename Op::Fetch f[kSpmvUnroll];
 #pragma unroll
-            for (int u = 0; u < kSpmvUnroll; ++u) f[u] = op.fetch(c[u]);
+            for (int u = 0; u < kSpmvUnroll; ++u) f[u] = gather(c[u]);
 #pragma unroll
             for (int u = 0; u < kSpmvUnroll; ++u) {
                 const double t = add(sum, mul(v[u], op.value(f[u])));
@@ -216,7 +290,8 @@ __global__ void __launch_bounds__(kSpmvThreads, 1) k_spmv_tma(SpmvArgs A, Op op_
     Op op = op_in;
     if (!op.init()) return; // device-side early exit (converged / breakdown)
 
-    const int tid = threadIdx.x;
+    const int tid  = threadIdx.x;
+    const int nsrc = A.nwin ? op.num_src() : 0;
     if (tid == 0) {
         for (int s = 0; s < A.stages; ++s) {
             mbar_init(&full[s], 1);
@@ -229,7 +304,8 @@ __global__ void __launch_bounds__(kSpmvThreads, 1) k_spmv_tma(SpmvArgs A, Op op_
     if (tid < 32) {
         // ===================== producer warp =====================
         if (tid == 0) {
-            const uint64_t pol = policy_evict_first();
+            const uint64_t pol_stream = policy_evict_first(); // CSR: read once
+            const uint64_t pol_keep   = policy_evict_last();  // x-windows: reused by 3 tiles
             int64_t        t   = blockIdx.x;
             int64_t        k0 = 0, k1 = 0; // slab bounds, prefetched one tile ahead
             if (t < A.n_tiles) {
@@ -251,21 +327,46 @@ __global__ void __launch_bounds__(kSpmvThreads, 1) k_spmv_tma(SpmvArgs A, Op op_
                 const int64_t kc0 = ck0 & ~int64_t(3), kc1 = (ck1 + 3) & ~int64_t(3);
                 const bool    last   = r1 >= A.n_rows;
                 const bool    direct = last || (kv1 - kv0) > A.cap || (kc1 - kc0) > A.cap;
-                meta[s].kv0          = kv0;
-                meta[s].kc0          = kc0;
-                meta[s].direct       = direct ? 1 : 0;
+                SpmvStageMeta& m     = meta[s];
+                m.kv0                = kv0;
+                m.kc0                = kc0;
+                m.direct             = direct ? 1 : 0;
                 if (direct) {
                     mbar_arrive(&full[s]);
-                } else {
-                    unsigned char* st = stage0 + (size_t)s * A.stage_bytes;
-                    const uint32_t ob = (uint32_t)((A.R + 2) * 8);
-                    const uint32_t vb = (uint32_t)((kv1 - kv0) * 8);
-                    const uint32_t cb = (uint32_t)((kc1 - kc0) * 4);
-                    mbar_arrive_expect_tx(&full[s], ob + vb + cb);
-                    bulk_g2s(st, A.off + r0, ob, &full[s], pol);
-                    if (vb) bulk_g2s(st + A.off_bytes, A.vals + kv0, vb, &full[s], pol);
-                    if (cb)
-                        bulk_g2s(st + A.off_bytes + A.val_bytes, A.cols + kc0, cb, &full[s], pol);
+                    continue;
+                }
+                // x-windows: columns [r0 + lo_w, r1 - 1 + hi_w] clipped to
+                // [0, n_cols) and rounded OUTWARD to 16-B boundaries -- the
+                // gathered sources are plan-owned buffers padded by >= 2
+                // doubles, so the rounded end stays inside the allocation
+                uint32_t wbytes = 0;
+                for (int w = 0; w < A.nwin; ++w) {
+                    int64_t lo = r0 + A.win_lo[w], hi = r1 + A.win_hi[w]; // exclusive hi
+                    lo = max(lo, (int64_t)0);
+                    hi = min(hi, A.n_cols);
+                    lo = lo & ~int64_t(1);
+                    hi = (hi + 1) & ~int64_t(1);
+                    if (hi < lo) hi = lo;
+                    m.wlo[w] = lo;
+                    m.whi[w] = hi;
+                    wbytes += (uint32_t)(hi - lo) * 8;
+                }
+                unsigned char* st = stage0 + (size_t)s * A.stage_bytes;
+                const uint32_t ob = (uint32_t)((A.R + 2) * 8);
+                const uint32_t vb = (uint32_t)((kv1 - kv0) * 8);
+                const uint32_t cb = (uint32_t)((kc1 - kc0) * 4);
+                mbar_arrive_expect_tx(&full[s], ob + vb + cb + wbytes * nsrc);
+                bulk_g2s(st, A.off + r0, ob, &full[s], pol_stream);
+                if (vb) bulk_g2s(st + A.off_bytes, A.vals + kv0, vb, &full[s], pol_stream);
+                if (cb) bulk_g2s(st + A.off_bytes + A.val_bytes, A.cols + kc0, cb, &full[s], pol_stream);
+                double* win0 = reinterpret_cast<double*>(st + A.off_bytes + A.val_bytes + A.col_bytes);
+                for (int k = 0; k < nsrc; ++k) {
+                    const double* src = op.src_ptr(k);
+                    double*       dst = win0 + (size_t)k * A.win_elems;
+                    for (int w = 0; w < A.nwin; ++w) {
+                        const uint32_t b = (uint32_t)(m.whi[w] - m.wlo[w]) * 8;
+                        if (b) bulk_g2s(dst + A.win_base[w], src + m.wlo[w], b, &full[s], pol_keep);
+                    }
                 }
             }
         }
@@ -285,17 +386,31 @@ __global__ void __launch_bounds__(kSpmvThreads, 1) k_spmv_tma(SpmvArgs A, Op op_
         mbar_wait(&full[s], (j / A.stages) & 1);
         const int64_t r0   = t * A.R;
         const int     rows = (int)min((int64_t)A.R, A.n_rows - r0);
-        if (meta[s].direct) {
+        const SpmvStageMeta& m = meta[s];
+        if (m.direct) {
             acc = spmv_rows_direct(op, acc, gtid, gs, rows, r0, A.off + r0, A.cols, A.vals);
         } else {
             unsigned char* st  = stage0 + (size_t)s * A.stage_bytes;
-            const int64_t  kv0 = meta[s].kv0;
+            const int64_t  kv0 = m.kv0;
             // columns were copied from kc0 <= kv0: shift so both use kv0-local indices
             const int32_t* Cc = reinterpret_cast<const int32_t*>(st + A.off_bytes + A.val_bytes) +
-                                (kv0 - meta[s].kc0);
-            acc = spmv_rows_staged(op, acc, gtid, gs, rows, r0,
-                                   reinterpret_cast<const int64_t*>(st), kv0, Cc,
-                                   reinterpret_cast<const double*>(st + A.off_bytes));
+                                (kv0 - m.kc0);
+            StageWindows W;
+            W.n = nsrc ? A.nwin : 0;
+            const double* win0 =
+                reinterpret_cast<const double*>(st + A.off_bytes + A.val_bytes + A.col_bytes);
+            W.s0 = win0;
+            W.s1 = win0 + A.win_elems;
+#pragma unroll
+            for (int w = 0; w < kSpmvMaxWin; ++w) {
+                W.lo[w]   = m.wlo[w];
+                W.hi[w]   = m.whi[w];
+                W.base[w] = A.win_base[w];
+            }
+            const int64_t* O = reinterpret_cast<const int64_t*>(st);
+            const double*  V = reinterpret_cast<const double*>(st + A.off_bytes);
+            if (W.n) acc = spmv_rows_staged<true>(op, acc, gtid, gs, rows, r0, O, kv0, Cc, V, W);
+            else acc = spmv_rows_staged<false>(op, acc, gtid, gs, rows, r0, O, kv0, Cc, V, W);
         }
         __syncwarp();
         if ((ctid & 31) == 0) mbar_arrive(&empty[s]);
@@ -322,12 +437,17 @@ struct SpmvPlainOp {
     struct Fetch {
         double x;
     };
-    __device__ __forceinline__ bool   init() { return true; }
-    __device__ __forceinline__ Fetch  fetch(int32_t j) const { return Fetch{__ldg(x + j)}; }
-    __device__ __forceinline__ double value(const Fetch& f) const { return f.x; }
-    struct Own {};
-    __device__ __forceinline__ Own    own_fetch(int64_t) const { return Own{}; }
-    __device__ __forceinline__ double row(int64_t i, double sum, double acc, Own) const
+    __device__ __forceinline__ bool          init() { return true; }
+    __device__ __forceinline__ int           num_src() const { return 1; }
+    __device__ __forceinline__ const double* src_ptr(int) const { return x; }
+    __device__ __forceinline__ Fetch         fetch(int32_t j) const { return Fetch{__ldg(x + j)}; }
+    __device__ __forceinline__ Fetch fetch_smem(const double* s0, const double*, int i) const
+    {
+        return Fetch{s0[i]};
+    }
+    __device__ __forceinline__ double  value(const Fetch& f) const { return f.x; }
+    __device__ __forceinline__ int64_t own_col(int64_t) const { return 0; } // unused by row()
+    __device__ __forceinline__ double  row(int64_t i, double sum, double acc, const Fetch&) const
     {
         y[i] = sum;
         return acc;
@@ -349,5 +469,11 @@ rvk_status launch_spmv(cudaStream_t stream, const SpmvArgs& a, const Op& op, Tai
     RVK_CHECK_LAUNCH("k_spmv_tma");
     return RVK_OK;
 }
+
+// Stencil structure of a CSR (plan time, one host sync): the distinct
+// diagonals (col - row), clustered into at most kSpmvMaxWin bands.  n = 0
+// when the matrix is not stencil-like (more than 64 diagonals, or bands that
+// would not fit).  Implemented in rvk_cg.cu.
+rvk_status csr_windows(cudaStream_t s, const rvk_csr& A, SpmvWindows* out);
 
 } // namespace rvk

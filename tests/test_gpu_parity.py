@@ -373,3 +373,31 @@ def test_fused_equals_unfused_elementwise_state(ctx):
         x, res = plan.solve_host(b)
         xs.append((x, res.hist))
     assert np.max(np.abs(xs[0][1] - xs[1][1]) / xs[1][1]) < 1e-12
+
+
+def test_xwindow_spmv_path_parity():
+    """The opt-in x-window SpMV path (RVK_WINDOWS=1: the gathered vectors'
+    diagonal bands staged by TMA) stays parity-green; run in a subprocess
+    because the switch is read at plan creation."""
+    import subprocess
+    import sys
+    code = r'''
+import sys, numpy as np
+sys.path.insert(0, ".")
+import oracle as O
+from paper_2306_17801_b200 import rvk
+ctx = rvk.Ctx()
+for dim, pts, g in [(2, 5, (1024, 64)), (2, 9, (300, 200)), (2, 5, (200, 200))]:
+    Ah = O.build_laplacian(dim, pts, g); b = O.rhs(Ah.n_rows)
+    ref = O.cg_solve(Ah, b, max_it=20)
+    A = rvk.DeviceCsr.laplacian(ctx, dim, pts, g)
+    for mode in ("fused", "unfused"):
+        x, res = rvk.CgPlan(ctx, A, max_it=20, mode=mode).solve_host(b)
+        assert np.max(np.abs(res.hist - ref.hist) / ref.hist) < 1e-10, (g, mode)
+        assert np.linalg.norm(x - ref.x) / np.linalg.norm(ref.x) < 1e-10, (g, mode)
+print("ok")
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    p = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True,
+                       env=dict(os.environ, RVK_WINDOWS="1"), timeout=600)
+    assert p.returncode == 0 and "ok" in p.stdout, p.stdout + p.stderr
