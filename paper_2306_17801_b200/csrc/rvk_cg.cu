@@ -470,21 +470,29 @@ rvk_status csr_windows(cudaStream_t s, const rvk_csr& A, SpmvWindows* out)
     for (int i = 0; i < kDiagTable; ++i)
         if (h[i] != kDiagEmpty) d.push_back((int64_t)(long long)(h[i] ^ (1ull << 63)));
     std::sort(d.begin(), d.end());
-    // bands: diagonals closer than kGap share a window (at most kGap wasted
-    // doubles per gap); give up beyond kSpmvMaxWin bands or wide bands
+    // bands: diagonals closer than kGap share a band (at most kGap wasted
+    // doubles per gap)
     constexpr int64_t kGap = 64, kMaxBand = 4096;
-    SpmvWindows W;
+    std::vector<std::pair<int64_t, int64_t>> bands;
     for (int64_t v : d) {
-        if (W.n > 0 && v - W.hi[W.n - 1] <= kGap) {
-            W.hi[W.n - 1] = v;
-        } else {
-            if (W.n == kSpmvMaxWin) return RVK_OK;
-            W.lo[W.n] = W.hi[W.n] = v;
-            ++W.n;
+        if (!bands.empty() && v - bands.back().second <= kGap) bands.back().second = v;
+        else bands.emplace_back(v, v);
+    }
+    SpmvWindows W;
+    if (!bands.empty() && bands.back().second - bands.back().first <= kMaxBand) {
+        W.has_lead = true;
+        W.lead_lo  = bands.back().first;
+        W.lead_hi  = bands.back().second;
+    }
+    bool fits = (int)bands.size() <= kSpmvMaxWin;
+    for (auto& b : bands) fits = fits && b.second - b.first <= kMaxBand;
+    if (fits) {
+        W.n = (int)bands.size();
+        for (int w = 0; w < W.n; ++w) {
+            W.lo[w] = bands[w].first;
+            W.hi[w] = bands[w].second;
         }
     }
-    for (int w = 0; w < W.n; ++w)
-        if (W.hi[w] - W.lo[w] > kMaxBand) return RVK_OK;
     *out = W;
     return RVK_OK;
 }
@@ -873,8 +881,9 @@ rvk_status rvk_cg_plan_create(rvk_ctx ctx, const rvk_csr* A, rvk_cg_config cfg, 
     // gathers on the 2D stencils (9-pt 4096^2 K1 806 vs 467 us, window
     // lookup made the consumers issue-bound); the 3D stencils have > 4 bands.
     SpmvWindows win;
-    if (!std::getenv("RVK_WINDOWS") || csr_windows(ctx->stream, *A, &win) != RVK_OK)
-        win = SpmvWindows{};
+    if (csr_windows(ctx->stream, *A, &win) != RVK_OK) win = SpmvWindows{};
+    if (!std::getenv("RVK_WINDOWS")) win.n = 0;
+    if (std::getenv("RVK_NO_PREFETCH")) win.has_lead = false;
     P->sa        = make_spmv_args(*A, maxlen, &win, 2);
     if (std::getenv("RVK_DEBUG")) {
         std::fprintf(stderr, "[rvk] plan n=%lld nnz=%lld R=%d stages=%d groups=%d cap=%d nwin=%d",

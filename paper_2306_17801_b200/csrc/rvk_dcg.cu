@@ -570,9 +570,10 @@ rvk_status rvk_dcg_plan_create(rvk_ctx ctx, const rvk_csr* A, rvk_shard sh, rvk_
     P->A           = *A;
     P->sh          = sh;
     P->cfg         = cfg;
-    SpmvWindows win; // opt-in, see rvk_cg.cu
-    if (!std::getenv("RVK_WINDOWS") || csr_windows(ctx->stream, *A, &win) != RVK_OK)
-        win = SpmvWindows{};
+    SpmvWindows win; // x-windows opt-in, leading-edge prefetch default (see rvk_cg.cu)
+    if (csr_windows(ctx->stream, *A, &win) != RVK_OK) win = SpmvWindows{};
+    if (!std::getenv("RVK_WINDOWS")) win.n = 0;
+    if (std::getenv("RVK_NO_PREFETCH")) win.has_lead = false;
     P->sa          = make_spmv_args(*A, maxlen, &win, 2);
     P->upd_grid    = resident_grid(k_dcg_update<true>, kUpdThreads, sh.n_own);
     P->owns_gather = shared_gather == nullptr;

@@ -69,6 +69,10 @@ struct SpmvWindows {
     int     n = 0;
     int64_t lo[kSpmvMaxWin] = {0, 0, 0, 0};
     int64_t hi[kSpmvMaxWin] = {0, 0, 0, 0};
+    // highest diagonal band [lead_lo, lead_hi] (any band count): the columns a
+    // tile touches FIRST in a row-ordered sweep -- prefetched into L2 one tile ahead
+    bool    has_lead = false;
+    int64_t lead_lo = 0, lead_hi = 0;
 };
 
 struct SpmvArgs {
@@ -85,6 +89,8 @@ struct SpmvArgs {
     int64_t        win_hi[kSpmvMaxWin];
     int            win_base[kSpmvMaxWin]; // element offset of window w inside one source's area
     int            win_elems;             // doubles per source per stage
+    int            pf;                    // 1: L2-prefetch the next tile's leading-edge columns
+    int64_t        pf_lo, pf_hi;          // ... the band [pf_lo, pf_hi] of (col - row)
     const int64_t* off;
     const int32_t* cols;
     const double*  vals;
@@ -158,6 +164,9 @@ inline SpmvArgs make_spmv_args(const rvk_csr& A, int64_t max_row_len,
         a.stage_bytes = a.off_bytes + a.val_bytes + a.col_bytes;
     }
     a.n_tiles = (A.n_rows + a.R - 1) / a.R;
+    a.pf      = (W && W->has_lead && W->lead_lo > 0) ? 1 : 0;
+    a.pf_lo   = a.pf ? W->lead_lo : 0;
+    a.pf_hi   = a.pf ? W->lead_hi : 0;
     // enough groups that every consumer thread owns a row of some tile
     a.groups = 1;
     while (a.groups * 2 <= a.stages && a.stages % (a.groups * 2) == 0 &&
@@ -359,6 +368,19 @@ __global__ void __launch_bounds__(kSpmvThreads, 1) k_spmv_tma(SpmvArgs A, Op op_
                 bulk_g2s(st, A.off + r0, ob, &full[s], pol_stream);
                 if (vb) bulk_g2s(st + A.off_bytes, A.vals + kv0, vb, &full[s], pol_stream);
                 if (cb) bulk_g2s(st + A.off_bytes + A.val_bytes, A.cols + kc0, cb, &full[s], pol_stream);
+                // leading edge of this CTA's NEXT tile: its highest-diagonal
+                // columns are first-touch DRAM misses for the gathers; start
+                // them now (L2 prefetch, no smem, no barrier)
+                if (A.pf && tn < A.n_tiles) {
+                    const int64_t q0 = tn * A.R, q1 = min(q0 + A.R, A.n_rows);
+                    int64_t       lo = max(q0 + A.pf_lo, (int64_t)0) & ~int64_t(1);
+                    int64_t       hi = min(q1 + A.pf_hi, A.n_cols) & ~int64_t(1);
+                    if (hi > lo) {
+                        const int nps = op.num_src();
+                        for (int k = 0; k < nps; ++k)
+                            bulk_prefetch_l2(op.src_ptr(k) + lo, (uint32_t)(hi - lo) * 8);
+                    }
+                }
                 double* win0 = reinterpret_cast<double*>(st + A.off_bytes + A.val_bytes + A.col_bytes);
                 for (int k = 0; k < nsrc; ++k) {
                     const double* src = op.src_ptr(k);
