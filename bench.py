@@ -60,6 +60,13 @@ def peaks():
 def bytes_model(n: int, nnz: int, mode: str = "fused"):
     """Algorithmic HBM bytes.  All FP64 + int64 offsets + int32 cols.
     k1 = the SpMV launch (fused: + on-the-fly AYPX), k2 = the rest of an iteration."""
+    if mode == "stencil":                        # matrix-free: no CSR, constant dinv
+        k1 = 32 * n                              # z, p_old -> p_new, w
+        k2 = 56 * n                              # x, p, r, w -> x, r, z
+        b_min = k1 + k2
+        return {"k1": k1, "k2": k2, "b_min_iter": b_min, "b_ref_iter": b_min,
+                "b_min_solve": MAX_IT * b_min + 32 * n, "b_ref_solve": MAX_IT * b_min + 32 * n,
+                "flops_iter": 2 * nnz + 13 * n}
     if mode == "fused":
         k1 = 12 * nnz + 8 * (n + 1) + 32 * n    # off, cols, vals, z, p_old -> p_new, w
         k2 = 64 * n                              # x, p, r, w, dinv -> x, r, z
@@ -212,13 +219,22 @@ def run_gpu(args, cfg):
     dim, pts, grid, desc = cfg
     stream = torch.cuda.Stream()
     ctx = rvk.Ctx(stream.cuda_stream)
-    A = rvk.DeviceCsr.laplacian(ctx, dim, pts, grid)
-    n, nnz = A.n_rows, A.nnz
+    if args.operator == "stencil":
+        import ctypes
+        nn, nz_ = ctypes.c_int64(), ctypes.c_int64()
+        gx, gy, gz = (list(grid) + [1, 1])[:3]
+        rvk.check(rvk.lib().rvk_laplacian_size(dim, pts, gx, gy, gz, ctypes.byref(nn), ctypes.byref(nz_)))
+        n, nnz = nn.value, nz_.value
+        A = (dim, pts, grid)
+    else:
+        A = rvk.DeviceCsr.laplacian(ctx, dim, pts, grid)
+        n, nnz = A.n_rows, A.nnz
     b = rvk.DeviceArray(n)
     x = rvk.DeviceArray(n)
     rvk.check(rvk.lib().rvk_fill_rhs(ctx.h, 0x9E3779B97F4A7C15, n, b.ptr))
     plan = rvk.CgPlan(ctx, A, max_it=MAX_IT, mode=args.mode, use_graph=not args.no_graph)
-    bm = bytes_model(n, nnz, "unfused" if args.mode == "unfused" else "fused")
+    bm = bytes_model(n, nnz, "stencil" if args.operator == "stencil" else
+                     ("unfused" if args.mode == "unfused" else "fused"))
     hbm_peak, peak_src = peaks()
     ws_bytes = 20 * nnz + 8 * (n + 1) + 9 * 8 * n
     log(f"{desc}: n={n} nnz={nnz} working set {ws_bytes/1e9:.2f} GB (L2 {L2_BYTES/1e6:.0f} MB)")
@@ -284,7 +300,7 @@ def run_gpu(args, cfg):
         k1_gbs = bm["k1"] / (ms * 1e-3) / 1e9
         k2_gbs = 0.0
     solve_gbs = bm["b_min_solve"] / (ms * 1e-3) / 1e9
-    traffic = ncu_traffic(args.config) if mode == "fused" else None
+    traffic = ncu_traffic(args.config) if (mode == "fused" and args.operator == "csr") else None
 
     # ---- e2e through the C-ABI with host buffers (pinned) ----------------------
     bh = torch.empty(n, dtype=torch.float64, pin_memory=True)
@@ -315,12 +331,15 @@ def run_gpu(args, cfg):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{desc}, Jacobi-CG {MAX_IT} iterations, x0=0, splitmix64 RHS",
                    "n": n, "nnz": nnz, "mode": mode, "graph": not args.no_graph,
+                   "operator": args.operator,
                    "l2": (f"no flush: working set {ws_bytes/1e9:.2f} GB >> 126 MB L2 "
                           "(every operand streams from HBM each step)") if flush is None else
                          (f"L2 flushed between steps (512 MiB write); working set "
                           f"{ws_bytes/1e6:.1f} MB")},
         "roofline": {"bound": "hbm",
-                     "kernel": {"fused": "k_spmv_tma<CgSpmvOp> (SpMV + on-the-fly AYPX + p.w)",
+                     "kernel": {"fused": ("k_mf_cg (matrix-free stencil + on-the-fly AYPX + p.w)"
+                                          if args.operator == "stencil" else
+                                          "k_spmv_tma<CgSpmvOp> (SpMV + on-the-fly AYPX + p.w)"),
                                 "unfused": "k_spmv_tma<SpmvGuardedOp> (SpMV)",
                                 "persistent": "k_cg_persistent (whole solve, one launch)",
                                 "hostsync": "whole solve (host-sync baseline)"}[mode],
@@ -357,6 +376,8 @@ def main():
     ap.add_argument("--mode", choices=["fused", "unfused", "persistent", "auto", "hostsync"],
                     default="auto", help="auto: one persistent kernel for L2-sized grids, "
                                          "else the fused 2-kernel/iteration graph")
+    ap.add_argument("--operator", choices=["csr", "stencil"], default="csr",
+                    help="csr: the AIJ/CSR operator (headline); stencil: matrix-free (SURVEY 8f)")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

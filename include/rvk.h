@@ -191,6 +191,13 @@ typedef struct rvk_cg_plan_s* rvk_cg_plan;
  * the SpMV tiles, allocates the work vectors r, z, p0, p1, w. */
 rvk_status rvk_cg_plan_create(rvk_ctx ctx, const rvk_csr* A_dev, rvk_cg_config cfg,
                               rvk_cg_plan* out);
+/* Matrix-free variant (PETSc MatShell analogue): the
+ * same constant-coefficient stencil rvk_build_laplacian assembles, applied
+ * on the fly -- no CSR bytes, constant Jacobi diagonal.  Element arithmetic
+ * and neighbour order are those of the assembled CSR (bit-identical w).
+ * FUSED / AUTO mode only. */
+rvk_status rvk_cg_plan_create_stencil(rvk_ctx ctx, int dim, int points, int64_t nx, int64_t ny,
+                                      int64_t nz, rvk_cg_config cfg, rvk_cg_plan* out);
 rvk_status rvk_cg_plan_destroy(rvk_cg_plan plan);
 /* Enqueue one full solve (x0 = 0, r0 = b; max_it iterations or device-side
  * convergence/breakdown exit).  ZERO host synchronisations. */

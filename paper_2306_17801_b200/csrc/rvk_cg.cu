@@ -52,12 +52,12 @@ constexpr int64_t kPersistentMaxBytes = 0;
 // ---------------------------------------------------------------------------
 // K0: setup.  r = b; x = 0; z = B r; partials z.z, z.r.
 // ---------------------------------------------------------------------------
-template <bool VEC, bool JACOBI>
+template <bool VEC, int PC> // PC: 0 none, 1 dinv vector, 2 constant dinv (matrix-free stencil)
 __global__ void __launch_bounds__(kUpdThreads)
     k_cg_setup(int64_t n, const double* __restrict__ b, const double* __restrict__ dinv,
                double* __restrict__ x, double* __restrict__ r, double* __restrict__ z,
                CgState* st, double* hist, double rtol, double atol, double* partials,
-               unsigned int* ticket)
+               unsigned int* ticket, double dconst)
 {
     __shared__ double smem[64];
     __shared__ int    flag;
@@ -69,8 +69,9 @@ __global__ void __launch_bounds__(kUpdThreads)
         for (int64_t i = t0; i < n2; i += stride) {
             const double2 bi = ld_stream(reinterpret_cast<const double2*>(b) + i);
             double2       zi = bi;
-            if (JACOBI) {
-                const double2 d = ld_stream(reinterpret_cast<const double2*>(dinv) + i);
+            if (PC != 0) {
+                const double2 d = PC == 1 ? ld_stream(reinterpret_cast<const double2*>(dinv) + i)
+                                          : make_double2(dconst, dconst);
                 zi.x = mul(d.x, bi.x);
                 zi.y = mul(d.y, bi.y);
             }
@@ -85,7 +86,7 @@ __global__ void __launch_bounds__(kUpdThreads)
     }
     for (int64_t i = (VEC ? (n & ~int64_t(1)) : 0) + t0; i < n; i += stride) {
         const double bi = b[i];
-        const double zi = JACOBI ? mul(dinv[i], bi) : bi;
+        const double zi = PC == 0 ? bi : mul(PC == 1 ? dinv[i] : dconst, bi);
         r[i] = bi;
         z[i] = zi;
         x[i] = 0.0;
@@ -118,88 +119,16 @@ __global__ void __launch_bounds__(kUpdThreads)
     }
 }
 
-// ---------------------------------------------------------------------------
-// K1 op: p_new = z + b p_old on the fly; w = A p_new; tail alpha.
-// ---------------------------------------------------------------------------
-template <bool FIRST>
-struct CgSpmvOp {
-    static constexpr bool kHasTail = true;
-    const double* __restrict__ z;
-    const double* __restrict__ p_old;
-    double* __restrict__ p_new;
-    double* __restrict__ w;
-    CgState* st;
-    int64_t  n;
-    int      it;
-    double   b; // set by init()
-
-    __device__ __forceinline__ bool init()
-    {
-        if (st->done) return false;
-        if (!FIRST) {
-            const double bo = st->betaold;
-            if (bo == 0.0) { // breakdown in beta/betaold
-                if (blockIdx.x == 0 && threadIdx.x == 0) {
-                    st->state          = RVK_CG_BREAKDOWN;
-                    st->breakdown_iter = it;
-                    st->done           = 1;
-                }
-                return false;
-            }
-            b = st->beta / bo;
-        }
-        return true;
-    }
-    struct Fetch {
-        double z, p;
-    };
-    __device__ __forceinline__ int           num_src() const { return FIRST ? 1 : 2; }
-    __device__ __forceinline__ const double* src_ptr(int k) const { return k == 0 ? z : p_old; }
-    __device__ __forceinline__ Fetch         fetch(int32_t j) const
-    {
-        return Fetch{__ldg(z + j), FIRST ? 0.0 : __ldg(p_old + j)};
-    }
-    __device__ __forceinline__ Fetch fetch_smem(const double* s0, const double* s1, int i) const
-    {
-        return Fetch{s0[i], FIRST ? 0.0 : s1[i]};
-    }
-    __device__ __forceinline__ double value(const Fetch& f) const
-    {
-        return FIRST ? f.z : aypx1(b, f.z, f.p); // z + b*p  (kernels_scalar.cpp:33)
-    }
-    __device__ __forceinline__ int64_t own_col(int64_t i) const { return i; }
-    // p_new[i] = z[i] + b p_old[i] from the row's own (gathered) operands
-    __device__ __forceinline__ double row(int64_t i, double sum, double acc, const Fetch& o) const
-    {
-        const double p = value(o);
-        p_new[i]       = p;
-        w[i]           = sum;
-        return add(acc, mul(p, sum));
-    }
-    __device__ __forceinline__ void tail(double pAp) const
-    {
-        const double a = st->beta / pAp;
-        st->pAp        = pAp;
-        if (pAp == 0.0 || !isfinite(a)) {
-            st->state          = RVK_CG_BREAKDOWN;
-            st->breakdown_iter = it;
-            st->done           = 1;
-        } else {
-            st->alpha   = a;
-            st->betaold = st->beta;
-        }
-    }
-};
 
 // ---------------------------------------------------------------------------
 // K2: x += a p; r += (-a) w; z = B r; partials z.z, z.r; tail dp/hist/beta.
 // ---------------------------------------------------------------------------
-template <bool VEC, bool JACOBI>
+template <bool VEC, int PC> // PC: 0 none, 1 dinv vector, 2 constant dinv (matrix-free stencil)
 __global__ void __launch_bounds__(kUpdThreads)
     k_cg_update(int64_t n, const double* __restrict__ p, const double* __restrict__ w,
                 const double* __restrict__ dinv, double* __restrict__ x, double* __restrict__ r,
                 double* __restrict__ z, CgState* st, double* hist, int it, double rtol,
-                double atol, double* partials, unsigned int* ticket)
+                double atol, double* partials, unsigned int* ticket, double dconst)
 {
     if (st->done) return;
     __shared__ double smem[64];
@@ -225,7 +154,7 @@ __global__ void __launch_bounds__(kUpdThreads)
             ri.x = axpy1(na, wi.x, ri.x);
             ri.y = axpy1(na, wi.y, ri.y);
             double2 zi = ri;
-            if (JACOBI) {
+            if (PC != 0) {
                 zi.x = mul(d.x, ri.x);
                 zi.y = mul(d.y, ri.y);
             }
@@ -244,8 +173,8 @@ __global__ void __launch_bounds__(kUpdThreads)
             const double2 wa = ld_stream(w2 + i), wb = ld_stream(w2 + j);
             const double2 xa = ld_stream(x2 + i), xb = ld_stream(x2 + j);
             const double2 ra = ld_stream(r2 + i), rb = ld_stream(r2 + j);
-            double2 da = make_double2(0, 0), db = make_double2(0, 0);
-            if (JACOBI) {
+            double2 da = make_double2(dconst, dconst), db = da;
+            if (PC == 1) {
                 da = ld_stream(d2 + i);
                 db = ld_stream(d2 + j);
             }
@@ -253,15 +182,15 @@ __global__ void __launch_bounds__(kUpdThreads)
             step(pb, wb, xb, rb, db, j);
         }
         if (i < n2) {
-            double2 d = make_double2(0, 0);
-            if (JACOBI) d = ld_stream(d2 + i);
+            double2 d = make_double2(dconst, dconst);
+            if (PC == 1) d = ld_stream(d2 + i);
             step(ld_stream(p2 + i), ld_stream(w2 + i), ld_stream(x2 + i), ld_stream(r2 + i), d, i);
         }
     }
     for (int64_t i = (VEC ? (n & ~int64_t(1)) : 0) + t0; i < n; i += stride) {
         x[i]            = axpy1(a, p[i], x[i]);
         const double ri = axpy1(na, w[i], r[i]);
-        const double zi = JACOBI ? mul(dinv[i], ri) : ri;
+        const double zi = PC == 0 ? ri : mul(PC == 1 ? dinv[i] : dconst, ri);
         r[i]            = ri;
         z[i]            = zi;
         acc[0]          = add(acc[0], mul(zi, zi));
@@ -517,6 +446,10 @@ struct rvk_cg_plan_s {
     SpmvArgs      sa{};
     int           spmv_grid = 0, upd_grid = 0, setup_grid = 0, persist_grid = 0;
     int           mode = RVK_CG_MODE_FUSED; // resolved (AUTO -> FUSED | PERSISTENT)
+    bool          stencil = false;          // matrix-free operator (rvk_cg_plan_create_stencil)
+    StencilGeom   geom{};
+    double        dconst = 0.0;             // constant dinv of the stencil
+    int           mf_grid = 0;
     double*       dinv = nullptr;
     double*       r = nullptr;
     double*       z = nullptr;
@@ -542,58 +475,77 @@ struct rvk_cg_plan_s {
 
 namespace {
 
+// Launch K0 / K2 for the preconditioner mode: 0 none, 1 dinv vector (CSR),
+// 2 constant dinv (matrix-free stencil: the diagonal is the centre weight).
+template <bool V>
+rvk_status launch_setup(rvk_cg_plan P, int pcm, const double* b, double* x)
+{
+    cudaStream_t s = P->ctx->stream;
+    auto go = [&](auto kern) {
+        kern<<<P->setup_grid, kUpdThreads, 0, s>>>(P->A.n_rows, b, P->dinv, x, P->r, P->z, P->st,
+                                                   P->hist, P->cfg.rtol, P->cfg.atol, P->partials,
+                                                   P->tickets, P->dconst);
+    };
+    if (pcm == 0) go(k_cg_setup<V, 0>);
+    else if (pcm == 1) go(k_cg_setup<V, 1>);
+    else go(k_cg_setup<V, 2>);
+    RVK_CHECK_LAUNCH("k_cg_setup");
+    return RVK_OK;
+}
+
+template <bool V>
+rvk_status launch_update(rvk_cg_plan P, int pcm, const double* p_new, double* x, int it)
+{
+    cudaStream_t s = P->ctx->stream;
+    auto go = [&](auto kern) {
+        kern<<<P->upd_grid, kUpdThreads, 0, s>>>(P->A.n_rows, p_new, P->w, P->dinv, x, P->r, P->z,
+                                                 P->st, P->hist, it, P->cfg.rtol, P->cfg.atol,
+                                                 P->partials, P->tickets, P->dconst);
+    };
+    if (pcm == 0) go(k_cg_update<V, 0>);
+    else if (pcm == 1) go(k_cg_update<V, 1>);
+    else go(k_cg_update<V, 2>);
+    RVK_CHECK_LAUNCH("k_cg_update");
+    return RVK_OK;
+}
+
 rvk_status enqueue_fused(rvk_cg_plan P, const double* b, double* x)
 {
-    const int64_t n     = P->A.n_rows;
-    cudaStream_t  s     = P->ctx->stream;
-    const bool    jac   = P->cfg.pc == RVK_PC_JACOBI;
-    const bool    vec   = aligned16(b) && aligned16(x) && aligned16(P->dinv);
-    const int     ug    = P->upd_grid;
-    const double  rtol  = P->cfg.rtol, atol = P->cfg.atol;
-    unsigned int* tk0   = P->tickets;
-    unsigned int* tk1   = P->tickets + 1;
-    double*       part0 = P->partials;
-    double*       part1 = P->partials + 2 * kMaxReduceBlocks;
-    P->launches         = 0;
-
-#define RVK_SETUP(V, J)                                                                        \
-    k_cg_setup<V, J><<<P->setup_grid, kUpdThreads, 0, s>>>(n, b, P->dinv, x, P->r, P->z, P->st, P->hist,  \
-                                                rtol, atol, part0, tk0)
-    if (vec) { if (jac) RVK_SETUP(true, true); else RVK_SETUP(true, false); }
-    else { if (jac) RVK_SETUP(false, true); else RVK_SETUP(false, false); }
-#undef RVK_SETUP
-    RVK_CHECK_LAUNCH("k_cg_setup");
+    const int64_t n    = P->A.n_rows;
+    cudaStream_t  s    = P->ctx->stream;
+    const int     pcm  = P->cfg.pc != RVK_PC_JACOBI ? 0 : (P->stencil ? 2 : 1);
+    const bool    vec  = aligned16(b) && aligned16(x) && aligned16(P->dinv);
+    const TailArgs ta{P->partials + 2 * kMaxReduceBlocks, P->tickets + 1};
+    P->launches = 0;
+    auto rec = [&](int k) -> rvk_status {
+        if (P->profiling)
+            RVK_CUDA(cudaEventRecordWithFlags(P->ev[k], s, cudaEventRecordExternal));
+        return RVK_OK;
+    };
+    rvk_status rc = vec ? launch_setup<true>(P, pcm, b, x) : launch_setup<false>(P, pcm, b, x);
+    if (rc != RVK_OK) return rc;
     ++P->launches;
-
-    const SpmvArgs& sa = P->sa;
-    const TailArgs ta{part1, tk1};
     for (int it = 0; it < P->cfg.max_it; ++it) {
         const double* p_old = P->p[it & 1];
         double*       p_new = P->p[(it + 1) & 1];
-        if (P->profiling) RVK_CUDA(cudaEventRecordWithFlags(P->ev[4 * it + 0], s, cudaEventRecordExternal));
-        rvk_status rc;
-        if (it == 0) {
+        if ((rc = rec(4 * it + 0)) != RVK_OK) return rc;
+        if (P->stencil) {
+            rc = launch_mf_k1(s, P->geom, it == 0, P->z, p_old, p_new, P->w, P->st, n, it, ta.partials,
+                              ta.ticket, P->mf_grid);
+        } else if (it == 0) {
             CgSpmvOp<true> op{P->z, p_old, p_new, P->w, P->st, n, it, 0.0};
-            rc = launch_spmv(s, sa, op, ta, P->spmv_grid);
+            rc = launch_spmv(s, P->sa, op, ta, P->spmv_grid);
         } else {
             CgSpmvOp<false> op{P->z, p_old, p_new, P->w, P->st, n, it, 0.0};
-            rc = launch_spmv(s, sa, op, ta, P->spmv_grid);
+            rc = launch_spmv(s, P->sa, op, ta, P->spmv_grid);
         }
         if (rc != RVK_OK) return rc;
         ++P->launches;
-        if (P->profiling) {
-            RVK_CUDA(cudaEventRecordWithFlags(P->ev[4 * it + 1], s, cudaEventRecordExternal));
-            RVK_CUDA(cudaEventRecordWithFlags(P->ev[4 * it + 2], s, cudaEventRecordExternal));
-        }
-#define RVK_UPD(V, J)                                                                          \
-    k_cg_update<V, J><<<ug, kUpdThreads, 0, s>>>(n, p_new, P->w, P->dinv, x, P->r, P->z, P->st, \
-                                                 P->hist, it, rtol, atol, part0, tk0)
-        if (vec) { if (jac) RVK_UPD(true, true); else RVK_UPD(true, false); }
-        else { if (jac) RVK_UPD(false, true); else RVK_UPD(false, false); }
-#undef RVK_UPD
-        RVK_CHECK_LAUNCH("k_cg_update");
+        if ((rc = rec(4 * it + 1)) != RVK_OK || (rc = rec(4 * it + 2)) != RVK_OK) return rc;
+        rc = vec ? launch_update<true>(P, pcm, p_new, x, it) : launch_update<false>(P, pcm, p_new, x, it);
+        if (rc != RVK_OK) return rc;
         ++P->launches;
-        if (P->profiling) RVK_CUDA(cudaEventRecordWithFlags(P->ev[4 * it + 3], s, cudaEventRecordExternal));
+        if ((rc = rec(4 * it + 3)) != RVK_OK) return rc;
     }
     return RVK_OK;
 }
@@ -896,8 +848,8 @@ rvk_status rvk_cg_plan_create(rvk_ctx ctx, const rvk_csr* A, rvk_cg_config cfg, 
     }
     P->spmv_grid = sm_count();
     // one resident wave each (the vectorised loops take 2 elements per thread)
-    P->upd_grid   = resident_grid(k_cg_update<true, true>, kUpdThreads, (A->n_rows + 1) / 2);
-    P->setup_grid = resident_grid(k_cg_setup<true, true>, kUpdThreads, (A->n_rows + 1) / 2);
+    P->upd_grid   = resident_grid(k_cg_update<true, 1>, kUpdThreads, (A->n_rows + 1) / 2);
+    P->setup_grid = resident_grid(k_cg_setup<true, 1>, kUpdThreads, (A->n_rows + 1) / 2);
     P->persist_grid = persistent_grid(A->n_rows);
     P->mode         = cfg.mode;
     if (cfg.mode == RVK_CG_MODE_AUTO) {
@@ -943,6 +895,62 @@ rvk_status rvk_cg_plan_create(rvk_ctx ctx, const rvk_csr* A, rvk_cg_config cfg, 
     if (rc != RVK_OK) {
         rvk_cg_plan_destroy(P);
         return rc;
+    }
+    *out = P;
+    return RVK_OK;
+}
+
+rvk_status rvk_cg_plan_create_stencil(rvk_ctx ctx, int dim, int points, int64_t nx, int64_t ny,
+                                      int64_t nz, rvk_cg_config cfg, rvk_cg_plan* out)
+{
+    if (!ctx || !out) return set_error(RVK_ERR_INVALID, "cg_plan_create_stencil: null argument");
+    *out = nullptr;
+    if (dim == 2) nz = 1;
+    int64_t n = 0, nnz = 0;
+    RVK_TRY(rvk_laplacian_size(dim, points, nx, ny, nz, &n, &nnz));
+    if (cfg.max_it < 1) return set_error(RVK_ERR_INVALID, "cg_solve: max_it must be >= 1");
+    if (cfg.pc != RVK_PC_NONE && cfg.pc != RVK_PC_JACOBI)
+        return set_error(RVK_ERR_INVALID, "cg_solve: unknown preconditioner %d", cfg.pc);
+    if (cfg.mode != RVK_CG_MODE_FUSED && cfg.mode != RVK_CG_MODE_AUTO)
+        return set_error(RVK_ERR_UNSUPPORTED, "matrix-free stencil plans run the FUSED mode only");
+    auto P        = new rvk_cg_plan_s();
+    P->ctx        = ctx;
+    P->A          = rvk_csr{n, n, nnz, nullptr, nullptr, nullptr};
+    P->cfg        = cfg;
+    P->mode       = RVK_CG_MODE_FUSED;
+    P->stencil    = true;
+    P->geom       = StencilGeom{nx, ny, nz, n, dim, (points == 9 || points == 27) ? 1 : 0,
+                          (double)(points - 1)};
+    P->dconst     = 1.0 / (double)(points - 1); // == 1/diag, as the CSR path's dinv
+    P->mf_grid    = mf_grid(P->geom);
+    P->spmv_grid  = sm_count();
+    P->upd_grid   = resident_grid(k_cg_update<true, 2>, kUpdThreads, (n + 1) / 2);
+    P->setup_grid = resident_grid(k_cg_setup<true, 2>, kUpdThreads, (n + 1) / 2);
+    const size_t vb = (size_t)n * sizeof(double);
+    cudaError_t  e  = cudaSuccess;
+    auto alloc = [&](void** q, size_t bytes) {
+        if (e == cudaSuccess) e = cudaMalloc(q, bytes);
+    };
+    alloc(reinterpret_cast<void**>(&P->dinv), 64); // unused: the diagonal is constant
+    alloc(reinterpret_cast<void**>(&P->r), vb);
+    alloc(reinterpret_cast<void**>(&P->z), vb + 32);
+    alloc(reinterpret_cast<void**>(&P->p[0]), vb + 32);
+    alloc(reinterpret_cast<void**>(&P->p[1]), vb + 32);
+    alloc(reinterpret_cast<void**>(&P->w), vb);
+    alloc(reinterpret_cast<void**>(&P->hist), sizeof(double) * (cfg.max_it + 1));
+    alloc(reinterpret_cast<void**>(&P->st), sizeof(CgState));
+    alloc(reinterpret_cast<void**>(&P->partials), sizeof(double) * 4 * kMaxReduceBlocks);
+    alloc(reinterpret_cast<void**>(&P->tickets), 16 * sizeof(unsigned int));
+    alloc(reinterpret_cast<void**>(&P->tmp), 16 * sizeof(double));
+    cudaStream_t s = ctx->stream;
+    if (e == cudaSuccess) e = cudaMemsetAsync(P->tickets, 0, 16 * sizeof(unsigned int), s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(P->p[0], 0, vb, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(P->p[1], 0, vb, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(P->st, 0, sizeof(CgState), s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(P->hist, 0, sizeof(double) * (cfg.max_it + 1), s);
+    if (e != cudaSuccess) {
+        rvk_cg_plan_destroy(P);
+        return cuda_error(e, "rvk_cg_plan_create_stencil");
     }
     *out = P;
     return RVK_OK;

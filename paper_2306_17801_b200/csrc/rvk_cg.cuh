@@ -35,6 +35,96 @@ int resident_grid(K kernel, int threads, int64_t n_items)
     return (int)(want < 1 ? 1 : (want > cap ? cap : want));
 }
 
+// ---------------------------------------------------------------------------
+// K1 op: p_new = z + b p_old on the fly; w = A p_new; tail alpha.
+// ---------------------------------------------------------------------------
+template <bool FIRST>
+struct CgSpmvOp {
+    static constexpr bool kHasTail = true;
+    const double* __restrict__ z;
+    const double* __restrict__ p_old;
+    double* __restrict__ p_new;
+    double* __restrict__ w;
+    CgState* st;
+    int64_t  n;
+    int      it;
+    double   b; // set by init()
+
+    __device__ __forceinline__ bool init()
+    {
+        if (st->done) return false;
+        if (!FIRST) {
+            const double bo = st->betaold;
+            if (bo == 0.0) { // breakdown in beta/betaold
+                if (blockIdx.x == 0 && threadIdx.x == 0) {
+                    st->state          = RVK_CG_BREAKDOWN;
+                    st->breakdown_iter = it;
+                    st->done           = 1;
+                }
+                return false;
+            }
+            b = st->beta / bo;
+        }
+        return true;
+    }
+    struct Fetch {
+        double z, p;
+    };
+    __device__ __forceinline__ int           num_src() const { return FIRST ? 1 : 2; }
+    __device__ __forceinline__ const double* src_ptr(int k) const { return k == 0 ? z : p_old; }
+    __device__ __forceinline__ Fetch         fetch(int32_t j) const
+    {
+        return Fetch{__ldg(z + j), FIRST ? 0.0 : __ldg(p_old + j)};
+    }
+    __device__ __forceinline__ Fetch fetch_smem(const double* s0, const double* s1, int i) const
+    {
+        return Fetch{s0[i], FIRST ? 0.0 : s1[i]};
+    }
+    __device__ __forceinline__ double value(const Fetch& f) const
+    {
+        return FIRST ? f.z : aypx1(b, f.z, f.p); // z + b*p  (kernels_scalar.cpp:33)
+    }
+    __device__ __forceinline__ int64_t own_col(int64_t i) const { return i; }
+    // p_new[i] = z[i] + b p_old[i] from the row's own (gathered) operands
+    __device__ __forceinline__ double row(int64_t i, double sum, double acc, const Fetch& o) const
+    {
+        const double p = value(o);
+        p_new[i]       = p;
+        w[i]           = sum;
+        return add(acc, mul(p, sum));
+    }
+    __device__ __forceinline__ void tail(double pAp) const
+    {
+        const double a = st->beta / pAp;
+        st->pAp        = pAp;
+        if (pAp == 0.0 || !isfinite(a)) {
+            st->state          = RVK_CG_BREAKDOWN;
+            st->breakdown_iter = it;
+            st->done           = 1;
+        } else {
+            st->alpha   = a;
+            st->betaold = st->beta;
+        }
+    }
+};
+
+// Constant-coefficient stencil geometry for the matrix-free operator
+// (rvk_mf.cu): the same operator rvk_build_laplacian assembles, applied
+// without storing it (PETSc MatShell analogue).
+struct StencilGeom {
+    int64_t nx, ny, nz, n;
+    int     dim, box; // box: 9/27-point, else 5/7-point
+    double  centre;   // points - 1; every neighbour is -1
+};
+// K1 on the stencil: p = z + b p_old on the fly, w = A p, p.w; same
+// CgSpmvOp semantics (init/tail) as the CSR kernel.  Bit-identical w to the
+// CSR path: the neighbours are visited in ascending column order with the
+// same coefficients.
+rvk_status launch_mf_k1(cudaStream_t s, const StencilGeom& g, bool first, const double* z,
+                        const double* p_old, double* p_new, double* w, CgState* st, int64_t n,
+                        int it, double* partials, unsigned int* ticket, int grid);
+int        mf_grid(const StencilGeom& g);
+
 // Arguments of the single-kernel persistent solve (rvk_cg_small.cu).
 struct PersistArgs {
     int64_t        n;

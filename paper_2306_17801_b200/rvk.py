@@ -35,7 +35,7 @@ EXPORTS = [
     "rvk_dot", "rvk_nrm2", "rvk_dot2", "rvk_axpy", "rvk_aypx", "rvk_waxpy", "rvk_scale",
     "rvk_pointwise_mult", "rvk_copy", "rvk_set", "rvk_csr_spmv", "rvk_csr_diagonal",
     "rvk_csr_diagonal_inverse", "rvk_csr_validate", "rvk_laplacian_size",
-    "rvk_build_laplacian", "rvk_fill_rhs", "rvk_cg_plan_create", "rvk_cg_plan_destroy",
+    "rvk_build_laplacian", "rvk_fill_rhs", "rvk_cg_plan_create", "rvk_cg_plan_create_stencil", "rvk_cg_plan_destroy",
     "rvk_cg_solve_dev", "rvk_cg_history_dev", "rvk_cg_result", "rvk_cg_solve_host",
     "rvk_cg_set_profiling", "rvk_cg_kernel_times", "rvk_cg_plan_mode",
     "rvk_laplacian_rows_nnz", "rvk_build_laplacian_rows", "rvk_comm_unique_id", "rvk_comm_init",
@@ -133,6 +133,7 @@ def lib():
         "rvk_build_laplacian": (i, [vp, i, i, i64, i64, i64, vp, vp, vp]),
         "rvk_fill_rhs": (i, [vp, C.c_uint64, i64, vp]),
         "rvk_cg_plan_create": (i, [vp, C.POINTER(Csr), CgConfig, C.POINTER(vp)]),
+        "rvk_cg_plan_create_stencil": (i, [vp, i, i, i64, i64, i64, CgConfig, C.POINTER(vp)]),
         "rvk_cg_plan_destroy": (i, [vp]),
         "rvk_cg_solve_dev": (i, [vp, vp, vp]),
         "rvk_cg_history_dev": (vp, [vp]),
@@ -317,9 +318,10 @@ class CgResult:
 
 
 class CgPlan:
-    """KSPSetUp + KSPSolve for Jacobi-PCG (rvk_cg_plan_*)."""
+    """KSPSetUp + KSPSolve for Jacobi-PCG (rvk_cg_plan_*).  A is a DeviceCsr,
+    or a stencil spec (dim, points, grid) for the matrix-free operator."""
 
-    def __init__(self, ctx: Ctx, A: DeviceCsr, max_it: int = 20, pc: str = "jacobi",
+    def __init__(self, ctx: Ctx, A, max_it: int = 20, pc: str = "jacobi",
                  rtol: float = 0.0, atol: float = 0.0, mode: str = "fused",
                  use_graph: bool = True):
         self.ctx, self.A = ctx, A
@@ -327,7 +329,13 @@ class CgPlan:
         cfg = CgConfig(max_it, PC_JACOBI if pc == "jacobi" else PC_NONE, rtol, atol,
                        MODES[mode], 1 if use_graph else 0)
         h = C.c_void_p()
-        check(lib().rvk_cg_plan_create(ctx.h, C.byref(A.c), cfg, C.byref(h)))
+        if isinstance(A, DeviceCsr):
+            check(lib().rvk_cg_plan_create(ctx.h, C.byref(A.c), cfg, C.byref(h)))
+        else:
+            dim, points, grid = A
+            nx, ny, nz = (list(grid) + [1, 1])[:3]
+            check(lib().rvk_cg_plan_create_stencil(ctx.h, dim, points, nx, ny, nz, cfg,
+                                                   C.byref(h)))
         self.h = h
 
     def close(self):

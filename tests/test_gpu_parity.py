@@ -401,3 +401,33 @@ print("ok")
     p = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True,
                        env=dict(os.environ, RVK_WINDOWS="1"), timeout=600)
     assert p.returncode == 0 and "ok" in p.stdout, p.stdout + p.stderr
+
+
+@pytest.mark.parametrize("spec", [(2, 5, (96, 77)), (2, 9, (64, 50)), (3, 7, (40, 33, 21)),
+                                  (3, 27, (24, 20, 18)), (3, 7, (256, 256, 256))])
+def test_matrix_free_stencil_cg_vs_oracle(ctx, spec):
+    """Matrix-free operator: same neighbour order and
+    coefficients as the assembled CSR, constant Jacobi diagonal."""
+    dim, pts, g = spec
+    Ah = O.build_laplacian(dim, pts, g)
+    b = O.rhs(Ah.n_rows)
+    ref = O.cg_solve(Ah, b, max_it=20)
+    plan = rvk.CgPlan(ctx, (dim, pts, g), max_it=20)
+    x, res = plan.solve_host(b)
+    check_cg(res, x, ref)
+    # and it agrees with the CSR plan to reduction-order rounding
+    A = rvk.DeviceCsr.laplacian(ctx, dim, pts, g)
+    x2, res2 = rvk.CgPlan(ctx, A, max_it=20).solve_host(b)
+    assert np.max(np.abs(res.hist - res2.hist) / res2.hist) < 1e-12
+
+
+def test_matrix_free_stencil_rtol_and_modes(ctx):
+    dim, pts, g = 2, 5, (64, 64)
+    Ah = O.build_laplacian(dim, pts, g)
+    b = O.rhs(Ah.n_rows)
+    ref = O.cg_solve(Ah, b, max_it=500, rtol=1e-8)
+    plan = rvk.CgPlan(ctx, (dim, pts, g), max_it=500, rtol=1e-8)
+    x, res = plan.solve_host(b)
+    check_cg(res, x, ref)
+    with pytest.raises(rvk.RvkError):
+        rvk.CgPlan(ctx, (dim, pts, g), max_it=20, mode="unfused")
