@@ -176,7 +176,10 @@ typedef struct {
     double rtol;      /* converged if dp <= max(rtol*dp0, atol); 0,0 => only 0   */
     double atol;
     int    mode;      /* rvk_cg_mode                                             */
-    int    use_graph; /* capture the whole solve as one CUDA graph (replayed)    */
+    int    use_graph; /* 1: the whole solve as one CUDA graph (max_it iterations
+                         unrolled, replayed); 2: graph with a device-side WHILE
+                         node -- no launches after convergence (FUSED only);
+                         0: plain stream launches                             */
 } rvk_cg_config;
 
 typedef struct {

@@ -128,9 +128,16 @@ __global__ void __launch_bounds__(kUpdThreads)
     k_cg_update(int64_t n, const double* __restrict__ p, const double* __restrict__ w,
                 const double* __restrict__ dinv, double* __restrict__ x, double* __restrict__ r,
                 double* __restrict__ z, CgState* st, double* hist, int it, double rtol,
-                double atol, double* partials, unsigned int* ticket, double dconst)
+                double atol, double* partials, unsigned int* ticket, double dconst, int max_it,
+                cudaGraphConditionalHandle cond, int use_cond)
 {
-    if (st->done) return;
+    // In the device WHILE loop (use_cond) `it` comes from the device state and
+    // this kernel decides whether the loop body runs again.
+    if (st->done) {
+        if (use_cond && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(cond, 0);
+        return;
+    }
+    if (it < 0) it = st->iterations;
     __shared__ double smem[64];
     __shared__ int    flag;
     const double      a      = st->alpha;
@@ -209,12 +216,16 @@ __global__ void __launch_bounds__(kUpdThreads)
         hist[it + 1]    = dp;
         st->dp          = dp;
         st->iterations  = it + 1;
+        bool more = it + 1 < max_it;
         if (cg_converged(dp, st->dp0, rtol, atol)) {
             st->state = RVK_CG_CONVERGED;
             st->done  = 1;
+            more      = false;
         } else {
             st->beta = acc[1];
+            if (!more) st->done = 1; // ran max_it: later kernels of a WHILE body no-op
         }
+        if (use_cond) cudaGraphSetConditional(cond, more ? 1u : 0u);
         *ticket = 0u;
     }
 }
@@ -494,18 +505,99 @@ rvk_status launch_setup(rvk_cg_plan P, int pcm, const double* b, double* x)
 }
 
 template <bool V>
-rvk_status launch_update(rvk_cg_plan P, int pcm, const double* p_new, double* x, int it)
+rvk_status launch_update(rvk_cg_plan P, int pcm, const double* p_new, double* x, int it,
+                         cudaGraphConditionalHandle cond = 0, int use_cond = 0)
 {
     cudaStream_t s = P->ctx->stream;
     auto go = [&](auto kern) {
         kern<<<P->upd_grid, kUpdThreads, 0, s>>>(P->A.n_rows, p_new, P->w, P->dinv, x, P->r, P->z,
                                                  P->st, P->hist, it, P->cfg.rtol, P->cfg.atol,
-                                                 P->partials, P->tickets, P->dconst);
+                                                 P->partials, P->tickets, P->dconst,
+                                                 P->cfg.max_it, cond, use_cond);
     };
     if (pcm == 0) go(k_cg_update<V, 0>);
     else if (pcm == 1) go(k_cg_update<V, 1>);
     else go(k_cg_update<V, 2>);
     RVK_CHECK_LAUNCH("k_cg_update");
+    return RVK_OK;
+}
+
+// K1 of one iteration: it >= 0 static index, it == -1 read from the device
+// (WHILE body); `first` selects the p = z variant of iteration 0.
+rvk_status launch_k1(rvk_cg_plan P, int it, bool first, const double* p_old, double* p_new)
+{
+    cudaStream_t   s = P->ctx->stream;
+    const int64_t  n = P->A.n_rows;
+    const TailArgs ta{P->partials + 2 * kMaxReduceBlocks, P->tickets + 1};
+    if (P->stencil)
+        return launch_mf_k1(s, P->geom, first, P->z, p_old, p_new, P->w, P->st, n, it, ta.partials,
+                            ta.ticket, P->mf_grid);
+    if (first) {
+        CgSpmvOp<true> op{P->z, p_old, p_new, P->w, P->st, n, it, 0.0};
+        return launch_spmv(s, P->sa, op, ta, P->spmv_grid);
+    }
+    CgSpmvOp<false> op{P->z, p_old, p_new, P->w, P->st, n, it, 0.0};
+    return launch_spmv(s, P->sa, op, ta, P->spmv_grid);
+}
+
+// the convergence loop entirely on the device.  Graph =
+// [K0, K1(0), K2(0)] -> WHILE(cond) { K1, K2, K1, K2 } where K2's last block
+// sets the condition (not converged, no breakdown, iterations < max_it); the
+// body holds two iterations so the p ping-pong is static.  No kernel launches
+// after convergence, no host involvement.
+rvk_status build_while_graph(rvk_cg_plan P, const double* b, double* x, cudaGraphExec_t* out)
+{
+    cudaStream_t s   = P->ctx->stream;
+    const int    pcm = P->cfg.pc != RVK_PC_JACOBI ? 0 : (P->stencil ? 2 : 1);
+    const bool   vec = aligned16(b) && aligned16(x) && aligned16(P->dinv);
+    cudaGraph_t  g = nullptr, pro = nullptr, tmp = nullptr;
+    RVK_CUDA(cudaGraphCreate(&g, 0));
+    cudaGraphConditionalHandle h;
+    RVK_CUDA(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+    auto fail = [&](rvk_status rc) {
+        if (pro) cudaGraphDestroy(pro);
+        cudaGraphDestroy(g);
+        return rc;
+    };
+    // prologue
+    RVK_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeGlobal));
+    rvk_status rc = vec ? launch_setup<true>(P, pcm, b, x) : launch_setup<false>(P, pcm, b, x);
+    if (rc == RVK_OK) rc = launch_k1(P, 0, true, P->p[0], P->p[1]);
+    if (rc == RVK_OK)
+        rc = vec ? launch_update<true>(P, pcm, P->p[1], x, 0, h, 1)
+                 : launch_update<false>(P, pcm, P->p[1], x, 0, h, 1);
+    cudaError_t e = cudaStreamEndCapture(s, &pro);
+    if (rc != RVK_OK) return fail(rc);
+    if (e != cudaSuccess) return fail(cuda_error(e, "capture (while prologue)"));
+    cudaGraphNode_t npro, nwhile;
+    if ((e = cudaGraphAddChildGraphNode(&npro, g, nullptr, 0, pro)) != cudaSuccess)
+        return fail(cuda_error(e, "cudaGraphAddChildGraphNode"));
+    cudaGraphNodeParams prm = {};
+    prm.type               = cudaGraphNodeTypeConditional;
+    prm.conditional.handle = h;
+    prm.conditional.type   = cudaGraphCondTypeWhile;
+    prm.conditional.size   = 1;
+    if ((e = cudaGraphAddNode(&nwhile, g, &npro, 1, &prm)) != cudaSuccess)
+        return fail(cuda_error(e, "cudaGraphAddNode(WHILE)"));
+    cudaGraph_t body = prm.conditional.phGraph_out[0];
+    // body: odd iteration (p_old = p[1]) then even iteration (p_old = p[0])
+    if ((e = cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0,
+                                           cudaStreamCaptureModeGlobal)) != cudaSuccess)
+        return fail(cuda_error(e, "cudaStreamBeginCaptureToGraph"));
+    rc = launch_k1(P, -1, false, P->p[1], P->p[0]);
+    if (rc == RVK_OK)
+        rc = vec ? launch_update<true>(P, pcm, P->p[0], x, -1, h, 1)
+                 : launch_update<false>(P, pcm, P->p[0], x, -1, h, 1);
+    if (rc == RVK_OK) rc = launch_k1(P, -1, false, P->p[0], P->p[1]);
+    if (rc == RVK_OK)
+        rc = vec ? launch_update<true>(P, pcm, P->p[1], x, -1, h, 1)
+                 : launch_update<false>(P, pcm, P->p[1], x, -1, h, 1);
+    e = cudaStreamEndCapture(s, &tmp);
+    if (rc != RVK_OK) return fail(rc);
+    if (e != cudaSuccess) return fail(cuda_error(e, "capture (while body)"));
+    e = cudaGraphInstantiate(out, g, 0);
+    fail(RVK_OK);
+    if (e != cudaSuccess) return cuda_error(e, "cudaGraphInstantiate (while)");
     return RVK_OK;
 }
 
@@ -990,6 +1082,18 @@ rvk_status rvk_cg_solve_dev(rvk_cg_plan P, const double* b, double* x)
     if (P->mode == RVK_CG_MODE_HOSTSYNC) return solve_hostsync(P, b, x);
     // one cooperative launch needs no graph
     if (!P->cfg.use_graph || P->mode == RVK_CG_MODE_PERSISTENT) return enqueue_solve(P, b, x);
+    if (P->cfg.use_graph == 2 && P->mode == RVK_CG_MODE_FUSED) { // device WHILE loop
+        if (!P->graph || P->g_b != b || P->g_x != x) {
+            destroy_graph(P);
+            RVK_TRY(build_while_graph(P, b, x, &P->graph));
+            P->g_b      = b;
+            P->g_x      = x;
+            P->g_prof   = false;
+            P->launches = -1; // data-dependent: 3 + 4 per body pass
+        }
+        RVK_CUDA(cudaGraphLaunch(P->graph, s));
+        return RVK_OK;
+    }
     if (!P->graph || P->g_b != b || P->g_x != x || P->g_prof != P->profiling) {
         destroy_graph(P);
         cudaGraph_t g = nullptr;

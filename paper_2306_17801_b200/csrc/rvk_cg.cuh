@@ -53,6 +53,7 @@ struct CgSpmvOp {
     __device__ __forceinline__ bool init()
     {
         if (st->done) return false;
+        if (it < 0) it = st->iterations; // device WHILE loop: the iteration index lives on device
         if (!FIRST) {
             const double bo = st->betaold;
             if (bo == 0.0) { // breakdown in beta/betaold

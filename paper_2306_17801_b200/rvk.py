@@ -9,6 +9,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import weakref
 from dataclasses import dataclass
 
 import numpy as np
@@ -191,9 +192,12 @@ class Ctx:
         h = C.c_void_p()
         check(lib().rvk_ctx_create(stream, C.byref(h)))
         self.h = h
+        self._deps = weakref.WeakSet()   # plans bound to this context
 
     def close(self):
         if self.h:
+            for d in list(self._deps):     # a plan must not outlive its stream
+                d.close()
             lib().rvk_ctx_destroy(self.h)
             self.h = None
 
@@ -326,8 +330,9 @@ class CgPlan:
                  use_graph: bool = True):
         self.ctx, self.A = ctx, A
         self.max_it = max_it
+        graph = 2 if use_graph == "while" else (1 if use_graph else 0)
         cfg = CgConfig(max_it, PC_JACOBI if pc == "jacobi" else PC_NONE, rtol, atol,
-                       MODES[mode], 1 if use_graph else 0)
+                       MODES[mode], graph)
         h = C.c_void_p()
         if isinstance(A, DeviceCsr):
             check(lib().rvk_cg_plan_create(ctx.h, C.byref(A.c), cfg, C.byref(h)))
@@ -337,6 +342,7 @@ class CgPlan:
             check(lib().rvk_cg_plan_create_stencil(ctx.h, dim, points, nx, ny, nz, cfg,
                                                    C.byref(h)))
         self.h = h
+        ctx._deps.add(self)
 
     def close(self):
         if self.h:

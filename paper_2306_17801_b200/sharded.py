@@ -99,6 +99,7 @@ class ShardPlan:
                                                 _cfg(max_it, pc, rtol, atol), comm, shared_gather,
                                                 C.byref(h)))
         self.h = h
+        ctx._deps.add(self)
 
     def solve_dev(self, b: "rvk.DeviceArray", x: "rvk.DeviceArray"):
         rvk.check(rvk.lib().rvk_dcg_solve_dev(self.h, b.ptr, x.ptr))

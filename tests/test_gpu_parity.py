@@ -431,3 +431,29 @@ def test_matrix_free_stencil_rtol_and_modes(ctx):
     check_cg(res, x, ref)
     with pytest.raises(rvk.RvkError):
         rvk.CgPlan(ctx, (dim, pts, g), max_it=20, mode="unfused")
+
+
+@pytest.mark.parametrize("op", ["csr", "stencil"])
+@pytest.mark.parametrize("max_it,rtol", [(1, 0.0), (7, 0.0), (20, 0.0), (500, 1e-8), (501, 1e-9)])
+def test_device_while_loop(ctx, op, max_it, rtol):
+    """convergence loop as a CUDA-graph WHILE node."""
+    dim, pts, g = 2, 5, (64, 48)
+    Ah = O.build_laplacian(dim, pts, g)
+    b = O.rhs(Ah.n_rows)
+    ref = O.cg_solve(Ah, b, max_it=max_it, rtol=rtol)
+    A = rvk.DeviceCsr.laplacian(ctx, dim, pts, g) if op == "csr" else (dim, pts, g)
+    plan = rvk.CgPlan(ctx, A, max_it=max_it, rtol=rtol, use_graph="while")
+    for _ in range(2):  # replay
+        x, res = plan.solve_host(b)
+        check_cg(res, x, ref)
+
+
+def test_device_while_loop_breakdown(ctx):
+    Ah = O.Csr(2, 2, np.array([0, 1, 2], np.int64), np.array([0, 1], np.int32),
+               np.array([1.0, -1.0]))
+    A = rvk.DeviceCsr.from_host(ctx, 2, 2, Ah.off, Ah.cols, Ah.vals)
+    plan = rvk.CgPlan(ctx, A, max_it=50, pc="none", use_graph="while")
+    plan.solve_dev(up(ctx, np.array([1.0, 1.0])), rvk.DeviceArray(2))
+    with pytest.raises(rvk.BreakdownError) as ei:
+        plan.result()
+    assert ei.value.iteration == 0
