@@ -51,7 +51,7 @@ struct SolveResult {
 SolveResult cg_solve(const CsrMatrix& A, const DenseVector& b, DenseVector& x,
                      const SolverConfig& cfg = {});
 SolveResult tfqmr_solve(const CsrMatrix& A, const DenseVector& b, DenseVector& x,
-                        const SolverConfig& cfg = {}); // out of scope: throws
+                        const SolverConfig& cfg = {}); // left-Jacobi TFQMR; history 2*its+1
 
 // z <- diag(A)^-1 r.
 void pc_jacobi_apply(const DenseVector& diag_inv, const DenseVector& r, DenseVector& z,

@@ -220,6 +220,24 @@ rvk_status rvk_cg_set_profiling(rvk_cg_plan plan, int on);
 rvk_status rvk_cg_kernel_times(rvk_cg_plan plan, float* spmv_ms, float* update_ms,
                                int* launches);
 
+/* ---- KSP: left-Jacobi TFQMR --------
+ * Freund's transpose-free QMR in PETSc KSPSolve_TFQMR operation order
+ * (oracle/rvk_oracle.c:ro_tfqmr_solve): two B*A products and three
+ * reductions per outer iteration, all scalars device-resident, zero host
+ * syncs.  cfg.mode is ignored; cfg.use_graph 1 captures the whole solve as
+ * one CUDA graph.  hist holds 2*max_it+1 doubles: ||B r0|| then the
+ * residual bound sqrt(2i+m+2)*tau after half step m of outer iteration i. */
+typedef struct rvk_tfqmr_plan_s* rvk_tfqmr_plan;
+rvk_status rvk_tfqmr_plan_create(rvk_ctx ctx, const rvk_csr* A_dev, rvk_cg_config cfg,
+                                 rvk_tfqmr_plan* out);
+rvk_status rvk_tfqmr_plan_destroy(rvk_tfqmr_plan plan);
+rvk_status rvk_tfqmr_solve_dev(rvk_tfqmr_plan plan, const double* b_dev, double* x_dev);
+/* Synchronise; hist_host (2*max_it+1 doubles, may be NULL), *n_hist = valid
+ * entries, info.iterations = outer iterations.  RVK_ERR_BREAKDOWN on
+ * (v, rp) == 0 or rho_old == 0. */
+rvk_status rvk_tfqmr_result(rvk_tfqmr_plan plan, double* hist_host, int* n_hist,
+                            rvk_cg_info* info);
+
 /* ---- row sharding across GPUs -----------------------------
  * The global grid is split into contiguous slabs of planes; shard `rank`
  * owns n_own rows and keeps one halo plane (halo_lo / halo_hi rows, 0 at the

@@ -15,7 +15,7 @@ REF_SO = os.path.join(HERE, "_ref", "librivulet_ref.so")
 __all__ = [
     "build", "lib", "ref_lib", "ref_available", "Csr", "build_laplacian", "laplacian_nnz",
     "rhs", "diagonal", "cg_solve", "ref_cg_solve", "spmv", "ref_spmv", "dot", "nrm2",
-    "CgResult", "DEFAULT_SEED",
+    "CgResult", "DEFAULT_SEED", "tfqmr_solve",
 ]
 
 DEFAULT_SEED = 0x9E3779B97F4A7C15
@@ -71,6 +71,9 @@ def lib():
         L.ro_splitmix64.restype = C.c_uint64
         L.ro_splitmix64.argtypes = [C.c_uint64]
         L.ro_rhs.argtypes = [C.c_uint64, C.c_int64, _f64p]
+        L.ro_tfqmr_solve.restype = _CgRes
+        L.ro_tfqmr_solve.argtypes = [C.c_int64, _i64p, _i32p, _f64p, _f64p, _f64p, _f64p,
+                                     _CgCfg, _f64p, C.POINTER(C.c_int)]
         L.ro_cg_solve.restype = _CgRes
         L.ro_cg_solve.argtypes = [C.c_int64, _i64p, _i32p, _f64p, _f64p, _f64p, _f64p,
                                   _CgCfg, _f64p]
@@ -212,3 +215,19 @@ def ref_cg_solve(A: Csr, b: np.ndarray, max_it: int = 20, pc: str = "jacobi",
     ref_lib().ref_cg_solve(backend, n, A.nnz, A.off, A.cols, A.vals, b, x, hist, max_it,
                            1 if pc == "jacobi" else 0, rtol, atol, work, out)
     return CgResult(x, hist[: out[1] + 1].copy(), int(out[0]), int(out[1]), int(out[2]))
+
+
+def tfqmr_solve(A: Csr, b: np.ndarray, max_it: int = 20, pc: str = "jacobi",
+                rtol: float = 0.0, atol: float = 0.0) -> CgResult:
+    """ro_tfqmr_solve: left-Jacobi TFQMR, PETSc KSPSolve_TFQMR operation order
+    (restated: the reference ships no TFQMR source).  hist = the initial
+    residual followed by the quasi-residual estimate of every half step."""
+    n = A.n_rows
+    b = np.ascontiguousarray(b, np.float64)
+    x = np.empty(n, np.float64)
+    hist = np.full(2 * max_it + 1, np.nan)
+    work = np.empty(11 * n, np.float64)
+    nh = C.c_int(0)
+    cfg = _CgCfg(max_it, 1 if pc == "jacobi" else 0, rtol, atol)
+    r = lib().ro_tfqmr_solve(n, A.off, A.cols, A.vals, b, x, hist, cfg, work, C.byref(nh))
+    return CgResult(x, hist[: nh.value].copy(), r.status, r.iterations, r.breakdown_iter)

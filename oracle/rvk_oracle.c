@@ -247,3 +247,99 @@ ro_cg_result ro_cg_solve(int64_t n, const int64_t* off, const int32_t* cols,
     }
     return res;
 }
+
+/* ------------------------------------------------------------------------ */
+/* TFQMR (see rvk_oracle.h).  B = Jacobi applied on the left: every operator
+ * application is T1 = A v, out = dinv .* T1. */
+static void apply_BA(int64_t n, const int64_t* off, const int32_t* cols, const double* vals,
+                     const double* dinv, int pc, const double* v, double* t1, double* out)
+{
+    ro_csr_spmv(n, off, cols, vals, v, t1);
+    if (pc == RO_PC_JACOBI) ro_pointwise_mult(n, dinv, t1, out);
+    else memcpy(out, t1, (size_t)n * sizeof(double));
+}
+
+ro_cg_result ro_tfqmr_solve(int64_t n, const int64_t* off, const int32_t* cols,
+                            const double* vals, const double* b, double* x,
+                            double* hist, ro_cg_config cfg, double* work, int* n_hist)
+{
+    ro_cg_result res = {RO_OK, 0, -1};
+    double *R = work, *RP = work + n, *U = work + 2 * n, *P = work + 3 * n, *V = work + 4 * n;
+    double *D = work + 5 * n, *Q = work + 6 * n, *T = work + 7 * n, *AUQ = work + 8 * n;
+    double *T1 = work + 9 * n, *dinv = work + 10 * n;
+    const size_t bytes = (size_t)n * sizeof(double);
+    *n_hist = 0;
+
+    memset(x, 0, bytes);
+    if (cfg.pc == RO_PC_JACOBI) {
+        ro_csr_diagonal(n, off, cols, vals, dinv);
+        for (int64_t i = 0; i < n; ++i) dinv[i] = 1.0 / dinv[i];
+        ro_pointwise_mult(n, dinv, b, R); /* R = B (b - A x0), x0 = 0 */
+    } else {
+        memcpy(R, b, bytes);
+    }
+    double dp = ro_nrm2(n, R);
+    hist[(*n_hist)++] = dp;
+    const double dp0 = dp;
+    if (converged(dp, dp0, &cfg)) {
+        res.status = RO_CONVERGED;
+        return res;
+    }
+    memcpy(RP, R, bytes);
+    double etaold = 0.0, psiold = 0.0, tau = dp, dpold = dp;
+    double rhoold = ro_dot(n, R, RP);
+    memcpy(U, R, bytes);
+    memcpy(P, R, bytes);
+    apply_BA(n, off, cols, vals, dinv, cfg.pc, P, T1, V);
+    memset(D, 0, bytes);
+
+    for (int i = 0; i < cfg.max_it; ++i) {
+        const double s = ro_dot(n, V, RP);
+        if (s == 0.0) {
+            res.status = RO_BREAKDOWN;
+            res.breakdown_iter = i;
+            return res;
+        }
+        const double a = rhoold / s;
+        ro_waxpy(n, -a, V, U, Q);  /* q = u - a v       */
+        ro_waxpy(n, 1.0, U, Q, T); /* t = u + q         */
+        apply_BA(n, off, cols, vals, dinv, cfg.pc, T, T1, AUQ);
+        ro_axpy(n, -a, AUQ, R);    /* r = r - a B A (u + q) */
+        dp = ro_nrm2(n, R);
+        for (int m = 0; m < 2; ++m) {
+            const double w   = m == 0 ? sqrt(dp * dpold) : dp;
+            const double psi = w / tau;
+            const double cm  = 1.0 / sqrt(1.0 + psi * psi);
+            tau              = tau * psi * cm;
+            const double eta = cm * cm * a;
+            const double cf  = psiold * psiold * etaold / a;
+            ro_aypx(n, cf, m == 0 ? U : Q, D); /* d = (u|q) + cf d */
+            ro_axpy(n, eta, D, x);             /* x = x + eta d    */
+            /* residual bound ||r_k|| <= sqrt(k+1) tau_k, k = 2i+m+1 half steps */
+            const double dpest = sqrt(2.0 * i + m + 2.0) * tau;
+            hist[(*n_hist)++]  = dpest;
+            if (converged(dpest, dp0, &cfg)) {
+                res.status     = RO_CONVERGED;
+                res.iterations = i + 1;
+                return res;
+            }
+            etaold = eta;
+            psiold = psi;
+        }
+        res.iterations = i + 1;
+        const double rho = ro_dot(n, R, RP);
+        if (rhoold == 0.0) {
+            res.status = RO_BREAKDOWN;
+            res.breakdown_iter = i;
+            return res;
+        }
+        const double bb = rho / rhoold;
+        ro_waxpy(n, bb, Q, R, U); /* u = r + b q        */
+        ro_axpy(n, bb, P, Q);     /* q = q + b p        */
+        ro_waxpy(n, bb, Q, U, P); /* p = u + b q        */
+        apply_BA(n, off, cols, vals, dinv, cfg.pc, P, T1, V);
+        rhoold = rho;
+        dpold  = dp;
+    }
+    return res;
+}

@@ -31,9 +31,11 @@ namespace detail {
 struct CgPlanCache {
     Context ctx{StreamType::DefaultBlocking, "cg_fused"};
     std::map<std::tuple<int, int, double, double>, rvk_cg_plan> plans;
+    std::map<std::tuple<int, int, double, double>, rvk_tfqmr_plan> tfqmr;
     ~CgPlanCache()
     {
         for (auto& [k, p] : plans) rvk_cg_plan_destroy(p);
+        for (auto& [k, p] : tfqmr) rvk_tfqmr_plan_destroy(p);
     }
 };
 
@@ -60,7 +62,7 @@ FlopLog make_floplog(const runtime::Census& d, const runtime::CopyCounts& c0)
     f.matmult     = d.flops_of(KernelKind::MatMult);
     f.dot         = d.flops_of(KernelKind::Dot);
     f.norm        = d.flops_of(KernelKind::Norm);
-    f.axpy        = d.flops_of(KernelKind::Axpy);
+    f.axpy        = d.flops_of(KernelKind::Axpy) + d.flops_of(KernelKind::Waxpy);
     f.aypx        = d.flops_of(KernelKind::Aypx);
     f.scalar_expr = d.flops_of(KernelKind::ExprEval);
     f.total_flops = f.matmult + f.dot + f.norm + f.axpy + f.aypx + f.scalar_expr;
@@ -256,9 +258,86 @@ SolveResult cg_solve(const CsrMatrix& A, const DenseVector& b, DenseVector& x, c
     return cg_listing(A, b, x, cfg);
 }
 
-SolveResult tfqmr_solve(const CsrMatrix&, const DenseVector&, DenseVector&, const SolverConfig&)
+// Left-Jacobi TFQMR through librvk's TFQMR plan (rvk_tfqmr.cu): PETSc
+// KSPSolve_TFQMR order, all scalars device-resident, the solve one CUDA graph.
+// SolverMode is not consulted (there is no op-per-call listing for TFQMR in
+// the paper); the history is ||B r0|| followed by one residual bound per half
+// step (2 per outer iteration).
+SolveResult tfqmr_solve(const CsrMatrix& A, const DenseVector& b, DenseVector& x, const SolverConfig& cfg)
 {
-    throw Error("tfqmr_solve: TFQMR is outside the B200 hot path this round (SURVEY.md 8f row 3)");
+    if (cfg.max_it < 1) throw Error("tfqmr_solve: max_it must be >= 1");
+    if (A.rows() != A.cols()) throw Error("tfqmr_solve: matrix is not square");
+    if (b.size() != A.rows() || x.size() != A.rows()) throw Error("tfqmr_solve: dimension mismatch");
+    if (cfg.convergence_callback)
+        throw Error("tfqmr_solve: convergence_callback is not supported (the solve is one device graph; "
+                    "use rtol/atol)");
+    auto& ms = *A.state();
+    if (!ms.plans) ms.plans = std::make_shared<detail::CgPlanCache>();
+    auto&      cache = *ms.plans;
+    const auto key   = std::make_tuple(cfg.max_it, cfg.pc == PcType::Jacobi ? 1 : 0, cfg.rtol, cfg.atol);
+    auto       it    = cache.tfqmr.find(key);
+    if (it == cache.tfqmr.end()) {
+        rvk_cg_config  c{cfg.max_it, cfg.pc == PcType::Jacobi ? RVK_PC_JACOBI : RVK_PC_NONE,
+                         cfg.rtol, cfg.atol, RVK_CG_MODE_FUSED, 1};
+        rvk_tfqmr_plan p = nullptr;
+        const rvk_csr  v = ms.view();
+        detail::check(rvk_tfqmr_plan_create(cache.ctx.handle(), &v, c, &p), "tfqmr_solve(setup)");
+        it = cache.tfqmr.emplace(key, p).first;
+    }
+    rvk_tfqmr_plan plan = it->second;
+    const auto     c0   = runtime::census();
+    const auto     cc0  = runtime::copy_counts();
+    Launch         L(cache.ctx, "tfqmr_solve");
+    L.read(A.id()).read(b.id()).write(x.id());
+    L.begin();
+    detail::check(rvk_tfqmr_solve_dev(plan, b.device_data(), x.device_data()), "tfqmr_solve");
+    L.end();
+    detail::device_wrote(*x.state());
+
+    std::vector<double> hist(2 * (std::size_t)cfg.max_it + 1);
+    rvk_cg_info         info{};
+    int                 nh = 0;
+    const rvk_status    st = rvk_tfqmr_result(plan, hist.data(), &nh, &info);
+    runtime::log_d2h(hist.size() * sizeof(double));
+    // census: setup (B b, ||r||, (r, rp), v = B A p), then per outer iteration
+    // 2 matmults, 3 reductions, 7 vector updates (+2 on the continuing path)
+    const std::size_t n = A.rows(), nnz = A.nnz();
+    runtime::log_kernel(KernelKind::PcApply, 0);
+    runtime::log_kernel(KernelKind::Norm, 2 * n);
+    runtime::log_kernel(KernelKind::Dot, 2 * n);
+    runtime::log_kernel(KernelKind::Copy, 0, 3);
+    runtime::log_kernel(KernelKind::MatMult, 2 * nnz);
+    runtime::log_kernel(KernelKind::PcApply, 0);
+    for (int i = 0; i < info.iterations; ++i) {
+        const bool last_conv = info.state == RVK_CG_CONVERGED && i + 1 == info.iterations;
+        runtime::log_kernel(KernelKind::Dot, 2 * n);
+        runtime::log_kernel(KernelKind::Waxpy, 4 * n, 2);
+        runtime::log_kernel(KernelKind::MatMult, 2 * nnz);
+        runtime::log_kernel(KernelKind::PcApply, 0);
+        runtime::log_kernel(KernelKind::Axpy, 2 * n);
+        runtime::log_kernel(KernelKind::Norm, 2 * n);
+        runtime::log_kernel(KernelKind::ExprEval, 2, 2); // a, -a
+        runtime::log_kernel(KernelKind::Aypx, 4 * n, 2);
+        runtime::log_kernel(KernelKind::Axpy, 4 * n, 2);
+        runtime::log_kernel(KernelKind::ExprEval, 28, 2); // psi, cm, tau, eta, cf, bound
+        if (last_conv) continue;
+        runtime::log_kernel(KernelKind::Dot, 2 * n);
+        runtime::log_kernel(KernelKind::ExprEval, 1, 1); // b
+        runtime::log_kernel(KernelKind::Waxpy, 4 * n, 2);
+        runtime::log_kernel(KernelKind::Axpy, 2 * n);
+        runtime::log_kernel(KernelKind::MatMult, 2 * nnz);
+        runtime::log_kernel(KernelKind::PcApply, 0);
+    }
+    if (st == RVK_ERR_BREAKDOWN)
+        throw BreakdownError("tfqmr_solve: breakdown at iteration " + std::to_string(info.breakdown_iter),
+                             info.breakdown_iter);
+    detail::check(st, "tfqmr_solve");
+    SolveResult r;
+    r.iterations = info.iterations;
+    r.converged  = info.state == RVK_CG_CONVERGED;
+    r.history.assign(hist.begin(), hist.begin() + nh);
+    r.flops = make_floplog(runtime::census() - c0, cc0);
+    return r;
 }
 
 void pc_jacobi_apply(const DenseVector& diag_inv, const DenseVector& r, DenseVector& z, const Context& ctx)

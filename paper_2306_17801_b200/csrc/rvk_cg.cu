@@ -295,11 +295,6 @@ __global__ void k_guarded_copy(int64_t n, const double* __restrict__ src, double
         dst[i] = src[i];
 }
 
-// Guarded plain SpMV op for the unfused sequence.
-struct SpmvGuardedOp : SpmvPlainOp {
-    const int* guard;
-    __device__ __forceinline__ bool init() { return *guard == 0; }
-};
 
 // diag / dinv (csr.hpp:76-77): zero where absent; dinv = 1/diag.
 // col_off: column of row r's diagonal is r + col_off (0, or a shard's lo halo).

@@ -477,6 +477,13 @@ struct SpmvPlainOp {
     __device__ __forceinline__ void tail(double) const {}
 };
 
+// Plain SpMV that is a no-op once a device flag is set (the early-exit of
+// the op-per-kernel solver sequences).
+struct SpmvGuardedOp : SpmvPlainOp {
+    const int* guard;
+    __device__ __forceinline__ bool init() { return *guard == 0; }
+};
+
 template <class Op>
 rvk_status launch_spmv(cudaStream_t stream, const SpmvArgs& a, const Op& op, TailArgs tail,
                        int grid)

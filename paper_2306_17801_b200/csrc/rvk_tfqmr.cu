@@ -1,0 +1,351 @@
+// rvk_tfqmr.cu -- left-Jacobi TFQMR on sm_100a (SPEC.md
+// :467-475; "two matrix-vector products and roughly twice
+// the number of vector inner products").
+//
+// Same recurrence and operation order as oracle/rvk_oracle.c:ro_tfqmr_solve
+// (PETSc KSPSolve_TFQMR order).  Every vector op is one of the library's
+// HBM-streaming kernels with device-scalar arguments; the scalar recurrence
+// (a, psi, cm, tau, eta, cf, b) runs in one-thread tail kernels, so the solve
+// is stream-ordered with ZERO host syncs and captured as one CUDA graph.  A
+// device `done` flag (convergence / breakdown) turns every later kernel of
+// the solve into a no-op.  Elementwise results are bit-identical to the
+// oracle's; the three reductions per iteration use tree order (SPEC's TFQMR
+// tolerance is 1e-8).
+#include "rvk_cg.cuh"
+#include "rvk_common.cuh"
+#include "rvk_context.hpp"
+#include "rvk_internal.hpp"
+#include "rvk_spmv.cuh"
+
+#include <cmath>
+#include <vector>
+
+namespace rvk {
+
+struct TfqState {
+    double rhoold, rho, s, a, b, dp, dpold, tau, etaold, psiold, eta, psi, cf, dp0;
+    int    done, state, iterations, breakdown_iter, nhist;
+};
+
+namespace {
+
+__device__ __forceinline__ bool tfq_conv(double v, double dp0, double rtol, double atol)
+{
+    return v <= fmax(rtol * dp0, atol);
+}
+
+// after dp = ||R0|| and rho = (R0, RP): hist[0], initial scalars
+__global__ void k_tfq_init(TfqState* st, double* hist, double rtol, double atol)
+{
+    const double dp    = st->dp;
+    hist[0]            = dp;
+    st->dp0            = dp;
+    st->nhist          = 1;
+    st->iterations     = 0;
+    st->breakdown_iter = -1;
+    st->etaold         = 0.0;
+    st->psiold         = 0.0;
+    st->tau            = dp;
+    st->dpold          = dp;
+    st->rhoold         = st->rho;
+    const bool conv    = tfq_conv(dp, dp, rtol, atol);
+    st->state          = conv ? RVK_CG_CONVERGED : RVK_CG_RUNNING;
+    st->done           = conv ? 1 : 0;
+}
+
+// a = rho_old / s with s = (V, RP); serious breakdown when s == 0
+__global__ void k_tfq_alpha(TfqState* st, int it)
+{
+    if (st->done) return;
+    if (st->s == 0.0) {
+        st->state          = RVK_CG_BREAKDOWN;
+        st->breakdown_iter = it;
+        st->done           = 1;
+        return;
+    }
+    st->a = st->rhoold / st->s;
+}
+
+// half step m, before the D / X updates: w, psi, cm, tau, eta, cf
+__global__ void k_tfq_half(TfqState* st, int m)
+{
+    if (st->done) return;
+    const double w   = m == 0 ? sqrt(__dmul_rn(st->dp, st->dpold)) : st->dp;
+    const double psi = w / st->tau;
+    const double cm  = 1.0 / sqrt(__dadd_rn(1.0, __dmul_rn(psi, psi)));
+    st->tau          = __dmul_rn(__dmul_rn(st->tau, psi), cm);
+    st->eta          = __dmul_rn(__dmul_rn(cm, cm), st->a);
+    st->cf           = __dmul_rn(__dmul_rn(st->psiold, st->psiold), st->etaold) / st->a;
+    st->psi          = psi;
+}
+
+// after X += eta D: quasi-residual estimate, convergence, shift eta/psi
+__global__ void k_tfq_post(TfqState* st, double* hist, int m, int it, double rtol, double atol)
+{
+    if (st->done) return;
+    const double dpest = __dmul_rn(sqrt(2.0 * it + m + 2.0), st->tau); // ||r_k|| <= sqrt(k+1) tau
+    hist[st->nhist++]  = dpest;
+    if (tfq_conv(dpest, st->dp0, rtol, atol)) {
+        st->state      = RVK_CG_CONVERGED;
+        st->iterations = it + 1;
+        st->done       = 1;
+        return;
+    }
+    st->etaold = st->eta;
+    st->psiold = st->psi;
+}
+
+// b = rho / rho_old (rho = (R, RP)); breakdown when rho_old == 0
+__global__ void k_tfq_beta(TfqState* st, int it)
+{
+    if (st->done) return;
+    st->iterations = it + 1;
+    if (st->rhoold == 0.0) {
+        st->state          = RVK_CG_BREAKDOWN;
+        st->breakdown_iter = it;
+        st->done           = 1;
+        return;
+    }
+    st->b = st->rho / st->rhoold;
+}
+
+__global__ void k_tfq_shift(TfqState* st)
+{
+    if (st->done) return;
+    st->rhoold = st->rho;
+    st->dpold  = st->dp;
+}
+
+__global__ void k_tfq_copy(int64_t n, const double* __restrict__ src, double* __restrict__ dst,
+                           const int* guard)
+{
+    if (guard && *guard) return;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) dst[i] = src[i];
+}
+
+} // namespace
+
+// Distinct op type: k_spmv_tma<TfqSpmvOp> is this file's own instantiation
+// (no template kernel shared across non-rdc translation units).
+struct TfqSpmvOp : SpmvGuardedOp {};
+
+} // namespace rvk
+
+using namespace rvk;
+
+struct rvk_tfqmr_plan_s {
+    rvk_ctx       ctx = nullptr;
+    rvk_csr       A{};
+    rvk_cg_config cfg{};
+    SpmvArgs      sa{};
+    double *R = nullptr, *RP = nullptr, *U = nullptr, *P = nullptr, *V = nullptr, *D = nullptr;
+    double *Q = nullptr, *T = nullptr, *AUQ = nullptr, *T1 = nullptr, *dinv = nullptr;
+    double*         hist = nullptr;
+    TfqState*       st = nullptr;
+    double*         partials = nullptr;
+    unsigned int*   tickets = nullptr;
+    cudaGraphExec_t graph = nullptr;
+    const double*   g_b = nullptr;
+    double*         g_x = nullptr;
+};
+
+namespace {
+
+#define RVK_TRY(x)                                                                             \
+    do {                                                                                       \
+        rvk_status rc_ = (x);                                                                  \
+        if (rc_ != RVK_OK) return rc_;                                                         \
+    } while (0)
+
+rvk_scalar sptr(const double* p, int kind = RVK_SCALAR_PTR)
+{
+    return rvk_scalar{kind, 0.0, p, nullptr};
+}
+
+int copy_grid(int64_t n)
+{
+    const int64_t want = (n + 255) / 256;
+    return (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sm_count() * 8));
+}
+
+// out = B A v: T1 = A v, out = dinv .* T1 (no PC: the SpMV writes `out`)
+rvk_status apply_BA(rvk_tfqmr_plan P, const double* v, double* out, const int* g)
+{
+    cudaStream_t  s   = P->ctx->stream;
+    const bool    jac = P->cfg.pc == RVK_PC_JACOBI;
+    TfqSpmvOp     op;
+    op.x     = v;
+    op.y     = jac ? P->T1 : out;
+    op.guard = g;
+    RVK_TRY(launch_spmv(s, P->sa, op, TailArgs{nullptr, nullptr}, sm_count()));
+    if (jac) RVK_TRY(vec_ew(s, EW_PMULT, P->A.n_rows, const_scalar(0), P->dinv, P->T1, out, g));
+    return RVK_OK;
+}
+
+rvk_status enqueue_tfqmr(rvk_tfqmr_plan P, const double* b, double* x)
+{
+    const int64_t n   = P->A.n_rows;
+    cudaStream_t  s   = P->ctx->stream;
+    const bool    jac = P->cfg.pc == RVK_PC_JACOBI;
+    Scratch       sc{P->partials, P->tickets};
+    TfqState*     st  = P->st;
+    const int*    g   = &st->done;
+    const double  rtol = P->cfg.rtol, atol = P->cfg.atol;
+    const int     cg  = copy_grid(n);
+
+    // setup: x = 0, R = B b, dp = ||R||, RP = R, rho = (R, RP), U = P = R, V = B A P, D = 0
+    RVK_CUDA(cudaMemsetAsync(x, 0, n * 8, s));
+    if (jac) RVK_TRY(vec_ew(s, EW_PMULT, n, const_scalar(0), P->dinv, b, P->R, nullptr));
+    else RVK_CUDA(cudaMemcpyAsync(P->R, b, n * 8, cudaMemcpyDeviceToDevice, s));
+    RVK_TRY(vec_reduce(s, sc, RED_NRM2, n, P->R, nullptr, &st->dp, nullptr, nullptr));
+    RVK_CUDA(cudaMemcpyAsync(P->RP, P->R, n * 8, cudaMemcpyDeviceToDevice, s));
+    RVK_TRY(vec_reduce(s, sc, RED_DOT, n, P->R, P->RP, &st->rho, nullptr, nullptr));
+    k_tfq_init<<<1, 1, 0, s>>>(st, P->hist, rtol, atol);
+    RVK_CHECK_LAUNCH("k_tfq_init");
+    k_tfq_copy<<<cg, 256, 0, s>>>(n, P->R, P->U, g);
+    k_tfq_copy<<<cg, 256, 0, s>>>(n, P->R, P->P, g);
+    RVK_TRY(apply_BA(P, P->P, P->V, g));
+    RVK_CUDA(cudaMemsetAsync(P->D, 0, n * 8, s));
+
+    for (int it = 0; it < P->cfg.max_it; ++it) {
+        RVK_TRY(vec_reduce(s, sc, RED_DOT, n, P->V, P->RP, &st->s, nullptr, g));        // s = (v, rp)
+        k_tfq_alpha<<<1, 1, 0, s>>>(st, it);                                              // a = rho/s
+        RVK_TRY(vec_ew(s, EW_WAXPY, n, sptr(&st->a, RVK_SCALAR_NEG_PTR), P->V, P->U, P->Q, g)); // q = u - a v
+        RVK_TRY(vec_ew(s, EW_WAXPY, n, const_scalar(1.0), P->U, P->Q, P->T, g));          // t = u + q
+        RVK_TRY(apply_BA(P, P->T, P->AUQ, g));                                            // B A t
+        RVK_TRY(vec_ew(s, EW_AXPY, n, sptr(&st->a, RVK_SCALAR_NEG_PTR), P->AUQ, P->R, P->R, g)); // r -= a BAt
+        RVK_TRY(vec_reduce(s, sc, RED_NRM2, n, P->R, nullptr, &st->dp, nullptr, g));      // dp = ||r||
+        for (int m = 0; m < 2; ++m) {
+            k_tfq_half<<<1, 1, 0, s>>>(st, m);
+            RVK_TRY(vec_ew(s, EW_AYPX, n, sptr(&st->cf), m == 0 ? P->U : P->Q, P->D, P->D, g)); // d = (u|q) + cf d
+            RVK_TRY(vec_ew(s, EW_AXPY, n, sptr(&st->eta), P->D, x, x, g));                      // x += eta d
+            k_tfq_post<<<1, 1, 0, s>>>(st, P->hist, m, it, rtol, atol);
+        }
+        RVK_TRY(vec_reduce(s, sc, RED_DOT, n, P->R, P->RP, &st->rho, nullptr, g));      // rho = (r, rp)
+        k_tfq_beta<<<1, 1, 0, s>>>(st, it);                                               // b = rho/rho_old
+        RVK_TRY(vec_ew(s, EW_WAXPY, n, sptr(&st->b), P->Q, P->R, P->U, g));             // u = r + b q
+        RVK_TRY(vec_ew(s, EW_AXPY, n, sptr(&st->b), P->P, P->Q, P->Q, g));              // q += b p
+        RVK_TRY(vec_ew(s, EW_WAXPY, n, sptr(&st->b), P->Q, P->U, P->P, g));             // p = u + b q
+        RVK_TRY(apply_BA(P, P->P, P->V, g));                                              // v = B A p
+        k_tfq_shift<<<1, 1, 0, s>>>(st);
+        RVK_CHECK_LAUNCH("tfqmr iteration");
+    }
+    return RVK_OK;
+}
+
+} // namespace
+
+extern "C" {
+
+rvk_status rvk_tfqmr_plan_create(rvk_ctx ctx, const rvk_csr* A, rvk_cg_config cfg,
+                                 rvk_tfqmr_plan* out)
+{
+    if (!ctx || !A || !out) return set_error(RVK_ERR_INVALID, "tfqmr_plan_create: null argument");
+    *out = nullptr;
+    if (A->n_rows != A->n_cols) return set_error(RVK_ERR_DIM, "tfqmr_solve: matrix is not square");
+    if (A->n_rows < 1) return set_error(RVK_ERR_DIM, "tfqmr_solve: empty system");
+    if (cfg.max_it < 1) return set_error(RVK_ERR_INVALID, "tfqmr_solve: max_it must be >= 1");
+    if (cfg.pc != RVK_PC_NONE && cfg.pc != RVK_PC_JACOBI)
+        return set_error(RVK_ERR_INVALID, "tfqmr_solve: unknown preconditioner %d", cfg.pc);
+    int64_t maxlen = 0;
+    RVK_TRY(rvk_csr_validate(ctx, A, &maxlen));
+    auto P = new rvk_tfqmr_plan_s();
+    P->ctx = ctx;
+    P->A   = *A;
+    P->cfg = cfg;
+    SpmvWindows win;
+    if (csr_windows(ctx->stream, *A, &win) != RVK_OK) win = SpmvWindows{};
+    win.n = 0; // leading-edge prefetch only
+    P->sa = make_spmv_args(*A, maxlen, &win, 1);
+    const size_t vb = (size_t)A->n_rows * 8;
+    cudaError_t  e  = cudaSuccess;
+    auto alloc = [&](double** p, size_t bytes) {
+        if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(p), bytes);
+    };
+    for (double** v : {&P->R, &P->RP, &P->U, &P->P, &P->V, &P->D, &P->Q, &P->T, &P->AUQ, &P->T1,
+                       &P->dinv})
+        alloc(v, vb + 32);
+    alloc(&P->hist, 8 * (2 * (size_t)cfg.max_it + 1));
+    alloc(&P->partials, 8 * 4 * (size_t)kMaxReduceBlocks);
+    if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&P->st), sizeof(TfqState));
+    if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&P->tickets), 64);
+    if (e == cudaSuccess) e = cudaMemsetAsync(P->tickets, 0, 64, ctx->stream);
+    if (e == cudaSuccess) e = cudaMemsetAsync(P->st, 0, sizeof(TfqState), ctx->stream);
+    if (e != cudaSuccess) {
+        rvk_tfqmr_plan_destroy(P);
+        return cuda_error(e, "rvk_tfqmr_plan_create");
+    }
+    rvk_status rc = cfg.pc == RVK_PC_JACOBI ? rvk_csr_diagonal_inverse(ctx, A, P->dinv) : RVK_OK;
+    if (rc != RVK_OK) {
+        rvk_tfqmr_plan_destroy(P);
+        return rc;
+    }
+    *out = P;
+    return RVK_OK;
+}
+
+rvk_status rvk_tfqmr_plan_destroy(rvk_tfqmr_plan P)
+{
+    if (!P) return RVK_OK;
+    if (P->ctx) cudaStreamSynchronize(P->ctx->stream);
+    if (P->graph) cudaGraphExecDestroy(P->graph);
+    void* bufs[] = {P->R, P->RP, P->U, P->P, P->V, P->D, P->Q, P->T, P->AUQ, P->T1, P->dinv,
+                    P->hist, P->st, P->partials, P->tickets};
+    for (void* q : bufs)
+        if (q) cudaFree(q);
+    delete P;
+    return RVK_OK;
+}
+
+rvk_status rvk_tfqmr_solve_dev(rvk_tfqmr_plan P, const double* b, double* x)
+{
+    if (!P || !b || !x) return set_error(RVK_ERR_INVALID, "tfqmr_solve: null argument");
+    if (b == x) return set_error(RVK_ERR_INVALID, "tfqmr_solve: b and x must not alias");
+    cudaStream_t s = P->ctx->stream;
+    if (!P->cfg.use_graph) return enqueue_tfqmr(P, b, x);
+    if (!P->graph || P->g_b != b || P->g_x != x) {
+        if (P->graph) cudaGraphExecDestroy(P->graph);
+        P->graph      = nullptr;
+        cudaGraph_t g = nullptr;
+        RVK_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeGlobal)); // proves 0 host syncs
+        rvk_status  rc = enqueue_tfqmr(P, b, x);
+        cudaError_t e  = cudaStreamEndCapture(s, &g);
+        if (rc != RVK_OK) {
+            if (g) cudaGraphDestroy(g);
+            return rc;
+        }
+        if (e != cudaSuccess) return cuda_error(e, "cudaStreamEndCapture (tfqmr)");
+        e = cudaGraphInstantiate(&P->graph, g, 0);
+        cudaGraphDestroy(g);
+        if (e != cudaSuccess) return cuda_error(e, "cudaGraphInstantiate (tfqmr)");
+        P->g_b = b;
+        P->g_x = x;
+    }
+    RVK_CUDA(cudaGraphLaunch(P->graph, s));
+    return RVK_OK;
+}
+
+rvk_status rvk_tfqmr_result(rvk_tfqmr_plan P, double* hist_host, int* n_hist, rvk_cg_info* info)
+{
+    if (!P) return set_error(RVK_ERR_INVALID, "null plan");
+    TfqState     h{};
+    cudaStream_t s = P->ctx->stream;
+    RVK_CUDA(cudaMemcpyAsync(&h, P->st, sizeof h, cudaMemcpyDeviceToHost, s));
+    if (hist_host)
+        RVK_CUDA(cudaMemcpyAsync(hist_host, P->hist, 8 * (2 * (size_t)P->cfg.max_it + 1),
+                                 cudaMemcpyDeviceToHost, s));
+    note_host_sync();
+    RVK_CUDA(cudaStreamSynchronize(s));
+    if (n_hist) *n_hist = h.nhist;
+    if (info) {
+        info->state          = h.state;
+        info->iterations     = h.iterations;
+        info->breakdown_iter = h.breakdown_iter;
+    }
+    if (h.state == RVK_CG_BREAKDOWN)
+        return set_error(RVK_ERR_BREAKDOWN, "tfqmr_solve: breakdown at iteration %d", h.breakdown_iter);
+    return RVK_OK;
+}
+
+} // extern "C"

@@ -41,7 +41,8 @@ EXPORTS = [
     "rvk_cg_set_profiling", "rvk_cg_kernel_times", "rvk_cg_plan_mode",
     "rvk_laplacian_rows_nnz", "rvk_build_laplacian_rows", "rvk_comm_unique_id", "rvk_comm_init",
     "rvk_comm_destroy", "rvk_dcg_plan_create", "rvk_dcg_plan_destroy", "rvk_dcg_solve_dev",
-    "rvk_dcg_loopback_solve", "rvk_dcg_result",
+    "rvk_dcg_loopback_solve", "rvk_dcg_result", "rvk_tfqmr_plan_create",
+    "rvk_tfqmr_plan_destroy", "rvk_tfqmr_solve_dev", "rvk_tfqmr_result",
 ]
 
 
@@ -154,6 +155,10 @@ def lib():
         "rvk_dcg_solve_dev": (i, [vp, vp, vp]),
         "rvk_dcg_loopback_solve": (i, [C.POINTER(vp), i, C.POINTER(vp), C.POINTER(vp)]),
         "rvk_dcg_result": (i, [vp, vp, C.POINTER(CgInfo)]),
+        "rvk_tfqmr_plan_create": (i, [vp, C.POINTER(Csr), CgConfig, C.POINTER(vp)]),
+        "rvk_tfqmr_plan_destroy": (i, [vp]),
+        "rvk_tfqmr_solve_dev": (i, [vp, vp, vp]),
+        "rvk_tfqmr_result": (i, [vp, vp, C.POINTER(C.c_int), C.POINTER(CgInfo)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -398,3 +403,44 @@ class CgPlan:
         n = C.c_int()
         lib().rvk_cg_kernel_times(self.h, None, None, C.byref(n))
         return n.value
+
+
+class TfqmrPlan:
+    """KSPSetUp + KSPSolve for left-Jacobi TFQMR (rvk_tfqmr_plan_*).
+    result().hist = ||B r0|| then one quasi-residual estimate per half step."""
+
+    def __init__(self, ctx: Ctx, A: DeviceCsr, max_it: int = 20, pc: str = "jacobi",
+                 rtol: float = 0.0, atol: float = 0.0, use_graph: bool = True):
+        self.ctx, self.A, self.max_it = ctx, A, max_it
+        cfg = CgConfig(max_it, PC_JACOBI if pc == "jacobi" else PC_NONE, rtol, atol,
+                       MODE_FUSED, 1 if use_graph else 0)
+        h = C.c_void_p()
+        check(lib().rvk_tfqmr_plan_create(ctx.h, C.byref(A.c), cfg, C.byref(h)))
+        self.h = h
+        ctx._deps.add(self)
+
+    def close(self):
+        if self.h:
+            lib().rvk_tfqmr_plan_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def solve_dev(self, b: DeviceArray, x: DeviceArray):
+        check(lib().rvk_tfqmr_solve_dev(self.h, b.ptr, x.ptr))
+
+    def result(self, raise_breakdown: bool = True) -> CgResult:
+        hist = np.full(2 * self.max_it + 1, np.nan)
+        info, nh = CgInfo(), C.c_int()
+        st = lib().rvk_tfqmr_result(self.h, _ptr(hist), C.byref(nh), C.byref(info))
+        res = CgResult(hist[: nh.value].copy(), info.state, info.iterations, info.breakdown_iter)
+        if st == RVK_ERR_BREAKDOWN:
+            if raise_breakdown:
+                raise BreakdownError(st, lib().rvk_last_error().decode(), info.breakdown_iter)
+            return res
+        check(st)
+        return res

@@ -363,6 +363,60 @@ int main()
         cg_solve(A, b, x, c);
         EXPECT(runtime::host_syncs() - s1 >= 20); // reading dp syncs every iteration
     });
+    // ---- TFQMR -----------------------------------------------------------------
+    run("tfqmr_solve vs oracle (5-pt 32x32, 1e-8) + census", [] {
+        auto h = oracle_laplacian(2, 5, 32, 32, 1);
+        std::vector<double> bh(h.n), xo(h.n), hist(41), work(11 * h.n);
+        ro_rhs(0x9E3779B97F4A7C15ull, (int64_t)h.n, bh.data());
+        ro_cg_config cfg{20, RO_PC_JACOBI, 0.0, 0.0};
+        int          nh = 0;
+        ro_cg_result rr = ro_tfqmr_solve((int64_t)h.n, h.off.data(), h.cols.data(), h.vals.data(),
+                                         bh.data(), xo.data(), hist.data(), cfg, work.data(), &nh);
+        EXPECT(rr.iterations == 20 && nh == 41);
+        CsrMatrix   A(h.n, h.n, h.off, h.cols, h.vals);
+        DenseVector b(bh), x(h.n);
+        const auto  census0 = runtime::census();
+        auto        res     = tfqmr_solve(A, b, x, SolverConfig{});
+        const auto  d       = runtime::census() - census0;
+        EXPECT(res.iterations == 20 && res.history.size() == 41);
+        for (int k = 0; k < 41 && k < (int)res.history.size(); ++k)
+            if (!(rel(res.history[k], hist[k]) < 1e-8)) {
+                std::printf("  k %d got %.17g want %.17g\n", k, res.history[k], hist[k]);
+                EXPECT(false);
+            }
+        auto   xh  = x.to_host();
+        double num = 0, den = 0;
+        for (std::size_t i = 0; i < h.n; ++i) {
+            num += (xh[i] - xo[i]) * (xh[i] - xo[i]);
+            den += xo[i] * xo[i];
+        }
+        EXPECT(std::sqrt(num / den) < 1e-8);
+        // exactly 2 matmults per iteration (+1 in setup:
+        // v = B A p), reductions >= 2x... the PETSc loop has 3 per iteration
+        EXPECT(d.kernels_of(runtime::KernelKind::MatMult) == 1 + 2 * 20);
+        EXPECT(d.reductions() == 2 + 3 * 20);
+    });
+    run("tfqmr identity converges in the first half step; breakdown reported", [] {
+        auto        I = CsrMatrix::identity(100);
+        std::vector<double> bh(100);
+        ro_rhs(3, 100, bh.data());
+        DenseVector  b(bh), x(100);
+        SolverConfig c;
+        c.pc   = PcType::None;
+        auto r = tfqmr_solve(I, b, x, c);
+        EXPECT(r.converged && r.iterations == 1 && r.history.size() == 2);
+        auto xh = x.to_host();
+        for (int i = 0; i < 100; ++i) EXPECT(xh[i] == bh[i]);
+        CsrMatrix   S(2, 2, {0, 1, 2}, {1, 0}, {1.0, 1.0}); // (A b, b) = 0 for b = e0
+        DenseVector b2(std::vector<double>{1, 0}), x2(2);
+        bool        got = false;
+        try {
+            tfqmr_solve(S, b2, x2, c);
+        } catch (const BreakdownError& e) {
+            got = e.iteration() == 0;
+        }
+        EXPECT(got);
+    });
     std::printf("%s: %d failure(s)\n", g_fail ? "FAILED" : "OK", g_fail);
     return g_fail ? 1 : 0;
 }

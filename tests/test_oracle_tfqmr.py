@@ -1,0 +1,185 @@
+"""CPU tests: pin the TFQMR restatement (oracle/rvk_oracle.c:ro_tfqmr_solve).
+
+The reference ships no TFQMR source (SPEC.md:467-475,
+:501 fix only "the standard Freund single-loop formulation with two
+half-iterations fused per outer iteration").  So the restatement is pinned
+by (1) an independent pure-Python transcription of the same recurrence,
+element-for-element, on small systems; (2) the SPEC known answers (A = I
+exact in the first iteration, breakdown with iteration index); (3) the
+method's defining properties: the history is a residual BOUND
+(||B(b - A x_k)|| <= sqrt(k+1) tau_k) and the solve converges on a
+non-symmetric system, TFQMR's raison d'etre.
+Parity vs the reference itself stays unpinned for TFQMR.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle as O
+
+
+def _dense(A):
+    M = np.zeros((A.n_rows, A.n_cols))
+    for r in range(A.n_rows):
+        for k in range(A.off[r], A.off[r + 1]):
+            M[r, A.cols[k]] = A.vals[k]
+    return M
+
+
+def _spmv(A, x):
+    y = np.zeros(A.n_rows)
+    for r in range(A.n_rows):
+        s = 0.0
+        for k in range(A.off[r], A.off[r + 1]):
+            s = s + A.vals[k] * x[A.cols[k]]
+        y[r] = s
+    return y
+
+
+def _dot(x, y):
+    s = 0.0
+    for a, b in zip(x, y):
+        s = s + a * b
+    return s
+
+
+def py_tfqmr(A, b, max_it, pc="jacobi", rtol=0.0, atol=0.0):
+    """Independent transcription (PETSc KSPSolve_TFQMR order, scalar loops)."""
+    n = A.n_rows
+    d = O.diagonal(A)
+    dinv = np.array([1.0 / v for v in d]) if pc == "jacobi" else None
+
+    def BA(v):
+        w = _spmv(A, v)
+        return np.array([dinv[i] * w[i] for i in range(n)]) if dinv is not None else w
+
+    x = np.zeros(n)
+    R = np.array([dinv[i] * b[i] for i in range(n)]) if dinv is not None else b.copy()
+    dp = math.sqrt(_dot(R, R))
+    hist = [dp]
+    dp0 = dp
+    conv = lambda v: v <= max(rtol * dp0, atol)
+    if conv(dp):
+        return x, hist, 1, 0
+    RP = R.copy()
+    etaold = psiold = 0.0
+    tau = dpold = dp
+    rhoold = _dot(R, RP)
+    U, P = R.copy(), R.copy()
+    V = BA(P)
+    D = np.zeros(n)
+    for i in range(max_it):
+        s = _dot(V, RP)
+        if s == 0.0:
+            return x, hist, 2, i
+        a = rhoold / s
+        Q = np.array([-a * V[k] + U[k] for k in range(n)])
+        T = np.array([1.0 * U[k] + Q[k] for k in range(n)])
+        AUQ = BA(T)
+        R = np.array([R[k] + (-a) * AUQ[k] for k in range(n)])
+        dp = math.sqrt(_dot(R, R))
+        for m in range(2):
+            w = math.sqrt(dp * dpold) if m == 0 else dp
+            psi = w / tau
+            cm = 1.0 / math.sqrt(1.0 + psi * psi)
+            tau = tau * psi * cm
+            eta = cm * cm * a
+            cf = psiold * psiold * etaold / a
+            src = U if m == 0 else Q
+            D = np.array([src[k] + cf * D[k] for k in range(n)])
+            x = np.array([x[k] + eta * D[k] for k in range(n)])
+            dpest = math.sqrt(2.0 * i + m + 2.0) * tau
+            hist.append(dpest)
+            if conv(dpest):
+                return x, hist, 1, i + 1
+            etaold, psiold = eta, psi
+        rho = _dot(R, RP)
+        if rhoold == 0.0:
+            return x, hist, 2, i
+        bb = rho / rhoold
+        U = np.array([bb * Q[k] + R[k] for k in range(n)])
+        Q = np.array([Q[k] + bb * P[k] for k in range(n)])
+        P = np.array([bb * Q[k] + U[k] for k in range(n)])
+        V = BA(P)
+        rhoold, dpold = rho, dp
+    return x, hist, 0, max_it
+
+
+@pytest.mark.parametrize("spec", [(2, 5, (7, 5)), (2, 9, (6, 6)), (3, 7, (4, 3, 3)), (3, 27, (3, 3, 3))])
+@pytest.mark.parametrize("pc", ["jacobi", "none"])
+def test_restatement_matches_independent_transcription(spec, pc):
+    dim, pts, g = spec
+    A = O.build_laplacian(dim, pts, g)
+    b = O.rhs(A.n_rows)
+    r = O.tfqmr_solve(A, b, max_it=6, pc=pc)
+    x, hist, status, its = py_tfqmr(A, b, 6, pc)
+    assert (r.status, r.iterations) == (status, its)
+    # identical operation order: the dots are the same left-to-right chain
+    assert np.array_equal(r.hist, np.array(hist))
+    assert np.array_equal(r.x, x)
+
+
+def test_identity_exact_first_iteration():
+    n = 50
+    I = O.Csr(n, n, np.arange(n + 1, dtype=np.int64), np.arange(n, dtype=np.int32), np.ones(n))
+    b = O.rhs(n)
+    r = O.tfqmr_solve(I, b, pc="none")
+    assert r.status == 1 and r.iterations == 1 and r.hist.size == 2 and r.hist[1] == 0.0
+    assert np.array_equal(r.x, b)
+
+
+def test_breakdown_reported_with_iteration():
+    A = O.Csr(2, 2, np.array([0, 1, 2], np.int64), np.array([1, 0], np.int32), np.array([1.0, 1.0]))
+    r = O.tfqmr_solve(A, np.array([1.0, 0.0]), pc="none")
+    assert r.status == 2 and r.breakdown_iter == 0
+
+
+@pytest.mark.parametrize("spec", [(2, 5, (32, 32)), (3, 27, (8, 8, 8))])
+def test_history_bounds_true_residual(spec):
+    dim, pts, g = spec
+    A = O.build_laplacian(dim, pts, g)
+    b = O.rhs(A.n_rows)
+    dinv = 1.0 / O.diagonal(A)
+    for its in (1, 3, 10, 20):
+        r = O.tfqmr_solve(A, b, max_it=its)
+        true = np.linalg.norm(dinv * (b - O.spmv(A, r.x)))
+        # rounding floor: once the bound nears eps*||r0|| the true residual stalls
+        assert true <= r.hist[-1] * (1 + 1e-10) + 1e-13 * r.hist[0], (its, true, r.hist[-1])
+
+
+def test_converges_on_nonsymmetric_system():
+    """Upwind convection-diffusion (non-symmetric): TFQMR still converges."""
+    nx = 20
+    n = nx * nx
+    rows, cols, vals = [], [], []
+    off = [0]
+    for i in range(n):
+        x, y = i % nx, i // nx
+        ent = {i: 4.0 + 0.8}
+        if x > 0: ent[i - 1] = -1.0 - 0.8
+        if x < nx - 1: ent[i + 1] = -1.0
+        if y > 0: ent[i - nx] = -1.0
+        if y < nx - 1: ent[i + nx] = -1.0
+        for c in sorted(ent):
+            cols.append(c)
+            vals.append(ent[c])
+        off.append(len(cols))
+    A = O.Csr(n, n, np.array(off, np.int64), np.array(cols, np.int32), np.array(vals))
+    M = _dense(A)
+    assert not np.allclose(M, M.T)
+    b = O.rhs(n)
+    r = O.tfqmr_solve(A, b, max_it=300, rtol=1e-10)
+    assert r.status == 1
+    xs = np.linalg.solve(M, b)
+    assert np.linalg.norm(r.x - xs) / np.linalg.norm(xs) < 1e-7
+
+
+def test_rtol_exit_is_prefix_of_full_run():
+    A = O.build_laplacian(2, 5, (16, 16))
+    b = O.rhs(A.n_rows)
+    full = O.tfqmr_solve(A, b, max_it=200)
+    r = O.tfqmr_solve(A, b, max_it=200, rtol=1e-6)
+    assert r.status == 1
+    assert np.array_equal(r.hist, full.hist[: r.hist.size])
+    assert r.hist[-1] <= 1e-6 * r.hist[0] < r.hist[-2]
