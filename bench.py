@@ -203,6 +203,121 @@ def run_reference(args, cfg):
     print(json.dumps(out), flush=True)
 
 
+def tfqmr_bytes(n: int, nnz: int):
+    """Algorithmic HBM bytes of the fused TFQMR solve (rvk_tfqmr.cu header):
+    KA = CSR + 7n doubles, KM = 11n (6n in the last iteration), KB = CSR + 4n;
+    setup K0 = 8n, plus one KB; no KB after the last iteration."""
+    csr = 12 * nnz + 8 * (n + 1)
+    ka, km, km_last, kb, k0 = csr + 56 * n, 88 * n, 48 * n, csr + 32 * n, 64 * n
+    solve = k0 + kb + MAX_IT * ka + (MAX_IT - 1) * (km + kb) + km_last
+    return {"ka": ka, "km": km, "kb": kb, "b_min_solve": solve}
+
+
+def run_tfqmr(args, cfg):
+    """--solver tfqmr: the 20-iteration left-Jacobi TFQMR solve (SURVEY.md 8f
+    row 3), same workload, timing rules and JSON shape."""
+    import torch
+    from paper_2306_17801_b200 import rvk
+
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        raise SystemExit("--solver tfqmr is single-GPU (replicas only)")
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dim, pts, grid, desc = cfg
+    stream = torch.cuda.Stream()
+    ctx = rvk.Ctx(stream.cuda_stream)
+    A = rvk.DeviceCsr.laplacian(ctx, dim, pts, grid)
+    n, nnz = A.n_rows, A.nnz
+    b, x = rvk.DeviceArray(n), rvk.DeviceArray(n)
+    rvk.check(rvk.lib().rvk_fill_rhs(ctx.h, 0x9E3779B97F4A7C15, n, b.ptr))
+    mode = "unfused" if args.mode == "unfused" else "fused"
+    plan = rvk.TfqmrPlan(ctx, A, max_it=MAX_IT, use_graph=not args.no_graph, mode=mode)
+    bm = tfqmr_bytes(n, nnz)
+    hbm_peak, peak_src = peaks()
+    ws_bytes = 20 * nnz + 8 * (n + 1) + 11 * 8 * n
+    for _ in range(args.warmup):
+        plan.solve_dev(b, x)
+    res = plan.result()
+    assert res.iterations == MAX_IT, res
+    flush = None
+    if ws_bytes < 2 * L2_BYTES:
+        flush = torch.empty(512 * 2 ** 20, dtype=torch.uint8, device=f"cuda:{local}")
+    syncs0 = rvk.host_syncs()
+    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        with torch.cuda.stream(stream):
+            for k in range(args.steps):
+                if flush is not None:
+                    flush.fill_(k & 0xFF)
+                ev0[k].record(stream)
+                plan.solve_dev(b, x)
+                ev1[k].record(stream)
+        stream.synchronize()
+    syncs = rvk.host_syncs() - syncs0
+    step_ms = [ev0[k].elapsed_time(ev1[k]) for k in range(args.steps)]
+    ms = sum(step_ms) / args.steps
+    res = plan.result()
+    solve_gbs = bm["b_min_solve"] / (ms * 1e-3) / 1e9
+    launches = (2 + MAX_IT * 3 - 1) if mode == "fused" else None
+    # e2e: pinned host b -> device, solve, x + history back
+    bh = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    xh = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    bh.numpy()[:] = b.download(ctx)
+    L = rvk.lib()
+
+    def e2e_once():
+        rvk.check(L.rvk_memcpy_h2d(ctx.h, b.ptr, bh.data_ptr(), 8 * n))
+        plan.solve_dev(b, x)
+        rvk.check(L.rvk_memcpy_d2h(ctx.h, xh.data_ptr(), x.ptr, 8 * n))
+        plan.result()
+
+    for _ in range(max(1, args.warmup)):
+        e2e_once()
+    e2e = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        e2e_once()
+        e2e.append((time.perf_counter() - t0) * 1e3)
+    e2e_ms = statistics.mean(e2e)
+    cpu = None
+    if not args.no_cpu_baseline:
+        import oracle as O
+        Ah = O.build_laplacian(dim, pts, grid)
+        bb = O.rhs(Ah.n_rows)
+        t0 = time.perf_counter()
+        O.tfqmr_solve(Ah, bb, max_it=MAX_IT)
+        cpu = {"value": round((time.perf_counter() - t0) * 1e3, 1), "unit": "ms/solve", "cores": 1,
+               "kind": "port",
+               "sample": f"1 full {MAX_IT}-iteration TFQMR solve of {desc} (oracle restatement; "
+                         "the reference ships no TFQMR source)"}
+    out = {
+        "metric": f"20-iter Jacobi-TFQMR solve time, achieved HBM GB/s vs peak, host syncs/iter",
+        "value": round(ms, 4), "unit": "ms/solve", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms, 4), "min_ms": round(min(step_ms), 4),
+        "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": f"{desc}, left-Jacobi TFQMR {MAX_IT} iterations, x0=0, splitmix64 RHS",
+                   "n": n, "nnz": nnz, "mode": mode, "graph": not args.no_graph,
+                   "l2": "no flush: working set >> L2" if flush is None else "L2 flushed between steps"},
+        "solve_roofline": {"bound": "hbm", "alg_bytes_per_solve": bm["b_min_solve"],
+                           "achieved": round(solve_gbs, 1), "peak": hbm_peak, "unit": "GB/s",
+                           "frac": round(solve_gbs / hbm_peak, 4), "peak_source": peak_src},
+        "host_syncs_per_iter": syncs / (args.steps * MAX_IT),
+        "e2e": {"value": round(e2e_ms, 4), "unit": "ms/solve", "h2d_bytes_per_step": 8 * n,
+                "d2h_bytes_per_step": 8 * n + 8 * (2 * MAX_IT + 1) + 64},
+        "gpu_launches": launches * args.steps if launches else None,
+        "cpu_baseline": cpu,
+        "clocks": clk.summary(),
+    }
+    log(f"tfqmr {mode}: solve {ms:.3f} ms (min {min(step_ms):.3f}); {solve_gbs:.0f} GB/s "
+        f"({solve_gbs/hbm_peak:.1%}); e2e {e2e_ms:.2f} ms; syncs {syncs}")
+    print(json.dumps(out), flush=True)
+    plan.close()
+    ctx.close()
+
+
 def run_gpu(args, cfg):
     import torch
     from paper_2306_17801_b200 import rvk
@@ -380,6 +495,8 @@ def main():
                     help="csr: the AIJ/CSR operator (headline); stencil: matrix-free (SURVEY 8f)")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--solver", choices=["cg", "tfqmr"], default="cg",
+                    help="cg: the headline Jacobi-PCG; tfqmr: left-Jacobi TFQMR (SURVEY 8f)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "rvk":
         log("note: raising --warmup to 3 (timing rule)")
@@ -387,6 +504,8 @@ def main():
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         run_reference(args, cfg)
+    elif args.solver == "tfqmr":
+        run_tfqmr(args, cfg)
     else:
         run_gpu(args, cfg)
 

@@ -40,6 +40,8 @@
 
 #include "rvk_common.cuh"
 
+#include <type_traits>
+
 namespace rvk {
 
 constexpr int    kSpmvConsumerWarps = 16;
@@ -49,7 +51,7 @@ constexpr int    kSpmvMaxStages     = 4;
 constexpr int    kSpmvUnroll        = 8;                   // nonzeros per lane per batch
 constexpr int    kSpmvMaxWin        = 4;                   // x-windows per tile
 constexpr int    kSpmvMaxSrc        = 2;                   // gathered vectors per column
-constexpr size_t kSpmvHeaderBytes   = 1024;                // barriers, meta, reduction scratch
+constexpr size_t kSpmvHeaderBytes   = 2048;                // barriers, meta, reduction scratch
 constexpr size_t kSpmvStageBudget   = 200 * 1024;          // dynamic smem for the ring
 
 struct SpmvStageMeta {
@@ -175,18 +177,34 @@ inline SpmvArgs make_spmv_args(const rvk_csr& A, int64_t max_row_len,
     return a;
 }
 
+// Epilogue operands of row i, loaded before the row's gathers so their
+// latency hides under the products: Op::own(i) when the op declares an `Own`
+// type (row-owned vectors the epilogue reads), else the op's gathered
+// operands at its own column.
+template <class Op, class = void>
+struct spmv_has_own : std::false_type {};
+template <class Op>
+struct spmv_has_own<Op, std::void_t<typename Op::Own>> : std::true_type {};
+
+template <class Op, class G>
+__device__ __forceinline__ auto spmv_own(const Op& op, int64_t i, const G& gather)
+{
+    if constexpr (spmv_has_own<Op>::value) return op.own(i);
+    else return gather(op.own_col(i));
+}
+
 // ---------------------------------------------------------------------------
 // Direct tiles: thread-per-row straight from global memory (rare path).
 // ---------------------------------------------------------------------------
-template <class Op>
-__device__ __forceinline__ double spmv_rows_direct(const Op& op, double acc, int gtid, int gsize,
+template <class Op, class Acc>
+__device__ __forceinline__ Acc spmv_rows_direct(const Op& op, Acc acc, int gtid, int gsize,
                                                    int rows, int64_t r0,
                                                    const int64_t* __restrict__ O,
                                                    const int32_t* __restrict__ Cc,
                                                    const double* __restrict__ V)
 {
     for (int lr = gtid; lr < rows; lr += gsize) {
-        const auto    own = op.fetch(op.own_col(r0 + lr));
+        const auto    own = spmv_own(op, r0 + lr, [&](int64_t c) { return op.fetch((int32_t)c); });
         const int64_t kb = O[lr], ke = O[lr + 1];
         double        sum = 0.0;
         for (int64_t k = kb; k < ke; k += kSpmvUnroll) {
@@ -245,8 +263,8 @@ __device__ __forceinline__ int window_index(const StageWindows& W, int64_t c)
 // Stage-local 32-bit indices keep the address arithmetic cheap.  WIN: the
 // gathers read the stage's x-windows (LDS) instead of global memory.
 // ---------------------------------------------------------------------------
-template <bool WIN, class Op>
-__device__ __forceinline__ double spmv_rows_staged(const Op& op, double acc, int gtid, int gsize,
+template <bool WIN, class Op, class Acc>
+__device__ __forceinline__ Acc spmv_rows_staged(const Op& op, Acc acc, int gtid, int gsize,
                                                    int rows, int64_t r0, const int64_t* O,
                                                    int64_t kv0, const int32_t* Cc,
                                                    const double* V, const StageWindows& W)
@@ -256,7 +274,7 @@ __device__ __forceinline__ double spmv_rows_staged(const Op& op, double acc, int
         else return op.fetch((int32_t)c);
     };
     for (int lr = gtid; lr < rows; lr += gsize) {
-        const auto own = gather(op.own_col(r0 + lr)); // epilogue operand, in flight early
+        const auto own = spmv_own(op, r0 + lr, gather); // epilogue operands, in flight early
         const int  kb  = (int)(O[lr] - kv0);
         const int  ke  = (int)(O[lr + 1] - kv0);
         double     sum = 0.0;
@@ -285,6 +303,24 @@ __device__ __forceinline__ double spmv_rows_staged(const Op& op, double acc, int
     return acc;
 }
 
+// Number of fused reductions an op accumulates (Op::kSums, default 1): the
+// row() accumulator is a double, or SumVec<N> for N > 1, and tail() receives
+// the folded sums (double, or const double (&)[N]).
+template <int N>
+struct SumVec {
+    double v[N];
+};
+template <class Op, class = void>
+struct spmv_sums {
+    static constexpr int value = 1;
+};
+template <class Op>
+struct spmv_sums<Op, std::void_t<decltype(Op::kSums)>> {
+    static constexpr int value = Op::kSums;
+};
+template <class Op>
+using spmv_acc_t = std::conditional_t<spmv_sums<Op>::value == 1, double, SumVec<spmv_sums<Op>::value>>;
+
 template <class Op>
 __global__ void __launch_bounds__(kSpmvThreads, 1) k_spmv_tma(SpmvArgs A, Op op_in, TailArgs tail)
 {
@@ -292,8 +328,8 @@ __global__ void __launch_bounds__(kSpmvThreads, 1) k_spmv_tma(SpmvArgs A, Op op_
     uint64_t*      full   = reinterpret_cast<uint64_t*>(smem_raw);
     uint64_t*      empty  = full + kSpmvMaxStages;
     SpmvStageMeta* meta   = reinterpret_cast<SpmvStageMeta*>(smem_raw + 128);
-    double*        red    = reinterpret_cast<double*>(smem_raw + 512); // 32 doubles
-    int*           flag   = reinterpret_cast<int*>(smem_raw + 512 + 256);
+    double*        red    = reinterpret_cast<double*>(smem_raw + 512); // 32 doubles per sum (<= 4)
+    int*           flag   = reinterpret_cast<int*>(smem_raw + 512 + 1024);
     unsigned char* stage0 = smem_raw + kSpmvHeaderBytes;
 
     Op op = op_in;
@@ -401,7 +437,9 @@ __global__ void __launch_bounds__(kSpmvThreads, 1) k_spmv_tma(SpmvArgs A, Op op_
     const int ctid  = tid - 32;
     const int gs    = kSpmvConsumers / A.groups;
     const int group = ctid / gs, gtid = ctid % gs;
-    double    acc   = 0.0;
+    constexpr int NS = spmv_sums<Op>::value;
+    static_assert(NS >= 1 && NS <= 4, "at most 4 fused reductions");
+    spmv_acc_t<Op> acc{};
     int64_t   t     = blockIdx.x + (int64_t)group * gridDim.x;
     for (int j = group; t < A.n_tiles; j += A.groups, t += (int64_t)A.groups * gridDim.x) {
         const int s = j % A.stages;
@@ -439,13 +477,22 @@ __global__ void __launch_bounds__(kSpmvThreads, 1) k_spmv_tma(SpmvArgs A, Op op_
     }
 
     if constexpr (Op::kHasTail) {
-        double v[1] = {acc};
-        block_sum<1>(v, red, ctid, kSpmvConsumers, 1);
-        if (ctid == 0) tail.partials[blockIdx.x] = v[0];
-        if (!last_block(tail.ticket, ctid, flag, kSpmvConsumers, 1)) return;
-        fold_partials<1>(tail.partials, gridDim.x, v, red, ctid, kSpmvConsumers, 1);
+        double v[NS];
+        if constexpr (NS == 1) v[0] = acc;
+        else {
+#pragma unroll
+            for (int j = 0; j < NS; ++j) v[j] = acc.v[j];
+        }
+        block_sum<NS>(v, red, ctid, kSpmvConsumers, 1);
         if (ctid == 0) {
-            op.tail(v[0]);
+#pragma unroll
+            for (int j = 0; j < NS; ++j) tail.partials[(size_t)blockIdx.x * NS + j] = v[j];
+        }
+        if (!last_block(tail.ticket, ctid, flag, kSpmvConsumers, 1)) return;
+        fold_partials<NS>(tail.partials, gridDim.x, v, red, ctid, kSpmvConsumers, 1);
+        if (ctid == 0) {
+            if constexpr (NS == 1) op.tail(v[0]);
+            else op.tail(v);
             *tail.ticket = 0u;
         }
     }

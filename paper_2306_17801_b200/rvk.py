@@ -410,10 +410,11 @@ class TfqmrPlan:
     result().hist = ||B r0|| then one quasi-residual estimate per half step."""
 
     def __init__(self, ctx: Ctx, A: DeviceCsr, max_it: int = 20, pc: str = "jacobi",
-                 rtol: float = 0.0, atol: float = 0.0, use_graph: bool = True):
+                 rtol: float = 0.0, atol: float = 0.0, use_graph: bool = True,
+                 mode: str = "fused"):
         self.ctx, self.A, self.max_it = ctx, A, max_it
         cfg = CgConfig(max_it, PC_JACOBI if pc == "jacobi" else PC_NONE, rtol, atol,
-                       MODE_FUSED, 1 if use_graph else 0)
+                       MODES[mode], 1 if use_graph else 0)
         h = C.c_void_p()
         check(lib().rvk_tfqmr_plan_create(ctx.h, C.byref(A.c), cfg, C.byref(h)))
         self.h = h

@@ -4,9 +4,9 @@
 Bar: SPEC.md:474 / :496 -- residual histories within 1e-8 relative
 ("looser than CG because TFQMR recurrences amplify rounding"); x within 1e-8
 relative in the 2-norm.  Entries that have fallen to the rounding floor of
-the recurrence (below 1e-15 ||B r0||: e.g. 27-point 8^3 reaches 1e-16 in 20
-iterations, where the true residual stalls -- tests/test_oracle_tfqmr.py)
-are compared absolutely at 1e-15 ||B r0||.  Elementwise updates are bit-identical to the
+the recurrence (27-point 8^3 and 5-point 7x5 reach 1e-16 in 20 iterations,
+where the true residual stalls -- tests/test_oracle_tfqmr.py) are compared
+absolutely at 1e-14 ||B r0|| (a few dozen ulp of the initial residual).  Elementwise updates are bit-identical to the
 oracle's; only the three reductions per iteration differ in tree order.
 """
 import numpy as np
@@ -18,8 +18,9 @@ from paper_2306_17801_b200 import rvk
 pytestmark = pytest.mark.gpu
 
 HIST_RTOL = 1e-8
-HIST_FLOOR = 1e-15  # x hist[0]
+HIST_FLOOR = 1e-14  # x hist[0]: ~45 ulp of ||B r0||
 X_RTOL = 1e-8
+MODES = ["fused", "unfused"]
 
 
 def up(ctx, a):
@@ -49,25 +50,27 @@ def check(res, x, ref, hist_rtol=HIST_RTOL, x_rtol=X_RTOL):
                                   (3, 7, (8, 8, 8)), (3, 27, (8, 8, 8)), (2, 5, (7, 5)),
                                   (3, 7, (5, 4, 3)), (3, 27, (6, 5, 4))])
 @pytest.mark.parametrize("pc", ["jacobi", "none"])
-def test_tfqmr_vs_oracle_small(ctx, spec, pc):
+@pytest.mark.parametrize("mode", MODES)
+def test_tfqmr_vs_oracle_small(ctx, spec, pc, mode):
     dim, pts, g = spec
     Ah = O.build_laplacian(dim, pts, g)
     b = O.rhs(Ah.n_rows)
     ref = O.tfqmr_solve(Ah, b, max_it=20, pc=pc)
     A = rvk.DeviceCsr.laplacian(ctx, dim, pts, g)
-    _, x, res = solve(ctx, A, b, max_it=20, pc=pc)
+    _, x, res = solve(ctx, A, b, max_it=20, pc=pc, mode=mode)
     check(res, x, ref)
 
 
 @pytest.mark.parametrize("spec", [(2, 5, (1024, 1024)), (3, 7, (96, 80, 64)), (3, 27, (48, 48, 48))])
 @pytest.mark.parametrize("graph", [True, False])
-def test_tfqmr_vs_oracle_large(ctx, spec, graph):
+@pytest.mark.parametrize("mode", MODES)
+def test_tfqmr_vs_oracle_large(ctx, spec, graph, mode):
     dim, pts, g = spec
     Ah = O.build_laplacian(dim, pts, g)
     b = O.rhs(Ah.n_rows)
     ref = O.tfqmr_solve(Ah, b, max_it=20)
     A = rvk.DeviceCsr.laplacian(ctx, dim, pts, g)
-    plan, x, res = solve(ctx, A, b, max_it=20, use_graph=graph)
+    plan, x, res = solve(ctx, A, b, max_it=20, use_graph=graph, mode=mode)
     check(res, x, ref)
     # replay is bit-reproducible
     db, dx = up(ctx, b), rvk.DeviceArray(b.size)
@@ -83,8 +86,9 @@ def test_tfqmr_headline_grid(ctx):
     b = O.rhs(Ah.n_rows)
     ref = O.tfqmr_solve(Ah, b, max_it=20)
     A = rvk.DeviceCsr.laplacian(ctx, 3, 7, g)
-    _, x, res = solve(ctx, A, b, max_it=20)
-    check(res, x, ref)
+    for mode in MODES:
+        _, x, res = solve(ctx, A, b, max_it=20, mode=mode)
+        check(res, x, ref)
 
 
 def test_tfqmr_rtol_early_exit(ctx):
@@ -93,7 +97,9 @@ def test_tfqmr_rtol_early_exit(ctx):
     ref = O.tfqmr_solve(Ah, b, max_it=500, rtol=1e-8)
     assert ref.status == 1 and ref.iterations < 500
     A = rvk.DeviceCsr.laplacian(ctx, 2, 5, (64, 64))
-    _, x, res = solve(ctx, A, b, max_it=500, rtol=1e-8)
+    for mode in MODES:
+        _, x, res = solve(ctx, A, b, max_it=500, rtol=1e-8, mode=mode)
+        check(res, x, ref, hist_rtol=1e-5, x_rtol=1e-6)
     # SPEC's 1e-8 is a 20-iteration bar; over ~150 iterations the reduction
     # order drift compounds (measured 4.6e-7 relative at the exit), so the
     # long run is held to 1e-5 -- the exit iteration must still match exactly
@@ -106,10 +112,19 @@ def test_tfqmr_identity_exact(ctx):
     I = rvk.DeviceCsr.from_host(ctx, n, n, np.arange(n + 1, dtype=np.int64),
                                 np.arange(n, dtype=np.int32), np.ones(n))
     b = O.rhs(n)
-    _, x, res = solve(ctx, I, b, max_it=20, pc="none")
-    assert res.state == rvk.CG_CONVERGED and res.iterations == 1
-    assert res.hist.size == 2 and res.hist[1] == 0.0
-    assert np.array_equal(x, b)
+    for mode in MODES:
+        _, x, res = solve(ctx, I, b, max_it=20, pc="none", mode=mode)
+        assert res.state == rvk.CG_CONVERGED and res.iterations == 1
+        assert res.hist.size == 2 and res.hist[1] == 0.0
+        if mode == "unfused":
+            # rho_old = (r, rp) and s = (v, rp) are the same reduction kernel
+            # over identical vectors: a = 1 exactly, x = b bit for bit
+            assert np.array_equal(x, b)
+        else:
+            # fused: rho_old comes from the setup kernel's tree, s from the
+            # SpMV epilogue's -- a = 1 +- 1 ulp (same caveat as the fused CG
+            # identity test), so x = b to one ulp
+            assert np.max(np.abs(x - b)) <= 2.3e-16 * np.max(np.abs(b))
 
 
 def test_tfqmr_breakdown(ctx):
@@ -119,22 +134,54 @@ def test_tfqmr_breakdown(ctx):
     Ah = O.Csr(2, 2, np.array([0, 1, 2], np.int64), np.array([1, 0], np.int32), np.array([1.0, 1.0]))
     ref = O.tfqmr_solve(Ah, np.array([1.0, 0.0]), max_it=20, pc="none")
     assert ref.status == 2 and ref.breakdown_iter == 0
-    plan = rvk.TfqmrPlan(ctx, A, max_it=20, pc="none")
-    plan.solve_dev(up(ctx, np.array([1.0, 0.0])), rvk.DeviceArray(2))
-    with pytest.raises(rvk.BreakdownError) as ei:
-        plan.result()
-    assert ei.value.iteration == 0
+    for mode in MODES:
+        plan = rvk.TfqmrPlan(ctx, A, max_it=20, pc="none", mode=mode)
+        plan.solve_dev(up(ctx, np.array([1.0, 0.0])), rvk.DeviceArray(2))
+        with pytest.raises(rvk.BreakdownError) as ei:
+            plan.result()
+        assert ei.value.iteration == 0
 
 
 def test_tfqmr_zero_host_syncs(ctx):
     A = rvk.DeviceCsr.laplacian(ctx, 3, 7, (32, 32, 32))
     b = up(ctx, O.rhs(A.n_rows))
     x = rvk.DeviceArray(A.n_rows)
+    for mode in MODES:
+        plan = rvk.TfqmrPlan(ctx, A, max_it=20, mode=mode)
+        ctx.synchronize()
+        before = rvk.host_syncs()
+        plan.solve_dev(b, x)
+        plan.solve_dev(b, x)
+        assert rvk.host_syncs() == before
+        res = plan.result()
+        assert rvk.host_syncs() == before + 1 and res.iterations == 20
+
+
+def test_tfqmr_fused_misaligned_user_vectors(ctx):
+    """b / x at 8-byte (not 16-byte) offsets: the scalar tail paths."""
+    Ah = O.build_laplacian(2, 9, (33, 31))
+    b = O.rhs(Ah.n_rows)
+    ref = O.tfqmr_solve(Ah, b, max_it=20)
+    A = rvk.DeviceCsr.laplacian(ctx, 2, 9, (33, 31))
+    n = Ah.n_rows
+    big_b, big_x = up(ctx, np.concatenate([[0.0], b])), rvk.DeviceArray(n + 1)
     plan = rvk.TfqmrPlan(ctx, A, max_it=20)
-    ctx.synchronize()
-    before = rvk.host_syncs()
-    plan.solve_dev(b, x)
-    plan.solve_dev(b, x)
-    assert rvk.host_syncs() == before
+    rvk.check(rvk.lib().rvk_tfqmr_solve_dev(plan.h, big_b.ptr + 8, big_x.ptr + 8))
     res = plan.result()
-    assert rvk.host_syncs() == before + 1 and res.iterations == 20
+    check(res, big_x.download(ctx)[1:], ref)
+
+
+def test_tfqmr_early_exit_each_half_step(ctx):
+    """Convergence at the first vs the second half step of an iteration:
+    pick atol between consecutive bounds of the oracle's history."""
+    Ah = O.build_laplacian(2, 5, (24, 24))
+    b = O.rhs(Ah.n_rows)
+    full = O.tfqmr_solve(Ah, b, max_it=30)
+    A = rvk.DeviceCsr.laplacian(ctx, 2, 5, (24, 24))
+    for k in (5, 6, 11, 12):   # hist index k: k odd = first half, even = second half
+        atol = float(np.sqrt(full.hist[k] * full.hist[k - 1]))  # strictly between
+        ref = O.tfqmr_solve(Ah, b, max_it=30, atol=atol)
+        assert ref.hist.size == k + 1
+        for mode in MODES:
+            _, x, res = solve(ctx, A, b, max_it=30, atol=atol, mode=mode)
+            check(res, x, ref)
