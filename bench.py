@@ -495,6 +495,9 @@ def main():
                     help="csr: the AIJ/CSR operator (headline); stencil: matrix-free (SURVEY 8f)")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--comm", choices=["peer", "nccl"], default="peer",
+                    help="N>1: peer = in-kernel NVLink halo/partial pushes (fused); nccl = "
+                         "library collectives between kernels (baseline)")
     ap.add_argument("--solver", choices=["cg", "tfqmr"], default="cg",
                     help="cg: the headline Jacobi-PCG; tfqmr: left-Jacobi TFQMR (SURVEY 8f)")
     args = ap.parse_args()

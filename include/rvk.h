@@ -168,7 +168,12 @@ typedef enum {
     RVK_CG_MODE_HOSTSYNC   = 4  /* baseline: every dot/norm read back to the host (3 syncs
                                    per iteration, PETSc main_gpu behaviour) */
 } rvk_cg_mode;
-typedef enum { RVK_CG_RUNNING = 0, RVK_CG_CONVERGED = 1, RVK_CG_BREAKDOWN = 2 } rvk_cg_state;
+typedef enum {
+    RVK_CG_RUNNING    = 0,
+    RVK_CG_CONVERGED  = 1,
+    RVK_CG_BREAKDOWN  = 2,
+    RVK_CG_COMM_ERROR = 3 /* row-sharded PEER backend: a peer never arrived (bounded wait) */
+} rvk_cg_state;
 
 typedef struct {
     int    max_it;    /* SPEC.md:444 default 20                                  */
@@ -263,9 +268,10 @@ rvk_status rvk_build_laplacian_rows(rvk_ctx ctx, int dim, int points, int64_t nx
 rvk_status rvk_comm_unique_id(void* id_out, int id_bytes);
 rvk_status rvk_comm_init(const void* id, int nranks, int rank, rvk_comm* out);
 rvk_status rvk_comm_destroy(rvk_comm comm);
-/* comm == NULL with nranks > 1: LOOPBACK shard (all shards on one device,
- * sharing `shared_gather`, 4*nranks doubles, solved by
- * rvk_dcg_loopback_solve).  Otherwise shared_gather must be NULL. */
+/* comm != NULL: NCCL backend.  comm == NULL with nranks > 1: either a
+ * LOOPBACK shard (all shards on one device, sharing `shared_gather`,
+ * 4*nranks doubles, solved by rvk_dcg_loopback_solve) or, with
+ * shared_gather == NULL, a PEER shard (rvk_dcg_attach_peers below). */
 rvk_status rvk_dcg_plan_create(rvk_ctx ctx, const rvk_csr* A_local, rvk_shard shard,
                                rvk_cg_config cfg, rvk_comm comm, double* shared_gather,
                                rvk_dcg_plan* out);
@@ -276,6 +282,25 @@ rvk_status rvk_dcg_solve_dev(rvk_dcg_plan plan, const double* b_own, double* x_o
 rvk_status rvk_dcg_loopback_solve(rvk_dcg_plan* plans, int nplans, const double* const* b_own,
                                   double* const* x_own);
 rvk_status rvk_dcg_result(rvk_dcg_plan plan, double* hist_host, rvk_cg_info* info);
+
+/* PEER backend (NVLink P2P; the fused compute+communication path).  Each
+ * plan owns one device window [flags | gather slots | z | p0 | p1]; once
+ * every rank's window is mapped (own window as is, peers' via the cudaIpc
+ * helpers below) and attached, rvk_dcg_solve_dev runs 2 kernels per
+ * iteration that push the halo planes of z and p straight into the
+ * neighbours' windows while computing them, broadcast the dot partials and
+ * synchronise on per-rank arrival flags (bounded wait; RVK_ERR_COMM from
+ * rvk_dcg_result if a peer never arrives).  Create the plan with comm = NULL
+ * and shared_gather = NULL.  All ranks must attach before any rank solves,
+ * and stay alive until every rank finished its last solve (barrier, then
+ * destroy).  With every window on ONE device (windows of plans in one
+ * process) the same kernels run as a PEER loopback (rvk_dcg_loopback_solve). */
+rvk_status rvk_dcg_window(rvk_dcg_plan plan, void** base_dev, size_t* bytes);
+rvk_status rvk_dcg_attach_peers(rvk_dcg_plan plan, void* const* windows, const rvk_shard* shards);
+/* cudaIpc plumbing for the windows (64-byte handles). */
+rvk_status rvk_ipc_get_handle(const void* dev_base, void* handle_out, int handle_bytes);
+rvk_status rvk_ipc_open_handle(const void* handle, void** dev_ptr);
+rvk_status rvk_ipc_close_handle(void* dev_ptr);
 
 #ifdef __cplusplus
 }

@@ -123,7 +123,10 @@ __global__ void __launch_bounds__(kUpdThreads)
 // ---------------------------------------------------------------------------
 // K2: x += a p; r += (-a) w; z = B r; partials z.z, z.r; tail dp/hist/beta.
 // ---------------------------------------------------------------------------
-template <bool VEC, int PC> // PC: 0 none, 1 dinv vector, 2 constant dinv (matrix-free stencil)
+// COND: this instantiation may set the WHILE node's condition.  Kept a
+// template parameter so the plain-graph/stream variant contains no
+// cudaGraphSetConditional (ncu refuses to profile kernels that can set one).
+template <bool VEC, int PC, bool COND = false> // PC: 0 none, 1 dinv vector, 2 constant dinv
 __global__ void __launch_bounds__(kUpdThreads)
     k_cg_update(int64_t n, const double* __restrict__ p, const double* __restrict__ w,
                 const double* __restrict__ dinv, double* __restrict__ x, double* __restrict__ r,
@@ -134,7 +137,8 @@ __global__ void __launch_bounds__(kUpdThreads)
     // In the device WHILE loop (use_cond) `it` comes from the device state and
     // this kernel decides whether the loop body runs again.
     if (st->done) {
-        if (use_cond && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(cond, 0);
+        if constexpr (COND)
+            if (use_cond && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(cond, 0);
         return;
     }
     if (it < 0) it = st->iterations;
@@ -225,7 +229,8 @@ __global__ void __launch_bounds__(kUpdThreads)
             st->beta = acc[1];
             if (!more) st->done = 1; // ran max_it: later kernels of a WHILE body no-op
         }
-        if (use_cond) cudaGraphSetConditional(cond, more ? 1u : 0u);
+        if constexpr (COND)
+            if (use_cond) cudaGraphSetConditional(cond, more ? 1u : 0u);
         *ticket = 0u;
     }
 }
@@ -510,9 +515,15 @@ rvk_status launch_update(rvk_cg_plan P, int pcm, const double* p_new, double* x,
                                                  P->partials, P->tickets, P->dconst,
                                                  P->cfg.max_it, cond, use_cond);
     };
-    if (pcm == 0) go(k_cg_update<V, 0>);
-    else if (pcm == 1) go(k_cg_update<V, 1>);
-    else go(k_cg_update<V, 2>);
+    if (use_cond) {
+        if (pcm == 0) go(k_cg_update<V, 0, true>);
+        else if (pcm == 1) go(k_cg_update<V, 1, true>);
+        else go(k_cg_update<V, 2, true>);
+    } else {
+        if (pcm == 0) go(k_cg_update<V, 0>);
+        else if (pcm == 1) go(k_cg_update<V, 1>);
+        else go(k_cg_update<V, 2>);
+    }
     RVK_CHECK_LAUNCH("k_cg_update");
     return RVK_OK;
 }

@@ -11,6 +11,8 @@ namespace rvk {
 struct CgState {
     double beta, betaold, alpha, pAp, dp0, dp;
     int    done, state, iterations, breakdown_iter;
+    int    comm_error; // row-sharded PEER backend: a flag wait timed out
+    unsigned int seq;  // row-sharded PEER backend: solves started on this plan
 };
 
 constexpr int kUpdThreads = 256;

@@ -80,12 +80,16 @@ __device__ __forceinline__ void block_sum(double (&v)[NV], double* smem, int tid
 
 // Grid-level ticket: returns true in exactly one block (the last to arrive)
 // after every block has published its partials.  Call from ALL threads of
-// the participating thread group; `flag` is a shared int.
+// the participating thread group; `flag` is a shared int.  SYS: the block's
+// earlier stores include stores to PEER GPUs' memory -- fence at system
+// scope so the last block's release covers them.
+template <bool SYS = false>
 __device__ __forceinline__ bool last_block(unsigned int* ticket, int tid, int* flag, int nthreads,
                                            int bar)
 {
     if (tid == 0) {
-        __threadfence();
+        if constexpr (SYS) __threadfence_system();
+        else __threadfence();
         const unsigned int t = atomicAdd(ticket, 1u);
         *flag                = (t == gridDim.x - 1);
     }

@@ -18,12 +18,41 @@
 // partials itself; block 0 publishes state/hist), because the reduction is
 // only complete after the collective.  Every scalar stays on the device.
 //
-// Backends: NCCL (one process per GPU; ncclSend/Recv for halos, ncclAllGather
-// for the partials, all stream-ordered on the solve stream, no host sync), or
-// LOOPBACK (all P shards on one device in one process: halos are D2D copies
-// and the partials land in one shared gather buffer) -- the loopback path
-// exercises the partition, halo indexing and the distributed kernels on a
-// single GPU.
+// Backends:
+//  * PEER (the product on an NVSwitch box): every shard exports ONE device
+//    window [flags | gather | z | p0 | p1] (cudaIpc handle, mapped by every
+//    other rank).  The kernels do the communication themselves, tile by tile:
+//    K2/setup store the boundary planes of z straight into the neighbours'
+//    halo planes while they compute them, K1 does the same for p, and each
+//    kernel's last block stores its dot partials into every rank's gather
+//    slot and then releases a per-source arrival flag (st.release.sys) on
+//    every rank.  The next kernel's prologue waits (ld.acquire.sys) until all
+//    P flags reached its phase.  No NCCL call and no separate halo/allreduce
+//    step remains on the data path; the NVLink transfer overlaps the math.
+//  * NCCL (one process per GPU; ncclSend/Recv for halos, ncclAllGather for
+//    the partials, all stream-ordered on the solve stream, no host sync) --
+//    the library-collective baseline.
+//  * LOOPBACK (all P shards on one device in one process: halos are D2D
+//    copies and the partials land in one shared gather buffer), and PEER
+//    LOOPBACK (the PEER kernels with every "remote" window on the same
+//    device) -- exercise the partition, halo indexing, the in-kernel pushes
+//    and the flag protocol on a single GPU.
+//
+// PEER flag protocol.  Flags are 64-bit (solve_seq << 32 | phase), one per
+// source rank, stored monotonically by that source only.  Phases of solve s:
+// setup = 1, K1(it) = 2 + 2 it, K2(it) = 3 + 2 it, finish = 0xffffffff.
+//   K1(it) waits for phase 2 it + 1 (z halos + z.z/z.r partials of z_it);
+//   K2(it) waits for 2 it + 2 (p.w partials); finish waits for 2 max_it + 1;
+//   setup(s) waits for every rank's finish(s - 1), so no rank overwrites a
+//   slot or halo a slower peer still reads.
+// Write-after-read safety of the halos / slots follows from the waits: a
+// rank's K2(it) (which overwrites the neighbours' z halos and z.z slots)
+// starts only after every rank's K1(it) completed reading them; K1(it)
+// writes p_new = p[(it+1)&1], whose halo was last read by K1(it-1), which
+// precedes every rank's K2(it-1) that K1(it) waited for.  Every block fences
+// at system scope before its grid ticket, so the last block's release of the
+// flag covers all blocks' remote stores.  Waits are bounded (kPeerTimeoutNs):
+// a missing peer turns into RVK_CG_COMM_ERROR on every rank, never a hang.
 #include "rvk_cg.cuh"
 #include "rvk_common.cuh"
 #include "rvk_context.hpp"
@@ -100,33 +129,132 @@ __device__ __forceinline__ void fold_gather(const double* g, int nranks, int j0,
 {
     for (int v = 0; v < nv; ++v) out[v] = 0.0;
     for (int r = 0; r < nranks; ++r)
-        for (int v = 0; v < nv; ++v) out[v] += g[r * 4 + j0 + v];
+        for (int v = 0; v < nv; ++v) out[v] += __ldcv(g + r * 4 + j0 + v);
+}
+
+// ---- PEER backend: system-scope flag protocol ------------------------------
+constexpr uint32_t kPhaseFinish   = 0xffffffffu;
+constexpr uint64_t kPeerTimeoutNs = 30ull * 1000 * 1000 * 1000; // 30 s
+
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p)
+{
+    uint64_t v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v)
+{
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t globaltimer_ns()
+{
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ uint64_t phase_tag(uint32_t seq, uint32_t phase)
+{
+    return ((uint64_t)seq << 32) | phase;
+}
+
+// Everything a PEER-mode kernel needs to reach the other ranks.  Pointers are
+// valid on this device (own window, or peers' windows mapped by cudaIpc).
+struct DcgPeer {
+    int             on;                  // 0: NCCL / loopback phases, no in-kernel comm
+    int             rank, nranks;
+    double* const*  gather;              // [nranks] every rank's gather slots
+    uint64_t* const* flags;              // [nranks] every rank's arrival flags
+    const uint64_t* my_flags;            // this rank's flags (peers store into it)
+    double*         lo_z;                // where my first owned plane lands in rank-1 (or null)
+    double*         lo_p[2];
+    double*         hi_z;                // where my last owned plane lands in rank+1 (or null)
+    double*         hi_p[2];
+    int64_t         plane, n_own;
+};
+
+// Block-wide wait until every rank's flag reached `tag`.  Returns false (and
+// marks the solve failed) on timeout, or when another block of this rank
+// already timed out.  Call from ALL threads of the block.
+__device__ __forceinline__ bool peer_wait(const DcgPeer& pr, CgState* st, uint64_t tag)
+{
+    __shared__ int ok;
+    if (threadIdx.x == 0) {
+        int            good = 1;
+        const uint64_t t0   = globaltimer_ns();
+        for (int q = 0; q < pr.nranks && good; ++q) {
+            while (ld_acquire_sys(pr.my_flags + q) < tag) {
+                __nanosleep(128);
+                if (globaltimer_ns() - t0 > kPeerTimeoutNs || *(volatile int*)&st->comm_error) {
+                    good = 0;
+                    break;
+                }
+            }
+        }
+        if (!good && atomicCAS(&st->comm_error, 0, 1) == 0) {
+            st->state = RVK_CG_COMM_ERROR;
+            st->done  = 1;
+        }
+        ok = good;
+    }
+    __syncthreads();
+    return ok != 0;
+}
+
+// Single thread: store v[0..nv) into slot [rank*4 + j0] of every rank, then
+// release phase `tag` on every rank.  The caller has fenced its block's
+// remote stores (last_block<true>), so the release covers the whole grid.
+__device__ __forceinline__ void peer_publish(const DcgPeer& pr, int j0, const double* v, int nv,
+                                             uint64_t tag)
+{
+    for (int q = 0; q < pr.nranks; ++q)
+        for (int k = 0; k < nv; ++k) pr.gather[q][pr.rank * 4 + j0 + k] = v[k];
+    __threadfence_system();
+    for (int q = 0; q < pr.nranks; ++q) st_release_sys(pr.flags[q] + pr.rank, tag);
+}
+
+// Boundary-plane push of one owned element (row i of the shard).
+__device__ __forceinline__ void peer_push(double* lo, double* hi, int64_t plane, int64_t n_own,
+                                          int64_t i, double v)
+{
+    if (lo && i < plane) lo[i] = v;
+    const int64_t j = i - (n_own - plane);
+    if (hi && j >= 0) hi[j] = v;
 }
 
 } // namespace
 
 // ---------------------------------------------------------------------------
-// Kernels
+// Kernels.  PEER = true: in-kernel halo pushes, partial broadcast and flag
+// waits (see the protocol at the top); false: NCCL / loopback phases do the
+// exchange between kernels.
 // ---------------------------------------------------------------------------
 namespace {
 
 // K0: r = b, x = 0, z = B b on the owned rows; partial z.z, z.r -> gather[rank][0..1]
-template <bool JACOBI>
+template <bool JACOBI, bool PEER>
 __global__ void __launch_bounds__(kUpdThreads)
     k_dcg_setup(int64_t n, const double* __restrict__ b, const double* __restrict__ dinv,
                 double* __restrict__ x, double* __restrict__ r, double* __restrict__ z,
-                double* gather, int rank, double* partials, unsigned int* ticket)
+                double* gather, int rank, double* partials, unsigned int* ticket, CgState* st,
+                DcgPeer pr)
 {
     __shared__ double smem[64];
     __shared__ int    flag;
-    double            acc[2] = {0.0, 0.0};
-    const int64_t     stride = (int64_t)gridDim.x * blockDim.x;
+    uint32_t          seq = 0;
+    if constexpr (PEER) {
+        // every rank finished the previous solve (its slots / halos are free)
+        seq = st->seq;
+        if (seq > 1 && !peer_wait(pr, st, phase_tag(seq - 1, kPhaseFinish))) return;
+    }
+    double        acc[2] = {0.0, 0.0};
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
         const double bi = b[i];
         const double zi = JACOBI ? mul(dinv[i], bi) : bi;
         r[i] = bi;
         z[i] = zi;
         x[i] = 0.0;
+        if constexpr (PEER) peer_push(pr.lo_z, pr.hi_z, pr.plane, n, i, zi);
         acc[0] = add(acc[0], mul(zi, zi));
         acc[1] = add(acc[1], mul(zi, bi));
     }
@@ -136,12 +264,15 @@ __global__ void __launch_bounds__(kUpdThreads)
         partials[2 * blockIdx.x]     = acc[0];
         partials[2 * blockIdx.x + 1] = acc[1];
     }
-    if (!last_block(ticket, tid, &flag, blockDim.x, 1)) return;
+    if (!last_block<PEER>(ticket, tid, &flag, blockDim.x, 1)) return;
     fold_partials<2>(partials, gridDim.x, acc, smem, tid, blockDim.x, 1);
     if (tid == 0) {
-        gather[rank * 4 + 0] = acc[0];
-        gather[rank * 4 + 1] = acc[1];
-        *ticket              = 0u;
+        *ticket = 0u;
+        if constexpr (PEER) peer_publish(pr, 0, acc, 2, phase_tag(seq, 1));
+        else {
+            gather[rank * 4 + 0] = acc[0];
+            gather[rank * 4 + 1] = acc[1];
+        }
     }
 }
 
@@ -156,9 +287,10 @@ struct DcgScalars {
     double   rtol, atol;
 };
 
-template <bool FIRST>
+template <bool FIRST, bool PEER>
 struct DcgSpmvOp {
-    static constexpr bool kHasTail = true;
+    static constexpr bool kHasTail  = true;
+    static constexpr bool kSysFence = PEER;
     const double* __restrict__ z;     // extended (halo) layout
     const double* __restrict__ p_old; // extended
     double* __restrict__ p_new;       // extended
@@ -168,11 +300,19 @@ struct DcgSpmvOp {
     double*    gather_out;            // &gather[rank*4 + 2]
     int        it;
     double     b;
+    DcgPeer    pr;                    // PEER: neighbours' p_new halo planes etc.
+    double*    lo_pn;                 // PEER: pr.lo_p / hi_p of this iteration's p_new
+    double*    hi_pn;
+    uint32_t   seq;
 
     __device__ __forceinline__ bool init()
     {
         CgState* st = sc.st;
         if (st->done) return false;
+        if constexpr (PEER) {
+            seq = st->seq;
+            if (!peer_wait(pr, st, phase_tag(seq, 2 * it + 1))) return false;
+        }
         double v[2];
         fold_gather(sc.gather, sc.nranks, 0, 2, v); // z.z, z.r of z_it
         const double dp    = sqrt(v[0]);
@@ -232,22 +372,32 @@ struct DcgSpmvOp {
     {
         const double p     = value(o);
         p_new[i + own_off] = p;
+        if constexpr (PEER) peer_push(lo_pn, hi_pn, pr.plane, pr.n_own, i, p);
         w[i]               = sum;
         return add(acc, mul(p, sum));
     }
-    __device__ __forceinline__ void tail(double pAp_local) const { *gather_out = pAp_local; }
+    __device__ __forceinline__ void tail(double pAp_local) const
+    {
+        if constexpr (PEER) peer_publish(pr, 2, &pAp_local, 1, phase_tag(seq, 2 * it + 2));
+        else *gather_out = pAp_local;
+    }
 };
 
 // K2(it): fold p.w; alpha = beta_it / pAp; updates; partial z.z, z.r.
-template <bool JACOBI>
+template <bool JACOBI, bool PEER>
 __global__ void __launch_bounds__(kUpdThreads)
     k_dcg_update(int64_t n, const double* __restrict__ p, const double* __restrict__ w,
                  const double* __restrict__ dinv, double* __restrict__ x, double* __restrict__ r,
                  double* __restrict__ z, DcgScalars sc, int it, int rank, double* gather_out,
-                 double* partials, unsigned int* ticket)
+                 double* partials, unsigned int* ticket, DcgPeer pr)
 {
     CgState* st = sc.st;
     if (st->done) return;
+    uint32_t seq = 0;
+    if constexpr (PEER) {
+        seq = st->seq;
+        if (!peer_wait(pr, st, phase_tag(seq, 2 * it + 2))) return;
+    }
     double pv[1];
     fold_gather(sc.gather, sc.nranks, 2, 1, pv);
     const double pAp = pv[0];
@@ -275,6 +425,7 @@ __global__ void __launch_bounds__(kUpdThreads)
         const double zi = JACOBI ? mul(dinv[i], ri) : ri;
         r[i]            = ri;
         z[i]            = zi;
+        if constexpr (PEER) peer_push(pr.lo_z, pr.hi_z, pr.plane, n, i, zi);
         acc[0]          = add(acc[0], mul(zi, zi));
         acc[1]          = add(acc[1], mul(zi, ri));
     }
@@ -284,32 +435,47 @@ __global__ void __launch_bounds__(kUpdThreads)
         partials[2 * blockIdx.x]     = acc[0];
         partials[2 * blockIdx.x + 1] = acc[1];
     }
-    if (!last_block(ticket, tid, &flag, blockDim.x, 1)) return;
+    if (!last_block<PEER>(ticket, tid, &flag, blockDim.x, 1)) return;
     fold_partials<2>(partials, gridDim.x, acc, smem, tid, blockDim.x, 1);
     if (tid == 0) {
-        gather_out[0] = acc[0];
-        gather_out[1] = acc[1];
-        *ticket       = 0u;
+        *ticket = 0u;
+        if constexpr (PEER) peer_publish(pr, 0, acc, 2, phase_tag(seq, 2 * it + 3));
+        else {
+            gather_out[0] = acc[0];
+            gather_out[1] = acc[1];
+        }
     }
     (void)rank;
 }
 
 // After the last iteration: publish hist[max_it] (the K1 prologue that would
-// normally do it does not run).
-__global__ void k_dcg_finish(DcgScalars sc, int it)
+// normally do it does not run).  PEER: then release "finished" to every rank.
+template <bool PEER>
+__global__ void k_dcg_finish(DcgScalars sc, int it, DcgPeer pr)
 {
-    CgState* st = sc.st;
-    if (st->done) return;
-    double v[2];
-    fold_gather(sc.gather, sc.nranks, 0, 2, v);
-    const double dp = sqrt(v[0]);
-    sc.hist[it]     = dp;
-    sc.beta[it]     = v[1];
-    st->dp          = dp;
-    st->iterations  = it;
-    if (cg_converged(dp, st->dp0, sc.rtol, sc.atol)) {
-        st->state = RVK_CG_CONVERGED;
-        st->done  = 1;
+    CgState*       st  = sc.st;
+    const uint32_t seq = st->seq;
+    bool           run = !st->done; // uniform over the block
+    if constexpr (PEER)
+        if (run) run = peer_wait(pr, st, phase_tag(seq, 2 * it + 1));
+    if (threadIdx.x != 0) return;
+    if (run) {
+        double v[2];
+        fold_gather(sc.gather, sc.nranks, 0, 2, v);
+        const double dp = sqrt(v[0]);
+        sc.hist[it]     = dp;
+        sc.beta[it]     = v[1];
+        st->dp          = dp;
+        st->iterations  = it;
+        if (cg_converged(dp, st->dp0, sc.rtol, sc.atol)) {
+            st->state = RVK_CG_CONVERGED;
+            st->done  = 1;
+        }
+    }
+    if constexpr (PEER) {
+        __threadfence_system();
+        for (int q = 0; q < pr.nranks; ++q)
+            st_release_sys(pr.flags[q] + pr.rank, phase_tag(seq, kPhaseFinish));
     }
 }
 
@@ -319,6 +485,8 @@ __global__ void k_dcg_reset(CgState* st)
     st->state = RVK_CG_RUNNING;
     st->iterations = 0;
     st->breakdown_iter = -1;
+    st->comm_error = 0;
+    st->seq += 1;
 }
 
 } // namespace
@@ -333,21 +501,47 @@ struct rvk_comm_s {
 
 struct rvk_dcg_plan_s {
     rvk_ctx       ctx = nullptr;
-    rvk_comm      comm = nullptr; // null: loopback group member
+    rvk_comm      comm = nullptr; // null: loopback group member (or PEER backend)
     rvk_csr       A{};
     rvk_shard     sh{};
     rvk_cg_config cfg{};
     SpmvArgs      sa{};
     int           upd_grid = 0;
     int64_t       n_ext = 0;
+    unsigned char* win = nullptr;  // [flags | gather | z | p0 | p1], the exported PEER window
+    size_t        win_bytes = 0;
     double *dinv = nullptr, *r = nullptr, *z = nullptr, *p[2] = {nullptr, nullptr}, *w = nullptr;
     double *hist = nullptr, *beta = nullptr, *gather = nullptr, *partials = nullptr;
     bool          owns_gather = true;
     CgState*      st = nullptr;
     unsigned int* tickets = nullptr;
+    DcgPeer       peer{};          // peer.on: PEER backend attached
+    void**        peer_tab = nullptr; // device: gather[nranks] then flags[nranks]
 };
 
 namespace {
+
+// Byte layout of a shard's window (identical rule on every rank, so a rank
+// can address a peer's halo planes from the peer's shard geometry alone).
+struct WindowLayout {
+    size_t flags, gather, z, p0, p1, bytes;
+};
+WindowLayout window_layout(int64_t n_ext)
+{
+    auto         up = [](size_t v) { return (v + 255) & ~size_t(255); };
+    WindowLayout L{};
+    size_t       o = 0;
+    L.flags        = o;
+    o              = up(o + kMaxRanks * sizeof(uint64_t));
+    L.gather       = o;
+    o              = up(o + kMaxRanks * 4 * sizeof(double));
+    const size_t vb = up((size_t)n_ext * 8 + 32); // padded: x-windows round up
+    L.z            = o;
+    L.p0           = o + vb;
+    L.p1           = o + 2 * vb;
+    L.bytes        = o + 3 * vb;
+    return L;
+}
 
 rvk_status alloc_plan_buffers(rvk_dcg_plan P)
 {
@@ -358,18 +552,23 @@ rvk_status alloc_plan_buffers(rvk_dcg_plan P)
         if (e == cudaSuccess) e = cudaMalloc(p, b);
         if (e == cudaSuccess) e = cudaMemsetAsync(*p, 0, b, P->ctx->stream);
     };
+    const WindowLayout L = window_layout(P->n_ext);
+    alloc((void**)&P->win, L.bytes);
+    if (e == cudaSuccess) {
+        P->win_bytes = L.bytes;
+        P->z         = reinterpret_cast<double*>(P->win + L.z);
+        P->p[0]      = reinterpret_cast<double*>(P->win + L.p0);
+        P->p[1]      = reinterpret_cast<double*>(P->win + L.p1);
+        if (P->owns_gather) P->gather = reinterpret_cast<double*>(P->win + L.gather);
+    }
     alloc((void**)&P->dinv, n * 8);
     alloc((void**)&P->r, n * 8);
     alloc((void**)&P->w, n * 8);
-    alloc((void**)&P->z, P->n_ext * 8 + 32); // padded: x-windows round up
-    alloc((void**)&P->p[0], P->n_ext * 8 + 32);
-    alloc((void**)&P->p[1], P->n_ext * 8 + 32);
     alloc((void**)&P->hist, (P->cfg.max_it + 1) * 8);
     alloc((void**)&P->beta, (P->cfg.max_it + 1) * 8);
     alloc((void**)&P->st, sizeof(CgState));
     alloc((void**)&P->partials, 4 * kMaxReduceBlocks * 8);
     alloc((void**)&P->tickets, 16 * 4);
-    if (P->owns_gather) alloc((void**)&P->gather, 4 * kMaxRanks * 8);
     if (e != cudaSuccess) return cuda_error(e, "rvk_dcg_plan_create: allocation");
     return RVK_OK;
 }
@@ -382,58 +581,67 @@ DcgScalars scalars(rvk_dcg_plan P)
 int64_t plane(const rvk_dcg_plan P) { return P->sh.halo_lo ? P->sh.halo_lo : P->sh.halo_hi; }
 
 // ---- per-phase enqueue (one shard) -----------------------------------------
+// The PEER variants carry the in-kernel communication; otherwise the NCCL /
+// loopback exchange is enqueued between the phases by the caller.
+template <bool J, bool PEER>
+void launch_setup_k(rvk_dcg_plan P, const double* b, double* x)
+{
+    k_dcg_setup<J, PEER><<<P->upd_grid, kUpdThreads, 0, P->ctx->stream>>>(
+        P->sh.n_own, b, P->dinv, x, P->r, P->z + P->sh.halo_lo, P->gather, P->sh.rank, P->partials,
+        P->tickets, P->st, P->peer);
+}
+
 rvk_status phase_setup(rvk_dcg_plan P, const double* b, double* x)
 {
-    cudaStream_t s = P->ctx->stream;
-    k_dcg_reset<<<1, 1, 0, s>>>(P->st);
-    const int g = P->upd_grid;
-    double*   z_own = P->z + P->sh.halo_lo;
-    if (P->cfg.pc == RVK_PC_JACOBI)
-        k_dcg_setup<true><<<g, kUpdThreads, 0, s>>>(P->sh.n_own, b, P->dinv, x, P->r, z_own, P->gather,
-                                                    P->sh.rank, P->partials, P->tickets);
-    else
-        k_dcg_setup<false><<<g, kUpdThreads, 0, s>>>(P->sh.n_own, b, P->dinv, x, P->r, z_own, P->gather,
-                                                     P->sh.rank, P->partials, P->tickets);
+    k_dcg_reset<<<1, 1, 0, P->ctx->stream>>>(P->st);
+    const bool j = P->cfg.pc == RVK_PC_JACOBI;
+    if (P->peer.on) j ? launch_setup_k<true, true>(P, b, x) : launch_setup_k<false, true>(P, b, x);
+    else j ? launch_setup_k<true, false>(P, b, x) : launch_setup_k<false, false>(P, b, x);
     RVK_CHECK_LAUNCH("k_dcg_setup");
     return RVK_OK;
 }
 
-rvk_status phase_k1(rvk_dcg_plan P, int it)
+template <bool FIRST, bool PEER>
+rvk_status launch_k1(rvk_dcg_plan P, int it)
 {
-    cudaStream_t   s  = P->ctx->stream;
     const double*  po = P->p[it & 1];
     double*        pn = P->p[(it + 1) & 1];
     const TailArgs ta{P->partials + 2 * kMaxReduceBlocks, P->tickets + 1};
     double*        go = P->gather + P->sh.rank * 4 + 2;
-    if (it == 0) {
-        DcgSpmvOp<true> op{P->z, po, pn, P->w, scalars(P), P->sh.halo_lo, go, it, 0.0};
-        return launch_spmv(s, P->sa, op, ta, sm_count());
-    }
-    DcgSpmvOp<false> op{P->z, po, pn, P->w, scalars(P), P->sh.halo_lo, go, it, 0.0};
-    return launch_spmv(s, P->sa, op, ta, sm_count());
+    const int      k  = (it + 1) & 1; // p_new's buffer index, also in the neighbours
+    DcgSpmvOp<FIRST, PEER> op{P->z, po, pn, P->w, scalars(P), P->sh.halo_lo, go, it, 0.0, P->peer,
+                              P->peer.lo_p[k], P->peer.hi_p[k], 0u};
+    return launch_spmv(P->ctx->stream, P->sa, op, ta, sm_count());
+}
+
+rvk_status phase_k1(rvk_dcg_plan P, int it)
+{
+    if (P->peer.on) return it == 0 ? launch_k1<true, true>(P, it) : launch_k1<false, true>(P, it);
+    return it == 0 ? launch_k1<true, false>(P, it) : launch_k1<false, false>(P, it);
+}
+
+template <bool J, bool PEER>
+void launch_update_k(rvk_dcg_plan P, int it, double* x)
+{
+    k_dcg_update<J, PEER><<<P->upd_grid, kUpdThreads, 0, P->ctx->stream>>>(
+        P->sh.n_own, P->p[(it + 1) & 1] + P->sh.halo_lo, P->w, P->dinv, x, P->r,
+        P->z + P->sh.halo_lo, scalars(P), it, P->sh.rank, P->gather + P->sh.rank * 4, P->partials,
+        P->tickets, P->peer);
 }
 
 rvk_status phase_k2(rvk_dcg_plan P, int it, double* x)
 {
-    cudaStream_t  s  = P->ctx->stream;
-    const double* pn = P->p[(it + 1) & 1] + P->sh.halo_lo;
-    double*       z  = P->z + P->sh.halo_lo;
-    double*       go = P->gather + P->sh.rank * 4;
-    if (P->cfg.pc == RVK_PC_JACOBI)
-        k_dcg_update<true><<<P->upd_grid, kUpdThreads, 0, s>>>(P->sh.n_own, pn, P->w, P->dinv, x, P->r, z,
-                                                               scalars(P), it, P->sh.rank, go,
-                                                               P->partials, P->tickets);
-    else
-        k_dcg_update<false><<<P->upd_grid, kUpdThreads, 0, s>>>(P->sh.n_own, pn, P->w, P->dinv, x, P->r, z,
-                                                                scalars(P), it, P->sh.rank, go,
-                                                                P->partials, P->tickets);
+    const bool j = P->cfg.pc == RVK_PC_JACOBI;
+    if (P->peer.on) j ? launch_update_k<true, true>(P, it, x) : launch_update_k<false, true>(P, it, x);
+    else j ? launch_update_k<true, false>(P, it, x) : launch_update_k<false, false>(P, it, x);
     RVK_CHECK_LAUNCH("k_dcg_update");
     return RVK_OK;
 }
 
 rvk_status phase_finish(rvk_dcg_plan P)
 {
-    k_dcg_finish<<<1, 1, 0, P->ctx->stream>>>(scalars(P), P->cfg.max_it);
+    if (P->peer.on) k_dcg_finish<true><<<1, 32, 0, P->ctx->stream>>>(scalars(P), P->cfg.max_it, P->peer);
+    else k_dcg_finish<false><<<1, 32, 0, P->ctx->stream>>>(scalars(P), P->cfg.max_it, P->peer);
     RVK_CHECK_LAUNCH("k_dcg_finish");
     return RVK_OK;
 }
@@ -560,8 +768,8 @@ rvk_status rvk_dcg_plan_create(rvk_ctx ctx, const rvk_csr* A, rvk_shard sh, rvk_
     if ((sh.halo_lo > sh.n_own) || (sh.halo_hi > sh.n_own))
         return set_error(RVK_ERR_INVALID, "dcg_plan_create: shard thinner than a halo plane");
     if (cfg.max_it < 1) return set_error(RVK_ERR_INVALID, "max_it must be >= 1");
-    if (!comm && !shared_gather && sh.nranks > 1)
-        return set_error(RVK_ERR_INVALID, "dcg_plan_create: loopback shards need a shared gather buffer");
+    if (comm && shared_gather)
+        return set_error(RVK_ERR_INVALID, "dcg_plan_create: shared_gather is for loopback shards only");
     int64_t maxlen = 0;
     RVK_TRY(rvk_csr_validate(ctx, A, &maxlen));
     auto P         = new rvk_dcg_plan_s();
@@ -575,7 +783,7 @@ rvk_status rvk_dcg_plan_create(rvk_ctx ctx, const rvk_csr* A, rvk_shard sh, rvk_
     if (!std::getenv("RVK_WINDOWS")) win.n = 0;
     if (std::getenv("RVK_NO_PREFETCH")) win.has_lead = false;
     P->sa          = make_spmv_args(*A, maxlen, &win, 2);
-    P->upd_grid    = resident_grid(k_dcg_update<true>, kUpdThreads, sh.n_own);
+    P->upd_grid    = resident_grid(k_dcg_update<true, true>, kUpdThreads, sh.n_own);
     P->owns_gather = shared_gather == nullptr;
     P->gather      = shared_gather;
     rvk_status rc  = alloc_plan_buffers(P);
@@ -596,22 +804,25 @@ rvk_status rvk_dcg_plan_destroy(rvk_dcg_plan P)
 {
     if (!P) return RVK_OK;
     if (P->ctx) cudaStreamSynchronize(P->ctx->stream);
-    void* bufs[] = {P->dinv, P->r, P->w, P->z, P->p[0], P->p[1], P->hist, P->beta, P->st, P->partials,
-                    P->tickets};
+    // (PEER: the caller keeps every rank alive past its last solve -- a
+    // barrier before destroy -- since peers store into this window)
+    void* bufs[] = {P->win, P->dinv, P->r, P->w, P->hist, P->beta, P->st, P->partials, P->tickets,
+                    P->peer_tab};
     for (void* b : bufs)
         if (b) cudaFree(b);
-    if (P->owns_gather && P->gather) cudaFree(P->gather);
     delete P;
     return RVK_OK;
 }
 
-// One shard per process (NCCL): the whole solve, stream-ordered, no host sync.
+// One shard per process: the whole solve, stream-ordered, no host sync.
+// PEER: 2 kernels per iteration carry all communication; NCCL: halo
+// send/recv + 2 allgathers per iteration between the kernels.
 rvk_status rvk_dcg_solve_dev(rvk_dcg_plan P, const double* b_own, double* x_own)
 {
     if (!P || !b_own || !x_own) return set_error(RVK_ERR_INVALID, "null argument");
-    if (!P->comm && P->sh.nranks > 1)
+    if (!P->comm && !P->peer.on && P->sh.nranks > 1)
         return set_error(RVK_ERR_INVALID, "loopback shards are solved with rvk_dcg_loopback_solve");
-    const bool dist = P->comm && P->sh.nranks > 1;
+    const bool dist = !P->peer.on && P->comm && P->sh.nranks > 1;
     RVK_TRY(phase_setup(P, b_own, x_own));
     if (dist) RVK_TRY(nccl_allgather(P));
     for (int it = 0; it < P->cfg.max_it; ++it) {
@@ -629,12 +840,20 @@ rvk_status rvk_dcg_solve_dev(rvk_dcg_plan P, const double* b_own, double* x_own)
 rvk_status rvk_dcg_loopback_solve(rvk_dcg_plan* Ps, int np, const double* const* b, double* const* x)
 {
     if (!Ps || np < 1 || !b || !x) return set_error(RVK_ERR_INVALID, "null argument");
-    for (int r = 0; r < np; ++r)
+    const bool peer = Ps[0]->peer.on;
+    for (int r = 0; r < np; ++r) {
         if (Ps[r]->ctx->stream != Ps[0]->ctx->stream)
             return set_error(RVK_ERR_INVALID, "loopback shards must share one context/stream");
+        if (Ps[r]->peer.on != peer || Ps[r]->comm)
+            return set_error(RVK_ERR_INVALID, "loopback shards: all PEER-attached or all shared-gather");
+        if (!peer && np > 1 && (Ps[r]->owns_gather || Ps[r]->gather != Ps[0]->gather))
+            return set_error(RVK_ERR_INVALID, "loopback shards need one shared gather buffer");
+    }
+    // phase-major order: every flag a PEER kernel waits for was released by
+    // a kernel enqueued before it on this stream (no spin ever blocks)
     for (int r = 0; r < np; ++r) RVK_TRY(phase_setup(Ps[r], b[r], x[r]));
     for (int it = 0; it < Ps[0]->cfg.max_it; ++it) {
-        RVK_TRY(loop_halo(Ps, np, it > 0, it));
+        if (!peer) RVK_TRY(loop_halo(Ps, np, it > 0, it));
         for (int r = 0; r < np; ++r) RVK_TRY(phase_k1(Ps[r], it));
         for (int r = 0; r < np; ++r) RVK_TRY(phase_k2(Ps[r], it, x[r]));
     }
@@ -659,6 +878,103 @@ rvk_status rvk_dcg_result(rvk_dcg_plan P, double* hist_host, rvk_cg_info* info)
     }
     if (h.state == RVK_CG_BREAKDOWN)
         return set_error(RVK_ERR_BREAKDOWN, "cg_solve: breakdown at iteration %d", h.breakdown_iter);
+    if (h.state == RVK_CG_COMM_ERROR)
+        return set_error(RVK_ERR_COMM, "dcg_solve: a peer did not arrive within %llu s (PEER backend)",
+                         (unsigned long long)(kPeerTimeoutNs / 1000000000ull));
+    return RVK_OK;
+}
+
+// ---- PEER backend ----------------------------------------------------------
+rvk_status rvk_dcg_window(rvk_dcg_plan P, void** base, size_t* bytes)
+{
+    if (!P || !base || !bytes) return set_error(RVK_ERR_INVALID, "null argument");
+    *base  = P->win;
+    *bytes = P->win_bytes;
+    return RVK_OK;
+}
+
+rvk_status rvk_dcg_attach_peers(rvk_dcg_plan P, void* const* windows, const rvk_shard* shards)
+{
+    if (!P || !windows || !shards) return set_error(RVK_ERR_INVALID, "null argument");
+    const int np = P->sh.nranks, me = P->sh.rank;
+    if (P->comm || !P->owns_gather)
+        return set_error(RVK_ERR_INVALID, "attach_peers: plan was created for the NCCL / shared-gather loopback backend");
+    if (windows[me] != P->win)
+        return set_error(RVK_ERR_INVALID, "attach_peers: windows[rank] must be this plan's own window");
+    for (int q = 0; q < np; ++q) {
+        const rvk_shard& s = shards[q];
+        if (!windows[q] || s.rank != q || s.nranks != np)
+            return set_error(RVK_ERR_INVALID, "attach_peers: shard %d does not describe rank %d of %d", q, q, np);
+    }
+    const int64_t pl = plane(P);
+    auto ext = [&](int q) { return shards[q].halo_lo + shards[q].n_own + shards[q].halo_hi; };
+    auto at  = [&](int q, size_t off) { return reinterpret_cast<unsigned char*>(windows[q]) + off; };
+    std::vector<void*> tab(2 * np);
+    for (int q = 0; q < np; ++q) {
+        const WindowLayout L = window_layout(ext(q));
+        tab[q]               = at(q, L.gather);
+        tab[np + q]          = at(q, L.flags);
+    }
+    DcgPeer pr{};
+    pr.on     = 1;
+    pr.rank   = me;
+    pr.nranks = np;
+    pr.plane  = pl;
+    pr.n_own  = P->sh.n_own;
+    const WindowLayout Lme = window_layout(P->n_ext);
+    pr.my_flags            = reinterpret_cast<const uint64_t*>(P->win + Lme.flags);
+    if (me > 0) { // my first owned plane -> the upper halo of rank-1
+        const rvk_shard&   d   = shards[me - 1];
+        const WindowLayout L   = window_layout(ext(me - 1));
+        const size_t       off = (size_t)(d.halo_lo + d.n_own) * 8;
+        if (d.halo_hi != pl) return set_error(RVK_ERR_DIM, "attach_peers: plane size mismatch with rank %d", me - 1);
+        pr.lo_z    = reinterpret_cast<double*>(at(me - 1, L.z + off));
+        pr.lo_p[0] = reinterpret_cast<double*>(at(me - 1, L.p0 + off));
+        pr.lo_p[1] = reinterpret_cast<double*>(at(me - 1, L.p1 + off));
+    }
+    if (me < np - 1) { // my last owned plane -> the lower halo of rank+1 (element 0)
+        const rvk_shard&   u = shards[me + 1];
+        const WindowLayout L = window_layout(ext(me + 1));
+        if (u.halo_lo != pl) return set_error(RVK_ERR_DIM, "attach_peers: plane size mismatch with rank %d", me + 1);
+        pr.hi_z    = reinterpret_cast<double*>(at(me + 1, L.z));
+        pr.hi_p[0] = reinterpret_cast<double*>(at(me + 1, L.p0));
+        pr.hi_p[1] = reinterpret_cast<double*>(at(me + 1, L.p1));
+    }
+    if (!P->peer_tab) RVK_CUDA(cudaMalloc(&P->peer_tab, 2 * kMaxRanks * sizeof(void*)));
+    RVK_CUDA(cudaMemcpy(P->peer_tab, tab.data(), tab.size() * sizeof(void*), cudaMemcpyHostToDevice));
+    pr.gather = reinterpret_cast<double* const*>(P->peer_tab);
+    pr.flags  = reinterpret_cast<uint64_t* const*>(P->peer_tab + np);
+    // fresh protocol state: flags 0, solve counter 0 (before any peer stores)
+    RVK_CUDA(cudaMemsetAsync(P->win + Lme.flags, 0, kMaxRanks * sizeof(uint64_t), P->ctx->stream));
+    RVK_CUDA(cudaMemsetAsync(P->st, 0, sizeof(CgState), P->ctx->stream));
+    RVK_CUDA(cudaStreamSynchronize(P->ctx->stream));
+    P->peer = pr;
+    return RVK_OK;
+}
+
+rvk_status rvk_ipc_get_handle(const void* dev_base, void* handle_out, int handle_bytes)
+{
+    if (!dev_base || !handle_out || handle_bytes < (int)sizeof(cudaIpcMemHandle_t))
+        return set_error(RVK_ERR_INVALID, "ipc_get_handle: need %d bytes", (int)sizeof(cudaIpcMemHandle_t));
+    cudaIpcMemHandle_t h;
+    RVK_CUDA(cudaIpcGetMemHandle(&h, const_cast<void*>(dev_base)));
+    std::memcpy(handle_out, &h, sizeof h);
+    return RVK_OK;
+}
+
+rvk_status rvk_ipc_open_handle(const void* handle, void** dev_ptr)
+{
+    if (!handle || !dev_ptr) return set_error(RVK_ERR_INVALID, "null argument");
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof h);
+    RVK_CUDA(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    return RVK_OK;
+}
+
+rvk_status rvk_ipc_close_handle(void* dev_ptr)
+{
+    if (!dev_ptr) return RVK_OK;
+    RVK_CUDA(cudaIpcCloseMemHandle(dev_ptr));
     return RVK_OK;
 }
 

@@ -318,6 +318,12 @@ template <class Op>
 struct spmv_sums<Op, std::void_t<decltype(Op::kSums)>> {
     static constexpr int value = Op::kSums;
 };
+// Op::kSysFence: the op stores into peer GPUs' memory (PEER backend).
+template <class Op, class = void>
+struct spmv_sys_fence : std::false_type {};
+template <class Op>
+struct spmv_sys_fence<Op, std::void_t<decltype(Op::kSysFence)>>
+    : std::integral_constant<bool, Op::kSysFence> {};
 template <class Op>
 using spmv_acc_t = std::conditional_t<spmv_sums<Op>::value == 1, double, SumVec<spmv_sums<Op>::value>>;
 
@@ -488,7 +494,7 @@ __global__ void __launch_bounds__(kSpmvThreads, 1) k_spmv_tma(SpmvArgs A, Op op_
 #pragma unroll
             for (int j = 0; j < NS; ++j) tail.partials[(size_t)blockIdx.x * NS + j] = v[j];
         }
-        if (!last_block(tail.ticket, ctid, flag, kSpmvConsumers, 1)) return;
+        if (!last_block<spmv_sys_fence<Op>::value>(tail.ticket, ctid, flag, kSpmvConsumers, 1)) return;
         fold_partials<NS>(tail.partials, gridDim.x, v, red, ctid, kSpmvConsumers, 1);
         if (ctid == 0) {
             if constexpr (NS == 1) op.tail(v[0]);

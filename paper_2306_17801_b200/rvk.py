@@ -19,12 +19,13 @@ LIB_PATH = os.path.join(HERE, "lib", "librvk.so")
 
 RVK_OK = 0
 RVK_ERR_BREAKDOWN = 5
+RVK_ERR_COMM = 6
 SCALAR_CONST, SCALAR_PTR, SCALAR_NEG_PTR, SCALAR_DIV, SCALAR_SQRT, SCALAR_RECIP = range(6)
 PC_NONE, PC_JACOBI = 0, 1
 MODE_FUSED, MODE_UNFUSED, MODE_PERSISTENT, MODE_AUTO, MODE_HOSTSYNC = 0, 1, 2, 3, 4
 MODES = {"fused": MODE_FUSED, "unfused": MODE_UNFUSED, "persistent": MODE_PERSISTENT,
          "auto": MODE_AUTO, "hostsync": MODE_HOSTSYNC}
-CG_RUNNING, CG_CONVERGED, CG_BREAKDOWN = 0, 1, 2
+CG_RUNNING, CG_CONVERGED, CG_BREAKDOWN, CG_COMM_ERROR = 0, 1, 2, 3
 
 # every symbol include/rvk.h declares (checked by tests/test_abi.py)
 EXPORTS = [
@@ -41,7 +42,8 @@ EXPORTS = [
     "rvk_cg_set_profiling", "rvk_cg_kernel_times", "rvk_cg_plan_mode",
     "rvk_laplacian_rows_nnz", "rvk_build_laplacian_rows", "rvk_comm_unique_id", "rvk_comm_init",
     "rvk_comm_destroy", "rvk_dcg_plan_create", "rvk_dcg_plan_destroy", "rvk_dcg_solve_dev",
-    "rvk_dcg_loopback_solve", "rvk_dcg_result", "rvk_tfqmr_plan_create",
+    "rvk_dcg_loopback_solve", "rvk_dcg_result", "rvk_dcg_window", "rvk_dcg_attach_peers",
+    "rvk_ipc_get_handle", "rvk_ipc_open_handle", "rvk_ipc_close_handle", "rvk_tfqmr_plan_create",
     "rvk_tfqmr_plan_destroy", "rvk_tfqmr_solve_dev", "rvk_tfqmr_result",
 ]
 
@@ -155,6 +157,11 @@ def lib():
         "rvk_dcg_solve_dev": (i, [vp, vp, vp]),
         "rvk_dcg_loopback_solve": (i, [C.POINTER(vp), i, C.POINTER(vp), C.POINTER(vp)]),
         "rvk_dcg_result": (i, [vp, vp, C.POINTER(CgInfo)]),
+        "rvk_dcg_window": (i, [vp, C.POINTER(vp), C.POINTER(C.c_size_t)]),
+        "rvk_dcg_attach_peers": (i, [vp, C.POINTER(vp), C.POINTER(Shard)]),
+        "rvk_ipc_get_handle": (i, [vp, vp, i]),
+        "rvk_ipc_open_handle": (i, [vp, C.POINTER(vp)]),
+        "rvk_ipc_close_handle": (i, [vp]),
         "rvk_tfqmr_plan_create": (i, [vp, C.POINTER(Csr), CgConfig, C.POINTER(vp)]),
         "rvk_tfqmr_plan_destroy": (i, [vp]),
         "rvk_tfqmr_solve_dev": (i, [vp, vp, vp]),

@@ -5,10 +5,15 @@ The global stencil grid is cut into contiguous slabs of planes (z-planes in
 vectors (z, p) carry one halo plane on each interior side, and its local CSR
 (assembled on the device by ``rvk_build_laplacian_rows``) indexes columns in
 that extended space.  The per-iteration exchange is the halo of z and p plus
-an allgather of the three dot-product partials, all issued by librvk on the
-solve stream (NCCL, or a single-device LOOPBACK that runs every shard on one
-GPU for testing).  ``torch.distributed`` is only used to broadcast NCCL's
-unique id.
+the three dot-product partials, all on the solve stream:
+
+* ``peer`` (default across GPUs): the kernels themselves store the halo
+  planes and partials into the neighbours' windows over NVLink and sync on
+  device flags (rvk_dcg_attach_peers) -- windows are shared with cudaIpc;
+* ``nccl``: ncclSend/Recv halos + ncclAllGather of partials between kernels;
+* loopback variants of both run every shard on ONE GPU for testing.
+
+``torch.distributed`` only moves setup bytes (NCCL id, cudaIpc handles).
 
 Everything here is plumbing around the C ABI (include/rvk.h); no compute.
 """
@@ -101,6 +106,19 @@ class ShardPlan:
         self.h = h
         ctx._deps.add(self)
 
+    def window(self) -> tuple[int, int]:
+        base, nbytes = C.c_void_p(), C.c_size_t()
+        rvk.check(rvk.lib().rvk_dcg_window(self.h, C.byref(base), C.byref(nbytes)))
+        return base.value, nbytes.value
+
+    def attach_peers(self, windows: list[int], shards: list[ShardSpec]):
+        """PEER backend: windows[q] = rank q's window as mapped on this device."""
+        n = len(shards)
+        W = (C.c_void_p * n)(*windows)
+        S = (rvk.Shard * n)(*[rvk.Shard(s.n_own, s.halo_lo, s.halo_hi, s.rank, s.nranks)
+                              for s in shards])
+        rvk.check(rvk.lib().rvk_dcg_attach_peers(self.h, W, S))
+
     def solve_dev(self, b: "rvk.DeviceArray", x: "rvk.DeviceArray"):
         rvk.check(rvk.lib().rvk_dcg_solve_dev(self.h, b.ptr, x.ptr))
 
@@ -130,21 +148,34 @@ class ShardPlan:
 
 
 def loopback_solve(ctx, dim, points, grid, nranks, b_host: np.ndarray, max_it=20, pc="jacobi",
-                   rtol=0.0, atol=0.0):
+                   rtol=0.0, atol=0.0, backend="gather", repeats=1):
     """All shards on one device (test path): returns (x, CgResult of shard 0,
-    per-shard results)."""
+    per-shard results).  backend "gather": D2D halo copies + one shared
+    gather buffer between kernels; "peer": the PEER kernels (in-kernel halo
+    pushes, partial broadcast, flag protocol) with every window on this GPU.
+    `repeats` > 1 re-solves on the same plans (exercises the solve counter
+    and the finish -> setup barrier of the flag protocol)."""
     shards = partition(dim, grid, nranks)
-    gather = rvk.DeviceArray(4 * nranks)
-    rvk.check(rvk.lib().rvk_set(ctx.h, 4 * nranks, 0.0, gather.ptr))
+    peer = backend == "peer"
+    gather = None
+    if not peer:
+        gather = rvk.DeviceArray(4 * nranks)
+        rvk.check(rvk.lib().rvk_set(ctx.h, 4 * nranks, 0.0, gather.ptr))
     mats = [local_laplacian(ctx, dim, points, grid, s) for s in shards]
     plans = [ShardPlan(ctx, mats[i], s, max_it, pc, rtol, atol, None,
-                       gather.ptr if nranks > 1 else None) for i, s in enumerate(shards)]
+                       gather.ptr if (gather is not None and nranks > 1) else None)
+             for i, s in enumerate(shards)]
+    if peer:
+        windows = [p.window()[0] for p in plans]
+        for p in plans:
+            p.attach_peers(windows, shards)
     bs = [rvk.DeviceArray.from_host(ctx, b_host[s.row_begin:s.row_end]) for s in shards]
     xs = [rvk.DeviceArray(s.n_own) for s in shards]
     P = (C.c_void_p * nranks)(*[p.h.value for p in plans])
     B = (C.c_void_p * nranks)(*[b.ptr for b in bs])
     X = (C.c_void_p * nranks)(*[x.ptr for x in xs])
-    rvk.check(rvk.lib().rvk_dcg_loopback_solve(P, nranks, B, X))
+    for _ in range(repeats):
+        rvk.check(rvk.lib().rvk_dcg_loopback_solve(P, nranks, B, X))
     results = [p.result(raise_breakdown=False) for p in plans]
     x = np.concatenate([xx.download(ctx) for xx in xs])
     for p in plans:
@@ -155,6 +186,37 @@ def loopback_solve(ctx, dim, points, grid, nranks, b_host: np.ndarray, max_it=20
 # ---------------------------------------------------------------------------
 # one process per GPU (torchrun)
 # ---------------------------------------------------------------------------
+def connect_peers(plan: ShardPlan, shards: list[ShardSpec], rank: int, world: int) -> list[int]:
+    """PEER backend across processes: exchange cudaIpc handles of every
+    rank's window (torch.distributed all_gather_object), map the peers'
+    windows on this device, attach.  Returns the mapped pointers (close with
+    disconnect_peers after a barrier)."""
+    import torch.distributed as dist
+
+    base, _ = plan.window()
+    h = (C.c_char * 64)()
+    rvk.check(rvk.lib().rvk_ipc_get_handle(base, h, 64))
+    handles = [None] * world
+    dist.all_gather_object(handles, bytes(h))
+    windows, opened = [], []
+    for q in range(world):
+        if q == rank:
+            windows.append(base)
+            continue
+        p = C.c_void_p()
+        rvk.check(rvk.lib().rvk_ipc_open_handle(handles[q], C.byref(p)))
+        windows.append(p.value)
+        opened.append(p.value)
+    plan.attach_peers(windows, shards)
+    dist.barrier()  # every rank attached (flags zeroed) before anyone solves
+    return opened
+
+
+def disconnect_peers(opened: list[int]):
+    for p in opened:
+        rvk.lib().rvk_ipc_close_handle(p)
+
+
 def init_comm(rank: int, world: int):
     """NCCL communicator: rank 0 makes the unique id, torch.distributed
     broadcasts it (the only thing torch does on this path)."""
@@ -175,14 +237,18 @@ def init_comm(rank: int, world: int):
 
 
 def bench_main(args, cfg):
-    """bench.py under torchrun: one shard per rank, NCCL halo + allgather."""
+    """bench.py under torchrun: one shard per rank.  Backend PEER (in-kernel
+    NVLink halo pushes + partial broadcast, no NCCL on the data path) unless
+    --comm nccl, or unless the PEER setup fails / its first solve differs
+    from the NCCL solve bit for bit (then NCCL, with the reason in the JSON)."""
     import json
-    import statistics
     import sys
-    import time
 
     import torch
     import torch.distributed as dist
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from bench import ClockSampler, peaks  # noqa: E402  (bench.py is the caller)
 
     rank = int(os.environ["RANK"])
     world = int(os.environ["WORLD_SIZE"])
@@ -205,7 +271,28 @@ def bench_main(args, cfg):
     full_seed = 0x9E3779B97F4A7C15
     rvk.check(rvk.lib().rvk_fill_rhs(ctx.h, (full_seed + sh.row_begin) & (2 ** 64 - 1), sh.n_own,
                                      b.ptr))
-    plan = ShardPlan(ctx, A, sh, 20, comm=comm)
+    nccl_plan = ShardPlan(ctx, A, sh, 20, comm=comm)
+    nccl_plan.solve_dev(b, x)
+    ref_hist = nccl_plan.result().hist
+    ref_x = x.download(ctx)
+
+    backend, fallback, opened, plan = "nccl", None, [], nccl_plan
+    if getattr(args, "comm", "peer") == "peer":
+        try:
+            peer_plan = ShardPlan(ctx, A, sh, 20)
+            opened = connect_peers(peer_plan, shards, rank, world)
+            peer_plan.solve_dev(b, x)
+            ok = np.array_equal(peer_plan.result().hist, ref_hist) and \
+                np.array_equal(x.download(ctx), ref_x)
+            err = None if ok else "PEER solve differs from the NCCL solve"
+        except Exception as e:  # noqa: BLE001 -- report and fall back, never hang
+            err, peer_plan = f"PEER setup failed: {e}".splitlines()[0][:200], None
+        flags = torch.tensor([0 if err is None else 1], device=f"cuda:{local}")
+        dist.all_reduce(flags)  # every rank takes the same backend
+        if int(flags.item()) == 0:
+            backend, plan = "peer", peer_plan
+        else:
+            fallback = err or "another rank's PEER check failed"
     for _ in range(args.warmup):
         plan.solve_dev(b, x)
     plan.result()
@@ -214,11 +301,12 @@ def bench_main(args, cfg):
     dist.barrier()
     torch.cuda.synchronize()
     syncs0 = rvk.host_syncs()
-    for k in range(args.steps):
-        ev0[k].record(stream)
-        plan.solve_dev(b, x)
-        ev1[k].record(stream)
-    stream.synchronize()
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            ev0[k].record(stream)
+            plan.solve_dev(b, x)
+            ev1[k].record(stream)
+        stream.synchronize()
     syncs = rvk.host_syncs() - syncs0
     dist.barrier()
     ms_local = sum(ev0[k].elapsed_time(ev1[k]) for k in range(args.steps)) / args.steps
@@ -226,10 +314,40 @@ def bench_main(args, cfg):
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
     res = plan.result()
+
+    # ---- e2e: pinned host b shard -> device, solve, x shard -> host (events) --
+    bh = torch.empty(sh.n_own, dtype=torch.float64, pin_memory=True)
+    xh = torch.empty(sh.n_own, dtype=torch.float64, pin_memory=True)
+    bh.numpy()[:] = b.download(ctx)
+    e0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    e1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    L = rvk.lib()
+    dist.barrier()
+    for k in range(args.steps):
+        e0[k].record(stream)
+        rvk.check(L.rvk_memcpy_h2d(ctx.h, b.ptr, bh.data_ptr(), 8 * sh.n_own))
+        plan.solve_dev(b, x)
+        rvk.check(L.rvk_memcpy_d2h(ctx.h, xh.data_ptr(), x.ptr, 8 * sh.n_own))
+        e1[k].record(stream)
+    stream.synchronize()
+    e2e_local = sum(e0[k].elapsed_time(e1[k]) for k in range(args.steps)) / args.steps
+    t = torch.tensor([e2e_local], device=f"cuda:{local}")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_ms = float(t.item())
+    plan.result()
+
     n_glob = int(np.prod(grid))
     nnz_glob = _global_nnz(dim, pts, grid)
     b_min = 20 * (12 * nnz_glob + 8 * (n_glob + 1) + 96 * n_glob) + 64 * n_glob
+    hbm_peak, peak_src = peaks()
+    per_gpu = b_min / world / (ms * 1e-3) / 1e9
+    launches = 3 + 2 * 20  # reset, setup, 20 x (K1, K2), finish  (our kernels, per rank)
     if rank == 0:
+        comm_desc = {"peer": "PEER: K1/K2 store halo planes + dot partials into the neighbours' "
+                             "windows over NVLink (cudaIpc), device flag sync; no NCCL on the "
+                             "data path",
+                     "nccl": "NCCL halo (ncclSend/Recv, 1 plane/neighbour, z and p) + "
+                             "ncclAllGather of dot partials between kernels"}[backend]
         out = {
             "metric": "20-iter Jacobi-CG solve time, achieved HBM GB/s vs peak, host syncs/iter",
             "value": round(ms, 4), "unit": "ms/solve", "n_gpus": world, "steps": args.steps,
@@ -239,15 +357,28 @@ def bench_main(args, cfg):
             "config": {"workload": f"{desc} row-sharded over {world} GPUs"
                                    + (f" (weak: global grid {grid})" if weak else ""),
                        "n": n_glob, "nnz": nnz_glob, "parallelism": f"rows{world}",
-                       "comm": "NCCL halo (1 plane/neighbour, z and p) + allgather of dot partials"},
+                       "comm": comm_desc, "comm_fallback": fallback,
+                       "l2": "no flush: per-GPU working set >> 126 MB L2"},
+            "roofline": {"bound": "hbm", "kernel": "whole sharded solve, per GPU (K1+K2+comm)",
+                         "achieved": round(per_gpu, 1), "peak": hbm_peak, "unit": "GB/s",
+                         "frac": round(per_gpu / hbm_peak, 4), "traffic": None,
+                         "peak_source": peak_src},
             "solve_roofline": {"alg_bytes_per_solve": b_min,
                                "achieved_aggregate_gbs": round(b_min / (ms * 1e-3) / 1e9, 1)},
             "host_syncs_per_iter": syncs / (args.steps * 20),
             "iterations": res.iterations,
-            "gpu_launches": None,
+            "e2e": {"value": round(e2e_ms, 4), "unit": "ms/solve",
+                    "h2d_bytes_per_step": 8 * n_glob, "d2h_bytes_per_step": 8 * n_glob},
+            "gpu_launches": launches * args.steps * world,
+            "cpu_baseline": None,
+            "clocks": clk.summary(),
         }
         print(json.dumps(out), flush=True)
+    dist.barrier()  # no rank frees a window a peer may still store into
     plan.close()
+    if plan is not nccl_plan:
+        nccl_plan.close()
+    disconnect_peers(opened)
     rvk.lib().rvk_comm_destroy(comm)
     dist.destroy_process_group()
 

@@ -24,14 +24,15 @@ def test_local_csr_matches_global_rows_bitexact(ctx, dim, pts, grid):
         assert np.array_equal(L.vals.download(ctx), A.vals[k0:k1])
 
 
+@pytest.mark.parametrize("backend", ["gather", "peer"])
 @pytest.mark.parametrize("P", [1, 2, 3, 4, 8])
 @pytest.mark.parametrize("dim,pts,grid", [(3, 7, (32, 32, 40)), (3, 27, (16, 16, 24)),
                                           (2, 5, (128, 96)), (2, 9, (64, 80))])
-def test_loopback_sharded_cg_vs_oracle(ctx, P, dim, pts, grid):
+def test_loopback_sharded_cg_vs_oracle(ctx, P, dim, pts, grid, backend):
     A = O.build_laplacian(dim, pts, grid)
     b = O.rhs(A.n_rows)
     ref = O.cg_solve(A, b, max_it=20)
-    x, res, per = loopback_solve(ctx, dim, pts, grid, P, b, max_it=20)
+    x, res, per = loopback_solve(ctx, dim, pts, grid, P, b, max_it=20, backend=backend)
     assert res.iterations == 20
     for r in per:  # every shard holds the identical scalar history
         assert np.array_equal(r.hist, res.hist)
@@ -39,21 +40,54 @@ def test_loopback_sharded_cg_vs_oracle(ctx, P, dim, pts, grid):
     assert np.linalg.norm(x - ref.x) / np.linalg.norm(ref.x) < 1e-10
 
 
-def test_loopback_rtol_exit_and_single_shard(ctx):
+@pytest.mark.parametrize("backend", ["gather", "peer"])
+def test_loopback_rtol_exit_and_single_shard(ctx, backend):
     dim, pts, grid = 2, 5, (48, 48)
     A = O.build_laplacian(dim, pts, grid)
     b = O.rhs(A.n_rows)
     ref = O.cg_solve(A, b, max_it=300, rtol=1e-7)
     for P in (1, 3):
-        x, res, _ = loopback_solve(ctx, dim, pts, grid, P, b, max_it=300, rtol=1e-7)
+        x, res, _ = loopback_solve(ctx, dim, pts, grid, P, b, max_it=300, rtol=1e-7,
+                                   backend=backend)
         assert res.state == rvk.CG_CONVERGED and res.iterations == ref.iterations
         assert np.linalg.norm(x - ref.x) / np.linalg.norm(ref.x) < 1e-10
 
 
-def test_loopback_headline_256cubed_4_shards(ctx):
+@pytest.mark.parametrize("P", [2, 5])
+def test_peer_loopback_bitwise_equals_gather_backend_and_resolves(ctx, P):
+    """The PEER kernels (in-kernel halo pushes, partial broadcast, flag
+    waits) produce exactly the gather backend's numbers -- same reduction
+    order -- and stay correct over repeated solves on the same plans (solve
+    counter + finish->setup barrier of the flag protocol)."""
+    dim, pts, grid = 3, 7, (24, 20, 30)
+    A = O.build_laplacian(dim, pts, grid)
+    b = O.rhs(A.n_rows)
+    xg, rg, _ = loopback_solve(ctx, dim, pts, grid, P, b, max_it=20, backend="gather")
+    xp, rp, per = loopback_solve(ctx, dim, pts, grid, P, b, max_it=20, backend="peer", repeats=3)
+    assert np.array_equal(rp.hist, rg.hist)
+    assert np.array_equal(xp, xg)
+    assert all(r.state == rvk.CG_RUNNING and r.iterations == 20 for r in per)
+
+
+def test_peer_loopback_early_exit_then_resolve(ctx):
+    """Converged early (kernels skip their signals), then solved again: the
+    finish kernel still releases every rank, so the next setup proceeds."""
+    dim, pts, grid = 2, 5, (40, 36)
+    A = O.build_laplacian(dim, pts, grid)
+    b = O.rhs(A.n_rows)
+    ref = O.cg_solve(A, b, max_it=400, rtol=1e-6)
+    x, res, per = loopback_solve(ctx, dim, pts, grid, 4, b, max_it=400, rtol=1e-6,
+                                 backend="peer", repeats=2)
+    assert res.state == rvk.CG_CONVERGED and res.iterations == ref.iterations
+    assert all(r.iterations == res.iterations for r in per)
+    assert np.linalg.norm(x - ref.x) / np.linalg.norm(ref.x) < 1e-10
+
+
+@pytest.mark.parametrize("backend", ["gather", "peer"])
+def test_loopback_headline_256cubed_4_shards(ctx, backend):
     A = O.build_laplacian(3, 7, (256, 256, 256))
     b = O.rhs(A.n_rows)
     ref = O.cg_solve(A, b, max_it=20)
-    x, res, _ = loopback_solve(ctx, 3, 7, (256, 256, 256), 4, b, max_it=20)
+    x, res, _ = loopback_solve(ctx, 3, 7, (256, 256, 256), 4, b, max_it=20, backend=backend)
     assert np.max(np.abs(res.hist - ref.hist) / ref.hist) < 1e-10
     assert np.linalg.norm(x - ref.x) / np.linalg.norm(ref.x) < 1e-10
