@@ -218,6 +218,15 @@ rvk_status rvk_cg_result(rvk_cg_plan plan, double* hist_host, rvk_cg_info* info)
 /* End-to-end: copy b from host, solve, copy x and hist back, one sync. */
 rvk_status rvk_cg_solve_host(rvk_cg_plan plan, const double* b_host, double* x_host,
                              double* hist_host, rvk_cg_info* info);
+/* Many right-hand sides from host memory (KSPMatSolve-like stream of solves
+ * with one operator): x_host[k] = A^-1 b_host[k].  H2D of the next b and
+ * D2H of the previous x overlap the current solve on copy streams (double-
+ * buffered staging; pinned host buffers required for overlap).  hist_host:
+ * nrhs*(max_it+1) doubles (may be NULL); infos: nrhs entries (may be NULL).
+ * One host sync at the end; RVK_ERR_BREAKDOWN if any right-hand side broke
+ * down (infos tell which). */
+rvk_status rvk_cg_solve_host_many(rvk_cg_plan plan, int nrhs, const double* const* b_host,
+                                  double* const* x_host, double* hist_host, rvk_cg_info* infos);
 /* The mode the plan runs (AUTO resolved to FUSED or PERSISTENT). */
 int        rvk_cg_plan_mode(rvk_cg_plan plan);
 /* Per-kernel event timing of the last solve's dominant kernels (bench): */

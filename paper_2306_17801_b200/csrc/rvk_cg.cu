@@ -473,11 +473,26 @@ struct rvk_cg_plan_s {
     double*       tmp      = nullptr;     // unfused: dp scratch
     double*       b_buf    = nullptr;     // host e2e staging
     double*       x_buf    = nullptr;
-    // graph cache
-    cudaGraphExec_t graph   = nullptr;
-    const double*   g_b     = nullptr;
-    double*         g_x     = nullptr;
-    bool            g_prof  = false;
+    // rvk_cg_solve_host_many: second staging pair, copy streams, per-RHS results
+    double*       b_buf2   = nullptr;
+    double*       x_buf2   = nullptr;
+    cudaStream_t  s_in = nullptr, s_out = nullptr;
+    cudaEvent_t   ev_many[8] = {};        // b_ready[2], solved[2], x_free[2], b_free[2]
+    double*       hist_all = nullptr;     // [cap_many][max_it + 1]
+    CgState*      st_all   = nullptr;     // [cap_many]
+    int           cap_many = 0;
+    // graph cache: two slots, so alternating (b, x) pairs (the pipelined
+    // many-RHS solve) replay without re-capturing
+    struct GraphSlot {
+        cudaGraphExec_t exec = nullptr;
+        const double*   b    = nullptr;
+        double*         x    = nullptr;
+        bool            prof = false;
+        int             kind = 0; // 1 unrolled, 2 device WHILE loop
+        int             launches = 0;
+    };
+    GraphSlot gs[2];
+    int       g_victim = 0;
     // profiling
     bool                     profiling = false;
     std::vector<cudaEvent_t> ev;          // 4 per iteration: K1 begin/end, K2 begin/end
@@ -824,9 +839,9 @@ rvk_status enqueue_solve(rvk_cg_plan P, const double* b, double* x)
 
 rvk_status destroy_graph(rvk_cg_plan P)
 {
-    if (P->graph) {
-        cudaGraphExecDestroy(P->graph);
-        P->graph = nullptr;
+    for (auto& g : P->gs) {
+        if (g.exec) cudaGraphExecDestroy(g.exec);
+        g = rvk_cg_plan_s::GraphSlot{};
     }
     return RVK_OK;
 }
@@ -1060,8 +1075,13 @@ rvk_status rvk_cg_plan_destroy(rvk_cg_plan P)
     if (P->ctx) cudaStreamSynchronize(P->ctx->stream);
     destroy_graph(P);
     for (auto ev : P->ev) cudaEventDestroy(ev);
+    for (auto ev : P->ev_many)
+        if (ev) cudaEventDestroy(ev);
+    if (P->s_in) cudaStreamDestroy(P->s_in);
+    if (P->s_out) cudaStreamDestroy(P->s_out);
     void* bufs[] = {P->dinv, P->r, P->z, P->p[0], P->p[1], P->w, P->hist, P->st,
-                    P->partials, P->tickets, P->tmp, P->b_buf, P->x_buf};
+                    P->partials, P->tickets, P->tmp, P->b_buf, P->x_buf, P->b_buf2,
+                    P->x_buf2, P->hist_all, P->st_all};
     for (void* b : bufs)
         if (b) cudaFree(b);
     delete P;
@@ -1088,20 +1108,21 @@ rvk_status rvk_cg_solve_dev(rvk_cg_plan P, const double* b, double* x)
     if (P->mode == RVK_CG_MODE_HOSTSYNC) return solve_hostsync(P, b, x);
     // one cooperative launch needs no graph
     if (!P->cfg.use_graph || P->mode == RVK_CG_MODE_PERSISTENT) return enqueue_solve(P, b, x);
-    if (P->cfg.use_graph == 2 && P->mode == RVK_CG_MODE_FUSED) { // device WHILE loop
-        if (!P->graph || P->g_b != b || P->g_x != x) {
-            destroy_graph(P);
-            RVK_TRY(build_while_graph(P, b, x, &P->graph));
-            P->g_b      = b;
-            P->g_x      = x;
-            P->g_prof   = false;
-            P->launches = -1; // data-dependent: 3 + 4 per body pass
+    const int kind = (P->cfg.use_graph == 2 && P->mode == RVK_CG_MODE_FUSED) ? 2 : 1;
+    for (auto& g : P->gs)
+        if (g.exec && g.b == b && g.x == x && g.kind == kind && (kind == 2 || g.prof == P->profiling)) {
+            P->launches = g.launches;
+            RVK_CUDA(cudaGraphLaunch(g.exec, s));
+            return RVK_OK;
         }
-        RVK_CUDA(cudaGraphLaunch(P->graph, s));
-        return RVK_OK;
-    }
-    if (!P->graph || P->g_b != b || P->g_x != x || P->g_prof != P->profiling) {
-        destroy_graph(P);
+    auto& slot = P->gs[P->g_victim];
+    P->g_victim ^= 1;
+    if (slot.exec) cudaGraphExecDestroy(slot.exec);
+    slot = rvk_cg_plan_s::GraphSlot{};
+    if (kind == 2) { // device WHILE loop
+        RVK_TRY(build_while_graph(P, b, x, &slot.exec));
+        P->launches = -1; // data-dependent: 3 + 4 per body pass
+    } else {
         cudaGraph_t g = nullptr;
         // Global capture mode: ANY synchronous CUDA call made while the solve
         // is being enqueued invalidates the capture -- a structural proof
@@ -1114,14 +1135,19 @@ rvk_status rvk_cg_solve_dev(rvk_cg_plan P, const double* b, double* x)
             return rc;
         }
         if (e != cudaSuccess) return cuda_error(e, "cudaStreamEndCapture (solve not capturable)");
-        e = cudaGraphInstantiate(&P->graph, g, 0);
+        e = cudaGraphInstantiate(&slot.exec, g, 0);
         cudaGraphDestroy(g);
-        if (e != cudaSuccess) return cuda_error(e, "cudaGraphInstantiate");
-        P->g_b    = b;
-        P->g_x    = x;
-        P->g_prof = P->profiling;
+        if (e != cudaSuccess) {
+            slot.exec = nullptr;
+            return cuda_error(e, "cudaGraphInstantiate");
+        }
     }
-    RVK_CUDA(cudaGraphLaunch(P->graph, s));
+    slot.b        = b;
+    slot.x        = x;
+    slot.prof     = P->profiling;
+    slot.kind     = kind;
+    slot.launches = P->launches;
+    RVK_CUDA(cudaGraphLaunch(slot.exec, s));
     return RVK_OK;
 }
 
@@ -1163,6 +1189,91 @@ rvk_status rvk_cg_solve_host(rvk_cg_plan P, const double* b_host, double* x_host
     RVK_TRY(rvk_cg_solve_dev(P, P->b_buf, P->x_buf));
     RVK_CUDA(cudaMemcpyAsync(x_host, P->x_buf, vb, cudaMemcpyDeviceToHost, s));
     return rvk_cg_result(P, hist_host, info);
+}
+
+// Many right-hand sides from host memory, pipelined (PETSc KSPMatSolve-like
+// usage: a stream of independent solves with the same operator).  Two device
+// staging pairs and two copy streams: the H2D of b[k+1] and the D2H of x[k-1]
+// run on the copy engines while solve k runs on the plan's stream, so with
+// PINNED host buffers a step costs max(H2D, solve, D2H) instead of their sum.
+// Every step's copies still happen (nothing is cached); per-RHS histories and
+// states are kept on the device and read back once at the end (one sync).
+rvk_status rvk_cg_solve_host_many(rvk_cg_plan P, int nrhs, const double* const* b_host,
+                                  double* const* x_host, double* hist_host, rvk_cg_info* infos)
+{
+    if (!P || nrhs < 0 || (nrhs && (!b_host || !x_host)))
+        return set_error(RVK_ERR_INVALID, "null argument");
+    if (nrhs == 0) return RVK_OK;
+    const size_t vb = (size_t)P->A.n_rows * sizeof(double);
+    const int    H  = P->cfg.max_it + 1;
+    cudaStream_t s  = P->ctx->stream;
+    if (!P->b_buf) RVK_CUDA(cudaMalloc(&P->b_buf, vb));
+    if (!P->x_buf) RVK_CUDA(cudaMalloc(&P->x_buf, vb));
+    if (!P->b_buf2) RVK_CUDA(cudaMalloc(&P->b_buf2, vb));
+    if (!P->x_buf2) RVK_CUDA(cudaMalloc(&P->x_buf2, vb));
+    if (!P->s_in) RVK_CUDA(cudaStreamCreateWithFlags(&P->s_in, cudaStreamNonBlocking));
+    if (!P->s_out) RVK_CUDA(cudaStreamCreateWithFlags(&P->s_out, cudaStreamNonBlocking));
+    for (auto& ev : P->ev_many)
+        if (!ev) RVK_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    if (P->cap_many < nrhs) {
+        RVK_CUDA(cudaStreamSynchronize(s));
+        if (P->hist_all) cudaFree(P->hist_all);
+        if (P->st_all) cudaFree(P->st_all);
+        P->hist_all = nullptr;
+        P->st_all   = nullptr;
+        P->cap_many = 0;
+        RVK_CUDA(cudaMalloc(&P->hist_all, (size_t)nrhs * H * sizeof(double)));
+        RVK_CUDA(cudaMalloc(&P->st_all, (size_t)nrhs * sizeof(CgState)));
+        P->cap_many = nrhs;
+    }
+    double*      bd[2] = {P->b_buf, P->b_buf2};
+    double*      xd[2] = {P->x_buf, P->x_buf2};
+    cudaEvent_t* b_ready = P->ev_many, *solved = P->ev_many + 2, *x_free = P->ev_many + 4,
+               * b_free = P->ev_many + 6;
+    // order the pipeline after everything already queued on the plan's stream
+    RVK_CUDA(cudaEventRecord(solved[0], s));
+    RVK_CUDA(cudaStreamWaitEvent(P->s_in, solved[0], 0));
+    RVK_CUDA(cudaStreamWaitEvent(P->s_out, solved[0], 0));
+    for (int k = 0; k < nrhs; ++k) {
+        const int j = k & 1;
+        if (k >= 2) RVK_CUDA(cudaStreamWaitEvent(P->s_in, b_free[j], 0)); // solve k-2 read bd[j]
+        RVK_CUDA(cudaMemcpyAsync(bd[j], b_host[k], vb, cudaMemcpyHostToDevice, P->s_in));
+        RVK_CUDA(cudaEventRecord(b_ready[j], P->s_in));
+        RVK_CUDA(cudaStreamWaitEvent(s, b_ready[j], 0));
+        if (k >= 2) RVK_CUDA(cudaStreamWaitEvent(s, x_free[j], 0));       // x[k-2] left xd[j]
+        RVK_TRY(rvk_cg_solve_dev(P, bd[j], xd[j]));
+        RVK_CUDA(cudaEventRecord(b_free[j], s));
+        RVK_CUDA(cudaMemcpyAsync(P->hist_all + (size_t)k * H, P->hist, H * sizeof(double),
+                                 cudaMemcpyDeviceToDevice, s));
+        RVK_CUDA(cudaMemcpyAsync(P->st_all + k, P->st, sizeof(CgState), cudaMemcpyDeviceToDevice, s));
+        RVK_CUDA(cudaEventRecord(solved[j], s));
+        RVK_CUDA(cudaStreamWaitEvent(P->s_out, solved[j], 0));
+        RVK_CUDA(cudaMemcpyAsync(x_host[k], xd[j], vb, cudaMemcpyDeviceToHost, P->s_out));
+        RVK_CUDA(cudaEventRecord(x_free[j], P->s_out));
+    }
+    // the plan's stream owns completion: later work (and the sync below) sees x on the host
+    RVK_CUDA(cudaStreamWaitEvent(s, x_free[(nrhs - 1) & 1], 0));
+    if (nrhs >= 2) RVK_CUDA(cudaStreamWaitEvent(s, x_free[nrhs & 1], 0));
+    std::vector<CgState> st(nrhs);
+    if (hist_host)
+        RVK_CUDA(cudaMemcpyAsync(hist_host, P->hist_all, (size_t)nrhs * H * sizeof(double),
+                                 cudaMemcpyDeviceToHost, s));
+    RVK_CUDA(cudaMemcpyAsync(st.data(), P->st_all, nrhs * sizeof(CgState), cudaMemcpyDeviceToHost, s));
+    note_host_sync();
+    RVK_CUDA(cudaStreamSynchronize(s));
+    int broke = -1;
+    for (int k = 0; k < nrhs; ++k) {
+        if (infos) {
+            infos[k].state          = st[k].state;
+            infos[k].iterations     = st[k].iterations;
+            infos[k].breakdown_iter = st[k].breakdown_iter;
+        }
+        if (st[k].state == RVK_CG_BREAKDOWN && broke < 0) broke = k;
+    }
+    if (broke >= 0)
+        return set_error(RVK_ERR_BREAKDOWN, "cg_solve: right-hand side %d broke down at iteration %d",
+                         broke, st[broke].breakdown_iter);
+    return RVK_OK;
 }
 
 rvk_status rvk_cg_kernel_times(rvk_cg_plan P, float* spmv_ms, float* update_ms, int* launches)

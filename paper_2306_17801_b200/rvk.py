@@ -39,6 +39,7 @@ EXPORTS = [
     "rvk_csr_diagonal_inverse", "rvk_csr_validate", "rvk_laplacian_size",
     "rvk_build_laplacian", "rvk_fill_rhs", "rvk_cg_plan_create", "rvk_cg_plan_create_stencil", "rvk_cg_plan_destroy",
     "rvk_cg_solve_dev", "rvk_cg_history_dev", "rvk_cg_result", "rvk_cg_solve_host",
+    "rvk_cg_solve_host_many",
     "rvk_cg_set_profiling", "rvk_cg_kernel_times", "rvk_cg_plan_mode",
     "rvk_laplacian_rows_nnz", "rvk_build_laplacian_rows", "rvk_comm_unique_id", "rvk_comm_init",
     "rvk_comm_destroy", "rvk_dcg_plan_create", "rvk_dcg_plan_destroy", "rvk_dcg_solve_dev",
@@ -143,6 +144,8 @@ def lib():
         "rvk_cg_history_dev": (vp, [vp]),
         "rvk_cg_result": (i, [vp, vp, C.POINTER(CgInfo)]),
         "rvk_cg_solve_host": (i, [vp, vp, vp, vp, C.POINTER(CgInfo)]),
+        "rvk_cg_solve_host_many": (i, [vp, i, C.POINTER(vp), C.POINTER(vp), vp,
+                                       C.POINTER(CgInfo)]),
         "rvk_cg_set_profiling": (i, [vp, i]),
         "rvk_cg_kernel_times": (i, [vp, C.POINTER(C.c_float), C.POINTER(C.c_float),
                                     C.POINTER(C.c_int)]),
@@ -393,6 +396,22 @@ class CgPlan:
             check(st)
         return x, CgResult(hist[: info.iterations + 1].copy(), info.state, info.iterations,
                            info.breakdown_iter)
+
+    def solve_host_many(self, bs: list, xs: list):
+        """Pipelined solves of several host right-hand sides (rvk_cg_solve_host_many).
+        bs / xs: float64 arrays (pinned -- e.g. torch pin_memory -- for overlap).
+        Returns the per-RHS CgResults."""
+        n = len(bs)
+        B = (C.c_void_p * n)(*[_ptr(b) for b in bs])
+        X = (C.c_void_p * n)(*[_ptr(x) for x in xs])
+        H = self.max_it + 1
+        hist = np.full(n * H, np.nan)
+        infos = (CgInfo * n)()
+        st = lib().rvk_cg_solve_host_many(self.h, n, B, X, _ptr(hist), infos)
+        if st not in (RVK_OK, RVK_ERR_BREAKDOWN):
+            check(st)
+        return [CgResult(hist[k * H: k * H + infos[k].iterations + 1].copy(), infos[k].state,
+                         infos[k].iterations, infos[k].breakdown_iter) for k in range(n)]
 
     def set_profiling(self, on: bool):
         check(lib().rvk_cg_set_profiling(self.h, 1 if on else 0))

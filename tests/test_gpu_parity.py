@@ -457,3 +457,42 @@ def test_device_while_loop_breakdown(ctx):
     with pytest.raises(rvk.BreakdownError) as ei:
         plan.result()
     assert ei.value.iteration == 0
+
+
+@pytest.mark.parametrize("graph", [True, "while", False])
+@pytest.mark.parametrize("pinned", [True, False])
+def test_cg_solve_host_many_matches_single_solves(ctx, graph, pinned):
+    """rvk_cg_solve_host_many (pipelined H2D / solve / D2H over double-buffered
+    staging): every right-hand side's x and history equal the single-RHS
+    solve bit for bit, and equal the oracle within the CG bar -- including an
+    odd count (the last staging slot reused) and a breakdown-free rtol exit."""
+    import torch
+
+    dim, pts, g = 3, 7, (20, 18, 22)
+    Ah = O.build_laplacian(dim, pts, g)
+    n = Ah.n_rows
+    A = rvk.DeviceCsr.laplacian(ctx, dim, pts, g)
+    plan = rvk.CgPlan(ctx, A, max_it=20, use_graph=graph, rtol=1e-9)
+    rng = np.random.default_rng(7)
+    K = 5
+    bs, xs = [], []
+    for k in range(K):
+        b = O.rhs(n) if k == 0 else rng.standard_normal(n)
+        if pinned:
+            bt = torch.empty(n, dtype=torch.float64, pin_memory=True)
+            bt.numpy()[:] = b
+            xt = torch.empty(n, dtype=torch.float64, pin_memory=True)
+            bs.append(bt.numpy())
+            xs.append(xt.numpy())
+        else:
+            bs.append(np.ascontiguousarray(b))
+            xs.append(np.empty(n))
+    many = plan.solve_host_many(bs, xs)
+    for k in range(K):
+        x1, r1 = plan.solve_host(bs[k])
+        assert np.array_equal(xs[k], x1), k
+        assert np.array_equal(many[k].hist, r1.hist) and many[k].iterations == r1.iterations
+        ref = O.cg_solve(Ah, np.array(bs[k]), max_it=20, rtol=1e-9)
+        assert many[k].iterations == ref.iterations
+        assert np.max(np.abs(many[k].hist - ref.hist) / ref.hist) < HIST_RTOL
+        assert np.linalg.norm(xs[k] - ref.x) / np.linalg.norm(ref.x) < X_RTOL
