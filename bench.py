@@ -34,6 +34,8 @@ CONFIGS = {
     "7pt256": (3, 7, (256, 256, 256), "3D 7-point Laplacian 256^3"),
     "27pt256": (3, 27, (256, 256, 256), "3D 27-point Laplacian 256^3"),
     "7pt768": (3, 7, (768, 768, 768), "3D 7-point Laplacian 768^3"),
+    "7pt384": (3, 7, (384, 384, 384), "3D 7-point Laplacian 384^3 (plane-size study)"),
+    "7pt512": (3, 7, (512, 512, 512), "3D 7-point Laplacian 512^3 (plane-size study)"),
     "5pt64": (2, 5, (64, 64), "2D 5-point Laplacian 64x64 (latency sweep)"),
     "5pt128": (2, 5, (128, 128), "2D 5-point Laplacian 128x128 (latency sweep)"),
     "5pt256": (2, 5, (256, 256), "2D 5-point Laplacian 256x256 (latency sweep)"),

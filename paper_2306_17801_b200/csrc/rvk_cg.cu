@@ -424,6 +424,10 @@ rvk_status csr_windows(cudaStream_t s, const rvk_csr& A, SpmvWindows* out)
         W.lead_lo  = bands.back().first;
         W.lead_hi  = bands.back().second;
     }
+    if (!bands.empty()) {
+        W.trail_lo = bands.front().first;
+        W.trail_hi = bands.front().second;
+    }
     bool fits = (int)bands.size() <= kSpmvMaxWin;
     for (auto& b : bands) fits = fits && b.second - b.first <= kMaxBand;
     if (fits) {
@@ -947,13 +951,17 @@ rvk_status rvk_cg_plan_create(rvk_ctx ctx, const rvk_csr* A, rvk_cg_config cfg, 
     // lookup made the consumers issue-bound); the 3D stencils have > 4 bands.
     SpmvWindows win;
     if (csr_windows(ctx->stream, *A, &win) != RVK_OK) win = SpmvWindows{};
+    const SpmvWindows bands = win; // the band scan, before the opt-in/out knobs
     if (!std::getenv("RVK_WINDOWS")) win.n = 0;
     if (std::getenv("RVK_NO_PREFETCH")) win.has_lead = false;
     P->sa        = make_spmv_args(*A, maxlen, &win, 2);
+    spmv_set_order(P->sa, bands, A->nnz, 2, sm_count());
     if (std::getenv("RVK_DEBUG")) {
-        std::fprintf(stderr, "[rvk] plan n=%lld nnz=%lld R=%d stages=%d groups=%d cap=%d nwin=%d",
+        std::fprintf(stderr, "[rvk] plan n=%lld nnz=%lld R=%d stages=%d groups=%d cap=%d nwin=%d "
+                             "order=%s(tiles/plane=%lld tiles/chunk=%lld)",
                      (long long)A->n_rows, (long long)A->nnz, P->sa.R, P->sa.stages, P->sa.groups,
-                     P->sa.cap, P->sa.nwin);
+                     P->sa.cap, P->sa.nwin, P->sa.ord_tc ? "chunked" : "row",
+                     (long long)P->sa.ord_tp, (long long)P->sa.ord_tc);
         for (int w = 0; w < P->sa.nwin; ++w)
             std::fprintf(stderr, " [%lld,%lld]@%d", (long long)P->sa.win_lo[w],
                          (long long)P->sa.win_hi[w], P->sa.win_base[w]);

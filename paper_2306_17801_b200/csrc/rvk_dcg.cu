@@ -780,9 +780,11 @@ rvk_status rvk_dcg_plan_create(rvk_ctx ctx, const rvk_csr* A, rvk_shard sh, rvk_
     P->cfg         = cfg;
     SpmvWindows win; // x-windows opt-in, leading-edge prefetch default (see rvk_cg.cu)
     if (csr_windows(ctx->stream, *A, &win) != RVK_OK) win = SpmvWindows{};
+    const SpmvWindows bands = win; // the band scan, before the opt-in/out knobs
     if (!std::getenv("RVK_WINDOWS")) win.n = 0;
     if (std::getenv("RVK_NO_PREFETCH")) win.has_lead = false;
     P->sa          = make_spmv_args(*A, maxlen, &win, 2);
+    spmv_set_order(P->sa, bands, A->nnz, 2, sm_count());
     P->upd_grid    = resident_grid(k_dcg_update<true, true>, kUpdThreads, sh.n_own);
     P->owns_gather = shared_gather == nullptr;
     P->gather      = shared_gather;

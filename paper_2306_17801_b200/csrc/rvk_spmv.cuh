@@ -40,6 +40,8 @@
 
 #include "rvk_common.cuh"
 
+#include <cstdlib>
+#include <cstring>
 #include <type_traits>
 
 namespace rvk {
@@ -75,6 +77,9 @@ struct SpmvWindows {
     // tile touches FIRST in a row-ordered sweep -- prefetched into L2 one tile ahead
     bool    has_lead = false;
     int64_t lead_lo = 0, lead_hi = 0;
+    // lowest diagonal band: (lead centre - trail centre) / 2 = the plane
+    // stride of a symmetric stencil, in any (shifted, halo-extended) column space
+    int64_t trail_lo = 0, trail_hi = 0;
 };
 
 struct SpmvArgs {
@@ -93,6 +98,13 @@ struct SpmvArgs {
     int            win_elems;             // doubles per source per stage
     int            pf;                    // 1: L2-prefetch the next tile's leading-edge columns
     int64_t        pf_lo, pf_hi;          // ... the band [pf_lo, pf_hi] of (col - row)
+    // tile ORDER (spmv_set_order): ord_tc == 0 = row order; else 2.5D
+    // blocking -- each plane (ord_tp tiles) is cut into chunks of ord_tc
+    // consecutive tiles, and the grid sweeps chunk 0 through all ord_np
+    // planes, then chunk 1, ...  The frontier stays one contiguous chunk of
+    // one plane, and the +-plane gathers are reused from L2 one CHUNK later
+    // instead of one plane later
+    int64_t        ord_tp, ord_tc, ord_np;
     const int64_t* off;
     const int32_t* cols;
     const double*  vals;
@@ -107,6 +119,16 @@ struct TailArgs {
 };
 
 __host__ __device__ inline int align16(int64_t b) { return (int)((b + 15) & ~int64_t(15)); }
+
+// Virtual tile index -> tile (row block) index.
+__host__ __device__ __forceinline__ int64_t spmv_tile(const SpmvArgs& a, int64_t v)
+{
+    if (!a.ord_tc) return v;
+    const int64_t per_chunk = a.ord_np * a.ord_tc;
+    const int64_t c = v / per_chunk, rem = v - c * per_chunk;
+    const int64_t k = rem / a.ord_tc, u = rem - k * a.ord_tc;
+    return k * a.ord_tp + c * a.ord_tc + u;
+}
 
 // Tile geometry: the largest R (power of two, <= 1024) whose worst-case slab
 // (CSR rows of max_row_len, plus nsrc x-windows when W is given) fits a stage
@@ -175,6 +197,52 @@ inline SpmvArgs make_spmv_args(const rvk_csr& A, int64_t max_row_len,
            a.R * a.groups * 2 <= kSpmvConsumers)
         a.groups *= 2;
     return a;
+}
+
+// Tile order policy (plan time).  Row order is the default: it keeps the
+// chip-wide frontier one contiguous window.  Opt-in (RVK_CHUNK_MB=<budget>):
+// when two planes of streamed bytes (CSR + vectors) exceed the budget, the
+// planes are cut into the fewest chunks that bring two CHUNKS under it
+// (>= RVK_CHUNK_MIN_TILES tiles per chunk, default one per SM).  Measured on
+// B200 at 768^3 (profiles/r01_summary.md): chunking removes the -plane
+// re-reads (K1 DRAM reads 55.3 -> 49.8 GB vs 48.9 algorithmic) but the DRAM
+// throughput drops more (5.29 -> 4.51 TB/s), and a pure pencil sweep (one
+// tile per plane) is slower still -- so it stays off by default.  The plane
+// is half the distance between the centres of the highest and lowest
+// diagonal bands (7/5-point: exactly nx*ny / nx; 27/9-point: the bands
+// around them; also in a shard's halo-extended column space).
+// RVK_TILE_ORDER=row forces row order.
+inline void spmv_set_order(SpmvArgs& a, const SpmvWindows& W, int64_t nnz, int nsrc, int sms)
+{
+    a.ord_tp = a.ord_tc = a.ord_np = 0;
+    const char* env = std::getenv("RVK_TILE_ORDER");
+    if (env && std::strcmp(env, "row") == 0) return;
+    if (!W.has_lead || W.lead_lo <= 0 || a.n_rows <= 0) return;
+    const int64_t plane = ((W.lead_lo + W.lead_hi) - (W.trail_lo + W.trail_hi)) / 4;
+    if (plane < a.R || plane % a.R) return;
+    const int64_t tp = plane / a.R;
+    if (a.n_tiles % tp || a.n_tiles / tp < 3) return;
+    const char*  mb        = std::getenv("RVK_CHUNK_MB");
+    if (!mb) return;
+    const double budget    = std::atof(mb) * 1024 * 1024;
+    const double row_bytes = 12.0 * (double)nnz / (double)a.n_rows + 8.0 + 16.0 * (nsrc + 1);
+    if (2.0 * (double)plane * row_bytes <= budget) return; // row order already reuses
+    const char*   mt     = std::getenv("RVK_CHUNK_MIN_TILES"); // tests: chunk small grids
+    const int64_t min_tc = mt ? std::atoll(mt) : sms;
+    // fewest chunks under the budget; if none, the smallest chunk allowed
+    int64_t best = 0;
+    for (int64_t cp = 2; cp <= tp; ++cp) {
+        if (tp % cp) continue;
+        const int64_t tc = tp / cp;
+        if (tc < min_tc) break;
+        best = tc;
+        if (2.0 * (double)(tc * a.R) * row_bytes <= budget) break;
+    }
+    if (best) {
+        a.ord_tp = tp;
+        a.ord_tc = best;
+        a.ord_np = a.n_tiles / tp;
+    }
 }
 
 // Epilogue operands of row i, loaded before the row's gathers so their
@@ -357,19 +425,22 @@ __global__ void __launch_bounds__(kSpmvThreads, 1) k_spmv_tma(SpmvArgs A, Op op_
         if (tid == 0) {
             const uint64_t pol_stream = policy_evict_first(); // CSR: read once
             const uint64_t pol_keep   = policy_evict_last();  // x-windows: reused by 3 tiles
-            int64_t        t   = blockIdx.x;
+            int64_t        v   = blockIdx.x;
             int64_t        k0 = 0, k1 = 0; // slab bounds, prefetched one tile ahead
-            if (t < A.n_tiles) {
+            if (v < A.n_tiles) {
+                const int64_t t = spmv_tile(A, v);
                 k0 = __ldg(A.off + t * A.R);
                 k1 = __ldg(A.off + min(t * A.R + A.R, A.n_rows));
             }
-            for (int j = 0; t < A.n_tiles; ++j, t += gridDim.x) {
+            for (int j = 0; v < A.n_tiles; ++j, v += gridDim.x) {
                 const int s = j % A.stages;
                 if (j >= A.stages) mbar_wait(&empty[s], ((j / A.stages) - 1) & 1);
+                const int64_t t  = spmv_tile(A, v);
                 const int64_t r0 = t * A.R;
                 const int64_t r1 = min(r0 + A.R, A.n_rows);
                 const int64_t ck0 = k0, ck1 = k1;
-                const int64_t tn  = t + gridDim.x;
+                const int64_t vn  = v + gridDim.x;
+                const int64_t tn  = vn < A.n_tiles ? spmv_tile(A, vn) : A.n_tiles;
                 if (tn < A.n_tiles) {
                     k0 = __ldg(A.off + tn * A.R);
                     k1 = __ldg(A.off + min(tn * A.R + A.R, A.n_rows));
@@ -446,9 +517,10 @@ __global__ void __launch_bounds__(kSpmvThreads, 1) k_spmv_tma(SpmvArgs A, Op op_
     constexpr int NS = spmv_sums<Op>::value;
     static_assert(NS >= 1 && NS <= 4, "at most 4 fused reductions");
     spmv_acc_t<Op> acc{};
-    int64_t   t     = blockIdx.x + (int64_t)group * gridDim.x;
-    for (int j = group; t < A.n_tiles; j += A.groups, t += (int64_t)A.groups * gridDim.x) {
+    int64_t   v     = blockIdx.x + (int64_t)group * gridDim.x;
+    for (int j = group; v < A.n_tiles; j += A.groups, v += (int64_t)A.groups * gridDim.x) {
         const int s = j % A.stages;
+        const int64_t t = spmv_tile(A, v);
         mbar_wait(&full[s], (j / A.stages) & 1);
         const int64_t r0   = t * A.R;
         const int     rows = (int)min((int64_t)A.R, A.n_rows - r0);

@@ -600,9 +600,11 @@ rvk_status rvk_tfqmr_plan_create(rvk_ctx ctx, const rvk_csr* A, rvk_cg_config cf
     P->cfg = cfg;
     SpmvWindows win;
     if (csr_windows(ctx->stream, *A, &win) != RVK_OK) win = SpmvWindows{};
+    const SpmvWindows bands = win; // the band scan, before the opt-in/out knobs
     win.n = 0; // leading-edge prefetch only
     P->fused    = cfg.mode != RVK_CG_MODE_UNFUSED;
     P->sa       = make_spmv_args(*A, maxlen, &win, P->fused ? 2 : 1);
+    spmv_set_order(P->sa, bands, A->nnz, P->fused ? 2 : 1, sm_count());
     P->upd_grid = resident_grid(k_tfq_merge<true>, kTfqThreads, (A->n_rows + 1) / 2);
     const size_t vb = (size_t)A->n_rows * 8;
     cudaError_t  e  = cudaSuccess;
