@@ -89,6 +89,7 @@ struct SpmvArgs {
     int            R;        // rows per tile (multiple of 32)
     int            stages;   // ring depth (<= kSpmvMaxStages)
     int            groups;   // consumer groups working on distinct stages (divides stages)
+    int            consumers; // consumer threads (multiple of 32, <= kSpmvConsumers)
     int            cap;      // nonzeros per stage
     int            off_bytes, val_bytes, col_bytes, stage_bytes; // [off | vals | cols | windows]
     int            nwin;                  // 0: no x-windows
@@ -192,10 +193,24 @@ inline SpmvArgs make_spmv_args(const rvk_csr& A, int64_t max_row_len,
     a.pf_lo   = a.pf ? W->lead_lo : 0;
     a.pf_hi   = a.pf ? W->lead_hi : 0;
     // enough groups that every consumer thread owns a row of some tile
-    a.groups = 1;
-    while (a.groups * 2 <= a.stages && a.stages % (a.groups * 2) == 0 &&
-           a.R * a.groups * 2 <= kSpmvConsumers)
-        a.groups *= 2;
+    auto set_groups = [&] {
+        a.groups = 1;
+        while (a.groups * 2 <= a.stages && a.stages % (a.groups * 2) == 0 &&
+               a.R * a.groups * 2 <= a.consumers)
+            a.groups *= 2;
+    };
+    a.consumers = kSpmvConsumers;
+    set_groups();
+    // Long rows (short tiles): every ring stage is consumed at once, so the
+    // producer has no stage to fill ahead.  Opt-in (RVK_SPMV_SLACK=1): halve
+    // the consumer warps so half the ring is always in flight.  Measured
+    // slower on B200 (27-point 256^3 K1 1288 vs 1066 us): the gathers need
+    // the thread-level parallelism more than the TMA needs the slack.
+    const char* slack = std::getenv("RVK_SPMV_SLACK");
+    if (ok && a.groups == a.stages && a.stages >= 2 && slack && slack[0] == '1') {
+        a.consumers = kSpmvConsumers / 2;
+        set_groups();
+    }
     return a;
 }
 
@@ -414,7 +429,7 @@ __global__ void __launch_bounds__(kSpmvThreads, 1) k_spmv_tma(SpmvArgs A, Op op_
     if (tid == 0) {
         for (int s = 0; s < A.stages; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], kSpmvConsumerWarps / A.groups);
+            mbar_init(&empty[s], (A.consumers / 32) / A.groups);
         }
         fence_mbar_init();
     }
@@ -512,7 +527,7 @@ __global__ void __launch_bounds__(kSpmvThreads, 1) k_spmv_tma(SpmvArgs A, Op op_
     // NG groups of GS threads; group q takes the tiles j with j % NG == q
     // (NG divides the ring depth, so a group always owns the same stages).
     const int ctid  = tid - 32;
-    const int gs    = kSpmvConsumers / A.groups;
+    const int gs    = A.consumers / A.groups;
     const int group = ctid / gs, gtid = ctid % gs;
     constexpr int NS = spmv_sums<Op>::value;
     static_assert(NS >= 1 && NS <= 4, "at most 4 fused reductions");
@@ -561,13 +576,13 @@ __global__ void __launch_bounds__(kSpmvThreads, 1) k_spmv_tma(SpmvArgs A, Op op_
 #pragma unroll
             for (int j = 0; j < NS; ++j) v[j] = acc.v[j];
         }
-        block_sum<NS>(v, red, ctid, kSpmvConsumers, 1);
+        block_sum<NS>(v, red, ctid, A.consumers, 1);
         if (ctid == 0) {
 #pragma unroll
             for (int j = 0; j < NS; ++j) tail.partials[(size_t)blockIdx.x * NS + j] = v[j];
         }
-        if (!last_block<spmv_sys_fence<Op>::value>(tail.ticket, ctid, flag, kSpmvConsumers, 1)) return;
-        fold_partials<NS>(tail.partials, gridDim.x, v, red, ctid, kSpmvConsumers, 1);
+        if (!last_block<spmv_sys_fence<Op>::value>(tail.ticket, ctid, flag, A.consumers, 1)) return;
+        fold_partials<NS>(tail.partials, gridDim.x, v, red, ctid, A.consumers, 1);
         if (ctid == 0) {
             if constexpr (NS == 1) op.tail(v[0]);
             else op.tail(v);
@@ -619,7 +634,7 @@ rvk_status launch_spmv(cudaStream_t stream, const SpmvArgs& a, const Op& op, Tai
                                       (int)(kSpmvHeaderBytes + kSpmvStageBudget)));
         configured = true;
     }
-    k_spmv_tma<Op><<<grid, kSpmvThreads, a.smem_bytes(), stream>>>(a, op, tail);
+    k_spmv_tma<Op><<<grid, 32 + a.consumers, a.smem_bytes(), stream>>>(a, op, tail);
     RVK_CHECK_LAUNCH("k_spmv_tma");
     return RVK_OK;
 }
