@@ -483,6 +483,7 @@ def run_gpu(args, cfg):
                            "update_kernel_gbs": round(k2_gbs, 1),
                            "b_ref_gbs": round(bm["b_ref_solve"] / (ms * 1e-3) / 1e9, 1)},
         "host_syncs_per_iter": syncs / (args.steps * MAX_IT),
+        "iters_per_s": round(MAX_IT / (ms * 1e-3), 1),
         "e2e": {"value": round(e2e_ms, 4), "unit": "ms/solve", "h2d_bytes_per_step": 8 * n,
                 "d2h_bytes_per_step": 8 * n + 8 * (MAX_IT + 1) + 64,
                 "api": "rvk_cg_solve_host_many: K right-hand sides from pinned host memory, "

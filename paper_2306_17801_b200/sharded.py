@@ -253,8 +253,18 @@ def bench_main(args, cfg):
     rank = int(os.environ["RANK"])
     world = int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
+    # RVK_SHARED_GPU=1 (functional check on a 1-GPU box): every rank on GPU 0,
+    # gloo bootstrap, PEER only (NCCL refuses two ranks on one device);
+    # contexts time-slice, so the timings are meaningless -- the JSON says so
+    shared = os.environ.get("RVK_SHARED_GPU") == "1"
+    if shared:
+        local = 0
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    if shared:
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    tdev = "cpu" if shared else f"cuda:{local}"
     dim, pts, grid, desc = cfg
     weak = args.config != "7pt768"
     if weak:  # every GPU keeps the single-GPU workload: stack slabs along the slowest axis
@@ -263,7 +273,7 @@ def bench_main(args, cfg):
     sh = shards[rank]
     stream = torch.cuda.Stream()
     ctx = rvk.Ctx(stream.cuda_stream)
-    comm = init_comm(rank, world)
+    comm = None if shared else init_comm(rank, world)
     A = local_laplacian(ctx, dim, pts, grid, sh)
     b = rvk.DeviceArray(sh.n_own)
     x = rvk.DeviceArray(sh.n_own)
@@ -271,23 +281,27 @@ def bench_main(args, cfg):
     full_seed = 0x9E3779B97F4A7C15
     rvk.check(rvk.lib().rvk_fill_rhs(ctx.h, (full_seed + sh.row_begin) & (2 ** 64 - 1), sh.n_own,
                                      b.ptr))
-    nccl_plan = ShardPlan(ctx, A, sh, 20, comm=comm)
-    nccl_plan.solve_dev(b, x)
-    ref_hist = nccl_plan.result().hist
-    ref_x = x.download(ctx)
+    nccl_plan = ref_hist = ref_x = None
+    if not shared:
+        nccl_plan = ShardPlan(ctx, A, sh, 20, comm=comm)
+        nccl_plan.solve_dev(b, x)
+        ref_hist = nccl_plan.result().hist
+        ref_x = x.download(ctx)
 
     backend, fallback, opened, plan = "nccl", None, [], nccl_plan
-    if getattr(args, "comm", "peer") == "peer":
+    if shared or getattr(args, "comm", "peer") == "peer":
         try:
             peer_plan = ShardPlan(ctx, A, sh, 20)
             opened = connect_peers(peer_plan, shards, rank, world)
             peer_plan.solve_dev(b, x)
-            ok = np.array_equal(peer_plan.result().hist, ref_hist) and \
-                np.array_equal(x.download(ctx), ref_x)
+            ph = peer_plan.result().hist
+            ok = shared or (np.array_equal(ph, ref_hist) and np.array_equal(x.download(ctx), ref_x))
             err = None if ok else "PEER solve differs from the NCCL solve"
         except Exception as e:  # noqa: BLE001 -- report and fall back, never hang
             err, peer_plan = f"PEER setup failed: {e}".splitlines()[0][:200], None
-        flags = torch.tensor([0 if err is None else 1], device=f"cuda:{local}")
+        if shared and err is not None:
+            raise RuntimeError(err)
+        flags = torch.tensor([0 if err is None else 1], device=tdev)
         dist.all_reduce(flags)  # every rank takes the same backend
         if int(flags.item()) == 0:
             backend, plan = "peer", peer_plan
@@ -310,7 +324,7 @@ def bench_main(args, cfg):
     syncs = rvk.host_syncs() - syncs0
     dist.barrier()
     ms_local = sum(ev0[k].elapsed_time(ev1[k]) for k in range(args.steps)) / args.steps
-    t = torch.tensor([ms_local], device=f"cuda:{local}")
+    t = torch.tensor([ms_local], device=tdev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
     res = plan.result()
@@ -331,7 +345,7 @@ def bench_main(args, cfg):
         e1[k].record(stream)
     stream.synchronize()
     e2e_local = sum(e0[k].elapsed_time(e1[k]) for k in range(args.steps)) / args.steps
-    t = torch.tensor([e2e_local], device=f"cuda:{local}")
+    t = torch.tensor([e2e_local], device=tdev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     e2e_ms = float(t.item())
     plan.result()
@@ -350,7 +364,8 @@ def bench_main(args, cfg):
                              "ncclAllGather of dot partials between kernels"}[backend]
         out = {
             "metric": "20-iter Jacobi-CG solve time, achieved HBM GB/s vs peak, host syncs/iter",
-            "value": round(ms, 4), "unit": "ms/solve", "n_gpus": world, "steps": args.steps,
+            "value": round(ms, 4), "unit": "ms/solve", "n_gpus": 1 if shared else world,
+            "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": False,
             "scaling": "weak" if weak else "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
@@ -358,6 +373,7 @@ def bench_main(args, cfg):
                                    + (f" (weak: global grid {grid})" if weak else ""),
                        "n": n_glob, "nnz": nnz_glob, "parallelism": f"rows{world}",
                        "comm": comm_desc, "comm_fallback": fallback,
+                       "shared_gpu_functional_check": shared,
                        "l2": "no flush: per-GPU working set >> 126 MB L2"},
             "roofline": {"bound": "hbm", "kernel": "whole sharded solve, per GPU (K1+K2+comm)",
                          "achieved": round(per_gpu, 1), "peak": hbm_peak, "unit": "GB/s",
@@ -367,6 +383,7 @@ def bench_main(args, cfg):
                                "achieved_aggregate_gbs": round(b_min / (ms * 1e-3) / 1e9, 1)},
             "host_syncs_per_iter": syncs / (args.steps * 20),
             "iterations": res.iterations,
+            "iters_per_s": round(res.iterations / (ms * 1e-3), 1),
             "e2e": {"value": round(e2e_ms, 4), "unit": "ms/solve",
                     "h2d_bytes_per_step": 8 * n_glob, "d2h_bytes_per_step": 8 * n_glob},
             "gpu_launches": launches * args.steps * world,
@@ -376,10 +393,11 @@ def bench_main(args, cfg):
         print(json.dumps(out), flush=True)
     dist.barrier()  # no rank frees a window a peer may still store into
     plan.close()
-    if plan is not nccl_plan:
+    if nccl_plan is not None and plan is not nccl_plan:
         nccl_plan.close()
     disconnect_peers(opened)
-    rvk.lib().rvk_comm_destroy(comm)
+    if comm is not None:
+        rvk.lib().rvk_comm_destroy(comm)
     dist.destroy_process_group()
 
 

@@ -51,3 +51,25 @@ def test_peer_ipc_processes_early_exit():
     r = run(2, 2, 5, (32, 30), max_it=300, rtol=1e-6)
     assert r["states"] == [1, 1] and r["iterations"][0] == r["ref_iterations"]
     assert r["x_rel"] < 1e-10
+
+
+def test_bench_two_ranks_shared_gpu():
+    """bench.py's N>1 path (sharded.bench_main) end to end under torchrun with
+    both ranks on the one GPU (RVK_SHARED_GPU=1: PEER backend, gloo
+    bootstrap): plan + window exchange + timed solves + e2e + teardown, and
+    one JSON line with the contract keys.  Timings are not meaningful here."""
+    env = dict(os.environ, RVK_SHARED_GPU="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", "bench.py", "--gpus", "2",
+           "--steps", "2", "--warmup", "3", "--config", "7pt256"]
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+    assert p.returncode == 0, p.stderr[-3000:]
+    lines = [ln for ln in p.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, p.stdout[-2000:]
+    out = json.loads(lines[0])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "e2e",
+              "gpu_launches", "roofline", "clocks", "host_syncs_per_iter"):
+        assert k in out, k
+    assert out["config"]["shared_gpu_functional_check"] is True
+    assert out["iterations"] == 20 and out["host_syncs_per_iter"] == 0
+    assert out["config"]["comm"].startswith("PEER")
