@@ -59,9 +59,12 @@ def peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def bytes_model(n: int, nnz: int, mode: str = "fused"):
+def bytes_model(n: int, nnz: int, mode: str = "fused", const_diag: bool = False):
     """Algorithmic HBM bytes.  All FP64 + int64 offsets + int32 cols.
-    k1 = the SpMV launch (fused: + on-the-fly AYPX), k2 = the rest of an iteration."""
+    k1 = the SpMV launch (fused: + on-the-fly AYPX), k2 = the rest of an iteration.
+    const_diag: the plan folded a constant Jacobi diagonal into a scalar
+    (RVK_PLAN_CONST_DIAG), so the dinv stream (8n per iteration and in the
+    setup) is not part of the algorithm's traffic any more."""
     if mode == "stencil":                        # matrix-free: no CSR, constant dinv
         k1 = 32 * n                              # z, p_old -> p_new, w
         k2 = 56 * n                              # x, p, r, w -> x, r, z
@@ -71,16 +74,17 @@ def bytes_model(n: int, nnz: int, mode: str = "fused"):
                 "flops_iter": 2 * nnz + 13 * n}
     if mode == "fused":
         k1 = 12 * nnz + 8 * (n + 1) + 32 * n    # off, cols, vals, z, p_old -> p_new, w
-        k2 = 64 * n                              # x, p, r, w, dinv -> x, r, z
+        k2 = (56 if const_diag else 64) * n      # x, p, r, w, (dinv) -> x, r, z
     else:
         k1 = 12 * nnz + 8 * (n + 1) + 16 * n    # off, cols, vals, p -> w
         k2 = 136 * n                             # aypx 24, dot 16, 2 axpy 48, jacobi 24, norm 8, dot 16
-    b_min = k1 + k2                              # = 12 nnz + 8 (n+1) + 96 n
+    b_min = k1 + k2                              # = 12 nnz + 8 (n+1) + 96 n  (88 n const_diag)
     b_ref = 12 * nnz + 8 * (n + 1) + 152 * n     # reference's unfused sequence
-    setup = 64 * n
+    setup = (56 if (const_diag and mode == "fused") else 64) * n
+    survey = MAX_IT * (12 * nnz + 8 * (n + 1) + 96 * n) + 64 * n  # SURVEY.md 8d B_min as stated
     return {"k1": k1, "k2": k2, "b_min_iter": b_min, "b_ref_iter": b_ref,
             "b_min_solve": MAX_IT * b_min + setup, "b_ref_solve": MAX_IT * b_ref + setup,
-            "flops_iter": 2 * nnz + 13 * n}
+            "b_min_survey_solve": survey, "flops_iter": 2 * nnz + 13 * n}
 
 
 class ClockSampler:
@@ -350,8 +354,9 @@ def run_gpu(args, cfg):
     x = rvk.DeviceArray(n)
     rvk.check(rvk.lib().rvk_fill_rhs(ctx.h, 0x9E3779B97F4A7C15, n, b.ptr))
     plan = rvk.CgPlan(ctx, A, max_it=MAX_IT, mode=args.mode, use_graph=not args.no_graph)
+    const_diag = bool(plan.flags() & 1)
     bm = bytes_model(n, nnz, "stencil" if args.operator == "stencil" else
-                     ("unfused" if args.mode == "unfused" else "fused"))
+                     ("unfused" if args.mode == "unfused" else "fused"), const_diag)
     hbm_peak, peak_src = peaks()
     ws_bytes = 20 * nnz + 8 * (n + 1) + 9 * 8 * n
     log(f"{desc}: n={n} nnz={nnz} working set {ws_bytes/1e9:.2f} GB (L2 {L2_BYTES/1e6:.0f} MB)")
@@ -481,6 +486,8 @@ def run_gpu(args, cfg):
         "solve_roofline": {"alg_bytes_per_solve": bm["b_min_solve"],
                            "achieved": round(solve_gbs, 1), "frac": round(solve_gbs / hbm_peak, 4),
                            "update_kernel_gbs": round(k2_gbs, 1),
+                           "const_diag_folded": const_diag,
+                           "survey_b_min_gbs": round(bm["b_min_survey_solve"] / (ms * 1e-3) / 1e9, 1),
                            "b_ref_gbs": round(bm["b_ref_solve"] / (ms * 1e-3) / 1e9, 1)},
         "host_syncs_per_iter": syncs / (args.steps * MAX_IT),
         "iters_per_s": round(MAX_IT / (ms * 1e-3), 1),

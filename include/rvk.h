@@ -227,6 +227,14 @@ rvk_status rvk_cg_solve_host(rvk_cg_plan plan, const double* b_host, double* x_h
  * down (infos tell which). */
 rvk_status rvk_cg_solve_host_many(rvk_cg_plan plan, int nrhs, const double* const* b_host,
                                   double* const* x_host, double* hist_host, rvk_cg_info* infos);
+/* Plan structure the solve exploits (bitmask):
+ *   RVK_PLAN_CONST_DIAG   every diagonal entry is the same bit pattern (constant-
+ *                         coefficient stencils): Jacobi uses the scalar, no dinv
+ *                         stream (opt-in: env RVK_CONST_DIAG=1 at plan creation)
+ *   RVK_PLAN_MATRIX_FREE  rvk_cg_plan_create_stencil operator                       */
+#define RVK_PLAN_CONST_DIAG  1
+#define RVK_PLAN_MATRIX_FREE 2
+int        rvk_cg_plan_flags(rvk_cg_plan plan);
 /* The mode the plan runs (AUTO resolved to FUSED or PERSISTENT). */
 int        rvk_cg_plan_mode(rvk_cg_plan plan);
 /* Per-kernel event timing of the last solve's dominant kernels (bench): */

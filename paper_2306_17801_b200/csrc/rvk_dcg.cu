@@ -230,13 +230,21 @@ __device__ __forceinline__ void peer_push(double* lo, double* hi, int64_t plane,
 // ---------------------------------------------------------------------------
 namespace {
 
+// PC: 0 none, 1 dinv vector, 2 constant dinv (constant-coefficient diagonal,
+// folded to the scalar dconst at plan time -- bit-identical, no dinv stream)
+__device__ __forceinline__ double jacobi_z(int PC, const double* __restrict__ dinv, double dconst,
+                                           int64_t i, double ri)
+{
+    return PC == 0 ? ri : mul(PC == 1 ? dinv[i] : dconst, ri);
+}
+
 // K0: r = b, x = 0, z = B b on the owned rows; partial z.z, z.r -> gather[rank][0..1]
-template <bool JACOBI, bool PEER>
+template <int PC, bool PEER>
 __global__ void __launch_bounds__(kUpdThreads)
     k_dcg_setup(int64_t n, const double* __restrict__ b, const double* __restrict__ dinv,
-                double* __restrict__ x, double* __restrict__ r, double* __restrict__ z,
-                double* gather, int rank, double* partials, unsigned int* ticket, CgState* st,
-                DcgPeer pr)
+                double dconst, double* __restrict__ x, double* __restrict__ r,
+                double* __restrict__ z, double* gather, int rank, double* partials,
+                unsigned int* ticket, CgState* st, DcgPeer pr)
 {
     __shared__ double smem[64];
     __shared__ int    flag;
@@ -250,7 +258,7 @@ __global__ void __launch_bounds__(kUpdThreads)
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
         const double bi = b[i];
-        const double zi = JACOBI ? mul(dinv[i], bi) : bi;
+        const double zi = jacobi_z(PC, dinv, dconst, i, bi);
         r[i] = bi;
         z[i] = zi;
         x[i] = 0.0;
@@ -384,10 +392,11 @@ struct DcgSpmvOp {
 };
 
 // K2(it): fold p.w; alpha = beta_it / pAp; updates; partial z.z, z.r.
-template <bool JACOBI, bool PEER>
+template <int PC, bool PEER>
 __global__ void __launch_bounds__(kUpdThreads)
     k_dcg_update(int64_t n, const double* __restrict__ p, const double* __restrict__ w,
-                 const double* __restrict__ dinv, double* __restrict__ x, double* __restrict__ r,
+                 const double* __restrict__ dinv, double dconst, double* __restrict__ x,
+                 double* __restrict__ r,
                  double* __restrict__ z, DcgScalars sc, int it, int rank, double* gather_out,
                  double* partials, unsigned int* ticket, DcgPeer pr)
 {
@@ -422,7 +431,7 @@ __global__ void __launch_bounds__(kUpdThreads)
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
         x[i]            = axpy1(a, p[i], x[i]);
         const double ri = axpy1(na, w[i], r[i]);
-        const double zi = JACOBI ? mul(dinv[i], ri) : ri;
+        const double zi = jacobi_z(PC, dinv, dconst, i, ri);
         r[i]            = ri;
         z[i]            = zi;
         if constexpr (PEER) peer_push(pr.lo_z, pr.hi_z, pr.plane, n, i, zi);
@@ -516,6 +525,8 @@ struct rvk_dcg_plan_s {
     CgState*      st = nullptr;
     unsigned int* tickets = nullptr;
     DcgPeer       peer{};          // peer.on: PEER backend attached
+    bool          const_diag = false; // Jacobi diagonal is one value: dconst
+    double        dconst     = 0.0;
     void**        peer_tab = nullptr; // device: gather[nranks] then flags[nranks]
 };
 
@@ -583,20 +594,34 @@ int64_t plane(const rvk_dcg_plan P) { return P->sh.halo_lo ? P->sh.halo_lo : P->
 // ---- per-phase enqueue (one shard) -----------------------------------------
 // The PEER variants carry the in-kernel communication; otherwise the NCCL /
 // loopback exchange is enqueued between the phases by the caller.
-template <bool J, bool PEER>
+int pc_mode(const rvk_dcg_plan P)
+{
+    return P->cfg.pc != RVK_PC_JACOBI ? 0 : (P->const_diag ? 2 : 1);
+}
+
+template <int PC, bool PEER>
 void launch_setup_k(rvk_dcg_plan P, const double* b, double* x)
 {
-    k_dcg_setup<J, PEER><<<P->upd_grid, kUpdThreads, 0, P->ctx->stream>>>(
-        P->sh.n_own, b, P->dinv, x, P->r, P->z + P->sh.halo_lo, P->gather, P->sh.rank, P->partials,
-        P->tickets, P->st, P->peer);
+    k_dcg_setup<PC, PEER><<<P->upd_grid, kUpdThreads, 0, P->ctx->stream>>>(
+        P->sh.n_own, b, P->dinv, P->dconst, x, P->r, P->z + P->sh.halo_lo, P->gather, P->sh.rank,
+        P->partials, P->tickets, P->st, P->peer);
+}
+
+template <bool PEER>
+void dispatch_setup(rvk_dcg_plan P, const double* b, double* x)
+{
+    switch (pc_mode(P)) {
+    case 0: launch_setup_k<0, PEER>(P, b, x); break;
+    case 1: launch_setup_k<1, PEER>(P, b, x); break;
+    default: launch_setup_k<2, PEER>(P, b, x);
+    }
 }
 
 rvk_status phase_setup(rvk_dcg_plan P, const double* b, double* x)
 {
     k_dcg_reset<<<1, 1, 0, P->ctx->stream>>>(P->st);
-    const bool j = P->cfg.pc == RVK_PC_JACOBI;
-    if (P->peer.on) j ? launch_setup_k<true, true>(P, b, x) : launch_setup_k<false, true>(P, b, x);
-    else j ? launch_setup_k<true, false>(P, b, x) : launch_setup_k<false, false>(P, b, x);
+    if (P->peer.on) dispatch_setup<true>(P, b, x);
+    else dispatch_setup<false>(P, b, x);
     RVK_CHECK_LAUNCH("k_dcg_setup");
     return RVK_OK;
 }
@@ -620,20 +645,29 @@ rvk_status phase_k1(rvk_dcg_plan P, int it)
     return it == 0 ? launch_k1<true, false>(P, it) : launch_k1<false, false>(P, it);
 }
 
-template <bool J, bool PEER>
+template <int PC, bool PEER>
 void launch_update_k(rvk_dcg_plan P, int it, double* x)
 {
-    k_dcg_update<J, PEER><<<P->upd_grid, kUpdThreads, 0, P->ctx->stream>>>(
-        P->sh.n_own, P->p[(it + 1) & 1] + P->sh.halo_lo, P->w, P->dinv, x, P->r,
+    k_dcg_update<PC, PEER><<<P->upd_grid, kUpdThreads, 0, P->ctx->stream>>>(
+        P->sh.n_own, P->p[(it + 1) & 1] + P->sh.halo_lo, P->w, P->dinv, P->dconst, x, P->r,
         P->z + P->sh.halo_lo, scalars(P), it, P->sh.rank, P->gather + P->sh.rank * 4, P->partials,
         P->tickets, P->peer);
 }
 
+template <bool PEER>
+void dispatch_update(rvk_dcg_plan P, int it, double* x)
+{
+    switch (pc_mode(P)) {
+    case 0: launch_update_k<0, PEER>(P, it, x); break;
+    case 1: launch_update_k<1, PEER>(P, it, x); break;
+    default: launch_update_k<2, PEER>(P, it, x);
+    }
+}
+
 rvk_status phase_k2(rvk_dcg_plan P, int it, double* x)
 {
-    const bool j = P->cfg.pc == RVK_PC_JACOBI;
-    if (P->peer.on) j ? launch_update_k<true, true>(P, it, x) : launch_update_k<false, true>(P, it, x);
-    else j ? launch_update_k<true, false>(P, it, x) : launch_update_k<false, false>(P, it, x);
+    if (P->peer.on) dispatch_update<true>(P, it, x);
+    else dispatch_update<false>(P, it, x);
     RVK_CHECK_LAUNCH("k_dcg_update");
     return RVK_OK;
 }
@@ -785,7 +819,7 @@ rvk_status rvk_dcg_plan_create(rvk_ctx ctx, const rvk_csr* A, rvk_shard sh, rvk_
     if (std::getenv("RVK_NO_PREFETCH")) win.has_lead = false;
     P->sa          = make_spmv_args(*A, maxlen, &win, 2);
     spmv_set_order(P->sa, bands, A->nnz, 2, sm_count());
-    P->upd_grid    = resident_grid(k_dcg_update<true, true>, kUpdThreads, sh.n_own);
+    P->upd_grid    = resident_grid(k_dcg_update<1, true>, kUpdThreads, sh.n_own);
     P->owns_gather = shared_gather == nullptr;
     P->gather      = shared_gather;
     rvk_status rc  = alloc_plan_buffers(P);
@@ -794,6 +828,11 @@ rvk_status rvk_dcg_plan_create(rvk_ctx ctx, const rvk_csr* A, rvk_shard sh, rvk_
         if (cfg.pc == RVK_PC_JACOBI) rc = diag_inverse(ctx->stream, *A, sh.halo_lo, P->dinv);
         else rc = rvk_set(ctx, sh.n_own, 1.0, P->dinv);
     }
+    // constant diagonal -> scalar Jacobi (as rvk_cg_plan_create; opt-in RVK_CONST_DIAG=1).
+    // Every shard of a constant-coefficient operator sees the same value.
+    const char* cd = std::getenv("RVK_CONST_DIAG");
+    if (rc == RVK_OK && cfg.pc == RVK_PC_JACOBI && sh.n_own > 0 && cd && cd[0] == '1')
+        rc = vector_is_constant(ctx->stream, sh.n_own, P->dinv, &P->const_diag, &P->dconst);
     if (rc != RVK_OK) {
         rvk_dcg_plan_destroy(P);
         return rc;

@@ -16,6 +16,9 @@ rvk_status vec_reduce(cudaStream_t st, Scratch sc, int op, int64_t n, const doub
 rvk_status vec_ew(cudaStream_t st, int op, int64_t n, rvk_scalar s, const double* x,
                   const double* y, double* out, const int* guard);
 
+// Is v[0..n) a single bit pattern (plan time, one counted sync)?  *value = v[0].
+rvk_status vector_is_constant(cudaStream_t s, int64_t n, const double* v, bool* is_const,
+                              double* value);
 // dinv[r] = 1 / A[r, r + col_off] (0 -> inf, as the reference's 1/diag).
 rvk_status diag_inverse(cudaStream_t s, const rvk_csr& A, int64_t col_off, double* dinv);
 

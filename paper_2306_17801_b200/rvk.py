@@ -40,7 +40,7 @@ EXPORTS = [
     "rvk_build_laplacian", "rvk_fill_rhs", "rvk_cg_plan_create", "rvk_cg_plan_create_stencil", "rvk_cg_plan_destroy",
     "rvk_cg_solve_dev", "rvk_cg_history_dev", "rvk_cg_result", "rvk_cg_solve_host",
     "rvk_cg_solve_host_many",
-    "rvk_cg_set_profiling", "rvk_cg_kernel_times", "rvk_cg_plan_mode",
+    "rvk_cg_set_profiling", "rvk_cg_kernel_times", "rvk_cg_plan_mode", "rvk_cg_plan_flags",
     "rvk_laplacian_rows_nnz", "rvk_build_laplacian_rows", "rvk_comm_unique_id", "rvk_comm_init",
     "rvk_comm_destroy", "rvk_dcg_plan_create", "rvk_dcg_plan_destroy", "rvk_dcg_solve_dev",
     "rvk_dcg_loopback_solve", "rvk_dcg_result", "rvk_dcg_window", "rvk_dcg_attach_peers",
@@ -150,6 +150,7 @@ def lib():
         "rvk_cg_kernel_times": (i, [vp, C.POINTER(C.c_float), C.POINTER(C.c_float),
                                     C.POINTER(C.c_int)]),
         "rvk_cg_plan_mode": (i, [vp]),
+        "rvk_cg_plan_flags": (i, [vp]),
         "rvk_laplacian_rows_nnz": (i, [i, i, i64, i64, i64, i64, i64, C.POINTER(i64)]),
         "rvk_build_laplacian_rows": (i, [vp, i, i, i64, i64, i64, i64, i64, i64, vp, vp, vp]),
         "rvk_comm_unique_id": (i, [vp, i]),
@@ -420,6 +421,10 @@ class CgPlan:
         a, b, n = C.c_float(), C.c_float(), C.c_int()
         check(lib().rvk_cg_kernel_times(self.h, C.byref(a), C.byref(b), C.byref(n)))
         return a.value, b.value, n.value
+
+    def flags(self) -> int:
+        """RVK_PLAN_* bits: 1 constant diagonal folded to a scalar, 2 matrix-free."""
+        return lib().rvk_cg_plan_flags(self.h)
 
     def mode(self) -> str:
         m = lib().rvk_cg_plan_mode(self.h)

@@ -531,3 +531,42 @@ def test_chunked_tile_order_parity(ctx, spec, monkeypatch, capfd):
     tr = tp.result()
     assert np.max(np.abs(tr.hist - tref.hist) / np.abs(tref.hist)) < 1e-8
     tp.close()
+
+
+@pytest.mark.parametrize("spec", [(3, 7, (20, 16, 12)), (2, 9, (40, 33)), (3, 27, (10, 9, 8))])
+def test_constant_diagonal_folding_bitexact(ctx, spec, monkeypatch):
+    """Constant-coefficient Laplacians have one diagonal value: with
+    RVK_CONST_DIAG=1 the plan folds dinv into a scalar (RVK_PLAN_CONST_DIAG)
+    and the fused kernels skip the dinv stream.  Results are bit-identical to
+    the dinv-vector path (also sharded); a matrix whose diagonal varies keeps
+    the vector."""
+    dim, pts, g = spec
+    Ah = O.build_laplacian(dim, pts, g)
+    b = O.rhs(Ah.n_rows)
+    A = rvk.DeviceCsr.laplacian(ctx, dim, pts, g)
+    p0 = rvk.CgPlan(ctx, A, max_it=20)
+    assert not p0.flags() & 1  # opt-in
+    x0, r0 = p0.solve_host(b)
+    monkeypatch.setenv("RVK_CONST_DIAG", "1")
+    p1 = rvk.CgPlan(ctx, A, max_it=20)
+    assert p1.flags() & 1
+    x1, r1 = p1.solve_host(b)
+    assert np.array_equal(x1, x0) and np.array_equal(r1.hist, r0.hist)
+    from paper_2306_17801_b200.sharded import loopback_solve
+    xs, rs, _ = loopback_solve(ctx, dim, pts, g, 2, b, max_it=20, backend="peer")
+    check_cg(rs, xs, O.cg_solve(Ah, b, max_it=20))
+    # scale one row: the diagonal is no longer constant (SPD kept: symmetric scaling)
+    off, cols, vals = Ah.off.copy(), Ah.cols.copy(), Ah.vals.copy()
+    vals[off[3]:off[4]] *= 2.0
+    for r in range(Ah.n_rows):
+        for k in range(off[r], off[r + 1]):
+            if cols[k] == 3 and r != 3:
+                vals[k] *= 2.0
+    kd = off[3] + int(np.nonzero(cols[off[3]:off[4]] == 3)[0][0])
+    vals[kd] *= 2.0  # D A D with d_3 = 2: the (3,3) entry scales by 4
+    Bh = O.Csr(Ah.n_rows, Ah.n_cols, off, cols, vals)
+    B = rvk.DeviceCsr.from_host(ctx, Bh.n_rows, Bh.n_cols, off, cols, vals)
+    pb = rvk.CgPlan(ctx, B, max_it=20)
+    assert not pb.flags() & 1
+    xb, rb = pb.solve_host(b)
+    check_cg(rb, xb, O.cg_solve(Bh, b, max_it=20))
