@@ -417,6 +417,163 @@ int main()
         }
         EXPECT(got);
     });
+    // ---- property tests ---------------------------------------------------
+    run("10,000 random expression DAGs vs a host interpreter (SPEC.md:624)", [] {
+        // IEEE + - * / min max neg abs sqrt are exact on both sides (bitwise);
+        // DAGs with sin/cos/exp (libdevice vs glibc, <= 2 ulp) are built without
+        // subtraction/division so no cancellation amplifies the ulps: 1e-12.
+        std::uint64_t rng = 0x2545F4914F6CDD1Dull;
+        auto next = [&] {
+            rng ^= rng << 13;
+            rng ^= rng >> 7;
+            rng ^= rng << 17;
+            return rng;
+        };
+        auto unif = [&](double lo, double hi) { return lo + (hi - lo) * (double)(next() >> 11) * 0x1.0p-53; };
+        Context ctx;
+        std::vector<Managed> leaves;
+        std::vector<double>  lv;
+        for (int i = 0; i < 6; ++i) {
+            lv.push_back(unif(0.5, 2.0));
+            leaves.emplace_back(lv.back());
+        }
+        struct Node {
+            Expr   e;
+            double v;
+        };
+        // transcendental: false -> exact ops only
+        std::function<Node(int, bool)> gen = [&](int depth, bool tr) -> Node {
+            const int pick = (int)(next() % 16);
+            if (depth == 0 || pick < 3) {
+                if (next() % 3 == 0) {
+                    const double c = unif(0.5, 2.0);
+                    return {Expr(c), c};
+                }
+                const int k = (int)(next() % leaves.size());
+                return {Expr(leaves[k]), lv[k]};
+            }
+            if (pick < 6) { // unary
+                Node a = gen(depth - 1, tr);
+                const int u = (int)(next() % (tr ? 6 : 3));
+                switch (u) {
+                case 0: return {-a.e, -a.v};
+                case 1: return {abs(a.e), std::fabs(a.v)};
+                case 2: return {sqrt(abs(a.e)), std::sqrt(std::fabs(a.v))};
+                case 3: return {sin(a.e), std::sin(a.v)};
+                case 4: return {cos(a.e), std::cos(a.v)};
+                default: return {exp(sin(a.e)), std::exp(std::sin(a.v))};
+                }
+            }
+            Node a = gen(depth - 1, tr), b = gen(depth - 1, tr);
+            const int o = (int)(next() % (tr ? 4 : 6));
+            static const int kTrOps[4] = {0, 2, 4, 5}; // + * min max
+            const int        op         = tr ? kTrOps[o] : o;
+            switch (op) {
+            case 0: return {a.e + b.e, a.v + b.v};
+            case 1: return {a.e - b.e, a.v - b.v};
+            case 2: return {a.e * b.e, a.v * b.v};
+            case 3: return {a.e / b.e, a.v / b.v};
+            case 4: return {min(a.e, b.e), std::fmin(a.v, b.v)};
+            default: return {max(a.e, b.e), std::fmax(a.v, b.v)};
+            }
+        };
+        int exact = 0, approx = 0, skipped = 0;
+        for (int t = 0; t < 10000; ++t) {
+            const bool tr = t % 4 == 3;
+            Node       nd = gen(5, tr);
+            Managed    out;
+            try {
+                Eval(nd.e, ctx).execute(out);
+            } catch (const Error&) { // a program over kMaxExprSteps: rejected up front
+                ++skipped;
+                continue;
+            }
+            const double got = out.front();
+            if (tr) {
+                ++approx;
+                if (!(std::fabs(got - nd.v) <= 1e-12 * std::max(1.0, std::fabs(nd.v)))) {
+                    std::printf("  dag %d: got %.17g want %.17g\n", t, got, nd.v);
+                    EXPECT(false);
+                }
+            } else {
+                ++exact;
+                const bool same = std::memcmp(&got, &nd.v, 8) == 0 || (std::isnan(got) && std::isnan(nd.v));
+                if (!same) {
+                    std::printf("  dag %d: got %.17g want %.17g\n", t, got, nd.v);
+                    EXPECT(false);
+                }
+            }
+        }
+        std::printf("  exact %d, transcendental %d, too large %d\n", exact, approx, skipped);
+        EXPECT(skipped < 100);
+    });
+    run("1,000 random cross-context access programs vs sequential replay (SPEC.md:622)", [] {
+        // Random elementwise programs over 4 vectors issued round-robin-at-random
+        // on 3 contexts: the RAW/WAR/WAW edges the API installs must make the
+        // device result equal the program-order replay on the host, bit for bit
+        // (every op is elementwise IEEE, rounded exactly like the oracle).
+        std::uint64_t rng = 0x9E3779B97F4A7C15ull;
+        auto next = [&] {
+            rng ^= rng << 13;
+            rng ^= rng >> 7;
+            rng ^= rng << 17;
+            return rng;
+        };
+        const std::size_t n = 3000;
+        Context ctxs[3];
+        int     programs = 0;
+        for (int prog = 0; prog < 1000; ++prog) {
+            std::vector<std::vector<double>> h(4, std::vector<double>(n));
+            std::vector<DenseVector>         v;
+            for (int k = 0; k < 4; ++k) {
+                for (std::size_t i = 0; i < n; ++i) h[k][i] = 0.5 + (double)((i * 7 + k * 13) % 17) / 16.0;
+                v.emplace_back(std::span<const double>(h[k]));
+            }
+            const int nops = 4 + (int)(next() % 20);
+            for (int o = 0; o < nops; ++o) {
+                const Context& c = ctxs[next() % 3];
+                const int      y = (int)(next() % 4), x = (int)(next() % 4), w = (int)(next() % 4);
+                const double   a = 0.25 + (double)(next() % 8) / 8.0;
+                switch (next() % 6) {
+                case 0: // y += a x
+                    vec_axpy_async(v[y], a, v[x], c);
+                    for (std::size_t i = 0; i < n; ++i) h[y][i] = h[y][i] + a * h[x][i];
+                    break;
+                case 1: // y = x + a y
+                    vec_aypx_async(v[y], a, v[x], c);
+                    for (std::size_t i = 0; i < n; ++i) h[y][i] = h[x][i] + a * h[y][i];
+                    break;
+                case 2: // y *= a
+                    vec_scale_async(v[y], a, c);
+                    for (std::size_t i = 0; i < n; ++i) h[y][i] = h[y][i] * a;
+                    break;
+                case 3: // copy x -> y
+                    if (x == y) break;
+                    vec_copy_async(v[x], v[y], c);
+                    h[y] = h[x];
+                    break;
+                case 4: // w = a x + y
+                    if (w == x || w == y) break;
+                    vec_waxpy_async(v[w], a, v[x], v[y], c);
+                    for (std::size_t i = 0; i < n; ++i) h[w][i] = a * h[x][i] + h[y][i];
+                    break;
+                default: // w = x .* y
+                    if (w == x || w == y) break;
+                    vec_pointwise_mult_async(v[x], v[y], v[w], c);
+                    for (std::size_t i = 0; i < n; ++i) h[w][i] = h[x][i] * h[y][i];
+                }
+            }
+            for (int k = 0; k < 4; ++k) {
+                auto d = v[k].to_host();
+                if (std::memcmp(d.data(), h[k].data(), n * 8) != 0) {
+                    std::printf("  program %d vector %d differs\n", prog, k);
+                    EXPECT(false);
+                }
+            }
+            ++programs;
+        }
+        std::printf("  %d programs\n", programs);
+    });
     std::printf("%s: %d failure(s)\n", g_fail ? "FAILED" : "OK", g_fail);
     return g_fail ? 1 : 0;
 }

@@ -570,3 +570,24 @@ def test_constant_diagonal_folding_bitexact(ctx, spec, monkeypatch):
     assert not pb.flags() & 1
     xb, rb = pb.solve_host(b)
     check_cg(rb, xb, O.cg_solve(Bh, b, max_it=20))
+
+
+def test_fingerprint_identical_across_processes():
+    """identical result fingerprints across repetitions AND
+    processes (deterministic reductions, fixed grids, no atomics in FP)."""
+    import subprocess
+    import sys
+    code = ("import hashlib, numpy as np, sys; sys.path.insert(0, %r);"
+            "from paper_2306_17801_b200 import rvk; import oracle as O;"
+            "ctx = rvk.Ctx(); A = rvk.DeviceCsr.laplacian(ctx, 3, 27, (40, 36, 30));"
+            "b = O.rhs(A.n_rows); p = rvk.CgPlan(ctx, A, max_it=20);"
+            "x, r = p.solve_host(b); x2, r2 = p.solve_host(b);"
+            "assert np.array_equal(x, x2) and np.array_equal(r.hist, r2.hist);"
+            "print(hashlib.sha256(x.tobytes() + r.hist.tobytes()).hexdigest())"
+            % os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    fps = []
+    for _ in range(2):
+        p = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
+        assert p.returncode == 0, p.stderr[-2000:]
+        fps.append(p.stdout.strip().splitlines()[-1])
+    assert fps[0] == fps[1]
