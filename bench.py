@@ -71,6 +71,7 @@ def bytes_model(n: int, nnz: int, mode: str = "fused", const_diag: bool = False)
         b_min = k1 + k2
         return {"k1": k1, "k2": k2, "b_min_iter": b_min, "b_ref_iter": b_min,
                 "b_min_solve": MAX_IT * b_min + 32 * n, "b_ref_solve": MAX_IT * b_min + 32 * n,
+                "b_min_survey_solve": MAX_IT * (12 * nnz + 8 * (n + 1) + 96 * n) + 64 * n,
                 "flops_iter": 2 * nnz + 13 * n}
     if mode == "fused":
         k1 = 12 * nnz + 8 * (n + 1) + 32 * n    # off, cols, vals, z, p_old -> p_new, w

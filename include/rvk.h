@@ -234,7 +234,13 @@ rvk_status rvk_cg_solve_host_many(rvk_cg_plan plan, int nrhs, const double* cons
  *   RVK_PLAN_MATRIX_FREE  rvk_cg_plan_create_stencil operator                       */
 #define RVK_PLAN_CONST_DIAG  1
 #define RVK_PLAN_MATRIX_FREE 2
+#define RVK_PLAN_MF_TMA      4  /* matrix-free K1 is the TMA 2.5D marching kernel */
 int        rvk_cg_plan_flags(rvk_cg_plan plan);
+/* Test hook (the reference's "exposed for equivalence tests" spirit,
+ * kernels.hpp:50-76): device pointer of a plan work vector after a solve.
+ * p0 / p1 alternate as p_old / p_new; iteration k writes p[(k+1)&1]. */
+enum { RVK_VEC_R = 0, RVK_VEC_Z = 1, RVK_VEC_P0 = 2, RVK_VEC_P1 = 3, RVK_VEC_W = 4 };
+const double* rvk_cg_plan_vector(rvk_cg_plan plan, int which);
 /* The mode the plan runs (AUTO resolved to FUSED or PERSISTENT). */
 int        rvk_cg_plan_mode(rvk_cg_plan plan);
 /* Per-kernel event timing of the last solve's dominant kernels (bench): */

@@ -496,6 +496,7 @@ struct rvk_cg_plan_s {
     double        dconst = 0.0;             // constant dinv (stencil, or a detected constant diagonal)
     bool          const_diag = false;       // CSR plan: every dinv[i] bit-identical -> scalar
     int           mf_grid = 0;
+    MfTma*        mf_tma  = nullptr;         // TMA 2.5D matrix-free kernel state (or null)
     double*       dinv = nullptr;
     double*       r = nullptr;
     double*       z = nullptr;
@@ -587,7 +588,7 @@ rvk_status launch_k1(rvk_cg_plan P, int it, bool first, const double* p_old, dou
     const TailArgs ta{P->partials + 2 * kMaxReduceBlocks, P->tickets + 1};
     if (P->stencil)
         return launch_mf_k1(s, P->geom, first, P->z, p_old, p_new, P->w, P->st, n, it, ta.partials,
-                            ta.ticket, P->mf_grid);
+                            ta.ticket, P->mf_grid, P->mf_tma);
     if (first) {
         CgSpmvOp<true> op{P->z, p_old, p_new, P->w, P->st, n, it, 0.0};
         return launch_spmv(s, P->sa, op, ta, P->spmv_grid);
@@ -679,7 +680,7 @@ rvk_status enqueue_fused(rvk_cg_plan P, const double* b, double* x)
         if ((rc = rec(4 * it + 0)) != RVK_OK) return rc;
         if (P->stencil) {
             rc = launch_mf_k1(s, P->geom, it == 0, P->z, p_old, p_new, P->w, P->st, n, it, ta.partials,
-                              ta.ticket, P->mf_grid);
+                              ta.ticket, P->mf_grid, P->mf_tma);
         } else if (it == 0) {
             CgSpmvOp<true> op{P->z, p_old, p_new, P->w, P->st, n, it, 0.0};
             rc = launch_spmv(s, P->sa, op, ta, P->spmv_grid);
@@ -1064,7 +1065,21 @@ rvk_status rvk_cg_plan_create(rvk_ctx ctx, const rvk_csr* A, rvk_cg_config cfg, 
 int rvk_cg_plan_flags(rvk_cg_plan P)
 {
     if (!P) return -1;
-    return (P->const_diag ? RVK_PLAN_CONST_DIAG : 0) | (P->stencil ? RVK_PLAN_MATRIX_FREE : 0);
+    return (P->const_diag ? RVK_PLAN_CONST_DIAG : 0) | (P->stencil ? RVK_PLAN_MATRIX_FREE : 0) |
+           (P->mf_tma ? RVK_PLAN_MF_TMA : 0);
+}
+
+const double* rvk_cg_plan_vector(rvk_cg_plan P, int which)
+{
+    if (!P) return nullptr;
+    switch (which) {
+    case RVK_VEC_R: return P->r;
+    case RVK_VEC_Z: return P->z;
+    case RVK_VEC_P0: return P->p[0];
+    case RVK_VEC_P1: return P->p[1];
+    case RVK_VEC_W: return P->w;
+    }
+    return nullptr;
 }
 
 rvk_status rvk_cg_plan_create_stencil(rvk_ctx ctx, int dim, int points, int64_t nx, int64_t ny,
@@ -1119,6 +1134,7 @@ rvk_status rvk_cg_plan_create_stencil(rvk_ctx ctx, int dim, int points, int64_t 
         rvk_cg_plan_destroy(P);
         return cuda_error(e, "rvk_cg_plan_create_stencil");
     }
+    P->mf_tma = mf_tma_create(P->geom, P->z, P->p[0], P->p[1]);
     *out = P;
     return RVK_OK;
 }
@@ -1128,6 +1144,7 @@ rvk_status rvk_cg_plan_destroy(rvk_cg_plan P)
     if (!P) return RVK_OK;
     if (P->ctx) cudaStreamSynchronize(P->ctx->stream);
     destroy_graph(P);
+    mf_tma_destroy(P->mf_tma);
     for (auto ev : P->ev) cudaEventDestroy(ev);
     for (auto ev : P->ev_many)
         if (ev) cudaEventDestroy(ev);

@@ -123,9 +123,15 @@ struct StencilGeom {
 // CgSpmvOp semantics (init/tail) as the CSR kernel.  Bit-identical w to the
 // CSR path: the neighbours are visited in ascending column order with the
 // same coefficients.
+// The TMA 2.5D variant's plan state (tensor maps of z, p0, p1); null when the
+// geometry does not allow it (odd nx) or RVK_MF_TMA=0.
+struct MfTma;
+MfTma*     mf_tma_create(const StencilGeom& g, const double* z, const double* p0, const double* p1);
+void       mf_tma_destroy(MfTma* t);
 rvk_status launch_mf_k1(cudaStream_t s, const StencilGeom& g, bool first, const double* z,
                         const double* p_old, double* p_new, double* w, CgState* st, int64_t n,
-                        int it, double* partials, unsigned int* ticket, int grid);
+                        int it, double* partials, unsigned int* ticket, int grid,
+                        const MfTma* tma);
 int        mf_grid(const StencilGeom& g);
 
 // Arguments of the single-kernel persistent solve (rvk_cg_small.cu).

@@ -11,8 +11,30 @@
 // to the CSR path while the 12 B/nnz + 8 B/row of CSR traffic disappear.
 // Per iteration HBM bytes drop from 12 nnz + 8 (n+1) + 96 n to 88 n (K2 reads
 // no dinv: the Jacobi diagonal is the constant centre weight).
+//
+// Two kernels:
+//  * k_mf_tma (default when the grid allows a TMA tensor map: even nx): 2.5D
+//    marching.  A block owns a TX x TY tile of the (x, y) plane (2D: a TX
+//    segment of x) and marches through a chunk of planes (2D: rows).  Each
+//    plane's (TX+4) x (TY+2) box of z and p_old (the halo included; x starts
+//    at x0-2 because TMA needs a 16-B aligned innermost start) arrives by
+//    ONE cp.async.bulk.tensor per vector into a kTmaStages-deep ring; OOB
+//    coordinates are zero-filled by the TMA unit, so the grid boundary needs
+//    no branches: p = z + b p_old is formed ONCE per element into a 4-plane
+//    ring (p(OOB) = +0), and every row adds its neighbours in ascending
+//    column order -- an out-of-grid neighbour contributes (-1) * (+0) = -0,
+//    and sum + (-0) == sum exactly, so w is bit-identical to the CSR path,
+//    which skips it.  Each z / p_old element is fetched once (plus the halo,
+//    served by L2 from the neighbouring tiles): no index division, no
+//    redundant gathers.
+//  * k_mf_cg: one row per thread with fast-divmod coordinates and warp
+//    shuffles for the x-neighbours (any geometry; the fallback).
 #include "rvk_cg.cuh"
 #include "rvk_common.cuh"
+
+#include <cuda.h> // CUtensorMap + enums; cuTensorMapEncodeTiled is resolved at run time
+
+#include <mutex>
 #include "rvk_context.hpp"
 #include "rvk_internal.hpp"
 #include "rvk_spmv.cuh"
@@ -158,6 +180,146 @@ __global__ void __launch_bounds__(kMfThreads, 2)
     }
 }
 
+// ---------------------------------------------------------------------------
+// TMA 2.5D marching kernel
+// ---------------------------------------------------------------------------
+constexpr int kTmaStages = 6; // planes in flight per block
+
+struct MfTmaGeom {
+    int32_t nx, ny, nm;       // plane extent (2D: nx, 1) and marching extent (3D nz, 2D ny)
+    int32_t tiles_x, tiles_y; // plane tiles
+    int32_t chunk;            // planes per block
+    double  centre;
+};
+
+template <int DIM>
+struct MfShape;
+template <>
+struct MfShape<3> {
+    static constexpr int TX = 32, TY = 8;
+};
+template <>
+struct MfShape<2> {
+    static constexpr int TX = 128, TY = 1;
+};
+
+template <int DIM>
+__device__ __forceinline__ void tma_plane(void* dst, const CUtensorMap* map, int32_t x, int32_t y,
+                                          int32_t m, uint64_t* bar)
+{
+    if constexpr (DIM == 3)
+        asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                     " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+                     "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(m), "r"(smem_u32(bar))
+                     : "memory");
+    else
+        asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                     " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+                     "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(m), "r"(smem_u32(bar))
+                     : "memory");
+    (void)y;
+}
+
+template <bool FIRST, int DIM, bool BOX>
+__global__ void __launch_bounds__(MfShape<DIM>::TX * MfShape<DIM>::TY)
+    k_mf_tma(const __grid_constant__ CUtensorMap tz, const __grid_constant__ CUtensorMap tp,
+             MfTmaGeom g, CgSpmvOp<FIRST> op_in, TailArgs tail)
+{
+    constexpr int TX = MfShape<DIM>::TX, TY = MfShape<DIM>::TY, NT = TX * TY;
+    // box: x0-2 .. x0+TX+1 (the innermost TMA start coordinate must be 16-B
+    // aligned -- x0-1 traps with an illegal instruction on B200, measured),
+    // y0-1 .. y0+TY (3D), one plane
+    constexpr int BW = TX + 4, BH = DIM == 3 ? TY + 2 : 1, BE = BW * BH;
+    constexpr int BP   = (BE + 15) & ~15; // box pitch: every TMA destination 128-B aligned
+    constexpr int NSRC = FIRST ? 1 : 2;
+    __shared__ __align__(128) double stage[kTmaStages][2][BP]; // [z | p_old] boxes
+    __shared__ double                pr[4][BE];                 // p = z + b p_old, 4-plane ring
+    __shared__ __align__(8) uint64_t full[kTmaStages];
+    __shared__ double                red[32];
+    __shared__ int                   flag;
+
+    CgSpmvOp<FIRST> op = op_in;
+    if (!op.init()) return; // device-side early exit (converged / breakdown)
+    const int     tid = threadIdx.x, tx = tid % TX, ty = tid / TX;
+    const int32_t tiles = g.tiles_x * g.tiles_y;
+    const int32_t tile = (int32_t)blockIdx.x % tiles, ch = (int32_t)blockIdx.x / tiles;
+    const int32_t x0 = (tile % g.tiles_x) * TX, y0 = (tile / g.tiles_x) * TY;
+    const int32_t m0 = ch * g.chunk, m1 = min(m0 + g.chunk, g.nm);
+    const int     nsteps = (m1 - m0) + 2; // planes m0-1 .. m1 (p of both neighbours)
+    if (tid == 0) {
+        for (int k = 0; k < kTmaStages; ++k) mbar_init(&full[k], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    // the tensor maps must be addressed in parameter space (a lambda capture
+    // would copy them to local memory, where TMA cannot read a descriptor)
+    const CUtensorMap* mz = &tz;
+    const CUtensorMap* mp = &tp;
+#define RVK_MF_ISSUE(j)                                                                            \
+    do {                                                                                           \
+        const int k_ = (j) % kTmaStages;                                                           \
+        mbar_arrive_expect_tx(&full[k_], NSRC * BE * 8);                                           \
+        tma_plane<DIM>(&stage[k_][0][0], mz, x0 - 2, y0 - 1, m0 - 1 + (j), &full[k_]);             \
+        if (!FIRST) tma_plane<DIM>(&stage[k_][1][0], mp, x0 - 2, y0 - 1, m0 - 1 + (j), &full[k_]); \
+    } while (0)
+    if (tid == 0)
+        for (int j = 0; j < min(kTmaStages, nsteps); ++j) RVK_MF_ISSUE(j);
+    const int     c  = (DIM == 3 ? (ty + 1) * BW : 0) + tx + 2; // this row's box index
+    const int32_t x = x0 + tx, y = y0 + ty;
+    const bool    own = x < g.nx && y < g.ny;
+    double        acc = 0.0;
+    for (int j = 0; j < nsteps; ++j) {
+        const int k = j % kTmaStages;
+        mbar_wait(&full[k], (j / kTmaStages) & 1);
+        double* P = pr[j & 3];
+        for (int e = tid; e < BE; e += NT) {
+            const double zv = stage[k][0][e];
+            P[e]            = FIRST ? zv : aypx1(op.b, zv, stage[k][1][e]);
+        }
+        __syncthreads(); // ring slot j complete; stage k consumed by every thread
+        if (tid == 0 && j + kTmaStages < nsteps) RVK_MF_ISSUE(j + kTmaStages);
+        if (j < 2) continue;
+        // row (x, y, m) with m = m0 + j - 2: planes m-1, m, m+1 = ring j-2, j-1, j
+        const double* Pl[3] = {pr[(j - 2) & 3], pr[(j - 1) & 3], pr[j & 3]};
+        double        sum   = 0.0;
+        auto term = [&](double coef, double v) { sum = add(sum, mul(coef, v)); };
+        if constexpr (BOX) {
+#pragma unroll
+            for (int dz = 0; dz < 3; ++dz)
+#pragma unroll
+                for (int dy = (DIM == 3 ? -1 : 0); dy <= (DIM == 3 ? 1 : 0); ++dy)
+#pragma unroll
+                    for (int dx = -1; dx <= 1; ++dx)
+                        term(dz == 1 && dy == 0 && dx == 0 ? g.centre : -1.0, Pl[dz][c + dy * BW + dx]);
+        } else {
+            term(-1.0, Pl[0][c]);
+            if (DIM == 3) term(-1.0, Pl[1][c - BW]);
+            term(-1.0, Pl[1][c - 1]);
+            term(g.centre, Pl[1][c]);
+            term(-1.0, Pl[1][c + 1]);
+            if (DIM == 3) term(-1.0, Pl[1][c + BW]);
+            term(-1.0, Pl[2][c]);
+        }
+        if (own) {
+            const int64_t i = ((int64_t)(m0 + j - 2) * g.ny + y) * g.nx + x;
+            const double  p = Pl[1][c];
+            op.p_new[i]     = p;
+            op.w[i]         = sum;
+            acc             = add(acc, mul(p, sum));
+        }
+    }
+#undef RVK_MF_ISSUE
+    double v[1] = {acc};
+    block_sum<1>(v, red, tid, NT, 1);
+    if (tid == 0) tail.partials[blockIdx.x] = v[0];
+    if (!last_block(tail.ticket, tid, &flag, NT, 1)) return;
+    fold_partials<1>(tail.partials, gridDim.x, v, red, tid, NT, 1);
+    if (tid == 0) {
+        op.tail(v[0]);
+        *tail.ticket = 0u;
+    }
+}
+
 template <bool FIRST>
 rvk_status launch_first(cudaStream_t s, const StencilGeom& g, const CgSpmvOp<FIRST>& op,
                         TailArgs ta, int grid)
@@ -176,6 +338,128 @@ rvk_status launch_first(cudaStream_t s, const StencilGeom& g, const CgSpmvOp<FIR
 
 } // namespace
 
+// ---- TMA plan state -----------------------------------------------------------
+struct MfTma {
+    CUtensorMap   z, p0, p1;
+    MfTmaGeom     g{};
+    const double* p0_ptr = nullptr;
+    const double* p1_ptr = nullptr;
+    int           grid   = 0;
+    int           dim    = 3;
+    bool          box    = false;
+};
+
+namespace {
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_tiled()
+{
+    static EncodeTiledFn  fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void*                           f = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(f);
+    });
+    return fn;
+}
+
+// Box (TX+4) x (TY+2) x 1 (2D: (TX+4) x 1) over the grid viewed as
+// [march][y][x]; OOB coordinates read as zero (FLOAT_OOB_FILL_NONE).
+bool encode_plane_map(CUtensorMap* m, const double* base, const StencilGeom& g, int bw, int bh)
+{
+    EncodeTiledFn enc = encode_tiled();
+    if (!enc) return false;
+    cuuint64_t dims[3], strides[2];
+    cuuint32_t box[3], es[3] = {1, 1, 1};
+    cuuint32_t rank;
+    if (g.dim == 3) {
+        rank    = 3;
+        dims[0] = (cuuint64_t)g.nx;
+        dims[1] = (cuuint64_t)g.ny;
+        dims[2] = (cuuint64_t)g.nz;
+        strides[0] = (cuuint64_t)g.nx * 8;
+        strides[1] = (cuuint64_t)g.nx * g.ny * 8;
+        box[0] = (cuuint32_t)bw;
+        box[1] = (cuuint32_t)bh;
+        box[2] = 1;
+    } else {
+        rank    = 2;
+        dims[0] = (cuuint64_t)g.nx;
+        dims[1] = (cuuint64_t)g.ny;
+        strides[0] = (cuuint64_t)g.nx * 8;
+        box[0] = (cuuint32_t)bw;
+        box[1] = 1;
+    }
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank, const_cast<double*>(base), dims, strides, box,
+               es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int DIM, bool BOX>
+int tma_blocks_per_sm()
+{
+    int per_sm = 0;
+    constexpr int nt = MfShape<DIM>::TX * MfShape<DIM>::TY;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mf_tma<false, DIM, BOX>, nt, 0) !=
+            cudaSuccess ||
+        per_sm < 1)
+        per_sm = 1;
+    return per_sm;
+}
+} // namespace
+
+MfTma* mf_tma_create(const StencilGeom& g, const double* z, const double* p0, const double* p1)
+{
+    const char* env = std::getenv("RVK_MF_TMA");
+    if (env && env[0] == '0') return nullptr;
+    // TMA needs 16-B global strides (nx even) and 32-bit coordinates
+    if (g.nx % 2 || g.nx > (1 << 30) || g.ny > (1 << 30) || g.nz > (1 << 30)) return nullptr;
+    auto* t = new MfTma();
+    t->dim  = g.dim;
+    t->box  = g.box != 0;
+    const int TX = g.dim == 3 ? MfShape<3>::TX : MfShape<2>::TX;
+    const int TY = g.dim == 3 ? MfShape<3>::TY : MfShape<2>::TY;
+    const int bw = TX + 4, bh = g.dim == 3 ? TY + 2 : 1; // see k_mf_tma: 16-B aligned x start
+    if (!encode_plane_map(&t->z, z, g, bw, bh) || !encode_plane_map(&t->p0, p0, g, bw, bh) ||
+        !encode_plane_map(&t->p1, p1, g, bw, bh)) {
+        delete t;
+        return nullptr;
+    }
+    t->p0_ptr = p0;
+    t->p1_ptr = p1;
+    MfTmaGeom& G = t->g;
+    G.nx      = (int32_t)g.nx;
+    G.ny      = g.dim == 3 ? (int32_t)g.ny : 1;
+    G.nm      = g.dim == 3 ? (int32_t)g.nz : (int32_t)g.ny;
+    G.tiles_x = (int32_t)((g.nx + TX - 1) / TX);
+    G.tiles_y = g.dim == 3 ? (int32_t)((g.ny + TY - 1) / TY) : 1;
+    G.centre  = g.centre;
+    // chunks of planes: about two waves of resident blocks, >= 16 planes each
+    // (every chunk re-reads 2 halo planes), grid within the reduction scratch
+    int per_sm = 1;
+    if (g.dim == 3) per_sm = g.box ? tma_blocks_per_sm<3, true>() : tma_blocks_per_sm<3, false>();
+    else per_sm = g.box ? tma_blocks_per_sm<2, true>() : tma_blocks_per_sm<2, false>();
+    const int64_t tiles  = (int64_t)G.tiles_x * G.tiles_y;
+    const int64_t want   = 2LL * sm_count() * per_sm;
+    int64_t       chunks = std::max<int64_t>(1, (want + tiles - 1) / tiles);
+    chunks               = std::min<int64_t>(chunks, std::max<int64_t>(1, G.nm / 16));
+    while (chunks > 1 && tiles * chunks > kMaxReduceBlocks) --chunks;
+    if (tiles * chunks > kMaxReduceBlocks) { // too many plane tiles for one launch's scratch
+        delete t;
+        return nullptr;
+    }
+    G.chunk = (int32_t)((G.nm + chunks - 1) / chunks);
+    t->grid = (int)(tiles * ((G.nm + G.chunk - 1) / G.chunk));
+    return t;
+}
+
+void mf_tma_destroy(MfTma* t) { delete t; }
+
 int mf_grid(const StencilGeom& g)
 {
     int per_sm = 0;
@@ -189,11 +473,33 @@ int mf_grid(const StencilGeom& g)
     return (int)std::min<int64_t>(tiles, (int64_t)sm_count() * per_sm);
 }
 
+namespace {
+template <bool FIRST>
+rvk_status launch_tma(cudaStream_t s, const MfTma& t, const CgSpmvOp<FIRST>& op, TailArgs ta)
+{
+    const CUtensorMap& tp = op.p_old == t.p1_ptr ? t.p1 : t.p0;
+    if (t.dim == 3 && t.box)
+        k_mf_tma<FIRST, 3, true><<<t.grid, MfShape<3>::TX * MfShape<3>::TY, 0, s>>>(t.z, tp, t.g, op, ta);
+    else if (t.dim == 3)
+        k_mf_tma<FIRST, 3, false><<<t.grid, MfShape<3>::TX * MfShape<3>::TY, 0, s>>>(t.z, tp, t.g, op, ta);
+    else if (t.box)
+        k_mf_tma<FIRST, 2, true><<<t.grid, MfShape<2>::TX * MfShape<2>::TY, 0, s>>>(t.z, tp, t.g, op, ta);
+    else
+        k_mf_tma<FIRST, 2, false><<<t.grid, MfShape<2>::TX * MfShape<2>::TY, 0, s>>>(t.z, tp, t.g, op, ta);
+    RVK_CHECK_LAUNCH("k_mf_tma");
+    return RVK_OK;
+}
+} // namespace
+
 rvk_status launch_mf_k1(cudaStream_t s, const StencilGeom& g, bool first, const double* z,
                         const double* p_old, double* p_new, double* w, CgState* st, int64_t n,
-                        int it, double* partials, unsigned int* ticket, int grid)
+                        int it, double* partials, unsigned int* ticket, int grid, const MfTma* tma)
 {
     const TailArgs ta{partials, ticket};
+    if (tma) {
+        if (first) return launch_tma(s, *tma, CgSpmvOp<true>{z, p_old, p_new, w, st, n, it, 0.0}, ta);
+        return launch_tma(s, *tma, CgSpmvOp<false>{z, p_old, p_new, w, st, n, it, 0.0}, ta);
+    }
     if (first) return launch_first(s, g, CgSpmvOp<true>{z, p_old, p_new, w, st, n, it, 0.0}, ta, grid);
     return launch_first(s, g, CgSpmvOp<false>{z, p_old, p_new, w, st, n, it, 0.0}, ta, grid);
 }

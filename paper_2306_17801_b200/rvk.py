@@ -41,6 +41,7 @@ EXPORTS = [
     "rvk_cg_solve_dev", "rvk_cg_history_dev", "rvk_cg_result", "rvk_cg_solve_host",
     "rvk_cg_solve_host_many",
     "rvk_cg_set_profiling", "rvk_cg_kernel_times", "rvk_cg_plan_mode", "rvk_cg_plan_flags",
+    "rvk_cg_plan_vector",
     "rvk_laplacian_rows_nnz", "rvk_build_laplacian_rows", "rvk_comm_unique_id", "rvk_comm_init",
     "rvk_comm_destroy", "rvk_dcg_plan_create", "rvk_dcg_plan_destroy", "rvk_dcg_solve_dev",
     "rvk_dcg_loopback_solve", "rvk_dcg_result", "rvk_dcg_window", "rvk_dcg_attach_peers",
@@ -151,6 +152,7 @@ def lib():
                                     C.POINTER(C.c_int)]),
         "rvk_cg_plan_mode": (i, [vp]),
         "rvk_cg_plan_flags": (i, [vp]),
+        "rvk_cg_plan_vector": (vp, [vp, i]),
         "rvk_laplacian_rows_nnz": (i, [i, i, i64, i64, i64, i64, i64, C.POINTER(i64)]),
         "rvk_build_laplacian_rows": (i, [vp, i, i, i64, i64, i64, i64, i64, i64, vp, vp, vp]),
         "rvk_comm_unique_id": (i, [vp, i]),
@@ -351,10 +353,12 @@ class CgPlan:
                        MODES[mode], graph)
         h = C.c_void_p()
         if isinstance(A, DeviceCsr):
+            self.n = A.n_rows
             check(lib().rvk_cg_plan_create(ctx.h, C.byref(A.c), cfg, C.byref(h)))
         else:
             dim, points, grid = A
             nx, ny, nz = (list(grid) + [1, 1])[:3]
+            self.n = nx * ny * (nz if dim == 3 else 1)
             check(lib().rvk_cg_plan_create_stencil(ctx.h, dim, points, nx, ny, nz, cfg,
                                                    C.byref(h)))
         self.h = h
@@ -423,8 +427,19 @@ class CgPlan:
         return a.value, b.value, n.value
 
     def flags(self) -> int:
-        """RVK_PLAN_* bits: 1 constant diagonal folded to a scalar, 2 matrix-free."""
+        """RVK_PLAN_* bits: 1 constant diagonal folded to a scalar, 2 matrix-free,
+        4 matrix-free via the TMA 2.5D kernel."""
         return lib().rvk_cg_plan_flags(self.h)
+
+    VEC = {"r": 0, "z": 1, "p0": 2, "p1": 3, "w": 4}
+
+    def work_vector(self, which: str) -> np.ndarray:
+        """Test hook: a plan work vector (after a synchronised solve)."""
+        ptr = lib().rvk_cg_plan_vector(self.h, self.VEC[which])
+        out = np.empty(self.n, np.float64)
+        check(lib().rvk_memcpy_d2h(self.ctx.h, out.ctypes.data, ptr, out.nbytes))
+        check(lib().rvk_ctx_synchronize(self.ctx.h))
+        return out
 
     def mode(self) -> str:
         m = lib().rvk_cg_plan_mode(self.h)
