@@ -439,13 +439,17 @@ MfTma* mf_tma_create(const StencilGeom& g, const double* z, const double* p0, co
     G.tiles_x = (int32_t)((g.nx + TX - 1) / TX);
     G.tiles_y = g.dim == 3 ? (int32_t)((g.ny + TY - 1) / TY) : 1;
     G.centre  = g.centre;
-    // chunks of planes: about two waves of resident blocks, >= 16 planes each
+    // chunks of planes: a few waves of resident blocks, >= 16 planes each
     // (every chunk re-reads 2 halo planes), grid within the reduction scratch
     int per_sm = 1;
     if (g.dim == 3) per_sm = g.box ? tma_blocks_per_sm<3, true>() : tma_blocks_per_sm<3, false>();
     else per_sm = g.box ? tma_blocks_per_sm<2, true>() : tma_blocks_per_sm<2, false>();
     const int64_t tiles  = (int64_t)G.tiles_x * G.tiles_y;
-    const int64_t want   = 2LL * sm_count() * per_sm;
+    // ~4 waves of resident blocks (measured: 7-point 256^3 K1 125 / 110 / 107 /
+    // 101 / 101 us at 1 / 2 / 3 / 4 / 8 waves; RVK_MF_WAVES overrides)
+    const char*   wv     = std::getenv("RVK_MF_WAVES");
+    const int64_t waves  = wv ? std::max(1, std::atoi(wv)) : 4;
+    const int64_t want   = waves * sm_count() * per_sm;
     int64_t       chunks = std::max<int64_t>(1, (want + tiles - 1) / tiles);
     chunks               = std::min<int64_t>(chunks, std::max<int64_t>(1, G.nm / 16));
     while (chunks > 1 && tiles * chunks > kMaxReduceBlocks) --chunks;

@@ -273,7 +273,12 @@ def bench_main(args, cfg):
     sh = shards[rank]
     stream = torch.cuda.Stream()
     ctx = rvk.Ctx(stream.cuda_stream)
-    comm = None if shared else init_comm(rank, world)
+    comm, comm_err = None, None
+    if not shared:
+        try:
+            comm = init_comm(rank, world)
+        except Exception as e:  # noqa: BLE001 -- PEER needs no NCCL; report it
+            comm_err = f"NCCL unavailable: {e}".splitlines()[0][:200]
     A = local_laplacian(ctx, dim, pts, grid, sh)
     b = rvk.DeviceArray(sh.n_own)
     x = rvk.DeviceArray(sh.n_own)
@@ -282,25 +287,26 @@ def bench_main(args, cfg):
     rvk.check(rvk.lib().rvk_fill_rhs(ctx.h, (full_seed + sh.row_begin) & (2 ** 64 - 1), sh.n_own,
                                      b.ptr))
     nccl_plan = ref_hist = ref_x = None
-    if not shared:
+    if comm is not None:
         nccl_plan = ShardPlan(ctx, A, sh, 20, comm=comm)
         nccl_plan.solve_dev(b, x)
         ref_hist = nccl_plan.result().hist
         ref_x = x.download(ctx)
 
-    backend, fallback, opened, plan = "nccl", None, [], nccl_plan
-    if shared or getattr(args, "comm", "peer") == "peer":
+    backend, fallback, opened, plan = "nccl", comm_err, [], nccl_plan
+    if comm is None or getattr(args, "comm", "peer") == "peer":
         try:
             peer_plan = ShardPlan(ctx, A, sh, 20)
             opened = connect_peers(peer_plan, shards, rank, world)
             peer_plan.solve_dev(b, x)
             ph = peer_plan.result().hist
-            ok = shared or (np.array_equal(ph, ref_hist) and np.array_equal(x.download(ctx), ref_x))
+            ok = nccl_plan is None or (np.array_equal(ph, ref_hist) and
+                                       np.array_equal(x.download(ctx), ref_x))
             err = None if ok else "PEER solve differs from the NCCL solve"
         except Exception as e:  # noqa: BLE001 -- report and fall back, never hang
             err, peer_plan = f"PEER setup failed: {e}".splitlines()[0][:200], None
-        if shared and err is not None:
-            raise RuntimeError(err)
+        if nccl_plan is None and err is not None:
+            raise RuntimeError(err)  # no backend left
         flags = torch.tensor([0 if err is None else 1], device=tdev)
         dist.all_reduce(flags)  # every rank takes the same backend
         if int(flags.item()) == 0:
