@@ -183,8 +183,6 @@ __global__ void __launch_bounds__(kMfThreads, 2)
 // ---------------------------------------------------------------------------
 // TMA 2.5D marching kernel
 // ---------------------------------------------------------------------------
-constexpr int kTmaStages = 6; // planes in flight per block
-
 struct MfTmaGeom {
     int32_t nx, ny, nm;       // plane extent (2D: nx, 1) and marching extent (3D nz, 2D ny)
     int32_t tiles_x, tiles_y; // plane tiles
@@ -192,16 +190,37 @@ struct MfTmaGeom {
     double  centre;
 };
 
-template <int DIM>
-struct MfShape;
-template <>
-struct MfShape<3> {
-    static constexpr int TX = 32, TY = 8;
+// Tile of the plane per block (TX x TY rows), RY rows per thread along y,
+// ring depth.  27-point: each thread sweeps 2 y-rows so every loaded p value
+// of a (plane, line) serves the up-to-3 rows it neighbours -- 12 shared-memory
+// loads per plane for 2 rows instead of 18 (the 1-row kernel is bound by its
+// 27 LDS per row).
+template <int DIM, bool BOX>
+struct MfShape {
+    static constexpr int TX = 128, TY = 1, RY = 1, STAGES = 6; // 2D
 };
 template <>
-struct MfShape<2> {
-    static constexpr int TX = 128, TY = 1;
+struct MfShape<3, false> {
+    static constexpr int TX = 32, TY = 8, RY = 1, STAGES = 6;
 };
+template <>
+struct MfShape<3, true> {
+    static constexpr int TX = 32, TY = 16, RY = 2, STAGES = 4;
+};
+template <int DIM, bool BOX>
+constexpr int mf_threads()
+{
+    return MfShape<DIM, BOX>::TX * (MfShape<DIM, BOX>::TY / MfShape<DIM, BOX>::RY);
+}
+// dynamic shared memory of k_mf_tma: STAGES x 2 boxes + 4 p planes (box pitch BP)
+template <int DIM, bool BOX>
+constexpr size_t mf_smem_bytes()
+{
+    using S          = MfShape<DIM, BOX>;
+    constexpr int be = (S::TX + 4) * (DIM == 3 ? S::TY + 2 : 1);
+    constexpr int bp = (be + 15) & ~15;
+    return sizeof(double) * (size_t)bp * (2 * S::STAGES + 4);
+}
 
 template <int DIM>
 __device__ __forceinline__ void tma_plane(void* dst, const CUtensorMap* map, int32_t x, int32_t y,
@@ -221,19 +240,24 @@ __device__ __forceinline__ void tma_plane(void* dst, const CUtensorMap* map, int
 }
 
 template <bool FIRST, int DIM, bool BOX>
-__global__ void __launch_bounds__(MfShape<DIM>::TX * MfShape<DIM>::TY)
+__global__ void __launch_bounds__(mf_threads<DIM, BOX>())
     k_mf_tma(const __grid_constant__ CUtensorMap tz, const __grid_constant__ CUtensorMap tp,
              MfTmaGeom g, CgSpmvOp<FIRST> op_in, TailArgs tail)
 {
-    constexpr int TX = MfShape<DIM>::TX, TY = MfShape<DIM>::TY, NT = TX * TY;
+    using S                    = MfShape<DIM, BOX>;
+    constexpr int TX = S::TX, TY = S::TY, RY = S::RY, NT = mf_threads<DIM, BOX>();
+    constexpr int kTmaStages   = S::STAGES;
     // box: x0-2 .. x0+TX+1 (the innermost TMA start coordinate must be 16-B
     // aligned -- x0-1 traps with an illegal instruction on B200, measured),
     // y0-1 .. y0+TY (3D), one plane
     constexpr int BW = TX + 4, BH = DIM == 3 ? TY + 2 : 1, BE = BW * BH;
     constexpr int BP   = (BE + 15) & ~15; // box pitch: every TMA destination 128-B aligned
     constexpr int NSRC = FIRST ? 1 : 2;
-    __shared__ __align__(128) double stage[kTmaStages][2][BP]; // [z | p_old] boxes
-    __shared__ double                pr[4][BE];                 // p = z + b p_old, 4-plane ring
+    // dynamic shared memory (> 48 KB for the 27-point tile): [z | p_old] box
+    // ring, then the 4-plane p ring
+    extern __shared__ __align__(128) unsigned char mf_smem[];
+    auto stage = reinterpret_cast<double(*)[2][BP]>(mf_smem);
+    auto pr    = reinterpret_cast<double(*)[BP]>(mf_smem + sizeof(double) * kTmaStages * 2 * BP);
     __shared__ __align__(8) uint64_t full[kTmaStages];
     __shared__ double                red[32];
     __shared__ int                   flag;
@@ -264,9 +288,9 @@ __global__ void __launch_bounds__(MfShape<DIM>::TX * MfShape<DIM>::TY)
     } while (0)
     if (tid == 0)
         for (int j = 0; j < min(kTmaStages, nsteps); ++j) RVK_MF_ISSUE(j);
-    const int     c  = (DIM == 3 ? (ty + 1) * BW : 0) + tx + 2; // this row's box index
-    const int32_t x = x0 + tx, y = y0 + ty;
-    const bool    own = x < g.nx && y < g.ny;
+    // this thread's rows: (x, y0 + ty*RY + r), r < RY; box index of row r: c + r*BW
+    const int     c  = (DIM == 3 ? (ty * RY + 1) * BW : 0) + tx + 2;
+    const int32_t x = x0 + tx, y = y0 + ty * RY;
     double        acc = 0.0;
     for (int j = 0; j < nsteps; ++j) {
         const int k = j % kTmaStages;
@@ -279,34 +303,48 @@ __global__ void __launch_bounds__(MfShape<DIM>::TX * MfShape<DIM>::TY)
         __syncthreads(); // ring slot j complete; stage k consumed by every thread
         if (tid == 0 && j + kTmaStages < nsteps) RVK_MF_ISSUE(j + kTmaStages);
         if (j < 2) continue;
-        // row (x, y, m) with m = m0 + j - 2: planes m-1, m, m+1 = ring j-2, j-1, j
+        // rows (x, y+r, m) with m = m0 + j - 2: planes m-1, m, m+1 = ring j-2, j-1, j
         const double* Pl[3] = {pr[(j - 2) & 3], pr[(j - 1) & 3], pr[j & 3]};
-        double        sum   = 0.0;
-        auto term = [&](double coef, double v) { sum = add(sum, mul(coef, v)); };
+        double        sum[RY];
+#pragma unroll
+        for (int r = 0; r < RY; ++r) sum[r] = 0.0;
+        auto term = [&](int r, double coef, double v) { sum[r] = add(sum[r], mul(coef, v)); };
         if constexpr (BOX) {
+            // (dz, line, dx) ascending; a line yy feeds every row r with
+            // dy = yy - r in [-1, 1] -- per row the terms stay in ascending
+            // column order (dz, dy, dx), exactly the CSR's
 #pragma unroll
             for (int dz = 0; dz < 3; ++dz)
 #pragma unroll
-                for (int dy = (DIM == 3 ? -1 : 0); dy <= (DIM == 3 ? 1 : 0); ++dy)
+                for (int yy = (DIM == 3 ? -1 : 0); yy <= (DIM == 3 ? RY : 0); ++yy)
 #pragma unroll
-                    for (int dx = -1; dx <= 1; ++dx)
-                        term(dz == 1 && dy == 0 && dx == 0 ? g.centre : -1.0, Pl[dz][c + dy * BW + dx]);
+                    for (int dx = -1; dx <= 1; ++dx) {
+                        const double v = Pl[dz][c + yy * BW + dx];
+#pragma unroll
+                        for (int r = 0; r < RY; ++r) {
+                            const int dy = yy - r;
+                            if (DIM == 3 && (dy < -1 || dy > 1)) continue;
+                            term(r, dz == 1 && dy == 0 && dx == 0 ? g.centre : -1.0, v);
+                        }
+                    }
         } else {
-            term(-1.0, Pl[0][c]);
-            if (DIM == 3) term(-1.0, Pl[1][c - BW]);
-            term(-1.0, Pl[1][c - 1]);
-            term(g.centre, Pl[1][c]);
-            term(-1.0, Pl[1][c + 1]);
-            if (DIM == 3) term(-1.0, Pl[1][c + BW]);
-            term(-1.0, Pl[2][c]);
+            term(0, -1.0, Pl[0][c]);
+            if (DIM == 3) term(0, -1.0, Pl[1][c - BW]);
+            term(0, -1.0, Pl[1][c - 1]);
+            term(0, g.centre, Pl[1][c]);
+            term(0, -1.0, Pl[1][c + 1]);
+            if (DIM == 3) term(0, -1.0, Pl[1][c + BW]);
+            term(0, -1.0, Pl[2][c]);
         }
-        if (own) {
-            const int64_t i = ((int64_t)(m0 + j - 2) * g.ny + y) * g.nx + x;
-            const double  p = Pl[1][c];
-            op.p_new[i]     = p;
-            op.w[i]         = sum;
-            acc             = add(acc, mul(p, sum));
-        }
+#pragma unroll
+        for (int r = 0; r < RY; ++r)
+            if (x < g.nx && y + r < g.ny) {
+                const int64_t i = ((int64_t)(m0 + j - 2) * g.ny + y + r) * g.nx + x;
+                const double  p = Pl[1][c + r * BW];
+                op.p_new[i]     = p;
+                op.w[i]         = sum[r];
+                acc             = add(acc, mul(p, sum[r]));
+            }
     }
 #undef RVK_MF_ISSUE
     double v[1] = {acc};
@@ -401,12 +439,25 @@ bool encode_plane_map(CUtensorMap* m, const double* base, const StencilGeom& g, 
 }
 
 template <int DIM, bool BOX>
+void mf_configure()
+{
+    static std::once_flag once; // before any graph capture (plan creation)
+    std::call_once(once, [] {
+        cudaFuncSetAttribute(k_mf_tma<true, DIM, BOX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)mf_smem_bytes<DIM, BOX>());
+        cudaFuncSetAttribute(k_mf_tma<false, DIM, BOX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)mf_smem_bytes<DIM, BOX>());
+    });
+}
+
+template <int DIM, bool BOX>
 int tma_blocks_per_sm()
 {
+    mf_configure<DIM, BOX>();
     int per_sm = 0;
-    constexpr int nt = MfShape<DIM>::TX * MfShape<DIM>::TY;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mf_tma<false, DIM, BOX>, nt, 0) !=
-            cudaSuccess ||
+    constexpr int nt = mf_threads<DIM, BOX>();
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mf_tma<false, DIM, BOX>, nt,
+                                                      mf_smem_bytes<DIM, BOX>()) != cudaSuccess ||
         per_sm < 1)
         per_sm = 1;
     return per_sm;
@@ -422,8 +473,8 @@ MfTma* mf_tma_create(const StencilGeom& g, const double* z, const double* p0, co
     auto* t = new MfTma();
     t->dim  = g.dim;
     t->box  = g.box != 0;
-    const int TX = g.dim == 3 ? MfShape<3>::TX : MfShape<2>::TX;
-    const int TY = g.dim == 3 ? MfShape<3>::TY : MfShape<2>::TY;
+    const int TX = g.dim == 3 ? (g.box ? MfShape<3, true>::TX : MfShape<3, false>::TX) : MfShape<2, false>::TX;
+    const int TY = g.dim == 3 ? (g.box ? MfShape<3, true>::TY : MfShape<3, false>::TY) : MfShape<2, false>::TY;
     const int bw = TX + 4, bh = g.dim == 3 ? TY + 2 : 1; // see k_mf_tma: 16-B aligned x start
     if (!encode_plane_map(&t->z, z, g, bw, bh) || !encode_plane_map(&t->p0, p0, g, bw, bh) ||
         !encode_plane_map(&t->p1, p1, g, bw, bh)) {
@@ -482,14 +533,13 @@ template <bool FIRST>
 rvk_status launch_tma(cudaStream_t s, const MfTma& t, const CgSpmvOp<FIRST>& op, TailArgs ta)
 {
     const CUtensorMap& tp = op.p_old == t.p1_ptr ? t.p1 : t.p0;
-    if (t.dim == 3 && t.box)
-        k_mf_tma<FIRST, 3, true><<<t.grid, MfShape<3>::TX * MfShape<3>::TY, 0, s>>>(t.z, tp, t.g, op, ta);
-    else if (t.dim == 3)
-        k_mf_tma<FIRST, 3, false><<<t.grid, MfShape<3>::TX * MfShape<3>::TY, 0, s>>>(t.z, tp, t.g, op, ta);
-    else if (t.box)
-        k_mf_tma<FIRST, 2, true><<<t.grid, MfShape<2>::TX * MfShape<2>::TY, 0, s>>>(t.z, tp, t.g, op, ta);
-    else
-        k_mf_tma<FIRST, 2, false><<<t.grid, MfShape<2>::TX * MfShape<2>::TY, 0, s>>>(t.z, tp, t.g, op, ta);
+#define RVK_MF_LAUNCH(D, B)                                                                        \
+    k_mf_tma<FIRST, D, B><<<t.grid, mf_threads<D, B>(), mf_smem_bytes<D, B>(), s>>>(t.z, tp, t.g, op, ta)
+    if (t.dim == 3 && t.box) RVK_MF_LAUNCH(3, true);
+    else if (t.dim == 3) RVK_MF_LAUNCH(3, false);
+    else if (t.box) RVK_MF_LAUNCH(2, true);
+    else RVK_MF_LAUNCH(2, false);
+#undef RVK_MF_LAUNCH
     RVK_CHECK_LAUNCH("k_mf_tma");
     return RVK_OK;
 }

@@ -34,7 +34,9 @@ def main(tag="r01"):
     out = {"_note": f"{tag}: ncu --set full --clock-control none, one launch each "
                     "(serialised, after 4 warm launches); per-launch DRAM bytes = traffic"}
     for cfg, files in {"7pt256": {"k1": "prof_k1", "k2": "prof_k2"},
-                       "27pt256": {"k1": "prof_k1_27pt"}, "9pt4096": {"k1": "prof_k1_9pt"}}.items():
+                       "27pt256": {"k1": "prof_k1_27pt"}, "9pt4096": {"k1": "prof_k1_9pt"},
+                       "7pt256_matrix_free": {"k1": "prof_mf"},
+                       "27pt256_matrix_free": {"k1": "prof_mf_27pt"}}.items():
         for k, f in files.items():
             path = os.path.join(G, f + ".ncu-rep")
             if os.path.exists(path):
