@@ -205,7 +205,7 @@ struct MfShape<3, false> {
 };
 template <>
 struct MfShape<3, true> {
-    static constexpr int TX = 32, TY = 16, RY = 2, STAGES = 4;
+    static constexpr int TX = 32, TY = 16, RY = 2, STAGES = 2;
 };
 template <int DIM, bool BOX>
 constexpr int mf_threads()
