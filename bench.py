@@ -59,12 +59,16 @@ def peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def bytes_model(n: int, nnz: int, mode: str = "fused", const_diag: bool = False):
+def bytes_model(n: int, nnz: int, mode: str = "fused", const_diag: bool = False,
+                off32: bool = False):
     """Algorithmic HBM bytes.  All FP64 + int64 offsets + int32 cols.
     k1 = the SpMV launch (fused: + on-the-fly AYPX), k2 = the rest of an iteration.
     const_diag: the plan folded a constant Jacobi diagonal into a scalar
     (RVK_PLAN_CONST_DIAG), so the dinv stream (8n per iteration and in the
-    setup) is not part of the algorithm's traffic any more."""
+    setup) is not part of the algorithm's traffic any more.  off32: the SpMV
+    streams the plan's int32 copy of the row offsets (RVK_PLAN_OFF32): 4 instead
+    of 8 bytes per row."""
+    ob = 4 if off32 else 8
     if mode == "stencil":                        # matrix-free: no CSR, constant dinv
         k1 = 32 * n                              # z, p_old -> p_new, w
         k2 = 56 * n                              # x, p, r, w -> x, r, z
@@ -74,10 +78,10 @@ def bytes_model(n: int, nnz: int, mode: str = "fused", const_diag: bool = False)
                 "b_min_survey_solve": MAX_IT * (12 * nnz + 8 * (n + 1) + 96 * n) + 64 * n,
                 "flops_iter": 2 * nnz + 13 * n}
     if mode == "fused":
-        k1 = 12 * nnz + 8 * (n + 1) + 32 * n    # off, cols, vals, z, p_old -> p_new, w
+        k1 = 12 * nnz + ob * (n + 1) + 32 * n   # off, cols, vals, z, p_old -> p_new, w
         k2 = (56 if const_diag else 64) * n      # x, p, r, w, (dinv) -> x, r, z
     else:
-        k1 = 12 * nnz + 8 * (n + 1) + 16 * n    # off, cols, vals, p -> w
+        k1 = 12 * nnz + ob * (n + 1) + 16 * n   # off, cols, vals, p -> w
         k2 = 136 * n                             # aypx 24, dot 16, 2 axpy 48, jacobi 24, norm 8, dot 16
     b_min = k1 + k2                              # = 12 nnz + 8 (n+1) + 96 n  (88 n const_diag)
     b_ref = 12 * nnz + 8 * (n + 1) + 152 * n     # reference's unfused sequence
@@ -356,8 +360,9 @@ def run_gpu(args, cfg):
     rvk.check(rvk.lib().rvk_fill_rhs(ctx.h, 0x9E3779B97F4A7C15, n, b.ptr))
     plan = rvk.CgPlan(ctx, A, max_it=MAX_IT, mode=args.mode, use_graph=not args.no_graph)
     const_diag = bool(plan.flags() & 1)
+    off32 = bool(plan.flags() & 8)
     bm = bytes_model(n, nnz, "stencil" if args.operator == "stencil" else
-                     ("unfused" if args.mode == "unfused" else "fused"), const_diag)
+                     ("unfused" if args.mode == "unfused" else "fused"), const_diag, off32)
     hbm_peak, peak_src = peaks()
     ws_bytes = 20 * nnz + 8 * (n + 1) + 9 * 8 * n
     log(f"{desc}: n={n} nnz={nnz} working set {ws_bytes/1e9:.2f} GB (L2 {L2_BYTES/1e6:.0f} MB)")
@@ -488,6 +493,7 @@ def run_gpu(args, cfg):
                            "achieved": round(solve_gbs, 1), "frac": round(solve_gbs / hbm_peak, 4),
                            "update_kernel_gbs": round(k2_gbs, 1),
                            "const_diag_folded": const_diag,
+                           "int32_row_offsets": off32,
                            "survey_b_min_gbs": round(bm["b_min_survey_solve"] / (ms * 1e-3) / 1e9, 1),
                            "b_ref_gbs": round(bm["b_ref_solve"] / (ms * 1e-3) / 1e9, 1)},
         "host_syncs_per_iter": syncs / (args.steps * MAX_IT),

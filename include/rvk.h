@@ -235,6 +235,7 @@ rvk_status rvk_cg_solve_host_many(rvk_cg_plan plan, int nrhs, const double* cons
 #define RVK_PLAN_CONST_DIAG  1
 #define RVK_PLAN_MATRIX_FREE 2
 #define RVK_PLAN_MF_TMA      4  /* matrix-free K1 is the TMA 2.5D marching kernel */
+#define RVK_PLAN_OFF32       8  /* the SpMV streams a plan-owned int32 copy of the row offsets */
 int        rvk_cg_plan_flags(rvk_cg_plan plan);
 /* Test hook (the reference's "exposed for equivalence tests" spirit,
  * kernels.hpp:50-76): device pointer of a plan work vector after a solve.
@@ -305,6 +306,7 @@ rvk_status rvk_dcg_solve_dev(rvk_dcg_plan plan, const double* b_own, double* x_o
 rvk_status rvk_dcg_loopback_solve(rvk_dcg_plan* plans, int nplans, const double* const* b_own,
                                   double* const* x_own);
 rvk_status rvk_dcg_result(rvk_dcg_plan plan, double* hist_host, rvk_cg_info* info);
+int        rvk_dcg_plan_flags(rvk_dcg_plan plan); /* RVK_PLAN_* bits (CONST_DIAG, OFF32) */
 
 /* PEER backend (NVLink P2P; the fused compute+communication path).  Each
  * plan owns one device window [flags | gather slots | z | p0 | p1]; once

@@ -462,6 +462,29 @@ __global__ void k_const_check(int64_t n, const unsigned long long* __restrict__ 
         }
 }
 
+__global__ void k_off_narrow(int64_t n1, const int64_t* __restrict__ off, int32_t* __restrict__ o32)
+{
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n1;
+         i += (int64_t)gridDim.x * blockDim.x)
+        o32[i] = (int32_t)off[i];
+}
+
+rvk_status make_off32(cudaStream_t s, const rvk_csr& A, int32_t** out)
+{
+    *out = nullptr;
+    // opt-in (RVK_OFF32=1): bit-exact, but measured SLOWER on B200 (7-point
+    // 256^3 K1 372 vs 337 us, 27-point 1274 vs 1056 us) despite 4 B/row less
+    const char* env = std::getenv("RVK_OFF32");
+    if (!(env && env[0] == '1') || A.nnz >= ((int64_t)1 << 31) - 16 || A.n_rows < 1) return RVK_OK;
+    int32_t* o = nullptr;
+    RVK_CUDA(cudaMalloc(reinterpret_cast<void**>(&o), (size_t)(A.n_rows + 1 + 8) * sizeof(int32_t)));
+    RVK_CUDA(cudaMemsetAsync(o, 0, (size_t)(A.n_rows + 1 + 8) * sizeof(int32_t), s));
+    k_off_narrow<<<update_grid(A.n_rows + 1), kUpdThreads, 0, s>>>(A.n_rows + 1, A.row_offsets, o);
+    RVK_CHECK_LAUNCH("k_off_narrow");
+    *out = o;
+    return RVK_OK;
+}
+
 rvk_status vector_is_constant(cudaStream_t s, int64_t n, const double* v, bool* is_const,
                               double* value)
 {
@@ -495,6 +518,7 @@ struct rvk_cg_plan_s {
     StencilGeom   geom{};
     double        dconst = 0.0;             // constant dinv (stencil, or a detected constant diagonal)
     bool          const_diag = false;       // CSR plan: every dinv[i] bit-identical -> scalar
+    int32_t*      off32      = nullptr;     // int32 row offsets for the SpMV stream (nnz < 2^31)
     int           mf_grid = 0;
     MfTma*        mf_tma  = nullptr;         // TMA 2.5D matrix-free kernel state (or null)
     double*       dinv = nullptr;
@@ -1045,6 +1069,10 @@ rvk_status rvk_cg_plan_create(rvk_ctx ctx, const rvk_csr* A, rvk_cg_config cfg, 
     rvk_status rc = RVK_OK;
     if (cfg.pc == RVK_PC_JACOBI) rc = rvk_csr_diagonal_inverse(ctx, A, P->dinv);
     else rc = rvk_set(ctx, A->n_rows, 1.0, P->dinv);
+    // optional one-time int32 copy of the row offsets the SpMV streams
+    // (opt-in RVK_OFF32=1, see make_off32)
+    if (rc == RVK_OK) rc = make_off32(s, *A, &P->off32);
+    if (rc == RVK_OK) P->sa.off32 = P->off32;
     // Constant-coefficient operators with Dirichlet truncation have ONE
     // diagonal value, so dinv is a constant vector: the fused K0/K2 then
     // multiply by the scalar (bit-identical z = dinv[i] * r[i]) and skip the
@@ -1066,7 +1094,7 @@ int rvk_cg_plan_flags(rvk_cg_plan P)
 {
     if (!P) return -1;
     return (P->const_diag ? RVK_PLAN_CONST_DIAG : 0) | (P->stencil ? RVK_PLAN_MATRIX_FREE : 0) |
-           (P->mf_tma ? RVK_PLAN_MF_TMA : 0);
+           (P->mf_tma ? RVK_PLAN_MF_TMA : 0) | (P->off32 ? RVK_PLAN_OFF32 : 0);
 }
 
 const double* rvk_cg_plan_vector(rvk_cg_plan P, int which)
@@ -1152,7 +1180,7 @@ rvk_status rvk_cg_plan_destroy(rvk_cg_plan P)
     if (P->s_out) cudaStreamDestroy(P->s_out);
     void* bufs[] = {P->dinv, P->r, P->z, P->p[0], P->p[1], P->w, P->hist, P->st,
                     P->partials, P->tickets, P->tmp, P->b_buf, P->x_buf, P->b_buf2,
-                    P->x_buf2, P->hist_all, P->st_all};
+                    P->x_buf2, P->hist_all, P->st_all, P->off32};
     for (void* b : bufs)
         if (b) cudaFree(b);
     delete P;

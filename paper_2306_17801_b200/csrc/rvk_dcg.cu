@@ -526,6 +526,7 @@ struct rvk_dcg_plan_s {
     unsigned int* tickets = nullptr;
     DcgPeer       peer{};          // peer.on: PEER backend attached
     bool          const_diag = false; // Jacobi diagonal is one value: dconst
+    int32_t*      off32      = nullptr; // int32 row offsets for the SpMV stream
     double        dconst     = 0.0;
     void**        peer_tab = nullptr; // device: gather[nranks] then flags[nranks]
 };
@@ -833,6 +834,8 @@ rvk_status rvk_dcg_plan_create(rvk_ctx ctx, const rvk_csr* A, rvk_shard sh, rvk_
     const char* cd = std::getenv("RVK_CONST_DIAG");
     if (rc == RVK_OK && cfg.pc == RVK_PC_JACOBI && sh.n_own > 0 && cd && cd[0] == '1')
         rc = vector_is_constant(ctx->stream, sh.n_own, P->dinv, &P->const_diag, &P->dconst);
+    if (rc == RVK_OK) rc = make_off32(ctx->stream, *A, &P->off32);
+    if (rc == RVK_OK) P->sa.off32 = P->off32;
     if (rc != RVK_OK) {
         rvk_dcg_plan_destroy(P);
         return rc;
@@ -848,7 +851,7 @@ rvk_status rvk_dcg_plan_destroy(rvk_dcg_plan P)
     // (PEER: the caller keeps every rank alive past its last solve -- a
     // barrier before destroy -- since peers store into this window)
     void* bufs[] = {P->win, P->dinv, P->r, P->w, P->hist, P->beta, P->st, P->partials, P->tickets,
-                    P->peer_tab};
+                    P->peer_tab, P->off32};
     for (void* b : bufs)
         if (b) cudaFree(b);
     delete P;
@@ -923,6 +926,12 @@ rvk_status rvk_dcg_result(rvk_dcg_plan P, double* hist_host, rvk_cg_info* info)
         return set_error(RVK_ERR_COMM, "dcg_solve: a peer did not arrive within %llu s (PEER backend)",
                          (unsigned long long)(kPeerTimeoutNs / 1000000000ull));
     return RVK_OK;
+}
+
+int rvk_dcg_plan_flags(rvk_dcg_plan P)
+{
+    if (!P) return -1;
+    return (P->const_diag ? RVK_PLAN_CONST_DIAG : 0) | (P->off32 ? RVK_PLAN_OFF32 : 0);
 }
 
 // ---- PEER backend ----------------------------------------------------------

@@ -109,6 +109,9 @@ struct SpmvArgs {
     const int64_t* off;
     const int32_t* cols;
     const double*  vals;
+    // plan-owned int32 copy of the row offsets (nnz < 2^31; padded by >= 4
+    // entries) or null: the mainloop then streams 4 instead of 8 B per row
+    const int32_t* off32;
 
     size_t smem_bytes() const { return kSpmvHeaderBytes + (size_t)stages * stage_bytes; }
 };
@@ -279,16 +282,16 @@ __device__ __forceinline__ auto spmv_own(const Op& op, int64_t i, const G& gathe
 // ---------------------------------------------------------------------------
 // Direct tiles: thread-per-row straight from global memory (rare path).
 // ---------------------------------------------------------------------------
-template <class Op, class Acc>
+template <class Op, class Acc, class OffT>
 __device__ __forceinline__ Acc spmv_rows_direct(const Op& op, Acc acc, int gtid, int gsize,
                                                    int rows, int64_t r0,
-                                                   const int64_t* __restrict__ O,
+                                                   const OffT* __restrict__ O,
                                                    const int32_t* __restrict__ Cc,
                                                    const double* __restrict__ V)
 {
     for (int lr = gtid; lr < rows; lr += gsize) {
         const auto    own = spmv_own(op, r0 + lr, [&](int64_t c) { return op.fetch((int32_t)c); });
-        const int64_t kb = O[lr], ke = O[lr + 1];
+        const int64_t kb = (int64_t)O[lr], ke = (int64_t)O[lr + 1];
         double        sum = 0.0;
         for (int64_t k = kb; k < ke; k += kSpmvUnroll) {
             int32_t c[kSpmvUnroll];
@@ -346,9 +349,9 @@ __device__ __forceinline__ int window_index(const StageWindows& W, int64_t c)
 // Stage-local 32-bit indices keep the address arithmetic cheap.  WIN: the
 // gathers read the stage's x-windows (LDS) instead of global memory.
 // ---------------------------------------------------------------------------
-template <bool WIN, class Op, class Acc>
+template <bool WIN, class Op, class Acc, class OffT>
 __device__ __forceinline__ Acc spmv_rows_staged(const Op& op, Acc acc, int gtid, int gsize,
-                                                   int rows, int64_t r0, const int64_t* O,
+                                                   int rows, int64_t r0, const OffT* O,
                                                    int64_t kv0, const int32_t* Cc,
                                                    const double* V, const StageWindows& W)
 {
@@ -358,8 +361,8 @@ __device__ __forceinline__ Acc spmv_rows_staged(const Op& op, Acc acc, int gtid,
     };
     for (int lr = gtid; lr < rows; lr += gsize) {
         const auto own = spmv_own(op, r0 + lr, gather); // epilogue operands, in flight early
-        const int  kb  = (int)(O[lr] - kv0);
-        const int  ke  = (int)(O[lr + 1] - kv0);
+        const int  kb  = (int)((int64_t)O[lr] - kv0);
+        const int  ke  = (int)((int64_t)O[lr + 1] - kv0);
         double     sum = 0.0;
         for (int k = kb; k < ke; k += kSpmvUnroll) {
             int32_t c[kSpmvUnroll];
@@ -410,9 +413,18 @@ struct spmv_sys_fence<Op, std::void_t<decltype(Op::kSysFence)>>
 template <class Op>
 using spmv_acc_t = std::conditional_t<spmv_sums<Op>::value == 1, double, SumVec<spmv_sums<Op>::value>>;
 
-template <class Op>
+template <class OffT>
+__device__ __forceinline__ const OffT* spmv_offsets(const SpmvArgs& A)
+{
+    if constexpr (sizeof(OffT) == 4) return A.off32;
+    else return A.off;
+}
+
+// OffT: int64_t (the matrix's own offsets) or int32_t (SpmvArgs::off32).
+template <class Op, class OffT = int64_t>
 __global__ void __launch_bounds__(kSpmvThreads, 1) k_spmv_tma(SpmvArgs A, Op op_in, TailArgs tail)
 {
+    const OffT* __restrict__ OFF = spmv_offsets<OffT>(A);
     extern __shared__ __align__(128) unsigned char smem_raw[];
     uint64_t*      full   = reinterpret_cast<uint64_t*>(smem_raw);
     uint64_t*      empty  = full + kSpmvMaxStages;
@@ -444,8 +456,8 @@ __global__ void __launch_bounds__(kSpmvThreads, 1) k_spmv_tma(SpmvArgs A, Op op_
             int64_t        k0 = 0, k1 = 0; // slab bounds, prefetched one tile ahead
             if (v < A.n_tiles) {
                 const int64_t t = spmv_tile(A, v);
-                k0 = __ldg(A.off + t * A.R);
-                k1 = __ldg(A.off + min(t * A.R + A.R, A.n_rows));
+                k0 = (int64_t)__ldg(OFF + t * A.R);
+                k1 = (int64_t)__ldg(OFF + min(t * A.R + A.R, A.n_rows));
             }
             for (int j = 0; v < A.n_tiles; ++j, v += gridDim.x) {
                 const int s = j % A.stages;
@@ -457,8 +469,8 @@ __global__ void __launch_bounds__(kSpmvThreads, 1) k_spmv_tma(SpmvArgs A, Op op_
                 const int64_t vn  = v + gridDim.x;
                 const int64_t tn  = vn < A.n_tiles ? spmv_tile(A, vn) : A.n_tiles;
                 if (tn < A.n_tiles) {
-                    k0 = __ldg(A.off + tn * A.R);
-                    k1 = __ldg(A.off + min(tn * A.R + A.R, A.n_rows));
+                    k0 = (int64_t)__ldg(OFF + tn * A.R);
+                    k1 = (int64_t)__ldg(OFF + min(tn * A.R + A.R, A.n_rows));
                 }
                 const int64_t kv0 = ck0 & ~int64_t(1), kv1 = (ck1 + 1) & ~int64_t(1);
                 const int64_t kc0 = ck0 & ~int64_t(3), kc1 = (ck1 + 3) & ~int64_t(3);
@@ -489,11 +501,12 @@ __global__ void __launch_bounds__(kSpmvThreads, 1) k_spmv_tma(SpmvArgs A, Op op_
                     wbytes += (uint32_t)(hi - lo) * 8;
                 }
                 unsigned char* st = stage0 + (size_t)s * A.stage_bytes;
-                const uint32_t ob = (uint32_t)((A.R + 2) * 8);
+                // R+2 offsets (R+4 for int32: 16-B multiple; off32 is padded)
+                const uint32_t ob = sizeof(OffT) == 8 ? (uint32_t)((A.R + 2) * 8) : (uint32_t)((A.R + 4) * 4);
                 const uint32_t vb = (uint32_t)((kv1 - kv0) * 8);
                 const uint32_t cb = (uint32_t)((kc1 - kc0) * 4);
                 mbar_arrive_expect_tx(&full[s], ob + vb + cb + wbytes * nsrc);
-                bulk_g2s(st, A.off + r0, ob, &full[s], pol_stream);
+                bulk_g2s(st, OFF + r0, ob, &full[s], pol_stream);
                 if (vb) bulk_g2s(st + A.off_bytes, A.vals + kv0, vb, &full[s], pol_stream);
                 if (cb) bulk_g2s(st + A.off_bytes + A.val_bytes, A.cols + kc0, cb, &full[s], pol_stream);
                 // leading edge of this CTA's NEXT tile: its highest-diagonal
@@ -541,7 +554,7 @@ __global__ void __launch_bounds__(kSpmvThreads, 1) k_spmv_tma(SpmvArgs A, Op op_
         const int     rows = (int)min((int64_t)A.R, A.n_rows - r0);
         const SpmvStageMeta& m = meta[s];
         if (m.direct) {
-            acc = spmv_rows_direct(op, acc, gtid, gs, rows, r0, A.off + r0, A.cols, A.vals);
+            acc = spmv_rows_direct(op, acc, gtid, gs, rows, r0, OFF + r0, A.cols, A.vals);
         } else {
             unsigned char* st  = stage0 + (size_t)s * A.stage_bytes;
             const int64_t  kv0 = m.kv0;
@@ -560,7 +573,7 @@ __global__ void __launch_bounds__(kSpmvThreads, 1) k_spmv_tma(SpmvArgs A, Op op_
                 W.hi[w]   = m.whi[w];
                 W.base[w] = A.win_base[w];
             }
-            const int64_t* O = reinterpret_cast<const int64_t*>(st);
+            const OffT* O = reinterpret_cast<const OffT*>(st);
             const double*  V = reinterpret_cast<const double*>(st + A.off_bytes);
             if (W.n) acc = spmv_rows_staged<true>(op, acc, gtid, gs, rows, r0, O, kv0, Cc, V, W);
             else acc = spmv_rows_staged<false>(op, acc, gtid, gs, rows, r0, O, kv0, Cc, V, W);
@@ -630,11 +643,14 @@ rvk_status launch_spmv(cudaStream_t stream, const SpmvArgs& a, const Op& op, Tai
 {
     static bool configured = false; // per instantiation; before any graph capture
     if (!configured) {
-        RVK_CUDA(cudaFuncSetAttribute(k_spmv_tma<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        RVK_CUDA(cudaFuncSetAttribute(k_spmv_tma<Op, int64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)(kSpmvHeaderBytes + kSpmvStageBudget)));
+        RVK_CUDA(cudaFuncSetAttribute(k_spmv_tma<Op, int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)(kSpmvHeaderBytes + kSpmvStageBudget)));
         configured = true;
     }
-    k_spmv_tma<Op><<<grid, 32 + a.consumers, a.smem_bytes(), stream>>>(a, op, tail);
+    if (a.off32) k_spmv_tma<Op, int32_t><<<grid, 32 + a.consumers, a.smem_bytes(), stream>>>(a, op, tail);
+    else k_spmv_tma<Op, int64_t><<<grid, 32 + a.consumers, a.smem_bytes(), stream>>>(a, op, tail);
     RVK_CHECK_LAUNCH("k_spmv_tma");
     return RVK_OK;
 }

@@ -44,7 +44,7 @@ EXPORTS = [
     "rvk_cg_plan_vector",
     "rvk_laplacian_rows_nnz", "rvk_build_laplacian_rows", "rvk_comm_unique_id", "rvk_comm_init",
     "rvk_comm_destroy", "rvk_dcg_plan_create", "rvk_dcg_plan_destroy", "rvk_dcg_solve_dev",
-    "rvk_dcg_loopback_solve", "rvk_dcg_result", "rvk_dcg_window", "rvk_dcg_attach_peers",
+    "rvk_dcg_loopback_solve", "rvk_dcg_result", "rvk_dcg_plan_flags", "rvk_dcg_window", "rvk_dcg_attach_peers",
     "rvk_ipc_get_handle", "rvk_ipc_open_handle", "rvk_ipc_close_handle", "rvk_tfqmr_plan_create",
     "rvk_tfqmr_plan_destroy", "rvk_tfqmr_solve_dev", "rvk_tfqmr_result",
 ]
@@ -163,6 +163,7 @@ def lib():
         "rvk_dcg_solve_dev": (i, [vp, vp, vp]),
         "rvk_dcg_loopback_solve": (i, [C.POINTER(vp), i, C.POINTER(vp), C.POINTER(vp)]),
         "rvk_dcg_result": (i, [vp, vp, C.POINTER(CgInfo)]),
+        "rvk_dcg_plan_flags": (i, [vp]),
         "rvk_dcg_window": (i, [vp, C.POINTER(vp), C.POINTER(C.c_size_t)]),
         "rvk_dcg_attach_peers": (i, [vp, C.POINTER(vp), C.POINTER(Shard)]),
         "rvk_ipc_get_handle": (i, [vp, vp, i]),
@@ -428,7 +429,7 @@ class CgPlan:
 
     def flags(self) -> int:
         """RVK_PLAN_* bits: 1 constant diagonal folded to a scalar, 2 matrix-free,
-        4 matrix-free via the TMA 2.5D kernel."""
+        4 matrix-free via the TMA 2.5D kernel, 8 int32 row offsets streamed."""
         return lib().rvk_cg_plan_flags(self.h)
 
     VEC = {"r": 0, "z": 1, "p0": 2, "p1": 3, "w": 4}
