@@ -257,8 +257,8 @@ def bench_main(args, cfg):
     # gloo bootstrap, PEER only (NCCL refuses two ranks on one device);
     # contexts time-slice, so the timings are meaningless -- the JSON says so
     shared = os.environ.get("RVK_SHARED_GPU") == "1"
-    if shared:
-        local = 0
+    if shared or torch.cuda.device_count() == 1:
+        local = 0  # (a launcher that pins one visible GPU per process)
     torch.cuda.set_device(local)
     if shared:
         dist.init_process_group("gloo")
