@@ -123,6 +123,43 @@ __global__ void __launch_bounds__(kUpdThreads)
 // ---------------------------------------------------------------------------
 // K2: x += a p; r += (-a) w; z = B r; partials z.z, z.r; tail dp/hist/beta.
 // ---------------------------------------------------------------------------
+// Shared K2 tail: block sums -> last block -> dp into hist, convergence,
+// beta = z.r, the WHILE condition.  Call from all threads of the block.
+template <bool COND>
+__device__ __forceinline__ void cg_update_tail(double (&acc)[2], double* smem, int* flag, CgState* st,
+                                               double* hist, int it, double rtol, double atol,
+                                               double* partials, unsigned int* ticket, int max_it,
+                                               cudaGraphConditionalHandle cond, int use_cond)
+{
+    const int tid = threadIdx.x;
+    block_sum<2>(acc, smem, tid, blockDim.x, 1);
+    if (tid == 0) {
+        partials[2 * blockIdx.x]     = acc[0];
+        partials[2 * blockIdx.x + 1] = acc[1];
+    }
+    if (!last_block(ticket, tid, flag, blockDim.x, 1)) return;
+    fold_partials<2>(partials, gridDim.x, acc, smem, tid, blockDim.x, 1);
+    if (tid == 0) {
+        const double dp = sqrt(acc[0]);
+        hist[it + 1]    = dp;
+        st->dp          = dp;
+        st->iterations  = it + 1;
+        bool more = it + 1 < max_it;
+        if (cg_converged(dp, st->dp0, rtol, atol)) {
+            st->state = RVK_CG_CONVERGED;
+            st->done  = 1;
+            more      = false;
+        } else {
+            st->beta = acc[1];
+            if (!more) st->done = 1; // ran max_it: later kernels of a WHILE body no-op
+        }
+        if constexpr (COND) {
+            if (use_cond) cudaGraphSetConditional(cond, more ? 1u : 0u);
+        }
+        *ticket = 0u;
+    }
+}
+
 // COND: this instantiation may set the WHILE node's condition.  Kept a
 // template parameter so the plain-graph/stream variant contains no
 // cudaGraphSetConditional (ncu refuses to profile kernels that can set one).
@@ -207,32 +244,116 @@ __global__ void __launch_bounds__(kUpdThreads)
         acc[0]          = add(acc[0], mul(zi, zi));
         acc[1]          = add(acc[1], mul(zi, ri));
     }
-    const int tid = threadIdx.x;
-    block_sum<2>(acc, smem, tid, blockDim.x, 1);
-    if (tid == 0) {
-        partials[2 * blockIdx.x]     = acc[0];
-        partials[2 * blockIdx.x + 1] = acc[1];
-    }
-    if (!last_block(ticket, tid, &flag, blockDim.x, 1)) return;
-    fold_partials<2>(partials, gridDim.x, acc, smem, tid, blockDim.x, 1);
-    if (tid == 0) {
-        const double dp = sqrt(acc[0]);
-        hist[it + 1]    = dp;
-        st->dp          = dp;
-        st->iterations  = it + 1;
-        bool more = it + 1 < max_it;
-        if (cg_converged(dp, st->dp0, rtol, atol)) {
-            st->state = RVK_CG_CONVERGED;
-            st->done  = 1;
-            more      = false;
-        } else {
-            st->beta = acc[1];
-            if (!more) st->done = 1; // ran max_it: later kernels of a WHILE body no-op
-        }
+    cg_update_tail<COND>(acc, smem, &flag, st, hist, it, rtol, atol, partials, ticket, max_it, cond,
+                         use_cond);
+}
+
+// K2, streaming variant (RVK_K2_TMA=1 opt-in / A-B): one CTA per SM; the
+// 4-5 input streams (p, w, x, r[, dinv]) of each 1024-element tile arrive by
+// cp.async.bulk into a kK2Stages-deep shared-memory ring (mbarrier per
+// stage) and the outputs leave by coalesced 16-B stores.  Same element
+// arithmetic as k_cg_update (bit-identical x, r, z); the z.z / z.r partial
+// order differs (another fixed partition).  Full tiles only; the n %% 1024
+// remainder is a grid-stride tail.  All pointers 16-B aligned (VEC).
+constexpr int kK2Tile    = 1024;
+constexpr int kK2Stages  = 4;
+constexpr int kK2Threads = 256;
+template <int PC>
+constexpr size_t k2_smem_bytes()
+{
+    return sizeof(double) * (size_t)kK2Stages * (PC == 1 ? 5 : 4) * kK2Tile;
+}
+
+template <int PC, bool COND = false>
+__global__ void __launch_bounds__(kK2Threads, 1)
+    k_cg_update_tma(int64_t n, const double* __restrict__ p, const double* __restrict__ w,
+                    const double* __restrict__ dinv, double* __restrict__ x, double* __restrict__ r,
+                    double* __restrict__ z, CgState* st, double* hist, int it, double rtol,
+                    double atol, double* partials, unsigned int* ticket, double dconst, int max_it,
+                    cudaGraphConditionalHandle cond, int use_cond)
+{
+    if (st->done) {
         if constexpr (COND)
-            if (use_cond) cudaGraphSetConditional(cond, more ? 1u : 0u);
-        *ticket = 0u;
+            if (use_cond && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(cond, 0);
+        return;
     }
+    if (it < 0) it = st->iterations;
+    constexpr int NS = PC == 1 ? 5 : 4; // p, w, x, r, (dinv)
+    extern __shared__ __align__(128) unsigned char k2_smem[];
+    double*                          buf = reinterpret_cast<double*>(k2_smem);
+    __shared__ __align__(8) uint64_t full[kK2Stages];
+    __shared__ double                smem[64];
+    __shared__ int                   flag;
+    const double  a = st->alpha, na = -a;
+    const int     tid    = threadIdx.x;
+    const int64_t ntiles = n / kK2Tile;
+    const int64_t my     = ntiles > (int64_t)blockIdx.x
+                               ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    if (tid == 0) {
+        for (int k = 0; k < kK2Stages; ++k) mbar_init(&full[k], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const uint64_t pol = policy_evict_first();
+#define RVK_K2_ISSUE(J)                                                                            \
+    do {                                                                                           \
+        const int     k_  = (int)((J) % kK2Stages);                                                \
+        const int64_t e0_ = ((int64_t)blockIdx.x + (J) * (int64_t)gridDim.x) * kK2Tile;            \
+        double*       sb_ = buf + (size_t)k_ * NS * kK2Tile;                                       \
+        mbar_arrive_expect_tx(&full[k_], NS * kK2Tile * 8);                                        \
+        bulk_g2s(sb_, p + e0_, kK2Tile * 8, &full[k_], pol);                                       \
+        bulk_g2s(sb_ + kK2Tile, w + e0_, kK2Tile * 8, &full[k_], pol);                             \
+        bulk_g2s(sb_ + 2 * kK2Tile, x + e0_, kK2Tile * 8, &full[k_], pol);                         \
+        bulk_g2s(sb_ + 3 * kK2Tile, r + e0_, kK2Tile * 8, &full[k_], pol);                         \
+        if (PC == 1) bulk_g2s(sb_ + 4 * kK2Tile, dinv + e0_, kK2Tile * 8, &full[k_], pol);         \
+    } while (0)
+    if (tid == 0)
+        for (int64_t j = 0; j < my && j < kK2Stages; ++j) RVK_K2_ISSUE(j);
+    double acc[2] = {0.0, 0.0};
+    for (int64_t j = 0; j < my; ++j) {
+        const int k = (int)(j % kK2Stages);
+        mbar_wait(&full[k], (uint32_t)((j / kK2Stages) & 1));
+        const double2* sb = reinterpret_cast<const double2*>(buf + (size_t)k * NS * kK2Tile);
+        const int64_t  h0 = ((int64_t)blockIdx.x + j * (int64_t)gridDim.x) * (kK2Tile / 2);
+#pragma unroll
+        for (int q = tid; q < kK2Tile / 2; q += kK2Threads) {
+            const double2 pi = sb[q], wi = sb[kK2Tile / 2 + q];
+            double2       xi = sb[kK2Tile + q], ri = sb[3 * (kK2Tile / 2) + q];
+            double2       d  = make_double2(dconst, dconst);
+            if (PC == 1) d = sb[2 * kK2Tile + q];
+            xi.x = axpy1(a, pi.x, xi.x);
+            xi.y = axpy1(a, pi.y, xi.y);
+            ri.x = axpy1(na, wi.x, ri.x);
+            ri.y = axpy1(na, wi.y, ri.y);
+            double2 zi = ri;
+            if (PC != 0) {
+                zi.x = mul(d.x, ri.x);
+                zi.y = mul(d.y, ri.y);
+            }
+            st_stream(reinterpret_cast<double2*>(x) + h0 + q, xi);
+            reinterpret_cast<double2*>(r)[h0 + q] = ri;
+            reinterpret_cast<double2*>(z)[h0 + q] = zi;
+            acc[0] = add(acc[0], mul(zi.x, zi.x));
+            acc[0] = add(acc[0], mul(zi.y, zi.y));
+            acc[1] = add(acc[1], mul(zi.x, ri.x));
+            acc[1] = add(acc[1], mul(zi.y, ri.y));
+        }
+        __syncthreads(); // stage k consumed by every thread
+        if (tid == 0 && j + kK2Stages < my) RVK_K2_ISSUE(j + kK2Stages);
+    }
+#undef RVK_K2_ISSUE
+    for (int64_t i = ntiles * kK2Tile + (int64_t)blockIdx.x * blockDim.x + tid; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        x[i]            = axpy1(a, p[i], x[i]);
+        const double ri = axpy1(na, w[i], r[i]);
+        const double zi = PC == 0 ? ri : mul(PC == 1 ? dinv[i] : dconst, ri);
+        r[i]            = ri;
+        z[i]            = zi;
+        acc[0]          = add(acc[0], mul(zi, zi));
+        acc[1]          = add(acc[1], mul(zi, ri));
+    }
+    cg_update_tail<COND>(acc, smem, &flag, st, hist, it, rtol, atol, partials, ticket, max_it, cond,
+                         use_cond);
 }
 
 // ---------------------------------------------------------------------------
@@ -519,6 +640,7 @@ struct rvk_cg_plan_s {
     double        dconst = 0.0;             // constant dinv (stencil, or a detected constant diagonal)
     bool          const_diag = false;       // CSR plan: every dinv[i] bit-identical -> scalar
     int32_t*      off32      = nullptr;     // int32 row offsets for the SpMV stream (nnz < 2^31)
+    bool          k2_tma     = false;       // K2 = k_cg_update_tma (RVK_K2_TMA=1)
     int           mf_grid = 0;
     MfTma*        mf_tma  = nullptr;         // TMA 2.5D matrix-free kernel state (or null)
     double*       dinv = nullptr;
@@ -590,6 +712,25 @@ rvk_status launch_update(rvk_cg_plan P, int pcm, const double* p_new, double* x,
                                                  P->partials, P->tickets, P->dconst,
                                                  P->cfg.max_it, cond, use_cond);
     };
+    if (V && P->k2_tma) {
+        auto gt = [&](auto kern, size_t smem) {
+            kern<<<sm_count(), kK2Threads, smem, s>>>(P->A.n_rows, p_new, P->w, P->dinv, x, P->r, P->z,
+                                                      P->st, P->hist, it, P->cfg.rtol, P->cfg.atol,
+                                                      P->partials, P->tickets, P->dconst,
+                                                      P->cfg.max_it, cond, use_cond);
+        };
+        if (use_cond) {
+            if (pcm == 0) gt(k_cg_update_tma<0, true>, k2_smem_bytes<0>());
+            else if (pcm == 1) gt(k_cg_update_tma<1, true>, k2_smem_bytes<1>());
+            else gt(k_cg_update_tma<2, true>, k2_smem_bytes<2>());
+        } else {
+            if (pcm == 0) gt(k_cg_update_tma<0>, k2_smem_bytes<0>());
+            else if (pcm == 1) gt(k_cg_update_tma<1>, k2_smem_bytes<1>());
+            else gt(k_cg_update_tma<2>, k2_smem_bytes<2>());
+        }
+        RVK_CHECK_LAUNCH("k_cg_update_tma");
+        return RVK_OK;
+    }
     if (use_cond) {
         if (pcm == 0) go(k_cg_update<V, 0, true>);
         else if (pcm == 1) go(k_cg_update<V, 1, true>);
@@ -897,6 +1038,25 @@ rvk_status enqueue_solve(rvk_cg_plan P, const double* b, double* x)
     }
 }
 
+// K2 streaming variant: opt-in (RVK_K2_TMA=1); the ring needs > 48 KB of
+// dynamic shared memory, configured here, before any capture.
+rvk_status k2_tma_setup(rvk_cg_plan P)
+{
+    const char* e = std::getenv("RVK_K2_TMA");
+    if (!(e && e[0] == '1')) return RVK_OK;
+    auto cfg = [](auto kern, size_t smem) {
+        return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    };
+    RVK_CUDA(cfg(k_cg_update_tma<0>, k2_smem_bytes<0>()));
+    RVK_CUDA(cfg(k_cg_update_tma<1>, k2_smem_bytes<1>()));
+    RVK_CUDA(cfg(k_cg_update_tma<2>, k2_smem_bytes<2>()));
+    RVK_CUDA(cfg(k_cg_update_tma<0, true>, k2_smem_bytes<0>()));
+    RVK_CUDA(cfg(k_cg_update_tma<1, true>, k2_smem_bytes<1>()));
+    RVK_CUDA(cfg(k_cg_update_tma<2, true>, k2_smem_bytes<2>()));
+    P->k2_tma = true;
+    return RVK_OK;
+}
+
 rvk_status destroy_graph(rvk_cg_plan P)
 {
     for (auto& g : P->gs) {
@@ -1073,6 +1233,7 @@ rvk_status rvk_cg_plan_create(rvk_ctx ctx, const rvk_csr* A, rvk_cg_config cfg, 
     // (opt-in RVK_OFF32=1, see make_off32)
     if (rc == RVK_OK) rc = make_off32(s, *A, &P->off32);
     if (rc == RVK_OK) P->sa.off32 = P->off32;
+    if (rc == RVK_OK) rc = k2_tma_setup(P);
     // Constant-coefficient operators with Dirichlet truncation have ONE
     // diagonal value, so dinv is a constant vector: the fused K0/K2 then
     // multiply by the scalar (bit-identical z = dinv[i] * r[i]) and skip the
