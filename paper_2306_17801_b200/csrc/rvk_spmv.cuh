@@ -50,7 +50,7 @@ constexpr int    kSpmvConsumerWarps = 16;
 constexpr int    kSpmvConsumers     = kSpmvConsumerWarps * 32;
 constexpr int    kSpmvThreads       = kSpmvConsumers + 32; // + producer warp
 constexpr int    kSpmvMaxStages     = 4;
-constexpr int    kSpmvUnroll        = 8;                   // nonzeros per lane per batch
+constexpr int    kSpmvUnroll        = 8;                   // default nonzeros per lane per batch
 constexpr int    kSpmvMaxWin        = 4;                   // x-windows per tile
 constexpr int    kSpmvMaxSrc        = 2;                   // gathered vectors per column
 constexpr size_t kSpmvHeaderBytes   = 2048;                // barriers, meta, reduction scratch
@@ -90,6 +90,7 @@ struct SpmvArgs {
     int            stages;   // ring depth (<= kSpmvMaxStages)
     int            groups;   // consumer groups working on distinct stages (divides stages)
     int            consumers; // consumer threads (multiple of 32, <= kSpmvConsumers)
+    int            unroll;    // nonzeros per lane per gather batch: 7, 8 or 9 (spmv_unroll)
     int            cap;      // nonzeros per stage
     int            off_bytes, val_bytes, col_bytes, stage_bytes; // [off | vals | cols | windows]
     int            nwin;                  // 0: no x-windows
@@ -204,6 +205,15 @@ inline SpmvArgs make_spmv_args(const rvk_csr& A, int64_t max_row_len,
     };
     a.consumers = kSpmvConsumers;
     set_groups();
+    // gather batch size: one batch per 7- / 9-point row (and 3 per 27-point
+    // row) instead of batches of 8 with masked-off slots (RVK_SPMV_UNROLL=8
+    // restores the fixed batch)
+    const char* un = std::getenv("RVK_SPMV_UNROLL");
+    a.unroll = 8;
+    if (!(un && un[0] == '8')) {
+        if (max_row_len <= 7) a.unroll = 7;
+        else if (max_row_len == 9 || max_row_len % 9 == 0) a.unroll = 9;
+    }
     // Long rows (short tiles): every ring stage is consumed at once, so the
     // producer has no stage to fill ahead.  Opt-in (RVK_SPMV_SLACK=1): halve
     // the consumer warps so half the ring is always in flight.  Measured
@@ -282,7 +292,7 @@ __device__ __forceinline__ auto spmv_own(const Op& op, int64_t i, const G& gathe
 // ---------------------------------------------------------------------------
 // Direct tiles: thread-per-row straight from global memory (rare path).
 // ---------------------------------------------------------------------------
-template <class Op, class Acc, class OffT>
+template <int U, class Op, class Acc, class OffT>
 __device__ __forceinline__ Acc spmv_rows_direct(const Op& op, Acc acc, int gtid, int gsize,
                                                    int rows, int64_t r0,
                                                    const OffT* __restrict__ O,
@@ -293,22 +303,22 @@ __device__ __forceinline__ Acc spmv_rows_direct(const Op& op, Acc acc, int gtid,
         const auto    own = spmv_own(op, r0 + lr, [&](int64_t c) { return op.fetch((int32_t)c); });
         const int64_t kb = (int64_t)O[lr], ke = (int64_t)O[lr + 1];
         double        sum = 0.0;
-        for (int64_t k = kb; k < ke; k += kSpmvUnroll) {
-            int32_t c[kSpmvUnroll];
-            double  v[kSpmvUnroll];
-            bool    ok[kSpmvUnroll];
+        for (int64_t k = kb; k < ke; k += U) {
+            int32_t c[U];
+            double  v[U];
+            bool    ok[U];
 #pragma unroll
-            for (int u = 0; u < kSpmvUnroll; ++u) {
+            for (int u = 0; u < U; ++u) {
                 ok[u]            = k + u < ke;
                 const int64_t ks = ok[u] ? k + u : ke - 1;
                 c[u]             = __ldg(Cc + ks);
                 v[u]             = __ldg(V + ks);
             }
-            typename Op::Fetch f[kSpmvUnroll];
+            typename Op::Fetch f[U];
 #pragma unroll
-            for (int u = 0; u < kSpmvUnroll; ++u) f[u] = op.fetch(c[u]);
+            for (int u = 0; u < U; ++u) f[u] = op.fetch(c[u]);
 #pragma unroll
-            for (int u = 0; u < kSpmvUnroll; ++u) {
+            for (int u = 0; u < U; ++u) {
                 const double t = add(sum, mul(v[u], op.value(f[u])));
                 sum            = ok[u] ? t : sum;
             }
@@ -349,7 +359,7 @@ __device__ __forceinline__ int window_index(const StageWindows& W, int64_t c)
 // Stage-local 32-bit indices keep the address arithmetic cheap.  WIN: the
 // gathers read the stage's x-windows (LDS) instead of global memory.
 // ---------------------------------------------------------------------------
-template <bool WIN, class Op, class Acc, class OffT>
+template <bool WIN, int U, class Op, class Acc, class OffT>
 __device__ __forceinline__ Acc spmv_rows_staged(const Op& op, Acc acc, int gtid, int gsize,
                                                    int rows, int64_t r0, const OffT* O,
                                                    int64_t kv0, const int32_t* Cc,
@@ -364,22 +374,22 @@ __device__ __forceinline__ Acc spmv_rows_staged(const Op& op, Acc acc, int gtid,
         const int  kb  = (int)((int64_t)O[lr] - kv0);
         const int  ke  = (int)((int64_t)O[lr + 1] - kv0);
         double     sum = 0.0;
-        for (int k = kb; k < ke; k += kSpmvUnroll) {
-            int32_t c[kSpmvUnroll];
-            double  v[kSpmvUnroll];
-            bool    ok[kSpmvUnroll];
+        for (int k = kb; k < ke; k += U) {
+            int32_t c[U];
+            double  v[U];
+            bool    ok[U];
 #pragma unroll
-            for (int u = 0; u < kSpmvUnroll; ++u) {
+            for (int u = 0; u < U; ++u) {
                 ok[u]        = k + u < ke;
                 const int ks = ok[u] ? k + u : k; // k < ke: a valid entry
                 c[u]         = Cc[ks];
                 v[u]         = V[ks];
             }
-            typename Op::Fetch f[kSpmvUnroll];
+            typename Op::Fetch f[U];
 #pragma unroll
-            for (int u = 0; u < kSpmvUnroll; ++u) f[u] = gather(c[u]);
+            for (int u = 0; u < U; ++u) f[u] = gather(c[u]);
 #pragma unroll
-            for (int u = 0; u < kSpmvUnroll; ++u) {
+            for (int u = 0; u < U; ++u) {
                 const double t = add(sum, mul(v[u], op.value(f[u])));
                 sum            = ok[u] ? t : sum;
             }
@@ -421,7 +431,8 @@ __device__ __forceinline__ const OffT* spmv_offsets(const SpmvArgs& A)
 }
 
 // OffT: int64_t (the matrix's own offsets) or int32_t (SpmvArgs::off32).
-template <class Op, class OffT = int64_t>
+// U: nonzeros per lane per gather batch (SpmvArgs::unroll).
+template <class Op, class OffT = int64_t, int U = kSpmvUnroll>
 __global__ void __launch_bounds__(kSpmvThreads, 1) k_spmv_tma(SpmvArgs A, Op op_in, TailArgs tail)
 {
     const OffT* __restrict__ OFF = spmv_offsets<OffT>(A);
@@ -554,7 +565,7 @@ __global__ void __launch_bounds__(kSpmvThreads, 1) k_spmv_tma(SpmvArgs A, Op op_
         const int     rows = (int)min((int64_t)A.R, A.n_rows - r0);
         const SpmvStageMeta& m = meta[s];
         if (m.direct) {
-            acc = spmv_rows_direct(op, acc, gtid, gs, rows, r0, OFF + r0, A.cols, A.vals);
+            acc = spmv_rows_direct<U>(op, acc, gtid, gs, rows, r0, OFF + r0, A.cols, A.vals);
         } else {
             unsigned char* st  = stage0 + (size_t)s * A.stage_bytes;
             const int64_t  kv0 = m.kv0;
@@ -575,8 +586,8 @@ __global__ void __launch_bounds__(kSpmvThreads, 1) k_spmv_tma(SpmvArgs A, Op op_
             }
             const OffT* O = reinterpret_cast<const OffT*>(st);
             const double*  V = reinterpret_cast<const double*>(st + A.off_bytes);
-            if (W.n) acc = spmv_rows_staged<true>(op, acc, gtid, gs, rows, r0, O, kv0, Cc, V, W);
-            else acc = spmv_rows_staged<false>(op, acc, gtid, gs, rows, r0, O, kv0, Cc, V, W);
+            if (W.n) acc = spmv_rows_staged<true, U>(op, acc, gtid, gs, rows, r0, O, kv0, Cc, V, W);
+            else acc = spmv_rows_staged<false, U>(op, acc, gtid, gs, rows, r0, O, kv0, Cc, V, W);
         }
         __syncwarp();
         if ((ctid & 31) == 0) mbar_arrive(&empty[s]);
@@ -642,15 +653,20 @@ rvk_status launch_spmv(cudaStream_t stream, const SpmvArgs& a, const Op& op, Tai
                        int grid)
 {
     static bool configured = false; // per instantiation; before any graph capture
+    const int   smax       = (int)(kSpmvHeaderBytes + kSpmvStageBudget);
     if (!configured) {
-        RVK_CUDA(cudaFuncSetAttribute(k_spmv_tma<Op, int64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)(kSpmvHeaderBytes + kSpmvStageBudget)));
-        RVK_CUDA(cudaFuncSetAttribute(k_spmv_tma<Op, int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)(kSpmvHeaderBytes + kSpmvStageBudget)));
+        RVK_CUDA(cudaFuncSetAttribute(k_spmv_tma<Op, int64_t, 7>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax));
+        RVK_CUDA(cudaFuncSetAttribute(k_spmv_tma<Op, int64_t, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax));
+        RVK_CUDA(cudaFuncSetAttribute(k_spmv_tma<Op, int64_t, 9>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax));
+        RVK_CUDA(cudaFuncSetAttribute(k_spmv_tma<Op, int32_t, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax));
         configured = true;
     }
-    if (a.off32) k_spmv_tma<Op, int32_t><<<grid, 32 + a.consumers, a.smem_bytes(), stream>>>(a, op, tail);
-    else k_spmv_tma<Op, int64_t><<<grid, 32 + a.consumers, a.smem_bytes(), stream>>>(a, op, tail);
+    const int th = 32 + a.consumers;
+    const size_t sm = a.smem_bytes();
+    if (a.off32) k_spmv_tma<Op, int32_t, 8><<<grid, th, sm, stream>>>(a, op, tail);
+    else if (a.unroll == 7) k_spmv_tma<Op, int64_t, 7><<<grid, th, sm, stream>>>(a, op, tail);
+    else if (a.unroll == 9) k_spmv_tma<Op, int64_t, 9><<<grid, th, sm, stream>>>(a, op, tail);
+    else k_spmv_tma<Op, int64_t, 8><<<grid, th, sm, stream>>>(a, op, tail);
     RVK_CHECK_LAUNCH("k_spmv_tma");
     return RVK_OK;
 }
