@@ -15,7 +15,8 @@ from dataclasses import dataclass
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "librvk.so")
+# RVK_LIB_PATH: an alternative in-tree build for A/B experiments (same ABI)
+LIB_PATH = os.environ.get("RVK_LIB_PATH") or os.path.join(HERE, "lib", "librvk.so")
 
 RVK_OK = 0
 RVK_ERR_BREAKDOWN = 5
