@@ -74,6 +74,11 @@ void     rvk_host_sync_reset(void);
 /* ---- device memory (plumbing) -------------------------------------------- */
 rvk_status rvk_malloc(void** dev, size_t bytes);
 rvk_status rvk_free(void* dev);
+/* stream-ordered (cudaMallocAsync pool): valid for work enqueued on ctx after
+ * the call; freed after the work enqueued before rvk_free_async -- the
+ * deferred release of managed_state.hpp:13-15 / dual_buffer.cpp:9-17 */
+rvk_status rvk_malloc_async(rvk_ctx ctx, void** dev, size_t bytes);
+rvk_status rvk_free_async(rvk_ctx ctx, void* dev);
 rvk_status rvk_host_alloc(void** host, size_t bytes);    /* pinned */
 rvk_status rvk_host_free(void* host);
 rvk_status rvk_memcpy_h2d(rvk_ctx ctx, void* dst_dev, const void* src_host, size_t bytes);

@@ -166,6 +166,27 @@ rvk_status rvk_free(void* dev)
     return RVK_OK;
 }
 
+// Stream-ordered allocation: the allocation is usable by work enqueued on ctx
+// after this call; the release happens once the work enqueued before
+// rvk_free_async has run -- the reference's "resource lifetime extends past
+// handle destruction until the stream is idle" (managed_state.hpp:13-15)
+// without a host wait.
+rvk_status rvk_malloc_async(rvk_ctx ctx, void** dev, size_t bytes)
+{
+    if (!ctx || !dev) return set_error(RVK_ERR_INVALID, "null argument");
+    *dev = nullptr;
+    if (bytes == 0) return RVK_OK;
+    RVK_CUDA(cudaMallocAsync(dev, bytes, ctx->stream));
+    return RVK_OK;
+}
+
+rvk_status rvk_free_async(rvk_ctx ctx, void* dev)
+{
+    if (!ctx) return set_error(RVK_ERR_INVALID, "null context");
+    if (dev) RVK_CUDA(cudaFreeAsync(dev, ctx->stream));
+    return RVK_OK;
+}
+
 rvk_status rvk_host_alloc(void** host, size_t bytes)
 {
     if (!host) return set_error(RVK_ERR_INVALID, "null out");

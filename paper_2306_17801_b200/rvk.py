@@ -33,7 +33,7 @@ EXPORTS = [
     "rvk_last_error", "rvk_abi_version", "rvk_device_info",
     "rvk_ctx_create", "rvk_ctx_destroy", "rvk_ctx_stream", "rvk_ctx_synchronize",
     "rvk_ctx_query_idle", "rvk_ctx_wait_for", "rvk_host_sync_count", "rvk_host_sync_reset",
-    "rvk_malloc", "rvk_free", "rvk_host_alloc", "rvk_host_free", "rvk_memcpy_h2d",
+    "rvk_malloc", "rvk_free", "rvk_malloc_async", "rvk_free_async", "rvk_host_alloc", "rvk_host_free", "rvk_memcpy_h2d",
     "rvk_memcpy_d2h", "rvk_memcpy_d2d", "rvk_scalar_eval", "rvk_scalar_read",
     "rvk_dot", "rvk_nrm2", "rvk_dot2", "rvk_axpy", "rvk_aypx", "rvk_waxpy", "rvk_scale",
     "rvk_pointwise_mult", "rvk_copy", "rvk_set", "rvk_csr_spmv", "rvk_csr_diagonal",
@@ -115,6 +115,8 @@ def lib():
         "rvk_host_sync_reset": (None, []),
         "rvk_malloc": (i, [C.POINTER(vp), C.c_size_t]),
         "rvk_free": (i, [vp]),
+        "rvk_malloc_async": (i, [vp, C.POINTER(vp), C.c_size_t]),
+        "rvk_free_async": (i, [vp, vp]),
         "rvk_host_alloc": (i, [C.POINTER(vp), C.c_size_t]),
         "rvk_host_free": (i, [vp]),
         "rvk_memcpy_h2d": (i, [vp, vp, vp, C.c_size_t]),

@@ -623,3 +623,19 @@ def test_matrix_free_tma_w_bitexact_vs_csr(ctx, spec, monkeypatch):
     monkeypatch.setenv("RVK_MF_TMA", "1")
     x, res = rvk.CgPlan(ctx, (dim, pts, g), max_it=20).solve_host(b)
     check_cg(res, x, O.cg_solve(Ah, b, max_it=20))
+
+
+def test_stream_ordered_alloc_deferred_release(ctx):
+    """rvk_malloc_async / rvk_free_async (managed_state.hpp:13-15: storage
+    outlives the handle until the stream is done with it): a buffer freed
+    right after enqueueing work that reads it still feeds that work."""
+    import ctypes as C
+    L = rvk.lib()
+    n = 1 << 20
+    p = C.c_void_p()
+    rvk.check(L.rvk_malloc_async(ctx.h, C.byref(p), 8 * n))
+    rvk.check(L.rvk_set(ctx.h, n, 3.0, p))
+    out = rvk.DeviceArray(1)
+    rvk.check(L.rvk_nrm2(ctx.h, n, p, out.ptr))
+    rvk.check(L.rvk_free_async(ctx.h, p))  # before the reduction has run
+    assert out.download(ctx)[0] == pytest.approx(3.0 * np.sqrt(n), rel=1e-14)
