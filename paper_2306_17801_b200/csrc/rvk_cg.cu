@@ -107,6 +107,7 @@ __global__ void __launch_bounds__(kUpdThreads)
         st->dp0            = dp0;
         st->dp             = dp0;
         st->beta           = acc[1];
+        st->x_pending      = 0;
         st->betaold        = 0.0;
         st->alpha          = 0.0;
         st->pAp            = 0.0;
@@ -163,14 +164,21 @@ __device__ __forceinline__ void cg_update_tail(double (&acc)[2], double* smem, i
 // COND: this instantiation may set the WHILE node's condition.  Kept a
 // template parameter so the plain-graph/stream variant contains no
 // cudaGraphSetConditional (ncu refuses to profile kernels that can set one).
-template <bool VEC, int PC, bool COND = false> // PC: 0 none, 1 dinv vector, 2 constant dinv
+// XM (x update): 0 x += a p; 1 DEFER (even iteration: x untouched, (a, it)
+// recorded as pending); 2 FLUSH2 (odd iteration: x = (x + a' p_prev) + a p
+// with the pending a' -- the same two roundings, in the same order, as two
+// single updates, so x is bit-identical while one x read + write and one p
+// read per iteration pair disappear).  k_cg_xfix applies a pending update
+// left by an early exit.
+template <bool VEC, int PC, bool COND = false, int XM = 0> // PC: 0 none, 1 dinv vector, 2 constant dinv
 __global__ void __launch_bounds__(kUpdThreads)
     k_cg_update(int64_t n, const double* __restrict__ p, const double* __restrict__ w,
                 const double* __restrict__ dinv, double* __restrict__ x, double* __restrict__ r,
                 double* __restrict__ z, CgState* st, double* hist, int it, double rtol,
                 double atol, double* partials, unsigned int* ticket, double dconst, int max_it,
-                cudaGraphConditionalHandle cond, int use_cond)
+                cudaGraphConditionalHandle cond, int use_cond, const double* __restrict__ p_prev)
 {
+    static_assert(VEC || XM == 0, "deferred x updates use the vector path");
     // In the device WHILE loop (use_cond) `it` comes from the device state and
     // this kernel decides whether the loop body runs again.
     if (st->done) {
@@ -183,22 +191,42 @@ __global__ void __launch_bounds__(kUpdThreads)
     __shared__ int    flag;
     const double      a      = st->alpha;
     const double      na     = -a;
+    const double      ap     = XM == 2 ? st->pend_alpha : 0.0; // pending a of iteration it-1
     double            acc[2] = {0.0, 0.0};
     const int64_t     stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t     t0     = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        // every block has read pend_alpha / alpha before any of them can be
+        // re-written: the next writer is a later kernel
+        if (XM == 1) {
+            st->pend_alpha = a;
+            st->pend_it    = it;
+            st->x_pending  = 1;
+        } else if (XM == 2) {
+            st->x_pending = 0;
+        }
+    }
     if (VEC) {
-        // two double2 per thread per trip: 10 independent 16-B loads in flight
+        // two double2 per thread per trip: up to 12 independent 16-B loads in flight
         const int64_t  n2 = n >> 1;
         const double2* p2 = reinterpret_cast<const double2*>(p);
+        const double2* q2 = reinterpret_cast<const double2*>(p_prev);
         const double2* w2 = reinterpret_cast<const double2*>(w);
         const double2* d2 = reinterpret_cast<const double2*>(dinv);
         double2*       x2 = reinterpret_cast<double2*>(x);
         double2*       r2 = reinterpret_cast<double2*>(r);
         double2*       z2 = reinterpret_cast<double2*>(z);
-        auto step = [&](const double2& pi, const double2& wi, double2 xi, double2 ri,
-                        const double2& d, int64_t i) {
-            xi.x = axpy1(a, pi.x, xi.x);
-            xi.y = axpy1(a, pi.y, xi.y);
+        auto step = [&](const double2& pi, const double2& qi, const double2& wi, double2 xi,
+                        double2 ri, const double2& d, int64_t i) {
+            if (XM == 2) {
+                xi.x = axpy1(ap, qi.x, xi.x);
+                xi.y = axpy1(ap, qi.y, xi.y);
+            }
+            if (XM != 1) {
+                xi.x = axpy1(a, pi.x, xi.x);
+                xi.y = axpy1(a, pi.y, xi.y);
+                st_stream(x2 + i, xi);
+            }
             ri.x = axpy1(na, wi.x, ri.x);
             ri.y = axpy1(na, wi.y, ri.y);
             double2 zi = ri;
@@ -206,7 +234,6 @@ __global__ void __launch_bounds__(kUpdThreads)
                 zi.x = mul(d.x, ri.x);
                 zi.y = mul(d.y, ri.y);
             }
-            st_stream(x2 + i, xi);
             r2[i] = ri;
             z2[i] = zi;
             acc[0] = add(acc[0], mul(zi.x, zi.x));
@@ -214,29 +241,35 @@ __global__ void __launch_bounds__(kUpdThreads)
             acc[1] = add(acc[1], mul(zi.x, ri.x));
             acc[1] = add(acc[1], mul(zi.y, ri.y));
         };
+        const double2 zero = make_double2(0.0, 0.0);
+        auto ldp = [&](int64_t i) { return XM != 1 ? ld_stream(p2 + i) : zero; };
+        auto ldq = [&](int64_t i) { return XM == 2 ? ld_stream(q2 + i) : zero; };
+        auto ldx = [&](int64_t i) { return XM != 1 ? ld_stream(x2 + i) : zero; };
         int64_t i = t0;
         for (; i + stride < n2; i += 2 * stride) {
             const int64_t j  = i + stride;
-            const double2 pa = ld_stream(p2 + i), pb = ld_stream(p2 + j);
+            const double2 pa = ldp(i), pb = ldp(j);
+            const double2 qa = ldq(i), qb = ldq(j);
             const double2 wa = ld_stream(w2 + i), wb = ld_stream(w2 + j);
-            const double2 xa = ld_stream(x2 + i), xb = ld_stream(x2 + j);
+            const double2 xa = ldx(i), xb = ldx(j);
             const double2 ra = ld_stream(r2 + i), rb = ld_stream(r2 + j);
             double2 da = make_double2(dconst, dconst), db = da;
             if (PC == 1) {
                 da = ld_stream(d2 + i);
                 db = ld_stream(d2 + j);
             }
-            step(pa, wa, xa, ra, da, i);
-            step(pb, wb, xb, rb, db, j);
+            step(pa, qa, wa, xa, ra, da, i);
+            step(pb, qb, wb, xb, rb, db, j);
         }
         if (i < n2) {
             double2 d = make_double2(dconst, dconst);
             if (PC == 1) d = ld_stream(d2 + i);
-            step(ld_stream(p2 + i), ld_stream(w2 + i), ld_stream(x2 + i), ld_stream(r2 + i), d, i);
+            step(ldp(i), ldq(i), ld_stream(w2 + i), ldx(i), ld_stream(r2 + i), d, i);
         }
     }
     for (int64_t i = (VEC ? (n & ~int64_t(1)) : 0) + t0; i < n; i += stride) {
-        x[i]            = axpy1(a, p[i], x[i]);
+        if (XM == 2) x[i] = axpy1(ap, p_prev[i], x[i]);
+        if (XM != 1) x[i] = axpy1(a, p[i], x[i]);
         const double ri = axpy1(na, w[i], r[i]);
         const double zi = PC == 0 ? ri : mul(PC == 1 ? dinv[i] : dconst, ri);
         r[i]            = ri;
@@ -246,6 +279,21 @@ __global__ void __launch_bounds__(kUpdThreads)
     }
     cg_update_tail<COND>(acc, smem, &flag, st, hist, it, rtol, atol, partials, ticket, max_it, cond,
                          use_cond);
+}
+
+// After the last iteration (or an early exit): apply an update a DEFER K2
+// left pending.  p0/p1: the plan's ping-pong buffers; iteration it wrote
+// p[(it + 1) & 1].  No-op (one flag read per block) when nothing is pending.
+__global__ void __launch_bounds__(kUpdThreads)
+    k_cg_xfix(int64_t n, double* __restrict__ x, const double* __restrict__ p0,
+              const double* __restrict__ p1, const CgState* __restrict__ st)
+{
+    if (!st->x_pending) return;
+    const double  a  = st->pend_alpha;
+    const double* pp = ((st->pend_it + 1) & 1) ? p1 : p0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        x[i] = axpy1(a, pp[i], x[i]);
 }
 
 // K2, streaming variant (RVK_K2_TMA=1 opt-in / A-B): one CTA per SM; the
@@ -701,16 +749,50 @@ rvk_status launch_setup(rvk_cg_plan P, int pcm, const double* b, double* x)
     return RVK_OK;
 }
 
+// xm: x-update mode of k_cg_update (0 plain, 1 defer, 2 flush pair; the
+// deferred modes need the vector path), p_prev: p of the previous iteration.
+template <int PC, bool COND, int XM>
+void launch_update_k(rvk_cg_plan P, const double* p_new, const double* p_prev, double* x, int it,
+                     cudaGraphConditionalHandle cond, int use_cond)
+{
+    k_cg_update<true, PC, COND, XM><<<P->upd_grid, kUpdThreads, 0, P->ctx->stream>>>(
+        P->A.n_rows, p_new, P->w, P->dinv, x, P->r, P->z, P->st, P->hist, it, P->cfg.rtol,
+        P->cfg.atol, P->partials, P->tickets, P->dconst, P->cfg.max_it, cond, use_cond, p_prev);
+}
+
+template <int PC, bool COND>
+void launch_update_xm(rvk_cg_plan P, int xm, const double* p_new, const double* p_prev, double* x,
+                      int it, cudaGraphConditionalHandle cond, int use_cond)
+{
+    if (xm == 1) launch_update_k<PC, COND, 1>(P, p_new, p_prev, x, it, cond, use_cond);
+    else if (xm == 2) launch_update_k<PC, COND, 2>(P, p_new, p_prev, x, it, cond, use_cond);
+    else launch_update_k<PC, COND, 0>(P, p_new, p_prev, x, it, cond, use_cond);
+}
+
 template <bool V>
 rvk_status launch_update(rvk_cg_plan P, int pcm, const double* p_new, double* x, int it,
-                         cudaGraphConditionalHandle cond = 0, int use_cond = 0)
+                         cudaGraphConditionalHandle cond = 0, int use_cond = 0, int xm = 0,
+                         const double* p_prev = nullptr)
 {
     cudaStream_t s = P->ctx->stream;
+    if (V && xm != 0) {
+        if (use_cond) {
+            if (pcm == 0) launch_update_xm<0, true>(P, xm, p_new, p_prev, x, it, cond, use_cond);
+            else if (pcm == 1) launch_update_xm<1, true>(P, xm, p_new, p_prev, x, it, cond, use_cond);
+            else launch_update_xm<2, true>(P, xm, p_new, p_prev, x, it, cond, use_cond);
+        } else {
+            if (pcm == 0) launch_update_xm<0, false>(P, xm, p_new, p_prev, x, it, cond, use_cond);
+            else if (pcm == 1) launch_update_xm<1, false>(P, xm, p_new, p_prev, x, it, cond, use_cond);
+            else launch_update_xm<2, false>(P, xm, p_new, p_prev, x, it, cond, use_cond);
+        }
+        RVK_CHECK_LAUNCH("k_cg_update");
+        return RVK_OK;
+    }
     auto go = [&](auto kern) {
         kern<<<P->upd_grid, kUpdThreads, 0, s>>>(P->A.n_rows, p_new, P->w, P->dinv, x, P->r, P->z,
                                                  P->st, P->hist, it, P->cfg.rtol, P->cfg.atol,
                                                  P->partials, P->tickets, P->dconst,
-                                                 P->cfg.max_it, cond, use_cond);
+                                                 P->cfg.max_it, cond, use_cond, p_new);
     };
     if (V && P->k2_tma) {
         auto gt = [&](auto kern, size_t smem) {
@@ -742,6 +824,21 @@ rvk_status launch_update(rvk_cg_plan P, int pcm, const double* p_new, double* x,
     }
     RVK_CHECK_LAUNCH("k_cg_update");
     return RVK_OK;
+}
+
+rvk_status launch_xfix(rvk_cg_plan P, double* x)
+{
+    k_cg_xfix<<<P->upd_grid, kUpdThreads, 0, P->ctx->stream>>>(P->A.n_rows, x, P->p[0], P->p[1], P->st);
+    RVK_CHECK_LAUNCH("k_cg_xfix");
+    return RVK_OK;
+}
+
+// Deferred x updates on this solve? (vector path, classic K2, max_it >= 2;
+// RVK_X_DEFER=0 disables)
+bool x_defer(rvk_cg_plan P, bool vec)
+{
+    const char* e = std::getenv("RVK_X_DEFER");
+    return vec && !P->k2_tma && P->cfg.max_it >= 2 && !(e && e[0] == '0');
 }
 
 // K1 of one iteration: it >= 0 static index, it == -1 read from the device
@@ -785,8 +882,9 @@ rvk_status build_while_graph(rvk_cg_plan P, const double* b, double* x, cudaGrap
     RVK_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeGlobal));
     rvk_status rc = vec ? launch_setup<true>(P, pcm, b, x) : launch_setup<false>(P, pcm, b, x);
     if (rc == RVK_OK) rc = launch_k1(P, 0, true, P->p[0], P->p[1]);
+    const bool defer = x_defer(P, vec);
     if (rc == RVK_OK)
-        rc = vec ? launch_update<true>(P, pcm, P->p[1], x, 0, h, 1)
+        rc = vec ? launch_update<true>(P, pcm, P->p[1], x, 0, h, 1, defer ? 1 : 0, P->p[0])
                  : launch_update<false>(P, pcm, P->p[1], x, 0, h, 1);
     cudaError_t e = cudaStreamEndCapture(s, &pro);
     if (rc != RVK_OK) return fail(rc);
@@ -807,16 +905,28 @@ rvk_status build_while_graph(rvk_cg_plan P, const double* b, double* x, cudaGrap
                                            cudaStreamCaptureModeGlobal)) != cudaSuccess)
         return fail(cuda_error(e, "cudaStreamBeginCaptureToGraph"));
     rc = launch_k1(P, -1, false, P->p[1], P->p[0]);
-    if (rc == RVK_OK)
-        rc = vec ? launch_update<true>(P, pcm, P->p[0], x, -1, h, 1)
+    if (rc == RVK_OK) // odd iteration: flushes the pending even update
+        rc = vec ? launch_update<true>(P, pcm, P->p[0], x, -1, h, 1, defer ? 2 : 0, P->p[1])
                  : launch_update<false>(P, pcm, P->p[0], x, -1, h, 1);
     if (rc == RVK_OK) rc = launch_k1(P, -1, false, P->p[0], P->p[1]);
-    if (rc == RVK_OK)
-        rc = vec ? launch_update<true>(P, pcm, P->p[1], x, -1, h, 1)
+    if (rc == RVK_OK) // even iteration: defers
+        rc = vec ? launch_update<true>(P, pcm, P->p[1], x, -1, h, 1, defer ? 1 : 0, P->p[0])
                  : launch_update<false>(P, pcm, P->p[1], x, -1, h, 1);
     e = cudaStreamEndCapture(s, &tmp);
     if (rc != RVK_OK) return fail(rc);
     if (e != cudaSuccess) return fail(cuda_error(e, "capture (while body)"));
+    if (defer) { // epilogue after the loop: apply an update left pending
+        cudaGraph_t epi = nullptr;
+        RVK_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeGlobal));
+        rc = launch_xfix(P, x);
+        e  = cudaStreamEndCapture(s, &epi);
+        if (rc != RVK_OK) return fail(rc);
+        if (e != cudaSuccess) return fail(cuda_error(e, "capture (while epilogue)"));
+        cudaGraphNode_t nepi;
+        e = cudaGraphAddChildGraphNode(&nepi, g, &nwhile, 1, epi);
+        cudaGraphDestroy(epi);
+        if (e != cudaSuccess) return fail(cuda_error(e, "cudaGraphAddChildGraphNode (epilogue)"));
+    }
     e = cudaGraphInstantiate(out, g, 0);
     fail(RVK_OK);
     if (e != cudaSuccess) return cuda_error(e, "cudaGraphInstantiate (while)");
@@ -830,6 +940,7 @@ rvk_status enqueue_fused(rvk_cg_plan P, const double* b, double* x)
     const int     pcm  = P->cfg.pc != RVK_PC_JACOBI ? 0 : ((P->stencil || P->const_diag) ? 2 : 1);
     const bool    vec  = aligned16(b) && aligned16(x) && aligned16(P->dinv);
     const TailArgs ta{P->partials + 2 * kMaxReduceBlocks, P->tickets + 1};
+    const bool     defer = x_defer(P, vec);
     P->launches = 0;
     auto rec = [&](int k) -> rvk_status {
         if (P->profiling)
@@ -856,10 +967,17 @@ rvk_status enqueue_fused(rvk_cg_plan P, const double* b, double* x)
         if (rc != RVK_OK) return rc;
         ++P->launches;
         if ((rc = rec(4 * it + 1)) != RVK_OK || (rc = rec(4 * it + 2)) != RVK_OK) return rc;
-        rc = vec ? launch_update<true>(P, pcm, p_new, x, it) : launch_update<false>(P, pcm, p_new, x, it);
+        // deferred x: even iterations defer (unless last), odd ones flush the pair
+        const int xm = !defer ? 0 : (it & 1) ? 2 : (it + 1 < P->cfg.max_it ? 1 : 0);
+        rc = vec ? launch_update<true>(P, pcm, p_new, x, it, 0, 0, xm, p_old)
+                 : launch_update<false>(P, pcm, p_new, x, it);
         if (rc != RVK_OK) return rc;
         ++P->launches;
         if ((rc = rec(4 * it + 3)) != RVK_OK) return rc;
+    }
+    if (defer) { // an early exit after a deferring iteration leaves x pending
+        if ((rc = launch_xfix(P, x)) != RVK_OK) return rc;
+        ++P->launches;
     }
     return RVK_OK;
 }
@@ -1255,7 +1373,8 @@ int rvk_cg_plan_flags(rvk_cg_plan P)
 {
     if (!P) return -1;
     return (P->const_diag ? RVK_PLAN_CONST_DIAG : 0) | (P->stencil ? RVK_PLAN_MATRIX_FREE : 0) |
-           (P->mf_tma ? RVK_PLAN_MF_TMA : 0) | (P->off32 ? RVK_PLAN_OFF32 : 0);
+           (P->mf_tma ? RVK_PLAN_MF_TMA : 0) | (P->off32 ? RVK_PLAN_OFF32 : 0) |
+           ((P->mode == RVK_CG_MODE_FUSED && x_defer(P, true)) ? RVK_PLAN_X_DEFER : 0);
 }
 
 const double* rvk_cg_plan_vector(rvk_cg_plan P, int which)

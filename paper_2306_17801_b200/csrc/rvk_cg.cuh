@@ -13,6 +13,8 @@ struct CgState {
     int    done, state, iterations, breakdown_iter;
     int    comm_error; // row-sharded PEER backend: a flag wait timed out
     unsigned int seq;  // row-sharded PEER backend: solves started on this plan
+    double pend_alpha; // fused CG: x += pend_alpha * p_{pend_it} not yet applied
+    int    x_pending, pend_it;
 };
 
 constexpr int kUpdThreads = 256;
