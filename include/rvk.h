@@ -313,7 +313,7 @@ rvk_status rvk_dcg_solve_dev(rvk_dcg_plan plan, const double* b_own, double* x_o
 rvk_status rvk_dcg_loopback_solve(rvk_dcg_plan* plans, int nplans, const double* const* b_own,
                                   double* const* x_own);
 rvk_status rvk_dcg_result(rvk_dcg_plan plan, double* hist_host, rvk_cg_info* info);
-int        rvk_dcg_plan_flags(rvk_dcg_plan plan); /* RVK_PLAN_* bits (CONST_DIAG, OFF32) */
+int        rvk_dcg_plan_flags(rvk_dcg_plan plan); /* RVK_PLAN_* bits (CONST_DIAG, OFF32, X_DEFER) */
 
 /* PEER backend (NVLink P2P; the fused compute+communication path).  Each
  * plan owns one device window [flags | gather slots | z | p0 | p1]; once

@@ -392,13 +392,16 @@ struct DcgSpmvOp {
 };
 
 // K2(it): fold p.w; alpha = beta_it / pAp; updates; partial z.z, z.r.
-template <int PC, bool PEER>
+// XM: x-update mode as the single-GPU k_cg_update (0 x += a p; 1 defer to
+// the next iteration; 2 x = (x + a' p_prev) + a p) -- bit-identical x.
+template <int PC, bool PEER, int XM = 0>
 __global__ void __launch_bounds__(kUpdThreads)
     k_dcg_update(int64_t n, const double* __restrict__ p, const double* __restrict__ w,
                  const double* __restrict__ dinv, double dconst, double* __restrict__ x,
                  double* __restrict__ r,
                  double* __restrict__ z, DcgScalars sc, int it, int rank, double* gather_out,
-                 double* partials, unsigned int* ticket, DcgPeer pr)
+                 double* partials, unsigned int* ticket, DcgPeer pr,
+                 const double* __restrict__ p_prev)
 {
     CgState* st = sc.st;
     if (st->done) return;
@@ -419,9 +422,18 @@ __global__ void __launch_bounds__(kUpdThreads)
         }
         return;
     }
+    // pend_alpha is only written by a DEFER (XM 1) launch, read by XM 2: no race
+    const double ap = XM == 2 ? st->pend_alpha : 0.0;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         st->pAp   = pAp;
         st->alpha = a;
+        if (XM == 1) {
+            st->pend_alpha = a;
+            st->pend_it    = it;
+            st->x_pending  = 1;
+        } else if (XM == 2) {
+            st->x_pending = 0;
+        }
     }
     __shared__ double smem[64];
     __shared__ int    flag;
@@ -429,7 +441,8 @@ __global__ void __launch_bounds__(kUpdThreads)
     double            acc[2] = {0.0, 0.0};
     const int64_t     stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-        x[i]            = axpy1(a, p[i], x[i]);
+        if (XM == 2) x[i] = axpy1(ap, p_prev[i], x[i]);
+        if (XM != 1) x[i] = axpy1(a, p[i], x[i]);
         const double ri = axpy1(na, w[i], r[i]);
         const double zi = jacobi_z(PC, dinv, dconst, i, ri);
         r[i]            = ri;
@@ -488,8 +501,23 @@ __global__ void k_dcg_finish(DcgScalars sc, int it, DcgPeer pr)
     }
 }
 
+// After the last iteration / an early exit: apply a deferred x update.
+// p0 / p1: the owned part of the ping-pong buffers.
+__global__ void __launch_bounds__(kUpdThreads)
+    k_dcg_xfix(int64_t n, double* __restrict__ x, const double* __restrict__ p0,
+               const double* __restrict__ p1, const CgState* __restrict__ st)
+{
+    if (!st->x_pending) return;
+    const double  a  = st->pend_alpha;
+    const double* pp = ((st->pend_it + 1) & 1) ? p1 : p0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        x[i] = axpy1(a, pp[i], x[i]);
+}
+
 __global__ void k_dcg_reset(CgState* st)
 {
+    st->x_pending = 0;
     st->done = 0;
     st->state = RVK_CG_RUNNING;
     st->iterations = 0;
@@ -646,30 +674,61 @@ rvk_status phase_k1(rvk_dcg_plan P, int it)
     return it == 0 ? launch_k1<true, false>(P, it) : launch_k1<false, false>(P, it);
 }
 
-template <int PC, bool PEER>
-void launch_update_k(rvk_dcg_plan P, int it, double* x)
+// x update per iteration pair (as rvk_cg.cu; RVK_X_DEFER=0 disables)
+bool x_defer(const rvk_dcg_plan P)
 {
-    k_dcg_update<PC, PEER><<<P->upd_grid, kUpdThreads, 0, P->ctx->stream>>>(
-        P->sh.n_own, P->p[(it + 1) & 1] + P->sh.halo_lo, P->w, P->dinv, P->dconst, x, P->r,
-        P->z + P->sh.halo_lo, scalars(P), it, P->sh.rank, P->gather + P->sh.rank * 4, P->partials,
-        P->tickets, P->peer);
+    const char* e = std::getenv("RVK_X_DEFER");
+    return P->cfg.max_it >= 2 && !(e && e[0] == '0');
+}
+int x_mode(const rvk_dcg_plan P, int it)
+{
+    if (!x_defer(P)) return 0;
+    return (it & 1) ? 2 : (it + 1 < P->cfg.max_it ? 1 : 0);
 }
 
-template <bool PEER>
+template <int PC, bool PEER, int XM>
+void launch_update_k(rvk_dcg_plan P, int it, double* x)
+{
+    k_dcg_update<PC, PEER, XM><<<P->upd_grid, kUpdThreads, 0, P->ctx->stream>>>(
+        P->sh.n_own, P->p[(it + 1) & 1] + P->sh.halo_lo, P->w, P->dinv, P->dconst, x, P->r,
+        P->z + P->sh.halo_lo, scalars(P), it, P->sh.rank, P->gather + P->sh.rank * 4, P->partials,
+        P->tickets, P->peer, P->p[it & 1] + P->sh.halo_lo);
+}
+
+template <bool PEER, int XM>
 void dispatch_update(rvk_dcg_plan P, int it, double* x)
 {
     switch (pc_mode(P)) {
-    case 0: launch_update_k<0, PEER>(P, it, x); break;
-    case 1: launch_update_k<1, PEER>(P, it, x); break;
-    default: launch_update_k<2, PEER>(P, it, x);
+    case 0: launch_update_k<0, PEER, XM>(P, it, x); break;
+    case 1: launch_update_k<1, PEER, XM>(P, it, x); break;
+    default: launch_update_k<2, PEER, XM>(P, it, x);
+    }
+}
+
+template <bool PEER>
+void dispatch_update_xm(rvk_dcg_plan P, int it, double* x)
+{
+    switch (x_mode(P, it)) {
+    case 1: dispatch_update<PEER, 1>(P, it, x); break;
+    case 2: dispatch_update<PEER, 2>(P, it, x); break;
+    default: dispatch_update<PEER, 0>(P, it, x);
     }
 }
 
 rvk_status phase_k2(rvk_dcg_plan P, int it, double* x)
 {
-    if (P->peer.on) dispatch_update<true>(P, it, x);
-    else dispatch_update<false>(P, it, x);
+    if (P->peer.on) dispatch_update_xm<true>(P, it, x);
+    else dispatch_update_xm<false>(P, it, x);
     RVK_CHECK_LAUNCH("k_dcg_update");
+    return RVK_OK;
+}
+
+rvk_status phase_xfix(rvk_dcg_plan P, double* x)
+{
+    if (!x_defer(P)) return RVK_OK;
+    k_dcg_xfix<<<P->upd_grid, kUpdThreads, 0, P->ctx->stream>>>(
+        P->sh.n_own, x, P->p[0] + P->sh.halo_lo, P->p[1] + P->sh.halo_lo, P->st);
+    RVK_CHECK_LAUNCH("k_dcg_xfix");
     return RVK_OK;
 }
 
@@ -820,7 +879,7 @@ rvk_status rvk_dcg_plan_create(rvk_ctx ctx, const rvk_csr* A, rvk_shard sh, rvk_
     if (std::getenv("RVK_NO_PREFETCH")) win.has_lead = false;
     P->sa          = make_spmv_args(*A, maxlen, &win, 2);
     spmv_set_order(P->sa, bands, A->nnz, 2, sm_count());
-    P->upd_grid    = resident_grid(k_dcg_update<1, true>, kUpdThreads, sh.n_own);
+    P->upd_grid    = resident_grid(k_dcg_update<1, true, 2>, kUpdThreads, sh.n_own);
     P->owns_gather = shared_gather == nullptr;
     P->gather      = shared_gather;
     rvk_status rc  = alloc_plan_buffers(P);
@@ -876,7 +935,8 @@ rvk_status rvk_dcg_solve_dev(rvk_dcg_plan P, const double* b_own, double* x_own)
         RVK_TRY(phase_k2(P, it, x_own));
         if (dist) RVK_TRY(nccl_allgather(P));
     }
-    return phase_finish(P);
+    RVK_TRY(phase_finish(P));
+    return phase_xfix(P, x_own);
 }
 
 // All P shards on one device, enqueued phase by phase on shard 0's stream
@@ -902,6 +962,7 @@ rvk_status rvk_dcg_loopback_solve(rvk_dcg_plan* Ps, int np, const double* const*
         for (int r = 0; r < np; ++r) RVK_TRY(phase_k2(Ps[r], it, x[r]));
     }
     for (int r = 0; r < np; ++r) RVK_TRY(phase_finish(Ps[r]));
+    for (int r = 0; r < np; ++r) RVK_TRY(phase_xfix(Ps[r], x[r]));
     return RVK_OK;
 }
 
@@ -931,7 +992,8 @@ rvk_status rvk_dcg_result(rvk_dcg_plan P, double* hist_host, rvk_cg_info* info)
 int rvk_dcg_plan_flags(rvk_dcg_plan P)
 {
     if (!P) return -1;
-    return (P->const_diag ? RVK_PLAN_CONST_DIAG : 0) | (P->off32 ? RVK_PLAN_OFF32 : 0);
+    return (P->const_diag ? RVK_PLAN_CONST_DIAG : 0) | (P->off32 ? RVK_PLAN_OFF32 : 0) |
+           (x_defer(P) ? RVK_PLAN_X_DEFER : 0);
 }
 
 // ---- PEER backend ----------------------------------------------------------

@@ -358,8 +358,10 @@ def bench_main(args, cfg):
 
     n_glob = int(np.prod(grid))
     nnz_glob = _global_nnz(dim, pts, grid)
-    ob = 4 if (rvk.lib().rvk_dcg_plan_flags(plan.h) & 8) else 8  # int32 row offsets streamed
-    b_min = 20 * (12 * nnz_glob + ob * (n_glob + 1) + 96 * n_glob) + 64 * n_glob
+    fl = rvk.lib().rvk_dcg_plan_flags(plan.h)
+    ob = 4 if fl & 8 else 8               # int32 row offsets streamed
+    vb = 88 if fl & 16 else 96            # x updated per iteration pair
+    b_min = 20 * (12 * nnz_glob + ob * (n_glob + 1) + vb * n_glob) + 64 * n_glob
     hbm_peak, peak_src = peaks()
     per_gpu = b_min / world / (ms * 1e-3) / 1e9
     launches = 3 + 2 * 20  # reset, setup, 20 x (K1, K2), finish  (our kernels, per rank)
