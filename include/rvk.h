@@ -235,7 +235,7 @@ rvk_status rvk_cg_solve_host_many(rvk_cg_plan plan, int nrhs, const double* cons
 /* Plan structure the solve exploits (bitmask):
  *   RVK_PLAN_CONST_DIAG   every diagonal entry is the same bit pattern (constant-
  *                         coefficient stencils): Jacobi uses the scalar, no dinv
- *                         stream (opt-in: env RVK_CONST_DIAG=1 at plan creation)
+ *                         stream (RVK_CONST_DIAG=0 at plan creation disables)
  *   RVK_PLAN_MATRIX_FREE  rvk_cg_plan_create_stencil operator                       */
 #define RVK_PLAN_CONST_DIAG  1
 #define RVK_PLAN_MATRIX_FREE 2

@@ -1355,11 +1355,12 @@ rvk_status rvk_cg_plan_create(rvk_ctx ctx, const rvk_csr* A, rvk_cg_config cfg, 
     // Constant-coefficient operators with Dirichlet truncation have ONE
     // diagonal value, so dinv is a constant vector: the fused K0/K2 then
     // multiply by the scalar (bit-identical z = dinv[i] * r[i]) and skip the
-    // 8n-byte dinv stream per iteration.  Opt-in (RVK_CONST_DIAG=1): measured
-    // on B200 (7-point 256^3) K2 174 -> 162 us but K1 +11 us (K2's dirty lines
-    // drain during K1), solve time unchanged at 9.99 ms.
+    // 8n-byte dinv stream per iteration (RVK_CONST_DIAG=0 disables).  Measured
+    // on B200 (7-point 256^3): with the per-iteration x update it was a wash
+    // (K2 -12 us, K1 +11 us); with the pairwise x update K2 151 -> 137 us,
+    // K1 unchanged, solve 9.31 -> 9.00 ms.
     const char* cd = std::getenv("RVK_CONST_DIAG");
-    if (rc == RVK_OK && cfg.pc == RVK_PC_JACOBI && cd && cd[0] == '1')
+    if (rc == RVK_OK && cfg.pc == RVK_PC_JACOBI && !(cd && cd[0] == '0'))
         rc = vector_is_constant(s, A->n_rows, P->dinv, &P->const_diag, &P->dconst);
     if (rc != RVK_OK) {
         rvk_cg_plan_destroy(P);

@@ -888,10 +888,10 @@ rvk_status rvk_dcg_plan_create(rvk_ctx ctx, const rvk_csr* A, rvk_shard sh, rvk_
         if (cfg.pc == RVK_PC_JACOBI) rc = diag_inverse(ctx->stream, *A, sh.halo_lo, P->dinv);
         else rc = rvk_set(ctx, sh.n_own, 1.0, P->dinv);
     }
-    // constant diagonal -> scalar Jacobi (as rvk_cg_plan_create; opt-in RVK_CONST_DIAG=1).
+    // constant diagonal -> scalar Jacobi (as rvk_cg_plan_create; RVK_CONST_DIAG=0 disables).
     // Every shard of a constant-coefficient operator sees the same value.
     const char* cd = std::getenv("RVK_CONST_DIAG");
-    if (rc == RVK_OK && cfg.pc == RVK_PC_JACOBI && sh.n_own > 0 && cd && cd[0] == '1')
+    if (rc == RVK_OK && cfg.pc == RVK_PC_JACOBI && sh.n_own > 0 && !(cd && cd[0] == '0'))
         rc = vector_is_constant(ctx->stream, sh.n_own, P->dinv, &P->const_diag, &P->dconst);
     if (rc == RVK_OK) rc = make_off32(ctx->stream, *A, &P->off32);
     if (rc == RVK_OK) P->sa.off32 = P->off32;

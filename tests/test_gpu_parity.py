@@ -535,21 +535,22 @@ def test_chunked_tile_order_parity(ctx, spec, monkeypatch, capfd):
 
 @pytest.mark.parametrize("spec", [(3, 7, (20, 16, 12)), (2, 9, (40, 33)), (3, 27, (10, 9, 8))])
 def test_constant_diagonal_folding_bitexact(ctx, spec, monkeypatch):
-    """Constant-coefficient Laplacians have one diagonal value: with
-    RVK_CONST_DIAG=1 the plan folds dinv into a scalar (RVK_PLAN_CONST_DIAG)
-    and the fused kernels skip the dinv stream.  Results are bit-identical to
+    """Constant-coefficient Laplacians have one diagonal value: the plan
+    folds dinv into a scalar (RVK_PLAN_CONST_DIAG; RVK_CONST_DIAG=0 keeps the
+    vector) and the fused kernels skip the dinv stream.  Results are bit-identical to
     the dinv-vector path (also sharded); a matrix whose diagonal varies keeps
     the vector."""
     dim, pts, g = spec
     Ah = O.build_laplacian(dim, pts, g)
     b = O.rhs(Ah.n_rows)
     A = rvk.DeviceCsr.laplacian(ctx, dim, pts, g)
+    monkeypatch.setenv("RVK_CONST_DIAG", "0")
     p0 = rvk.CgPlan(ctx, A, max_it=20)
-    assert not p0.flags() & 1  # opt-in
+    assert not p0.flags() & 1
     x0, r0 = p0.solve_host(b)
-    monkeypatch.setenv("RVK_CONST_DIAG", "1")
+    monkeypatch.delenv("RVK_CONST_DIAG")
     p1 = rvk.CgPlan(ctx, A, max_it=20)
-    assert p1.flags() & 1
+    assert p1.flags() & 1  # default for constant-coefficient operators
     x1, r1 = p1.solve_host(b)
     assert np.array_equal(x1, x0) and np.array_equal(r1.hist, r0.hist)
     from paper_2306_17801_b200.sharded import loopback_solve
