@@ -243,6 +243,8 @@ rvk_status rvk_cg_solve_host_many(rvk_cg_plan plan, int nrhs, const double* cons
 #define RVK_PLAN_OFF32       8  /* the SpMV streams a plan-owned int32 copy of the row offsets */
 #define RVK_PLAN_X_DEFER    16  /* fused solve applies x += a p for iteration pairs in one pass
                                    (16-B aligned b / x; bit-identical x; RVK_X_DEFER=0 disables) */
+#define RVK_PLAN_Z_VIRTUAL  32  /* fused solve never stores z = d r (constant diagonal / no PC):
+                                   the SpMV gathers r and forms d r (bit-identical; RVK_ZV=0) */
 int        rvk_cg_plan_flags(rvk_cg_plan plan);
 /* Test hook (the reference's "exposed for equivalence tests" spirit,
  * kernels.hpp:50-76): device pointer of a plan work vector after a solve.

@@ -57,7 +57,7 @@ __global__ void __launch_bounds__(kUpdThreads)
     k_cg_setup(int64_t n, const double* __restrict__ b, const double* __restrict__ dinv,
                double* __restrict__ x, double* __restrict__ r, double* __restrict__ z,
                CgState* st, double* hist, double rtol, double atol, double* partials,
-               unsigned int* ticket, double dconst)
+               unsigned int* ticket, double dconst, int zw)
 {
     __shared__ double smem[64];
     __shared__ int    flag;
@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(kUpdThreads)
                 zi.y = mul(d.y, bi.y);
             }
             reinterpret_cast<double2*>(r)[i] = bi;
-            reinterpret_cast<double2*>(z)[i] = zi;
+            if (zw) reinterpret_cast<double2*>(z)[i] = zi; // zw = 0: z stays virtual (d r)
             st_stream(reinterpret_cast<double2*>(x) + i, make_double2(0.0, 0.0));
             acc[0] = add(acc[0], mul(zi.x, zi.x));
             acc[0] = add(acc[0], mul(zi.y, zi.y));
@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(kUpdThreads)
         const double bi = b[i];
         const double zi = PC == 0 ? bi : mul(PC == 1 ? dinv[i] : dconst, bi);
         r[i] = bi;
-        z[i] = zi;
+        if (zw) z[i] = zi;
         x[i] = 0.0;
         acc[0] = add(acc[0], mul(zi, zi));
         acc[1] = add(acc[1], mul(zi, bi));
@@ -176,7 +176,8 @@ __global__ void __launch_bounds__(kUpdThreads)
                 const double* __restrict__ dinv, double* __restrict__ x, double* __restrict__ r,
                 double* __restrict__ z, CgState* st, double* hist, int it, double rtol,
                 double atol, double* partials, unsigned int* ticket, double dconst, int max_it,
-                cudaGraphConditionalHandle cond, int use_cond, const double* __restrict__ p_prev)
+                cudaGraphConditionalHandle cond, int use_cond, const double* __restrict__ p_prev,
+                int zw)
 {
     static_assert(VEC || XM == 0, "deferred x updates use the vector path");
     // In the device WHILE loop (use_cond) `it` comes from the device state and
@@ -235,7 +236,7 @@ __global__ void __launch_bounds__(kUpdThreads)
                 zi.y = mul(d.y, ri.y);
             }
             r2[i] = ri;
-            z2[i] = zi;
+            if (zw) z2[i] = zi; // zw = 0: z stays virtual (K1 forms d r)
             acc[0] = add(acc[0], mul(zi.x, zi.x));
             acc[0] = add(acc[0], mul(zi.y, zi.y));
             acc[1] = add(acc[1], mul(zi.x, ri.x));
@@ -273,7 +274,7 @@ __global__ void __launch_bounds__(kUpdThreads)
         const double ri = axpy1(na, w[i], r[i]);
         const double zi = PC == 0 ? ri : mul(PC == 1 ? dinv[i] : dconst, ri);
         r[i]            = ri;
-        z[i]            = zi;
+        if (zw) z[i]    = zi;
         acc[0]          = add(acc[0], mul(zi, zi));
         acc[1]          = add(acc[1], mul(zi, ri));
     }
@@ -689,6 +690,7 @@ struct rvk_cg_plan_s {
     bool          const_diag = false;       // CSR plan: every dinv[i] bit-identical -> scalar
     int32_t*      off32      = nullptr;     // int32 row offsets for the SpMV stream (nnz < 2^31)
     bool          k2_tma     = false;       // K2 = k_cg_update_tma (RVK_K2_TMA=1)
+    bool          zv         = false;       // fused solve keeps z virtual (z = d r; RVK_ZV=0 off)
     int           mf_grid = 0;
     MfTma*        mf_tma  = nullptr;         // TMA 2.5D matrix-free kernel state (or null)
     double*       dinv = nullptr;
@@ -740,7 +742,7 @@ rvk_status launch_setup(rvk_cg_plan P, int pcm, const double* b, double* x)
     auto go = [&](auto kern) {
         kern<<<P->setup_grid, kUpdThreads, 0, s>>>(P->A.n_rows, b, P->dinv, x, P->r, P->z, P->st,
                                                    P->hist, P->cfg.rtol, P->cfg.atol, P->partials,
-                                                   P->tickets, P->dconst);
+                                                   P->tickets, P->dconst, P->zv ? 0 : 1);
     };
     if (pcm == 0) go(k_cg_setup<V, 0>);
     else if (pcm == 1) go(k_cg_setup<V, 1>);
@@ -757,7 +759,8 @@ void launch_update_k(rvk_cg_plan P, const double* p_new, const double* p_prev, d
 {
     k_cg_update<true, PC, COND, XM><<<P->upd_grid, kUpdThreads, 0, P->ctx->stream>>>(
         P->A.n_rows, p_new, P->w, P->dinv, x, P->r, P->z, P->st, P->hist, it, P->cfg.rtol,
-        P->cfg.atol, P->partials, P->tickets, P->dconst, P->cfg.max_it, cond, use_cond, p_prev);
+        P->cfg.atol, P->partials, P->tickets, P->dconst, P->cfg.max_it, cond, use_cond, p_prev,
+        P->zv ? 0 : 1);
 }
 
 template <int PC, bool COND>
@@ -792,7 +795,8 @@ rvk_status launch_update(rvk_cg_plan P, int pcm, const double* p_new, double* x,
         kern<<<P->upd_grid, kUpdThreads, 0, s>>>(P->A.n_rows, p_new, P->w, P->dinv, x, P->r, P->z,
                                                  P->st, P->hist, it, P->cfg.rtol, P->cfg.atol,
                                                  P->partials, P->tickets, P->dconst,
-                                                 P->cfg.max_it, cond, use_cond, p_new);
+                                                 P->cfg.max_it, cond, use_cond, p_new,
+                                                 P->zv ? 0 : 1);
     };
     if (V && P->k2_tma) {
         auto gt = [&](auto kern, size_t smem) {
@@ -848,15 +852,42 @@ rvk_status launch_k1(rvk_cg_plan P, int it, bool first, const double* p_old, dou
     cudaStream_t   s = P->ctx->stream;
     const int64_t  n = P->A.n_rows;
     const TailArgs ta{P->partials + 2 * kMaxReduceBlocks, P->tickets + 1};
+    // virtual z: gather r and form z = d r (d = the constant diagonal, 1 w/o PC)
+    const double zs = P->cfg.pc == RVK_PC_JACOBI ? P->dconst : 1.0;
     if (P->stencil)
-        return launch_mf_k1(s, P->geom, first, P->z, p_old, p_new, P->w, P->st, n, it, ta.partials,
-                            ta.ticket, P->mf_grid, P->mf_tma);
+        return launch_mf_k1(s, P->geom, first, P->zv ? P->r : P->z, p_old, p_new, P->w, P->st, n,
+                            it, ta.partials, ta.ticket, P->mf_grid, P->mf_tma, P->zv, zs);
+    if (P->zv) {
+        if (first) {
+            CgSpmvOp<true, true> op{P->r, p_old, p_new, P->w, P->st, n, it, 0.0, zs};
+            return launch_spmv(s, P->sa, op, ta, P->spmv_grid);
+        }
+        CgSpmvOp<false, true> op{P->r, p_old, p_new, P->w, P->st, n, it, 0.0, zs};
+        return launch_spmv(s, P->sa, op, ta, P->spmv_grid);
+    }
     if (first) {
         CgSpmvOp<true> op{P->z, p_old, p_new, P->w, P->st, n, it, 0.0};
         return launch_spmv(s, P->sa, op, ta, P->spmv_grid);
     }
     CgSpmvOp<false> op{P->z, p_old, p_new, P->w, P->st, n, it, 0.0};
     return launch_spmv(s, P->sa, op, ta, P->spmv_grid);
+}
+
+// Virtual z for the fused solve (z = d r never stored): constant diagonal or
+// no preconditioner, FUSED mode, classic K2.  Measured (B200, 20-iteration
+// solves): K2 131 -> 107 us everywhere, but the extra d * r per gathered
+// nonzero costs the 7-nonzero-batch SpMV more than that (7-point 256^3 K1
+// 316 -> 347 us, solve 8.83 -> 8.95 ms; 5-point likewise), while the 9-batch
+// kernels absorb it (27-point 21.02 -> 20.50 ms, 9-point 10.01 -> 9.47 ms)
+// and the matrix-free operator gains (4.60 -> 4.10 ms).  So: matrix-free and
+// 9-batch CSR plans.  RVK_ZV=0 disables, RVK_ZV=1 forces.
+bool virtual_z(rvk_cg_plan P)
+{
+    const char* e = std::getenv("RVK_ZV");
+    if (e && e[0] == '0') return false;
+    const bool ok = P->mode == RVK_CG_MODE_FUSED && !P->k2_tma &&
+                    (P->cfg.pc == RVK_PC_NONE || P->const_diag || P->stencil);
+    return ok && (P->stencil || P->sa.unroll == 9 || (e && e[0] == '1'));
 }
 
 // the convergence loop entirely on the device.  Graph =
@@ -954,16 +985,7 @@ rvk_status enqueue_fused(rvk_cg_plan P, const double* b, double* x)
         const double* p_old = P->p[it & 1];
         double*       p_new = P->p[(it + 1) & 1];
         if ((rc = rec(4 * it + 0)) != RVK_OK) return rc;
-        if (P->stencil) {
-            rc = launch_mf_k1(s, P->geom, it == 0, P->z, p_old, p_new, P->w, P->st, n, it, ta.partials,
-                              ta.ticket, P->mf_grid, P->mf_tma);
-        } else if (it == 0) {
-            CgSpmvOp<true> op{P->z, p_old, p_new, P->w, P->st, n, it, 0.0};
-            rc = launch_spmv(s, P->sa, op, ta, P->spmv_grid);
-        } else {
-            CgSpmvOp<false> op{P->z, p_old, p_new, P->w, P->st, n, it, 0.0};
-            rc = launch_spmv(s, P->sa, op, ta, P->spmv_grid);
-        }
+        rc = launch_k1(P, it, it == 0, p_old, p_new);
         if (rc != RVK_OK) return rc;
         ++P->launches;
         if ((rc = rec(4 * it + 1)) != RVK_OK || (rc = rec(4 * it + 2)) != RVK_OK) return rc;
@@ -1362,6 +1384,7 @@ rvk_status rvk_cg_plan_create(rvk_ctx ctx, const rvk_csr* A, rvk_cg_config cfg, 
     const char* cd = std::getenv("RVK_CONST_DIAG");
     if (rc == RVK_OK && cfg.pc == RVK_PC_JACOBI && !(cd && cd[0] == '0'))
         rc = vector_is_constant(s, A->n_rows, P->dinv, &P->const_diag, &P->dconst);
+    if (rc == RVK_OK) P->zv = virtual_z(P); // after the constant-diagonal check
     if (rc != RVK_OK) {
         rvk_cg_plan_destroy(P);
         return rc;
@@ -1375,7 +1398,8 @@ int rvk_cg_plan_flags(rvk_cg_plan P)
     if (!P) return -1;
     return (P->const_diag ? RVK_PLAN_CONST_DIAG : 0) | (P->stencil ? RVK_PLAN_MATRIX_FREE : 0) |
            (P->mf_tma ? RVK_PLAN_MF_TMA : 0) | (P->off32 ? RVK_PLAN_OFF32 : 0) |
-           ((P->mode == RVK_CG_MODE_FUSED && x_defer(P, true)) ? RVK_PLAN_X_DEFER : 0);
+           ((P->mode == RVK_CG_MODE_FUSED && x_defer(P, true)) ? RVK_PLAN_X_DEFER : 0) |
+           (P->zv ? RVK_PLAN_Z_VIRTUAL : 0);
 }
 
 const double* rvk_cg_plan_vector(rvk_cg_plan P, int which)
@@ -1443,7 +1467,8 @@ rvk_status rvk_cg_plan_create_stencil(rvk_ctx ctx, int dim, int points, int64_t 
         rvk_cg_plan_destroy(P);
         return cuda_error(e, "rvk_cg_plan_create_stencil");
     }
-    P->mf_tma = mf_tma_create(P->geom, P->z, P->p[0], P->p[1]);
+    P->mf_tma = mf_tma_create(P->geom, P->z, P->p[0], P->p[1], P->r);
+    P->zv     = virtual_z(P);
     *out = P;
     return RVK_OK;
 }

@@ -41,18 +41,26 @@ int resident_grid(K kernel, int threads, int64_t n_items)
 
 // ---------------------------------------------------------------------------
 // K1 op: p_new = z + b p_old on the fly; w = A p_new; tail alpha.
+// ZV ("virtual z"): the Jacobi diagonal is one value d (or there is no
+// preconditioner, d = 1), so z is never stored -- `z` points at r and every
+// gathered z_j = d * r_j is formed here, the same single rounding K2 would
+// have stored (bit-identical), saving the 8 n-byte z write per iteration.
 // ---------------------------------------------------------------------------
-template <bool FIRST>
+template <bool FIRST, bool ZV = false>
 struct CgSpmvOp {
     static constexpr bool kHasTail = true;
-    const double* __restrict__ z;
+    static constexpr bool kFirst   = FIRST;
+    static constexpr bool kZv      = ZV;
+    const double* __restrict__ z; // ZV: r
     const double* __restrict__ p_old;
     double* __restrict__ p_new;
     double* __restrict__ w;
     CgState* st;
     int64_t  n;
     int      it;
-    double   b; // set by init()
+    double   b;       // set by init()
+    double   zs = 1.0; // ZV: the constant Jacobi diagonal d
+    __device__ __forceinline__ double zval(double raw) const { return ZV ? mul(zs, raw) : raw; }
 
     __device__ __forceinline__ bool init()
     {
@@ -87,7 +95,7 @@ struct CgSpmvOp {
     }
     __device__ __forceinline__ double value(const Fetch& f) const
     {
-        return FIRST ? f.z : aypx1(b, f.z, f.p); // z + b*p  (kernels_scalar.cpp:33)
+        return FIRST ? zval(f.z) : aypx1(b, zval(f.z), f.p); // z + b*p  (kernels_scalar.cpp:33)
     }
     __device__ __forceinline__ int64_t own_col(int64_t i) const { return i; }
     // p_new[i] = z[i] + b p_old[i] from the row's own (gathered) operands
@@ -128,12 +136,13 @@ struct StencilGeom {
 // The TMA 2.5D variant's plan state (tensor maps of z, p0, p1); null when the
 // geometry does not allow it (odd nx) or RVK_MF_TMA=0.
 struct MfTma;
-MfTma*     mf_tma_create(const StencilGeom& g, const double* z, const double* p0, const double* p1);
+MfTma*     mf_tma_create(const StencilGeom& g, const double* z, const double* p0, const double* p1,
+                         const double* r);
 void       mf_tma_destroy(MfTma* t);
 rvk_status launch_mf_k1(cudaStream_t s, const StencilGeom& g, bool first, const double* z,
                         const double* p_old, double* p_new, double* w, CgState* st, int64_t n,
                         int it, double* partials, unsigned int* ticket, int grid,
-                        const MfTma* tma);
+                        const MfTma* tma, bool zv = false, double zs = 1.0);
 int        mf_grid(const StencilGeom& g);
 
 // Arguments of the single-kernel persistent solve (rvk_cg_small.cu).

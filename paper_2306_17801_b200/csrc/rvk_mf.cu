@@ -83,13 +83,14 @@ __device__ __forceinline__ F shfl_fetch_down(const F& v)
 // x+1 neighbours of a grid line come from the neighbouring lanes by shuffle
 // (warp-edge lanes load them) and each (dy, dz) line costs one coalesced load
 // per vector.  All loads are issued before any product is formed.
-template <bool FIRST, int DIM, bool BOX>
+template <class OpT, int DIM, bool BOX>
 __global__ void __launch_bounds__(kMfThreads, 2)
-    k_mf_cg(StencilGeom g, FastDiv fdx, FastDiv fdy, CgSpmvOp<FIRST> op_in, TailArgs tail,
+    k_mf_cg(StencilGeom g, FastDiv fdx, FastDiv fdy, OpT op_in, TailArgs tail,
             int64_t lead_lo, int64_t lead_hi)
 {
-    using F = typename CgSpmvOp<FIRST>::Fetch;
-    CgSpmvOp<FIRST> op = op_in;
+    constexpr bool FIRST = OpT::kFirst;
+    using F              = typename OpT::Fetch;
+    OpT op               = op_in;
     if (!op.init()) return; // device-side early exit (converged / breakdown)
     __shared__ double red[32];
     __shared__ int    flag;
@@ -239,10 +240,10 @@ __device__ __forceinline__ void tma_plane(void* dst, const CUtensorMap* map, int
     (void)y;
 }
 
-template <bool FIRST, int DIM, bool BOX>
+template <class OpT, int DIM, bool BOX>
 __global__ void __launch_bounds__(mf_threads<DIM, BOX>())
     k_mf_tma(const __grid_constant__ CUtensorMap tz, const __grid_constant__ CUtensorMap tp,
-             MfTmaGeom g, CgSpmvOp<FIRST> op_in, TailArgs tail)
+             MfTmaGeom g, OpT op_in, TailArgs tail)
 {
     using S                    = MfShape<DIM, BOX>;
     constexpr int TX = S::TX, TY = S::TY, RY = S::RY, NT = mf_threads<DIM, BOX>();
@@ -252,6 +253,7 @@ __global__ void __launch_bounds__(mf_threads<DIM, BOX>())
     // y0-1 .. y0+TY (3D), one plane
     constexpr int BW = TX + 4, BH = DIM == 3 ? TY + 2 : 1, BE = BW * BH;
     constexpr int BP   = (BE + 15) & ~15; // box pitch: every TMA destination 128-B aligned
+    constexpr bool FIRST = OpT::kFirst;
     constexpr int NSRC = FIRST ? 1 : 2;
     // dynamic shared memory (> 48 KB for the 27-point tile): [z | p_old] box
     // ring, then the 4-plane p ring
@@ -262,7 +264,7 @@ __global__ void __launch_bounds__(mf_threads<DIM, BOX>())
     __shared__ double                red[32];
     __shared__ int                   flag;
 
-    CgSpmvOp<FIRST> op = op_in;
+    OpT op = op_in;
     if (!op.init()) return; // device-side early exit (converged / breakdown)
     const int     tid = threadIdx.x, tx = tid % TX, ty = tid / TX;
     const int32_t tiles = g.tiles_x * g.tiles_y;
@@ -297,7 +299,7 @@ __global__ void __launch_bounds__(mf_threads<DIM, BOX>())
         mbar_wait(&full[k], (j / kTmaStages) & 1);
         double* P = pr[j & 3];
         for (int e = tid; e < BE; e += NT) {
-            const double zv = stage[k][0][e];
+            const double zv = op.zval(stage[k][0][e]); // ZV: the box holds r, z = d r
             P[e]            = FIRST ? zv : aypx1(op.b, zv, stage[k][1][e]);
         }
         __syncthreads(); // ring slot j complete; stage k consumed by every thread
@@ -358,18 +360,18 @@ __global__ void __launch_bounds__(mf_threads<DIM, BOX>())
     }
 }
 
-template <bool FIRST>
-rvk_status launch_first(cudaStream_t s, const StencilGeom& g, const CgSpmvOp<FIRST>& op,
+template <class OpT>
+rvk_status launch_first(cudaStream_t s, const StencilGeom& g, const OpT& op,
                         TailArgs ta, int grid)
 {
     // leading edge: the dz = +1 plane (3D) or dy = +1 line (2D), +-1 row/column
     const int64_t far = g.dim == 3 ? g.nx * g.ny : g.nx;
     const int64_t lo = far - (g.dim == 3 ? g.nx : 0) - 1, hi = far + (g.dim == 3 ? g.nx : 0) + 1;
     const FastDiv fx = FastDiv::make((uint32_t)g.nx), fy = FastDiv::make((uint32_t)g.ny);
-    if (g.dim == 3 && g.box) k_mf_cg<FIRST, 3, true><<<grid, kMfThreads, 0, s>>>(g, fx, fy, op, ta, lo, hi);
-    else if (g.dim == 3) k_mf_cg<FIRST, 3, false><<<grid, kMfThreads, 0, s>>>(g, fx, fy, op, ta, lo, hi);
-    else if (g.box) k_mf_cg<FIRST, 2, true><<<grid, kMfThreads, 0, s>>>(g, fx, fy, op, ta, lo, hi);
-    else k_mf_cg<FIRST, 2, false><<<grid, kMfThreads, 0, s>>>(g, fx, fy, op, ta, lo, hi);
+    if (g.dim == 3 && g.box) k_mf_cg<OpT, 3, true><<<grid, kMfThreads, 0, s>>>(g, fx, fy, op, ta, lo, hi);
+    else if (g.dim == 3) k_mf_cg<OpT, 3, false><<<grid, kMfThreads, 0, s>>>(g, fx, fy, op, ta, lo, hi);
+    else if (g.box) k_mf_cg<OpT, 2, true><<<grid, kMfThreads, 0, s>>>(g, fx, fy, op, ta, lo, hi);
+    else k_mf_cg<OpT, 2, false><<<grid, kMfThreads, 0, s>>>(g, fx, fy, op, ta, lo, hi);
     RVK_CHECK_LAUNCH("k_mf_cg");
     return RVK_OK;
 }
@@ -378,7 +380,7 @@ rvk_status launch_first(cudaStream_t s, const StencilGeom& g, const CgSpmvOp<FIR
 
 // ---- TMA plan state -----------------------------------------------------------
 struct MfTma {
-    CUtensorMap   z, p0, p1;
+    CUtensorMap   z, p0, p1, r;
     MfTmaGeom     g{};
     const double* p0_ptr = nullptr;
     const double* p1_ptr = nullptr;
@@ -443,10 +445,11 @@ void mf_configure()
 {
     static std::once_flag once; // before any graph capture (plan creation)
     std::call_once(once, [] {
-        cudaFuncSetAttribute(k_mf_tma<true, DIM, BOX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)mf_smem_bytes<DIM, BOX>());
-        cudaFuncSetAttribute(k_mf_tma<false, DIM, BOX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)mf_smem_bytes<DIM, BOX>());
+        const int sm = (int)mf_smem_bytes<DIM, BOX>();
+        cudaFuncSetAttribute(k_mf_tma<CgSpmvOp<true, false>, DIM, BOX>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+        cudaFuncSetAttribute(k_mf_tma<CgSpmvOp<false, false>, DIM, BOX>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+        cudaFuncSetAttribute(k_mf_tma<CgSpmvOp<true, true>, DIM, BOX>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+        cudaFuncSetAttribute(k_mf_tma<CgSpmvOp<false, true>, DIM, BOX>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     });
 }
 
@@ -456,7 +459,7 @@ int tma_blocks_per_sm()
     mf_configure<DIM, BOX>();
     int per_sm = 0;
     constexpr int nt = mf_threads<DIM, BOX>();
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mf_tma<false, DIM, BOX>, nt,
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mf_tma<CgSpmvOp<false, true>, DIM, BOX>, nt,
                                                       mf_smem_bytes<DIM, BOX>()) != cudaSuccess ||
         per_sm < 1)
         per_sm = 1;
@@ -464,7 +467,8 @@ int tma_blocks_per_sm()
 }
 } // namespace
 
-MfTma* mf_tma_create(const StencilGeom& g, const double* z, const double* p0, const double* p1)
+MfTma* mf_tma_create(const StencilGeom& g, const double* z, const double* p0, const double* p1,
+                     const double* r)
 {
     const char* env = std::getenv("RVK_MF_TMA");
     if (env && env[0] == '0') return nullptr;
@@ -477,7 +481,7 @@ MfTma* mf_tma_create(const StencilGeom& g, const double* z, const double* p0, co
     const int TY = g.dim == 3 ? (g.box ? MfShape<3, true>::TY : MfShape<3, false>::TY) : MfShape<2, false>::TY;
     const int bw = TX + 4, bh = g.dim == 3 ? TY + 2 : 1; // see k_mf_tma: 16-B aligned x start
     if (!encode_plane_map(&t->z, z, g, bw, bh) || !encode_plane_map(&t->p0, p0, g, bw, bh) ||
-        !encode_plane_map(&t->p1, p1, g, bw, bh)) {
+        !encode_plane_map(&t->p1, p1, g, bw, bh) || !encode_plane_map(&t->r, r, g, bw, bh)) {
         delete t;
         return nullptr;
     }
@@ -519,22 +523,22 @@ int mf_grid(const StencilGeom& g)
 {
     int per_sm = 0;
     cudaError_t e;
-    if (g.dim == 3 && g.box) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mf_cg<false, 3, true>, kMfThreads, 0);
-    else if (g.dim == 3) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mf_cg<false, 3, false>, kMfThreads, 0);
-    else if (g.box) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mf_cg<false, 2, true>, kMfThreads, 0);
-    else e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mf_cg<false, 2, false>, kMfThreads, 0);
+    if (g.dim == 3 && g.box) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mf_cg<CgSpmvOp<false, true>, 3, true>, kMfThreads, 0);
+    else if (g.dim == 3) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mf_cg<CgSpmvOp<false, true>, 3, false>, kMfThreads, 0);
+    else if (g.box) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mf_cg<CgSpmvOp<false, true>, 2, true>, kMfThreads, 0);
+    else e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mf_cg<CgSpmvOp<false, true>, 2, false>, kMfThreads, 0);
     if (e != cudaSuccess || per_sm < 1) per_sm = 1;
     const int64_t tiles = (g.n + kMfThreads - 1) / kMfThreads;
     return (int)std::min<int64_t>(tiles, (int64_t)sm_count() * per_sm);
 }
 
 namespace {
-template <bool FIRST>
-rvk_status launch_tma(cudaStream_t s, const MfTma& t, const CgSpmvOp<FIRST>& op, TailArgs ta)
+template <class OpT>
+rvk_status launch_tma(cudaStream_t s, const MfTma& t, const OpT& op, TailArgs ta)
 {
     const CUtensorMap& tp = op.p_old == t.p1_ptr ? t.p1 : t.p0;
 #define RVK_MF_LAUNCH(D, B)                                                                        \
-    k_mf_tma<FIRST, D, B><<<t.grid, mf_threads<D, B>(), mf_smem_bytes<D, B>(), s>>>(t.z, tp, t.g, op, ta)
+    k_mf_tma<OpT, D, B><<<t.grid, mf_threads<D, B>(), mf_smem_bytes<D, B>(), s>>>(OpT::kZv ? t.r : t.z, tp, t.g, op, ta)
     if (t.dim == 3 && t.box) RVK_MF_LAUNCH(3, true);
     else if (t.dim == 3) RVK_MF_LAUNCH(3, false);
     else if (t.box) RVK_MF_LAUNCH(2, true);
@@ -547,12 +551,21 @@ rvk_status launch_tma(cudaStream_t s, const MfTma& t, const CgSpmvOp<FIRST>& op,
 
 rvk_status launch_mf_k1(cudaStream_t s, const StencilGeom& g, bool first, const double* z,
                         const double* p_old, double* p_new, double* w, CgState* st, int64_t n,
-                        int it, double* partials, unsigned int* ticket, int grid, const MfTma* tma)
+                        int it, double* partials, unsigned int* ticket, int grid, const MfTma* tma,
+                        bool zv, double zs)
 {
     const TailArgs ta{partials, ticket};
     if (tma) {
+        if (zv) {
+            if (first) return launch_tma(s, *tma, CgSpmvOp<true, true>{z, p_old, p_new, w, st, n, it, 0.0, zs}, ta);
+            return launch_tma(s, *tma, CgSpmvOp<false, true>{z, p_old, p_new, w, st, n, it, 0.0, zs}, ta);
+        }
         if (first) return launch_tma(s, *tma, CgSpmvOp<true>{z, p_old, p_new, w, st, n, it, 0.0}, ta);
         return launch_tma(s, *tma, CgSpmvOp<false>{z, p_old, p_new, w, st, n, it, 0.0}, ta);
+    }
+    if (zv) {
+        if (first) return launch_first(s, g, CgSpmvOp<true, true>{z, p_old, p_new, w, st, n, it, 0.0, zs}, ta, grid);
+        return launch_first(s, g, CgSpmvOp<false, true>{z, p_old, p_new, w, st, n, it, 0.0, zs}, ta, grid);
     }
     if (first) return launch_first(s, g, CgSpmvOp<true>{z, p_old, p_new, w, st, n, it, 0.0}, ta, grid);
     return launch_first(s, g, CgSpmvOp<false>{z, p_old, p_new, w, st, n, it, 0.0}, ta, grid);
