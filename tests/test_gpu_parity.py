@@ -640,3 +640,33 @@ def test_stream_ordered_alloc_deferred_release(ctx):
     rvk.check(L.rvk_nrm2(ctx.h, n, p, out.ptr))
     rvk.check(L.rvk_free_async(ctx.h, p))  # before the reduction has run
     assert out.download(ctx)[0] == pytest.approx(3.0 * np.sqrt(n), rel=1e-14)
+
+
+@pytest.mark.parametrize("spec", [(3, 7, (20, 16, 12)), (2, 9, (40, 33)), (3, 27, (10, 9, 8)),
+                                  (2, 5, (64, 48))])
+@pytest.mark.parametrize("pc", ["jacobi", "none"])
+def test_virtual_z_bitexact(ctx, spec, pc, monkeypatch):
+    """Virtual z (z = d r never stored; the SpMV forms d r_j) and the pairwise
+    x update change no arithmetic: x and the history are bit-identical with
+    both off, for every stencil, with and without the Jacobi diagonal, CSR
+    and matrix-free."""
+    dim, pts, g = spec
+    Ah = O.build_laplacian(dim, pts, g)
+    b = O.rhs(Ah.n_rows)
+    A = rvk.DeviceCsr.laplacian(ctx, dim, pts, g)
+    out = {}
+    for name, env in (("on", {"RVK_ZV": "1"}), ("off", {"RVK_ZV": "0", "RVK_X_DEFER": "0"})):
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        plan = rvk.CgPlan(ctx, A, max_it=20, pc=pc)
+        assert bool(plan.flags() & 32) == (name == "on")
+        out[name] = plan.solve_host(b)
+        mf = rvk.CgPlan(ctx, (dim, pts, g), max_it=20, pc=pc)
+        out[name + "_mf"] = mf.solve_host(b)
+        for k in env:
+            monkeypatch.delenv(k)
+    for k in ("", "_mf"):
+        assert np.array_equal(out["on" + k][0], out["off" + k][0])
+        assert np.array_equal(out["on" + k][1].hist, out["off" + k][1].hist)
+    ref = O.cg_solve(Ah, b, max_it=20, pc=pc)
+    check_cg(out["on"][1], out["on"][0], ref)
