@@ -59,6 +59,8 @@ __global__ void __launch_bounds__(kUpdThreads)
                CgState* st, double* hist, double rtol, double atol, double* partials,
                unsigned int* ticket, double dconst, int zw)
 {
+    pdl_trigger();
+    pdl_wait();
     __shared__ double smem[64];
     __shared__ int    flag;
     double            acc[2] = {0.0, 0.0};
@@ -180,6 +182,8 @@ __global__ void __launch_bounds__(kUpdThreads)
                 int zw)
 {
     static_assert(VEC || XM == 0, "deferred x updates use the vector path");
+    pdl_trigger();
+    pdl_wait();
     // In the device WHILE loop (use_cond) `it` comes from the device state and
     // this kernel decides whether the loop body runs again.
     if (st->done) {
@@ -289,6 +293,8 @@ __global__ void __launch_bounds__(kUpdThreads)
     k_cg_xfix(int64_t n, double* __restrict__ x, const double* __restrict__ p0,
               const double* __restrict__ p1, const CgState* __restrict__ st)
 {
+    pdl_trigger();
+    pdl_wait();
     if (!st->x_pending) return;
     const double  a  = st->pend_alpha;
     const double* pp = ((st->pend_it + 1) & 1) ? p1 : p0;
@@ -740,9 +746,9 @@ rvk_status launch_setup(rvk_cg_plan P, int pcm, const double* b, double* x)
 {
     cudaStream_t s = P->ctx->stream;
     auto go = [&](auto kern) {
-        kern<<<P->setup_grid, kUpdThreads, 0, s>>>(P->A.n_rows, b, P->dinv, x, P->r, P->z, P->st,
-                                                   P->hist, P->cfg.rtol, P->cfg.atol, P->partials,
-                                                   P->tickets, P->dconst, P->zv ? 0 : 1);
+        launch_pdl(kern, P->setup_grid, kUpdThreads, 0, s, P->A.n_rows, b, P->dinv, x, P->r, P->z,
+                   P->st, P->hist, P->cfg.rtol, P->cfg.atol, P->partials, P->tickets, P->dconst,
+                   P->zv ? 0 : 1);
     };
     if (pcm == 0) go(k_cg_setup<V, 0>);
     else if (pcm == 1) go(k_cg_setup<V, 1>);
@@ -757,10 +763,10 @@ template <int PC, bool COND, int XM>
 void launch_update_k(rvk_cg_plan P, const double* p_new, const double* p_prev, double* x, int it,
                      cudaGraphConditionalHandle cond, int use_cond)
 {
-    k_cg_update<true, PC, COND, XM><<<P->upd_grid, kUpdThreads, 0, P->ctx->stream>>>(
-        P->A.n_rows, p_new, P->w, P->dinv, x, P->r, P->z, P->st, P->hist, it, P->cfg.rtol,
-        P->cfg.atol, P->partials, P->tickets, P->dconst, P->cfg.max_it, cond, use_cond, p_prev,
-        P->zv ? 0 : 1);
+    launch_pdl(k_cg_update<true, PC, COND, XM>, P->upd_grid, kUpdThreads, 0, P->ctx->stream,
+               P->A.n_rows, p_new, P->w, P->dinv, x, P->r, P->z, P->st, P->hist, it, P->cfg.rtol,
+               P->cfg.atol, P->partials, P->tickets, P->dconst, P->cfg.max_it, cond, use_cond,
+               p_prev, P->zv ? 0 : 1);
 }
 
 template <int PC, bool COND>
@@ -792,11 +798,9 @@ rvk_status launch_update(rvk_cg_plan P, int pcm, const double* p_new, double* x,
         return RVK_OK;
     }
     auto go = [&](auto kern) {
-        kern<<<P->upd_grid, kUpdThreads, 0, s>>>(P->A.n_rows, p_new, P->w, P->dinv, x, P->r, P->z,
-                                                 P->st, P->hist, it, P->cfg.rtol, P->cfg.atol,
-                                                 P->partials, P->tickets, P->dconst,
-                                                 P->cfg.max_it, cond, use_cond, p_new,
-                                                 P->zv ? 0 : 1);
+        launch_pdl(kern, P->upd_grid, kUpdThreads, 0, s, P->A.n_rows, p_new, P->w, P->dinv, x,
+                   P->r, P->z, P->st, P->hist, it, P->cfg.rtol, P->cfg.atol, P->partials,
+                   P->tickets, P->dconst, P->cfg.max_it, cond, use_cond, p_new, P->zv ? 0 : 1);
     };
     if (V && P->k2_tma) {
         auto gt = [&](auto kern, size_t smem) {
@@ -832,7 +836,8 @@ rvk_status launch_update(rvk_cg_plan P, int pcm, const double* p_new, double* x,
 
 rvk_status launch_xfix(rvk_cg_plan P, double* x)
 {
-    k_cg_xfix<<<P->upd_grid, kUpdThreads, 0, P->ctx->stream>>>(P->A.n_rows, x, P->p[0], P->p[1], P->st);
+    launch_pdl(k_cg_xfix, P->upd_grid, kUpdThreads, 0, P->ctx->stream, P->A.n_rows, x,
+               (const double*)P->p[0], (const double*)P->p[1], (const CgState*)P->st);
     RVK_CHECK_LAUNCH("k_cg_xfix");
     return RVK_OK;
 }

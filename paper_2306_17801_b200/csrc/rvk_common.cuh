@@ -192,6 +192,14 @@ __device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
 
+// Programmatic dependent launch (sm_90+): a kernel launched with the
+// programmatic-serialization attribute may start while its predecessor in the
+// stream drains; pdl_wait() blocks until the predecessor has completed and
+// its memory is visible (a no-op for an ordinary launch), pdl_trigger() lets
+// the successor begin launching.  Every global access stays after pdl_wait().
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // Streaming global loads (read-once data).
 __device__ __forceinline__ double2 ld_stream(const double2* p) { return __ldcs(p); }
 __device__ __forceinline__ void st_stream(double2* p, double2 v) { __stcs(p, v); }
@@ -200,6 +208,26 @@ __device__ __forceinline__ void st_stream(double2* p, double2 v) { __stcs(p, v);
 
 // Host-side error plumbing shared by the .cu/.cpp translation units.
 namespace rvk {
+// Launch `kern` with programmatic stream serialization (PDL) when enabled
+// (opt-in RVK_PDL=1): the kernel must call pdl_wait() before touching
+// global memory its stream predecessor reads or writes.
+bool pdl_enabled();
+template <class... KArgs, class... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args&&... args)
+{
+    cudaLaunchConfig_t  cfg = {};
+    cudaLaunchAttribute attr[1];
+    cfg.gridDim          = grid;
+    cfg.blockDim         = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream           = s;
+    attr[0].id                                         = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs                                          = attr;
+    cfg.numAttrs                                       = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
 rvk_status set_error(rvk_status s, const char* fmt, ...);
 rvk_status cuda_error(cudaError_t e, const char* what);
 void       note_host_sync();

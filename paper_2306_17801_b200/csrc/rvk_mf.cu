@@ -90,6 +90,8 @@ __global__ void __launch_bounds__(kMfThreads, 2)
 {
     constexpr bool FIRST = OpT::kFirst;
     using F              = typename OpT::Fetch;
+    pdl_trigger();
+    pdl_wait();
     OpT op               = op_in;
     if (!op.init()) return; // device-side early exit (converged / breakdown)
     __shared__ double red[32];
@@ -264,6 +266,8 @@ __global__ void __launch_bounds__(mf_threads<DIM, BOX>())
     __shared__ double                red[32];
     __shared__ int                   flag;
 
+    pdl_trigger();
+    pdl_wait();
     OpT op = op_in;
     if (!op.init()) return; // device-side early exit (converged / breakdown)
     const int     tid = threadIdx.x, tx = tid % TX, ty = tid / TX;
@@ -368,10 +372,10 @@ rvk_status launch_first(cudaStream_t s, const StencilGeom& g, const OpT& op,
     const int64_t far = g.dim == 3 ? g.nx * g.ny : g.nx;
     const int64_t lo = far - (g.dim == 3 ? g.nx : 0) - 1, hi = far + (g.dim == 3 ? g.nx : 0) + 1;
     const FastDiv fx = FastDiv::make((uint32_t)g.nx), fy = FastDiv::make((uint32_t)g.ny);
-    if (g.dim == 3 && g.box) k_mf_cg<OpT, 3, true><<<grid, kMfThreads, 0, s>>>(g, fx, fy, op, ta, lo, hi);
-    else if (g.dim == 3) k_mf_cg<OpT, 3, false><<<grid, kMfThreads, 0, s>>>(g, fx, fy, op, ta, lo, hi);
-    else if (g.box) k_mf_cg<OpT, 2, true><<<grid, kMfThreads, 0, s>>>(g, fx, fy, op, ta, lo, hi);
-    else k_mf_cg<OpT, 2, false><<<grid, kMfThreads, 0, s>>>(g, fx, fy, op, ta, lo, hi);
+    if (g.dim == 3 && g.box) launch_pdl(k_mf_cg<OpT, 3, true>, grid, kMfThreads, 0, s, g, fx, fy, op, ta, lo, hi);
+    else if (g.dim == 3) launch_pdl(k_mf_cg<OpT, 3, false>, grid, kMfThreads, 0, s, g, fx, fy, op, ta, lo, hi);
+    else if (g.box) launch_pdl(k_mf_cg<OpT, 2, true>, grid, kMfThreads, 0, s, g, fx, fy, op, ta, lo, hi);
+    else launch_pdl(k_mf_cg<OpT, 2, false>, grid, kMfThreads, 0, s, g, fx, fy, op, ta, lo, hi);
     RVK_CHECK_LAUNCH("k_mf_cg");
     return RVK_OK;
 }
@@ -538,7 +542,8 @@ rvk_status launch_tma(cudaStream_t s, const MfTma& t, const OpT& op, TailArgs ta
 {
     const CUtensorMap& tp = op.p_old == t.p1_ptr ? t.p1 : t.p0;
 #define RVK_MF_LAUNCH(D, B)                                                                        \
-    k_mf_tma<OpT, D, B><<<t.grid, mf_threads<D, B>(), mf_smem_bytes<D, B>(), s>>>(OpT::kZv ? t.r : t.z, tp, t.g, op, ta)
+    launch_pdl(k_mf_tma<OpT, D, B>, t.grid, mf_threads<D, B>(), mf_smem_bytes<D, B>(), s,            \
+               OpT::kZv ? t.r : t.z, tp, t.g, op, ta)
     if (t.dim == 3 && t.box) RVK_MF_LAUNCH(3, true);
     else if (t.dim == 3) RVK_MF_LAUNCH(3, false);
     else if (t.box) RVK_MF_LAUNCH(2, true);

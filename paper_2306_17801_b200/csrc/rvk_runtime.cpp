@@ -6,6 +6,7 @@
 // wait_for (cudaStreamWaitEvent) and query_idle (cudaStreamQuery) are the
 // hardware's.  Every host-blocking call is counted like the reference's
 // trace::host_sync events (trace.hpp:40-41).
+#include <cstdlib>
 #include "rvk_common.cuh"
 #include "rvk_context.hpp"
 
@@ -14,6 +15,21 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
+
+namespace rvk {
+// Opt-in (RVK_PDL=1): measured slower on B200 in the captured solve graphs
+// (7-point 256^3 9.01 vs 8.87 ms, 27-point 21.15 vs 20.97, matrix-free 4.18
+// vs 4.10) -- the early-launched successors cost more than the launch
+// latency they hide.
+bool pdl_enabled()
+{
+    static const bool on = [] {
+        const char* e = std::getenv("RVK_PDL");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+} // namespace rvk
 
 namespace rvk {
 

@@ -464,6 +464,8 @@ __global__ void __launch_bounds__(kSpmvThreads, 1) k_spmv_tma(SpmvArgs A, Op op_
     int*           flag   = reinterpret_cast<int*>(smem_raw + 512 + 1024);
     unsigned char* stage0 = smem_raw + kSpmvHeaderBytes;
 
+    pdl_trigger(); // the successor may start launching (it waits for our completion)
+    pdl_wait();    // our predecessor's writes are visible from here on
     Op op = op_in;
     if (!op.init()) return; // device-side early exit (converged / breakdown)
 
@@ -683,10 +685,12 @@ rvk_status launch_spmv(cudaStream_t stream, const SpmvArgs& a, const Op& op, Tai
     }
     const int th = 32 + a.consumers;
     const size_t sm = a.smem_bytes();
-    if (a.off32) k_spmv_tma<Op, int32_t, 8><<<grid, th, sm, stream>>>(a, op, tail);
-    else if (a.unroll == 7) k_spmv_tma<Op, int64_t, 7><<<grid, th, sm, stream>>>(a, op, tail);
-    else if (a.unroll == 9) k_spmv_tma<Op, int64_t, 9><<<grid, th, sm, stream>>>(a, op, tail);
-    else k_spmv_tma<Op, int64_t, 8><<<grid, th, sm, stream>>>(a, op, tail);
+    cudaError_t e;
+    if (a.off32) e = launch_pdl(k_spmv_tma<Op, int32_t, 8>, grid, th, sm, stream, a, op, tail);
+    else if (a.unroll == 7) e = launch_pdl(k_spmv_tma<Op, int64_t, 7>, grid, th, sm, stream, a, op, tail);
+    else if (a.unroll == 9) e = launch_pdl(k_spmv_tma<Op, int64_t, 9>, grid, th, sm, stream, a, op, tail);
+    else e = launch_pdl(k_spmv_tma<Op, int64_t, 8>, grid, th, sm, stream, a, op, tail);
+    if (e != cudaSuccess) return cuda_error(e, "k_spmv_tma launch");
     RVK_CHECK_LAUNCH("k_spmv_tma");
     return RVK_OK;
 }
