@@ -312,11 +312,20 @@ struct DcgSpmvOp {
     double*    lo_pn;                 // PEER: pr.lo_p / hi_p of this iteration's p_new
     double*    hi_pn;
     uint32_t   seq;
+    // the owned rows' slices (pre-offset by own_off): the row epilogue and its
+    // operands index them directly, like the single-GPU op
+    const double* __restrict__ z_own;
+    const double* __restrict__ pold_own;
+    double* __restrict__       pnew_own;
 
     __device__ __forceinline__ bool init()
     {
         CgState* st = sc.st;
         if (st->done) return false;
+#ifdef DCG_TIMING_PROBE // A/B probe only: trivial prologue (wrong numbers, same traffic)
+        if (!FIRST) b = sc.beta[it - 1] == 0.0 ? 0.0 : 0.5;
+        return true;
+#endif
         if constexpr (PEER) {
             seq = st->seq;
             if (!peer_wait(pr, st, phase_tag(seq, 2 * it + 1))) return false;
@@ -376,10 +385,15 @@ struct DcgSpmvOp {
         return FIRST ? f.z : aypx1(b, f.z, f.p);
     }
     __device__ __forceinline__ int64_t own_col(int64_t i) const { return i + own_off; }
+    using Own = Fetch;
+    __device__ __forceinline__ Own own(int64_t i) const
+    {
+        return Fetch{__ldg(z_own + i), FIRST ? 0.0 : __ldg(pold_own + i)};
+    }
     __device__ __forceinline__ double row(int64_t i, double sum, double acc, const Fetch& o) const
     {
         const double p     = value(o);
-        p_new[i + own_off] = p;
+        pnew_own[i]        = p;
         if constexpr (PEER) peer_push(lo_pn, hi_pn, pr.plane, pr.n_own, i, p);
         w[i]               = sum;
         return add(acc, mul(p, sum));
@@ -394,7 +408,7 @@ struct DcgSpmvOp {
 // K2(it): fold p.w; alpha = beta_it / pAp; updates; partial z.z, z.r.
 // XM: x-update mode as the single-GPU k_cg_update (0 x += a p; 1 defer to
 // the next iteration; 2 x = (x + a' p_prev) + a p) -- bit-identical x.
-template <int PC, bool PEER, int XM = 0>
+template <int PC, bool PEER, int XM = 0, bool VEC = false>
 __global__ void __launch_bounds__(kUpdThreads)
     k_dcg_update(int64_t n, const double* __restrict__ p, const double* __restrict__ w,
                  const double* __restrict__ dinv, double dconst, double* __restrict__ x,
@@ -440,7 +454,72 @@ __global__ void __launch_bounds__(kUpdThreads)
     const double      na     = -a;
     double            acc[2] = {0.0, 0.0};
     const int64_t     stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const int64_t     t0     = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if constexpr (VEC) {
+        // as k_cg_update: 2 x double2 per thread per trip, all loads first
+        const int64_t  n2 = n >> 1;
+        const double2* p2 = reinterpret_cast<const double2*>(p);
+        const double2* q2 = reinterpret_cast<const double2*>(p_prev);
+        const double2* w2 = reinterpret_cast<const double2*>(w);
+        const double2* d2 = reinterpret_cast<const double2*>(dinv);
+        double2*       x2 = reinterpret_cast<double2*>(x);
+        double2*       r2 = reinterpret_cast<double2*>(r);
+        double2*       z2 = reinterpret_cast<double2*>(z);
+        const double2  zero = make_double2(0.0, 0.0);
+        auto ld = [&](bool use, const double2* a2, int64_t i) { return use ? ld_stream(a2 + i) : zero; };
+        auto step = [&](const double2& pi, const double2& qi, const double2& wi, double2 xi,
+                        double2 ri, const double2& d, int64_t i) {
+            if (XM == 2) {
+                xi.x = axpy1(ap, qi.x, xi.x);
+                xi.y = axpy1(ap, qi.y, xi.y);
+            }
+            if (XM != 1) {
+                xi.x = axpy1(a, pi.x, xi.x);
+                xi.y = axpy1(a, pi.y, xi.y);
+                st_stream(x2 + i, xi);
+            }
+            ri.x = axpy1(na, wi.x, ri.x);
+            ri.y = axpy1(na, wi.y, ri.y);
+            double2 zi = ri;
+            if (PC != 0) {
+                zi.x = mul(d.x, ri.x);
+                zi.y = mul(d.y, ri.y);
+            }
+            r2[i] = ri;
+            z2[i] = zi;
+            if constexpr (PEER) {
+                peer_push(pr.lo_z, pr.hi_z, pr.plane, n, 2 * i, zi.x);
+                peer_push(pr.lo_z, pr.hi_z, pr.plane, n, 2 * i + 1, zi.y);
+            }
+            acc[0] = add(acc[0], mul(zi.x, zi.x));
+            acc[0] = add(acc[0], mul(zi.y, zi.y));
+            acc[1] = add(acc[1], mul(zi.x, ri.x));
+            acc[1] = add(acc[1], mul(zi.y, ri.y));
+        };
+        int64_t i = t0;
+        for (; i + stride < n2; i += 2 * stride) {
+            const int64_t j  = i + stride;
+            const double2 pa = ld(XM != 1, p2, i), pb = ld(XM != 1, p2, j);
+            const double2 qa = ld(XM == 2, q2, i), qb = ld(XM == 2, q2, j);
+            const double2 wa = ld_stream(w2 + i), wb = ld_stream(w2 + j);
+            const double2 xa = ld(XM != 1, x2, i), xb = ld(XM != 1, x2, j);
+            const double2 ra = ld_stream(r2 + i), rb = ld_stream(r2 + j);
+            double2 da = make_double2(dconst, dconst), db = da;
+            if (PC == 1) {
+                da = ld_stream(d2 + i);
+                db = ld_stream(d2 + j);
+            }
+            step(pa, qa, wa, xa, ra, da, i);
+            step(pb, qb, wb, xb, rb, db, j);
+        }
+        if (i < n2) {
+            double2 d = make_double2(dconst, dconst);
+            if (PC == 1) d = ld_stream(d2 + i);
+            step(ld(XM != 1, p2, i), ld(XM == 2, q2, i), ld_stream(w2 + i), ld(XM != 1, x2, i),
+                 ld_stream(r2 + i), d, i);
+        }
+    }
+    for (int64_t i = (VEC ? (n & ~int64_t(1)) : 0) + t0; i < n; i += stride) {
         if (XM == 2) x[i] = axpy1(ap, p_prev[i], x[i]);
         if (XM != 1) x[i] = axpy1(a, p[i], x[i]);
         const double ri = axpy1(na, w[i], r[i]);
@@ -568,18 +647,34 @@ struct WindowLayout {
 };
 WindowLayout window_layout(int64_t n_ext)
 {
-    auto         up = [](size_t v) { return (v + 255) & ~size_t(255); };
+#ifndef DCG_LAYOUT
+#define DCG_LAYOUT 1
+#endif
+    auto         up  = [](size_t v) { return (v + 255) & ~size_t(255); };
+    auto         up2 = [](size_t v) { return (v + (size_t(2) << 20) - 1) & ~((size_t(2) << 20) - 1); };
     WindowLayout L{};
-    size_t       o = 0;
-    L.flags        = o;
-    o              = up(o + kMaxRanks * sizeof(uint64_t));
-    L.gather       = o;
-    o              = up(o + kMaxRanks * 4 * sizeof(double));
+    if (DCG_LAYOUT == 1) {
+        // the gathered vectors start 2 MB-aligned, as separate allocations
+        // would (a 256-B packed layout measured ~8% slower in the SpMV)
+        const size_t vb = up2((size_t)n_ext * 8 + 32);
+        L.z             = 0;
+        L.p0            = vb;
+        L.p1            = 2 * vb;
+        L.flags         = 3 * vb;
+        L.gather        = up(L.flags + kMaxRanks * sizeof(uint64_t));
+        L.bytes         = up(L.gather + kMaxRanks * 4 * sizeof(double));
+        return L;
+    }
+    size_t o = 0;
+    L.flags  = o;
+    o        = up(o + kMaxRanks * sizeof(uint64_t));
+    L.gather = o;
+    o        = up(o + kMaxRanks * 4 * sizeof(double));
     const size_t vb = up((size_t)n_ext * 8 + 32); // padded: x-windows round up
-    L.z            = o;
-    L.p0           = o + vb;
-    L.p1           = o + 2 * vb;
-    L.bytes        = o + 3 * vb;
+    L.z             = o;
+    L.p0            = o + vb;
+    L.p1            = o + 2 * vb;
+    L.bytes         = o + 3 * vb;
     return L;
 }
 
@@ -601,6 +696,11 @@ rvk_status alloc_plan_buffers(rvk_dcg_plan P)
         P->p[1]      = reinterpret_cast<double*>(P->win + L.p1);
         if (P->owns_gather) P->gather = reinterpret_cast<double*>(P->win + L.gather);
     }
+#ifdef DCG_SEPARATE_PROBE // A/B probe: gathered vectors in their own allocations (no PEER)
+    alloc((void**)&P->z, P->n_ext * 8 + 32);
+    alloc((void**)&P->p[0], P->n_ext * 8 + 32);
+    alloc((void**)&P->p[1], P->n_ext * 8 + 32);
+#endif
     alloc((void**)&P->dinv, n * 8);
     alloc((void**)&P->r, n * 8);
     alloc((void**)&P->w, n * 8);
@@ -663,8 +763,9 @@ rvk_status launch_k1(rvk_dcg_plan P, int it)
     const TailArgs ta{P->partials + 2 * kMaxReduceBlocks, P->tickets + 1};
     double*        go = P->gather + P->sh.rank * 4 + 2;
     const int      k  = (it + 1) & 1; // p_new's buffer index, also in the neighbours
-    DcgSpmvOp<FIRST, PEER> op{P->z, po, pn, P->w, scalars(P), P->sh.halo_lo, go, it, 0.0, P->peer,
-                              P->peer.lo_p[k], P->peer.hi_p[k], 0u};
+    const int64_t          ho = P->sh.halo_lo;
+    DcgSpmvOp<FIRST, PEER> op{P->z, po, pn, P->w, scalars(P), ho, go, it, 0.0, P->peer,
+                              P->peer.lo_p[k], P->peer.hi_p[k], 0u, P->z + ho, po + ho, pn + ho};
     return launch_spmv(P->ctx->stream, P->sa, op, ta, sm_count());
 }
 
@@ -689,10 +790,18 @@ int x_mode(const rvk_dcg_plan P, int it)
 template <int PC, bool PEER, int XM>
 void launch_update_k(rvk_dcg_plan P, int it, double* x)
 {
-    k_dcg_update<PC, PEER, XM><<<P->upd_grid, kUpdThreads, 0, P->ctx->stream>>>(
-        P->sh.n_own, P->p[(it + 1) & 1] + P->sh.halo_lo, P->w, P->dinv, P->dconst, x, P->r,
-        P->z + P->sh.halo_lo, scalars(P), it, P->sh.rank, P->gather + P->sh.rank * 4, P->partials,
-        P->tickets, P->peer, P->p[it & 1] + P->sh.halo_lo);
+    const double* pn = P->p[(it + 1) & 1] + P->sh.halo_lo;
+    const double* pp = P->p[it & 1] + P->sh.halo_lo;
+    double*       zo = P->z + P->sh.halo_lo;
+    auto a16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
+    const bool vec = a16(x) && a16(pn) && a16(pp) && a16(zo) && a16(P->dinv) && a16(P->r) && a16(P->w);
+    auto go = [&](auto kern) {
+        kern<<<P->upd_grid, kUpdThreads, 0, P->ctx->stream>>>(
+            P->sh.n_own, pn, P->w, P->dinv, P->dconst, x, P->r, zo, scalars(P), it, P->sh.rank,
+            P->gather + P->sh.rank * 4, P->partials, P->tickets, P->peer, pp);
+    };
+    if (vec) go(k_dcg_update<PC, PEER, XM, true>);
+    else go(k_dcg_update<PC, PEER, XM, false>);
 }
 
 template <bool PEER, int XM>
@@ -879,7 +988,7 @@ rvk_status rvk_dcg_plan_create(rvk_ctx ctx, const rvk_csr* A, rvk_shard sh, rvk_
     if (std::getenv("RVK_NO_PREFETCH")) win.has_lead = false;
     P->sa          = make_spmv_args(*A, maxlen, &win, 2);
     spmv_set_order(P->sa, bands, A->nnz, 2, sm_count());
-    P->upd_grid    = resident_grid(k_dcg_update<1, true, 2>, kUpdThreads, sh.n_own);
+    P->upd_grid    = resident_grid(k_dcg_update<1, true, 2, true>, kUpdThreads, (sh.n_own + 1) / 2);
     P->owns_gather = shared_gather == nullptr;
     P->gather      = shared_gather;
     rvk_status rc  = alloc_plan_buffers(P);
