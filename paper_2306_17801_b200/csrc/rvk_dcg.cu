@@ -129,7 +129,7 @@ __device__ __forceinline__ void fold_gather(const double* g, int nranks, int j0,
 {
     for (int v = 0; v < nv; ++v) out[v] = 0.0;
     for (int r = 0; r < nranks; ++r)
-        for (int v = 0; v < nv; ++v) out[v] += __ldcv(g + r * 4 + j0 + v);
+        for (int v = 0; v < nv; ++v) out[v] += __ldcg(g + r * 4 + j0 + v); // L2: coherent with peer stores
 }
 
 // ---- PEER backend: system-scope flag protocol ------------------------------
