@@ -6,6 +6,7 @@
 #include "rivulet/expr.hpp"
 #include "rivulet/linalg.hpp"
 #include "rivulet/managed.hpp"
+#include "rivulet/mmio.hpp"
 #include "rivulet/runtime.hpp"
 #include "rivulet/solvers.hpp"
 #include "rivulet/stencil.hpp"
@@ -416,6 +417,67 @@ int main()
             got = e.iteration() == 0;
         }
         EXPECT(got);
+    });
+    // ---- external interfaces -----------------------------------------------------
+    run("Matrix Market + raw vector round trips (SPEC.md:432)", [] {
+        auto same = [](const CsrMatrix& a, const CsrMatrix& b) {
+            return a.rows() == b.rows() && a.cols() == b.cols() && a.nnz() == b.nnz() &&
+                   std::memcmp(a.row_offsets().data(), b.row_offsets().data(), (a.rows() + 1) * 8) == 0 &&
+                   std::memcmp(a.col_indices().data(), b.col_indices().data(), a.nnz() * 4) == 0 &&
+                   std::memcmp(a.values().data(), b.values().data(), a.nnz() * 8) == 0;
+        };
+        auto h = oracle_laplacian(2, 9, 12, 10, 1);
+        CsrMatrix A(h.n, h.n, h.off, h.cols, h.vals);
+        write_matrix_market(A, "/tmp/rvk_test_gen.mtx");
+        write_matrix_market(A, "/tmp/rvk_test_sym.mtx", true);
+        EXPECT(same(read_matrix_market("/tmp/rvk_test_gen.mtx"), A));
+        EXPECT(same(read_matrix_market("/tmp/rvk_test_sym.mtx"), A));
+        // non-representable decimals survive (17 significant digits)
+        CsrMatrix B(3, 4, {0, 2, 2, 4}, {1, 3, 0, 2}, {0.1, -1.0 / 3.0, 1e-300, 6.02214076e23});
+        write_matrix_market(B, "/tmp/rvk_test_b.mtx");
+        EXPECT(same(read_matrix_market("/tmp/rvk_test_b.mtx"), B));
+        bool threw = false;
+        try {
+            write_matrix_market(B, "/tmp/rvk_test_x.mtx", true); // not square / symmetric
+        } catch (const Error&) {
+            threw = true;
+        }
+        EXPECT(threw);
+        // unsorted entries, duplicates summed in file order, pattern/symmetric
+        {
+            std::FILE* f = std::fopen("/tmp/rvk_test_dup.mtx", "w");
+            std::fprintf(f, "%%%%MatrixMarket matrix coordinate real general\n%% c\n3 3 5\n"
+                            "3 1 2.5\n1 1 1\n2 2 4\n1 1 0.25\n1 3 -1\n");
+            std::fclose(f);
+            auto D = read_matrix_market("/tmp/rvk_test_dup.mtx");
+            EXPECT(same(D, CsrMatrix(3, 3, {0, 2, 3, 4}, {0, 2, 1, 0}, {1.25, -1.0, 4.0, 2.5})));
+            f = std::fopen("/tmp/rvk_test_pat.mtx", "w");
+            std::fprintf(f, "%%%%MatrixMarket matrix coordinate pattern symmetric\n2 2 2\n1 1\n2 1\n");
+            std::fclose(f);
+            EXPECT(same(read_matrix_market("/tmp/rvk_test_pat.mtx"),
+                        CsrMatrix(2, 2, {0, 2, 3}, {0, 1, 0}, {1.0, 1.0, 1.0})));
+        }
+        threw = false;
+        try {
+            std::FILE* f = std::fopen("/tmp/rvk_test_bad.mtx", "w");
+            std::fprintf(f, "%%%%MatrixMarket matrix coordinate real general\n2 2 1\n3 1 1.0\n");
+            std::fclose(f);
+            read_matrix_market("/tmp/rvk_test_bad.mtx");
+        } catch (const Error&) {
+            threw = true;
+        }
+        EXPECT(threw);
+        // a solve on the read-back matrix is the solve on the original, bit for bit
+        std::vector<double> bh(h.n);
+        ro_rhs(7, (int64_t)h.n, bh.data());
+        DenseVector b(bh);
+        write_vector_binary(b, "/tmp/rvk_test_b.bin");
+        DenseVector b2 = read_vector_binary("/tmp/rvk_test_b.bin");
+        EXPECT(b2.to_host() == bh);
+        DenseVector x1(h.n), x2(h.n);
+        auto r1 = cg_solve(A, b, x1);
+        auto r2 = cg_solve(read_matrix_market("/tmp/rvk_test_sym.mtx"), b2, x2);
+        EXPECT(r1.history == r2.history && x1.to_host() == x2.to_host());
     });
     // ---- property tests ---------------------------------------------------
     run("10,000 random expression DAGs vs a host interpreter (SPEC.md:624)", [] {
