@@ -670,3 +670,30 @@ def test_virtual_z_bitexact(ctx, spec, pc, monkeypatch):
         assert np.array_equal(out["on" + k][1].hist, out["off" + k][1].hist)
     ref = O.cg_solve(Ah, b, max_it=20, pc=pc)
     check_cg(out["on"][1], out["on"][0], ref)
+
+
+@pytest.mark.parametrize("graph", [True, "while", False])
+def test_pairwise_x_update_exits_at_both_parities(ctx, graph, monkeypatch):
+    """Early exits (device rtol) after even and odd iterations, odd max_it:
+    the pairwise x update (even K2 defers, odd K2 applies both, k_cg_xfix
+    flushes a pending one) gives x bit-identical to the per-iteration update."""
+    dim, pts, g = 2, 5, (48, 40)
+    Ah = O.build_laplacian(dim, pts, g)
+    b = O.rhs(Ah.n_rows)
+    A = rvk.DeviceCsr.laplacian(ctx, dim, pts, g)
+    seen = set()
+    for max_it, rtol in [(7, 0.0), (8, 0.0), (200, 1e-3), (200, 3e-4), (200, 1e-4), (200, 3e-5),
+                         (200, 1e-5), (200, 3e-6)]:
+        xs = {}
+        for d in ("1", "0"):
+            monkeypatch.setenv("RVK_X_DEFER", d)
+            plan = rvk.CgPlan(ctx, A, max_it=max_it, rtol=rtol, use_graph=graph)
+            xs[d] = plan.solve_host(b)
+            plan.close()
+        monkeypatch.delenv("RVK_X_DEFER")
+        assert np.array_equal(xs["1"][0], xs["0"][0]), (max_it, rtol)
+        assert np.array_equal(xs["1"][1].hist, xs["0"][1].hist)
+        seen.add(xs["1"][1].iterations % 2)
+        ref = O.cg_solve(Ah, b, max_it=max_it, rtol=rtol)
+        check_cg(xs["1"][1], xs["1"][0], ref)
+    assert seen == {0, 1}  # exits after both parities were exercised
