@@ -318,7 +318,7 @@ rvk_status rvk_dcg_result(rvk_dcg_plan plan, double* hist_host, rvk_cg_info* inf
 int        rvk_dcg_plan_flags(rvk_dcg_plan plan); /* RVK_PLAN_* bits (CONST_DIAG, OFF32, X_DEFER) */
 
 /* PEER backend (NVLink P2P; the fused compute+communication path).  Each
- * plan owns one device window [flags | gather slots | z | p0 | p1]; once
+ * plan owns one device window [z | p0 | p1 | flags | gather slots]; once
  * every rank's window is mapped (own window as is, peers' via the cudaIpc
  * helpers below) and attached, rvk_dcg_solve_dev runs 2 kernels per
  * iteration that push the halo planes of z and p straight into the

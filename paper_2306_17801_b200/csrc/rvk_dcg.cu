@@ -20,7 +20,7 @@
 //
 // Backends:
 //  * PEER (the product on an NVSwitch box): every shard exports ONE device
-//    window [flags | gather | z | p0 | p1] (cudaIpc handle, mapped by every
+//    window [z | p0 | p1 | flags | gather] (cudaIpc handle, mapped by every
 //    other rank).  The kernels do the communication themselves, tile by tile:
 //    K2/setup store the boundary planes of z straight into the neighbours'
 //    halo planes while they compute them, K1 does the same for p, and each
@@ -322,10 +322,6 @@ struct DcgSpmvOp {
     {
         CgState* st = sc.st;
         if (st->done) return false;
-#ifdef DCG_TIMING_PROBE // A/B probe only: trivial prologue (wrong numbers, same traffic)
-        if (!FIRST) b = sc.beta[it - 1] == 0.0 ? 0.0 : 0.5;
-        return true;
-#endif
         if constexpr (PEER) {
             seq = st->seq;
             if (!peer_wait(pr, st, phase_tag(seq, 2 * it + 1))) return false;
@@ -624,7 +620,7 @@ struct rvk_dcg_plan_s {
     SpmvArgs      sa{};
     int           upd_grid = 0;
     int64_t       n_ext = 0;
-    unsigned char* win = nullptr;  // [flags | gather | z | p0 | p1], the exported PEER window
+    unsigned char* win = nullptr;  // [z | p0 | p1 | flags | gather], the exported PEER window
     size_t        win_bytes = 0;
     double *dinv = nullptr, *r = nullptr, *z = nullptr, *p[2] = {nullptr, nullptr}, *w = nullptr;
     double *hist = nullptr, *beta = nullptr, *gather = nullptr, *partials = nullptr;
@@ -647,34 +643,18 @@ struct WindowLayout {
 };
 WindowLayout window_layout(int64_t n_ext)
 {
-#ifndef DCG_LAYOUT
-#define DCG_LAYOUT 1
-#endif
+    // the gathered vectors start 2 MB-aligned, as separate allocations would;
+    // flags and gather slots after them
     auto         up  = [](size_t v) { return (v + 255) & ~size_t(255); };
     auto         up2 = [](size_t v) { return (v + (size_t(2) << 20) - 1) & ~((size_t(2) << 20) - 1); };
     WindowLayout L{};
-    if (DCG_LAYOUT == 1) {
-        // the gathered vectors start 2 MB-aligned, as separate allocations
-        // would (a 256-B packed layout measured ~8% slower in the SpMV)
-        const size_t vb = up2((size_t)n_ext * 8 + 32);
-        L.z             = 0;
-        L.p0            = vb;
-        L.p1            = 2 * vb;
-        L.flags         = 3 * vb;
-        L.gather        = up(L.flags + kMaxRanks * sizeof(uint64_t));
-        L.bytes         = up(L.gather + kMaxRanks * 4 * sizeof(double));
-        return L;
-    }
-    size_t o = 0;
-    L.flags  = o;
-    o        = up(o + kMaxRanks * sizeof(uint64_t));
-    L.gather = o;
-    o        = up(o + kMaxRanks * 4 * sizeof(double));
-    const size_t vb = up((size_t)n_ext * 8 + 32); // padded: x-windows round up
-    L.z             = o;
-    L.p0            = o + vb;
-    L.p1            = o + 2 * vb;
-    L.bytes         = o + 3 * vb;
+    const size_t vb = up2((size_t)n_ext * 8 + 32); // + 4 doubles: x-windows round up
+    L.z             = 0;
+    L.p0            = vb;
+    L.p1            = 2 * vb;
+    L.flags         = 3 * vb;
+    L.gather        = up(L.flags + kMaxRanks * sizeof(uint64_t));
+    L.bytes         = up(L.gather + kMaxRanks * 4 * sizeof(double));
     return L;
 }
 
@@ -696,11 +676,7 @@ rvk_status alloc_plan_buffers(rvk_dcg_plan P)
         P->p[1]      = reinterpret_cast<double*>(P->win + L.p1);
         if (P->owns_gather) P->gather = reinterpret_cast<double*>(P->win + L.gather);
     }
-#ifdef DCG_SEPARATE_PROBE // A/B probe: gathered vectors in their own allocations (no PEER)
-    alloc((void**)&P->z, P->n_ext * 8 + 32);
-    alloc((void**)&P->p[0], P->n_ext * 8 + 32);
-    alloc((void**)&P->p[1], P->n_ext * 8 + 32);
-#endif
+
     alloc((void**)&P->dinv, n * 8);
     alloc((void**)&P->r, n * 8);
     alloc((void**)&P->w, n * 8);
