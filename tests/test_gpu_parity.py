@@ -697,3 +697,30 @@ def test_pairwise_x_update_exits_at_both_parities(ctx, graph, monkeypatch):
         ref = O.cg_solve(Ah, b, max_it=max_it, rtol=rtol)
         check_cg(xs["1"][1], xs["1"][0], ref)
     assert seen == {0, 1}  # exits after both parities were exercised
+
+
+@pytest.mark.parametrize("spec", [(2, 5, (2, 2)), (2, 5, (3, 3)), (2, 9, (3, 2)), (3, 7, (2, 2, 2)),
+                                  (3, 27, (2, 2, 2)), (3, 7, (3, 3, 3)), (2, 5, (2, 7)),
+                                  (3, 27, (3, 2, 5))])
+@pytest.mark.parametrize("graph", [True, "while", False])
+def test_tiny_systems_every_path(ctx, spec, graph):
+    """Smallest valid grids (SPEC: >= 2 points per dimension; n = 4 .. 30,
+    odd n for the double2 paths, tiles almost entirely outside the grid for
+    the TMA boxes): CSR and matrix-free plans agree with the oracle."""
+    dim, pts, g = spec
+    Ah = O.build_laplacian(dim, pts, g)
+    b = O.rhs(Ah.n_rows)
+    ref = O.cg_solve(Ah, b, max_it=5)
+    A = rvk.DeviceCsr.laplacian(ctx, dim, pts, g)
+    for op in (A, (dim, pts, g)):
+        plan = rvk.CgPlan(ctx, op, max_it=5, use_graph=graph)
+        x, res = plan.solve_host(b)
+        assert res.iterations == ref.iterations and res.state == ref.status
+        # a tiny system is solved to rounding level within a few iterations:
+        # compare the history while it is above 1e-8 of its start (below that
+        # the entries are rounding noise of either implementation)
+        keep = ref.hist > 1e-8 * ref.hist[0]
+        rel = np.max(np.abs(res.hist[keep] - ref.hist[keep]) / ref.hist[keep])
+        assert rel < 1e-10, rel
+        assert np.linalg.norm(x - ref.x) <= 1e-10 * np.linalg.norm(ref.x)
+        plan.close()
