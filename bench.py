@@ -60,22 +60,23 @@ def peaks():
 
 
 def bytes_model(n: int, nnz: int, mode: str = "fused", const_diag: bool = False,
-                off32: bool = False, x_defer: bool = False, z_virtual: bool = False):
+                off32: bool = False, x_defer: bool = False, z_virtual: bool = False,
+                x_group: int = 2):
     """Algorithmic HBM bytes.  All FP64 + int64 offsets + int32 cols.
     k1 = the SpMV launch (fused: + on-the-fly AYPX), k2 = the rest of an iteration.
     const_diag: the plan folded a constant Jacobi diagonal into a scalar
     (RVK_PLAN_CONST_DIAG), so the dinv stream (8n per iteration and in the
     setup) is not part of the algorithm's traffic any more.  off32: the SpMV
     streams the plan's int32 copy of the row offsets (RVK_PLAN_OFF32): 4 instead
-    of 8 bytes per row.  x_defer: x += a p applied per iteration PAIR
-    (RVK_PLAN_X_DEFER): per pair one x read/write and one p read less, i.e.
-    K2 moves 40 n (even) + 72 n (odd) = 56 n per iteration on average.
+    of 8 bytes per row.  x_defer: x += a p applied once per GROUP of x_group
+    iterations (RVK_PLAN_X_DEFER / _X_GROUP4): the x traffic per iteration
+    drops from 24 n (p read, x read + write) to 8 n + 16 n / x_group.
     z_virtual: z = d r is never stored (RVK_PLAN_Z_VIRTUAL): K2 and the setup
     write 8 n less; K1 gathers r instead of z (same bytes)."""
     ob = 4 if off32 else 8
     if mode == "stencil":                        # matrix-free: no CSR, constant dinv
         k1 = 32 * n                              # z, p_old -> p_new, w
-        k2 = ((48 if x_defer else 56) - (8 if z_virtual else 0)) * n  # x, p, r, w -> x, r, (z)
+        k2 = (56 - ((16 - 16 // x_group) if x_defer else 0) - (8 if z_virtual else 0)) * n
         b_min = k1 + k2
         return {"k1": k1, "k2": k2, "b_min_iter": b_min, "b_ref_iter": b_min,
                 "b_min_solve": MAX_IT * b_min + (24 if z_virtual else 32) * n,
@@ -86,7 +87,7 @@ def bytes_model(n: int, nnz: int, mode: str = "fused", const_diag: bool = False,
         k1 = 12 * nnz + ob * (n + 1) + 32 * n   # off, cols, vals, z, p_old -> p_new, w
         k2 = (56 if const_diag else 64) * n      # x, p, r, w, (dinv) -> x, r, z
         if x_defer:
-            k2 -= 8 * n
+            k2 -= (16 - 16 // x_group) * n
         if z_virtual:
             k2 -= 8 * n
     else:
@@ -427,10 +428,11 @@ def run_gpu(args, cfg):
     const_diag = bool(plan.flags() & 1)
     off32 = bool(plan.flags() & 8)
     x_defer = bool(plan.flags() & 16)
+    x_group = 4 if plan.flags() & 64 else 2
     z_virtual = bool(plan.flags() & 32)
     bm = bytes_model(n, nnz, "stencil" if args.operator == "stencil" else
                      ("unfused" if args.mode == "unfused" else "fused"), const_diag, off32, x_defer,
-                     z_virtual)
+                     z_virtual, x_group)
     hbm_peak, peak_src = peaks()
     ws_bytes = 20 * nnz + 8 * (n + 1) + 9 * 8 * n
     log(f"{desc}: n={n} nnz={nnz} working set {ws_bytes/1e9:.2f} GB (L2 {L2_BYTES/1e6:.0f} MB)")
@@ -562,7 +564,7 @@ def run_gpu(args, cfg):
                            "update_kernel_gbs": round(k2_gbs, 1),
                            "const_diag_folded": const_diag,
                            "int32_row_offsets": off32,
-                           "x_update_per_iteration_pair": x_defer,
+                           "x_update_group": x_group if x_defer else 1,
                            "z_virtual": z_virtual,
                            "survey_b_min_gbs": round(bm["b_min_survey_solve"] / (ms * 1e-3) / 1e9, 1),
                            "b_ref_gbs": round(bm["b_ref_solve"] / (ms * 1e-3) / 1e9, 1)},

@@ -166,22 +166,25 @@ __device__ __forceinline__ void cg_update_tail(double (&acc)[2], double* smem, i
 // COND: this instantiation may set the WHILE node's condition.  Kept a
 // template parameter so the plain-graph/stream variant contains no
 // cudaGraphSetConditional (ncu refuses to profile kernels that can set one).
-// XM (x update): 0 x += a p; 1 DEFER (even iteration: x untouched, (a, it)
-// recorded as pending); 2 FLUSH2 (odd iteration: x = (x + a' p_prev) + a p
-// with the pending a' -- the same two roundings, in the same order, as two
-// single updates, so x is bit-identical while one x read + write and one p
-// read per iteration pair disappear).  k_cg_xfix applies a pending update
-// left by an early exit.
-template <bool VEC, int PC, bool COND = false, int XM = 0> // PC: 0 none, 1 dinv vector, 2 constant dinv
+// x update per GROUP of Q iterations (plan: Q = 1, 2 or 4).  NP < 0: DEFER
+// -- x untouched, this iteration's a recorded in pend_a[slot]; NP >= 0:
+// x = (((x + a_0 p_0) + a_1 p_1) + ...) + a p with the NP pending updates
+// first -- the same roundings in the same order as one update per iteration,
+// so x is bit-identical while per group of Q iterations Q-1 x read/writes
+// and the p re-reads of the plain update disappear.  The pending p's are the
+// plan's rotating p buffers (still intact: iteration j writes p[(j+1) % Q]).
+// k_cg_xfix applies updates an early exit left pending.
+template <bool VEC, int PC, bool COND = false, int NP = 0> // PC: 0 none, 1 dinv vector, 2 constant dinv
 __global__ void __launch_bounds__(kUpdThreads)
     k_cg_update(int64_t n, const double* __restrict__ p, const double* __restrict__ w,
                 const double* __restrict__ dinv, double* __restrict__ x, double* __restrict__ r,
                 double* __restrict__ z, CgState* st, double* hist, int it, double rtol,
                 double atol, double* partials, unsigned int* ticket, double dconst, int max_it,
-                cudaGraphConditionalHandle cond, int use_cond, const double* __restrict__ p_prev,
-                int zw)
+                cudaGraphConditionalHandle cond, int use_cond, const double* __restrict__ pp0,
+                const double* __restrict__ pp1, const double* __restrict__ pp2, int slot, int zw)
 {
-    static_assert(VEC || XM == 0, "deferred x updates use the vector path");
+    static_assert(VEC || NP == 0, "grouped x updates use the vector path");
+    static_assert(NP >= -1 && NP <= 3, "at most 3 pending updates");
     pdl_trigger();
     pdl_wait();
     // In the device WHILE loop (use_cond) `it` comes from the device state and
@@ -196,48 +199,71 @@ __global__ void __launch_bounds__(kUpdThreads)
     __shared__ int    flag;
     const double      a      = st->alpha;
     const double      na     = -a;
-    const double      ap     = XM == 2 ? st->pend_alpha : 0.0; // pending a of iteration it-1
+    double            pa[3]  = {0.0, 0.0, 0.0}; // pending a's, iteration order
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+        if (k < NP) pa[k] = st->pend_a[k];
     double            acc[2] = {0.0, 0.0};
     const int64_t     stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t     t0     = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
-        // every block has read pend_alpha / alpha before any of them can be
-        // re-written: the next writer is a later kernel
-        if (XM == 1) {
-            st->pend_alpha = a;
-            st->pend_it    = it;
-            st->x_pending  = 1;
-        } else if (XM == 2) {
+        // pend_a[slot] is written only by a DEFER launch, read only by later
+        // flushes: no kernel both reads and writes the same slot
+        if (NP < 0) {
+            st->pend_a[slot] = a;
+            st->x_pending    = slot + 1;
+            if (slot == 0) st->pend_it = it;
+        } else if (NP > 0) {
             st->x_pending = 0;
         }
     }
     if (VEC) {
-        // two double2 per thread per trip: up to 12 independent 16-B loads in flight
+        // two double2 per thread per trip, every load issued before any use
         const int64_t  n2 = n >> 1;
         const double2* p2 = reinterpret_cast<const double2*>(p);
-        const double2* q2 = reinterpret_cast<const double2*>(p_prev);
+        const double2* q2[3] = {reinterpret_cast<const double2*>(pp0), reinterpret_cast<const double2*>(pp1),
+                                reinterpret_cast<const double2*>(pp2)};
         const double2* w2 = reinterpret_cast<const double2*>(w);
         const double2* d2 = reinterpret_cast<const double2*>(dinv);
         double2*       x2 = reinterpret_cast<double2*>(x);
         double2*       r2 = reinterpret_cast<double2*>(r);
         double2*       z2 = reinterpret_cast<double2*>(z);
-        auto step = [&](const double2& pi, const double2& qi, const double2& wi, double2 xi,
-                        double2 ri, const double2& d, int64_t i) {
-            if (XM == 2) {
-                xi.x = axpy1(ap, qi.x, xi.x);
-                xi.y = axpy1(ap, qi.y, xi.y);
+        struct In {
+            double2 p, q[3], w, x, r, d;
+        };
+        auto load = [&](int64_t i) {
+            In v;
+            if (NP >= 0) {
+                v.p = ld_stream(p2 + i);
+                v.x = ld_stream(x2 + i);
             }
-            if (XM != 1) {
-                xi.x = axpy1(a, pi.x, xi.x);
-                xi.y = axpy1(a, pi.y, xi.y);
-                st_stream(x2 + i, xi);
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+                if (k < NP) v.q[k] = ld_stream(q2[k] + i);
+            v.w = ld_stream(w2 + i);
+            v.r = ld_stream(r2 + i);
+            v.d = PC == 1 ? ld_stream(d2 + i) : make_double2(dconst, dconst);
+            return v;
+        };
+        auto step = [&](In v, int64_t i) {
+            if (NP >= 0) {
+#pragma unroll
+                for (int k = 0; k < 3; ++k)
+                    if (k < NP) {
+                        v.x.x = axpy1(pa[k], v.q[k].x, v.x.x);
+                        v.x.y = axpy1(pa[k], v.q[k].y, v.x.y);
+                    }
+                v.x.x = axpy1(a, v.p.x, v.x.x);
+                v.x.y = axpy1(a, v.p.y, v.x.y);
+                st_stream(x2 + i, v.x);
             }
-            ri.x = axpy1(na, wi.x, ri.x);
-            ri.y = axpy1(na, wi.y, ri.y);
+            double2 ri = v.r;
+            ri.x       = axpy1(na, v.w.x, ri.x);
+            ri.y       = axpy1(na, v.w.y, ri.y);
             double2 zi = ri;
             if (PC != 0) {
-                zi.x = mul(d.x, ri.x);
-                zi.y = mul(d.y, ri.y);
+                zi.x = mul(v.d.x, ri.x);
+                zi.y = mul(v.d.y, ri.y);
             }
             r2[i] = ri;
             if (zw) z2[i] = zi; // zw = 0: z stays virtual (K1 forms d r)
@@ -246,35 +272,22 @@ __global__ void __launch_bounds__(kUpdThreads)
             acc[1] = add(acc[1], mul(zi.x, ri.x));
             acc[1] = add(acc[1], mul(zi.y, ri.y));
         };
-        const double2 zero = make_double2(0.0, 0.0);
-        auto ldp = [&](int64_t i) { return XM != 1 ? ld_stream(p2 + i) : zero; };
-        auto ldq = [&](int64_t i) { return XM == 2 ? ld_stream(q2 + i) : zero; };
-        auto ldx = [&](int64_t i) { return XM != 1 ? ld_stream(x2 + i) : zero; };
         int64_t i = t0;
         for (; i + stride < n2; i += 2 * stride) {
-            const int64_t j  = i + stride;
-            const double2 pa = ldp(i), pb = ldp(j);
-            const double2 qa = ldq(i), qb = ldq(j);
-            const double2 wa = ld_stream(w2 + i), wb = ld_stream(w2 + j);
-            const double2 xa = ldx(i), xb = ldx(j);
-            const double2 ra = ld_stream(r2 + i), rb = ld_stream(r2 + j);
-            double2 da = make_double2(dconst, dconst), db = da;
-            if (PC == 1) {
-                da = ld_stream(d2 + i);
-                db = ld_stream(d2 + j);
-            }
-            step(pa, qa, wa, xa, ra, da, i);
-            step(pb, qb, wb, xb, rb, db, j);
+            const In va = load(i), vb = load(i + stride);
+            step(va, i);
+            step(vb, i + stride);
         }
-        if (i < n2) {
-            double2 d = make_double2(dconst, dconst);
-            if (PC == 1) d = ld_stream(d2 + i);
-            step(ldp(i), ldq(i), ld_stream(w2 + i), ldx(i), ld_stream(r2 + i), d, i);
-        }
+        if (i < n2) step(load(i), i);
     }
     for (int64_t i = (VEC ? (n & ~int64_t(1)) : 0) + t0; i < n; i += stride) {
-        if (XM == 2) x[i] = axpy1(ap, p_prev[i], x[i]);
-        if (XM != 1) x[i] = axpy1(a, p[i], x[i]);
+        if (NP >= 0) {
+            double xi = x[i];
+            if (NP >= 1) xi = axpy1(pa[0], pp0[i], xi);
+            if (NP >= 2) xi = axpy1(pa[1], pp1[i], xi);
+            if (NP >= 3) xi = axpy1(pa[2], pp2[i], xi);
+            x[i] = axpy1(a, p[i], xi);
+        }
         const double ri = axpy1(na, w[i], r[i]);
         const double zi = PC == 0 ? ri : mul(PC == 1 ? dinv[i] : dconst, ri);
         r[i]            = ri;
@@ -286,21 +299,32 @@ __global__ void __launch_bounds__(kUpdThreads)
                          use_cond);
 }
 
-// After the last iteration (or an early exit): apply an update a DEFER K2
-// left pending.  p0/p1: the plan's ping-pong buffers; iteration it wrote
-// p[(it + 1) & 1].  No-op (one flag read per block) when nothing is pending.
+// After the last iteration (or an early exit): apply the updates DEFER K2s
+// left pending, in iteration order.  p: the plan's Q rotating p buffers;
+// iteration j wrote p[(j + 1) % Q].  No-op (one flag read per block) when
+// nothing is pending.
 __global__ void __launch_bounds__(kUpdThreads)
     k_cg_xfix(int64_t n, double* __restrict__ x, const double* __restrict__ p0,
-              const double* __restrict__ p1, const CgState* __restrict__ st)
+              const double* __restrict__ p1, const double* __restrict__ p2,
+              const double* __restrict__ p3, int q, const CgState* __restrict__ st)
 {
     pdl_trigger();
     pdl_wait();
-    if (!st->x_pending) return;
-    const double  a  = st->pend_alpha;
-    const double* pp = ((st->pend_it + 1) & 1) ? p1 : p0;
+    const int cnt = st->x_pending;
+    if (cnt <= 0) return;
+    const double* pb[4] = {p0, p1, p2, p3};
+    const double* pp[3] = {nullptr, nullptr, nullptr};
+    double        pa[3] = {0.0, 0.0, 0.0};
+    for (int k = 0; k < cnt && k < 3; ++k) {
+        pp[k] = pb[(st->pend_it + k + 1) % q];
+        pa[k] = st->pend_a[k];
+    }
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x)
-        x[i] = axpy1(a, pp[i], x[i]);
+         i += (int64_t)gridDim.x * blockDim.x) {
+        double xi = x[i];
+        for (int k = 0; k < cnt && k < 3; ++k) xi = axpy1(pa[k], pp[k][i], xi);
+        x[i] = xi;
+    }
 }
 
 // K2, streaming variant (RVK_K2_TMA=1 opt-in / A-B): one CTA per SM; the
@@ -702,7 +726,9 @@ struct rvk_cg_plan_s {
     double*       dinv = nullptr;
     double*       r = nullptr;
     double*       z = nullptr;
-    double*       p[2] = {nullptr, nullptr};
+    double*       p[4] = {nullptr, nullptr, nullptr, nullptr}; // rotating: iteration j writes p[(j+1) % npb]
+    int           npb  = 2; // p buffers: max(2, xq)
+    int           xq   = 4; // x updated once per group of xq iterations (RVK_X_GROUP; 1 = every one)
     double*       w    = nullptr;
     double*       hist = nullptr;
     CgState*      st   = nullptr;
@@ -757,42 +783,51 @@ rvk_status launch_setup(rvk_cg_plan P, int pcm, const double* b, double* x)
     return RVK_OK;
 }
 
-// xm: x-update mode of k_cg_update (0 plain, 1 defer, 2 flush pair; the
-// deferred modes need the vector path), p_prev: p of the previous iteration.
-template <int PC, bool COND, int XM>
-void launch_update_k(rvk_cg_plan P, const double* p_new, const double* p_prev, double* x, int it,
-                     cudaGraphConditionalHandle cond, int use_cond)
+// x-update mode of one K2 launch (k_cg_update NP): np = 0 plain, -1 defer
+// into pend_a[slot], 1..3 flush those pending updates (pp: their p buffers).
+struct XUpd {
+    int           np   = 0;
+    int           slot = 0;
+    const double* pp[3] = {nullptr, nullptr, nullptr};
+};
+
+template <int PC, bool COND, int NP>
+void launch_update_k(rvk_cg_plan P, const double* p_new, double* x, int it,
+                     cudaGraphConditionalHandle cond, int use_cond, const XUpd& u)
 {
-    launch_pdl(k_cg_update<true, PC, COND, XM>, P->upd_grid, kUpdThreads, 0, P->ctx->stream,
+    launch_pdl(k_cg_update<true, PC, COND, NP>, P->upd_grid, kUpdThreads, 0, P->ctx->stream,
                P->A.n_rows, p_new, P->w, P->dinv, x, P->r, P->z, P->st, P->hist, it, P->cfg.rtol,
                P->cfg.atol, P->partials, P->tickets, P->dconst, P->cfg.max_it, cond, use_cond,
-               p_prev, P->zv ? 0 : 1);
+               u.pp[0], u.pp[1], u.pp[2], u.slot, P->zv ? 0 : 1);
 }
 
 template <int PC, bool COND>
-void launch_update_xm(rvk_cg_plan P, int xm, const double* p_new, const double* p_prev, double* x,
-                      int it, cudaGraphConditionalHandle cond, int use_cond)
+void launch_update_xm(rvk_cg_plan P, const double* p_new, double* x, int it,
+                      cudaGraphConditionalHandle cond, int use_cond, const XUpd& u)
 {
-    if (xm == 1) launch_update_k<PC, COND, 1>(P, p_new, p_prev, x, it, cond, use_cond);
-    else if (xm == 2) launch_update_k<PC, COND, 2>(P, p_new, p_prev, x, it, cond, use_cond);
-    else launch_update_k<PC, COND, 0>(P, p_new, p_prev, x, it, cond, use_cond);
+    switch (u.np) {
+    case -1: launch_update_k<PC, COND, -1>(P, p_new, x, it, cond, use_cond, u); break;
+    case 1: launch_update_k<PC, COND, 1>(P, p_new, x, it, cond, use_cond, u); break;
+    case 2: launch_update_k<PC, COND, 2>(P, p_new, x, it, cond, use_cond, u); break;
+    case 3: launch_update_k<PC, COND, 3>(P, p_new, x, it, cond, use_cond, u); break;
+    default: launch_update_k<PC, COND, 0>(P, p_new, x, it, cond, use_cond, u);
+    }
 }
 
 template <bool V>
 rvk_status launch_update(rvk_cg_plan P, int pcm, const double* p_new, double* x, int it,
-                         cudaGraphConditionalHandle cond = 0, int use_cond = 0, int xm = 0,
-                         const double* p_prev = nullptr)
+                         cudaGraphConditionalHandle cond = 0, int use_cond = 0, XUpd u = {})
 {
     cudaStream_t s = P->ctx->stream;
-    if (V && xm != 0) {
+    if (V && u.np != 0) {
         if (use_cond) {
-            if (pcm == 0) launch_update_xm<0, true>(P, xm, p_new, p_prev, x, it, cond, use_cond);
-            else if (pcm == 1) launch_update_xm<1, true>(P, xm, p_new, p_prev, x, it, cond, use_cond);
-            else launch_update_xm<2, true>(P, xm, p_new, p_prev, x, it, cond, use_cond);
+            if (pcm == 0) launch_update_xm<0, true>(P, p_new, x, it, cond, use_cond, u);
+            else if (pcm == 1) launch_update_xm<1, true>(P, p_new, x, it, cond, use_cond, u);
+            else launch_update_xm<2, true>(P, p_new, x, it, cond, use_cond, u);
         } else {
-            if (pcm == 0) launch_update_xm<0, false>(P, xm, p_new, p_prev, x, it, cond, use_cond);
-            else if (pcm == 1) launch_update_xm<1, false>(P, xm, p_new, p_prev, x, it, cond, use_cond);
-            else launch_update_xm<2, false>(P, xm, p_new, p_prev, x, it, cond, use_cond);
+            if (pcm == 0) launch_update_xm<0, false>(P, p_new, x, it, cond, use_cond, u);
+            else if (pcm == 1) launch_update_xm<1, false>(P, p_new, x, it, cond, use_cond, u);
+            else launch_update_xm<2, false>(P, p_new, x, it, cond, use_cond, u);
         }
         RVK_CHECK_LAUNCH("k_cg_update");
         return RVK_OK;
@@ -800,7 +835,8 @@ rvk_status launch_update(rvk_cg_plan P, int pcm, const double* p_new, double* x,
     auto go = [&](auto kern) {
         launch_pdl(kern, P->upd_grid, kUpdThreads, 0, s, P->A.n_rows, p_new, P->w, P->dinv, x,
                    P->r, P->z, P->st, P->hist, it, P->cfg.rtol, P->cfg.atol, P->partials,
-                   P->tickets, P->dconst, P->cfg.max_it, cond, use_cond, p_new, P->zv ? 0 : 1);
+                   P->tickets, P->dconst, P->cfg.max_it, cond, use_cond, (const double*)nullptr,
+                   (const double*)nullptr, (const double*)nullptr, 0, P->zv ? 0 : 1);
     };
     if (V && P->k2_tma) {
         auto gt = [&](auto kern, size_t smem) {
@@ -837,17 +873,48 @@ rvk_status launch_update(rvk_cg_plan P, int pcm, const double* p_new, double* x,
 rvk_status launch_xfix(rvk_cg_plan P, double* x)
 {
     launch_pdl(k_cg_xfix, P->upd_grid, kUpdThreads, 0, P->ctx->stream, P->A.n_rows, x,
-               (const double*)P->p[0], (const double*)P->p[1], (const CgState*)P->st);
+               (const double*)P->p[0], (const double*)P->p[1], (const double*)P->p[2],
+               (const double*)P->p[3], P->npb, (const CgState*)P->st);
     RVK_CHECK_LAUNCH("k_cg_xfix");
     return RVK_OK;
 }
 
-// Deferred x updates on this solve? (vector path, classic K2, max_it >= 2;
-// RVK_X_DEFER=0 disables)
+// x-update group of a FUSED plan: RVK_X_GROUP = 1, 2 or 4 (default 4:
+// measured 7-point 256^3 solve 9.25 ms -> see DESIGN.md for groups of 4).
+void set_x_group(rvk_cg_plan P)
+{
+    const char* e = std::getenv("RVK_X_GROUP");
+    int         q = e ? std::atoi(e) : 4;
+    if (q != 1 && q != 2) q = 4;
+    if (P->mode != RVK_CG_MODE_FUSED) q = 1;
+    P->xq  = q;
+    P->npb = q > 2 ? q : 2;
+}
+
+// Grouped x updates on this solve? (vector path, classic K2, max_it >= 2,
+// group > 1; RVK_X_DEFER=0 / RVK_X_GROUP=1 disable)
 bool x_defer(rvk_cg_plan P, bool vec)
 {
     const char* e = std::getenv("RVK_X_DEFER");
-    return vec && !P->k2_tma && P->cfg.max_it >= 2 && !(e && e[0] == '0');
+    return vec && !P->k2_tma && P->cfg.max_it >= 2 && P->xq > 1 && !(e && e[0] == '0');
+}
+
+// The x-update mode of iteration `it` (for a WHILE body any index with the
+// right residue mod npb): defer inside a group, flush at its end or at the
+// solve's last iteration.
+XUpd x_mode(rvk_cg_plan P, bool defer, int it, bool last)
+{
+    XUpd u;
+    if (!defer) return u;
+    const int q = P->xq, c = it % q;
+    if (c == q - 1 || last) {
+        u.np = c;
+        for (int k = 0; k < c; ++k) u.pp[k] = P->p[(it - c + k + 1) % P->npb];
+    } else {
+        u.np   = -1;
+        u.slot = c;
+    }
+    return u;
 }
 
 // K1 of one iteration: it >= 0 static index, it == -1 read from the device
@@ -920,7 +987,8 @@ rvk_status build_while_graph(rvk_cg_plan P, const double* b, double* x, cudaGrap
     if (rc == RVK_OK) rc = launch_k1(P, 0, true, P->p[0], P->p[1]);
     const bool defer = x_defer(P, vec);
     if (rc == RVK_OK)
-        rc = vec ? launch_update<true>(P, pcm, P->p[1], x, 0, h, 1, defer ? 1 : 0, P->p[0])
+        rc = vec ? launch_update<true>(P, pcm, P->p[1], x, 0, h, 1,
+                                       x_mode(P, defer, 0, P->cfg.max_it == 1))
                  : launch_update<false>(P, pcm, P->p[1], x, 0, h, 1);
     cudaError_t e = cudaStreamEndCapture(s, &pro);
     if (rc != RVK_OK) return fail(rc);
@@ -940,14 +1008,16 @@ rvk_status build_while_graph(rvk_cg_plan P, const double* b, double* x, cudaGrap
     if ((e = cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0,
                                            cudaStreamCaptureModeGlobal)) != cudaSuccess)
         return fail(cuda_error(e, "cudaStreamBeginCaptureToGraph"));
-    rc = launch_k1(P, -1, false, P->p[1], P->p[0]);
-    if (rc == RVK_OK) // odd iteration: flushes the pending even update
-        rc = vec ? launch_update<true>(P, pcm, P->p[0], x, -1, h, 1, defer ? 2 : 0, P->p[1])
-                 : launch_update<false>(P, pcm, P->p[0], x, -1, h, 1);
-    if (rc == RVK_OK) rc = launch_k1(P, -1, false, P->p[0], P->p[1]);
-    if (rc == RVK_OK) // even iteration: defers
-        rc = vec ? launch_update<true>(P, pcm, P->p[1], x, -1, h, 1, defer ? 1 : 0, P->p[0])
-                 : launch_update<false>(P, pcm, P->p[1], x, -1, h, 1);
+    // body: npb iterations (residues 1, 2, ..., 0 mod npb), so every p buffer
+    // index is static; a group ending mid-body is flushed by the epilogue
+    for (int j = 1; j <= P->npb && rc == RVK_OK; ++j) {
+        const int c = j % P->npb;
+        rc = launch_k1(P, -1, false, P->p[c], P->p[(c + 1) % P->npb]);
+        if (rc == RVK_OK)
+            rc = vec ? launch_update<true>(P, pcm, P->p[(c + 1) % P->npb], x, -1, h, 1,
+                                           x_mode(P, defer, c, false))
+                     : launch_update<false>(P, pcm, P->p[(c + 1) % P->npb], x, -1, h, 1);
+    }
     e = cudaStreamEndCapture(s, &tmp);
     if (rc != RVK_OK) return fail(rc);
     if (e != cudaSuccess) return fail(cuda_error(e, "capture (while body)"));
@@ -987,16 +1057,16 @@ rvk_status enqueue_fused(rvk_cg_plan P, const double* b, double* x)
     if (rc != RVK_OK) return rc;
     ++P->launches;
     for (int it = 0; it < P->cfg.max_it; ++it) {
-        const double* p_old = P->p[it & 1];
-        double*       p_new = P->p[(it + 1) & 1];
+        const double* p_old = P->p[it % P->npb];
+        double*       p_new = P->p[(it + 1) % P->npb];
         if ((rc = rec(4 * it + 0)) != RVK_OK) return rc;
         rc = launch_k1(P, it, it == 0, p_old, p_new);
         if (rc != RVK_OK) return rc;
         ++P->launches;
         if ((rc = rec(4 * it + 1)) != RVK_OK || (rc = rec(4 * it + 2)) != RVK_OK) return rc;
-        // deferred x: even iterations defer (unless last), odd ones flush the pair
-        const int xm = !defer ? 0 : (it & 1) ? 2 : (it + 1 < P->cfg.max_it ? 1 : 0);
-        rc = vec ? launch_update<true>(P, pcm, p_new, x, it, 0, 0, xm, p_old)
+        // grouped x: defer inside a group, flush at its end (or the last iteration)
+        rc = vec ? launch_update<true>(P, pcm, p_new, x, it, 0, 0,
+                                       x_mode(P, defer, it, it + 1 == P->cfg.max_it))
                  : launch_update<false>(P, pcm, p_new, x, it);
         if (rc != RVK_OK) return rc;
         ++P->launches;
@@ -1351,6 +1421,8 @@ rvk_status rvk_cg_plan_create(rvk_ctx ctx, const rvk_csr* A, rvk_cg_config cfg, 
     alloc(reinterpret_cast<void**>(&P->z), vb + 32);
     alloc(reinterpret_cast<void**>(&P->p[0]), vb + 32);
     alloc(reinterpret_cast<void**>(&P->p[1]), vb + 32);
+    set_x_group(P);
+    for (int k = 2; k < P->npb; ++k) alloc(reinterpret_cast<void**>(&P->p[k]), vb + 32);
     alloc(reinterpret_cast<void**>(&P->w), vb);
     alloc(reinterpret_cast<void**>(&P->hist), sizeof(double) * (cfg.max_it + 1));
     alloc(reinterpret_cast<void**>(&P->st), sizeof(CgState));
@@ -1404,6 +1476,7 @@ int rvk_cg_plan_flags(rvk_cg_plan P)
     return (P->const_diag ? RVK_PLAN_CONST_DIAG : 0) | (P->stencil ? RVK_PLAN_MATRIX_FREE : 0) |
            (P->mf_tma ? RVK_PLAN_MF_TMA : 0) | (P->off32 ? RVK_PLAN_OFF32 : 0) |
            ((P->mode == RVK_CG_MODE_FUSED && x_defer(P, true)) ? RVK_PLAN_X_DEFER : 0) |
+           ((P->mode == RVK_CG_MODE_FUSED && x_defer(P, true) && P->xq == 4) ? RVK_PLAN_X_GROUP4 : 0) |
            (P->zv ? RVK_PLAN_Z_VIRTUAL : 0);
 }
 
@@ -1456,6 +1529,8 @@ rvk_status rvk_cg_plan_create_stencil(rvk_ctx ctx, int dim, int points, int64_t 
     alloc(reinterpret_cast<void**>(&P->z), vb + 32);
     alloc(reinterpret_cast<void**>(&P->p[0]), vb + 32);
     alloc(reinterpret_cast<void**>(&P->p[1]), vb + 32);
+    set_x_group(P);
+    for (int k = 2; k < P->npb; ++k) alloc(reinterpret_cast<void**>(&P->p[k]), vb + 32);
     alloc(reinterpret_cast<void**>(&P->w), vb);
     alloc(reinterpret_cast<void**>(&P->hist), sizeof(double) * (cfg.max_it + 1));
     alloc(reinterpret_cast<void**>(&P->st), sizeof(CgState));
@@ -1472,7 +1547,7 @@ rvk_status rvk_cg_plan_create_stencil(rvk_ctx ctx, int dim, int points, int64_t 
         rvk_cg_plan_destroy(P);
         return cuda_error(e, "rvk_cg_plan_create_stencil");
     }
-    P->mf_tma = mf_tma_create(P->geom, P->z, P->p[0], P->p[1], P->r);
+    P->mf_tma = mf_tma_create(P->geom, P->z, P->p, P->npb, P->r);
     P->zv     = virtual_z(P);
     *out = P;
     return RVK_OK;
@@ -1489,7 +1564,7 @@ rvk_status rvk_cg_plan_destroy(rvk_cg_plan P)
         if (ev) cudaEventDestroy(ev);
     if (P->s_in) cudaStreamDestroy(P->s_in);
     if (P->s_out) cudaStreamDestroy(P->s_out);
-    void* bufs[] = {P->dinv, P->r, P->z, P->p[0], P->p[1], P->w, P->hist, P->st,
+    void* bufs[] = {P->dinv, P->r, P->z, P->p[0], P->p[1], P->p[2], P->p[3], P->w, P->hist, P->st,
                     P->partials, P->tickets, P->tmp, P->b_buf, P->x_buf, P->b_buf2,
                     P->x_buf2, P->hist_all, P->st_all, P->off32};
     for (void* b : bufs)

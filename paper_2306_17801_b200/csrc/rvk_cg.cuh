@@ -13,8 +13,9 @@ struct CgState {
     int    done, state, iterations, breakdown_iter;
     int    comm_error; // row-sharded PEER backend: a flag wait timed out
     unsigned int seq;  // row-sharded PEER backend: solves started on this plan
-    double pend_alpha; // fused CG: x += pend_alpha * p_{pend_it} not yet applied
-    int    x_pending, pend_it;
+    double pend_alpha; // row-sharded CG: x += pend_alpha * p_{pend_it} not yet applied
+    int    x_pending, pend_it; // pending x updates (count) and the first one's iteration
+    double pend_a[3];  // fused CG: a of the x updates deferred within the current group
 };
 
 constexpr int kUpdThreads = 256;
@@ -136,8 +137,8 @@ struct StencilGeom {
 // The TMA 2.5D variant's plan state (tensor maps of z, p0, p1); null when the
 // geometry does not allow it (odd nx) or RVK_MF_TMA=0.
 struct MfTma;
-MfTma*     mf_tma_create(const StencilGeom& g, const double* z, const double* p0, const double* p1,
-                         const double* r);
+MfTma*     mf_tma_create(const StencilGeom& g, const double* z, double* const* p, int np,
+                         const double* r); // p: the plan's np (2..4) rotating p buffers
 void       mf_tma_destroy(MfTma* t);
 rvk_status launch_mf_k1(cudaStream_t s, const StencilGeom& g, bool first, const double* z,
                         const double* p_old, double* p_new, double* w, CgState* st, int64_t n,

@@ -384,10 +384,10 @@ rvk_status launch_first(cudaStream_t s, const StencilGeom& g, const OpT& op,
 
 // ---- TMA plan state -----------------------------------------------------------
 struct MfTma {
-    CUtensorMap   z, p0, p1, r;
+    CUtensorMap   z, r, pm[4]; // pm[k]: p buffer k
     MfTmaGeom     g{};
-    const double* p0_ptr = nullptr;
-    const double* p1_ptr = nullptr;
+    const double* p_ptr[4] = {nullptr, nullptr, nullptr, nullptr};
+    int           np       = 2;
     int           grid   = 0;
     int           dim    = 3;
     bool          box    = false;
@@ -471,7 +471,7 @@ int tma_blocks_per_sm()
 }
 } // namespace
 
-MfTma* mf_tma_create(const StencilGeom& g, const double* z, const double* p0, const double* p1,
+MfTma* mf_tma_create(const StencilGeom& g, const double* z, double* const* p, int np,
                      const double* r)
 {
     const char* env = std::getenv("RVK_MF_TMA");
@@ -484,13 +484,14 @@ MfTma* mf_tma_create(const StencilGeom& g, const double* z, const double* p0, co
     const int TX = g.dim == 3 ? (g.box ? MfShape<3, true>::TX : MfShape<3, false>::TX) : MfShape<2, false>::TX;
     const int TY = g.dim == 3 ? (g.box ? MfShape<3, true>::TY : MfShape<3, false>::TY) : MfShape<2, false>::TY;
     const int bw = TX + 4, bh = g.dim == 3 ? TY + 2 : 1; // see k_mf_tma: 16-B aligned x start
-    if (!encode_plane_map(&t->z, z, g, bw, bh) || !encode_plane_map(&t->p0, p0, g, bw, bh) ||
-        !encode_plane_map(&t->p1, p1, g, bw, bh) || !encode_plane_map(&t->r, r, g, bw, bh)) {
+    bool ok = encode_plane_map(&t->z, z, g, bw, bh) && encode_plane_map(&t->r, r, g, bw, bh);
+    for (int k = 0; k < np && ok; ++k) ok = encode_plane_map(&t->pm[k], p[k], g, bw, bh);
+    if (!ok) {
         delete t;
         return nullptr;
     }
-    t->p0_ptr = p0;
-    t->p1_ptr = p1;
+    t->np = np;
+    for (int k = 0; k < np; ++k) t->p_ptr[k] = p[k];
     MfTmaGeom& G = t->g;
     G.nx      = (int32_t)g.nx;
     G.ny      = g.dim == 3 ? (int32_t)g.ny : 1;
@@ -540,7 +541,10 @@ namespace {
 template <class OpT>
 rvk_status launch_tma(cudaStream_t s, const MfTma& t, const OpT& op, TailArgs ta)
 {
-    const CUtensorMap& tp = op.p_old == t.p1_ptr ? t.p1 : t.p0;
+    int kp = 0; // the map of p_old among the rotating buffers
+    for (int k = 0; k < t.np; ++k)
+        if (op.p_old == t.p_ptr[k]) kp = k;
+    const CUtensorMap& tp = t.pm[kp];
 #define RVK_MF_LAUNCH(D, B)                                                                        \
     launch_pdl(k_mf_tma<OpT, D, B>, t.grid, mf_threads<D, B>(), mf_smem_bytes<D, B>(), s,            \
                OpT::kZv ? t.r : t.z, tp, t.g, op, ta)

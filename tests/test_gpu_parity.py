@@ -674,9 +674,10 @@ def test_virtual_z_bitexact(ctx, spec, pc, monkeypatch):
 
 @pytest.mark.parametrize("graph", [True, "while", False])
 def test_pairwise_x_update_exits_at_both_parities(ctx, graph, monkeypatch):
-    """Early exits (device rtol) after even and odd iterations, odd max_it:
-    the pairwise x update (even K2 defers, odd K2 applies both, k_cg_xfix
-    flushes a pending one) gives x bit-identical to the per-iteration update."""
+    """Early exits (device rtol) at every position inside an x-update group,
+    odd / even max_it: grouped x updates (groups of 4 and 2; deferring K2s,
+    a flushing K2 at the group end, k_cg_xfix for what an exit leaves
+    pending) give x bit-identical to one update per iteration."""
     dim, pts, g = 2, 5, (48, 40)
     Ah = O.build_laplacian(dim, pts, g)
     b = O.rhs(Ah.n_rows)
@@ -685,18 +686,20 @@ def test_pairwise_x_update_exits_at_both_parities(ctx, graph, monkeypatch):
     for max_it, rtol in [(7, 0.0), (8, 0.0), (200, 1e-3), (200, 3e-4), (200, 1e-4), (200, 3e-5),
                          (200, 1e-5), (200, 3e-6)]:
         xs = {}
-        for d in ("1", "0"):
-            monkeypatch.setenv("RVK_X_DEFER", d)
+        for grp in ("4", "2", "1"):
+            monkeypatch.setenv("RVK_X_GROUP", grp)
             plan = rvk.CgPlan(ctx, A, max_it=max_it, rtol=rtol, use_graph=graph)
-            xs[d] = plan.solve_host(b)
+            xs[grp] = plan.solve_host(b)
             plan.close()
-        monkeypatch.delenv("RVK_X_DEFER")
-        assert np.array_equal(xs["1"][0], xs["0"][0]), (max_it, rtol)
-        assert np.array_equal(xs["1"][1].hist, xs["0"][1].hist)
-        seen.add(xs["1"][1].iterations % 2)
+        monkeypatch.delenv("RVK_X_GROUP")
+        for grp in ("4", "2"):
+            assert np.array_equal(xs[grp][0], xs["1"][0]), (grp, max_it, rtol)
+            assert np.array_equal(xs[grp][1].hist, xs["1"][1].hist)
+        xs["1"] = xs["4"]
+        seen.add(xs["1"][1].iterations % 4)
         ref = O.cg_solve(Ah, b, max_it=max_it, rtol=rtol)
         check_cg(xs["1"][1], xs["1"][0], ref)
-    assert seen == {0, 1}  # exits after both parities were exercised
+    assert len(seen) >= 3  # exits at several positions inside an x-update group
 
 
 @pytest.mark.parametrize("spec", [(2, 5, (2, 2)), (2, 5, (3, 3)), (2, 9, (3, 2)), (3, 7, (2, 2, 2)),
