@@ -69,15 +69,20 @@ def bytes_model(n: int, nnz: int, mode: str = "fused", const_diag: bool = False,
     setup) is not part of the algorithm's traffic any more.  off32: the SpMV
     streams the plan's int32 copy of the row offsets (RVK_PLAN_OFF32): 4 instead
     of 8 bytes per row.  x_defer: x += a p applied once per GROUP of x_group
-    iterations (RVK_PLAN_X_DEFER / _X_GROUP4): the x traffic per iteration
-    drops from 24 n (p read, x read + write) to 8 n + 16 n / x_group.
+    iterations (RVK_PLAN_X_DEFER / _X_GROUP4 / _X_SOLVE = the whole solve):
+    the x traffic per iteration drops from 24 n (p read, x read + write) to
+    8 n + 16 n / x_group.
     z_virtual: z = d r is never stored (RVK_PLAN_Z_VIRTUAL): K2 and the setup
     write 8 n less; K1 gathers r instead of z (same bytes)."""
     ob = 4 if off32 else 8
+    # x_group > 4 (the whole solve): K2 never touches x; one k_cg_xfix pass at
+    # the end reads x and the x_group p's and writes x -- counted per solve
+    x_pass = (16 * n + 8 * n * x_group) if (x_defer and x_group > 4) else 0
+    x_cut = (24 * n if x_pass else 16 * n - 16 * n // x_group) if x_defer else 0
     if mode == "stencil":                        # matrix-free: no CSR, constant dinv
         k1 = 32 * n                              # z, p_old -> p_new, w
-        k2 = (56 - ((16 - 16 // x_group) if x_defer else 0) - (8 if z_virtual else 0)) * n
-        b_min = k1 + k2
+        k2 = 56 * n - x_cut - (8 * n if z_virtual else 0)
+        b_min = k1 + k2 + x_pass // MAX_IT
         return {"k1": k1, "k2": k2, "b_min_iter": b_min, "b_ref_iter": b_min,
                 "b_min_solve": MAX_IT * b_min + (24 if z_virtual else 32) * n,
                 "b_ref_solve": MAX_IT * b_min + (24 if z_virtual else 32) * n,
@@ -86,14 +91,13 @@ def bytes_model(n: int, nnz: int, mode: str = "fused", const_diag: bool = False,
     if mode == "fused":
         k1 = 12 * nnz + ob * (n + 1) + 32 * n   # off, cols, vals, z, p_old -> p_new, w
         k2 = (56 if const_diag else 64) * n      # x, p, r, w, (dinv) -> x, r, z
-        if x_defer:
-            k2 -= (16 - 16 // x_group) * n
+        k2 -= x_cut
         if z_virtual:
             k2 -= 8 * n
     else:
         k1 = 12 * nnz + ob * (n + 1) + 16 * n   # off, cols, vals, p -> w
         k2 = 136 * n                             # aypx 24, dot 16, 2 axpy 48, jacobi 24, norm 8, dot 16
-    b_min = k1 + k2                              # = 12 nnz + 8 (n+1) + 96 n  (88 n const_diag)
+    b_min = k1 + k2 + (x_pass // MAX_IT if mode == "fused" else 0)  # 12 nnz + 8 (n+1) + 96 n plain
     b_ref = 12 * nnz + 8 * (n + 1) + 152 * n     # reference's unfused sequence
     setup = (56 if (const_diag and mode == "fused") else 64) * n - (8 * n if z_virtual else 0)
     survey = MAX_IT * (12 * nnz + 8 * (n + 1) + 96 * n) + 64 * n  # SURVEY.md 8d B_min as stated
@@ -428,7 +432,7 @@ def run_gpu(args, cfg):
     const_diag = bool(plan.flags() & 1)
     off32 = bool(plan.flags() & 8)
     x_defer = bool(plan.flags() & 16)
-    x_group = 4 if plan.flags() & 64 else 2
+    x_group = MAX_IT if plan.flags() & 128 else (4 if plan.flags() & 64 else 2)
     z_virtual = bool(plan.flags() & 32)
     bm = bytes_model(n, nnz, "stencil" if args.operator == "stencil" else
                      ("unfused" if args.mode == "unfused" else "fused"), const_diag, off32, x_defer,

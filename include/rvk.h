@@ -244,6 +244,9 @@ rvk_status rvk_cg_solve_host_many(rvk_cg_plan plan, int nrhs, const double* cons
 #define RVK_PLAN_X_DEFER    16  /* fused solve applies x += a p for a GROUP of iterations in one
                                    pass (16-B aligned b / x; bit-identical x; RVK_X_DEFER=0 disables) */
 #define RVK_PLAN_X_GROUP4   64  /* ... groups of 4 iterations (else pairs; RVK_X_GROUP=2|4)      */
+#define RVK_PLAN_X_SOLVE    128 /* ... one group = the whole fixed-iteration solve: x is written
+                                   once, at the end (CSR plans, max_it <= 32, p buffers fit;
+                                   RVK_X_GROUP=solve forces, =4 opts out)                     */
 #define RVK_PLAN_Z_VIRTUAL  32  /* fused solve never stores z = d r (constant diagonal / no PC):
                                    the SpMV gathers r and forms d r (bit-identical; RVK_ZV=0) */
 int        rvk_cg_plan_flags(rvk_cg_plan plan);

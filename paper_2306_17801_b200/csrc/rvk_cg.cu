@@ -38,6 +38,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <vector>
 
 namespace rvk {
@@ -300,30 +301,57 @@ __global__ void __launch_bounds__(kUpdThreads)
 }
 
 // After the last iteration (or an early exit): apply the updates DEFER K2s
-// left pending, in iteration order.  p: the plan's Q rotating p buffers;
-// iteration j wrote p[(j + 1) % Q].  No-op (one flag read per block) when
-// nothing is pending.
+// left pending, in iteration order: x = ((x + a_0 p_0) + a_1 p_1) + ... .
+// pb: the q rotating p buffers; iteration j wrote pb[(j + 1) % q].  With the
+// whole-solve group (q = max_it) this is the solve's only x pass: it streams
+// the max_it p's once (4 per trip, all loads issued before the adds).  No-op
+// (one flag read per block) when nothing is pending.
+struct XBufs {
+    const double* p[kMaxXq];
+};
+
 __global__ void __launch_bounds__(kUpdThreads)
-    k_cg_xfix(int64_t n, double* __restrict__ x, const double* __restrict__ p0,
-              const double* __restrict__ p1, const double* __restrict__ p2,
-              const double* __restrict__ p3, int q, const CgState* __restrict__ st)
+    k_cg_xfix(int64_t n, double* __restrict__ x, XBufs pb, int q, const CgState* __restrict__ st)
 {
     pdl_trigger();
     pdl_wait();
     const int cnt = st->x_pending;
     if (cnt <= 0) return;
-    const double* pb[4] = {p0, p1, p2, p3};
-    const double* pp[3] = {nullptr, nullptr, nullptr};
-    double        pa[3] = {0.0, 0.0, 0.0};
-    for (int k = 0; k < cnt && k < 3; ++k) {
-        pp[k] = pb[(st->pend_it + k + 1) % q];
-        pa[k] = st->pend_a[k];
+    __shared__ const double* sp[kMaxXq];
+    __shared__ double        sa[kMaxXq];
+    if (threadIdx.x < cnt) {
+        sp[threadIdx.x] = pb.p[(st->pend_it + threadIdx.x + 1) % q];
+        sa[threadIdx.x] = st->pend_a[threadIdx.x];
     }
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        double xi = x[i];
-        for (int k = 0; k < cnt && k < 3; ++k) xi = axpy1(pa[k], pp[k][i], xi);
-        x[i] = xi;
+    __syncthreads();
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t t0     = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t n2     = n >> 1; // deferral implies 16-B aligned x and p
+    double2*      x2     = reinterpret_cast<double2*>(x);
+    for (int64_t i = t0; i < n2; i += stride) {
+        double2 xi = ld_stream(x2 + i);
+        int     k  = 0;
+        for (; k + 4 <= cnt; k += 4) {
+            double2 v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v[u] = ld_stream(reinterpret_cast<const double2*>(sp[k + u]) + i);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                xi.x = axpy1(sa[k + u], v[u].x, xi.x);
+                xi.y = axpy1(sa[k + u], v[u].y, xi.y);
+            }
+        }
+        for (; k < cnt; ++k) {
+            const double2 v = ld_stream(reinterpret_cast<const double2*>(sp[k]) + i);
+            xi.x            = axpy1(sa[k], v.x, xi.x);
+            xi.y            = axpy1(sa[k], v.y, xi.y);
+        }
+        st_stream(x2 + i, xi);
+    }
+    if ((n & 1) && t0 == 0) {
+        double xi = x[n - 1];
+        for (int k = 0; k < cnt; ++k) xi = axpy1(sa[k], sp[k][n - 1], xi);
+        x[n - 1] = xi;
     }
 }
 
@@ -726,9 +754,10 @@ struct rvk_cg_plan_s {
     double*       dinv = nullptr;
     double*       r = nullptr;
     double*       z = nullptr;
-    double*       p[4] = {nullptr, nullptr, nullptr, nullptr}; // rotating: iteration j writes p[(j+1) % npb]
+    double*       p[kMaxXq] = {}; // rotating: iteration j writes p[(j+1) % npb]
     int           npb  = 2; // p buffers: max(2, xq)
-    int           xq   = 4; // x updated once per group of xq iterations (RVK_X_GROUP; 1 = every one)
+    int           xq   = 4; // x updated once per group of xq iterations (RVK_X_GROUP; 1 = every one;
+                            // max_it = the whole solve, one x pass at the end)
     double*       w    = nullptr;
     double*       hist = nullptr;
     CgState*      st   = nullptr;
@@ -870,26 +899,45 @@ rvk_status launch_update(rvk_cg_plan P, int pcm, const double* p_new, double* x,
     return RVK_OK;
 }
 
-rvk_status launch_xfix(rvk_cg_plan P, double* x)
+rvk_status launch_xfix(rvk_cg_plan P, double* x, int npb)
 {
-    launch_pdl(k_cg_xfix, P->upd_grid, kUpdThreads, 0, P->ctx->stream, P->A.n_rows, x,
-               (const double*)P->p[0], (const double*)P->p[1], (const double*)P->p[2],
-               (const double*)P->p[3], P->npb, (const CgState*)P->st);
+    XBufs pb{};
+    for (int k = 0; k < npb; ++k) pb.p[k] = P->p[k];
+    launch_pdl(k_cg_xfix, P->upd_grid, kUpdThreads, 0, P->ctx->stream, P->A.n_rows, x, pb, npb,
+               (const CgState*)P->st);
     RVK_CHECK_LAUNCH("k_cg_xfix");
     return RVK_OK;
 }
 
-// x-update group of a FUSED plan: RVK_X_GROUP = 1, 2 or 4 (default 4:
-// measured 7-point 256^3 solve 9.25 ms -> see DESIGN.md for groups of 4).
+// x-update group of a FUSED plan.  Default: the whole solve when it fits
+// (CSR operator, 5 <= max_it <= kMaxXq, max_it p buffers in free HBM): every
+// K2 defers and k_cg_xfix applies the max_it updates in one pass at the end
+// -- 16 n + 8 n max_it bytes per solve instead of 24 n per iteration.  Else
+// groups of 4 (the WHILE-loop graph always uses groups of <= 4: its p ring is
+// static).  RVK_X_GROUP = 1 | 2 | 4 | solve forces one (measured on B200,
+// 7-point 256^3: pairs 9.25 -> groups of 4 8.58 ms).
 void set_x_group(rvk_cg_plan P)
 {
-    const char* e = std::getenv("RVK_X_GROUP");
-    int         q = e ? std::atoi(e) : 4;
-    if (q != 1 && q != 2) q = 4;
+    const char* e  = std::getenv("RVK_X_GROUP");
+    const int   mi = P->cfg.max_it;
+    int         q  = 4;
+    if (e && (e[0] == '1' || e[0] == '2') && !e[1]) q = e[0] - '0';
+    const bool force_solve = e && std::strcmp(e, "solve") == 0;
+    if ((!e || force_solve) && !P->stencil && mi >= 5 && mi <= kMaxXq) {
+        const size_t vb = (size_t)P->A.n_rows * sizeof(double) + 32;
+        size_t       fr = 0, tot = 0;
+        const bool   fits = cudaMemGetInfo(&fr, &tot) == cudaSuccess &&
+                          fr > (size_t)(mi - 2) * vb + 8 * vb + (size_t(2) << 30);
+        if (fits || force_solve) q = mi;
+    }
     if (P->mode != RVK_CG_MODE_FUSED) q = 1;
     P->xq  = q;
     P->npb = q > 2 ? q : 2;
 }
+
+// Group and p-ring size of the device WHILE-loop graph (body = one ring turn)
+int while_group(rvk_cg_plan P) { return P->xq < 4 ? P->xq : 4; }
+int while_ring(rvk_cg_plan P) { return while_group(P) > 2 ? while_group(P) : 2; }
 
 // Grouped x updates on this solve? (vector path, classic K2, max_it >= 2,
 // group > 1; RVK_X_DEFER=0 / RVK_X_GROUP=1 disable)
@@ -902,14 +950,15 @@ bool x_defer(rvk_cg_plan P, bool vec)
 // The x-update mode of iteration `it` (for a WHILE body any index with the
 // right residue mod npb): defer inside a group, flush at its end or at the
 // solve's last iteration.
-XUpd x_mode(rvk_cg_plan P, bool defer, int it, bool last)
+// A group longer than 4 (the whole solve) is flushed by k_cg_xfix only.
+XUpd x_mode(rvk_cg_plan P, bool defer, int it, bool last, int q, int npb)
 {
     XUpd u;
     if (!defer) return u;
-    const int q = P->xq, c = it % q;
-    if (c == q - 1 || last) {
+    const int c = it % q;
+    if ((c == q - 1 || last) && q <= 4) {
         u.np = c;
-        for (int k = 0; k < c; ++k) u.pp[k] = P->p[(it - c + k + 1) % P->npb];
+        for (int k = 0; k < c; ++k) u.pp[k] = P->p[(it - c + k + 1) % npb];
     } else {
         u.np   = -1;
         u.slot = c;
@@ -986,9 +1035,10 @@ rvk_status build_while_graph(rvk_cg_plan P, const double* b, double* x, cudaGrap
     rvk_status rc = vec ? launch_setup<true>(P, pcm, b, x) : launch_setup<false>(P, pcm, b, x);
     if (rc == RVK_OK) rc = launch_k1(P, 0, true, P->p[0], P->p[1]);
     const bool defer = x_defer(P, vec);
+    const int wq = while_group(P), wr = while_ring(P);
     if (rc == RVK_OK)
         rc = vec ? launch_update<true>(P, pcm, P->p[1], x, 0, h, 1,
-                                       x_mode(P, defer, 0, P->cfg.max_it == 1))
+                                       x_mode(P, defer, 0, P->cfg.max_it == 1, wq, wr))
                  : launch_update<false>(P, pcm, P->p[1], x, 0, h, 1);
     cudaError_t e = cudaStreamEndCapture(s, &pro);
     if (rc != RVK_OK) return fail(rc);
@@ -1010,13 +1060,13 @@ rvk_status build_while_graph(rvk_cg_plan P, const double* b, double* x, cudaGrap
         return fail(cuda_error(e, "cudaStreamBeginCaptureToGraph"));
     // body: npb iterations (residues 1, 2, ..., 0 mod npb), so every p buffer
     // index is static; a group ending mid-body is flushed by the epilogue
-    for (int j = 1; j <= P->npb && rc == RVK_OK; ++j) {
-        const int c = j % P->npb;
-        rc = launch_k1(P, -1, false, P->p[c], P->p[(c + 1) % P->npb]);
+    for (int j = 1; j <= wr && rc == RVK_OK; ++j) {
+        const int c = j % wr;
+        rc = launch_k1(P, -1, false, P->p[c], P->p[(c + 1) % wr]);
         if (rc == RVK_OK)
-            rc = vec ? launch_update<true>(P, pcm, P->p[(c + 1) % P->npb], x, -1, h, 1,
-                                           x_mode(P, defer, c, false))
-                     : launch_update<false>(P, pcm, P->p[(c + 1) % P->npb], x, -1, h, 1);
+            rc = vec ? launch_update<true>(P, pcm, P->p[(c + 1) % wr], x, -1, h, 1,
+                                           x_mode(P, defer, c, false, wq, wr))
+                     : launch_update<false>(P, pcm, P->p[(c + 1) % wr], x, -1, h, 1);
     }
     e = cudaStreamEndCapture(s, &tmp);
     if (rc != RVK_OK) return fail(rc);
@@ -1024,7 +1074,7 @@ rvk_status build_while_graph(rvk_cg_plan P, const double* b, double* x, cudaGrap
     if (defer) { // epilogue after the loop: apply an update left pending
         cudaGraph_t epi = nullptr;
         RVK_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeGlobal));
-        rc = launch_xfix(P, x);
+        rc = launch_xfix(P, x, wr);
         e  = cudaStreamEndCapture(s, &epi);
         if (rc != RVK_OK) return fail(rc);
         if (e != cudaSuccess) return fail(cuda_error(e, "capture (while epilogue)"));
@@ -1066,14 +1116,14 @@ rvk_status enqueue_fused(rvk_cg_plan P, const double* b, double* x)
         if ((rc = rec(4 * it + 1)) != RVK_OK || (rc = rec(4 * it + 2)) != RVK_OK) return rc;
         // grouped x: defer inside a group, flush at its end (or the last iteration)
         rc = vec ? launch_update<true>(P, pcm, p_new, x, it, 0, 0,
-                                       x_mode(P, defer, it, it + 1 == P->cfg.max_it))
+                                       x_mode(P, defer, it, it + 1 == P->cfg.max_it, P->xq, P->npb))
                  : launch_update<false>(P, pcm, p_new, x, it);
         if (rc != RVK_OK) return rc;
         ++P->launches;
         if ((rc = rec(4 * it + 3)) != RVK_OK) return rc;
     }
-    if (defer) { // an early exit after a deferring iteration leaves x pending
-        if ((rc = launch_xfix(P, x)) != RVK_OK) return rc;
+    if (defer) { // the whole-solve group, or an early exit mid-group, leaves x pending
+        if ((rc = launch_xfix(P, x, P->npb)) != RVK_OK) return rc;
         ++P->launches;
     }
     return RVK_OK;
@@ -1477,6 +1527,7 @@ int rvk_cg_plan_flags(rvk_cg_plan P)
            (P->mf_tma ? RVK_PLAN_MF_TMA : 0) | (P->off32 ? RVK_PLAN_OFF32 : 0) |
            ((P->mode == RVK_CG_MODE_FUSED && x_defer(P, true)) ? RVK_PLAN_X_DEFER : 0) |
            ((P->mode == RVK_CG_MODE_FUSED && x_defer(P, true) && P->xq == 4) ? RVK_PLAN_X_GROUP4 : 0) |
+           ((P->mode == RVK_CG_MODE_FUSED && x_defer(P, true) && P->xq > 4) ? RVK_PLAN_X_SOLVE : 0) |
            (P->zv ? RVK_PLAN_Z_VIRTUAL : 0);
 }
 
@@ -1564,10 +1615,12 @@ rvk_status rvk_cg_plan_destroy(rvk_cg_plan P)
         if (ev) cudaEventDestroy(ev);
     if (P->s_in) cudaStreamDestroy(P->s_in);
     if (P->s_out) cudaStreamDestroy(P->s_out);
-    void* bufs[] = {P->dinv, P->r, P->z, P->p[0], P->p[1], P->p[2], P->p[3], P->w, P->hist, P->st,
+    void* bufs[] = {P->dinv, P->r, P->z, P->w, P->hist, P->st,
                     P->partials, P->tickets, P->tmp, P->b_buf, P->x_buf, P->b_buf2,
                     P->x_buf2, P->hist_all, P->st_all, P->off32};
     for (void* b : bufs)
+        if (b) cudaFree(b);
+    for (double* b : P->p)
         if (b) cudaFree(b);
     delete P;
     return RVK_OK;

@@ -8,6 +8,9 @@ namespace rvk {
 
 // Device-resident solver scalars (the reference's Managed a, b, beta,
 // betaold, dp of PAPER.md:108-109) plus the exit state.
+// Most x updates one fused solve may defer (p buffers a plan may rotate).
+constexpr int kMaxXq = 32;
+
 struct CgState {
     double beta, betaold, alpha, pAp, dp0, dp;
     int    done, state, iterations, breakdown_iter;
@@ -15,7 +18,7 @@ struct CgState {
     unsigned int seq;  // row-sharded PEER backend: solves started on this plan
     double pend_alpha; // row-sharded CG: x += pend_alpha * p_{pend_it} not yet applied
     int    x_pending, pend_it; // pending x updates (count) and the first one's iteration
-    double pend_a[3];  // fused CG: a of the x updates deferred within the current group
+    double pend_a[kMaxXq]; // fused CG: a of the x updates deferred within the current group
 };
 
 constexpr int kUpdThreads = 256;

@@ -675,24 +675,30 @@ def test_virtual_z_bitexact(ctx, spec, pc, monkeypatch):
 @pytest.mark.parametrize("graph", [True, "while", False])
 def test_pairwise_x_update_exits_at_both_parities(ctx, graph, monkeypatch):
     """Early exits (device rtol) at every position inside an x-update group,
-    odd / even max_it: grouped x updates (groups of 4 and 2; deferring K2s,
-    a flushing K2 at the group end, k_cg_xfix for what an exit leaves
-    pending) give x bit-identical to one update per iteration."""
+    odd / even max_it: grouped x updates (the whole solve, groups of 4 and
+    2; deferring K2s, a flushing K2 at the group end, k_cg_xfix for what an
+    exit or the whole-solve group leaves pending) give x bit-identical to one
+    update per iteration."""
     dim, pts, g = 2, 5, (48, 40)
     Ah = O.build_laplacian(dim, pts, g)
     b = O.rhs(Ah.n_rows)
     A = rvk.DeviceCsr.laplacian(ctx, dim, pts, g)
     seen = set()
+    seen_solve = set()
     for max_it, rtol in [(7, 0.0), (8, 0.0), (200, 1e-3), (200, 3e-4), (200, 1e-4), (200, 3e-5),
-                         (200, 1e-5), (200, 3e-6)]:
+                         (200, 1e-5), (200, 3e-6), (32, 0.0), (32, 3e-1), (32, 1e-1), (32, 3e-2),
+                         (32, 1e-2)]:
         xs = {}
-        for grp in ("4", "2", "1"):
+        for grp in ("solve", "4", "2", "1"):
             monkeypatch.setenv("RVK_X_GROUP", grp)
             plan = rvk.CgPlan(ctx, A, max_it=max_it, rtol=rtol, use_graph=graph)
+            assert bool(plan.flags() & 128) == (grp == "solve" and max_it <= 32)
             xs[grp] = plan.solve_host(b)
             plan.close()
         monkeypatch.delenv("RVK_X_GROUP")
-        for grp in ("4", "2"):
+        if max_it <= 32:
+            seen_solve.add(xs["solve"][1].iterations)
+        for grp in ("solve", "4", "2"):
             assert np.array_equal(xs[grp][0], xs["1"][0]), (grp, max_it, rtol)
             assert np.array_equal(xs[grp][1].hist, xs["1"][1].hist)
         xs["1"] = xs["4"]
@@ -700,6 +706,7 @@ def test_pairwise_x_update_exits_at_both_parities(ctx, graph, monkeypatch):
         ref = O.cg_solve(Ah, b, max_it=max_it, rtol=rtol)
         check_cg(xs["1"][1], xs["1"][0], ref)
     assert len(seen) >= 3  # exits at several positions inside an x-update group
+    assert len(seen_solve) >= 3  # the whole-solve group ended early at several iterations
 
 
 @pytest.mark.parametrize("spec", [(2, 5, (2, 2)), (2, 5, (3, 3)), (2, 9, (3, 2)), (3, 7, (2, 2, 2)),
