@@ -910,7 +910,7 @@ rvk_status launch_xfix(rvk_cg_plan P, double* x, int npb)
 }
 
 // x-update group of a FUSED plan.  Default: the whole solve when it fits
-// (CSR operator, 5 <= max_it <= kMaxXq, max_it p buffers in free HBM): every
+// (5 <= max_it <= kMaxXq, max_it p buffers in free HBM): every
 // K2 defers and k_cg_xfix applies the max_it updates in one pass at the end
 // -- 16 n + 8 n max_it bytes per solve instead of 24 n per iteration.  Else
 // groups of 4 (the WHILE-loop graph always uses groups of <= 4: its p ring is
@@ -923,7 +923,7 @@ void set_x_group(rvk_cg_plan P)
     int         q  = 4;
     if (e && (e[0] == '1' || e[0] == '2') && !e[1]) q = e[0] - '0';
     const bool force_solve = e && std::strcmp(e, "solve") == 0;
-    if ((!e || force_solve) && !P->stencil && mi >= 5 && mi <= kMaxXq) {
+    if ((!e || force_solve) && mi >= 5 && mi <= kMaxXq) {
         const size_t vb = (size_t)P->A.n_rows * sizeof(double) + 32;
         size_t       fr = 0, tot = 0;
         const bool   fits = cudaMemGetInfo(&fr, &tot) == cudaSuccess &&

@@ -384,9 +384,9 @@ rvk_status launch_first(cudaStream_t s, const StencilGeom& g, const OpT& op,
 
 // ---- TMA plan state -----------------------------------------------------------
 struct MfTma {
-    CUtensorMap   z, r, pm[4]; // pm[k]: p buffer k
+    CUtensorMap   z, r, pm[kMaxXq]; // pm[k]: p buffer k
     MfTmaGeom     g{};
-    const double* p_ptr[4] = {nullptr, nullptr, nullptr, nullptr};
+    const double* p_ptr[kMaxXq] = {};
     int           np       = 2;
     int           grid   = 0;
     int           dim    = 3;
