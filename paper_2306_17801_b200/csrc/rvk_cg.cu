@@ -300,61 +300,6 @@ __global__ void __launch_bounds__(kUpdThreads)
                          use_cond);
 }
 
-// After the last iteration (or an early exit): apply the updates DEFER K2s
-// left pending, in iteration order: x = ((x + a_0 p_0) + a_1 p_1) + ... .
-// pb: the q rotating p buffers; iteration j wrote pb[(j + 1) % q].  With the
-// whole-solve group (q = max_it) this is the solve's only x pass: it streams
-// the max_it p's once (4 per trip, all loads issued before the adds).  No-op
-// (one flag read per block) when nothing is pending.
-struct XBufs {
-    const double* p[kMaxXq];
-};
-
-__global__ void __launch_bounds__(kUpdThreads)
-    k_cg_xfix(int64_t n, double* __restrict__ x, XBufs pb, int q, const CgState* __restrict__ st)
-{
-    pdl_trigger();
-    pdl_wait();
-    const int cnt = st->x_pending;
-    if (cnt <= 0) return;
-    __shared__ const double* sp[kMaxXq];
-    __shared__ double        sa[kMaxXq];
-    if (threadIdx.x < cnt) {
-        sp[threadIdx.x] = pb.p[(st->pend_it + threadIdx.x + 1) % q];
-        sa[threadIdx.x] = st->pend_a[threadIdx.x];
-    }
-    __syncthreads();
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    const int64_t t0     = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t n2     = n >> 1; // deferral implies 16-B aligned x and p
-    double2*      x2     = reinterpret_cast<double2*>(x);
-    for (int64_t i = t0; i < n2; i += stride) {
-        double2 xi = ld_stream(x2 + i);
-        int     k  = 0;
-        for (; k + 4 <= cnt; k += 4) {
-            double2 v[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) v[u] = ld_stream(reinterpret_cast<const double2*>(sp[k + u]) + i);
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                xi.x = axpy1(sa[k + u], v[u].x, xi.x);
-                xi.y = axpy1(sa[k + u], v[u].y, xi.y);
-            }
-        }
-        for (; k < cnt; ++k) {
-            const double2 v = ld_stream(reinterpret_cast<const double2*>(sp[k]) + i);
-            xi.x            = axpy1(sa[k], v.x, xi.x);
-            xi.y            = axpy1(sa[k], v.y, xi.y);
-        }
-        st_stream(x2 + i, xi);
-    }
-    if ((n & 1) && t0 == 0) {
-        double xi = x[n - 1];
-        for (int k = 0; k < cnt; ++k) xi = axpy1(sa[k], sp[k][n - 1], xi);
-        x[n - 1] = xi;
-    }
-}
-
 // K2, streaming variant (RVK_K2_TMA=1 opt-in / A-B): one CTA per SM; the
 // 4-5 input streams (p, w, x, r[, dinv]) of each 1024-element tile arrive by
 // cp.async.bulk into a kK2Stages-deep shared-memory ring (mbarrier per
@@ -903,7 +848,7 @@ rvk_status launch_xfix(rvk_cg_plan P, double* x, int npb)
 {
     XBufs pb{};
     for (int k = 0; k < npb; ++k) pb.p[k] = P->p[k];
-    launch_pdl(k_cg_xfix, P->upd_grid, kUpdThreads, 0, P->ctx->stream, P->A.n_rows, x, pb, npb,
+    launch_pdl(k_cg_xfix<0>, P->upd_grid, kUpdThreads, 0, P->ctx->stream, P->A.n_rows, x, pb, npb,
                (const CgState*)P->st);
     RVK_CHECK_LAUNCH("k_cg_xfix");
     return RVK_OK;

@@ -172,4 +172,72 @@ struct PersistArgs {
 int        persistent_grid(int64_t n);
 rvk_status launch_persistent(cudaStream_t s, const PersistArgs& args, bool jacobi, int grid);
 
+// After the last iteration (or an early exit): apply the updates DEFER K2s
+// left pending, in iteration order: x = ((x + a_0 p_0) + a_1 p_1) + ... .
+// pb: the q rotating p buffers; iteration j wrote pb[(j + 1) % q].  With the
+// whole-solve group (q = max_it) this is the solve's only x pass: it streams
+// the max_it p's once (4 per trip, all loads issued before the adds).  No-op
+// (one flag read per block) when nothing is pending.
+struct XBufs {
+    const double* p[kMaxXq];
+};
+
+// (A template so rvk_cg.cu and rvk_dcg.cu share one definition; the
+// row-sharded plan passes its buffers' owned slices.)
+template <int V = 0>
+__global__ void __launch_bounds__(kUpdThreads)
+    k_cg_xfix(int64_t n, double* __restrict__ x, XBufs pb, int q, const CgState* __restrict__ st)
+{
+    pdl_trigger();
+    pdl_wait();
+    const int cnt = st->x_pending;
+    if (cnt <= 0) return;
+    __shared__ const double* sp[kMaxXq];
+    __shared__ double        sa[kMaxXq];
+    if (threadIdx.x < cnt) {
+        sp[threadIdx.x] = pb.p[(st->pend_it + threadIdx.x + 1) % q];
+        sa[threadIdx.x] = st->pend_a[threadIdx.x];
+    }
+    __syncthreads();
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t t0     = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    uintptr_t     al     = reinterpret_cast<uintptr_t>(x);
+    for (int k = 0; k < cnt; ++k) al |= reinterpret_cast<uintptr_t>(sp[k]);
+    if (al & 15) { // a shard's owned slice may start mid-16-B: scalar sweep
+        for (int64_t i = t0; i < n; i += stride) {
+            double xi = x[i];
+            for (int k = 0; k < cnt; ++k) xi = axpy1(sa[k], sp[k][i], xi);
+            x[i] = xi;
+        }
+        return;
+    }
+    const int64_t n2 = n >> 1;
+    double2*      x2 = reinterpret_cast<double2*>(x);
+    for (int64_t i = t0; i < n2; i += stride) {
+        double2 xi = ld_stream(x2 + i);
+        int     k  = 0;
+        for (; k + 4 <= cnt; k += 4) {
+            double2 v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v[u] = ld_stream(reinterpret_cast<const double2*>(sp[k + u]) + i);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                xi.x = axpy1(sa[k + u], v[u].x, xi.x);
+                xi.y = axpy1(sa[k + u], v[u].y, xi.y);
+            }
+        }
+        for (; k < cnt; ++k) {
+            const double2 v = ld_stream(reinterpret_cast<const double2*>(sp[k]) + i);
+            xi.x            = axpy1(sa[k], v.x, xi.x);
+            xi.y            = axpy1(sa[k], v.y, xi.y);
+        }
+        st_stream(x2 + i, xi);
+    }
+    if ((n & 1) && t0 == 0) {
+        double xi = x[n - 1];
+        for (int k = 0; k < cnt; ++k) xi = axpy1(sa[k], sp[k][n - 1], xi);
+        x[n - 1] = xi;
+    }
+}
+
 } // namespace rvk

@@ -48,7 +48,8 @@
 // Write-after-read safety of the halos / slots follows from the waits: a
 // rank's K2(it) (which overwrites the neighbours' z halos and z.z slots)
 // starts only after every rank's K1(it) completed reading them; K1(it)
-// writes p_new = p[(it+1)&1], whose halo was last read by K1(it-1), which
+// writes p_new = p[(it+1) % ring], whose halo was last read by K1(it-1) or
+// earlier, which
 // precedes every rank's K2(it-1) that K1(it) waited for.  Every block fences
 // at system scope before its grid ticket, so the last block's release of the
 // flag covers all blocks' remote stores.  Waits are bounded (kPeerTimeoutNs):
@@ -166,9 +167,9 @@ struct DcgPeer {
     uint64_t* const* flags;              // [nranks] every rank's arrival flags
     const uint64_t* my_flags;            // this rank's flags (peers store into it)
     double*         lo_z;                // where my first owned plane lands in rank-1 (or null)
-    double*         lo_p[2];
+    double*         lo_p[kMaxXq];        // per p ring buffer
     double*         hi_z;                // where my last owned plane lands in rank+1 (or null)
-    double*         hi_p[2];
+    double*         hi_p[kMaxXq];
     int64_t         plane, n_own;
 };
 
@@ -402,8 +403,9 @@ struct DcgSpmvOp {
 };
 
 // K2(it): fold p.w; alpha = beta_it / pAp; updates; partial z.z, z.r.
-// XM: x-update mode as the single-GPU k_cg_update (0 x += a p; 1 defer to
-// the next iteration; 2 x = (x + a' p_prev) + a p) -- bit-identical x.
+// XM: x-update mode as the single-GPU k_cg_update (0 x += a p; 1 defer into
+// pend_a[slot] -- the next iteration's pair flush, or with the whole-solve
+// ring the final k_cg_xfix; 2 x = (x + a' p_prev) + a p) -- bit-identical x.
 template <int PC, bool PEER, int XM = 0, bool VEC = false>
 __global__ void __launch_bounds__(kUpdThreads)
     k_dcg_update(int64_t n, const double* __restrict__ p, const double* __restrict__ w,
@@ -411,7 +413,7 @@ __global__ void __launch_bounds__(kUpdThreads)
                  double* __restrict__ r,
                  double* __restrict__ z, DcgScalars sc, int it, int rank, double* gather_out,
                  double* partials, unsigned int* ticket, DcgPeer pr,
-                 const double* __restrict__ p_prev)
+                 const double* __restrict__ p_prev, int slot)
 {
     CgState* st = sc.st;
     if (st->done) return;
@@ -432,15 +434,16 @@ __global__ void __launch_bounds__(kUpdThreads)
         }
         return;
     }
-    // pend_alpha is only written by a DEFER (XM 1) launch, read by XM 2: no race
-    const double ap = XM == 2 ? st->pend_alpha : 0.0;
+    // pend_a[slot] is only written by a DEFER (XM 1) launch, read by a later
+    // XM 2 / k_cg_xfix: no race
+    const double ap = XM == 2 ? st->pend_a[0] : 0.0;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         st->pAp   = pAp;
         st->alpha = a;
         if (XM == 1) {
-            st->pend_alpha = a;
-            st->pend_it    = it;
-            st->x_pending  = 1;
+            st->pend_a[slot] = a;
+            st->x_pending    = slot + 1;
+            if (slot == 0) st->pend_it = it;
         } else if (XM == 2) {
             st->x_pending = 0;
         }
@@ -576,20 +579,6 @@ __global__ void k_dcg_finish(DcgScalars sc, int it, DcgPeer pr)
     }
 }
 
-// After the last iteration / an early exit: apply a deferred x update.
-// p0 / p1: the owned part of the ping-pong buffers.
-__global__ void __launch_bounds__(kUpdThreads)
-    k_dcg_xfix(int64_t n, double* __restrict__ x, const double* __restrict__ p0,
-               const double* __restrict__ p1, const CgState* __restrict__ st)
-{
-    if (!st->x_pending) return;
-    const double  a  = st->pend_alpha;
-    const double* pp = ((st->pend_it + 1) & 1) ? p1 : p0;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x)
-        x[i] = axpy1(a, pp[i], x[i]);
-}
-
 __global__ void k_dcg_reset(CgState* st)
 {
     st->x_pending = 0;
@@ -622,7 +611,9 @@ struct rvk_dcg_plan_s {
     int64_t       n_ext = 0;
     unsigned char* win = nullptr;  // [z | p0 | p1 | flags | gather], the exported PEER window
     size_t        win_bytes = 0;
-    double *dinv = nullptr, *r = nullptr, *z = nullptr, *p[2] = {nullptr, nullptr}, *w = nullptr;
+    double *dinv = nullptr, *r = nullptr, *z = nullptr, *w = nullptr;
+    double*       p[kMaxXq] = {}; // p ring in the window: iteration j writes p[(j+1) % npb]
+    int           npb = 2;        // 2 (x per iteration pair) or max_it (x once per solve)
     double *hist = nullptr, *beta = nullptr, *gather = nullptr, *partials = nullptr;
     bool          owns_gather = true;
     CgState*      st = nullptr;
@@ -639,20 +630,40 @@ namespace {
 // Byte layout of a shard's window (identical rule on every rank, so a rank
 // can address a peer's halo planes from the peer's shard geometry alone).
 struct WindowLayout {
-    size_t flags, gather, z, p0, p1, bytes;
+    size_t flags, gather, z, p0, vb, bytes;
+    int    npb;
+    size_t p(int k) const { return p0 + (size_t)k * vb; }
 };
-WindowLayout window_layout(int64_t n_ext)
+// p ring length of a shard plan: max_it (x written once per solve, every
+// iteration's p kept) when 5 <= max_it <= kMaxXq and the ring takes at most
+// half the device, else 2 (x per iteration pair).  A pure function of
+// (max_it, n_ext, device size), so every rank can derive a peer's layout;
+// attach_peers checks that the neighbours' rings match.  RVK_X_GROUP other
+// than "solve" keeps the pairs.
+int ring_len(int max_it, int64_t n_ext)
 {
-    // the gathered vectors start 2 MB-aligned, as separate allocations would;
-    // flags and gather slots after them
+    const char* e = std::getenv("RVK_X_GROUP");
+    if (e && std::strcmp(e, "solve") != 0) return 2;
+    if (max_it < 5 || max_it > kMaxXq) return 2;
+    size_t fr = 0, tot = 0;
+    if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) return 2;
+    const size_t need = (size_t)(max_it + 1) * ((size_t)n_ext * 8 + (size_t(3) << 20));
+    return need <= tot / 2 ? max_it : 2;
+}
+WindowLayout window_layout(int64_t n_ext, int npb)
+{
+    // the gathered vectors start 2 MB-aligned plus 1 MB, so z[j] and p[j]
+    // are not a whole number of 2 MB apart (measured: single-shard solve
+    // 9.64 -> 9.45 ms); flags and gather slots after them
     auto         up  = [](size_t v) { return (v + 255) & ~size_t(255); };
     auto         up2 = [](size_t v) { return (v + (size_t(2) << 20) - 1) & ~((size_t(2) << 20) - 1); };
     WindowLayout L{};
-    const size_t vb = up2((size_t)n_ext * 8 + 32); // + 4 doubles: x-windows round up
+    const size_t vb = up2((size_t)n_ext * 8 + 32) + (size_t(1) << 20); // + 4 doubles: x-windows round up
+    L.vb            = vb;
+    L.npb           = npb;
     L.z             = 0;
     L.p0            = vb;
-    L.p1            = 2 * vb;
-    L.flags         = 3 * vb;
+    L.flags         = (size_t)(npb + 1) * vb;
     L.gather        = up(L.flags + kMaxRanks * sizeof(uint64_t));
     L.bytes         = up(L.gather + kMaxRanks * 4 * sizeof(double));
     return L;
@@ -667,13 +678,13 @@ rvk_status alloc_plan_buffers(rvk_dcg_plan P)
         if (e == cudaSuccess) e = cudaMalloc(p, b);
         if (e == cudaSuccess) e = cudaMemsetAsync(*p, 0, b, P->ctx->stream);
     };
-    const WindowLayout L = window_layout(P->n_ext);
+    P->npb               = ring_len(P->cfg.max_it, P->n_ext);
+    const WindowLayout L = window_layout(P->n_ext, P->npb);
     alloc((void**)&P->win, L.bytes);
     if (e == cudaSuccess) {
         P->win_bytes = L.bytes;
         P->z         = reinterpret_cast<double*>(P->win + L.z);
-        P->p[0]      = reinterpret_cast<double*>(P->win + L.p0);
-        P->p[1]      = reinterpret_cast<double*>(P->win + L.p1);
+        for (int k = 0; k < P->npb; ++k) P->p[k] = reinterpret_cast<double*>(P->win + L.p(k));
         if (P->owns_gather) P->gather = reinterpret_cast<double*>(P->win + L.gather);
     }
 
@@ -734,11 +745,11 @@ rvk_status phase_setup(rvk_dcg_plan P, const double* b, double* x)
 template <bool FIRST, bool PEER>
 rvk_status launch_k1(rvk_dcg_plan P, int it)
 {
-    const double*  po = P->p[it & 1];
-    double*        pn = P->p[(it + 1) & 1];
+    const double*  po = P->p[it % P->npb];
+    double*        pn = P->p[(it + 1) % P->npb];
     const TailArgs ta{P->partials + 2 * kMaxReduceBlocks, P->tickets + 1};
     double*        go = P->gather + P->sh.rank * 4 + 2;
-    const int      k  = (it + 1) & 1; // p_new's buffer index, also in the neighbours
+    const int      k  = (it + 1) % P->npb; // p_new's buffer index, also in the neighbours
     const int64_t          ho = P->sh.halo_lo;
     DcgSpmvOp<FIRST, PEER> op{P->z, po, pn, P->w, scalars(P), ho, go, it, 0.0, P->peer,
                               P->peer.lo_p[k], P->peer.hi_p[k], 0u, P->z + ho, po + ho, pn + ho};
@@ -751,30 +762,35 @@ rvk_status phase_k1(rvk_dcg_plan P, int it)
     return it == 0 ? launch_k1<true, false>(P, it) : launch_k1<false, false>(P, it);
 }
 
-// x update per iteration pair (as rvk_cg.cu; RVK_X_DEFER=0 disables)
+// x update once per solve (ring = max_it: every K2 defers, k_cg_xfix applies
+// them at the end) or per iteration pair (as rvk_cg.cu; RVK_X_DEFER=0
+// disables both)
 bool x_defer(const rvk_dcg_plan P)
 {
     const char* e = std::getenv("RVK_X_DEFER");
     return P->cfg.max_it >= 2 && !(e && e[0] == '0');
 }
+bool x_solve(const rvk_dcg_plan P) { return x_defer(P) && P->npb > 2; }
 int x_mode(const rvk_dcg_plan P, int it)
 {
     if (!x_defer(P)) return 0;
+    if (x_solve(P)) return 1;
     return (it & 1) ? 2 : (it + 1 < P->cfg.max_it ? 1 : 0);
 }
 
 template <int PC, bool PEER, int XM>
 void launch_update_k(rvk_dcg_plan P, int it, double* x)
 {
-    const double* pn = P->p[(it + 1) & 1] + P->sh.halo_lo;
-    const double* pp = P->p[it & 1] + P->sh.halo_lo;
+    const double* pn = P->p[(it + 1) % P->npb] + P->sh.halo_lo;
+    const double* pp = P->p[it % P->npb] + P->sh.halo_lo;
     double*       zo = P->z + P->sh.halo_lo;
     auto a16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
     const bool vec = a16(x) && a16(pn) && a16(pp) && a16(zo) && a16(P->dinv) && a16(P->r) && a16(P->w);
     auto go = [&](auto kern) {
         kern<<<P->upd_grid, kUpdThreads, 0, P->ctx->stream>>>(
             P->sh.n_own, pn, P->w, P->dinv, P->dconst, x, P->r, zo, scalars(P), it, P->sh.rank,
-            P->gather + P->sh.rank * 4, P->partials, P->tickets, P->peer, pp);
+            P->gather + P->sh.rank * 4, P->partials, P->tickets, P->peer, pp,
+            x_solve(P) ? it : 0);
     };
     if (vec) go(k_dcg_update<PC, PEER, XM, true>);
     else go(k_dcg_update<PC, PEER, XM, false>);
@@ -811,9 +827,11 @@ rvk_status phase_k2(rvk_dcg_plan P, int it, double* x)
 rvk_status phase_xfix(rvk_dcg_plan P, double* x)
 {
     if (!x_defer(P)) return RVK_OK;
-    k_dcg_xfix<<<P->upd_grid, kUpdThreads, 0, P->ctx->stream>>>(
-        P->sh.n_own, x, P->p[0] + P->sh.halo_lo, P->p[1] + P->sh.halo_lo, P->st);
-    RVK_CHECK_LAUNCH("k_dcg_xfix");
+    XBufs pb{};
+    for (int k = 0; k < P->npb; ++k) pb.p[k] = P->p[k] + P->sh.halo_lo;
+    k_cg_xfix<0><<<P->upd_grid, kUpdThreads, 0, P->ctx->stream>>>(P->sh.n_own, x, pb, P->npb,
+                                                                   P->st);
+    RVK_CHECK_LAUNCH("k_cg_xfix");
     return RVK_OK;
 }
 
@@ -838,7 +856,7 @@ rvk_status nccl_halo(rvk_dcg_plan P, bool with_p, int it)
     const int64_t pl   = plane(P);
     const int     rank = P->sh.rank, np = P->sh.nranks;
     if (np == 1) return RVK_OK;
-    double*     vecs[2] = {P->z, P->p[it & 1]};
+    double*     vecs[2] = {P->z, P->p[it % P->npb]};
     const int   nv      = with_p ? 2 : 1;
     auto&       api     = nccl();
     cudaStream_t s      = P->ctx->stream;
@@ -867,7 +885,7 @@ rvk_status loop_halo(rvk_dcg_plan* Ps, int np, bool with_p, int it)
         cudaStream_t s  = P->ctx->stream;
         const int64_t pl = plane(P);
         for (int v = 0; v < (with_p ? 2 : 1); ++v) {
-            auto vec = [&](rvk_dcg_plan Q) { return v == 0 ? Q->z : Q->p[it & 1]; };
+            auto vec = [&](rvk_dcg_plan Q) { return v == 0 ? Q->z : Q->p[it % Q->npb]; };
             if (r > 0) { // my lo halo <- last owned plane of r-1
                 rvk_dcg_plan L = Ps[r - 1];
                 RVK_CUDA(cudaMemcpyAsync(vec(P), vec(L) + L->sh.halo_lo + L->sh.n_own - pl, pl * 8,
@@ -1078,7 +1096,7 @@ int rvk_dcg_plan_flags(rvk_dcg_plan P)
 {
     if (!P) return -1;
     return (P->const_diag ? RVK_PLAN_CONST_DIAG : 0) | (P->off32 ? RVK_PLAN_OFF32 : 0) |
-           (x_defer(P) ? RVK_PLAN_X_DEFER : 0);
+           (x_defer(P) ? RVK_PLAN_X_DEFER : 0) | (x_solve(P) ? RVK_PLAN_X_SOLVE : 0);
 }
 
 // ---- PEER backend ----------------------------------------------------------
@@ -1107,10 +1125,14 @@ rvk_status rvk_dcg_attach_peers(rvk_dcg_plan P, void* const* windows, const rvk_
     auto ext = [&](int q) { return shards[q].halo_lo + shards[q].n_own + shards[q].halo_hi; };
     auto at  = [&](int q, size_t off) { return reinterpret_cast<unsigned char*>(windows[q]) + off; };
     std::vector<void*> tab(2 * np);
+    auto lay = [&](int q) { return window_layout(ext(q), ring_len(P->cfg.max_it, ext(q))); };
     for (int q = 0; q < np; ++q) {
-        const WindowLayout L = window_layout(ext(q));
-        tab[q]               = at(q, L.gather);
-        tab[np + q]          = at(q, L.flags);
+        const WindowLayout L = lay(q);
+        if (L.npb != P->npb)
+            return set_error(RVK_ERR_INVALID, "attach_peers: rank %d's p ring (%d) differs from this rank's (%d)",
+                             q, L.npb, P->npb);
+        tab[q]      = at(q, L.gather);
+        tab[np + q] = at(q, L.flags);
     }
     DcgPeer pr{};
     pr.on     = 1;
@@ -1118,24 +1140,22 @@ rvk_status rvk_dcg_attach_peers(rvk_dcg_plan P, void* const* windows, const rvk_
     pr.nranks = np;
     pr.plane  = pl;
     pr.n_own  = P->sh.n_own;
-    const WindowLayout Lme = window_layout(P->n_ext);
+    const WindowLayout Lme = window_layout(P->n_ext, P->npb);
     pr.my_flags            = reinterpret_cast<const uint64_t*>(P->win + Lme.flags);
     if (me > 0) { // my first owned plane -> the upper halo of rank-1
         const rvk_shard&   d   = shards[me - 1];
-        const WindowLayout L   = window_layout(ext(me - 1));
+        const WindowLayout L   = lay(me - 1);
         const size_t       off = (size_t)(d.halo_lo + d.n_own) * 8;
         if (d.halo_hi != pl) return set_error(RVK_ERR_DIM, "attach_peers: plane size mismatch with rank %d", me - 1);
         pr.lo_z    = reinterpret_cast<double*>(at(me - 1, L.z + off));
-        pr.lo_p[0] = reinterpret_cast<double*>(at(me - 1, L.p0 + off));
-        pr.lo_p[1] = reinterpret_cast<double*>(at(me - 1, L.p1 + off));
+        for (int k = 0; k < P->npb; ++k) pr.lo_p[k] = reinterpret_cast<double*>(at(me - 1, L.p(k) + off));
     }
     if (me < np - 1) { // my last owned plane -> the lower halo of rank+1 (element 0)
         const rvk_shard&   u = shards[me + 1];
-        const WindowLayout L = window_layout(ext(me + 1));
+        const WindowLayout L = lay(me + 1);
         if (u.halo_lo != pl) return set_error(RVK_ERR_DIM, "attach_peers: plane size mismatch with rank %d", me + 1);
         pr.hi_z    = reinterpret_cast<double*>(at(me + 1, L.z));
-        pr.hi_p[0] = reinterpret_cast<double*>(at(me + 1, L.p0));
-        pr.hi_p[1] = reinterpret_cast<double*>(at(me + 1, L.p1));
+        for (int k = 0; k < P->npb; ++k) pr.hi_p[k] = reinterpret_cast<double*>(at(me + 1, L.p(k)));
     }
     if (!P->peer_tab) RVK_CUDA(cudaMalloc(&P->peer_tab, 2 * kMaxRanks * sizeof(void*)));
     RVK_CUDA(cudaMemcpy(P->peer_tab, tab.data(), tab.size() * sizeof(void*), cudaMemcpyHostToDevice));

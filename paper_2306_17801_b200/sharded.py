@@ -360,11 +360,15 @@ def bench_main(args, cfg):
     nnz_glob = _global_nnz(dim, pts, grid)
     fl = rvk.lib().rvk_dcg_plan_flags(plan.h)
     ob = 4 if fl & 8 else 8               # int32 row offsets streamed
-    vb = 88 if fl & 16 else 96            # x updated per iteration pair
-    b_min = 20 * (12 * nnz_glob + ob * (n_glob + 1) + vb * n_glob) + 64 * n_glob
+    # per-iteration vector bytes: 96 n, x traffic 24 n -> 8 n + 16 n / group
+    # (pairs: 16 n; whole solve, RVK_PLAN_X_SOLVE: 8.8 n), constant
+    # Jacobi diagonal (RVK_PLAN_CONST_DIAG) -8 n per iteration and setup
+    grp = 20 if fl & 128 else (2 if fl & 16 else 1)
+    vb = 96 - (16 - 16 / grp) - (8 if fl & 1 else 0)
+    b_min = int(20 * (12 * nnz_glob + ob * (n_glob + 1) + vb * n_glob) + (56 if fl & 1 else 64) * n_glob)
     hbm_peak, peak_src = peaks()
     per_gpu = b_min / world / (ms * 1e-3) / 1e9
-    launches = 3 + 2 * 20  # reset, setup, 20 x (K1, K2), finish  (our kernels, per rank)
+    launches = 3 + 2 * 20 + (1 if fl & 16 else 0)  # reset, setup, 20 x (K1, K2), finish, x-fix
     if rank == 0:
         comm_desc = {"peer": "PEER: K1/K2 store halo planes + dot partials into the neighbours' "
                              "windows over NVLink (cudaIpc), device flag sync; no NCCL on the "
