@@ -216,12 +216,13 @@ __global__ void __launch_bounds__(kUpdThreads)
     for (int64_t i = t0; i < n2; i += stride) {
         double2 xi = ld_stream(x2 + i);
         int     k  = 0;
-        for (; k + 4 <= cnt; k += 4) {
-            double2 v[4];
+        constexpr int B = V > 0 ? V : 4; // p streams in flight per thread
+        for (; k + B <= cnt; k += B) {
+            double2 v[B];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) v[u] = ld_stream(reinterpret_cast<const double2*>(sp[k + u]) + i);
+            for (int u = 0; u < B; ++u) v[u] = ld_stream(reinterpret_cast<const double2*>(sp[k + u]) + i);
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < B; ++u) {
                 xi.x = axpy1(sa[k + u], v[u].x, xi.x);
                 xi.y = axpy1(sa[k + u], v[u].y, xi.y);
             }

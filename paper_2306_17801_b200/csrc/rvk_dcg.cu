@@ -663,7 +663,7 @@ WindowLayout window_layout(int64_t n_ext, int npb)
     L.npb           = npb;
     L.z             = 0;
     L.p0            = vb;
-    L.flags         = (size_t)(npb + 1) * vb;
+    L.flags         = L.p(npb);
     L.gather        = up(L.flags + kMaxRanks * sizeof(uint64_t));
     L.bytes         = up(L.gather + kMaxRanks * 4 * sizeof(double));
     return L;
@@ -829,7 +829,7 @@ rvk_status phase_xfix(rvk_dcg_plan P, double* x)
     if (!x_defer(P)) return RVK_OK;
     XBufs pb{};
     for (int k = 0; k < P->npb; ++k) pb.p[k] = P->p[k] + P->sh.halo_lo;
-    k_cg_xfix<0><<<P->upd_grid, kUpdThreads, 0, P->ctx->stream>>>(P->sh.n_own, x, pb, P->npb,
+    k_cg_xfix<4><<<P->upd_grid, kUpdThreads, 0, P->ctx->stream>>>(P->sh.n_own, x, pb, P->npb,
                                                                    P->st);
     RVK_CHECK_LAUNCH("k_cg_xfix");
     return RVK_OK;

@@ -30,10 +30,14 @@ def timed(solve, k=10):
     return e0.elapsed_time(e1) / k
 
 
+if os.environ.get("CG_FIRST"):  # allocation-order control
+    cp = rvk.CgPlan(ctx, A, max_it=20)
+    t_cg = timed(lambda: cp.solve_dev(b, x))
 dp = ShardPlan(ctx, A, sh, 20)
 t_dcg = timed(lambda: dp.solve_dev(b, x))
-cp = rvk.CgPlan(ctx, A, max_it=20)
-t_cg = timed(lambda: cp.solve_dev(b, x))
+if not os.environ.get("CG_FIRST"):
+    cp = rvk.CgPlan(ctx, A, max_it=20)
+    t_cg = timed(lambda: cp.solve_dev(b, x))
 print(f"grid {g}: dcg single shard {t_dcg:.3f} ms/solve, fused CG plan {t_cg:.3f} ms/solve")
 
 # the same dcg solve captured as one CUDA graph (launch overhead out of the picture)
