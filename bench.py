@@ -284,12 +284,14 @@ def _laplacian_size(dim, pts, grid):
     return n, nnz
 
 
-def tfqmr_bytes(n: int, nnz: int):
+def tfqmr_bytes(n: int, nnz: int, const_diag: bool = False):
     """Algorithmic HBM bytes of the fused TFQMR solve (rvk_tfqmr.cu header):
     KA = CSR + 7n doubles, KM = 11n (6n in the last iteration), KB = CSR + 4n;
-    setup K0 = 8n, plus one KB; no KB after the last iteration."""
+    setup K0 = 8n, plus one KB; no KB after the last iteration.  const_diag
+    (the plan's RVK_PLAN_CONST_DIAG): no dinv stream in K0, KA, KB (-8n each)."""
     csr = 12 * nnz + 8 * (n + 1)
-    ka, km, km_last, kb, k0 = csr + 56 * n, 88 * n, 48 * n, csr + 32 * n, 64 * n
+    dv = 0 if const_diag else 8 * n
+    ka, km, km_last, kb, k0 = csr + 48 * n + dv, 88 * n, 48 * n, csr + 24 * n + dv, 56 * n + dv
     solve = k0 + kb + MAX_IT * ka + (MAX_IT - 1) * (km + kb) + km_last
     return {"ka": ka, "km": km, "kb": kb, "b_min_solve": solve}
 
@@ -313,7 +315,7 @@ def run_tfqmr(args, cfg):
     rvk.check(rvk.lib().rvk_fill_rhs(ctx.h, 0x9E3779B97F4A7C15, n, b.ptr))
     mode = "unfused" if args.mode == "unfused" else "fused"
     plan = rvk.TfqmrPlan(ctx, A, max_it=MAX_IT, use_graph=not args.no_graph, mode=mode)
-    bm = tfqmr_bytes(n, nnz)
+    bm = tfqmr_bytes(n, nnz, bool(plan.flags() & 1) and mode == "fused")
     hbm_peak, peak_src = peaks()
     ws_bytes = 20 * nnz + 8 * (n + 1) + 11 * 8 * n
     for _ in range(args.warmup):

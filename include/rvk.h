@@ -279,6 +279,9 @@ rvk_status rvk_tfqmr_solve_dev(rvk_tfqmr_plan plan, const double* b_dev, double*
  * (v, rp) == 0 or rho_old == 0. */
 rvk_status rvk_tfqmr_result(rvk_tfqmr_plan plan, double* hist_host, int* n_hist,
                             rvk_cg_info* info);
+/* RVK_PLAN_CONST_DIAG when the fused kernels use the constant Jacobi
+ * diagonal as a scalar (bit-identical; no dinv stream); -1 on a null plan. */
+int        rvk_tfqmr_plan_flags(rvk_tfqmr_plan plan);
 
 /* ---- row sharding across GPUs -----------------------------
  * The global grid is split into contiguous slabs of planes; shard `rank`

@@ -27,6 +27,7 @@
 #include "rvk_spmv.cuh"
 
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 namespace rvk {
@@ -171,9 +172,12 @@ __device__ __forceinline__ void tfq_finish(TfqState* st, int state, int it, int 
 }
 
 // K0: r = B b; rp = u = p = r; d = x = 0; ||r||^2 (= (r, rp)); initial scalars.
-template <bool VEC, bool JAC>
+// PC: 0 no preconditioner, 1 dinv vector, 2 constant diagonal dc (every
+// dinv[i] the same bit pattern: the scalar gives bit-identical products and
+// the dinv stream disappears from K0, KA and KB)
+template <bool VEC, int PC>
 __global__ void __launch_bounds__(kTfqThreads)
-    k_tfq_setup(int64_t n, const double* __restrict__ b, const double* __restrict__ dinv,
+    k_tfq_setup(int64_t n, const double* __restrict__ b, const double* __restrict__ dinv, double dc,
                 double* __restrict__ R, double* __restrict__ RP, double* __restrict__ U,
                 double* __restrict__ P, double* __restrict__ D, double* __restrict__ X, TfqState* st,
                 double* hist, double rtol, double atol, double* partials, unsigned int* ticket)
@@ -187,8 +191,9 @@ __global__ void __launch_bounds__(kTfqThreads)
         for (int64_t i = t0; i < (n >> 1); i += stride) {
             const double2 bi = ld_stream(reinterpret_cast<const double2*>(b) + i);
             double2       r  = bi;
-            if (JAC) {
-                const double2 d = ld_stream(reinterpret_cast<const double2*>(dinv) + i);
+            if (PC) {
+                const double2 d = PC == 1 ? ld_stream(reinterpret_cast<const double2*>(dinv) + i)
+                                          : make_double2(dc, dc);
                 r.x             = mul(d.x, bi.x);
                 r.y             = mul(d.y, bi.y);
             }
@@ -203,7 +208,7 @@ __global__ void __launch_bounds__(kTfqThreads)
         }
     }
     for (int64_t i = (VEC ? (n & ~int64_t(1)) : 0) + t0; i < n; i += stride) {
-        const double r = JAC ? mul(dinv[i], b[i]) : b[i];
+        const double r = PC ? mul(PC == 1 ? dinv[i] : dc, b[i]) : b[i];
         R[i] = RP[i] = U[i] = P[i] = r;
         D[i] = X[i] = 0.0;
         acc[0]      = add(acc[0], mul(r, r));
@@ -233,7 +238,7 @@ __global__ void __launch_bounds__(kTfqThreads)
 
 // KA op: t = u + (u - a v) on the fly, q and r written by the row owner,
 // sums ||r||^2 and (r, rp); tail = the iteration's scalar recurrence.
-template <bool JAC>
+template <int PC>
 struct TfqAOp {
     static constexpr bool kHasTail = true;
     static constexpr int  kSums    = 2;
@@ -248,6 +253,7 @@ struct TfqAOp {
     double    rtol, atol;
     int       it;
     double    na; // -a, set by init()
+    double    dc; // PC 2: the constant diagonal
 
     __device__ __forceinline__ bool init()
     {
@@ -279,12 +285,13 @@ struct TfqAOp {
     };
     __device__ __forceinline__ Own own(int64_t i) const
     {
-        return Own{__ldg(u + i), __ldg(v + i), r[i], __ldg(rp + i), JAC ? __ldg(dinv + i) : 1.0};
+        return Own{__ldg(u + i), __ldg(v + i), r[i], __ldg(rp + i),
+                   PC == 1 ? __ldg(dinv + i) : (PC == 2 ? dc : 1.0)};
     }
     __device__ __forceinline__ SumVec<2> row(int64_t i, double sum, SumVec<2> acc, const Own& o) const
     {
         q[i]            = add(mul(na, o.v), o.u);
-        const double bt = JAC ? mul(o.d, sum) : sum;  // B A t
+        const double bt = PC ? mul(o.d, sum) : sum;   // B A t
         const double ri = add(o.r, mul(na, bt));      // r += (-a) B A t
         r[i]            = ri;
         acc.v[0]        = add(acc.v[0], mul(ri, ri));
@@ -316,7 +323,7 @@ struct TfqAOp {
 
 // KB op: v = B A p, (v, rp); tail: rho_old = rho, dp_old = dp, a = rho_old / s.
 // `it` = the iteration the new a belongs to (0 for the setup launch).
-template <bool JAC>
+template <int PC>
 struct TfqBOp {
     static constexpr bool kHasTail = true;
     const double* __restrict__ p;
@@ -325,6 +332,7 @@ struct TfqBOp {
     double* __restrict__ v;
     TfqState* st;
     int       it;
+    double    dc; // PC 2: the constant diagonal
 
     __device__ __forceinline__ bool init() { return st->done == 0; }
     struct Fetch {
@@ -344,11 +352,11 @@ struct TfqBOp {
     };
     __device__ __forceinline__ Own own(int64_t i) const
     {
-        return Own{__ldg(rp + i), JAC ? __ldg(dinv + i) : 1.0};
+        return Own{__ldg(rp + i), PC == 1 ? __ldg(dinv + i) : (PC == 2 ? dc : 1.0)};
     }
     __device__ __forceinline__ double row(int64_t i, double sum, double acc, const Own& o) const
     {
-        const double vi = JAC ? mul(o.d, sum) : sum;
+        const double vi = PC ? mul(o.d, sum) : sum;
         v[i]            = vi;
         return add(acc, mul(vi, o.rp));
     }
@@ -449,6 +457,8 @@ struct rvk_tfqmr_plan_s {
     double*         g_x = nullptr;
     bool            fused    = true;
     int             upd_grid = 1; // resident grid of the streaming kernels (K0, KM)
+    bool            const_diag = false; // fused: dinv is one value, dconst
+    double          dconst     = 0.0;
 };
 
 namespace {
@@ -484,7 +494,7 @@ rvk_status apply_BA(rvk_tfqmr_plan P, const double* v, double* out, const int* g
     return RVK_OK;
 }
 
-template <bool JAC>
+template <int PC>
 rvk_status enqueue_fused_t(rvk_tfqmr_plan P, const double* b, double* x)
 {
     const int64_t  n    = P->A.n_rows;
@@ -498,18 +508,18 @@ rvk_status enqueue_fused_t(rvk_tfqmr_plan P, const double* b, double* x)
     const TailArgs ta{P->partials, P->tickets + 1};
     const TailArgs tb{P->partials + 2 * kMaxReduceBlocks, P->tickets + 2};
     if (vec)
-        k_tfq_setup<true, JAC><<<P->upd_grid, kTfqThreads, 0, s>>>(
-            n, b, P->dinv, P->R, P->RP, P->U, P->P, P->D, x, st, P->hist, rtol, atol, P->partials,
+        k_tfq_setup<true, PC><<<P->upd_grid, kTfqThreads, 0, s>>>(
+            n, b, P->dinv, P->dconst, P->R, P->RP, P->U, P->P, P->D, x, st, P->hist, rtol, atol, P->partials,
             P->tickets);
     else
-        k_tfq_setup<false, JAC><<<P->upd_grid, kTfqThreads, 0, s>>>(
-            n, b, P->dinv, P->R, P->RP, P->U, P->P, P->D, x, st, P->hist, rtol, atol, P->partials,
+        k_tfq_setup<false, PC><<<P->upd_grid, kTfqThreads, 0, s>>>(
+            n, b, P->dinv, P->dconst, P->R, P->RP, P->U, P->P, P->D, x, st, P->hist, rtol, atol, P->partials,
             P->tickets);
     RVK_CHECK_LAUNCH("k_tfq_setup");
-    RVK_TRY(launch_spmv(s, P->sa, TfqBOp<JAC>{P->P, P->RP, P->dinv, P->V, st, 0}, tb, sg));
+    RVK_TRY(launch_spmv(s, P->sa, TfqBOp<PC>{P->P, P->RP, P->dinv, P->V, st, 0, P->dconst}, tb, sg));
     for (int it = 0; it < P->cfg.max_it; ++it) {
         const bool last = it + 1 == P->cfg.max_it;
-        TfqAOp<JAC> a{P->U, P->V, P->RP, P->dinv, P->Q, P->R, st, P->hist, rtol, atol, it, 0.0};
+        TfqAOp<PC> a{P->U, P->V, P->RP, P->dinv, P->Q, P->R, st, P->hist, rtol, atol, it, 0.0, P->dconst};
         RVK_TRY(launch_spmv(s, P->sa, a, ta, sg));
         if (vec)
             k_tfq_merge<true><<<P->upd_grid, kTfqThreads, 0, s>>>(n, P->U, P->Q, P->R, P->P, P->D, x,
@@ -518,7 +528,8 @@ rvk_status enqueue_fused_t(rvk_tfqmr_plan P, const double* b, double* x)
             k_tfq_merge<false><<<P->upd_grid, kTfqThreads, 0, s>>>(n, P->U, P->Q, P->R, P->P, P->D,
                                                                    x, st, it, last);
         RVK_CHECK_LAUNCH("k_tfq_merge");
-        if (!last) RVK_TRY(launch_spmv(s, P->sa, TfqBOp<JAC>{P->P, P->RP, P->dinv, P->V, st, it + 1}, tb, sg));
+        if (!last)
+            RVK_TRY(launch_spmv(s, P->sa, TfqBOp<PC>{P->P, P->RP, P->dinv, P->V, st, it + 1, P->dconst}, tb, sg));
     }
     return RVK_OK;
 }
@@ -526,7 +537,9 @@ rvk_status enqueue_fused_t(rvk_tfqmr_plan P, const double* b, double* x)
 rvk_status enqueue_tfqmr(rvk_tfqmr_plan P, const double* b, double* x)
 {
     if (P->fused)
-        return P->cfg.pc == RVK_PC_JACOBI ? enqueue_fused_t<true>(P, b, x) : enqueue_fused_t<false>(P, b, x);
+        return P->cfg.pc != RVK_PC_JACOBI ? enqueue_fused_t<0>(P, b, x)
+               : P->const_diag            ? enqueue_fused_t<2>(P, b, x)
+                                          : enqueue_fused_t<1>(P, b, x);
     const int64_t n   = P->A.n_rows;
     cudaStream_t  s   = P->ctx->stream;
     const bool    jac = P->cfg.pc == RVK_PC_JACOBI;
@@ -626,6 +639,11 @@ rvk_status rvk_tfqmr_plan_create(rvk_ctx ctx, const rvk_csr* A, rvk_cg_config cf
         return cuda_error(e, "rvk_tfqmr_plan_create");
     }
     rvk_status rc = cfg.pc == RVK_PC_JACOBI ? rvk_csr_diagonal_inverse(ctx, A, P->dinv) : RVK_OK;
+    // constant-coefficient operators: one diagonal value -> a scalar in the
+    // fused kernels (as the CG plans; RVK_CONST_DIAG=0 disables)
+    const char* cd = std::getenv("RVK_CONST_DIAG");
+    if (rc == RVK_OK && P->fused && cfg.pc == RVK_PC_JACOBI && !(cd && cd[0] == '0'))
+        rc = vector_is_constant(ctx->stream, A->n_rows, P->dinv, &P->const_diag, &P->dconst);
     if (rc != RVK_OK) {
         rvk_tfqmr_plan_destroy(P);
         return rc;
@@ -673,6 +691,12 @@ rvk_status rvk_tfqmr_solve_dev(rvk_tfqmr_plan P, const double* b, double* x)
     }
     RVK_CUDA(cudaGraphLaunch(P->graph, s));
     return RVK_OK;
+}
+
+int rvk_tfqmr_plan_flags(rvk_tfqmr_plan P)
+{
+    if (!P) return -1;
+    return P->const_diag ? RVK_PLAN_CONST_DIAG : 0;
 }
 
 rvk_status rvk_tfqmr_result(rvk_tfqmr_plan P, double* hist_host, int* n_hist, rvk_cg_info* info)

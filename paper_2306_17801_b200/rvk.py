@@ -47,7 +47,7 @@ EXPORTS = [
     "rvk_comm_destroy", "rvk_dcg_plan_create", "rvk_dcg_plan_destroy", "rvk_dcg_solve_dev",
     "rvk_dcg_loopback_solve", "rvk_dcg_result", "rvk_dcg_plan_flags", "rvk_dcg_window", "rvk_dcg_attach_peers",
     "rvk_ipc_get_handle", "rvk_ipc_open_handle", "rvk_ipc_close_handle", "rvk_tfqmr_plan_create",
-    "rvk_tfqmr_plan_destroy", "rvk_tfqmr_solve_dev", "rvk_tfqmr_result",
+    "rvk_tfqmr_plan_destroy", "rvk_tfqmr_solve_dev", "rvk_tfqmr_result", "rvk_tfqmr_plan_flags",
 ]
 
 
@@ -176,6 +176,7 @@ def lib():
         "rvk_tfqmr_plan_destroy": (i, [vp]),
         "rvk_tfqmr_solve_dev": (i, [vp, vp, vp]),
         "rvk_tfqmr_result": (i, [vp, vp, C.POINTER(C.c_int), C.POINTER(CgInfo)]),
+        "rvk_tfqmr_plan_flags": (i, [vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -483,6 +484,10 @@ class TfqmrPlan:
 
     def solve_dev(self, b: DeviceArray, x: DeviceArray):
         check(lib().rvk_tfqmr_solve_dev(self.h, b.ptr, x.ptr))
+
+    def flags(self) -> int:
+        """RVK_PLAN_* bits (CONST_DIAG = 1)."""
+        return lib().rvk_tfqmr_plan_flags(self.h)
 
     def result(self, raise_breakdown: bool = True) -> CgResult:
         hist = np.full(2 * self.max_it + 1, np.nan)

@@ -1,6 +1,6 @@
 exec > gpurun_out/dcg.log 2>&1
-for st in 0 262144 524288 1048576 0; do
-echo stagger $st
-RVK_WIN_STAGGER=$st timeout 300 python scripts/dcg_time.py 256x256x256 2>&1 | head -1
-RVK_WIN_STAGGER=$st timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"xfix|spmv" -c 6 python scripts/dcg_time.py 2>&1 | grep -E "gpu__time_duration" | tr -s ' ' | cut -d' ' -f4 | tr '\n' ' '; echo
+timeout 900 python -m pytest tests/test_gpu_tfqmr.py -x -q 2>&1 | tail -3
+for cd in 1 0; do
+RVK_CONST_DIAG=$cd timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --solver tfqmr 2>&1 >/dev/null | tail -1 | sed "s/^/cd=$cd /"
+RVK_CONST_DIAG=$cd timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --solver tfqmr --config 27pt256 2>&1 >/dev/null | tail -1 | sed "s/^/27pt cd=$cd /"
 done

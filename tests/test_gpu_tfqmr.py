@@ -185,3 +185,23 @@ def test_tfqmr_early_exit_each_half_step(ctx):
         for mode in MODES:
             _, x, res = solve(ctx, A, b, max_it=30, atol=atol, mode=mode)
             check(res, x, ref)
+
+
+@pytest.mark.parametrize("spec", [(2, 5, (40, 33)), (3, 7, (20, 16, 12)), (3, 27, (10, 9, 8)),
+                                  (2, 9, (64, 64))])
+def test_tfqmr_constant_diagonal_bitexact(ctx, spec, monkeypatch):
+    """Constant-coefficient Laplacians have one diagonal value: the fused
+    plan uses it as a scalar (RVK_PLAN_CONST_DIAG, no dinv stream in K0, KA,
+    KB) -- x and the history bit-identical to the dinv-vector kernels."""
+    dim, pts, g = spec
+    Ah = O.build_laplacian(dim, pts, g)
+    b = O.rhs(Ah.n_rows)
+    A = rvk.DeviceCsr.laplacian(ctx, dim, pts, g)
+    plan, x1, r1 = solve(ctx, A, b, max_it=20)
+    assert plan.flags() & 1
+    monkeypatch.setenv("RVK_CONST_DIAG", "0")
+    plan0, x0, r0 = solve(ctx, A, b, max_it=20)
+    assert not plan0.flags() & 1
+    assert np.array_equal(x1, x0)
+    assert np.array_equal(r1.hist, r0.hist)
+    check(r1, x1, O.tfqmr_solve(Ah, b, max_it=20))
