@@ -2,6 +2,7 @@
 // can reach on this B200, vs the 1:1 copy figure in MEASURED_PEAKS.json.
 // Prints GB/s for: read-only reduction, 1:1 copy, 7:1 read:write, at 2 GB.
 #include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 __device__ __forceinline__ double4 ldv(const double4* p)
@@ -64,11 +65,14 @@ void run(const char* name, double2* in, double2* out, long n2, double* sink, int
            ms * 1e3 / reps);
 }
 
-int main()
+int main(int argc, char** argv)
 {
     int sms;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    const long n2 = 1L << 26; // 1 GiB per stream
+    // argv[1]: GiB per stream (default 1; the footprint test runs 1, 4, 8)
+    const long gib = argc > 1 ? atol(argv[1]) : 1;
+    const long n2 = (1L << 26) * gib;
+    printf("stream size %ld GiB\n", gib);
     double2 *in, *out;
     double*  sink;
     cudaMalloc(&in, 8 * n2 * 16);
@@ -76,7 +80,7 @@ int main()
     cudaMalloc(&sink, 8);
     cudaMemset(in, 0, 8 * n2 * 16);
     cudaMemset(out, 0, 2 * n2 * 16);
-    for (int occ : {4, 8, 16}) {
+    for (int occ : {8}) {
         const int bl = sms * occ;
         run<2, 0, 4>("read 2 streams", in, out, n2, sink, bl, 256);
         run<1, 1, 4>("copy 1:1", in, out, n2, sink, bl, 256);
