@@ -9,7 +9,7 @@ for c in 7pt256 27pt256 9pt4096; do
   timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --operator stencil --config $c > gpurun_out/bench_mf_$c.json 2> gpurun_out/bench_mf_$c.err; echo "mf $c $(tail -1 gpurun_out/bench_mf_$c.err)"
 done
 timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --solver tfqmr > gpurun_out/bench_tfqmr.json 2> gpurun_out/bench_tfqmr.err; echo "tfqmr $(tail -1 gpurun_out/bench_tfqmr.err)"
-timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -s 123 -c 82 --csv --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline > /dev/null 2>&1; echo ncu launches rc $?
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -s 126 -c 84 --csv --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline > /dev/null 2>&1; echo ncu launches rc $?
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_spmv_tma -s 4 -c 1 -o gpurun_out/prof_k1 -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline > /dev/null 2>&1; echo ncu k1 rc $?
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_cg_update -s 4 -c 1 -o gpurun_out/prof_k2 -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline > /dev/null 2>&1; echo ncu k2 rc $?
 timeout 600 ncu --set full --clock-control none -k regex:k_spmv_tma -s 4 -c 1 -o gpurun_out/prof_k1_27pt -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline --config 27pt256 > /dev/null 2>&1; echo ncu k1 27pt rc $?
