@@ -687,6 +687,8 @@ struct rvk_cg_plan_s {
     SpmvArgs      sa{};
     int           spmv_grid = 0, upd_grid = 0, setup_grid = 0, persist_grid = 0;
     int           mode = RVK_CG_MODE_FUSED; // resolved (AUTO -> FUSED | PERSISTENT)
+    int           cluster = 0;              // PERSISTENT: CTAs of the one-cluster DSMEM solve (0: grid barriers)
+    int           maxlen  = 0;              // longest row
     bool          stencil = false;          // matrix-free operator (rvk_cg_plan_create_stencil)
     StencilGeom   geom{};
     double        dconst = 0.0;             // constant dinv (stencil, or a detected constant diagonal)
@@ -1153,6 +1155,8 @@ rvk_status enqueue_persistent(rvk_cg_plan P, const double* b, double* x)
                   P->z, P->p[0], P->p[1], P->w, P->hist, P->st, P->partials, P->cfg.max_it,
                   P->cfg.rtol, P->cfg.atol};
     P->launches = 1;
+    if (P->cluster)
+        return launch_cluster(P->ctx->stream, a, P->cfg.pc == RVK_PC_JACOBI, P->cluster, P->maxlen);
     return launch_persistent(P->ctx->stream, a, P->cfg.pc == RVK_PC_JACOBI, P->persist_grid);
 }
 
@@ -1401,11 +1405,14 @@ rvk_status rvk_cg_plan_create(rvk_ctx ctx, const rvk_csr* A, rvk_cg_config cfg, 
     P->setup_grid = resident_grid(k_cg_setup<true, 1>, kUpdThreads, (A->n_rows + 1) / 2);
     P->persist_grid = persistent_grid(A->n_rows);
     P->mode         = cfg.mode;
+    P->maxlen = (int)std::min<int64_t>(maxlen, 1 << 30);
+    if (cfg.mode == RVK_CG_MODE_AUTO || cfg.mode == RVK_CG_MODE_PERSISTENT)
+        P->cluster = cluster_ctas(A->n_rows, maxlen);
     if (cfg.mode == RVK_CG_MODE_AUTO) {
-        // one persistent kernel while the solve's working set stays in L2
-        // (launch latency dominates there); the HBM-streaming path beyond
+        // up to 16 K rows: the one-cluster DSMEM solve (one launch, cluster
+        // barriers); above, the HBM-streaming fused graph
         const int64_t ws = 12 * A->nnz + 8 * (A->n_rows + 1) + 9 * 8 * A->n_rows;
-        P->mode          = ws <= kPersistentMaxBytes ? RVK_CG_MODE_PERSISTENT : RVK_CG_MODE_FUSED;
+        P->mode = (P->cluster || ws <= kPersistentMaxBytes) ? RVK_CG_MODE_PERSISTENT : RVK_CG_MODE_FUSED;
     }
     const size_t vb = (size_t)A->n_rows * sizeof(double);
     cudaError_t  e  = cudaSuccess;

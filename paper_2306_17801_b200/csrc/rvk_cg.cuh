@@ -171,6 +171,9 @@ struct PersistArgs {
 };
 int        persistent_grid(int64_t n);
 rvk_status launch_persistent(cudaStream_t s, const PersistArgs& args, bool jacobi, int grid);
+// one-cluster DSMEM solve (rvk_cg_small.cu): cluster size or 0 (not eligible)
+int        cluster_ctas(int64_t n, int64_t max_row_len);
+rvk_status launch_cluster(cudaStream_t s, const PersistArgs& args, bool jacobi, int ctas, int max_row_len);
 
 // After the last iteration (or an early exit): apply the updates DEFER K2s
 // left pending, in iteration order: x = ((x + a_0 p_0) + a_1 p_1) + ... .

@@ -17,6 +17,7 @@
 #include "rvk_internal.hpp"
 
 #include <cooperative_groups.h>
+#include <cstdlib>
 
 namespace cg = cooperative_groups;
 
@@ -198,6 +199,167 @@ __global__ void __launch_bounds__(kPThreads) k_cg_persistent(PersistArgs a)
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// Thread-block-cluster solve for the smallest grids (n <= 16 x 1024 rows):
+// ONE cluster of C = ceil(n / 1024) CTAs (<= 16, non-portable size), one row
+// per thread.  The gathered vectors z and p (ping-pong) live in the CTAs'
+// shared memory and neighbours read them through distributed shared memory
+// (DSMEM); r, w, x, dinv and the row's CSR entries (<= 9) stay in registers
+// for the whole solve.  Two cluster barriers per iteration (after p.w and
+// after z.z / z.r), each preceded by every CTA storing its block partial into
+// a slot of EVERY CTA, so each CTA folds the C partials in rank order and all
+// derive identical scalars and exit decisions.  Element arithmetic as
+// k_cg_persistent (the reference's mul-then-add order).  Replaces 41 launches
+// (or 60 grid barriers) by one launch and 40 cluster barriers.
+constexpr int kCRows   = 1024; // rows per CTA = threads per CTA
+constexpr int kCMaxCta = 16;
+constexpr int kCMaxNnz = 9;
+
+template <bool JACOBI, int NZ> // NZ: longest row (5, 7 or 9), sizes the register arrays
+__global__ void __launch_bounds__(kCRows, 1) k_cg_cluster(PersistArgs a)
+{
+    cg::cluster_group cl = cg::this_cluster();
+    __shared__ double zs[kCRows], pb[2][kCRows];
+    __shared__ double slot_a[kCMaxCta], slot_b[kCMaxCta][2];
+    __shared__ double red[64];
+    const int     C    = (int)cl.num_blocks();
+    const int     q    = (int)cl.block_rank();
+    const int     tid  = threadIdx.x;
+    const int64_t i    = (int64_t)q * kCRows + tid;
+    const bool    own  = i < a.n;
+    const bool    lead = q == 0 && tid == 0;
+
+    // the row's entries: value + generic (DSMEM) address of z[col] in its CTA;
+    // p_old / p_new sit at fixed offsets from it (same layout in every CTA)
+    const double* zp[NZ];
+    double        va[NZ];
+    int           cnt = 0;
+    if (own) {
+        const int64_t kb = a.off[i], ke = a.off[i + 1];
+        cnt              = (int)(ke - kb);
+#pragma unroll
+        for (int k = 0; k < NZ; ++k) {
+            if (k < cnt) {
+                const int32_t c = a.cols[kb + k];
+                va[k]           = a.vals[kb + k];
+                zp[k]           = cl.map_shared_rank(&zs[c & (kCRows - 1)], c / kCRows);
+            } else {
+                va[k] = 0.0;
+                zp[k] = &zs[0];
+            }
+        }
+    }
+    const ptrdiff_t to_p0 = &pb[0][0] - &zs[0], to_p1 = &pb[1][0] - &zs[0];
+
+    // publish this CTA's block partial(s) into every CTA's slots, then barrier
+    auto publish = [&](double* slots, int stride_d, const double* v, int nv) {
+        if (tid == 0)
+            for (int t = 0; t < C; ++t) {
+                double* dst = cl.map_shared_rank(slots, t);
+                for (int j = 0; j < nv; ++j) dst[q * stride_d + j] = v[j];
+            }
+        cl.sync();
+    };
+    auto fold = [&](const double* slots, int stride_d, int j) {
+        double v = 0.0;
+        for (int t = 0; t < C; ++t) v = add(v, slots[t * stride_d + j]);
+        return v;
+    };
+
+    // ---- setup: r = b, x = 0, z = B r; z.z, z.r ------------------------------
+    const double d  = (own && JACOBI) ? a.dinv[i] : 1.0;
+    double       r  = own ? a.b[i] : 0.0;
+    double       z  = JACOBI ? mul(d, r) : r;
+    double       x  = 0.0;
+    double       pv = 0.0; // this row's current p
+    zs[tid]         = z;
+    double acc[2]   = {own ? mul(z, z) : 0.0, own ? mul(z, r) : 0.0};
+    block_sum<2>(acc, red, tid, kCRows, 1);
+    publish(&slot_b[0][0], 2, acc, 2);
+    double       beta = fold(&slot_b[0][0], 2, 1);
+    const double dp0  = sqrt(fold(&slot_b[0][0], 2, 0));
+    int          state = RVK_CG_RUNNING, iters = 0, bk = -1;
+    double       alpha = 0.0, pAp = 0.0, betaold = 0.0, dp = dp0;
+    if (cg_converged(dp0, dp0, a.rtol, a.atol)) state = RVK_CG_CONVERGED;
+
+    for (int it = 0; it < a.max_it && state == RVK_CG_RUNNING; ++it) {
+        // ---- w = A p with p = z + b p_old formed per gathered entry ----------
+        double bb = 0.0;
+        if (it > 0) {
+            if (betaold == 0.0) {
+                state = RVK_CG_BREAKDOWN;
+                bk    = it;
+                break;
+            }
+            bb = beta / betaold;
+        }
+        const int       po = it & 1, pn = po ^ 1;
+        const ptrdiff_t tp = po ? to_p1 : to_p0;
+        double          w  = 0.0;
+        if (own) {
+            double g[NZ];
+#pragma unroll
+            for (int k = 0; k < NZ; ++k) {
+                if (k < cnt) {
+                    const double zj = zp[k][0];
+                    g[k]            = it == 0 ? zj : aypx1(bb, zj, zp[k][tp]);
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < NZ; ++k)
+                if (k < cnt) w = add(w, mul(va[k], g[k]));
+            pv          = it == 0 ? zs[tid] : aypx1(bb, zs[tid], pb[po][tid]);
+            pb[pn][tid] = pv;
+        }
+        double v1[1] = {own ? mul(pv, w) : 0.0};
+        block_sum<1>(v1, red, tid, kCRows, 1);
+        publish(slot_a, 1, v1, 1);
+        pAp             = fold(slot_a, 1, 0);
+        const double al = beta / pAp;
+        if (pAp == 0.0 || !isfinite(al)) {
+            state = RVK_CG_BREAKDOWN;
+            bk    = it;
+            break;
+        }
+        alpha   = al;
+        betaold = beta;
+        // ---- x += a p, r += (-a) w, z = B r; z.z, z.r ------------------------
+        x        = axpy1(al, pv, x);
+        r        = axpy1(-al, w, r);
+        z        = JACOBI ? mul(d, r) : r;
+        zs[tid]  = z;
+        acc[0]   = own ? mul(z, z) : 0.0;
+        acc[1]   = own ? mul(z, r) : 0.0;
+        block_sum<2>(acc, red, tid, kCRows, 1);
+        publish(&slot_b[0][0], 2, acc, 2);
+        dp    = sqrt(fold(&slot_b[0][0], 2, 0));
+        iters = it + 1;
+        if (lead) a.hist[it + 1] = dp;
+        if (cg_converged(dp, dp0, a.rtol, a.atol)) state = RVK_CG_CONVERGED;
+        beta = fold(&slot_b[0][0], 2, 1);
+    }
+    if (own) {
+        a.x[i] = x;
+        a.r[i] = r;
+        a.z[i] = z;
+    }
+    if (lead) {
+        a.hist[0]            = dp0;
+        a.st->dp0            = dp0;
+        a.st->dp             = dp;
+        a.st->alpha          = alpha;
+        a.st->pAp            = pAp;
+        a.st->beta           = beta;
+        a.st->betaold        = betaold;
+        a.st->iterations     = iters;
+        a.st->breakdown_iter = bk;
+        a.st->state          = state;
+        a.st->done           = 1;
+    }
+    cl.sync(); // no CTA leaves while a neighbour may still address its shared memory
+}
+
 } // namespace
 
 int persistent_grid(int64_t n)
@@ -210,6 +372,57 @@ int persistent_grid(int64_t n)
     const int64_t cap  = (int64_t)sm_count() * std::min(per_sm, 2);
     const int64_t want = (n + kPThreads * 4 - 1) / (kPThreads * 4); // >= 4 rows per thread
     return (int)std::max<int64_t>(1, std::min(cap, want));
+}
+
+// Cluster size for the DSMEM solve, 0 when the system does not qualify
+// (n > 16 x 1024 rows, rows longer than kCMaxNnz, or no co-resident cluster).
+int cluster_ctas(int64_t n, int64_t max_row_len)
+{
+    const char* e = std::getenv("RVK_CLUSTER");
+    if ((e && e[0] == '0') || n < 1 || max_row_len > kCMaxNnz || n > (int64_t)kCMaxCta * kCRows) return 0;
+    const int C = (int)((n + kCRows - 1) / kCRows);
+    for (auto fn : {k_cg_cluster<true, 5>, k_cg_cluster<false, 5>, k_cg_cluster<true, 7>,
+                    k_cg_cluster<false, 7>, k_cg_cluster<true, 9>, k_cg_cluster<false, 9>})
+        if (C > 8 && cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+            cudaGetLastError();
+            return 0;
+        }
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id               = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = C;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.gridDim            = dim3(C);
+    cfg.blockDim           = dim3(kCRows);
+    cfg.attrs              = at;
+    cfg.numAttrs           = 1;
+    int nc                 = 0;
+    if (cudaOccupancyMaxActiveClusters(&nc, k_cg_cluster<true, 9>, &cfg) != cudaSuccess || nc < 1) {
+        cudaGetLastError();
+        return 0;
+    }
+    return C;
+}
+
+rvk_status launch_cluster(cudaStream_t s, const PersistArgs& args, bool jacobi, int C, int nz)
+{
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id               = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = C;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.gridDim            = dim3(C);
+    cfg.blockDim           = dim3(kCRows);
+    cfg.stream             = s;
+    cfg.attrs              = at;
+    cfg.numAttrs           = 1;
+    auto go = [&](auto fn) { return cudaLaunchKernelEx(&cfg, fn, args); };
+    if (nz <= 5) RVK_CUDA(jacobi ? go(k_cg_cluster<true, 5>) : go(k_cg_cluster<false, 5>));
+    else if (nz <= 7) RVK_CUDA(jacobi ? go(k_cg_cluster<true, 7>) : go(k_cg_cluster<false, 7>));
+    else RVK_CUDA(jacobi ? go(k_cg_cluster<true, 9>) : go(k_cg_cluster<false, 9>));
+    return RVK_OK;
 }
 
 rvk_status launch_persistent(cudaStream_t s, const PersistArgs& args, bool jacobi, int grid)

@@ -1,7 +1,7 @@
 exec > gpurun_out/dcg.log 2>&1
-for h in 0 1 3; do
-RVK_L2_HINTS=$h timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --config 7pt768 2>&1 >/dev/null | tail -1 | sed "s/^/768 h=$h /"
-done
-for h in 0 1 3; do
-RVK_L2_HINTS=$h timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline 2>&1 >/dev/null | tail -1 | sed "s/^/256 h=$h /"
-done
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "persistent" 2>&1 | tail -5
+for c in 5pt64 5pt128 5pt256 5pt512; do
+for m in auto fused; do
+timeout 300 python bench.py --steps 20 --warmup 5 --no-cpu-baseline --config $c --mode $m 2>&1 >/dev/null | tail -1 | sed "s/^/$c $m /"
+done; done
+RVK_CLUSTER=0 timeout 300 python bench.py --steps 20 --warmup 5 --no-cpu-baseline --config 5pt64 --mode persistent 2>&1 >/dev/null | tail -1 | sed "s/^/5pt64 gridbarrier /"
