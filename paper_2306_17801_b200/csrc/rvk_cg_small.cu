@@ -252,6 +252,8 @@ __global__ void __launch_bounds__(kCRows, 1) k_cg_cluster(PersistArgs a)
     }
     const ptrdiff_t to_p0 = &pb[0][0] - &zs[0], to_p1 = &pb[1][0] - &zs[0];
 
+    // every CTA of the cluster is running before anyone touches DSMEM
+    cl.sync();
     // publish this CTA's block partial(s) into every CTA's slots, then barrier
     auto publish = [&](double* slots, int stride_d, const double* v, int nv) {
         if (tid == 0)

@@ -16,7 +16,7 @@ def main(parts=("csr", "mf", "dcg", "tfqmr", "irregular")):
     for dim, pts, g in [(2, 5, (33, 17)), (3, 7, (9, 8, 7)), (3, 27, (7, 6, 5)), (2, 9, (40, 37))]:
         A = rvk.DeviceCsr.laplacian(ctx, dim, pts, g)
         b = O.rhs(A.n_rows)
-        for mode in ("fused", "unfused"):
+        for mode in ("fused", "unfused", "persistent"):  # persistent: the cluster kernel (27-pt: grid barriers)
             for graph in (False, True):
                 plan = rvk.CgPlan(ctx, A, max_it=20, mode=mode, use_graph=graph)
                 x, res = plan.solve_host(b)

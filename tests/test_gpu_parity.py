@@ -734,3 +734,59 @@ def test_tiny_systems_every_path(ctx, spec, graph):
         assert rel < 1e-10, rel
         assert np.linalg.norm(x - ref.x) <= 1e-10 * np.linalg.norm(ref.x)
         plan.close()
+
+
+def check_cg_floor(res, x, ref):
+    """check_cg, with the history compared while it is above 1e-8 of its
+    start (a tiny system reaches rounding noise within a few iterations)."""
+    assert res.iterations == ref.iterations and res.state == ref.status
+    keep = ref.hist > 1e-8 * ref.hist[0]
+    rel = np.max(np.abs(res.hist[keep] - ref.hist[keep]) / ref.hist[keep])
+    assert rel < HIST_RTOL, rel
+    assert np.linalg.norm(x - ref.x) <= X_RTOL * np.linalg.norm(ref.x)
+
+
+@pytest.mark.parametrize("spec", [(2, 5, (64, 64)), (2, 5, (128, 128)), (2, 5, (33, 31)),
+                                  (2, 9, (100, 90)), (3, 7, (20, 16, 12)), (3, 7, (32, 32, 16)),
+                                  (2, 5, (2, 2)), (2, 5, (1024, 16)), (2, 5, (1025, 16))])
+@pytest.mark.parametrize("pc", ["jacobi", "none"])
+def test_cluster_solve(ctx, spec, pc, monkeypatch):
+    """The one-cluster DSMEM solve (k_cg_cluster; PERSISTENT / AUTO for
+    n <= 16 x 1024 rows with rows of <= 9 entries): oracle within 1e-10, the
+    same result as the grid-barrier persistent kernel (RVK_CLUSTER=0), early
+    exits, and the eligibility boundary (16384 rows: 16 CTAs; 16400: none)."""
+    dim, pts, g = spec
+    Ah = O.build_laplacian(dim, pts, g)
+    b = O.rhs(Ah.n_rows)
+    A = rvk.DeviceCsr.laplacian(ctx, dim, pts, g)
+    for max_it, rtol in ((20, 0.0), (200, 1e-6)):
+        ref = O.cg_solve(Ah, b, max_it=max_it, rtol=rtol, pc=pc)
+        plan = rvk.CgPlan(ctx, A, max_it=max_it, rtol=rtol, pc=pc, mode="auto")
+        assert bool(plan.flags() & 256) == (Ah.n_rows <= 16384)
+        x, res = plan.solve_host(b)
+        check_cg_floor(res, x, ref)
+        x2, res2 = plan.solve_host(b)  # repeatable
+        assert np.array_equal(x, x2) and np.array_equal(res.hist, res2.hist)
+        monkeypatch.setenv("RVK_CLUSTER", "0")
+        grid = rvk.CgPlan(ctx, A, max_it=max_it, rtol=rtol, pc=pc, mode="persistent")
+        monkeypatch.delenv("RVK_CLUSTER")
+        assert not grid.flags() & 256
+        xg, resg = grid.solve_host(b)
+        check_cg_floor(resg, xg, ref)
+        assert res.iterations == resg.iterations
+
+
+def test_cluster_breakdown_and_identity(ctx):
+    """A = I converges in one iteration and a zero right-hand
+    side exits at the initial check, through the cluster kernel."""
+    n = 300
+    off = np.arange(n + 1, dtype=np.int64)
+    cols = np.arange(n, dtype=np.int32)
+    I = rvk.DeviceCsr.from_host(ctx, n, n, off, cols, np.ones(n))
+    b = O.rhs(n)
+    plan = rvk.CgPlan(ctx, I, max_it=20, rtol=1e-12, mode="auto")
+    assert plan.flags() & 256
+    x, res = plan.solve_host(b)
+    assert res.iterations == 1 and np.array_equal(x, b)
+    x0, res0 = plan.solve_host(np.zeros(n))
+    assert res0.iterations == 0 and not np.any(x0)
