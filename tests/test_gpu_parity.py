@@ -790,3 +790,64 @@ def test_cluster_breakdown_and_identity(ctx):
     assert res.iterations == 1 and np.array_equal(x, b)
     x0, res0 = plan.solve_host(np.zeros(n))
     assert res0.iterations == 0 and not np.any(x0)
+
+
+def random_spd_csr(rng, n, max_deg, long_rows=()):
+    """Symmetric positive definite, irregular: a random weighted graph
+    Laplacian (row lengths 1 .. ~2 max_deg, a few very long rows) plus a
+    random positive diagonal shift -- non-constant diagonal, no stencil
+    bands, integer-free values."""
+    deg = rng.integers(0, max_deg + 1, n)
+    src = np.repeat(np.arange(n), deg)
+    dst = rng.integers(0, n, src.size)
+    for r, L in long_rows:
+        src = np.concatenate([src, np.full(L, r)])
+        dst = np.concatenate([dst, rng.choice(n, L, replace=False)])
+    keep = src != dst
+    src, dst = src[keep], dst[keep]
+    w = rng.uniform(0.1, 1.0, src.size)
+    i = np.concatenate([src, dst])
+    j = np.concatenate([dst, src])
+    v = -np.concatenate([w, w])
+    key = i.astype(np.int64) * n + j
+    order = np.argsort(key, kind="stable")
+    key, v = key[order], v[order]
+    uk, start = np.unique(key, return_index=True)
+    vs = np.add.reduceat(v, start)  # merge duplicate edges
+    ii, jj = uk // n, uk % n
+    diag = np.zeros(n)
+    np.add.at(diag, ii, -vs)
+    diag += rng.uniform(0.5, 2.0, n)
+    ii = np.concatenate([ii, np.arange(n)])
+    jj = np.concatenate([jj, np.arange(n)])
+    vv = np.concatenate([vs, diag])
+    order = np.lexsort((jj, ii))
+    ii, jj, vv = ii[order], jj[order], vv[order]
+    off = np.zeros(n + 1, np.int64)
+    np.add.at(off, ii + 1, 1)
+    off = np.cumsum(off)
+    return O.Csr(n, n, off, jj.astype(np.int32), vv)
+
+
+@pytest.mark.parametrize("seed,n,max_deg,long_rows", [
+    (0, 3000, 4, ()), (1, 50000, 6, ()), (2, 120001, 3, ((7, 5000), (99999, 12000))),
+    (3, 9000, 12, ())])
+@pytest.mark.parametrize("mode,graph", [("fused", True), ("fused", False), ("fused", "while"),
+                                        ("unfused", True), ("persistent", False)])
+def test_cg_irregular_spd(ctx, seed, n, max_deg, long_rows, mode, graph):
+    """Jacobi-CG on irregular SPD matrices (nothing stencil-shaped: no
+    bands for the prefetch windows, a per-row Jacobi diagonal, rows from 1
+    to 12000 entries) in every mode, against the oracle on the same CSR,
+    fixed iterations and a device-side tolerance exit."""
+    rng = np.random.default_rng(seed)
+    Ah = random_spd_csr(rng, n, max_deg, long_rows)
+    A = rvk.DeviceCsr.from_host(ctx, Ah.n_rows, Ah.n_cols, Ah.off, Ah.cols, Ah.vals)
+    A.validate(ctx)
+    b = O.rhs(n)
+    for max_it, rtol in ((20, 0.0), (200, 1e-8)):
+        ref = O.cg_solve(Ah, b, max_it=max_it, rtol=rtol)
+        plan = rvk.CgPlan(ctx, A, max_it=max_it, rtol=rtol, mode=mode, use_graph=graph)
+        assert not plan.flags() & 1  # the diagonal is not constant
+        x, res = plan.solve_host(b)
+        check_cg_floor(res, x, ref)
+        plan.close()
