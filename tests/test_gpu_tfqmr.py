@@ -205,3 +205,27 @@ def test_tfqmr_constant_diagonal_bitexact(ctx, spec, monkeypatch):
     assert np.array_equal(x1, x0)
     assert np.array_equal(r1.hist, r0.hist)
     check(r1, x1, O.tfqmr_solve(Ah, b, max_it=20))
+
+
+@pytest.mark.parametrize("seed,n,nonsym", [(0, 4000, False), (1, 60000, False), (2, 30000, True)])
+@pytest.mark.parametrize("mode", MODES)
+def test_tfqmr_irregular(ctx, seed, n, nonsym, mode):
+    """Irregular matrices (random weighted graph Laplacian + positive shift;
+    nonsym: the off-diagonal entries of one triangle scaled by 0.5, still
+    diagonally dominant): fused and unfused TFQMR against the oracle on the
+    same CSR, per-row Jacobi diagonal."""
+    from test_gpu_parity import random_spd_csr
+    rng = np.random.default_rng(seed)
+    Ah = random_spd_csr(rng, n, 5)
+    if nonsym:
+        rows = np.repeat(np.arange(n), np.diff(Ah.off))
+        upper = Ah.cols > rows
+        vals = Ah.vals.copy()
+        vals[upper] *= 0.5
+        Ah = O.Csr(n, n, Ah.off, Ah.cols, vals)
+    A = rvk.DeviceCsr.from_host(ctx, Ah.n_rows, Ah.n_cols, Ah.off, Ah.cols, Ah.vals)
+    b = O.rhs(n)
+    ref = O.tfqmr_solve(Ah, b, max_it=20)
+    plan, x, res = solve(ctx, A, b, max_it=20, mode=mode)
+    assert not plan.flags() & 1
+    check(res, x, ref)
