@@ -17,7 +17,9 @@ enum class SolverMethod { CG, TFQMR };
 //        contexts (dctx_a/b/c exactly as SPEC.md:497 assigns them).
 // SyncBaseline: the same math on the globally-blocking context.
 // Fused: the B200 path -- 2 fused kernels per iteration captured as one CUDA
-//        graph, every scalar device-resident (default).
+//        graph, every scalar device-resident (default); CG on
+//        small systems (<= 16 K rows of <= 9 entries) runs as ONE kernel on
+//        one thread-block cluster instead.
 enum class SolverMode { Async, SyncBaseline, Fused };
 enum class PcType { Jacobi, None };
 
