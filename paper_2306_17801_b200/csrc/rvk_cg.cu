@@ -1388,6 +1388,10 @@ rvk_status rvk_cg_plan_create(rvk_ctx ctx, const rvk_csr* A, rvk_cg_config cfg, 
     if (std::getenv("RVK_NO_PREFETCH")) win.has_lead = false;
     P->sa        = make_spmv_args(*A, maxlen, &win, 2);
     spmv_set_order(P->sa, bands, A->nnz, 2, sm_count());
+    {
+        const char* e = std::getenv("RVK_SMALL_ROWS");
+        P->sa.small_rows = e ? std::min<int64_t>(std::atoll(e), 512 * 1024) : 0;
+    }
     if (std::getenv("RVK_DEBUG")) {
         std::fprintf(stderr, "[rvk] plan n=%lld nnz=%lld R=%d stages=%d groups=%d cap=%d nwin=%d "
                              "order=%s(tiles/plane=%lld tiles/chunk=%lld)",

@@ -116,6 +116,7 @@ struct SpmvArgs {
     // plan-owned int32 copy of the row offsets (nnz < 2^31; padded by >= 4
     // entries) or null: the mainloop then streams 4 instead of 8 B per row
     const int32_t* off32;
+    int64_t        small_rows; // > 0: systems up to this many rows use k_spmv_small (plan's choice)
 
     size_t smem_bytes() const { return kSpmvHeaderBytes + (size_t)stages * stage_bytes; }
 };
@@ -670,10 +671,65 @@ struct SpmvGuardedOp : SpmvPlainOp {
     __device__ __forceinline__ bool init() { return *guard == 0; }
 };
 
+// Small systems: no TMA ring, no warp specialisation -- plain blocks of
+// kSpmvSmallThreads, one row per thread through the same per-row code as the
+// TMA kernel's direct tiles (identical row sums), then the same block-sum /
+// last-block tail.  A 544-thread warp-specialised CTA per SM with its
+// mbarrier ring is pure ramp-up latency when the whole operand set is a few
+// MB in L2 (SpmvArgs::small_rows).
+constexpr int kSpmvSmallThreads = 256;
+template <class Op, int U>
+__global__ void __launch_bounds__(kSpmvSmallThreads) k_spmv_small(SpmvArgs A, Op op_in, TailArgs tail)
+{
+    __shared__ double red[32 * 4];
+    __shared__ int    flag;
+    pdl_trigger();
+    pdl_wait();
+    Op op = op_in;
+    if (!op.init()) return;
+    constexpr int NS = spmv_sums<Op>::value;
+    spmv_acc_t<Op> acc{};
+    const int64_t r0   = (int64_t)blockIdx.x * kSpmvSmallThreads;
+    const int     rows = (int)min((int64_t)kSpmvSmallThreads, A.n_rows - r0);
+    acc = spmv_rows_direct<U>(op, acc, (int)threadIdx.x, kSpmvSmallThreads, rows, r0, A.off + r0, A.cols,
+                              A.vals);
+    if constexpr (Op::kHasTail) {
+        const int tid = threadIdx.x;
+        double    v[NS];
+        if constexpr (NS == 1) v[0] = acc;
+        else {
+#pragma unroll
+            for (int j = 0; j < NS; ++j) v[j] = acc.v[j];
+        }
+        block_sum<NS>(v, red, tid, kSpmvSmallThreads, 1);
+        if (tid == 0) {
+#pragma unroll
+            for (int j = 0; j < NS; ++j) tail.partials[(size_t)blockIdx.x * NS + j] = v[j];
+        }
+        if (!last_block<spmv_sys_fence<Op>::value>(tail.ticket, tid, &flag, kSpmvSmallThreads, 1)) return;
+        fold_partials<NS>(tail.partials, gridDim.x, v, red, tid, kSpmvSmallThreads, 1);
+        if (tid == 0) {
+            if constexpr (NS == 1) op.tail(v[0]);
+            else op.tail(v);
+            *tail.ticket = 0u;
+        }
+    }
+}
+
 template <class Op>
 rvk_status launch_spmv(cudaStream_t stream, const SpmvArgs& a, const Op& op, TailArgs tail,
                        int grid)
 {
+    if (a.small_rows && a.n_rows <= a.small_rows && !a.off32) {
+        const int g = (int)((a.n_rows + kSpmvSmallThreads - 1) / kSpmvSmallThreads);
+        cudaError_t e;
+        if (a.unroll == 7) e = launch_pdl(k_spmv_small<Op, 7>, g, kSpmvSmallThreads, 0, stream, a, op, tail);
+        else if (a.unroll == 9) e = launch_pdl(k_spmv_small<Op, 9>, g, kSpmvSmallThreads, 0, stream, a, op, tail);
+        else e = launch_pdl(k_spmv_small<Op, 8>, g, kSpmvSmallThreads, 0, stream, a, op, tail);
+        if (e != cudaSuccess) return cuda_error(e, "k_spmv_small launch");
+        RVK_CHECK_LAUNCH("k_spmv_small");
+        return RVK_OK;
+    }
     static bool configured = false; // per instantiation; before any graph capture
     const int   smax       = (int)(kSpmvHeaderBytes + kSpmvStageBudget);
     if (!configured) {

@@ -851,3 +851,24 @@ def test_cg_irregular_spd(ctx, seed, n, max_deg, long_rows, mode, graph):
         x, res = plan.solve_host(b)
         check_cg_floor(res, x, ref)
         plan.close()
+
+
+@pytest.mark.parametrize("spec", [(2, 5, (256, 256)), (3, 7, (20, 16, 12)), (3, 27, (10, 9, 8)),
+                                  (2, 9, (33, 31)), (2, 5, (2, 2))])
+@pytest.mark.parametrize("graph", [True, "while"])
+def test_small_spmv_kernel(ctx, spec, graph, monkeypatch):
+    """Opt-in small-system K1 (RVK_SMALL_ROWS: k_spmv_small, plain blocks
+    through the TMA kernel's direct-row code): oracle within 1e-10 and the
+    same x as the TMA kernel up to the reduction order of p.w."""
+    dim, pts, g = spec
+    Ah = O.build_laplacian(dim, pts, g)
+    b = O.rhs(Ah.n_rows)
+    A = rvk.DeviceCsr.laplacian(ctx, dim, pts, g)
+    for max_it, rtol in ((20, 0.0), (200, 1e-6)):
+        ref = O.cg_solve(Ah, b, max_it=max_it, rtol=rtol)
+        monkeypatch.setenv("RVK_SMALL_ROWS", "524288")
+        plan = rvk.CgPlan(ctx, A, max_it=max_it, rtol=rtol, use_graph=graph)
+        monkeypatch.delenv("RVK_SMALL_ROWS")
+        x, res = plan.solve_host(b)
+        check_cg_floor(res, x, ref)
+        plan.close()
