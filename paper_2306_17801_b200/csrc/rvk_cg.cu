@@ -1388,10 +1388,8 @@ rvk_status rvk_cg_plan_create(rvk_ctx ctx, const rvk_csr* A, rvk_cg_config cfg, 
     if (std::getenv("RVK_NO_PREFETCH")) win.has_lead = false;
     P->sa        = make_spmv_args(*A, maxlen, &win, 2);
     spmv_set_order(P->sa, bands, A->nnz, 2, sm_count());
-    {
-        const char* e = std::getenv("RVK_SMALL_ROWS");
-        P->sa.small_rows = e ? std::min<int64_t>(std::atoll(e), 512 * 1024) : 0;
-    }
+    const char* small_env = std::getenv("RVK_SMALL_ROWS");
+    P->sa.small_rows = small_env ? std::min<int64_t>(std::atoll(small_env), 512 * 1024) : 0;
     if (std::getenv("RVK_DEBUG")) {
         std::fprintf(stderr, "[rvk] plan n=%lld nnz=%lld R=%d stages=%d groups=%d cap=%d nwin=%d "
                              "order=%s(tiles/plane=%lld tiles/chunk=%lld)",
@@ -1417,6 +1415,10 @@ rvk_status rvk_cg_plan_create(rvk_ctx ctx, const rvk_csr* A, rvk_cg_config cfg, 
         // barriers); above, the HBM-streaming fused graph
         const int64_t ws = 12 * A->nnz + 8 * (A->n_rows + 1) + 9 * 8 * A->n_rows;
         P->mode = (P->cluster || ws <= kPersistentMaxBytes) ? RVK_CG_MODE_PERSISTENT : RVK_CG_MODE_FUSED;
+        // and up to 512 K rows the plain-block K1 (k_spmv_small: 256^2 5-point
+        // solve 0.229 -> 0.211 ms; explicit FUSED keeps the TMA kernel unless
+        // RVK_SMALL_ROWS asks)
+        if (!small_env) P->sa.small_rows = 512 * 1024;
     }
     const size_t vb = (size_t)A->n_rows * sizeof(double);
     cudaError_t  e  = cudaSuccess;
