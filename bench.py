@@ -246,6 +246,13 @@ def run_reference(args, cfg):
         solve()
         times.append((time.perf_counter() - t0) * 1e3 * scale)
     ms = statistics.mean(times)
+    # the reference's scalar and AVX2 backends, one solve each
+    per_backend = {}
+    if kind == "reference":
+        for name, be in (("scalar", 0), ("avx2", 1)):
+            t0 = time.perf_counter()
+            O.ref_cg_solve(A, b, max_it=MAX_IT, backend=be)
+            per_backend[name] = round((time.perf_counter() - t0) * 1e3 * scale, 3)
     bm = bytes_model(n_full, nnz_full)
     what = (f"{args.steps} full {MAX_IT}-iteration solves of {desc}" if sample == full else
             f"{args.steps} {MAX_IT}-iteration solves of a {sample} slab of the {full} workload "
@@ -261,7 +268,8 @@ def run_reference(args, cfg):
         "config": {"workload": wl, "n": n_full, "nnz": nnz_full},
         "cpu_baseline": {"value": round(ms, 3), "unit": "ms/solve", "cores": 1, "kind": kind,
                          "sample": what + " (reference kernels_*.cpp, auto AVX2/scalar dispatch, "
-                                          "single-threaded like the reference's kernels)"},
+                                          "single-threaded like the reference's kernels)",
+                         "per_backend_ms": per_backend, "host_cpu": host_cpu()},
         "e2e": {"value": round(ms, 3), "unit": "ms/solve", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "achieved_gbs_bref": round(bm["b_ref_solve"] / (ms * 1e-3) / 1e9, 2),
@@ -269,6 +277,21 @@ def run_reference(args, cfg):
     }
     log(f"reference CPU: {ms:.1f} ms/solve (min {min(times):.1f}); total {time.perf_counter()-t_all:.0f}s")
     print(json.dumps(out), flush=True)
+
+
+def host_cpu() -> dict:
+    """Host CPU model and logical CPU count (stated beside the
+    CPU baseline)."""
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"model": model, "logical_cpus": os.cpu_count()}
 
 
 def _laplacian_size(dim, pts, grid):
@@ -540,7 +563,8 @@ def run_gpu(args, cfg):
         cpu = {"value": round(statistics.mean(ctimes), 1), "unit": "ms/solve", "cores": 1,
                "kind": kind,
                "sample": f"{what} of {desc} on the GPU box host "
-                         "(reference kernels_*.cpp from oracle/_ref, auto dispatch, 1 thread)"}
+                         "(reference kernels_*.cpp from oracle/_ref, auto dispatch, 1 thread)",
+               "host_cpu": host_cpu()}
 
     out = {
         "metric": METRIC, "value": round(ms, 4), "unit": "ms/solve", "n_gpus": 1,
