@@ -76,16 +76,18 @@ def bytes_model(n: int, nnz: int, mode: str = "fused", const_diag: bool = False,
     write 8 n less; K1 gathers r instead of z (same bytes)."""
     ob = 4 if off32 else 8
     # x_group > 4 (the whole solve): K2 never touches x; one k_cg_xfix pass at
-    # the end reads x and the x_group p's and writes x -- counted per solve
-    x_pass = (16 * n + 8 * n * x_group) if (x_defer and x_group > 4) else 0
+    # the end reads the x_group p's and writes x (starting from 0.0: the setup
+    # does not store x = 0 either) -- counted per solve
+    x_pass = (8 * n + 8 * n * x_group) if (x_defer and x_group > 4) else 0
     x_cut = (24 * n if x_pass else 16 * n - 16 * n // x_group) if x_defer else 0
     if mode == "stencil":                        # matrix-free: no CSR, constant dinv
         k1 = 32 * n                              # z, p_old -> p_new, w
         k2 = 56 * n - x_cut - (8 * n if z_virtual else 0)
         b_min = k1 + k2 + x_pass // MAX_IT
+        st = (24 if z_virtual else 32) * n - (8 * n if x_pass else 0)
         return {"k1": k1, "k2": k2, "b_min_iter": b_min, "b_ref_iter": b_min,
-                "b_min_solve": MAX_IT * b_min + (24 if z_virtual else 32) * n,
-                "b_ref_solve": MAX_IT * b_min + (24 if z_virtual else 32) * n,
+                "b_min_solve": MAX_IT * b_min + st,
+                "b_ref_solve": MAX_IT * b_min + st,
                 "b_min_survey_solve": MAX_IT * (12 * nnz + 8 * (n + 1) + 96 * n) + 64 * n,
                 "flops_iter": 2 * nnz + 13 * n}
     if mode == "fused":
@@ -99,7 +101,8 @@ def bytes_model(n: int, nnz: int, mode: str = "fused", const_diag: bool = False,
         k2 = 136 * n                             # aypx 24, dot 16, 2 axpy 48, jacobi 24, norm 8, dot 16
     b_min = k1 + k2 + (x_pass // MAX_IT if mode == "fused" else 0)  # 12 nnz + 8 (n+1) + 96 n plain
     b_ref = 12 * nnz + 8 * (n + 1) + 152 * n     # reference's unfused sequence
-    setup = (56 if (const_diag and mode == "fused") else 64) * n - (8 * n if z_virtual else 0)
+    setup = (56 if (const_diag and mode == "fused") else 64) * n - (8 * n if z_virtual else 0) \
+        - (8 * n if x_pass else 0)
     survey = MAX_IT * (12 * nnz + 8 * (n + 1) + 96 * n) + 64 * n  # SURVEY.md 8d B_min as stated
     return {"k1": k1, "k2": k2, "b_min_iter": b_min, "b_ref_iter": b_ref,
             "b_min_solve": MAX_IT * b_min + setup, "b_ref_solve": MAX_IT * b_ref + setup,

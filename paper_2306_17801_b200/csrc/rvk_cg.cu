@@ -58,7 +58,7 @@ __global__ void __launch_bounds__(kUpdThreads)
     k_cg_setup(int64_t n, const double* __restrict__ b, const double* __restrict__ dinv,
                double* __restrict__ x, double* __restrict__ r, double* __restrict__ z,
                CgState* st, double* hist, double rtol, double atol, double* partials,
-               unsigned int* ticket, double dconst, int zw)
+               unsigned int* ticket, double dconst, int zw, int xw)
 {
     pdl_trigger();
     pdl_wait();
@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(kUpdThreads)
             }
             reinterpret_cast<double2*>(r)[i] = bi;
             if (zw) reinterpret_cast<double2*>(z)[i] = zi; // zw = 0: z stays virtual (d r)
-            st_stream(reinterpret_cast<double2*>(x) + i, make_double2(0.0, 0.0));
+            if (xw) st_stream(reinterpret_cast<double2*>(x) + i, make_double2(0.0, 0.0));
             acc[0] = add(acc[0], mul(zi.x, zi.x));
             acc[0] = add(acc[0], mul(zi.y, zi.y));
             acc[1] = add(acc[1], mul(zi.x, bi.x));
@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(kUpdThreads)
         const double zi = PC == 0 ? bi : mul(PC == 1 ? dinv[i] : dconst, bi);
         r[i] = bi;
         if (zw) z[i] = zi;
-        x[i] = 0.0;
+        if (xw) x[i] = 0.0; // xw = 0: the whole-solve x pass starts from 0.0 itself
         acc[0] = add(acc[0], mul(zi, zi));
         acc[1] = add(acc[1], mul(zi, bi));
     }
@@ -744,13 +744,13 @@ namespace {
 // Launch K0 / K2 for the preconditioner mode: 0 none, 1 dinv vector (CSR),
 // 2 constant dinv (matrix-free stencil: the diagonal is the centre weight).
 template <bool V>
-rvk_status launch_setup(rvk_cg_plan P, int pcm, const double* b, double* x)
+rvk_status launch_setup(rvk_cg_plan P, int pcm, const double* b, double* x, bool xw = true)
 {
     cudaStream_t s = P->ctx->stream;
     auto go = [&](auto kern) {
         launch_pdl(kern, P->setup_grid, kUpdThreads, 0, s, P->A.n_rows, b, P->dinv, x, P->r, P->z,
                    P->st, P->hist, P->cfg.rtol, P->cfg.atol, P->partials, P->tickets, P->dconst,
-                   P->zv ? 0 : 1);
+                   P->zv ? 0 : 1, xw ? 1 : 0);
     };
     if (pcm == 0) go(k_cg_setup<V, 0>);
     else if (pcm == 1) go(k_cg_setup<V, 1>);
@@ -846,14 +846,14 @@ rvk_status launch_update(rvk_cg_plan P, int pcm, const double* p_new, double* x,
     return RVK_OK;
 }
 
-rvk_status launch_xfix(rvk_cg_plan P, double* x, int npb)
+rvk_status launch_xfix(rvk_cg_plan P, double* x, int npb, bool xzero = false)
 {
     XBufs pb{};
     for (int k = 0; k < npb; ++k) pb.p[k] = P->p[k];
     // 4 p streams in flight per thread (measured 7-point 256^3, 20 p's:
     // 2 / 4 / 8 per batch = 500 / 475 / 492 us)
     launch_pdl(k_cg_xfix<4>, P->upd_grid, kUpdThreads, 0, P->ctx->stream, P->A.n_rows, x, pb, npb,
-               (const CgState*)P->st);
+               (const CgState*)P->st, xzero ? 1 : 0);
     RVK_CHECK_LAUNCH("k_cg_xfix");
     return RVK_OK;
 }
@@ -1052,7 +1052,10 @@ rvk_status enqueue_fused(rvk_cg_plan P, const double* b, double* x)
             RVK_CUDA(cudaEventRecordWithFlags(P->ev[k], s, cudaEventRecordExternal));
         return RVK_OK;
     };
-    rvk_status rc = vec ? launch_setup<true>(P, pcm, b, x) : launch_setup<false>(P, pcm, b, x);
+    // whole-solve x group: x is written once, by the final pass, which starts
+    // from 0.0 itself -- the setup skips its x = 0 store (16 n bytes per solve)
+    const bool     xz = defer && P->xq > 4;
+    rvk_status rc = vec ? launch_setup<true>(P, pcm, b, x, !xz) : launch_setup<false>(P, pcm, b, x);
     if (rc != RVK_OK) return rc;
     ++P->launches;
     for (int it = 0; it < P->cfg.max_it; ++it) {
@@ -1072,7 +1075,7 @@ rvk_status enqueue_fused(rvk_cg_plan P, const double* b, double* x)
         if ((rc = rec(4 * it + 3)) != RVK_OK) return rc;
     }
     if (defer) { // the whole-solve group, or an early exit mid-group, leaves x pending
-        if ((rc = launch_xfix(P, x, P->npb)) != RVK_OK) return rc;
+        if ((rc = launch_xfix(P, x, P->npb, xz)) != RVK_OK) return rc;
         ++P->launches;
     }
     return RVK_OK;

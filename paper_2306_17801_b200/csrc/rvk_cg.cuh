@@ -189,12 +189,16 @@ struct XBufs {
 // row-sharded plan passes its buffers' owned slices.)
 template <int V = 0>
 __global__ void __launch_bounds__(kUpdThreads)
-    k_cg_xfix(int64_t n, double* __restrict__ x, XBufs pb, int q, const CgState* __restrict__ st)
+    k_cg_xfix(int64_t n, double* __restrict__ x, XBufs pb, int q, const CgState* __restrict__ st,
+              int xzero)
 {
     pdl_trigger();
     pdl_wait();
+    // xzero: x was not initialised (the whole-solve group): start every
+    // element from 0.0 -- the same adds as from a stored 0.0 -- and write x
+    // even when no update is pending (a solve converged at the setup)
     const int cnt = st->x_pending;
-    if (cnt <= 0) return;
+    if (cnt <= 0 && !xzero) return;
     __shared__ const double* sp[kMaxXq];
     __shared__ double        sa[kMaxXq];
     if (threadIdx.x < cnt) {
@@ -208,7 +212,7 @@ __global__ void __launch_bounds__(kUpdThreads)
     for (int k = 0; k < cnt; ++k) al |= reinterpret_cast<uintptr_t>(sp[k]);
     if (al & 15) { // a shard's owned slice may start mid-16-B: scalar sweep
         for (int64_t i = t0; i < n; i += stride) {
-            double xi = x[i];
+            double xi = xzero ? 0.0 : x[i];
             for (int k = 0; k < cnt; ++k) xi = axpy1(sa[k], sp[k][i], xi);
             x[i] = xi;
         }
@@ -217,7 +221,7 @@ __global__ void __launch_bounds__(kUpdThreads)
     const int64_t n2 = n >> 1;
     double2*      x2 = reinterpret_cast<double2*>(x);
     for (int64_t i = t0; i < n2; i += stride) {
-        double2 xi = ld_stream(x2 + i);
+        double2 xi = xzero ? make_double2(0.0, 0.0) : ld_stream(x2 + i);
         int     k  = 0;
         constexpr int B = V > 0 ? V : 4; // p streams in flight per thread
         for (; k + B <= cnt; k += B) {
@@ -238,7 +242,7 @@ __global__ void __launch_bounds__(kUpdThreads)
         st_stream(x2 + i, xi);
     }
     if ((n & 1) && t0 == 0) {
-        double xi = x[n - 1];
+        double xi = xzero ? 0.0 : x[n - 1];
         for (int k = 0; k < cnt; ++k) xi = axpy1(sa[k], sp[k][n - 1], xi);
         x[n - 1] = xi;
     }

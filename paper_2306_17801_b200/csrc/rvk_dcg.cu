@@ -830,7 +830,7 @@ rvk_status phase_xfix(rvk_dcg_plan P, double* x)
     XBufs pb{};
     for (int k = 0; k < P->npb; ++k) pb.p[k] = P->p[k] + P->sh.halo_lo;
     k_cg_xfix<4><<<P->upd_grid, kUpdThreads, 0, P->ctx->stream>>>(P->sh.n_own, x, pb, P->npb,
-                                                                   P->st);
+                                                                   P->st, 0);
     RVK_CHECK_LAUNCH("k_cg_xfix");
     return RVK_OK;
 }
