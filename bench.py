@@ -84,7 +84,7 @@ def bytes_model(n: int, nnz: int, mode: str = "fused", const_diag: bool = False,
         k1 = 32 * n                              # z, p_old -> p_new, w
         k2 = 56 * n - x_cut - (8 * n if z_virtual else 0)
         b_min = k1 + k2 + x_pass // MAX_IT
-        st = (24 if z_virtual else 32) * n - (8 * n if x_pass else 0)
+        st = (24 if z_virtual else 32) * n - (8 * n if x_pass else 0) - (8 * n if z_virtual else 16 * n)
         return {"k1": k1, "k2": k2, "b_min_iter": b_min, "b_ref_iter": b_min,
                 "b_min_solve": MAX_IT * b_min + st,
                 "b_ref_solve": MAX_IT * b_min + st,
@@ -104,8 +104,10 @@ def bytes_model(n: int, nnz: int, mode: str = "fused", const_diag: bool = False,
     setup = (56 if (const_diag and mode == "fused") else 64) * n - (8 * n if z_virtual else 0) \
         - (8 * n if x_pass else 0)
     survey = MAX_IT * (12 * nnz + 8 * (n + 1) + 96 * n) + 64 * n  # SURVEY.md 8d B_min as stated
+    # fused fixed-iteration solve: the last K2 stores neither r nor z (dead)
+    last = ((8 if z_virtual else 16) * n) if mode == "fused" else 0
     return {"k1": k1, "k2": k2, "b_min_iter": b_min, "b_ref_iter": b_ref,
-            "b_min_solve": MAX_IT * b_min + setup, "b_ref_solve": MAX_IT * b_ref + setup,
+            "b_min_solve": MAX_IT * b_min + setup - last, "b_ref_solve": MAX_IT * b_ref + setup,
             "b_min_survey_solve": survey, "flops_iter": 2 * nnz + 13 * n}
 
 

@@ -266,8 +266,8 @@ __global__ void __launch_bounds__(kUpdThreads)
                 zi.x = mul(v.d.x, ri.x);
                 zi.y = mul(v.d.y, ri.y);
             }
-            r2[i] = ri;
-            if (zw) z2[i] = zi; // zw = 0: z stays virtual (K1 forms d r)
+            if (!(zw & 2)) r2[i] = ri;
+            if (zw & 1) z2[i] = zi; // bit 0 clear: z stays virtual (K1 forms d r); bit 1: last K2, r and z dead
             acc[0] = add(acc[0], mul(zi.x, zi.x));
             acc[0] = add(acc[0], mul(zi.y, zi.y));
             acc[1] = add(acc[1], mul(zi.x, ri.x));
@@ -291,8 +291,8 @@ __global__ void __launch_bounds__(kUpdThreads)
         }
         const double ri = axpy1(na, w[i], r[i]);
         const double zi = PC == 0 ? ri : mul(PC == 1 ? dinv[i] : dconst, ri);
-        r[i]            = ri;
-        if (zw) z[i]    = zi;
+        if (!(zw & 2)) r[i] = ri;
+        if (zw & 1) z[i]    = zi;
         acc[0]          = add(acc[0], mul(zi, zi));
         acc[1]          = add(acc[1], mul(zi, ri));
     }
@@ -689,6 +689,7 @@ struct rvk_cg_plan_s {
     int           mode = RVK_CG_MODE_FUSED; // resolved (AUTO -> FUSED | PERSISTENT)
     int           cluster = 0;              // PERSISTENT: CTAs of the one-cluster DSMEM solve (0: grid barriers)
     int           maxlen  = 0;              // longest row
+    bool          k2_last = false;          // enqueue_fused: the K2 being launched is the solve's last
     bool          stencil = false;          // matrix-free operator (rvk_cg_plan_create_stencil)
     StencilGeom   geom{};
     double        dconst = 0.0;             // constant dinv (stencil, or a detected constant diagonal)
@@ -767,6 +768,11 @@ struct XUpd {
     const double* pp[3] = {nullptr, nullptr, nullptr};
 };
 
+// K2 store mask: bit 0 store z (clear: z virtual), bit 1 the last K2 of a
+// fixed-iteration solve -- its r and z are never read again (the next solve's
+// setup rewrites both), so neither is stored (16 n bytes per solve)
+int k2_store(rvk_cg_plan P) { return P->k2_last ? 2 : (P->zv ? 0 : 1); }
+
 template <int PC, bool COND, int NP>
 void launch_update_k(rvk_cg_plan P, const double* p_new, double* x, int it,
                      cudaGraphConditionalHandle cond, int use_cond, const XUpd& u)
@@ -774,7 +780,7 @@ void launch_update_k(rvk_cg_plan P, const double* p_new, double* x, int it,
     launch_pdl(k_cg_update<true, PC, COND, NP>, P->upd_grid, kUpdThreads, 0, P->ctx->stream,
                P->A.n_rows, p_new, P->w, P->dinv, x, P->r, P->z, P->st, P->hist, it, P->cfg.rtol,
                P->cfg.atol, P->partials, P->tickets, P->dconst, P->cfg.max_it, cond, use_cond,
-               u.pp[0], u.pp[1], u.pp[2], u.slot, P->zv ? 0 : 1);
+               u.pp[0], u.pp[1], u.pp[2], u.slot, k2_store(P));
 }
 
 template <int PC, bool COND>
@@ -812,7 +818,7 @@ rvk_status launch_update(rvk_cg_plan P, int pcm, const double* p_new, double* x,
         launch_pdl(kern, P->upd_grid, kUpdThreads, 0, s, P->A.n_rows, p_new, P->w, P->dinv, x,
                    P->r, P->z, P->st, P->hist, it, P->cfg.rtol, P->cfg.atol, P->partials,
                    P->tickets, P->dconst, P->cfg.max_it, cond, use_cond, (const double*)nullptr,
-                   (const double*)nullptr, (const double*)nullptr, 0, P->zv ? 0 : 1);
+                   (const double*)nullptr, (const double*)nullptr, 0, k2_store(P));
     };
     if (V && P->k2_tma) {
         auto gt = [&](auto kern, size_t smem) {
@@ -1067,9 +1073,11 @@ rvk_status enqueue_fused(rvk_cg_plan P, const double* b, double* x)
         ++P->launches;
         if ((rc = rec(4 * it + 1)) != RVK_OK || (rc = rec(4 * it + 2)) != RVK_OK) return rc;
         // grouped x: defer inside a group, flush at its end (or the last iteration)
+        P->k2_last = it + 1 == P->cfg.max_it && !std::getenv("RVK_KEEP_RZ");
         rc = vec ? launch_update<true>(P, pcm, p_new, x, it, 0, 0,
                                        x_mode(P, defer, it, it + 1 == P->cfg.max_it, P->xq, P->npb))
                  : launch_update<false>(P, pcm, p_new, x, it);
+        P->k2_last = false;
         if (rc != RVK_OK) return rc;
         ++P->launches;
         if ((rc = rec(4 * it + 3)) != RVK_OK) return rc;
