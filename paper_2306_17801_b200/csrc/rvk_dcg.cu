@@ -245,7 +245,7 @@ __global__ void __launch_bounds__(kUpdThreads)
     k_dcg_setup(int64_t n, const double* __restrict__ b, const double* __restrict__ dinv,
                 double dconst, double* __restrict__ x, double* __restrict__ r,
                 double* __restrict__ z, double* gather, int rank, double* partials,
-                unsigned int* ticket, CgState* st, DcgPeer pr)
+                unsigned int* ticket, CgState* st, DcgPeer pr, int xw)
 {
     __shared__ double smem[64];
     __shared__ int    flag;
@@ -262,7 +262,7 @@ __global__ void __launch_bounds__(kUpdThreads)
         const double zi = jacobi_z(PC, dinv, dconst, i, bi);
         r[i] = bi;
         z[i] = zi;
-        x[i] = 0.0;
+        if (xw) x[i] = 0.0; // xw = 0: the whole-solve x pass starts from 0.0 itself
         if constexpr (PEER) peer_push(pr.lo_z, pr.hi_z, pr.plane, n, i, zi);
         acc[0] = add(acc[0], mul(zi, zi));
         acc[1] = add(acc[1], mul(zi, bi));
@@ -413,7 +413,7 @@ __global__ void __launch_bounds__(kUpdThreads)
                  double* __restrict__ r,
                  double* __restrict__ z, DcgScalars sc, int it, int rank, double* gather_out,
                  double* partials, unsigned int* ticket, DcgPeer pr,
-                 const double* __restrict__ p_prev, int slot)
+                 const double* __restrict__ p_prev, int slot, int last)
 {
     CgState* st = sc.st;
     if (st->done) return;
@@ -484,11 +484,13 @@ __global__ void __launch_bounds__(kUpdThreads)
                 zi.x = mul(d.x, ri.x);
                 zi.y = mul(d.y, ri.y);
             }
-            r2[i] = ri;
-            z2[i] = zi;
-            if constexpr (PEER) {
-                peer_push(pr.lo_z, pr.hi_z, pr.plane, n, 2 * i, zi.x);
-                peer_push(pr.lo_z, pr.hi_z, pr.plane, n, 2 * i + 1, zi.y);
+            if (!last) { // the last K2's r, z (and z halos) are dead: the next setup rewrites them
+                r2[i] = ri;
+                z2[i] = zi;
+                if constexpr (PEER) {
+                    peer_push(pr.lo_z, pr.hi_z, pr.plane, n, 2 * i, zi.x);
+                    peer_push(pr.lo_z, pr.hi_z, pr.plane, n, 2 * i + 1, zi.y);
+                }
             }
             acc[0] = add(acc[0], mul(zi.x, zi.x));
             acc[0] = add(acc[0], mul(zi.y, zi.y));
@@ -523,9 +525,11 @@ __global__ void __launch_bounds__(kUpdThreads)
         if (XM != 1) x[i] = axpy1(a, p[i], x[i]);
         const double ri = axpy1(na, w[i], r[i]);
         const double zi = jacobi_z(PC, dinv, dconst, i, ri);
-        r[i]            = ri;
-        z[i]            = zi;
-        if constexpr (PEER) peer_push(pr.lo_z, pr.hi_z, pr.plane, n, i, zi);
+        if (!last) {
+            r[i] = ri;
+            z[i] = zi;
+            if constexpr (PEER) peer_push(pr.lo_z, pr.hi_z, pr.plane, n, i, zi);
+        }
         acc[0]          = add(acc[0], mul(zi, zi));
         acc[1]          = add(acc[1], mul(zi, ri));
     }
@@ -715,12 +719,14 @@ int pc_mode(const rvk_dcg_plan P)
     return P->cfg.pc != RVK_PC_JACOBI ? 0 : (P->const_diag ? 2 : 1);
 }
 
+bool x_solve(const rvk_dcg_plan P);
+
 template <int PC, bool PEER>
 void launch_setup_k(rvk_dcg_plan P, const double* b, double* x)
 {
     k_dcg_setup<PC, PEER><<<P->upd_grid, kUpdThreads, 0, P->ctx->stream>>>(
         P->sh.n_own, b, P->dinv, P->dconst, x, P->r, P->z + P->sh.halo_lo, P->gather, P->sh.rank,
-        P->partials, P->tickets, P->st, P->peer);
+        P->partials, P->tickets, P->st, P->peer, x_solve(P) ? 0 : 1);
 }
 
 template <bool PEER>
@@ -790,7 +796,7 @@ void launch_update_k(rvk_dcg_plan P, int it, double* x)
         kern<<<P->upd_grid, kUpdThreads, 0, P->ctx->stream>>>(
             P->sh.n_own, pn, P->w, P->dinv, P->dconst, x, P->r, zo, scalars(P), it, P->sh.rank,
             P->gather + P->sh.rank * 4, P->partials, P->tickets, P->peer, pp,
-            x_solve(P) ? it : 0);
+            x_solve(P) ? it : 0, (it + 1 == P->cfg.max_it && !std::getenv("RVK_KEEP_RZ")) ? 1 : 0);
     };
     if (vec) go(k_dcg_update<PC, PEER, XM, true>);
     else go(k_dcg_update<PC, PEER, XM, false>);
@@ -830,7 +836,7 @@ rvk_status phase_xfix(rvk_dcg_plan P, double* x)
     XBufs pb{};
     for (int k = 0; k < P->npb; ++k) pb.p[k] = P->p[k] + P->sh.halo_lo;
     k_cg_xfix<4><<<P->upd_grid, kUpdThreads, 0, P->ctx->stream>>>(P->sh.n_own, x, pb, P->npb,
-                                                                   P->st, 0);
+                                                                   P->st, x_solve(P) ? 1 : 0);
     RVK_CHECK_LAUNCH("k_cg_xfix");
     return RVK_OK;
 }
