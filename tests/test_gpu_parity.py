@@ -872,3 +872,35 @@ def test_small_spmv_kernel(ctx, spec, graph, monkeypatch):
         x, res = plan.solve_host(b)
         check_cg_floor(res, x, ref)
         plan.close()
+
+
+@pytest.mark.parametrize("graph", [True, False])
+@pytest.mark.parametrize("op", ["csr", "stencil"])
+def test_whole_solve_x_written_on_every_exit(ctx, graph, op):
+    """The whole-solve x group never stores x = 0 in the setup: the final
+    pass starts from 0.0 and writes x on every exit -- a zero right-hand
+    side (converged at the setup), an atol exit after a few iterations and
+    the full 20 -- even when the caller's x buffer held garbage (NaN)."""
+    dim, pts, g = 3, 7, (20, 16, 12)
+    Ah = O.build_laplacian(dim, pts, g)
+    n = Ah.n_rows
+    A = rvk.DeviceCsr.laplacian(ctx, dim, pts, g) if op == "csr" else (dim, pts, g)
+    b = O.rhs(n)
+    for rhs, atol, its in ((np.zeros(n), 0.0, 0), (b, 1e-1 * np.linalg.norm(b) / 6, None), (b, 0.0, 20)):
+        plan = rvk.CgPlan(ctx, A, max_it=20, atol=atol, use_graph=graph)
+        assert plan.flags() & 128 or op == "stencil"
+        db = rvk.DeviceArray.from_host(ctx, np.ascontiguousarray(rhs))
+        dx = rvk.DeviceArray.from_host(ctx, np.full(n, np.nan))
+        plan.solve_dev(db, dx)
+        res = plan.result()
+        x = dx.download(ctx)
+        ref = O.cg_solve(Ah, rhs, max_it=20, atol=atol)
+        assert res.iterations == ref.iterations
+        if its is not None:
+            assert res.iterations == its
+        assert np.all(np.isfinite(x))
+        if not np.any(rhs):
+            assert not np.any(x)
+        else:
+            assert np.linalg.norm(x - ref.x) <= 1e-10 * np.linalg.norm(ref.x)
+        plan.close()
