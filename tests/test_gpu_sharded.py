@@ -91,3 +91,15 @@ def test_loopback_headline_256cubed_4_shards(ctx, backend):
     x, res, _ = loopback_solve(ctx, 3, 7, (256, 256, 256), 4, b, max_it=20, backend=backend)
     assert np.max(np.abs(res.hist - ref.hist) / ref.hist) < 1e-10
     assert np.linalg.norm(x - ref.x) / np.linalg.norm(ref.x) < 1e-10
+
+
+@pytest.mark.parametrize("backend", ["gather", "peer"])
+def test_loopback_zero_rhs_writes_x(ctx, backend):
+    """The shard plans skip the x = 0 store of the setup (the whole-solve x
+    pass starts from 0.0): a zero right-hand side converges at the setup and
+    x must still come back all zeros on every shard."""
+    dim, pts, grid = 3, 7, (24, 20, 30)
+    n = grid[0] * grid[1] * grid[2]
+    x, res, per = loopback_solve(ctx, dim, pts, grid, 2, np.zeros(n), max_it=20, backend=backend)
+    assert res.iterations == 0
+    assert not np.any(x) and np.all(np.isfinite(x))
