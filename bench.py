@@ -61,7 +61,7 @@ def peaks():
 
 def bytes_model(n: int, nnz: int, mode: str = "fused", const_diag: bool = False,
                 off32: bool = False, x_defer: bool = False, z_virtual: bool = False,
-                x_group: int = 2):
+                x_group: int = 2, fold_setup: bool = False):
     """Algorithmic HBM bytes.  All FP64 + int64 offsets + int32 cols.
     k1 = the SpMV launch (fused: + on-the-fly AYPX), k2 = the rest of an iteration.
     const_diag: the plan folded a constant Jacobi diagonal into a scalar
@@ -103,6 +103,8 @@ def bytes_model(n: int, nnz: int, mode: str = "fused", const_diag: bool = False,
     b_ref = 12 * nnz + 8 * (n + 1) + 152 * n     # reference's unfused sequence
     setup = (56 if (const_diag and mode == "fused") else 64) * n - (8 * n if z_virtual else 0) \
         - (8 * n if x_pass else 0)
+    if fold_setup and mode == "fused":  # setup inside K1(0): only its r = b store is extra
+        setup = 8 * n
     survey = MAX_IT * (12 * nnz + 8 * (n + 1) + 96 * n) + 64 * n  # SURVEY.md 8d B_min as stated
     # fused fixed-iteration solve: the last K2 stores neither r nor z (dead)
     last = ((8 if z_virtual else 16) * n) if mode == "fused" else 0
@@ -466,7 +468,7 @@ def run_gpu(args, cfg):
     z_virtual = bool(plan.flags() & 32)
     bm = bytes_model(n, nnz, "stencil" if args.operator == "stencil" else
                      ("unfused" if args.mode == "unfused" else "fused"), const_diag, off32, x_defer,
-                     z_virtual, x_group)
+                     z_virtual, x_group, bool(plan.flags() & 512))
     hbm_peak, peak_src = peaks()
     ws_bytes = 20 * nnz + 8 * (n + 1) + 9 * 8 * n
     log(f"{desc}: n={n} nnz={nnz} working set {ws_bytes/1e9:.2f} GB (L2 {L2_BYTES/1e6:.0f} MB)")

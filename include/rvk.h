@@ -244,6 +244,8 @@ rvk_status rvk_cg_solve_host_many(rvk_cg_plan plan, int nrhs, const double* cons
 #define RVK_PLAN_X_DEFER    16  /* fused solve applies x += a p for a GROUP of iterations in one
                                    pass (16-B aligned b / x; bit-identical x; RVK_X_DEFER=0 disables) */
 #define RVK_PLAN_X_GROUP4   64  /* ... groups of 4 iterations (else pairs; RVK_X_GROUP=2|4)      */
+#define RVK_PLAN_FOLD_SETUP 512 /* fixed-iteration fused CSR solve: the setup runs inside K1(0)
+                                   (z = d b per gathered column; RVK_FOLD_SETUP=0 disables)   */
 #define RVK_PLAN_CLUSTER    256 /* PERSISTENT / AUTO plan runs the one-cluster DSMEM solve (<= 16 K rows,
                                    rows <= 9 entries; RVK_CLUSTER=0 disables)                 */
 #define RVK_PLAN_X_SOLVE    128 /* ... one group = the whole fixed-iteration solve: x is written

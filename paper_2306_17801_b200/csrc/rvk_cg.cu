@@ -43,12 +43,100 @@
 
 namespace rvk {
 
+// K1 of iteration 0 with the setup folded in (fixed-iteration fused CSR
+// plans with no or a constant Jacobi diagonal, x in the whole-solve group):
+// z_j = d b_j formed per gathered column, p = z, w = A p; the row owner
+// writes p, w and r = b; sums p.w, z.z and z.b; the tail does the setup's
+// scalars (hist[0], dp0, beta, the convergence test) and then K1's (alpha).
+// A one-thread reset (k_cg_reset) runs before it.  Element values are the
+// setup's and K1's (z = d b, p = z); only the reduction order of z.z / z.b
+// differs (another fixed tree).
+template <bool VECD> // VECD: per-row Jacobi diagonal (gathered beside b)
+struct CgFirstBOp {
+    static constexpr bool kHasTail = true;
+    static constexpr int  kSums    = 3;
+    const double* __restrict__ b;
+    const double* __restrict__ dinv;
+    double* __restrict__ p_new;
+    double* __restrict__ w;
+    double* __restrict__ r;
+    CgState* st;
+    double*  hist;
+    double   d; // the constant diagonal (1.0 without a preconditioner: 1 * b == b exactly)
+    double   rtol, atol;
+
+    __device__ __forceinline__ bool init() { return true; }
+    struct Fetch {
+        double b, dv;
+    };
+    __device__ __forceinline__ int           num_src() const { return VECD ? 2 : 1; }
+    __device__ __forceinline__ const double* src_ptr(int k) const { return k == 0 ? b : dinv; }
+    __device__ __forceinline__ Fetch         fetch(int32_t j) const
+    {
+        return Fetch{__ldg(b + j), VECD ? __ldg(dinv + j) : 0.0};
+    }
+    __device__ __forceinline__ Fetch fetch_smem(const double* s0, const double* s1, int i) const
+    {
+        return Fetch{s0[i], VECD ? s1[i] : 0.0};
+    }
+    __device__ __forceinline__ double  value(const Fetch& f) const { return mul(VECD ? f.dv : d, f.b); }
+    __device__ __forceinline__ int64_t own_col(int64_t i) const { return i; }
+    __device__ __forceinline__ SumVec<3> row(int64_t i, double sum, SumVec<3> acc, const Fetch& o) const
+    {
+        const double z = value(o);
+        p_new[i]       = z;
+        w[i]           = sum;
+        r[i]           = o.b;
+        acc.v[0]       = add(acc.v[0], mul(z, sum));
+        acc.v[1]       = add(acc.v[1], mul(z, z));
+        acc.v[2]       = add(acc.v[2], mul(z, o.b));
+        return acc;
+    }
+    __device__ __forceinline__ void tail(const double (&v)[3]) const
+    {
+        const double dp0 = sqrt(v[1]);
+        hist[0]          = dp0;
+        st->dp0          = dp0;
+        st->dp           = dp0;
+        st->beta         = v[2];
+        if (cg_converged(dp0, dp0, rtol, atol)) {
+            st->state = RVK_CG_CONVERGED;
+            st->done  = 1;
+            return;
+        }
+        const double pAp = v[0];
+        const double a   = st->beta / pAp;
+        st->pAp          = pAp;
+        if (pAp == 0.0 || !isfinite(a)) {
+            st->state          = RVK_CG_BREAKDOWN;
+            st->breakdown_iter = 0;
+            st->done           = 1;
+        } else {
+            st->alpha   = a;
+            st->betaold = st->beta;
+        }
+    }
+};
+
 // AUTO picks the single persistent kernel only below this working set.  The
 // grid-barrier version measured slower than the 41-node graph at every
 // sweep size (64^2: 0.27 vs 0.19 ms), so AUTO resolves to FUSED for now.
 constexpr int64_t kPersistentMaxBytes = 0;
 
 // CgState, kUpdThreads, cg_converged, resident_grid: rvk_cg.cuh
+
+// State reset of a solve whose setup is folded into K1(0) (CgFirstBOp).
+__global__ void k_cg_reset(CgState* st)
+{
+    st->x_pending      = 0;
+    st->betaold        = 0.0;
+    st->alpha          = 0.0;
+    st->pAp            = 0.0;
+    st->iterations     = 0;
+    st->breakdown_iter = -1;
+    st->state          = RVK_CG_RUNNING;
+    st->done           = 0;
+}
 
 // ---------------------------------------------------------------------------
 // K0: setup.  r = b; x = 0; z = B r; partials z.z, z.r.
@@ -1061,14 +1149,37 @@ rvk_status enqueue_fused(rvk_cg_plan P, const double* b, double* x)
     // whole-solve x group: x is written once, by the final pass, which starts
     // from 0.0 itself -- the setup skips its x = 0 store (16 n bytes per solve)
     const bool     xz = defer && P->xq > 4;
-    rvk_status rc = vec ? launch_setup<true>(P, pcm, b, x, !xz) : launch_setup<false>(P, pcm, b, x);
+    // setup folded into K1(0) (CSR, no / constant diagonal, whole-solve x;
+    // RVK_FOLD_SETUP=0 keeps the separate setup kernel)
+    const char*    fe   = std::getenv("RVK_FOLD_SETUP");
+    const bool     fold = !P->stencil && !P->k2_tma && !(fe && fe[0] == '0');
+    rvk_status     rc   = RVK_OK;
+    if (fold) {
+        // x = 0 only where a K2 reads x (no whole-solve group)
+        if (!xz) RVK_CUDA(cudaMemsetAsync(x, 0, n * sizeof(double), s));
+        k_cg_reset<<<1, 1, 0, s>>>(P->st);
+        RVK_CHECK_LAUNCH("k_cg_reset");
+    } else {
+        rc = vec ? launch_setup<true>(P, pcm, b, x, !xz) : launch_setup<false>(P, pcm, b, x);
+    }
     if (rc != RVK_OK) return rc;
     ++P->launches;
     for (int it = 0; it < P->cfg.max_it; ++it) {
         const double* p_old = P->p[it % P->npb];
         double*       p_new = P->p[(it + 1) % P->npb];
         if ((rc = rec(4 * it + 0)) != RVK_OK) return rc;
-        rc = launch_k1(P, it, it == 0, p_old, p_new);
+        if (fold && it == 0) {
+            const double d = pcm == 2 ? P->dconst : 1.0;
+            if (pcm == 1) {
+                CgFirstBOp<true> op{b, P->dinv, p_new, P->w, P->r, P->st, P->hist, d, P->cfg.rtol, P->cfg.atol};
+                rc = launch_spmv(s, P->sa, op, ta, P->spmv_grid);
+            } else {
+                CgFirstBOp<false> op{b, P->dinv, p_new, P->w, P->r, P->st, P->hist, d, P->cfg.rtol, P->cfg.atol};
+                rc = launch_spmv(s, P->sa, op, ta, P->spmv_grid);
+            }
+        } else {
+            rc = launch_k1(P, it, it == 0, p_old, p_new);
+        }
         if (rc != RVK_OK) return rc;
         ++P->launches;
         if ((rc = rec(4 * it + 1)) != RVK_OK || (rc = rec(4 * it + 2)) != RVK_OK) return rc;
@@ -1500,6 +1611,9 @@ int rvk_cg_plan_flags(rvk_cg_plan P)
            ((P->mode == RVK_CG_MODE_FUSED && x_defer(P, true) && P->xq == 4) ? RVK_PLAN_X_GROUP4 : 0) |
            ((P->mode == RVK_CG_MODE_FUSED && x_defer(P, true) && P->xq > 4) ? RVK_PLAN_X_SOLVE : 0) |
            ((P->mode == RVK_CG_MODE_PERSISTENT && P->cluster) ? RVK_PLAN_CLUSTER : 0) |
+           ((P->mode == RVK_CG_MODE_FUSED && !P->stencil && !P->k2_tma &&
+             !(std::getenv("RVK_FOLD_SETUP") && std::getenv("RVK_FOLD_SETUP")[0] == '0'))
+                ? RVK_PLAN_FOLD_SETUP : 0) |
            (P->zv ? RVK_PLAN_Z_VIRTUAL : 0);
 }
 

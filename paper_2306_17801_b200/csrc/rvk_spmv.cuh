@@ -720,7 +720,10 @@ template <class Op>
 rvk_status launch_spmv(cudaStream_t stream, const SpmvArgs& a, const Op& op, TailArgs tail,
                        int grid)
 {
-    if (a.small_rows && a.n_rows <= a.small_rows && !a.off32) {
+    // (the tail's partial slots: the plans reserve 2 x kMaxReduceBlocks doubles)
+    if (a.small_rows && a.n_rows <= a.small_rows && !a.off32 &&
+        ((a.n_rows + kSpmvSmallThreads - 1) / kSpmvSmallThreads) * spmv_sums<Op>::value <=
+            2 * (int64_t)kMaxReduceBlocks) {
         const int g = (int)((a.n_rows + kSpmvSmallThreads - 1) / kSpmvSmallThreads);
         cudaError_t e;
         if (a.unroll == 7) e = launch_pdl(k_spmv_small<Op, 7>, g, kSpmvSmallThreads, 0, stream, a, op, tail);
