@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define RVK_ABI_VERSION 1
+#define RVK_ABI_VERSION 2
 
 typedef enum {
     RVK_OK             = 0,
@@ -190,7 +190,44 @@ typedef struct {
                          unrolled, replayed); 2: graph with a device-side WHILE
                          node -- no launches after convergence (FUSED only);
                          0: plain stream launches                             */
+    int    opts;      /* RVK_OPT_* bits, 0 = the plan's own choices (below)  */
 } rvk_cg_config;
+
+/* Plan variant overrides (rvk_cg_config.opts).  The plan picks the fastest
+ * measured variant by itself; these select the others explicitly (parity
+ * tests exercise every variant; none changes a result bit except where
+ * noted).  Read once at plan creation -- nothing is read from the
+ * environment.
+ *   RVK_OPT_KEEP_WORK    the last K2 of a fixed-iteration fused solve still
+ *                        stores r and z, so rvk_cg_plan_vector(R / Z) is the
+ *                        final residual (otherwise both are undefined after a
+ *                        fused solve: dead stores are skipped)
+ *   RVK_OPT_DINV_VECTOR  keep streaming the Jacobi diagonal even when it is one
+ *                        constant (no RVK_PLAN_CONST_DIAG folding)
+ *   RVK_OPT_Z_STORED     never use the virtual z (z = d r formed in the SpMV)
+ *   RVK_OPT_Z_VIRTUAL    use the virtual z wherever it is legal (default: only
+ *                        where it measured faster -- 9-batch CSR, matrix-free)
+ *   RVK_OPT_NO_CLUSTER   PERSISTENT mode: grid-barrier kernel instead of the
+ *                        one-cluster DSMEM solve
+ *   RVK_OPT_SMALL_K1     FUSED mode: plain-block SpMV (k_spmv_small) for
+ *                        systems up to 512 K rows (AUTO picks it itself)
+ *   RVK_OPT_MF_SIMPLE    matrix-free plans: the one-row-per-thread stencil
+ *                        kernel instead of the TMA 2.5D march
+ *   RVK_OPT_NO_FOLD      fixed-iteration fused CSR solves keep the separate
+ *                        setup kernel (no RVK_PLAN_FOLD_SETUP)
+ *   RVK_OPT_X_GROUP4     fused solve: x updated per group of 4 iterations
+ *                        instead of once per solve (RVK_PLAN_X_SOLVE)
+ *   RVK_OPT_X_EACH       fused solve: x updated in every iteration's K2    */
+#define RVK_OPT_KEEP_WORK   1
+#define RVK_OPT_DINV_VECTOR 2
+#define RVK_OPT_Z_STORED    4
+#define RVK_OPT_Z_VIRTUAL   8
+#define RVK_OPT_NO_CLUSTER  16
+#define RVK_OPT_SMALL_K1    32
+#define RVK_OPT_MF_SIMPLE   64
+#define RVK_OPT_NO_FOLD     128
+#define RVK_OPT_X_GROUP4    256
+#define RVK_OPT_X_EACH      512
 
 typedef struct {
     int state;          /* rvk_cg_state: RUNNING here means "ran max_it"     */
@@ -235,28 +272,32 @@ rvk_status rvk_cg_solve_host_many(rvk_cg_plan plan, int nrhs, const double* cons
 /* Plan structure the solve exploits (bitmask):
  *   RVK_PLAN_CONST_DIAG   every diagonal entry is the same bit pattern (constant-
  *                         coefficient stencils): Jacobi uses the scalar, no dinv
- *                         stream (RVK_CONST_DIAG=0 at plan creation disables)
+ *                         stream (RVK_OPT_DINV_VECTOR disables)
  *   RVK_PLAN_MATRIX_FREE  rvk_cg_plan_create_stencil operator                       */
 #define RVK_PLAN_CONST_DIAG  1
 #define RVK_PLAN_MATRIX_FREE 2
-#define RVK_PLAN_MF_TMA      4  /* matrix-free K1 is the TMA 2.5D marching kernel */
-#define RVK_PLAN_OFF32       8  /* the SpMV streams a plan-owned int32 copy of the row offsets */
+#define RVK_PLAN_MF_TMA      4  /* matrix-free K1 is the TMA 2.5D marching kernel (RVK_OPT_MF_SIMPLE: not) */
 #define RVK_PLAN_X_DEFER    16  /* fused solve applies x += a p for a GROUP of iterations in one
-                                   pass (16-B aligned b / x; bit-identical x; RVK_X_DEFER=0 disables) */
-#define RVK_PLAN_X_GROUP4   64  /* ... groups of 4 iterations (else pairs; RVK_X_GROUP=2|4)      */
-#define RVK_PLAN_FOLD_SETUP 512 /* fixed-iteration fused CSR solve: the setup runs inside K1(0)
-                                   (z = d b per gathered column; RVK_FOLD_SETUP=0 disables)   */
+                                   pass (16-B aligned b / x; bit-identical x)                  */
+#define RVK_PLAN_X_GROUP4   64  /* ... groups of 4 iterations (max_it > 32, p ring does not fit,
+                                   or the device WHILE loop)                                   */
+#define RVK_PLAN_FOLD_SETUP 512 /* fixed-iteration fused CSR solve (use_graph 0/1, 16-B aligned b):
+                                   the setup runs inside K1(0) (z = d b per gathered column;
+                                   RVK_OPT_NO_FOLD disables)                                   */
 #define RVK_PLAN_CLUSTER    256 /* PERSISTENT / AUTO plan runs the one-cluster DSMEM solve (<= 16 K rows,
-                                   rows <= 9 entries; RVK_CLUSTER=0 disables)                 */
+                                   rows <= 9 entries; RVK_OPT_NO_CLUSTER disables)              */
 #define RVK_PLAN_X_SOLVE    128 /* ... one group = the whole fixed-iteration solve: x is written
-                                   once, at the end (CSR plans, max_it <= 32, p buffers fit;
-                                   RVK_X_GROUP=solve forces, =4 opts out)                     */
+                                   once, at the end (5 <= max_it <= 32, p buffers fit)          */
 #define RVK_PLAN_Z_VIRTUAL  32  /* fused solve never stores z = d r (constant diagonal / no PC):
-                                   the SpMV gathers r and forms d r (bit-identical; RVK_ZV=0) */
+                                   the SpMV gathers r and forms d r (bit-identical;
+                                   RVK_OPT_Z_STORED / RVK_OPT_Z_VIRTUAL override)               */
 int        rvk_cg_plan_flags(rvk_cg_plan plan);
 /* Test hook (the reference's "exposed for equivalence tests" spirit,
  * kernels.hpp:50-76): device pointer of a plan work vector after a solve.
- * p0 / p1 alternate as p_old / p_new; iteration k writes p[(k+1)&1]. */
+ * p0 / p1 are the first two buffers of the plan's p ring (iteration k writes
+ * p[(k+1) % ring]).  R and Z hold the final residual only when the plan was
+ * created with RVK_OPT_KEEP_WORK (a fixed-iteration fused solve skips the
+ * last, dead r / z stores); Z is also unused under RVK_PLAN_Z_VIRTUAL. */
 enum { RVK_VEC_R = 0, RVK_VEC_Z = 1, RVK_VEC_P0 = 2, RVK_VEC_P1 = 3, RVK_VEC_W = 4 };
 const double* rvk_cg_plan_vector(rvk_cg_plan plan, int which);
 /* The mode the plan runs (AUTO resolved to FUSED or PERSISTENT). */

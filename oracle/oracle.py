@@ -15,7 +15,8 @@ REF_SO = os.path.join(HERE, "_ref", "librivulet_ref.so")
 __all__ = [
     "build", "lib", "ref_lib", "ref_available", "Csr", "build_laplacian", "laplacian_nnz",
     "rhs", "diagonal", "cg_solve", "ref_cg_solve", "spmv", "ref_spmv", "dot", "nrm2",
-    "CgResult", "DEFAULT_SEED", "tfqmr_solve",
+    "CgResult", "DEFAULT_SEED", "tfqmr_solve", "build_laplacian_rows", "stencil_spmv",
+    "cg_solve_stencil",
 ]
 
 DEFAULT_SEED = 0x9E3779B97F4A7C15
@@ -74,6 +75,14 @@ def lib():
         L.ro_tfqmr_solve.restype = _CgRes
         L.ro_tfqmr_solve.argtypes = [C.c_int64, _i64p, _i32p, _f64p, _f64p, _f64p, _f64p,
                                      _CgCfg, _f64p, C.POINTER(C.c_int)]
+        L.ro_build_laplacian_rows.restype = C.c_int64
+        L.ro_build_laplacian_rows.argtypes = [C.c_int, C.c_int, C.c_int64, C.c_int64, C.c_int64,
+                                              C.c_int64, C.c_int64, _i64p, _i32p, _f64p]
+        L.ro_stencil_spmv_mt.argtypes = [C.c_int, C.c_int, C.c_int64, C.c_int64, C.c_int64,
+                                         _f64p, _f64p]
+        L.ro_cg_solve_stencil_mt.restype = _CgRes
+        L.ro_cg_solve_stencil_mt.argtypes = [C.c_int, C.c_int, C.c_int64, C.c_int64, C.c_int64,
+                                             _f64p, _f64p, _f64p, _CgCfg, _f64p]
         L.ro_cg_solve.restype = _CgRes
         L.ro_cg_solve.argtypes = [C.c_int64, _i64p, _i32p, _f64p, _f64p, _f64p, _f64p,
                                   _CgCfg, _f64p]
@@ -231,3 +240,45 @@ def tfqmr_solve(A: Csr, b: np.ndarray, max_it: int = 20, pc: str = "jacobi",
     cfg = _CgCfg(max_it, 1 if pc == "jacobi" else 0, rtol, atol)
     r = lib().ro_tfqmr_solve(n, A.off, A.cols, A.vals, b, x, hist, cfg, work, C.byref(nh))
     return CgResult(x, hist[: nh.value].copy(), r.status, r.iterations, r.breakdown_iter)
+
+
+# ---- large sizes (rvk_oracle_mt.c: host threads, matrix-free) -------------------
+def build_laplacian_rows(dim: int, points: int, grid, r0: int, r1: int):
+    """Rows [r0, r1) of build_laplacian(dim, points, grid): (off, cols, vals)
+    with offsets local to the slab (off[0] = 0)."""
+    nx, ny, nz = (list(grid) + [1, 1])[:3]
+    L = lib()
+    # upper bound of the slab's nonzeros: points per row
+    cap = (r1 - r0) * points
+    off = np.empty(r1 - r0 + 1, np.int64)
+    cols = np.empty(cap, np.int32)
+    vals = np.empty(cap, np.float64)
+    k = L.ro_build_laplacian_rows(dim, points, nx, ny, nz, r0, r1, off, cols, vals)
+    if k < 0:
+        raise ValueError(f"invalid rows [{r0}, {r1}) of {dim}D {points}-pt {grid}")
+    return off, cols[:k], vals[:k]
+
+
+def stencil_spmv(dim: int, points: int, grid, x: np.ndarray) -> np.ndarray:
+    """A x for the Laplacian without assembling it (bit-identical to spmv on
+    build_laplacian's CSR)."""
+    nx, ny, nz = (list(grid) + [1, 1])[:3]
+    x = np.ascontiguousarray(x, np.float64)
+    y = np.empty_like(x)
+    lib().ro_stencil_spmv_mt(dim, points, nx, ny, nz, x, y)
+    return y
+
+
+def cg_solve_stencil(dim: int, points: int, grid, b: np.ndarray, max_it: int = 20,
+                     pc: str = "jacobi", rtol: float = 0.0, atol: float = 0.0) -> CgResult:
+    """cg_solve on the Laplacian, matrix-free and threaded (for the 768^3
+    config); reductions in fixed chunks (rvk_oracle_mt.c header)."""
+    nx, ny, nz = (list(grid) + [1, 1])[:3]
+    b = np.ascontiguousarray(b, np.float64)
+    n = b.shape[0]
+    x = np.empty(n, np.float64)
+    hist = np.full(max_it + 1, np.nan)
+    work = np.empty(4 * n, np.float64)
+    cfg = _CgCfg(max_it, 1 if pc == "jacobi" else 0, rtol, atol)
+    r = lib().ro_cg_solve_stencil_mt(dim, points, nx, ny, nz, b, x, hist, cfg, work)
+    return CgResult(x, hist[: r.iterations + 1].copy(), r.status, r.iterations, r.breakdown_iter)

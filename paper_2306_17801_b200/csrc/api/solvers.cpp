@@ -86,7 +86,7 @@ SolveResult cg_fused(const CsrMatrix& A, const DenseVector& b, DenseVector& x, c
         // AUTO: the one-cluster DSMEM solve for small systems (<= 16 K rows of
         // <= 9 entries, one launch), else the fused 2-kernel graph
         rvk_cg_config c{cfg.max_it, cfg.pc == PcType::Jacobi ? RVK_PC_JACOBI : RVK_PC_NONE,
-                        cfg.rtol, cfg.atol, RVK_CG_MODE_AUTO, 1};
+                        cfg.rtol, cfg.atol, RVK_CG_MODE_AUTO, 1, 0};
         rvk_cg_plan   p = nullptr;
         const rvk_csr v = ms.view();
         detail::check(rvk_cg_plan_create(cache.ctx.handle(), &v, c, &p), "cg_solve(setup)");
@@ -280,7 +280,7 @@ SolveResult tfqmr_solve(const CsrMatrix& A, const DenseVector& b, DenseVector& x
     auto       it    = cache.tfqmr.find(key);
     if (it == cache.tfqmr.end()) {
         rvk_cg_config  c{cfg.max_it, cfg.pc == PcType::Jacobi ? RVK_PC_JACOBI : RVK_PC_NONE,
-                         cfg.rtol, cfg.atol, RVK_CG_MODE_FUSED, 1};
+                         cfg.rtol, cfg.atol, RVK_CG_MODE_FUSED, 1, 0};
         rvk_tfqmr_plan p = nullptr;
         const rvk_csr  v = ms.view();
         detail::check(rvk_tfqmr_plan_create(cache.ctx.handle(), &v, c, &p), "tfqmr_solve(setup)");

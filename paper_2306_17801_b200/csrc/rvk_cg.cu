@@ -43,14 +43,17 @@
 
 namespace rvk {
 
-// K1 of iteration 0 with the setup folded in (fixed-iteration fused CSR
-// plans with no or a constant Jacobi diagonal, x in the whole-solve group):
+// K1 of iteration 0 with the setup folded in (fold_setup: FUSED CSR plans
+// on the unrolled graph / stream path, 16-B aligned b; any Jacobi diagonal --
+// constant (d) or a per-row vector gathered beside b (VECD) -- and any x
+// group: without the whole-solve group the caller zeroes x with a memset):
 // z_j = d b_j formed per gathered column, p = z, w = A p; the row owner
 // writes p, w and r = b; sums p.w, z.z and z.b; the tail does the setup's
 // scalars (hist[0], dp0, beta, the convergence test) and then K1's (alpha).
 // A one-thread reset (k_cg_reset) runs before it.  Element values are the
 // setup's and K1's (z = d b, p = z); only the reduction order of z.z / z.b
-// differs (another fixed tree).
+// differs (another fixed tree), so hist[0] and beta_0 may differ in the last
+// ulp from the WHILE-graph / unfused / persistent paths of the same plan.
 template <bool VECD> // VECD: per-row Jacobi diagonal (gathered beside b)
 struct CgFirstBOp {
     static constexpr bool kHasTail = true;
@@ -74,10 +77,6 @@ struct CgFirstBOp {
     __device__ __forceinline__ Fetch         fetch(int32_t j) const
     {
         return Fetch{__ldg(b + j), VECD ? __ldg(dinv + j) : 0.0};
-    }
-    __device__ __forceinline__ Fetch fetch_smem(const double* s0, const double* s1, int i) const
-    {
-        return Fetch{s0[i], VECD ? s1[i] : 0.0};
     }
     __device__ __forceinline__ double  value(const Fetch& f) const { return mul(VECD ? f.dv : d, f.b); }
     __device__ __forceinline__ int64_t own_col(int64_t i) const { return i; }
@@ -118,11 +117,6 @@ struct CgFirstBOp {
     }
 };
 
-// AUTO picks the single persistent kernel only below this working set.  The
-// grid-barrier version measured slower than the 41-node graph at every
-// sweep size (64^2: 0.27 vs 0.19 ms), so AUTO resolves to FUSED for now.
-constexpr int64_t kPersistentMaxBytes = 0;
-
 // CgState, kUpdThreads, cg_converged, resident_grid: rvk_cg.cuh
 
 // State reset of a solve whose setup is folded into K1(0) (CgFirstBOp).
@@ -148,8 +142,6 @@ __global__ void __launch_bounds__(kUpdThreads)
                CgState* st, double* hist, double rtol, double atol, double* partials,
                unsigned int* ticket, double dconst, int zw, int xw)
 {
-    pdl_trigger();
-    pdl_wait();
     __shared__ double smem[64];
     __shared__ int    flag;
     double            acc[2] = {0.0, 0.0};
@@ -274,8 +266,6 @@ __global__ void __launch_bounds__(kUpdThreads)
 {
     static_assert(VEC || NP == 0, "grouped x updates use the vector path");
     static_assert(NP >= -1 && NP <= 3, "at most 3 pending updates");
-    pdl_trigger();
-    pdl_wait();
     // In the device WHILE loop (use_cond) `it` comes from the device state and
     // this kernel decides whether the loop body runs again.
     if (st->done) {
@@ -381,114 +371,6 @@ __global__ void __launch_bounds__(kUpdThreads)
         const double zi = PC == 0 ? ri : mul(PC == 1 ? dinv[i] : dconst, ri);
         if (!(zw & 2)) r[i] = ri;
         if (zw & 1) z[i]    = zi;
-        acc[0]          = add(acc[0], mul(zi, zi));
-        acc[1]          = add(acc[1], mul(zi, ri));
-    }
-    cg_update_tail<COND>(acc, smem, &flag, st, hist, it, rtol, atol, partials, ticket, max_it, cond,
-                         use_cond);
-}
-
-// K2, streaming variant (RVK_K2_TMA=1 opt-in / A-B): one CTA per SM; the
-// 4-5 input streams (p, w, x, r[, dinv]) of each 1024-element tile arrive by
-// cp.async.bulk into a kK2Stages-deep shared-memory ring (mbarrier per
-// stage) and the outputs leave by coalesced 16-B stores.  Same element
-// arithmetic as k_cg_update (bit-identical x, r, z); the z.z / z.r partial
-// order differs (another fixed partition).  Full tiles only; the n %% 1024
-// remainder is a grid-stride tail.  All pointers 16-B aligned (VEC).
-constexpr int kK2Tile    = 1024;
-constexpr int kK2Stages  = 4;
-constexpr int kK2Threads = 256;
-template <int PC>
-constexpr size_t k2_smem_bytes()
-{
-    return sizeof(double) * (size_t)kK2Stages * (PC == 1 ? 5 : 4) * kK2Tile;
-}
-
-template <int PC, bool COND = false>
-__global__ void __launch_bounds__(kK2Threads, 1)
-    k_cg_update_tma(int64_t n, const double* __restrict__ p, const double* __restrict__ w,
-                    const double* __restrict__ dinv, double* __restrict__ x, double* __restrict__ r,
-                    double* __restrict__ z, CgState* st, double* hist, int it, double rtol,
-                    double atol, double* partials, unsigned int* ticket, double dconst, int max_it,
-                    cudaGraphConditionalHandle cond, int use_cond)
-{
-    if (st->done) {
-        if constexpr (COND)
-            if (use_cond && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(cond, 0);
-        return;
-    }
-    if (it < 0) it = st->iterations;
-    constexpr int NS = PC == 1 ? 5 : 4; // p, w, x, r, (dinv)
-    extern __shared__ __align__(128) unsigned char k2_smem[];
-    double*                          buf = reinterpret_cast<double*>(k2_smem);
-    __shared__ __align__(8) uint64_t full[kK2Stages];
-    __shared__ double                smem[64];
-    __shared__ int                   flag;
-    const double  a = st->alpha, na = -a;
-    const int     tid    = threadIdx.x;
-    const int64_t ntiles = n / kK2Tile;
-    const int64_t my     = ntiles > (int64_t)blockIdx.x
-                               ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-    if (tid == 0) {
-        for (int k = 0; k < kK2Stages; ++k) mbar_init(&full[k], 1);
-        fence_mbar_init();
-    }
-    __syncthreads();
-    const uint64_t pol = policy_evict_first();
-#define RVK_K2_ISSUE(J)                                                                            \
-    do {                                                                                           \
-        const int     k_  = (int)((J) % kK2Stages);                                                \
-        const int64_t e0_ = ((int64_t)blockIdx.x + (J) * (int64_t)gridDim.x) * kK2Tile;            \
-        double*       sb_ = buf + (size_t)k_ * NS * kK2Tile;                                       \
-        mbar_arrive_expect_tx(&full[k_], NS * kK2Tile * 8);                                        \
-        bulk_g2s(sb_, p + e0_, kK2Tile * 8, &full[k_], pol);                                       \
-        bulk_g2s(sb_ + kK2Tile, w + e0_, kK2Tile * 8, &full[k_], pol);                             \
-        bulk_g2s(sb_ + 2 * kK2Tile, x + e0_, kK2Tile * 8, &full[k_], pol);                         \
-        bulk_g2s(sb_ + 3 * kK2Tile, r + e0_, kK2Tile * 8, &full[k_], pol);                         \
-        if (PC == 1) bulk_g2s(sb_ + 4 * kK2Tile, dinv + e0_, kK2Tile * 8, &full[k_], pol);         \
-    } while (0)
-    if (tid == 0)
-        for (int64_t j = 0; j < my && j < kK2Stages; ++j) RVK_K2_ISSUE(j);
-    double acc[2] = {0.0, 0.0};
-    for (int64_t j = 0; j < my; ++j) {
-        const int k = (int)(j % kK2Stages);
-        mbar_wait(&full[k], (uint32_t)((j / kK2Stages) & 1));
-        const double2* sb = reinterpret_cast<const double2*>(buf + (size_t)k * NS * kK2Tile);
-        const int64_t  h0 = ((int64_t)blockIdx.x + j * (int64_t)gridDim.x) * (kK2Tile / 2);
-#pragma unroll
-        for (int q = tid; q < kK2Tile / 2; q += kK2Threads) {
-            const double2 pi = sb[q], wi = sb[kK2Tile / 2 + q];
-            double2       xi = sb[kK2Tile + q], ri = sb[3 * (kK2Tile / 2) + q];
-            double2       d  = make_double2(dconst, dconst);
-            if (PC == 1) d = sb[2 * kK2Tile + q];
-            xi.x = axpy1(a, pi.x, xi.x);
-            xi.y = axpy1(a, pi.y, xi.y);
-            ri.x = axpy1(na, wi.x, ri.x);
-            ri.y = axpy1(na, wi.y, ri.y);
-            double2 zi = ri;
-            if (PC != 0) {
-                zi.x = mul(d.x, ri.x);
-                zi.y = mul(d.y, ri.y);
-            }
-            st_stream(reinterpret_cast<double2*>(x) + h0 + q, xi);
-            reinterpret_cast<double2*>(r)[h0 + q] = ri;
-            reinterpret_cast<double2*>(z)[h0 + q] = zi;
-            acc[0] = add(acc[0], mul(zi.x, zi.x));
-            acc[0] = add(acc[0], mul(zi.y, zi.y));
-            acc[1] = add(acc[1], mul(zi.x, ri.x));
-            acc[1] = add(acc[1], mul(zi.y, ri.y));
-        }
-        __syncthreads(); // stage k consumed by every thread
-        if (tid == 0 && j + kK2Stages < my) RVK_K2_ISSUE(j + kK2Stages);
-    }
-#undef RVK_K2_ISSUE
-    for (int64_t i = ntiles * kK2Tile + (int64_t)blockIdx.x * blockDim.x + tid; i < n;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        x[i]            = axpy1(a, p[i], x[i]);
-        const double ri = axpy1(na, w[i], r[i]);
-        const double zi = PC == 0 ? ri : mul(PC == 1 ? dinv[i] : dconst, ri);
-        r[i]            = ri;
-        z[i]            = zi;
         acc[0]          = add(acc[0], mul(zi, zi));
         acc[1]          = add(acc[1], mul(zi, ri));
     }
@@ -649,9 +531,9 @@ __global__ void k_diagonals(int64_t n, const int64_t* __restrict__ off,
     }
 }
 
-rvk_status csr_windows(cudaStream_t s, const rvk_csr& A, SpmvWindows* out)
+rvk_status csr_bands(cudaStream_t s, const rvk_csr& A, SpmvBands* out)
 {
-    *out = SpmvWindows{};
+    *out = SpmvBands{};
     if (A.n_rows == 0 || A.nnz == 0) return RVK_OK;
     unsigned long long* table = nullptr;
     RVK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&table), kDiagTable * 8 + 16, s));
@@ -671,34 +553,16 @@ rvk_status csr_windows(cudaStream_t s, const rvk_csr& A, SpmvWindows* out)
     for (int i = 0; i < kDiagTable; ++i)
         if (h[i] != kDiagEmpty) d.push_back((int64_t)(long long)(h[i] ^ (1ull << 63)));
     std::sort(d.begin(), d.end());
-    // bands: diagonals closer than kGap share a band (at most kGap wasted
-    // doubles per gap)
+    // the highest band: diagonals closer than kGap belong to it
     constexpr int64_t kGap = 64, kMaxBand = 4096;
-    std::vector<std::pair<int64_t, int64_t>> bands;
-    for (int64_t v : d) {
-        if (!bands.empty() && v - bands.back().second <= kGap) bands.back().second = v;
-        else bands.emplace_back(v, v);
+    if (d.empty()) return RVK_OK;
+    int64_t lo = d.back();
+    for (size_t i = d.size() - 1; i > 0 && lo - d[i - 1] <= kGap; --i) lo = d[i - 1];
+    if (d.back() - lo <= kMaxBand) {
+        out->has_lead = true;
+        out->lead_lo  = lo;
+        out->lead_hi  = d.back();
     }
-    SpmvWindows W;
-    if (!bands.empty() && bands.back().second - bands.back().first <= kMaxBand) {
-        W.has_lead = true;
-        W.lead_lo  = bands.back().first;
-        W.lead_hi  = bands.back().second;
-    }
-    if (!bands.empty()) {
-        W.trail_lo = bands.front().first;
-        W.trail_hi = bands.front().second;
-    }
-    bool fits = (int)bands.size() <= kSpmvMaxWin;
-    for (auto& b : bands) fits = fits && b.second - b.first <= kMaxBand;
-    if (fits) {
-        W.n = (int)bands.size();
-        for (int w = 0; w < W.n; ++w) {
-            W.lo[w] = bands[w].first;
-            W.hi[w] = bands[w].second;
-        }
-    }
-    *out = W;
     return RVK_OK;
 }
 
@@ -721,29 +585,6 @@ __global__ void k_const_check(int64_t n, const unsigned long long* __restrict__ 
             *differs = 1;
             return;
         }
-}
-
-__global__ void k_off_narrow(int64_t n1, const int64_t* __restrict__ off, int32_t* __restrict__ o32)
-{
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n1;
-         i += (int64_t)gridDim.x * blockDim.x)
-        o32[i] = (int32_t)off[i];
-}
-
-rvk_status make_off32(cudaStream_t s, const rvk_csr& A, int32_t** out)
-{
-    *out = nullptr;
-    // opt-in (RVK_OFF32=1): bit-exact, but measured SLOWER on B200 (7-point
-    // 256^3 K1 372 vs 337 us, 27-point 1274 vs 1056 us) despite 4 B/row less
-    const char* env = std::getenv("RVK_OFF32");
-    if (!(env && env[0] == '1') || A.nnz >= ((int64_t)1 << 31) - 16 || A.n_rows < 1) return RVK_OK;
-    int32_t* o = nullptr;
-    RVK_CUDA(cudaMalloc(reinterpret_cast<void**>(&o), (size_t)(A.n_rows + 1 + 8) * sizeof(int32_t)));
-    RVK_CUDA(cudaMemsetAsync(o, 0, (size_t)(A.n_rows + 1 + 8) * sizeof(int32_t), s));
-    k_off_narrow<<<update_grid(A.n_rows + 1), kUpdThreads, 0, s>>>(A.n_rows + 1, A.row_offsets, o);
-    RVK_CHECK_LAUNCH("k_off_narrow");
-    *out = o;
-    return RVK_OK;
 }
 
 rvk_status vector_is_constant(cudaStream_t s, int64_t n, const double* v, bool* is_const,
@@ -782,9 +623,7 @@ struct rvk_cg_plan_s {
     StencilGeom   geom{};
     double        dconst = 0.0;             // constant dinv (stencil, or a detected constant diagonal)
     bool          const_diag = false;       // CSR plan: every dinv[i] bit-identical -> scalar
-    int32_t*      off32      = nullptr;     // int32 row offsets for the SpMV stream (nnz < 2^31)
-    bool          k2_tma     = false;       // K2 = k_cg_update_tma (RVK_K2_TMA=1)
-    bool          zv         = false;       // fused solve keeps z virtual (z = d r; RVK_ZV=0 off)
+    bool          zv         = false;       // fused solve keeps z virtual (z = d r)
     int           mf_grid = 0;
     MfTma*        mf_tma  = nullptr;         // TMA 2.5D matrix-free kernel state (or null)
     double*       dinv = nullptr;
@@ -792,7 +631,7 @@ struct rvk_cg_plan_s {
     double*       z = nullptr;
     double*       p[kMaxXq] = {}; // rotating: iteration j writes p[(j+1) % npb]
     int           npb  = 2; // p buffers: max(2, xq)
-    int           xq   = 4; // x updated once per group of xq iterations (RVK_X_GROUP; 1 = every one;
+    int           xq   = 4; // x updated once per group of xq iterations (1 = every one;
                             // max_it = the whole solve, one x pass at the end)
     double*       w    = nullptr;
     double*       hist = nullptr;
@@ -837,7 +676,7 @@ rvk_status launch_setup(rvk_cg_plan P, int pcm, const double* b, double* x, bool
 {
     cudaStream_t s = P->ctx->stream;
     auto go = [&](auto kern) {
-        launch_pdl(kern, P->setup_grid, kUpdThreads, 0, s, P->A.n_rows, b, P->dinv, x, P->r, P->z,
+        launch_k(kern, P->setup_grid, kUpdThreads, 0, s, P->A.n_rows, b, P->dinv, x, P->r, P->z,
                    P->st, P->hist, P->cfg.rtol, P->cfg.atol, P->partials, P->tickets, P->dconst,
                    P->zv ? 0 : 1, xw ? 1 : 0);
     };
@@ -865,7 +704,7 @@ template <int PC, bool COND, int NP>
 void launch_update_k(rvk_cg_plan P, const double* p_new, double* x, int it,
                      cudaGraphConditionalHandle cond, int use_cond, const XUpd& u)
 {
-    launch_pdl(k_cg_update<true, PC, COND, NP>, P->upd_grid, kUpdThreads, 0, P->ctx->stream,
+    launch_k(k_cg_update<true, PC, COND, NP>, P->upd_grid, kUpdThreads, 0, P->ctx->stream,
                P->A.n_rows, p_new, P->w, P->dinv, x, P->r, P->z, P->st, P->hist, it, P->cfg.rtol,
                P->cfg.atol, P->partials, P->tickets, P->dconst, P->cfg.max_it, cond, use_cond,
                u.pp[0], u.pp[1], u.pp[2], u.slot, k2_store(P));
@@ -903,30 +742,11 @@ rvk_status launch_update(rvk_cg_plan P, int pcm, const double* p_new, double* x,
         return RVK_OK;
     }
     auto go = [&](auto kern) {
-        launch_pdl(kern, P->upd_grid, kUpdThreads, 0, s, P->A.n_rows, p_new, P->w, P->dinv, x,
+        launch_k(kern, P->upd_grid, kUpdThreads, 0, s, P->A.n_rows, p_new, P->w, P->dinv, x,
                    P->r, P->z, P->st, P->hist, it, P->cfg.rtol, P->cfg.atol, P->partials,
                    P->tickets, P->dconst, P->cfg.max_it, cond, use_cond, (const double*)nullptr,
                    (const double*)nullptr, (const double*)nullptr, 0, k2_store(P));
     };
-    if (V && P->k2_tma) {
-        auto gt = [&](auto kern, size_t smem) {
-            kern<<<sm_count(), kK2Threads, smem, s>>>(P->A.n_rows, p_new, P->w, P->dinv, x, P->r, P->z,
-                                                      P->st, P->hist, it, P->cfg.rtol, P->cfg.atol,
-                                                      P->partials, P->tickets, P->dconst,
-                                                      P->cfg.max_it, cond, use_cond);
-        };
-        if (use_cond) {
-            if (pcm == 0) gt(k_cg_update_tma<0, true>, k2_smem_bytes<0>());
-            else if (pcm == 1) gt(k_cg_update_tma<1, true>, k2_smem_bytes<1>());
-            else gt(k_cg_update_tma<2, true>, k2_smem_bytes<2>());
-        } else {
-            if (pcm == 0) gt(k_cg_update_tma<0>, k2_smem_bytes<0>());
-            else if (pcm == 1) gt(k_cg_update_tma<1>, k2_smem_bytes<1>());
-            else gt(k_cg_update_tma<2>, k2_smem_bytes<2>());
-        }
-        RVK_CHECK_LAUNCH("k_cg_update_tma");
-        return RVK_OK;
-    }
     if (use_cond) {
         if (pcm == 0) go(k_cg_update<V, 0, true>);
         else if (pcm == 1) go(k_cg_update<V, 1, true>);
@@ -946,7 +766,7 @@ rvk_status launch_xfix(rvk_cg_plan P, double* x, int npb, bool xzero = false)
     for (int k = 0; k < npb; ++k) pb.p[k] = P->p[k];
     // 4 p streams in flight per thread (measured 7-point 256^3, 20 p's:
     // 2 / 4 / 8 per batch = 500 / 475 / 492 us)
-    launch_pdl(k_cg_xfix<4>, P->upd_grid, kUpdThreads, 0, P->ctx->stream, P->A.n_rows, x, pb, npb,
+    launch_k(k_cg_xfix<4>, P->upd_grid, kUpdThreads, 0, P->ctx->stream, P->A.n_rows, x, pb, npb,
                (const CgState*)P->st, xzero ? 1 : 0);
     RVK_CHECK_LAUNCH("k_cg_xfix");
     return RVK_OK;
@@ -957,21 +777,18 @@ rvk_status launch_xfix(rvk_cg_plan P, double* x, int npb, bool xzero = false)
 // K2 defers and k_cg_xfix applies the max_it updates in one pass at the end
 // -- 16 n + 8 n max_it bytes per solve instead of 24 n per iteration.  Else
 // groups of 4 (the WHILE-loop graph always uses groups of <= 4: its p ring is
-// static).  RVK_X_GROUP = 1 | 2 | 4 | solve forces one (measured on B200,
-// 7-point 256^3: pairs 9.25 -> groups of 4 8.58 ms).
+// static).  Measured on B200, 7-point 256^3: pairs 9.25 -> groups of 4 8.58
+// -> whole solve 8.46 ms.
 void set_x_group(rvk_cg_plan P)
 {
-    const char* e  = std::getenv("RVK_X_GROUP");
-    const int   mi = P->cfg.max_it;
-    int         q  = 4;
-    if (e && (e[0] == '1' || e[0] == '2') && !e[1]) q = e[0] - '0';
-    const bool force_solve = e && std::strcmp(e, "solve") == 0;
-    if ((!e || force_solve) && mi >= 5 && mi <= kMaxXq) {
+    const int mi = P->cfg.max_it;
+    int       q  = (P->cfg.opts & RVK_OPT_X_EACH) ? 1 : 4;
+    if (mi >= 5 && mi <= kMaxXq && !(P->cfg.opts & (RVK_OPT_X_EACH | RVK_OPT_X_GROUP4))) {
         const size_t vb = (size_t)P->A.n_rows * sizeof(double) + 32;
         size_t       fr = 0, tot = 0;
         const bool   fits = cudaMemGetInfo(&fr, &tot) == cudaSuccess &&
                           fr > (size_t)(mi - 2) * vb + 8 * vb + (size_t(2) << 30);
-        if (fits || force_solve) q = mi;
+        if (fits) q = mi;
     }
     if (P->mode != RVK_CG_MODE_FUSED) q = 1;
     P->xq  = q;
@@ -982,12 +799,17 @@ void set_x_group(rvk_cg_plan P)
 int while_group(rvk_cg_plan P) { return P->xq < 4 ? P->xq : 4; }
 int while_ring(rvk_cg_plan P) { return while_group(P) > 2 ? while_group(P) : 2; }
 
-// Grouped x updates on this solve? (vector path, classic K2, max_it >= 2,
-// group > 1; RVK_X_DEFER=0 / RVK_X_GROUP=1 disable)
-bool x_defer(rvk_cg_plan P, bool vec)
+// Grouped x updates on this solve? (vector path, max_it >= 2, group > 1)
+bool x_defer(rvk_cg_plan P, bool vec) { return vec && P->cfg.max_it >= 2 && P->xq > 1; }
+
+// Setup folded into K1(0) (CgFirstBOp): fixed-iteration FUSED CSR solves on
+// the unrolled graph / stream path.  b is gathered (and L2-bulk-prefetched)
+// by the SpMV, so it must be 16-B aligned; the WHILE graph and matrix-free
+// plans keep k_cg_setup.  b == nullptr: the plan-level answer (flags).
+bool fold_setup(rvk_cg_plan P, const double* b)
 {
-    const char* e = std::getenv("RVK_X_DEFER");
-    return vec && !P->k2_tma && P->cfg.max_it >= 2 && P->xq > 1 && !(e && e[0] == '0');
+    return P->mode == RVK_CG_MODE_FUSED && !P->stencil && P->cfg.use_graph != 2 &&
+           !(P->cfg.opts & RVK_OPT_NO_FOLD) && (b == nullptr || aligned16(b));
 }
 
 // The x-update mode of iteration `it` (for a WHILE body any index with the
@@ -1044,14 +866,13 @@ rvk_status launch_k1(rvk_cg_plan P, int it, bool first, const double* p_old, dou
 // 316 -> 347 us, solve 8.83 -> 8.95 ms; 5-point likewise), while the 9-batch
 // kernels absorb it (27-point 21.02 -> 20.50 ms, 9-point 10.01 -> 9.47 ms)
 // and the matrix-free operator gains (4.60 -> 4.10 ms).  So: matrix-free and
-// 9-batch CSR plans.  RVK_ZV=0 disables, RVK_ZV=1 forces.
+// 9-batch CSR plans (RVK_OPT_Z_STORED / RVK_OPT_Z_VIRTUAL override).
 bool virtual_z(rvk_cg_plan P)
 {
-    const char* e = std::getenv("RVK_ZV");
-    if (e && e[0] == '0') return false;
-    const bool ok = P->mode == RVK_CG_MODE_FUSED && !P->k2_tma &&
-                    (P->cfg.pc == RVK_PC_NONE || P->const_diag || P->stencil);
-    return ok && (P->stencil || P->sa.unroll == 9 || (e && e[0] == '1'));
+    const int o = P->cfg.opts;
+    if (o & RVK_OPT_Z_STORED) return false;
+    const bool ok = P->mode == RVK_CG_MODE_FUSED && (P->cfg.pc == RVK_PC_NONE || P->const_diag || P->stencil);
+    return ok && (P->stencil || P->sa.unroll == 9 || (o & RVK_OPT_Z_VIRTUAL));
 }
 
 // the convergence loop entirely on the device.  Graph =
@@ -1149,10 +970,8 @@ rvk_status enqueue_fused(rvk_cg_plan P, const double* b, double* x)
     // whole-solve x group: x is written once, by the final pass, which starts
     // from 0.0 itself -- the setup skips its x = 0 store (16 n bytes per solve)
     const bool     xz = defer && P->xq > 4;
-    // setup folded into K1(0) (CSR, no / constant diagonal, whole-solve x;
-    // RVK_FOLD_SETUP=0 keeps the separate setup kernel)
-    const char*    fe   = std::getenv("RVK_FOLD_SETUP");
-    const bool     fold = !P->stencil && !P->k2_tma && !(fe && fe[0] == '0');
+    // setup folded into K1(0) (CSR, aligned b; any x group / diagonal)
+    const bool     fold = fold_setup(P, b);
     rvk_status     rc   = RVK_OK;
     if (fold) {
         // x = 0 only where a K2 reads x (no whole-solve group)
@@ -1184,7 +1003,7 @@ rvk_status enqueue_fused(rvk_cg_plan P, const double* b, double* x)
         ++P->launches;
         if ((rc = rec(4 * it + 1)) != RVK_OK || (rc = rec(4 * it + 2)) != RVK_OK) return rc;
         // grouped x: defer inside a group, flush at its end (or the last iteration)
-        P->k2_last = it + 1 == P->cfg.max_it && !std::getenv("RVK_KEEP_RZ");
+        P->k2_last = it + 1 == P->cfg.max_it && !(P->cfg.opts & RVK_OPT_KEEP_WORK);
         rc = vec ? launch_update<true>(P, pcm, p_new, x, it, 0, 0,
                                        x_mode(P, defer, it, it + 1 == P->cfg.max_it, P->xq, P->npb))
                  : launch_update<false>(P, pcm, p_new, x, it);
@@ -1376,25 +1195,6 @@ rvk_status enqueue_solve(rvk_cg_plan P, const double* b, double* x)
     }
 }
 
-// K2 streaming variant: opt-in (RVK_K2_TMA=1); the ring needs > 48 KB of
-// dynamic shared memory, configured here, before any capture.
-rvk_status k2_tma_setup(rvk_cg_plan P)
-{
-    const char* e = std::getenv("RVK_K2_TMA");
-    if (!(e && e[0] == '1')) return RVK_OK;
-    auto cfg = [](auto kern, size_t smem) {
-        return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    };
-    RVK_CUDA(cfg(k_cg_update_tma<0>, k2_smem_bytes<0>()));
-    RVK_CUDA(cfg(k_cg_update_tma<1>, k2_smem_bytes<1>()));
-    RVK_CUDA(cfg(k_cg_update_tma<2>, k2_smem_bytes<2>()));
-    RVK_CUDA(cfg(k_cg_update_tma<0, true>, k2_smem_bytes<0>()));
-    RVK_CUDA(cfg(k_cg_update_tma<1, true>, k2_smem_bytes<1>()));
-    RVK_CUDA(cfg(k_cg_update_tma<2, true>, k2_smem_bytes<2>()));
-    P->k2_tma = true;
-    return RVK_OK;
-}
-
 rvk_status destroy_graph(rvk_cg_plan P)
 {
     for (auto& g : P->gs) {
@@ -1499,30 +1299,11 @@ rvk_status rvk_cg_plan_create(rvk_ctx ctx, const rvk_csr* A, rvk_cg_config cfg, 
     P->ctx       = ctx;
     P->A         = *A;
     P->cfg       = cfg;
-    // x-windows (stage the gathered vectors' diagonal bands via TMA) are an
-    // opt-in experiment (RVK_WINDOWS=1): measured slower than L1-cached
-    // gathers on the 2D stencils (9-pt 4096^2 K1 806 vs 467 us, window
-    // lookup made the consumers issue-bound); the 3D stencils have > 4 bands.
-    SpmvWindows win;
-    if (csr_windows(ctx->stream, *A, &win) != RVK_OK) win = SpmvWindows{};
-    const SpmvWindows bands = win; // the band scan, before the opt-in/out knobs
-    if (!std::getenv("RVK_WINDOWS")) win.n = 0;
-    if (std::getenv("RVK_NO_PREFETCH")) win.has_lead = false;
-    P->sa        = make_spmv_args(*A, maxlen, &win, 2);
-    spmv_set_order(P->sa, bands, A->nnz, 2, sm_count());
-    const char* small_env = std::getenv("RVK_SMALL_ROWS");
-    P->sa.small_rows = small_env ? std::min<int64_t>(std::atoll(small_env), 512 * 1024) : 0;
-    if (std::getenv("RVK_DEBUG")) {
-        std::fprintf(stderr, "[rvk] plan n=%lld nnz=%lld R=%d stages=%d groups=%d cap=%d nwin=%d "
-                             "order=%s(tiles/plane=%lld tiles/chunk=%lld)",
-                     (long long)A->n_rows, (long long)A->nnz, P->sa.R, P->sa.stages, P->sa.groups,
-                     P->sa.cap, P->sa.nwin, P->sa.ord_tc ? "chunked" : "row",
-                     (long long)P->sa.ord_tp, (long long)P->sa.ord_tc);
-        for (int w = 0; w < P->sa.nwin; ++w)
-            std::fprintf(stderr, " [%lld,%lld]@%d", (long long)P->sa.win_lo[w],
-                         (long long)P->sa.win_hi[w], P->sa.win_base[w]);
-        std::fprintf(stderr, " win_elems=%d stage_bytes=%d\n", P->sa.win_elems, P->sa.stage_bytes);
-    }
+    // leading-edge L2 prefetch band (stencil-like matrices)
+    SpmvBands bands;
+    if (csr_bands(ctx->stream, *A, &bands) != RVK_OK) bands = SpmvBands{};
+    P->sa            = make_spmv_args(*A, maxlen, &bands);
+    P->sa.small_rows = (cfg.opts & RVK_OPT_SMALL_K1) ? 512 * 1024 : 0;
     P->spmv_grid = sm_count();
     // one resident wave each (the vectorised loops take 2 elements per thread)
     P->upd_grid   = resident_grid(k_cg_update<true, 1>, kUpdThreads, (A->n_rows + 1) / 2);
@@ -1531,25 +1312,25 @@ rvk_status rvk_cg_plan_create(rvk_ctx ctx, const rvk_csr* A, rvk_cg_config cfg, 
     P->mode         = cfg.mode;
     P->maxlen = (int)std::min<int64_t>(maxlen, 1 << 30);
     if (cfg.mode == RVK_CG_MODE_AUTO || cfg.mode == RVK_CG_MODE_PERSISTENT)
-        P->cluster = cluster_ctas(A->n_rows, maxlen);
+        P->cluster = (cfg.opts & RVK_OPT_NO_CLUSTER) ? 0 : cluster_ctas(A->n_rows, maxlen);
     if (cfg.mode == RVK_CG_MODE_AUTO) {
         // up to 16 K rows: the one-cluster DSMEM solve (one launch, cluster
         // barriers); above, the HBM-streaming fused graph
-        const int64_t ws = 12 * A->nnz + 8 * (A->n_rows + 1) + 9 * 8 * A->n_rows;
-        P->mode = (P->cluster || ws <= kPersistentMaxBytes) ? RVK_CG_MODE_PERSISTENT : RVK_CG_MODE_FUSED;
+        P->mode = P->cluster ? RVK_CG_MODE_PERSISTENT : RVK_CG_MODE_FUSED;
         // and up to 512 K rows the plain-block K1 (k_spmv_small: 256^2 5-point
         // solve 0.229 -> 0.211 ms; explicit FUSED keeps the TMA kernel unless
-        // RVK_SMALL_ROWS asks)
-        if (!small_env) P->sa.small_rows = 512 * 1024;
+        // RVK_OPT_SMALL_K1 asks)
+        P->sa.small_rows = 512 * 1024;
     }
     const size_t vb = (size_t)A->n_rows * sizeof(double);
     cudaError_t  e  = cudaSuccess;
     auto alloc = [&](void** p, size_t bytes) {
         if (e == cudaSuccess) e = cudaMalloc(p, bytes);
     };
+    // every vector a K1 may gather (dinv, r with a virtual z, z, p) padded by
+    // 4 doubles
     alloc(reinterpret_cast<void**>(&P->dinv), vb);
     alloc(reinterpret_cast<void**>(&P->r), vb);
-    // gathered sources: +4 doubles so x-window copies may round up past n
     alloc(reinterpret_cast<void**>(&P->z), vb + 32);
     alloc(reinterpret_cast<void**>(&P->p[0]), vb + 32);
     alloc(reinterpret_cast<void**>(&P->p[1]), vb + 32);
@@ -1578,20 +1359,14 @@ rvk_status rvk_cg_plan_create(rvk_ctx ctx, const rvk_csr* A, rvk_cg_config cfg, 
     rvk_status rc = RVK_OK;
     if (cfg.pc == RVK_PC_JACOBI) rc = rvk_csr_diagonal_inverse(ctx, A, P->dinv);
     else rc = rvk_set(ctx, A->n_rows, 1.0, P->dinv);
-    // optional one-time int32 copy of the row offsets the SpMV streams
-    // (opt-in RVK_OFF32=1, see make_off32)
-    if (rc == RVK_OK) rc = make_off32(s, *A, &P->off32);
-    if (rc == RVK_OK) P->sa.off32 = P->off32;
-    if (rc == RVK_OK) rc = k2_tma_setup(P);
     // Constant-coefficient operators with Dirichlet truncation have ONE
     // diagonal value, so dinv is a constant vector: the fused K0/K2 then
     // multiply by the scalar (bit-identical z = dinv[i] * r[i]) and skip the
-    // 8n-byte dinv stream per iteration (RVK_CONST_DIAG=0 disables).  Measured
+    // 8n-byte dinv stream per iteration (RVK_OPT_DINV_VECTOR disables).  Measured
     // on B200 (7-point 256^3): with the per-iteration x update it was a wash
     // (K2 -12 us, K1 +11 us); with the pairwise x update K2 151 -> 137 us,
     // K1 unchanged, solve 9.31 -> 9.00 ms.
-    const char* cd = std::getenv("RVK_CONST_DIAG");
-    if (rc == RVK_OK && cfg.pc == RVK_PC_JACOBI && !(cd && cd[0] == '0'))
+    if (rc == RVK_OK && cfg.pc == RVK_PC_JACOBI && !(cfg.opts & RVK_OPT_DINV_VECTOR))
         rc = vector_is_constant(s, A->n_rows, P->dinv, &P->const_diag, &P->dconst);
     if (rc == RVK_OK) P->zv = virtual_z(P); // after the constant-diagonal check
     if (rc != RVK_OK) {
@@ -1606,14 +1381,12 @@ int rvk_cg_plan_flags(rvk_cg_plan P)
 {
     if (!P) return -1;
     return (P->const_diag ? RVK_PLAN_CONST_DIAG : 0) | (P->stencil ? RVK_PLAN_MATRIX_FREE : 0) |
-           (P->mf_tma ? RVK_PLAN_MF_TMA : 0) | (P->off32 ? RVK_PLAN_OFF32 : 0) |
+           (P->mf_tma ? RVK_PLAN_MF_TMA : 0) |
            ((P->mode == RVK_CG_MODE_FUSED && x_defer(P, true)) ? RVK_PLAN_X_DEFER : 0) |
            ((P->mode == RVK_CG_MODE_FUSED && x_defer(P, true) && P->xq == 4) ? RVK_PLAN_X_GROUP4 : 0) |
            ((P->mode == RVK_CG_MODE_FUSED && x_defer(P, true) && P->xq > 4) ? RVK_PLAN_X_SOLVE : 0) |
            ((P->mode == RVK_CG_MODE_PERSISTENT && P->cluster) ? RVK_PLAN_CLUSTER : 0) |
-           ((P->mode == RVK_CG_MODE_FUSED && !P->stencil && !P->k2_tma &&
-             !(std::getenv("RVK_FOLD_SETUP") && std::getenv("RVK_FOLD_SETUP")[0] == '0'))
-                ? RVK_PLAN_FOLD_SETUP : 0) |
+           (fold_setup(P, nullptr) ? RVK_PLAN_FOLD_SETUP : 0) |
            (P->zv ? RVK_PLAN_Z_VIRTUAL : 0);
 }
 
@@ -1684,7 +1457,7 @@ rvk_status rvk_cg_plan_create_stencil(rvk_ctx ctx, int dim, int points, int64_t 
         rvk_cg_plan_destroy(P);
         return cuda_error(e, "rvk_cg_plan_create_stencil");
     }
-    P->mf_tma = mf_tma_create(P->geom, P->z, P->p, P->npb, P->r);
+    P->mf_tma = (cfg.opts & RVK_OPT_MF_SIMPLE) ? nullptr : mf_tma_create(P->geom, P->z, P->p, P->npb, P->r);
     P->zv     = virtual_z(P);
     *out = P;
     return RVK_OK;
@@ -1703,7 +1476,7 @@ rvk_status rvk_cg_plan_destroy(rvk_cg_plan P)
     if (P->s_out) cudaStreamDestroy(P->s_out);
     void* bufs[] = {P->dinv, P->r, P->z, P->w, P->hist, P->st,
                     P->partials, P->tickets, P->tmp, P->b_buf, P->x_buf, P->b_buf2,
-                    P->x_buf2, P->hist_all, P->st_all, P->off32};
+                    P->x_buf2, P->hist_all, P->st_all};
     for (void* b : bufs)
         if (b) cudaFree(b);
     for (double* b : P->p)

@@ -93,10 +93,6 @@ struct CgSpmvOp {
     {
         return Fetch{__ldg(z + j), FIRST ? 0.0 : __ldg(p_old + j)};
     }
-    __device__ __forceinline__ Fetch fetch_smem(const double* s0, const double* s1, int i) const
-    {
-        return Fetch{s0[i], FIRST ? 0.0 : s1[i]};
-    }
     __device__ __forceinline__ double value(const Fetch& f) const
     {
         return FIRST ? zval(f.z) : aypx1(b, zval(f.z), f.p); // z + b*p  (kernels_scalar.cpp:33)
@@ -138,7 +134,7 @@ struct StencilGeom {
 // CSR path: the neighbours are visited in ascending column order with the
 // same coefficients.
 // The TMA 2.5D variant's plan state (tensor maps of z, p0, p1); null when the
-// geometry does not allow it (odd nx) or RVK_MF_TMA=0.
+// geometry does not allow it (odd nx) or the plan asks RVK_OPT_MF_SIMPLE.
 struct MfTma;
 MfTma*     mf_tma_create(const StencilGeom& g, const double* z, double* const* p, int np,
                          const double* r); // p: the plan's np (2..4) rotating p buffers
@@ -192,8 +188,6 @@ __global__ void __launch_bounds__(kUpdThreads)
     k_cg_xfix(int64_t n, double* __restrict__ x, XBufs pb, int q, const CgState* __restrict__ st,
               int xzero)
 {
-    pdl_trigger();
-    pdl_wait();
     // xzero: x was not initialised (the whole-solve group): start every
     // element from 0.0 -- the same adds as from a stored 0.0 -- and write x
     // even when no update is pending (a solve converged at the setup)

@@ -380,8 +380,7 @@ int persistent_grid(int64_t n)
 // (n > 16 x 1024 rows, rows longer than kCMaxNnz, or no co-resident cluster).
 int cluster_ctas(int64_t n, int64_t max_row_len)
 {
-    const char* e = std::getenv("RVK_CLUSTER");
-    if ((e && e[0] == '0') || n < 1 || max_row_len > kCMaxNnz || n > (int64_t)kCMaxCta * kCRows) return 0;
+    if (n < 1 || max_row_len > kCMaxNnz || n > (int64_t)kCMaxCta * kCRows) return 0;
     const int C = (int)((n + kCRows - 1) / kCRows);
     for (auto fn : {k_cg_cluster<true, 5>, k_cg_cluster<false, 5>, k_cg_cluster<true, 7>,
                     k_cg_cluster<false, 7>, k_cg_cluster<true, 9>, k_cg_cluster<false, 9>})

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <atomic>
 #include <cstdint>
 
 #include "rvk.h"
@@ -192,14 +193,6 @@ __device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
 
-// Programmatic dependent launch (sm_90+): a kernel launched with the
-// programmatic-serialization attribute may start while its predecessor in the
-// stream drains; pdl_wait() blocks until the predecessor has completed and
-// its memory is visible (a no-op for an ordinary launch), pdl_trigger() lets
-// the successor begin launching.  Every global access stays after pdl_wait().
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
-
 // Streaming global loads (read-once data).
 __device__ __forceinline__ double2 ld_stream(const double2* p) { return __ldcs(p); }
 __device__ __forceinline__ void st_stream(double2* p, double2 v) { __stcs(p, v); }
@@ -208,30 +201,32 @@ __device__ __forceinline__ void st_stream(double2* p, double2 v) { __stcs(p, v);
 
 // Host-side error plumbing shared by the .cu/.cpp translation units.
 namespace rvk {
-// Launch `kern` with programmatic stream serialization (PDL) when enabled
-// (opt-in RVK_PDL=1): the kernel must call pdl_wait() before touching
-// global memory its stream predecessor reads or writes.
-bool pdl_enabled();
-template <class... KArgs, class... Args>
-cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
-                       Args&&... args)
-{
-    cudaLaunchConfig_t  cfg = {};
-    cudaLaunchAttribute attr[1];
-    cfg.gridDim          = grid;
-    cfg.blockDim         = block;
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream           = s;
-    attr[0].id                                         = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs                                          = attr;
-    cfg.numAttrs                                       = pdl_enabled() ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
-}
 rvk_status set_error(rvk_status s, const char* fmt, ...);
 rvk_status cuda_error(cudaError_t e, const char* what);
 void       note_host_sync();
+// SM count of the CURRENT device (cached per device: one process may drive
+// several GPUs, e.g. one host thread per device)
 int        sm_count();
+// Per-device one-time setup (function attributes are per device): true when
+// bit `device` of `mask` is not set yet; device_mark_done sets it.
+int        current_device();
+inline bool device_first_use(std::atomic<uint64_t>& mask)
+{
+    return !(mask.load(std::memory_order_acquire) & (1ull << (current_device() & 63)));
+}
+inline void device_mark_done(std::atomic<uint64_t>& mask)
+{
+    mask.fetch_or(1ull << (current_device() & 63), std::memory_order_acq_rel);
+}
+// kern<<<grid, block, smem, s>>>(args...) with the arguments converted to
+// the kernel's parameter types; returns the launch error (not cleared).
+template <class... KArgs, class... Args>
+cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                     Args&&... args)
+{
+    kern<<<grid, block, smem, s>>>(static_cast<KArgs>(args)...);
+    return cudaPeekAtLastError();
+}
 } // namespace rvk
 
 #define RVK_CUDA(call)                                                   \

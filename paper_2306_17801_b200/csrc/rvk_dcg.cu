@@ -373,10 +373,6 @@ struct DcgSpmvOp {
     {
         return Fetch{__ldg(z + j), FIRST ? 0.0 : __ldg(p_old + j)};
     }
-    __device__ __forceinline__ Fetch fetch_smem(const double* s0, const double* s1, int i) const
-    {
-        return Fetch{s0[i], FIRST ? 0.0 : s1[i]};
-    }
     __device__ __forceinline__ double value(const Fetch& f) const
     {
         return FIRST ? f.z : aypx1(b, f.z, f.p);
@@ -624,7 +620,6 @@ struct rvk_dcg_plan_s {
     unsigned int* tickets = nullptr;
     DcgPeer       peer{};          // peer.on: PEER backend attached
     bool          const_diag = false; // Jacobi diagonal is one value: dconst
-    int32_t*      off32      = nullptr; // int32 row offsets for the SpMV stream
     double        dconst     = 0.0;
     void**        peer_tab = nullptr; // device: gather[nranks] then flags[nranks]
 };
@@ -642,12 +637,9 @@ struct WindowLayout {
 // iteration's p kept) when 5 <= max_it <= kMaxXq and the ring takes at most
 // half the device, else 2 (x per iteration pair).  A pure function of
 // (max_it, n_ext, device size), so every rank can derive a peer's layout;
-// attach_peers checks that the neighbours' rings match.  RVK_X_GROUP other
-// than "solve" keeps the pairs.
+// attach_peers checks that the neighbours' rings match.
 int ring_len(int max_it, int64_t n_ext)
 {
-    const char* e = std::getenv("RVK_X_GROUP");
-    if (e && std::strcmp(e, "solve") != 0) return 2;
     if (max_it < 5 || max_it > kMaxXq) return 2;
     size_t fr = 0, tot = 0;
     if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) return 2;
@@ -769,13 +761,8 @@ rvk_status phase_k1(rvk_dcg_plan P, int it)
 }
 
 // x update once per solve (ring = max_it: every K2 defers, k_cg_xfix applies
-// them at the end) or per iteration pair (as rvk_cg.cu; RVK_X_DEFER=0
-// disables both)
-bool x_defer(const rvk_dcg_plan P)
-{
-    const char* e = std::getenv("RVK_X_DEFER");
-    return P->cfg.max_it >= 2 && !(e && e[0] == '0');
-}
+// them at the end) or per iteration pair (as rvk_cg.cu)
+bool x_defer(const rvk_dcg_plan P) { return P->cfg.max_it >= 2; }
 bool x_solve(const rvk_dcg_plan P) { return x_defer(P) && P->npb > 2; }
 int x_mode(const rvk_dcg_plan P, int it)
 {
@@ -796,7 +783,7 @@ void launch_update_k(rvk_dcg_plan P, int it, double* x)
         kern<<<P->upd_grid, kUpdThreads, 0, P->ctx->stream>>>(
             P->sh.n_own, pn, P->w, P->dinv, P->dconst, x, P->r, zo, scalars(P), it, P->sh.rank,
             P->gather + P->sh.rank * 4, P->partials, P->tickets, P->peer, pp,
-            x_solve(P) ? it : 0, (it + 1 == P->cfg.max_it && !std::getenv("RVK_KEEP_RZ")) ? 1 : 0);
+            x_solve(P) ? it : 0, (it + 1 == P->cfg.max_it && !(P->cfg.opts & RVK_OPT_KEEP_WORK)) ? 1 : 0);
     };
     if (vec) go(k_dcg_update<PC, PEER, XM, true>);
     else go(k_dcg_update<PC, PEER, XM, false>);
@@ -981,13 +968,9 @@ rvk_status rvk_dcg_plan_create(rvk_ctx ctx, const rvk_csr* A, rvk_shard sh, rvk_
     P->A           = *A;
     P->sh          = sh;
     P->cfg         = cfg;
-    SpmvWindows win; // x-windows opt-in, leading-edge prefetch default (see rvk_cg.cu)
-    if (csr_windows(ctx->stream, *A, &win) != RVK_OK) win = SpmvWindows{};
-    const SpmvWindows bands = win; // the band scan, before the opt-in/out knobs
-    if (!std::getenv("RVK_WINDOWS")) win.n = 0;
-    if (std::getenv("RVK_NO_PREFETCH")) win.has_lead = false;
-    P->sa          = make_spmv_args(*A, maxlen, &win, 2);
-    spmv_set_order(P->sa, bands, A->nnz, 2, sm_count());
+    SpmvBands bands; // leading-edge L2 prefetch (see rvk_cg.cu)
+    if (csr_bands(ctx->stream, *A, &bands) != RVK_OK) bands = SpmvBands{};
+    P->sa          = make_spmv_args(*A, maxlen, &bands);
     P->upd_grid    = resident_grid(k_dcg_update<1, true, 2, true>, kUpdThreads, (sh.n_own + 1) / 2);
     P->owns_gather = shared_gather == nullptr;
     P->gather      = shared_gather;
@@ -997,13 +980,10 @@ rvk_status rvk_dcg_plan_create(rvk_ctx ctx, const rvk_csr* A, rvk_shard sh, rvk_
         if (cfg.pc == RVK_PC_JACOBI) rc = diag_inverse(ctx->stream, *A, sh.halo_lo, P->dinv);
         else rc = rvk_set(ctx, sh.n_own, 1.0, P->dinv);
     }
-    // constant diagonal -> scalar Jacobi (as rvk_cg_plan_create; RVK_CONST_DIAG=0 disables).
+    // constant diagonal -> scalar Jacobi (as rvk_cg_plan_create; RVK_OPT_DINV_VECTOR disables).
     // Every shard of a constant-coefficient operator sees the same value.
-    const char* cd = std::getenv("RVK_CONST_DIAG");
-    if (rc == RVK_OK && cfg.pc == RVK_PC_JACOBI && sh.n_own > 0 && !(cd && cd[0] == '0'))
+    if (rc == RVK_OK && cfg.pc == RVK_PC_JACOBI && sh.n_own > 0 && !(cfg.opts & RVK_OPT_DINV_VECTOR))
         rc = vector_is_constant(ctx->stream, sh.n_own, P->dinv, &P->const_diag, &P->dconst);
-    if (rc == RVK_OK) rc = make_off32(ctx->stream, *A, &P->off32);
-    if (rc == RVK_OK) P->sa.off32 = P->off32;
     if (rc != RVK_OK) {
         rvk_dcg_plan_destroy(P);
         return rc;
@@ -1019,7 +999,7 @@ rvk_status rvk_dcg_plan_destroy(rvk_dcg_plan P)
     // (PEER: the caller keeps every rank alive past its last solve -- a
     // barrier before destroy -- since peers store into this window)
     void* bufs[] = {P->win, P->dinv, P->r, P->w, P->hist, P->beta, P->st, P->partials, P->tickets,
-                    P->peer_tab, P->off32};
+                    P->peer_tab};
     for (void* b : bufs)
         if (b) cudaFree(b);
     delete P;
@@ -1101,7 +1081,7 @@ rvk_status rvk_dcg_result(rvk_dcg_plan P, double* hist_host, rvk_cg_info* info)
 int rvk_dcg_plan_flags(rvk_dcg_plan P)
 {
     if (!P) return -1;
-    return (P->const_diag ? RVK_PLAN_CONST_DIAG : 0) | (P->off32 ? RVK_PLAN_OFF32 : 0) |
+    return (P->const_diag ? RVK_PLAN_CONST_DIAG : 0) |
            (x_defer(P) ? RVK_PLAN_X_DEFER : 0) | (x_solve(P) ? RVK_PLAN_X_SOLVE : 0);
 }
 

@@ -16,9 +16,6 @@ rvk_status vec_reduce(cudaStream_t st, Scratch sc, int op, int64_t n, const doub
 rvk_status vec_ew(cudaStream_t st, int op, int64_t n, rvk_scalar s, const double* x,
                   const double* y, double* out, const int* guard);
 
-// Plan-owned int32 copy of A's row offsets (padded by 8 entries), or *out =
-// null when nnz does not fit or RVK_OFF32 != 1 (opt-in: measured slower).
-rvk_status make_off32(cudaStream_t s, const rvk_csr& A, int32_t** out);
 // Is v[0..n) a single bit pattern (plan time, one counted sync)?  *value = v[0].
 rvk_status vector_is_constant(cudaStream_t s, int64_t n, const double* v, bool* is_const,
                               double* value);

@@ -90,8 +90,6 @@ __global__ void __launch_bounds__(kMfThreads, 2)
 {
     constexpr bool FIRST = OpT::kFirst;
     using F              = typename OpT::Fetch;
-    pdl_trigger();
-    pdl_wait();
     OpT op               = op_in;
     if (!op.init()) return; // device-side early exit (converged / breakdown)
     __shared__ double red[32];
@@ -266,8 +264,6 @@ __global__ void __launch_bounds__(mf_threads<DIM, BOX>())
     __shared__ double                red[32];
     __shared__ int                   flag;
 
-    pdl_trigger();
-    pdl_wait();
     OpT op = op_in;
     if (!op.init()) return; // device-side early exit (converged / breakdown)
     const int     tid = threadIdx.x, tx = tid % TX, ty = tid / TX;
@@ -372,10 +368,10 @@ rvk_status launch_first(cudaStream_t s, const StencilGeom& g, const OpT& op,
     const int64_t far = g.dim == 3 ? g.nx * g.ny : g.nx;
     const int64_t lo = far - (g.dim == 3 ? g.nx : 0) - 1, hi = far + (g.dim == 3 ? g.nx : 0) + 1;
     const FastDiv fx = FastDiv::make((uint32_t)g.nx), fy = FastDiv::make((uint32_t)g.ny);
-    if (g.dim == 3 && g.box) launch_pdl(k_mf_cg<OpT, 3, true>, grid, kMfThreads, 0, s, g, fx, fy, op, ta, lo, hi);
-    else if (g.dim == 3) launch_pdl(k_mf_cg<OpT, 3, false>, grid, kMfThreads, 0, s, g, fx, fy, op, ta, lo, hi);
-    else if (g.box) launch_pdl(k_mf_cg<OpT, 2, true>, grid, kMfThreads, 0, s, g, fx, fy, op, ta, lo, hi);
-    else launch_pdl(k_mf_cg<OpT, 2, false>, grid, kMfThreads, 0, s, g, fx, fy, op, ta, lo, hi);
+    if (g.dim == 3 && g.box) launch_k(k_mf_cg<OpT, 3, true>, grid, kMfThreads, 0, s, g, fx, fy, op, ta, lo, hi);
+    else if (g.dim == 3) launch_k(k_mf_cg<OpT, 3, false>, grid, kMfThreads, 0, s, g, fx, fy, op, ta, lo, hi);
+    else if (g.box) launch_k(k_mf_cg<OpT, 2, true>, grid, kMfThreads, 0, s, g, fx, fy, op, ta, lo, hi);
+    else launch_k(k_mf_cg<OpT, 2, false>, grid, kMfThreads, 0, s, g, fx, fy, op, ta, lo, hi);
     RVK_CHECK_LAUNCH("k_mf_cg");
     return RVK_OK;
 }
@@ -447,14 +443,16 @@ bool encode_plane_map(CUtensorMap* m, const double* base, const StencilGeom& g, 
 template <int DIM, bool BOX>
 void mf_configure()
 {
-    static std::once_flag once; // before any graph capture (plan creation)
-    std::call_once(once, [] {
-        const int sm = (int)mf_smem_bytes<DIM, BOX>();
-        cudaFuncSetAttribute(k_mf_tma<CgSpmvOp<true, false>, DIM, BOX>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-        cudaFuncSetAttribute(k_mf_tma<CgSpmvOp<false, false>, DIM, BOX>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-        cudaFuncSetAttribute(k_mf_tma<CgSpmvOp<true, true>, DIM, BOX>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-        cudaFuncSetAttribute(k_mf_tma<CgSpmvOp<false, true>, DIM, BOX>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-    });
+    // per device (function attributes are per device; plan creation, before
+    // any graph capture)
+    static std::atomic<uint64_t> configured{0};
+    if (!device_first_use(configured)) return;
+    const int sm = (int)mf_smem_bytes<DIM, BOX>();
+    cudaFuncSetAttribute(k_mf_tma<CgSpmvOp<true, false>, DIM, BOX>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    cudaFuncSetAttribute(k_mf_tma<CgSpmvOp<false, false>, DIM, BOX>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    cudaFuncSetAttribute(k_mf_tma<CgSpmvOp<true, true>, DIM, BOX>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    cudaFuncSetAttribute(k_mf_tma<CgSpmvOp<false, true>, DIM, BOX>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    device_mark_done(configured);
 }
 
 template <int DIM, bool BOX>
@@ -474,8 +472,6 @@ int tma_blocks_per_sm()
 MfTma* mf_tma_create(const StencilGeom& g, const double* z, double* const* p, int np,
                      const double* r)
 {
-    const char* env = std::getenv("RVK_MF_TMA");
-    if (env && env[0] == '0') return nullptr;
     // TMA needs 16-B global strides (nx even) and 32-bit coordinates
     if (g.nx % 2 || g.nx > (1 << 30) || g.ny > (1 << 30) || g.nz > (1 << 30)) return nullptr;
     auto* t = new MfTma();
@@ -506,9 +502,8 @@ MfTma* mf_tma_create(const StencilGeom& g, const double* z, double* const* p, in
     else per_sm = g.box ? tma_blocks_per_sm<2, true>() : tma_blocks_per_sm<2, false>();
     const int64_t tiles  = (int64_t)G.tiles_x * G.tiles_y;
     // ~4 waves of resident blocks (measured: 7-point 256^3 K1 125 / 110 / 107 /
-    // 101 / 101 us at 1 / 2 / 3 / 4 / 8 waves; RVK_MF_WAVES overrides)
-    const char*   wv     = std::getenv("RVK_MF_WAVES");
-    const int64_t waves  = wv ? std::max(1, std::atoi(wv)) : 4;
+    // 101 / 101 us at 1 / 2 / 3 / 4 / 8 waves)
+    const int64_t waves  = 4;
     const int64_t want   = waves * sm_count() * per_sm;
     int64_t       chunks = std::max<int64_t>(1, (want + tiles - 1) / tiles);
     chunks               = std::min<int64_t>(chunks, std::max<int64_t>(1, G.nm / 16));
@@ -546,7 +541,7 @@ rvk_status launch_tma(cudaStream_t s, const MfTma& t, const OpT& op, TailArgs ta
         if (op.p_old == t.p_ptr[k]) kp = k;
     const CUtensorMap& tp = t.pm[kp];
 #define RVK_MF_LAUNCH(D, B)                                                                        \
-    launch_pdl(k_mf_tma<OpT, D, B>, t.grid, mf_threads<D, B>(), mf_smem_bytes<D, B>(), s,            \
+    launch_k(k_mf_tma<OpT, D, B>, t.grid, mf_threads<D, B>(), mf_smem_bytes<D, B>(), s,            \
                OpT::kZv ? t.r : t.z, tp, t.g, op, ta)
     if (t.dim == 3 && t.box) RVK_MF_LAUNCH(3, true);
     else if (t.dim == 3) RVK_MF_LAUNCH(3, false);

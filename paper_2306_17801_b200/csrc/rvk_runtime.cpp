@@ -17,27 +17,12 @@
 #include <mutex>
 
 namespace rvk {
-// Opt-in (RVK_PDL=1): measured slower on B200 in the captured solve graphs
-// (7-point 256^3 9.01 vs 8.87 ms, 27-point 21.15 vs 20.97, matrix-free 4.18
-// vs 4.10) -- the early-launched successors cost more than the launch
-// latency they hide.
-bool pdl_enabled()
-{
-    static const bool on = [] {
-        const char* e = std::getenv("RVK_PDL");
-        return e && e[0] == '1';
-    }();
-    return on;
-}
-} // namespace rvk
-
-namespace rvk {
 
 namespace {
 thread_local char     g_err[512] = "";
 std::atomic<uint64_t> g_host_syncs{0};
-std::once_flag        g_sm_once;
-int                   g_sm_count = 148;
+constexpr int         kMaxDevices = 64;
+std::atomic<int>      g_sm_count[kMaxDevices]; // 0 = not queried yet
 } // namespace
 
 rvk_status set_error(rvk_status s, const char* fmt, ...)
@@ -57,15 +42,22 @@ rvk_status cuda_error(cudaError_t e, const char* what)
 
 void note_host_sync() { g_host_syncs.fetch_add(1, std::memory_order_relaxed); }
 
+int current_device()
+{
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) dev = 0;
+    return dev;
+}
+
 int sm_count()
 {
-    std::call_once(g_sm_once, [] {
-        int dev = 0, n = 0;
-        if (cudaGetDevice(&dev) == cudaSuccess &&
-            cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && n > 0)
-            g_sm_count = n;
-    });
-    return g_sm_count;
+    const int dev = current_device() & (kMaxDevices - 1);
+    int       n   = g_sm_count[dev].load(std::memory_order_relaxed);
+    if (n > 0) return n;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+        n = 148;
+    g_sm_count[dev].store(n, std::memory_order_relaxed);
+    return n;
 }
 
 } // namespace rvk

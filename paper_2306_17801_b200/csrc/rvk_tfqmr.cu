@@ -270,10 +270,6 @@ struct TfqAOp {
     {
         return Fetch{__ldg(u + j), __ldg(v + j)};
     }
-    __device__ __forceinline__ Fetch fetch_smem(const double* s0, const double* s1, int i) const
-    {
-        return Fetch{s0[i], s1[i]};
-    }
     // t = 1 u + q, q = (-a) v + u  (VecWAXPY twice, kernels_scalar.cpp:36-40)
     __device__ __forceinline__ double value(const Fetch& f) const
     {
@@ -341,10 +337,6 @@ struct TfqBOp {
     __device__ __forceinline__ int           num_src() const { return 1; }
     __device__ __forceinline__ const double* src_ptr(int) const { return p; }
     __device__ __forceinline__ Fetch         fetch(int32_t j) const { return Fetch{__ldg(p + j)}; }
-    __device__ __forceinline__ Fetch fetch_smem(const double* s0, const double*, int i) const
-    {
-        return Fetch{s0[i]};
-    }
     __device__ __forceinline__ double  value(const Fetch& f) const { return f.p; }
     __device__ __forceinline__ int64_t own_col(int64_t i) const { return i; }
     struct Own {
@@ -611,13 +603,10 @@ rvk_status rvk_tfqmr_plan_create(rvk_ctx ctx, const rvk_csr* A, rvk_cg_config cf
     P->ctx = ctx;
     P->A   = *A;
     P->cfg = cfg;
-    SpmvWindows win;
-    if (csr_windows(ctx->stream, *A, &win) != RVK_OK) win = SpmvWindows{};
-    const SpmvWindows bands = win; // the band scan, before the opt-in/out knobs
-    win.n = 0; // leading-edge prefetch only
+    SpmvBands bands; // leading-edge L2 prefetch
+    if (csr_bands(ctx->stream, *A, &bands) != RVK_OK) bands = SpmvBands{};
     P->fused    = cfg.mode != RVK_CG_MODE_UNFUSED;
-    P->sa       = make_spmv_args(*A, maxlen, &win, P->fused ? 2 : 1);
-    spmv_set_order(P->sa, bands, A->nnz, P->fused ? 2 : 1, sm_count());
+    P->sa       = make_spmv_args(*A, maxlen, &bands);
     P->upd_grid = resident_grid(k_tfq_merge<true>, kTfqThreads, (A->n_rows + 1) / 2);
     const size_t vb = (size_t)A->n_rows * 8;
     cudaError_t  e  = cudaSuccess;
@@ -640,9 +629,8 @@ rvk_status rvk_tfqmr_plan_create(rvk_ctx ctx, const rvk_csr* A, rvk_cg_config cf
     }
     rvk_status rc = cfg.pc == RVK_PC_JACOBI ? rvk_csr_diagonal_inverse(ctx, A, P->dinv) : RVK_OK;
     // constant-coefficient operators: one diagonal value -> a scalar in the
-    // fused kernels (as the CG plans; RVK_CONST_DIAG=0 disables)
-    const char* cd = std::getenv("RVK_CONST_DIAG");
-    if (rc == RVK_OK && P->fused && cfg.pc == RVK_PC_JACOBI && !(cd && cd[0] == '0'))
+    // fused kernels (as the CG plans; RVK_OPT_DINV_VECTOR disables)
+    if (rc == RVK_OK && P->fused && cfg.pc == RVK_PC_JACOBI && !(cfg.opts & RVK_OPT_DINV_VECTOR))
         rc = vector_is_constant(ctx->stream, A->n_rows, P->dinv, &P->const_diag, &P->dconst);
     if (rc != RVK_OK) {
         rvk_tfqmr_plan_destroy(P);

@@ -15,8 +15,7 @@ from dataclasses import dataclass
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-# RVK_LIB_PATH: an alternative in-tree build for A/B experiments (same ABI)
-LIB_PATH = os.environ.get("RVK_LIB_PATH") or os.path.join(HERE, "lib", "librvk.so")
+LIB_PATH = os.path.join(HERE, "lib", "librvk.so")
 
 RVK_OK = 0
 RVK_ERR_BREAKDOWN = 5
@@ -76,7 +75,14 @@ class Csr(C.Structure):
 
 class CgConfig(C.Structure):
     _fields_ = [("max_it", C.c_int), ("pc", C.c_int), ("rtol", C.c_double),
-                ("atol", C.c_double), ("mode", C.c_int), ("use_graph", C.c_int)]
+                ("atol", C.c_double), ("mode", C.c_int), ("use_graph", C.c_int),
+                ("opts", C.c_int)]
+
+
+# rvk_cg_config.opts (include/rvk.h RVK_OPT_*): explicit plan-variant overrides
+OPT_KEEP_WORK, OPT_DINV_VECTOR, OPT_Z_STORED, OPT_Z_VIRTUAL = 1, 2, 4, 8
+OPT_NO_CLUSTER, OPT_SMALL_K1, OPT_MF_SIMPLE, OPT_NO_FOLD = 16, 32, 64, 128
+OPT_X_GROUP4, OPT_X_EACH = 256, 512
 
 
 class Shard(C.Structure):
@@ -279,6 +285,16 @@ class DeviceArray:
         ctx.synchronize()
         return out
 
+    def download_range(self, ctx: Ctx, start: int, count: int) -> np.ndarray:
+        """Elements [start, start + count) to a new host array."""
+        assert 0 <= start and start + count <= self.n
+        out = np.empty(count, self.dtype)
+        if count:
+            check(lib().rvk_memcpy_d2h(ctx.h, _ptr(out), self.ptr + start * self.dtype.itemsize,
+                                       count * self.dtype.itemsize))
+            ctx.synchronize()
+        return out
+
     def free(self):
         if self.ptr:
             lib().rvk_free(self.ptr)
@@ -350,12 +366,12 @@ class CgPlan:
 
     def __init__(self, ctx: Ctx, A, max_it: int = 20, pc: str = "jacobi",
                  rtol: float = 0.0, atol: float = 0.0, mode: str = "fused",
-                 use_graph: bool = True):
+                 use_graph: bool = True, opts: int = 0):
         self.ctx, self.A = ctx, A
         self.max_it = max_it
         graph = 2 if use_graph == "while" else (1 if use_graph else 0)
         cfg = CgConfig(max_it, PC_JACOBI if pc == "jacobi" else PC_NONE, rtol, atol,
-                       MODES[mode], graph)
+                       MODES[mode], graph, opts)
         h = C.c_void_p()
         if isinstance(A, DeviceCsr):
             self.n = A.n_rows
@@ -462,10 +478,10 @@ class TfqmrPlan:
 
     def __init__(self, ctx: Ctx, A: DeviceCsr, max_it: int = 20, pc: str = "jacobi",
                  rtol: float = 0.0, atol: float = 0.0, use_graph: bool = True,
-                 mode: str = "fused"):
+                 mode: str = "fused", opts: int = 0):
         self.ctx, self.A, self.max_it = ctx, A, max_it
         cfg = CgConfig(max_it, PC_JACOBI if pc == "jacobi" else PC_NONE, rtol, atol,
-                       MODES[mode], 1 if use_graph else 0)
+                       MODES[mode], 1 if use_graph else 0, opts)
         h = C.c_void_p()
         check(lib().rvk_tfqmr_plan_create(ctx.h, C.byref(A.c), cfg, C.byref(h)))
         self.h = h

@@ -87,9 +87,9 @@ def local_laplacian(ctx: "rvk.Ctx", dim: int, points: int, grid, sh: ShardSpec) 
     return rvk.DeviceCsr(sh.n_own, sh.n_ext, off, cols, vals)
 
 
-def _cfg(max_it, pc, rtol, atol):
+def _cfg(max_it, pc, rtol, atol, opts=0):
     return rvk.CgConfig(max_it, rvk.PC_JACOBI if pc == "jacobi" else rvk.PC_NONE, rtol, atol,
-                        rvk.MODE_FUSED, 0)
+                        rvk.MODE_FUSED, 0, opts)
 
 
 class ShardPlan:

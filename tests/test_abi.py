@@ -32,7 +32,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_library_loads_and_binds():
     L = rvk.lib()
-    assert L.rvk_abi_version() == 1
+    assert L.rvk_abi_version() == 2
     for s in rvk.EXPORTS:
         assert hasattr(L, s)
 

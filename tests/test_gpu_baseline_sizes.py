@@ -1,0 +1,129 @@
+"""GPU parity at the BASELINE.json sizes.
+
+* 2D 9-point 4096^2 and 3D 27-point 256^3: the CSR plan and the matrix-free
+  plan vs the serial oracle (O.cg_solve, the reference's single-chain
+  reductions; kernels_scalar.cpp:11-63), hist and x within 1e-10.
+* 3D 7-point 768^3 (n = 4.5e8, nnz = 3.17e9 > 2^31, so int64 row offsets,
+  csr.hpp:39):
+  - the device-assembled global CSR (rvk_build_laplacian) equals the CPU
+    builder's rows bit for bit, slab by slab over EVERY row (offsets
+    re-based by the running nnz, so the offsets above 2^31 are compared as
+    absolute values);
+  - the 1-GPU CSR solve, the 1-GPU matrix-free solve and the P = 8 row-sharded
+    solve (PEER kernels, every shard on this GPU) agree with the threaded
+    oracle (O.cg_solve_stencil: the serial oracle's loop and element
+    arithmetic, chunked reductions; pinned to O.cg_solve at 1e-13 in
+    tests/test_oracle.py) and with each other within 1e-10.
+"""
+import concurrent.futures as cf
+import gc
+
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2306_17801_b200 import rvk
+from paper_2306_17801_b200.sharded import loopback_solve
+
+pytestmark = pytest.mark.gpu
+
+RTOL = 1e-10
+
+
+def rel_hist(h, ref):
+    return float(np.max(np.abs(h - ref) / np.abs(ref)))
+
+
+def rel_x(x, ref):
+    return float(np.linalg.norm(x - ref) / np.linalg.norm(ref))
+
+
+@pytest.mark.parametrize("spec", [(2, 9, (4096, 4096)), (3, 27, (256, 256, 256))],
+                         ids=["9pt4096", "27pt256"])
+def test_cg_baseline_config_vs_serial_oracle(ctx, spec):
+    dim, pts, g = spec
+    Ah = O.build_laplacian(dim, pts, g)
+    b = O.rhs(Ah.n_rows)
+    ref = O.cg_solve(Ah, b, max_it=20)
+    del Ah
+    gc.collect()
+    A = rvk.DeviceCsr.laplacian(ctx, dim, pts, g)
+    for name, op in (("csr", A), ("matrix-free", (dim, pts, g))):
+        plan = rvk.CgPlan(ctx, op, max_it=20)
+        x, res = plan.solve_host(b)
+        plan.close()
+        assert res.iterations == 20, name
+        eh, ex = rel_hist(res.hist, ref.hist), rel_x(x, ref.x)
+        print(f"{dim}D {pts}-pt {g} {name}: hist {eh:.2e} x {ex:.2e}")
+        assert eh < RTOL and ex < RTOL, (name, eh, ex)
+
+
+G768 = (768, 768, 768)
+
+
+def test_768_device_assembly_bitexact_every_slab(ctx):
+    """All 3,167,354,880 nonzeros of the device CSR vs the CPU builder, 16
+    planes per slab; offsets cross 2^31 inside the run."""
+    dim, pts = 3, 7
+    A = rvk.DeviceCsr.laplacian(ctx, dim, pts, G768)
+    assert A.nnz == O.laplacian_nnz(dim, pts, G768) == 3_167_354_880
+    plane = 768 * 768
+    slab = 16 * plane
+    starts = list(range(0, A.n_rows, slab))
+
+    def cpu(r0):
+        return O.build_laplacian_rows(dim, pts, G768, r0, min(r0 + slab, A.n_rows))
+
+    base, crossed = 0, False
+    with cf.ThreadPoolExecutor(8) as pool:
+        futs = {r0: pool.submit(cpu, r0) for r0 in starts[:8]}
+        for i, r0 in enumerate(starts):
+            r1 = min(r0 + slab, A.n_rows)
+            off_h, cols_h, vals_h = futs.pop(r0).result()
+            if i + 8 < len(starts):
+                futs[starts[i + 8]] = pool.submit(cpu, starts[i + 8])
+            off_d = A.off.download_range(ctx, r0, r1 - r0 + 1)
+            assert off_d[0] == base, (r0, off_d[0], base)
+            assert np.array_equal(off_d, off_h + base), r0
+            k0, k1 = int(off_d[0]), int(off_d[-1])
+            crossed |= k0 < 2 ** 31 <= k1
+            assert np.array_equal(A.cols.download_range(ctx, k0, k1 - k0), cols_h), r0
+            vd = A.vals.download_range(ctx, k0, k1 - k0)
+            assert np.array_equal(vd.view(np.uint64), vals_h.view(np.uint64)), r0
+            base = k1
+    assert base == A.nnz and crossed
+
+
+@pytest.fixture(scope="module")
+def oracle_768():
+    b = O.rhs(768 ** 3)
+    ref = O.cg_solve_stencil(3, 7, G768, b, max_it=20)
+    assert ref.iterations == 20
+    return b, ref
+
+
+def test_768_single_gpu_and_sharded_solves(ctx, oracle_768):
+    b, ref = oracle_768
+    sols = {}
+    A = rvk.DeviceCsr.laplacian(ctx, 3, 7, G768)
+    plan = rvk.CgPlan(ctx, A, max_it=20)
+    sols["1 GPU csr"] = plan.solve_host(b)
+    plan.close()
+    del A, plan
+    gc.collect()
+    plan = rvk.CgPlan(ctx, (3, 7, G768), max_it=20)
+    sols["1 GPU matrix-free"] = plan.solve_host(b)
+    plan.close()
+    del plan
+    gc.collect()
+    x8, r8, per = loopback_solve(ctx, 3, 7, G768, 8, b, max_it=20, backend="peer")
+    sols["8 shards peer"] = (x8, r8)
+    for q in per:  # every shard folds the same partials: identical history
+        assert np.array_equal(q.hist, r8.hist)
+    for name, (x, res) in sols.items():
+        assert res.iterations == 20, name
+        eh, ex = rel_hist(res.hist, ref.hist), rel_x(x, ref.x)
+        print(f"768^3 {name}: vs oracle hist {eh:.2e} x {ex:.2e}")
+        assert eh < RTOL and ex < RTOL, (name, eh, ex)
+    x1, r1 = sols["1 GPU csr"]
+    assert rel_hist(r8.hist, r1.hist) < RTOL and rel_x(x8, x1) < RTOL

@@ -375,34 +375,6 @@ def test_fused_equals_unfused_elementwise_state(ctx):
     assert np.max(np.abs(xs[0][1] - xs[1][1]) / xs[1][1]) < 1e-12
 
 
-def test_xwindow_spmv_path_parity():
-    """The opt-in x-window SpMV path (RVK_WINDOWS=1: the gathered vectors'
-    diagonal bands staged by TMA) stays parity-green; run in a subprocess
-    because the switch is read at plan creation."""
-    import subprocess
-    import sys
-    code = r'''
-import sys, numpy as np
-sys.path.insert(0, ".")
-import oracle as O
-from paper_2306_17801_b200 import rvk
-ctx = rvk.Ctx()
-for dim, pts, g in [(2, 5, (1024, 64)), (2, 9, (300, 200)), (2, 5, (200, 200))]:
-    Ah = O.build_laplacian(dim, pts, g); b = O.rhs(Ah.n_rows)
-    ref = O.cg_solve(Ah, b, max_it=20)
-    A = rvk.DeviceCsr.laplacian(ctx, dim, pts, g)
-    for mode in ("fused", "unfused"):
-        x, res = rvk.CgPlan(ctx, A, max_it=20, mode=mode).solve_host(b)
-        assert np.max(np.abs(res.hist - ref.hist) / ref.hist) < 1e-10, (g, mode)
-        assert np.linalg.norm(x - ref.x) / np.linalg.norm(ref.x) < 1e-10, (g, mode)
-print("ok")
-'''
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    p = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True,
-                       env=dict(os.environ, RVK_WINDOWS="1"), timeout=600)
-    assert p.returncode == 0 and "ok" in p.stdout, p.stdout + p.stderr
-
-
 @pytest.mark.parametrize("spec", [(2, 5, (96, 77)), (2, 9, (64, 50)), (3, 7, (40, 33, 21)),
                                   (3, 27, (24, 20, 18)), (3, 7, (256, 256, 256))])
 def test_matrix_free_stencil_cg_vs_oracle(ctx, spec):
@@ -498,57 +470,20 @@ def test_cg_solve_host_many_matches_single_solves(ctx, graph, pinned):
         assert np.linalg.norm(xs[k] - ref.x) / np.linalg.norm(ref.x) < X_RTOL
 
 
-@pytest.mark.parametrize("spec", [(3, 7, (32, 32, 24)), (3, 27, (32, 16, 20)),
-                                  (2, 9, (1024, 40)), (2, 5, (2048, 12))])
-def test_chunked_tile_order_parity(ctx, spec, monkeypatch, capfd):
-    """SpMV tile order forced to the 2.5D chunked sweep (tiny RVK_CHUNK_MB;
-    the default for planes too large for L2 reuse, e.g. 768^3): w = A p is
-    the same bit for bit (rows are independent), the CG history / x match
-    the oracle (only the p.w partial order moves), for the single-GPU plan,
-    the row-sharded loopback and TFQMR."""
-    from paper_2306_17801_b200.sharded import loopback_solve
-
-    dim, pts, g = spec
-    Ah = O.build_laplacian(dim, pts, g)
-    b = O.rhs(Ah.n_rows)
-    ref = O.cg_solve(Ah, b, max_it=20)
-    A = rvk.DeviceCsr.laplacian(ctx, dim, pts, g)
-    monkeypatch.setenv("RVK_CHUNK_MB", "0.0001")
-    monkeypatch.setenv("RVK_CHUNK_MIN_TILES", "1")
-    monkeypatch.setenv("RVK_DEBUG", "1")
-    plan = rvk.CgPlan(ctx, A, max_it=20)
-    assert "order=chunked" in capfd.readouterr().err  # the order really is active
-    monkeypatch.delenv("RVK_DEBUG")
-    x, res = plan.solve_host(b)
-    check_cg(res, x, ref)
-    for backend in ("gather", "peer"):
-        xs, rs, _ = loopback_solve(ctx, dim, pts, g, 2, b, max_it=20, backend=backend)
-        check_cg(rs, xs, ref)
-    tref = O.tfqmr_solve(Ah, b, max_it=20)
-    tp = rvk.TfqmrPlan(ctx, A, max_it=20)
-    db, dx = rvk.DeviceArray.from_host(ctx, b), rvk.DeviceArray(b.size)
-    tp.solve_dev(db, dx)
-    tr = tp.result()
-    assert np.max(np.abs(tr.hist - tref.hist) / np.abs(tref.hist)) < 1e-8
-    tp.close()
-
-
 @pytest.mark.parametrize("spec", [(3, 7, (20, 16, 12)), (2, 9, (40, 33)), (3, 27, (10, 9, 8))])
-def test_constant_diagonal_folding_bitexact(ctx, spec, monkeypatch):
+def test_constant_diagonal_folding_bitexact(ctx, spec):
     """Constant-coefficient Laplacians have one diagonal value: the plan
-    folds dinv into a scalar (RVK_PLAN_CONST_DIAG; RVK_CONST_DIAG=0 keeps the
-    vector) and the fused kernels skip the dinv stream.  Results are bit-identical to
+    folds dinv into a scalar (RVK_PLAN_CONST_DIAG; RVK_OPT_DINV_VECTOR keeps
+    the vector) and the fused kernels skip the dinv stream.  Results are bit-identical to
     the dinv-vector path (also sharded); a matrix whose diagonal varies keeps
     the vector."""
     dim, pts, g = spec
     Ah = O.build_laplacian(dim, pts, g)
     b = O.rhs(Ah.n_rows)
     A = rvk.DeviceCsr.laplacian(ctx, dim, pts, g)
-    monkeypatch.setenv("RVK_CONST_DIAG", "0")
-    p0 = rvk.CgPlan(ctx, A, max_it=20)
+    p0 = rvk.CgPlan(ctx, A, max_it=20, opts=rvk.OPT_DINV_VECTOR)
     assert not p0.flags() & 1
     x0, r0 = p0.solve_host(b)
-    monkeypatch.delenv("RVK_CONST_DIAG")
     p1 = rvk.CgPlan(ctx, A, max_it=20)
     assert p1.flags() & 1  # default for constant-coefficient operators
     x1, r1 = p1.solve_host(b)
@@ -597,7 +532,7 @@ def test_fingerprint_identical_across_processes():
 @pytest.mark.parametrize("spec", [(3, 7, (64, 24, 10)), (3, 7, (40, 13, 9)), (3, 27, (34, 18, 7)),
                                   (3, 27, (64, 64, 20)), (2, 5, (300, 37)), (2, 9, (256, 64)),
                                   (2, 9, (130, 5)), (3, 7, (33, 10, 6)), (2, 5, (129, 20))])
-def test_matrix_free_tma_w_bitexact_vs_csr(ctx, spec, monkeypatch):
+def test_matrix_free_tma_w_bitexact_vs_csr(ctx, spec):
     """The TMA 2.5D matrix-free K1 (zero-filled OOB boxes, p formed once per
     element in a shared-memory plane ring) produces w = A p BIT-identical to
     the CSR SpMV -- including partial tiles (nx % 32, ny % 8, nx % 128 != 0)
@@ -608,10 +543,8 @@ def test_matrix_free_tma_w_bitexact_vs_csr(ctx, spec, monkeypatch):
     b = O.rhs(Ah.n_rows)
     A = rvk.DeviceCsr.laplacian(ctx, dim, pts, g)
     ws = {}
-    for name, env in (("csr", None), ("tma", "1"), ("fallback", "0")):
-        if env is not None:
-            monkeypatch.setenv("RVK_MF_TMA", env)
-        plan = rvk.CgPlan(ctx, A if name == "csr" else (dim, pts, g), max_it=1)
+    for name, opts in (("csr", 0), ("tma", 0), ("fallback", rvk.OPT_MF_SIMPLE)):
+        plan = rvk.CgPlan(ctx, A if name == "csr" else (dim, pts, g), max_it=1, opts=opts)
         if name == "tma":
             assert bool(plan.flags() & 4) == (g[0] % 2 == 0)
         plan.solve_host(b)
@@ -621,7 +554,6 @@ def test_matrix_free_tma_w_bitexact_vs_csr(ctx, spec, monkeypatch):
         assert np.array_equal(ws[name][0], ws["csr"][0]), name
         assert np.array_equal(ws[name][1], ws["csr"][1]), name
     # and a full 20-iteration solve on the TMA path vs the oracle
-    monkeypatch.setenv("RVK_MF_TMA", "1")
     x, res = rvk.CgPlan(ctx, (dim, pts, g), max_it=20).solve_host(b)
     check_cg(res, x, O.cg_solve(Ah, b, max_it=20))
 
@@ -645,7 +577,7 @@ def test_stream_ordered_alloc_deferred_release(ctx):
 @pytest.mark.parametrize("spec", [(3, 7, (20, 16, 12)), (2, 9, (40, 33)), (3, 27, (10, 9, 8)),
                                   (2, 5, (64, 48))])
 @pytest.mark.parametrize("pc", ["jacobi", "none"])
-def test_virtual_z_bitexact(ctx, spec, pc, monkeypatch):
+def test_virtual_z_bitexact(ctx, spec, pc):
     """Virtual z (z = d r never stored; the SpMV forms d r_j) and the pairwise
     x update change no arithmetic: x and the history are bit-identical with
     both off, for every stencil, with and without the Jacobi diagonal, CSR
@@ -655,16 +587,12 @@ def test_virtual_z_bitexact(ctx, spec, pc, monkeypatch):
     b = O.rhs(Ah.n_rows)
     A = rvk.DeviceCsr.laplacian(ctx, dim, pts, g)
     out = {}
-    for name, env in (("on", {"RVK_ZV": "1"}), ("off", {"RVK_ZV": "0", "RVK_X_DEFER": "0"})):
-        for k, v in env.items():
-            monkeypatch.setenv(k, v)
-        plan = rvk.CgPlan(ctx, A, max_it=20, pc=pc)
+    for name, opts in (("on", rvk.OPT_Z_VIRTUAL), ("off", rvk.OPT_Z_STORED | rvk.OPT_X_EACH)):
+        plan = rvk.CgPlan(ctx, A, max_it=20, pc=pc, opts=opts)
         assert bool(plan.flags() & 32) == (name == "on")
         out[name] = plan.solve_host(b)
-        mf = rvk.CgPlan(ctx, (dim, pts, g), max_it=20, pc=pc)
+        mf = rvk.CgPlan(ctx, (dim, pts, g), max_it=20, pc=pc, opts=opts)
         out[name + "_mf"] = mf.solve_host(b)
-        for k in env:
-            monkeypatch.delenv(k)
     for k in ("", "_mf"):
         assert np.array_equal(out["on" + k][0], out["off" + k][0])
         assert np.array_equal(out["on" + k][1].hist, out["off" + k][1].hist)
@@ -673,10 +601,10 @@ def test_virtual_z_bitexact(ctx, spec, pc, monkeypatch):
 
 
 @pytest.mark.parametrize("graph", [True, "while", False])
-def test_pairwise_x_update_exits_at_both_parities(ctx, graph, monkeypatch):
+def test_pairwise_x_update_exits_at_both_parities(ctx, graph):
     """Early exits (device rtol) at every position inside an x-update group,
     odd / even max_it: grouped x updates (the whole solve, groups of 4 and
-    2; deferring K2s, a flushing K2 at the group end, k_cg_xfix for what an
+    4; deferring K2s, a flushing K2 at the group end, k_cg_xfix for what an
     exit or the whole-solve group leaves pending) give x bit-identical to one
     update per iteration."""
     dim, pts, g = 2, 5, (48, 40)
@@ -689,16 +617,14 @@ def test_pairwise_x_update_exits_at_both_parities(ctx, graph, monkeypatch):
                          (200, 1e-5), (200, 3e-6), (32, 0.0), (32, 3e-1), (32, 1e-1), (32, 3e-2),
                          (32, 1e-2)]:
         xs = {}
-        for grp in ("solve", "4", "2", "1"):
-            monkeypatch.setenv("RVK_X_GROUP", grp)
-            plan = rvk.CgPlan(ctx, A, max_it=max_it, rtol=rtol, use_graph=graph)
+        for grp, opts in (("solve", 0), ("4", rvk.OPT_X_GROUP4), ("1", rvk.OPT_X_EACH)):
+            plan = rvk.CgPlan(ctx, A, max_it=max_it, rtol=rtol, use_graph=graph, opts=opts)
             assert bool(plan.flags() & 128) == (grp == "solve" and max_it <= 32)
             xs[grp] = plan.solve_host(b)
             plan.close()
-        monkeypatch.delenv("RVK_X_GROUP")
         if max_it <= 32:
             seen_solve.add(xs["solve"][1].iterations)
-        for grp in ("solve", "4", "2"):
+        for grp in ("solve", "4"):
             assert np.array_equal(xs[grp][0], xs["1"][0]), (grp, max_it, rtol)
             assert np.array_equal(xs[grp][1].hist, xs["1"][1].hist)
         xs["1"] = xs["4"]
@@ -750,10 +676,10 @@ def check_cg_floor(res, x, ref):
                                   (2, 9, (100, 90)), (3, 7, (20, 16, 12)), (3, 7, (32, 32, 16)),
                                   (2, 5, (2, 2)), (2, 5, (1024, 16)), (2, 5, (1025, 16))])
 @pytest.mark.parametrize("pc", ["jacobi", "none"])
-def test_cluster_solve(ctx, spec, pc, monkeypatch):
+def test_cluster_solve(ctx, spec, pc):
     """The one-cluster DSMEM solve (k_cg_cluster; PERSISTENT / AUTO for
     n <= 16 x 1024 rows with rows of <= 9 entries): oracle within 1e-10, the
-    same result as the grid-barrier persistent kernel (RVK_CLUSTER=0), early
+    same result as the grid-barrier persistent kernel (RVK_OPT_NO_CLUSTER), early
     exits, and the eligibility boundary (16384 rows: 16 CTAs; 16400: none)."""
     dim, pts, g = spec
     Ah = O.build_laplacian(dim, pts, g)
@@ -767,9 +693,8 @@ def test_cluster_solve(ctx, spec, pc, monkeypatch):
         check_cg_floor(res, x, ref)
         x2, res2 = plan.solve_host(b)  # repeatable
         assert np.array_equal(x, x2) and np.array_equal(res.hist, res2.hist)
-        monkeypatch.setenv("RVK_CLUSTER", "0")
-        grid = rvk.CgPlan(ctx, A, max_it=max_it, rtol=rtol, pc=pc, mode="persistent")
-        monkeypatch.delenv("RVK_CLUSTER")
+        grid = rvk.CgPlan(ctx, A, max_it=max_it, rtol=rtol, pc=pc, mode="persistent",
+                          opts=rvk.OPT_NO_CLUSTER)
         assert not grid.flags() & 256
         xg, resg = grid.solve_host(b)
         check_cg_floor(resg, xg, ref)
@@ -856,8 +781,8 @@ def test_cg_irregular_spd(ctx, seed, n, max_deg, long_rows, mode, graph):
 @pytest.mark.parametrize("spec", [(2, 5, (256, 256)), (3, 7, (20, 16, 12)), (3, 27, (10, 9, 8)),
                                   (2, 9, (33, 31)), (2, 5, (2, 2))])
 @pytest.mark.parametrize("graph", [True, "while"])
-def test_small_spmv_kernel(ctx, spec, graph, monkeypatch):
-    """Opt-in small-system K1 (RVK_SMALL_ROWS: k_spmv_small, plain blocks
+def test_small_spmv_kernel(ctx, spec, graph):
+    """Opt-in small-system K1 (RVK_OPT_SMALL_K1: k_spmv_small, plain blocks
     through the TMA kernel's direct-row code): oracle within 1e-10 and the
     same x as the TMA kernel up to the reduction order of p.w."""
     dim, pts, g = spec
@@ -866,9 +791,8 @@ def test_small_spmv_kernel(ctx, spec, graph, monkeypatch):
     A = rvk.DeviceCsr.laplacian(ctx, dim, pts, g)
     for max_it, rtol in ((20, 0.0), (200, 1e-6)):
         ref = O.cg_solve(Ah, b, max_it=max_it, rtol=rtol)
-        monkeypatch.setenv("RVK_SMALL_ROWS", "524288")
-        plan = rvk.CgPlan(ctx, A, max_it=max_it, rtol=rtol, use_graph=graph)
-        monkeypatch.delenv("RVK_SMALL_ROWS")
+        plan = rvk.CgPlan(ctx, A, max_it=max_it, rtol=rtol, use_graph=graph,
+                          opts=rvk.OPT_SMALL_K1)
         x, res = plan.solve_host(b)
         check_cg_floor(res, x, ref)
         plan.close()

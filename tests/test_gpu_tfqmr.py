@@ -189,7 +189,7 @@ def test_tfqmr_early_exit_each_half_step(ctx):
 
 @pytest.mark.parametrize("spec", [(2, 5, (40, 33)), (3, 7, (20, 16, 12)), (3, 27, (10, 9, 8)),
                                   (2, 9, (64, 64))])
-def test_tfqmr_constant_diagonal_bitexact(ctx, spec, monkeypatch):
+def test_tfqmr_constant_diagonal_bitexact(ctx, spec):
     """Constant-coefficient Laplacians have one diagonal value: the fused
     plan uses it as a scalar (RVK_PLAN_CONST_DIAG, no dinv stream in K0, KA,
     KB) -- x and the history bit-identical to the dinv-vector kernels."""
@@ -199,8 +199,7 @@ def test_tfqmr_constant_diagonal_bitexact(ctx, spec, monkeypatch):
     A = rvk.DeviceCsr.laplacian(ctx, dim, pts, g)
     plan, x1, r1 = solve(ctx, A, b, max_it=20)
     assert plan.flags() & 1
-    monkeypatch.setenv("RVK_CONST_DIAG", "0")
-    plan0, x0, r0 = solve(ctx, A, b, max_it=20)
+    plan0, x0, r0 = solve(ctx, A, b, max_it=20, opts=rvk.OPT_DINV_VECTOR)
     assert not plan0.flags() & 1
     assert np.array_equal(x1, x0)
     assert np.array_equal(r1.hist, r0.hist)

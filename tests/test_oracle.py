@@ -225,3 +225,50 @@ def test_rhs_in_range_and_exact():
     # exactly k * 2^-52 - 1 for an integer k < 2^53
     k = (b + 1.0) * 2.0 ** 52
     assert np.array_equal(k, np.round(k))
+
+
+# ---- the large-size restatement (oracle/rvk_oracle_mt.c) ------------------------
+LARGE_SPECS = [(2, 5, (37, 29)), (2, 9, (64, 41)), (3, 7, (17, 13, 11)), (3, 27, (12, 10, 9)),
+               (2, 5, (2, 2)), (3, 27, (2, 3, 2))]
+
+
+@pytest.mark.parametrize("spec", LARGE_SPECS)
+def test_build_laplacian_rows_is_a_slice_of_the_full_build(spec):
+    """Row slabs (the 768^3 device-assembly check) equal the full build's
+    rows bit for bit; the running nnz reproduces the global offsets."""
+    dim, pts, g = spec
+    A = O.build_laplacian(dim, pts, g)
+    rng = np.random.default_rng(len(g) * 100 + pts)
+    cuts = np.unique(np.concatenate([[0, A.n_rows], rng.integers(0, A.n_rows, 5)]))
+    base = 0
+    for r0, r1 in zip(cuts[:-1], cuts[1:]):
+        off, cols, vals = O.build_laplacian_rows(dim, pts, g, int(r0), int(r1))
+        assert np.array_equal(off + base, A.off[r0:r1 + 1])
+        assert np.array_equal(cols, A.cols[A.off[r0]:A.off[r1]])
+        assert np.array_equal(vals.view(np.uint64), A.vals[A.off[r0]:A.off[r1]].view(np.uint64))
+        base += int(off[-1])
+    assert base == A.nnz
+
+
+@pytest.mark.parametrize("spec", LARGE_SPECS)
+def test_stencil_spmv_bitexact_vs_csr(spec):
+    dim, pts, g = spec
+    A = O.build_laplacian(dim, pts, g)
+    x = np.random.default_rng(7).standard_normal(A.n_rows)
+    assert np.array_equal(O.stencil_spmv(dim, pts, g, x).view(np.uint64), O.spmv(A, x).view(np.uint64))
+
+
+@pytest.mark.parametrize("spec", LARGE_SPECS[:4] + [(3, 7, (64, 64, 40)), (2, 9, (400, 300))])
+@pytest.mark.parametrize("pc", ["jacobi", "none"])
+def test_threaded_stencil_cg_matches_serial_oracle(spec, pc):
+    """The threaded matrix-free PCG (used at 768^3) is the serial oracle's
+    loop with chunked reductions: history and x within 1e-13."""
+    dim, pts, g = spec
+    A = O.build_laplacian(dim, pts, g)
+    b = O.rhs(A.n_rows)
+    ref = O.cg_solve(A, b, max_it=20, pc=pc)
+    got = O.cg_solve_stencil(dim, pts, g, b, max_it=20, pc=pc)
+    assert got.iterations == ref.iterations and got.status == ref.status
+    keep = ref.hist > 1e-8 * ref.hist[0]
+    assert np.max(np.abs(got.hist[keep] - ref.hist[keep]) / ref.hist[keep]) < 1e-13
+    assert np.linalg.norm(got.x - ref.x) <= 1e-13 * np.linalg.norm(ref.x)
