@@ -60,21 +60,20 @@ def peaks():
 
 
 def bytes_model(n: int, nnz: int, mode: str = "fused", const_diag: bool = False,
-                off32: bool = False, x_defer: bool = False, z_virtual: bool = False,
+                x_defer: bool = False, z_virtual: bool = False,
                 x_group: int = 2, fold_setup: bool = False):
     """Algorithmic HBM bytes.  All FP64 + int64 offsets + int32 cols.
     k1 = the SpMV launch (fused: + on-the-fly AYPX), k2 = the rest of an iteration.
     const_diag: the plan folded a constant Jacobi diagonal into a scalar
     (RVK_PLAN_CONST_DIAG), so the dinv stream (8n per iteration and in the
-    setup) is not part of the algorithm's traffic any more.  off32: the SpMV
-    streams the plan's int32 copy of the row offsets (RVK_PLAN_OFF32): 4 instead
-    of 8 bytes per row.  x_defer: x += a p applied once per GROUP of x_group
+    setup) is not part of the algorithm's traffic any more.  x_defer: x += a p
+    applied once per GROUP of x_group
     iterations (RVK_PLAN_X_DEFER / _X_GROUP4 / _X_SOLVE = the whole solve):
     the x traffic per iteration drops from 24 n (p read, x read + write) to
     8 n + 16 n / x_group.
     z_virtual: z = d r is never stored (RVK_PLAN_Z_VIRTUAL): K2 and the setup
     write 8 n less; K1 gathers r instead of z (same bytes)."""
-    ob = 4 if off32 else 8
+    ob = 8  # int64 row offsets
     # x_group > 4 (the whole solve): K2 never touches x; one k_cg_xfix pass at
     # the end reads the x_group p's and writes x (starting from 0.0: the setup
     # does not store x = 0 either) -- counted per solve
@@ -164,126 +163,173 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def ncu_traffic(config: str):
-    """DRAM bytes per K1 launch from the committed `ncu --set full` summary."""
+def _file_sha16(path: str) -> str | None:
+    import hashlib
+    try:
+        with open(path, "rb") as f:
+            return hashlib.sha256(f.read()).hexdigest()[:16]
+    except OSError:
+        return None
+
+
+def ncu_traffic(config: str, kernel: str = "k1"):
+    """DRAM bytes per launch of `kernel` from the committed `ncu --set full`
+    summary (profiles/ncu_summary.json), with where it came from: the capture
+    records the sha of the librvk.so it profiled, compared here with the
+    library this run loaded (a kernel change without a profile refresh shows
+    up as build_match = false)."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if not os.path.exists(p):
-        return None
+        return None, None
     with open(p) as f:
         d = json.load(f)
-    k = d.get(config, {}).get("k1")
-    return k.get("dram_bytes") if k else None
+    k = d.get(config, {}).get(kernel)
+    if not k:
+        return None, None
+    lib = os.path.join(ROOT, "paper_2306_17801_b200", "lib", "librvk.so")
+    src = {"file": "profiles/ncu_summary.json", "capture": d.get("_note"),
+           "captured_lib_sha16": d.get("lib_sha16"), "loaded_lib_sha16": _file_sha16(lib)}
+    src["build_match"] = bool(src["captured_lib_sha16"]) and \
+        src["captured_lib_sha16"] == src["loaded_lib_sha16"]
+    return k.get("dram_bytes"), src
 
 
-def cpu_baseline(dim, pts, grid, steps=1):
-    """The reference's own kernels (oracle/_ref, kernels_scalar.cpp via dispatch)
-    running the restated PCG, 1 host thread (the kernels are single-threaded).
-    Sample = `steps` full 20-iteration solves of the SAME workload, or, above
-    ~256^3 rows, of a slab of whole planes of it (~16.8 M rows) with each
-    time scaled to the workload by nnz.  Returns (kind, times_ms, sample)."""
-    import oracle as O
-    kind = "reference" if O.ref_available() else "port"
+# ---- workload and config (identical for the GPU arm and the reference arm) ----
+STRONG = {"7pt768"}   # configs whose total work is fixed as N grows
+
+
+def workload(args, world: int):
+    """(dim, pts, global grid, desc, strong): weak scaling stacks one
+    config-sized slab per GPU along the slowest axis; 7pt768 is the fixed
+    (strong-scaling) grid of BASELINE.json configs[4]."""
+    dim, pts, grid, desc = CONFIGS[args.config]
+    strong = args.config in STRONG
+    if world > 1 and not strong:
+        return dim, pts, tuple(grid[:-1]) + (grid[-1] * world,), desc, False
+    return dim, pts, tuple(grid), desc, strong
+
+
+def bench_config(args, world: int) -> dict:
+    dim, pts, g, desc, strong = workload(args, world)
+    n, nnz = _laplacian_size(dim, pts, g)
+    wl = f"{desc}, Jacobi-CG {MAX_IT} iterations, x0=0, splitmix64 RHS"
+    if g != tuple(CONFIGS[args.config][2]):
+        wl += f"; global grid {'x'.join(map(str, g))} ({world} row slabs)"
+    cfg = {"workload": wl, "n": n, "nnz": nnz}
+    if world > 1:
+        cfg["parallelism"] = f"rows{world}"
+    return cfg
+
+
+def scaling_label(args) -> str:
+    return "strong" if args.config in STRONG else "weak"
+
+
+# ---- the reference CPU solver (oracle/_ref), bounded sample ------------------
+SAMPLE_ROWS = 1 << 22
+
+
+def sample_grid(dim, grid):
+    """The CPU sample: whole planes (slowest axis) of the workload grid, at most
+    SAMPLE_ROWS rows (~1.5 s per 20-iteration solve on one core)."""
     nx, ny, nz = (list(grid) + [1, 1])[:3]
     plane, nplanes = (nx * ny, nz) if dim == 3 else (nx, ny)
-    sgrid = tuple(grid)
-    if plane * nplanes > 256 ** 3:
-        k = max(1, 256 ** 3 // plane)
-        sgrid = (nx, ny, k) if dim == 3 else (nx, k)
-    A = O.build_laplacian(dim, pts, sgrid)
+    k = max(2, min(nplanes, SAMPLE_ROWS // plane))
+    return ((nx, ny, k) if dim == 3 else (nx, k)) if k < nplanes else tuple(grid)
+
+
+def time_reference(dim, pts, grid, steps: int, warmup: int) -> dict:
+    """The reference's own kernels (oracle/_ref, kernels_{scalar,avx2}.cpp)
+    driving the PETSc-order PCG on this host, 1 thread (the reference's
+    kernels are single-threaded), on a bounded sample of the workload, each
+    time scaled to the whole workload by nnz (per-iteration cost is linear in
+    nnz and n at a fixed stencil).  Both backends are timed once; the FASTEST
+    is the baseline (the reference's auto dispatch picks AVX2 when present,
+    kernels_dispatch.cpp:76-89, which is not always the faster one).  The
+    oracle port stands in when oracle/_ref is absent (kind "port")."""
+    import oracle as O
+    kind = "reference" if O.ref_available() else "port"
+    sg = sample_grid(dim, grid)
+    A = O.build_laplacian(dim, pts, sg)
     b = O.rhs(A.n_rows)
     scale = _laplacian_size(dim, pts, grid)[1] / A.nnz
+    if kind == "reference":
+        backends = {"scalar": 0}
+        if O.ref_lib().ref_avx2_supported():
+            backends["avx2"] = 1
+        solvers = {k: (lambda be=be: O.ref_cg_solve(A, b, max_it=MAX_IT, backend=be))
+                   for k, be in backends.items()}
+    else:
+        solvers = {"port": lambda: O.cg_solve(A, b, max_it=MAX_IT)}
+    solvers[next(iter(solvers))]()  # first touch of the work arrays (page faults), untimed
+    per = {}
+    for name, f in solvers.items():
+        t0 = time.perf_counter()
+        f()
+        per[name] = (time.perf_counter() - t0) * 1e3 * scale
+    best = min(per, key=per.get)
+    for _ in range(warmup):
+        solvers[best]()
     times = []
     for _ in range(steps):
         t0 = time.perf_counter()
-        if kind == "reference":
-            O.ref_cg_solve(A, b, max_it=MAX_IT, backend=2)   # reference auto dispatch
-        else:
-            O.cg_solve(A, b, max_it=MAX_IT)
+        solvers[best]()
         times.append((time.perf_counter() - t0) * 1e3 * scale)
-    what = (f"{steps} full {MAX_IT}-iteration solve(s)" if sgrid == tuple(grid) else
-            f"{steps} {MAX_IT}-iteration solve(s) of a {sgrid} slab, scaled by nnz x{scale:.3f}")
-    return kind, times, what
-
-
-def workload_grid(args, cfg, world: int):
-    """The global grid bench.py solves at N = world GPUs (sharded.bench_main):
-    weak scaling stacks one config-sized slab per GPU along the slowest axis;
-    7pt768 is strong scaling of the fixed grid."""
-    dim, pts, grid, desc = cfg
-    if world > 1 and args.config != "7pt768":
-        return tuple(grid[:-1]) + (grid[-1] * world,)
-    return tuple(grid)
+    if not times:
+        times = [per[best]]
+    what = (f"full {MAX_IT}-iteration solves" if sg == tuple(grid) else
+            f"{MAX_IT}-iteration solves of a {'x'.join(map(str, sg))} slab (whole planes, "
+            f"{A.n_rows} rows) of the {'x'.join(map(str, grid))} workload, each scaled by nnz "
+            f"x{scale:.3f}")
+    return {"kind": kind, "best": best, "per_backend_ms": {k: round(v, 1) for k, v in per.items()},
+            "times_ms": times, "sample": what, "cores": 1}
 
 
 def run_reference(args, cfg):
-    """The reference CPU solver (reference kernels from oracle/_ref driving the
-    PETSc-order PCG, or the oracle port) on the host, rank 0 only.  For
-    workloads above ~256^3 rows (N > 1 weak scaling, 768^3) one bounded sample
-    is timed -- a slab of whole planes of the same grid holding ~16.8 M rows --
-    and scaled to the whole workload by nnz (per-iteration cost is linear in
-    nnz and n at fixed stencil)."""
+    """--impl reference: the reference CPU solver on this host, rank 0 only
+    (other ranks exit without work), on the GPU arm's workload / config /
+    metric.  Each step is one bounded sample solve with the reference's
+    fastest backend (time_reference)."""
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
-    dim, pts, grid, desc = cfg
     t_all = time.perf_counter()
-    import oracle as O
-    kind = "reference" if O.ref_available() else "port"
-    full = workload_grid(args, cfg, world)
-    nx, ny, nz = (list(full) + [1, 1])[:3]
-    plane = nx * ny if dim == 3 else nx
-    nplanes = nz if dim == 3 else ny
-    cap = 256 ** 3
-    sample = full
-    if plane * nplanes > cap:
-        k = max(1, cap // plane)
-        sample = (nx, ny, k) if dim == 3 else (nx, k)
-    A = O.build_laplacian(dim, pts, sample)
-    b = O.rhs(A.n_rows)
-    n_full, nnz_full = _laplacian_size(dim, pts, full)
-    scale = nnz_full / A.nnz
-    solve = (lambda: O.ref_cg_solve(A, b, max_it=MAX_IT, backend=2)) if kind == "reference" \
-        else (lambda: O.cg_solve(A, b, max_it=MAX_IT))
-    for _ in range(args.warmup):
-        solve()
-    times = []
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        solve()
-        times.append((time.perf_counter() - t0) * 1e3 * scale)
-    ms = statistics.mean(times)
-    # SURVEY.md 8d: the reference's scalar and AVX2 backends, one solve each
-    per_backend = {}
-    if kind == "reference":
-        for name, be in (("scalar", 0), ("avx2", 1)):
-            t0 = time.perf_counter()
-            O.ref_cg_solve(A, b, max_it=MAX_IT, backend=be)
-            per_backend[name] = round((time.perf_counter() - t0) * 1e3 * scale, 3)
-    bm = bytes_model(n_full, nnz_full)
-    what = (f"{args.steps} full {MAX_IT}-iteration solves of {desc}" if sample == full else
-            f"{args.steps} {MAX_IT}-iteration solves of a {sample} slab of the {full} workload "
-            f"(whole planes, {A.n_rows} rows), each scaled by nnz x{scale:.3f}")
-    wl = f"{desc}, Jacobi-CG {MAX_IT} iterations" + (f", global grid {full} (N={world})"
-                                                       if full != tuple(grid) else "")
+    dim, pts, g, desc, _ = workload(args, world)
+    ref = time_reference(dim, pts, g, args.steps, args.warmup)
+    ms = statistics.mean(ref["times_ms"])
+    n, nnz = _laplacian_size(dim, pts, g)
+    bm = bytes_model(n, nnz)
     out = {
         "metric": METRIC, "impl": "reference", "value": round(ms, 3), "unit": "ms/solve",
         "n_gpus": 0, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
-        "min_ms": round(min(times), 3), "higher_is_better": False,
-        "scaling": "strong" if args.config == "7pt768" else "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": wl, "n": n_full, "nnz": nnz_full},
-        "cpu_baseline": {"value": round(ms, 3), "unit": "ms/solve", "cores": 1, "kind": kind,
-                         "sample": what + " (reference kernels_*.cpp, auto AVX2/scalar dispatch, "
-                                          "single-threaded like the reference's kernels)",
-                         "per_backend_ms": per_backend, "host_cpu": host_cpu()},
+        "min_ms": round(min(ref["times_ms"]), 3), "higher_is_better": False,
+        "scaling": scaling_label(args), "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": bench_config(args, world),
+        "cpu_baseline": {"value": round(ms, 3), "unit": "ms/solve", "cores": ref["cores"],
+                         "kind": ref["kind"],
+                         "sample": ref["sample"] + f" ({ref['best']} backend: the fastest of "
+                                   + ", ".join(ref["per_backend_ms"]) + ")",
+                         "per_backend_ms": ref["per_backend_ms"], "host_cpu": host_cpu()},
         "e2e": {"value": round(ms, 3), "unit": "ms/solve", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "achieved_gbs_bref": round(bm["b_ref_solve"] / (ms * 1e-3) / 1e9, 2),
         "host_syncs_per_iter": 0,
     }
-    log(f"reference CPU: {ms:.1f} ms/solve (min {min(times):.1f}); total {time.perf_counter()-t_all:.0f}s")
+    log(f"reference CPU ({ref['best']}): {ms:.1f} ms/solve (min {min(ref['times_ms']):.1f}); "
+        f"per backend {ref['per_backend_ms']}; total {time.perf_counter()-t_all:.0f}s")
     print(json.dumps(out), flush=True)
+
+
+def cpu_baseline_entry(dim, pts, grid) -> dict:
+    """cpu_baseline of a GPU line: one sample solve per reference backend, the
+    fastest reported (time_reference)."""
+    ref = time_reference(dim, pts, grid, steps=0, warmup=0)
+    return {"value": round(ref["per_backend_ms"][ref["best"]], 1), "unit": "ms/solve",
+            "cores": ref["cores"], "kind": ref["kind"],
+            "sample": "1 " + ref["sample"] + f" on the GPU box host per backend; value = the "
+                      f"fastest ({ref['best']})",
+            "per_backend_ms": ref["per_backend_ms"], "host_cpu": host_cpu()}
 
 
 def host_cpu() -> dict:
@@ -431,11 +477,67 @@ def run_tfqmr(args, cfg):
     ctx.close()
 
 
+def time_solves(plan, b, x, stream, steps, warmup, flush=None):
+    """K solves bracketed by CUDA events on the solve stream (device time),
+    after `warmup` untimed ones; nvidia-smi clocks sampled during the timed
+    region.  Returns (per-step ms, clock summary, host syncs counted)."""
+    import torch
+    from paper_2306_17801_b200 import rvk
+    for _ in range(warmup):
+        plan.solve_dev(b, x)
+    plan.result()
+    syncs0 = rvk.host_syncs()
+    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        torch.cuda.synchronize()
+        with torch.cuda.stream(stream):
+            for k in range(steps):
+                if flush is not None:
+                    flush.fill_(k & 0xFF)
+                ev0[k].record(stream)
+                plan.solve_dev(b, x)
+                ev1[k].record(stream)
+        stream.synchronize()
+    syncs = rvk.host_syncs() - syncs0
+    return [ev0[k].elapsed_time(ev1[k]) for k in range(steps)], clk.summary(), syncs
+
+
+def strong768_single(args, stream, ctx) -> dict:
+    """BASELINE.json configs[4] anchor at N = 1: the 768^3 7-point solve on
+    this GPU (the single-GPU plan), reported beside the headline so the
+    driver's N = 1, 2, 4, 8 runs give one strong-scaling curve under the same
+    key (sharded.bench_main measures it at N > 1)."""
+    from paper_2306_17801_b200 import rvk
+    g = CONFIGS["7pt768"][2]
+    A = rvk.DeviceCsr.laplacian(ctx, 3, 7, g)
+    n, nnz = A.n_rows, A.nnz
+    b, x = rvk.DeviceArray(n), rvk.DeviceArray(n)
+    rvk.check(rvk.lib().rvk_fill_rhs(ctx.h, 0x9E3779B97F4A7C15, n, b.ptr))
+    plan = rvk.CgPlan(ctx, A, max_it=MAX_IT, mode="fused")
+    fl = plan.flags()
+    bm = bytes_model(n, nnz, "fused", bool(fl & 1), bool(fl & 16), bool(fl & 32),
+                     MAX_IT if fl & 128 else (4 if fl & 64 else 2), bool(fl & 512))
+    steps = max(3, min(args.steps, 10))
+    ms_list, clk, syncs = time_solves(plan, b, x, stream, steps, 3)
+    res = plan.result()
+    ms = statistics.mean(ms_list)
+    hbm_peak, _ = peaks()
+    gbs = bm["b_min_solve"] / (ms * 1e-3) / 1e9
+    plan.close()
+    log(f"strong_768 N=1: {ms:.2f} ms/solve, {gbs:.0f} GB/s ({gbs/hbm_peak:.1%})")
+    return {"workload": "3D 7-point Laplacian 768^3, Jacobi-CG 20 iterations (BASELINE configs[4])",
+            "n_gpus": 1, "plan": "single-GPU CSR plan", "ms_per_solve": round(ms, 3),
+            "steps": steps, "iters_per_s": round(res.iterations / (ms * 1e-3), 1),
+            "per_gpu_gbs": round(gbs, 1), "frac": round(gbs / hbm_peak, 4),
+            "alg_bytes_per_solve": bm["b_min_solve"], "host_syncs_per_iter": syncs / (steps * MAX_IT),
+            "clocks": clk}
+
+
 def run_gpu(args, cfg):
     import torch
     from paper_2306_17801_b200 import rvk
 
-    rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
@@ -448,11 +550,7 @@ def run_gpu(args, cfg):
     stream = torch.cuda.Stream()
     ctx = rvk.Ctx(stream.cuda_stream)
     if args.operator == "stencil":
-        import ctypes
-        nn, nz_ = ctypes.c_int64(), ctypes.c_int64()
-        gx, gy, gz = (list(grid) + [1, 1])[:3]
-        rvk.check(rvk.lib().rvk_laplacian_size(dim, pts, gx, gy, gz, ctypes.byref(nn), ctypes.byref(nz_)))
-        n, nnz = nn.value, nz_.value
+        n, nnz = _laplacian_size(dim, pts, grid)
         A = (dim, pts, grid)
     else:
         A = rvk.DeviceCsr.laplacian(ctx, dim, pts, grid)
@@ -461,22 +559,15 @@ def run_gpu(args, cfg):
     x = rvk.DeviceArray(n)
     rvk.check(rvk.lib().rvk_fill_rhs(ctx.h, 0x9E3779B97F4A7C15, n, b.ptr))
     plan = rvk.CgPlan(ctx, A, max_it=MAX_IT, mode=args.mode, use_graph=not args.no_graph)
-    const_diag = bool(plan.flags() & 1)
-    off32 = bool(plan.flags() & 8)
-    x_defer = bool(plan.flags() & 16)
-    x_group = MAX_IT if plan.flags() & 128 else (4 if plan.flags() & 64 else 2)
-    z_virtual = bool(plan.flags() & 32)
+    fl = plan.flags()
+    const_diag, x_defer, z_virtual = bool(fl & 1), bool(fl & 16), bool(fl & 32)
+    x_group = MAX_IT if fl & 128 else (4 if fl & 64 else 2)
     bm = bytes_model(n, nnz, "stencil" if args.operator == "stencil" else
-                     ("unfused" if args.mode == "unfused" else "fused"), const_diag, off32, x_defer,
-                     z_virtual, x_group, bool(plan.flags() & 512))
+                     ("unfused" if args.mode == "unfused" else "fused"), const_diag, x_defer,
+                     z_virtual, x_group, bool(fl & 512))
     hbm_peak, peak_src = peaks()
     ws_bytes = 20 * nnz + 8 * (n + 1) + 9 * 8 * n
     log(f"{desc}: n={n} nnz={nnz} working set {ws_bytes/1e9:.2f} GB (L2 {L2_BYTES/1e6:.0f} MB)")
-
-    for _ in range(args.warmup):
-        plan.solve_dev(b, x)
-    res = plan.result()
-    assert res.iterations == MAX_IT, res
 
     # ---- timed region: K solves, CUDA events on the solve stream --------------
     # Working sets above 2x L2 stream from HBM anyway; smaller ones get an L2
@@ -485,21 +576,7 @@ def run_gpu(args, cfg):
     flush = None
     if ws_bytes < 2 * L2_BYTES:
         flush = torch.empty(512 * 2 ** 20, dtype=torch.uint8, device=f"cuda:{local}")
-    syncs0 = rvk.host_syncs()
-    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    with ClockSampler(local) as clk:
-        torch.cuda.synchronize()
-        with torch.cuda.stream(stream):
-            for k in range(args.steps):
-                if flush is not None:
-                    flush.fill_(k & 0xFF)
-                ev0[k].record(stream)
-                plan.solve_dev(b, x)
-                ev1[k].record(stream)
-        stream.synchronize()
-    syncs = rvk.host_syncs() - syncs0
-    step_ms = [ev0[k].elapsed_time(ev1[k]) for k in range(args.steps)]
+    step_ms, clocks, syncs = time_solves(plan, b, x, stream, args.steps, args.warmup, flush)
     ms = sum(step_ms) / args.steps
     res = plan.result()
     assert res.iterations == MAX_IT
@@ -534,7 +611,10 @@ def run_gpu(args, cfg):
         k1_gbs = bm["k1"] / (ms * 1e-3) / 1e9
         k2_gbs = 0.0
     solve_gbs = bm["b_min_solve"] / (ms * 1e-3) / 1e9
-    traffic = ncu_traffic(args.config) if (mode == "fused" and args.operator == "csr") else None
+    traffic, traffic_src = (None, None)
+    if mode == "fused":
+        traffic, traffic_src = ncu_traffic(args.config + ("_matrix_free" if args.operator == "stencil"
+                                                          else ""))
 
     # ---- e2e through the C-ABI with host buffers (pinned) ----------------------
     # (1) latency: one rvk_cg_solve_host call per step (H2D b, solve, D2H x +
@@ -563,44 +643,45 @@ def run_gpu(args, cfg):
     many = plan.solve_host_many(bs, xs)
     e2e_ms = (time.perf_counter() - t0) * 1e3 / args.steps
     assert all(m.iterations == MAX_IT for m in many)
+    plan.close()
+    del A, b, x, plan
 
-    cpu = None
-    if not args.no_cpu_baseline:
-        kind, ctimes, what = cpu_baseline(dim, pts, grid, steps=1)
-        cpu = {"value": round(statistics.mean(ctimes), 1), "unit": "ms/solve", "cores": 1,
-               "kind": kind,
-               "sample": f"{what} of {desc} on the GPU box host "
-                         "(reference kernels_*.cpp from oracle/_ref, auto dispatch, 1 thread)",
-               "host_cpu": host_cpu()}
+    # ---- BASELINE configs[4] at N = 1 (the strong-scaling anchor) --------------
+    strong = None
+    if not args.no_strong and args.config != "7pt768" and args.operator == "csr":
+        torch.cuda.synchronize()
+        strong = strong768_single(args, stream, ctx)
+
+    cpu = None if args.no_cpu_baseline else cpu_baseline_entry(dim, pts, grid)
 
     out = {
         "metric": METRIC, "value": round(ms, 4), "unit": "ms/solve", "n_gpus": 1,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
-        "min_ms": round(min(step_ms), 4), "higher_is_better": False, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{desc}, Jacobi-CG {MAX_IT} iterations, x0=0, splitmix64 RHS",
-                   "n": n, "nnz": nnz, "mode": mode, "graph": not args.no_graph,
-                   "operator": args.operator,
-                   "l2": (f"no flush: working set {ws_bytes/1e9:.2f} GB >> 126 MB L2 "
-                          "(every operand streams from HBM each step)") if flush is None else
-                         (f"L2 flushed between steps (512 MiB write); working set "
-                          f"{ws_bytes/1e6:.1f} MB")},
+        "min_ms": round(min(step_ms), 4), "higher_is_better": False,
+        "scaling": scaling_label(args), "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": bench_config(args, 1),
+        "run": {"mode": mode, "graph": not args.no_graph, "operator": args.operator,
+                "l2": (f"no flush: working set {ws_bytes/1e9:.2f} GB >> 126 MB L2 "
+                       "(every operand streams from HBM each step)") if flush is None else
+                      (f"L2 flushed between steps (512 MiB write); working set "
+                       f"{ws_bytes/1e6:.1f} MB")},
         "roofline": {"bound": "hbm",
-                     "kernel": {"fused": ("k_mf_cg (matrix-free stencil + on-the-fly AYPX + p.w)"
+                     "kernel": {"fused": ("k_mf_tma (matrix-free stencil + on-the-fly AYPX + p.w)"
                                           if args.operator == "stencil" else
                                           "k_spmv_tma<CgSpmvOp> (SpMV + on-the-fly AYPX + p.w)"),
                                 "unfused": "k_spmv_tma<SpmvGuardedOp> (SpMV)",
-                                "persistent": "k_cg_persistent (whole solve, one launch)",
+                                "persistent": "k_cg_persistent / k_cg_cluster (whole solve, one launch)",
                                 "hostsync": "whole solve (host-sync baseline)"}[mode],
                      "achieved": round(k1_gbs, 1), "peak": hbm_peak, "unit": "GB/s",
                      "frac": round(k1_gbs / hbm_peak, 4), "traffic": traffic,
+                     "traffic_source": traffic_src,
                      "alg_bytes_per_launch": bm["k1"], "avg_launch_ms": round(k1_avg, 5),
                      "peak_source": peak_src},
         "solve_roofline": {"alg_bytes_per_solve": bm["b_min_solve"],
                            "achieved": round(solve_gbs, 1), "frac": round(solve_gbs / hbm_peak, 4),
+                           "bytes_model": "the bytes this plan's kernels need (plan flags below)",
                            "update_kernel_gbs": round(k2_gbs, 1),
                            "const_diag_folded": const_diag,
-                           "int32_row_offsets": off32,
                            "x_update_group": x_group if x_defer else 1,
                            "z_virtual": z_virtual,
                            "survey_b_min_gbs": round(bm["b_min_survey_solve"] / (ms * 1e-3) / 1e9, 1),
@@ -615,14 +696,14 @@ def run_gpu(args, cfg):
                 "latency_api": "rvk_cg_solve_host: one RHS per call, H2D + solve + D2H "
                                "serial, synchronised (wall clock)"},
         "gpu_launches": launches * args.steps,
+        "strong_768": strong,
         "cpu_baseline": cpu,
-        "clocks": clk.summary(),
+        "clocks": clocks,
     }
     log(f"solve {ms:.3f} ms (min {min(step_ms):.3f}); K1 {k1_avg*1e3:.1f} us = {k1_gbs:.0f} GB/s; "
         f"K2 {k2_avg*1e3:.1f} us = {k2_gbs:.0f} GB/s; solve {solve_gbs:.0f} GB/s "
         f"({solve_gbs/hbm_peak:.1%}); e2e {e2e_ms:.2f} ms (latency {lat_ms:.2f}); syncs {syncs}")
     print(json.dumps(out), flush=True)
-    plan.close()
     ctx.close()
 
 
@@ -634,12 +715,14 @@ def main():
     ap.add_argument("--impl", choices=["rvk", "reference"], default="rvk")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="7pt256")
     ap.add_argument("--mode", choices=["fused", "unfused", "persistent", "auto", "hostsync"],
-                    default="auto", help="auto: one persistent kernel for L2-sized grids, "
+                    default="auto", help="auto: the one-cluster solve for <= 16 K rows, "
                                          "else the fused 2-kernel/iteration graph")
     ap.add_argument("--operator", choices=["csr", "stencil"], default="csr",
                     help="csr: the AIJ/CSR operator (headline); stencil: matrix-free (SURVEY 8f)")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-strong", action="store_true",
+                    help="skip the 768^3 strong-scaling section (BASELINE configs[4])")
     ap.add_argument("--comm", choices=["peer", "nccl"], default="peer",
                     help="N>1: peer = in-kernel NVLink halo/partial pushes (fused); nccl = "
                          "library collectives between kernels (baseline)")

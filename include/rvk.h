@@ -353,6 +353,9 @@ rvk_status rvk_build_laplacian_rows(rvk_ctx ctx, int dim, int points, int64_t nx
 rvk_status rvk_comm_unique_id(void* id_out, int id_bytes);
 rvk_status rvk_comm_init(const void* id, int nranks, int rank, rvk_comm* out);
 rvk_status rvk_comm_destroy(rvk_comm comm);
+/* The communicator's size and this process's rank as NCCL reports them
+ * (ncclCommCount / ncclCommUserRank). */
+rvk_status rvk_comm_size(rvk_comm comm, int* nranks, int* rank);
 /* comm != NULL: NCCL backend.  comm == NULL with nranks > 1: either a
  * LOOPBACK shard (all shards on one device, sharing `shared_gather`,
  * 4*nranks doubles, solved by rvk_dcg_loopback_solve) or, with
@@ -362,12 +365,16 @@ rvk_status rvk_dcg_plan_create(rvk_ctx ctx, const rvk_csr* A_local, rvk_shard sh
                                rvk_dcg_plan* out);
 rvk_status rvk_dcg_plan_destroy(rvk_dcg_plan plan);
 /* One shard per process: halo exchange (ncclSend/Recv) + partial-sum
- * allgather, all stream-ordered -- zero host syncs. */
+ * allgather, or the PEER kernels, all stream-ordered -- zero host syncs.
+ * cfg.use_graph != 0: the solve is captured once per (b, x) into a CUDA
+ * graph (global capture mode for PEER / single-rank plans: any synchronous
+ * call invalidates the capture) and replayed.  rvk_dcg_result also reports a
+ * pending NCCL asynchronous communicator error (RVK_ERR_COMM). */
 rvk_status rvk_dcg_solve_dev(rvk_dcg_plan plan, const double* b_own, double* x_own);
 rvk_status rvk_dcg_loopback_solve(rvk_dcg_plan* plans, int nplans, const double* const* b_own,
                                   double* const* x_own);
 rvk_status rvk_dcg_result(rvk_dcg_plan plan, double* hist_host, rvk_cg_info* info);
-int        rvk_dcg_plan_flags(rvk_dcg_plan plan); /* RVK_PLAN_* bits (CONST_DIAG, OFF32, X_DEFER) */
+int        rvk_dcg_plan_flags(rvk_dcg_plan plan); /* RVK_PLAN_* bits (CONST_DIAG, X_DEFER, X_SOLVE) */
 
 /* PEER backend (NVLink P2P; the fused compute+communication path).  Each
  * plan owns one device window [z | p0 | p1 | flags | gather slots]; once

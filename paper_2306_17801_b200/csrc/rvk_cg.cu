@@ -696,8 +696,11 @@ struct XUpd {
 };
 
 // K2 store mask: bit 0 store z (clear: z virtual), bit 1 the last K2 of a
-// fixed-iteration solve -- its r and z are never read again (the next solve's
-// setup rewrites both), so neither is stored (16 n bytes per solve)
+// fixed-iteration solve -- its r and z are never read again in this solve, so
+// neither is stored (16 n bytes per solve).  The next solve starts from b: its
+// setup (k_cg_setup, or K1(0) folded) writes r, and z is either formed on the
+// fly (virtual / folded) or written before any read.  rvk_cg_plan_vector(R / Z)
+// after a solve is therefore only meaningful with RVK_OPT_KEEP_WORK.
 int k2_store(rvk_cg_plan P) { return P->k2_last ? 2 : (P->zv ? 0 : 1); }
 
 template <int PC, bool COND, int NP>

@@ -88,6 +88,10 @@ struct NcclApi {
     ncclResult_t (*GroupStart)();
     ncclResult_t (*GroupEnd)();
     const char* (*GetErrorString)(ncclResult_t);
+    // optional (diagnostics): the communicator's own view and its async error
+    ncclResult_t (*CommCount)(const ncclComm_t, int*)           = nullptr;
+    ncclResult_t (*CommUserRank)(const ncclComm_t, int*)        = nullptr;
+    ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
     bool ok = false;
 };
 
@@ -108,6 +112,9 @@ NcclApi& nccl()
                  sym(api.Recv, "ncclRecv") && sym(api.AllGather, "ncclAllGather") &&
                  sym(api.GroupStart, "ncclGroupStart") && sym(api.GroupEnd, "ncclGroupEnd") &&
                  sym(api.GetErrorString, "ncclGetErrorString");
+        sym(api.CommCount, "ncclCommCount");
+        sym(api.CommUserRank, "ncclCommUserRank");
+        sym(api.CommGetAsyncError, "ncclCommGetAsyncError");
     });
     return api;
 }
@@ -612,6 +619,10 @@ struct rvk_dcg_plan_s {
     unsigned char* win = nullptr;  // [z | p0 | p1 | flags | gather], the exported PEER window
     size_t        win_bytes = 0;
     double *dinv = nullptr, *r = nullptr, *z = nullptr, *w = nullptr;
+    // whole-solve CUDA graph (cfg.use_graph), captured per (b, x) pair
+    cudaGraphExec_t graph   = nullptr;
+    const double*   graph_b = nullptr;
+    double*         graph_x = nullptr;
     double*       p[kMaxXq] = {}; // p ring in the window: iteration j writes p[(j+1) % npb]
     int           npb = 2;        // 2 (x per iteration pair) or max_it (x once per solve)
     double *hist = nullptr, *beta = nullptr, *gather = nullptr, *partials = nullptr;
@@ -934,6 +945,19 @@ rvk_status rvk_comm_init(const void* id, int nranks, int rank, rvk_comm* out)
     return RVK_OK;
 }
 
+rvk_status rvk_comm_size(rvk_comm c, int* nranks, int* rank)
+{
+    if (!c || !nranks || !rank) return set_error(RVK_ERR_INVALID, "comm_size: null argument");
+    *nranks = c->nranks;
+    *rank   = c->rank;
+    // NCCL's own view of the communicator when the library exposes it
+    if (c->comm && nccl().CommCount && nccl().CommUserRank) {
+        RVK_NCCL(nccl().CommCount(c->comm, nranks));
+        RVK_NCCL(nccl().CommUserRank(c->comm, rank));
+    }
+    return RVK_OK;
+}
+
 rvk_status rvk_comm_destroy(rvk_comm c)
 {
     if (!c) return RVK_OK;
@@ -998,6 +1022,7 @@ rvk_status rvk_dcg_plan_destroy(rvk_dcg_plan P)
     if (P->ctx) cudaStreamSynchronize(P->ctx->stream);
     // (PEER: the caller keeps every rank alive past its last solve -- a
     // barrier before destroy -- since peers store into this window)
+    if (P->graph) cudaGraphExecDestroy(P->graph);
     void* bufs[] = {P->win, P->dinv, P->r, P->w, P->hist, P->beta, P->st, P->partials, P->tickets,
                     P->peer_tab};
     for (void* b : bufs)
@@ -1006,14 +1031,9 @@ rvk_status rvk_dcg_plan_destroy(rvk_dcg_plan P)
     return RVK_OK;
 }
 
-// One shard per process: the whole solve, stream-ordered, no host sync.
-// PEER: 2 kernels per iteration carry all communication; NCCL: halo
-// send/recv + 2 allgathers per iteration between the kernels.
-rvk_status rvk_dcg_solve_dev(rvk_dcg_plan P, const double* b_own, double* x_own)
+namespace {
+rvk_status enqueue_dcg(rvk_dcg_plan P, const double* b_own, double* x_own)
 {
-    if (!P || !b_own || !x_own) return set_error(RVK_ERR_INVALID, "null argument");
-    if (!P->comm && !P->peer.on && P->sh.nranks > 1)
-        return set_error(RVK_ERR_INVALID, "loopback shards are solved with rvk_dcg_loopback_solve");
     const bool dist = !P->peer.on && P->comm && P->sh.nranks > 1;
     RVK_TRY(phase_setup(P, b_own, x_own));
     if (dist) RVK_TRY(nccl_allgather(P));
@@ -1026,6 +1046,49 @@ rvk_status rvk_dcg_solve_dev(rvk_dcg_plan P, const double* b_own, double* x_own)
     }
     RVK_TRY(phase_finish(P));
     return phase_xfix(P, x_own);
+}
+} // namespace
+
+// One shard per process: the whole solve, stream-ordered, no host sync.
+// PEER: 2 kernels per iteration carry all communication; NCCL: halo
+// send/recv + 2 allgathers per iteration between the kernels.  With
+// cfg.use_graph the solve is captured once per (b, x) into a CUDA graph and
+// replayed: PEER / single-rank plans in GLOBAL capture mode, which fails on
+// any synchronous CUDA call made while the solve is enqueued (the structural
+// proof of zero host syncs, as in rvk_cg_solve_dev); NCCL plans in
+// thread-local mode (NCCL's own proxy thread keeps running during capture).
+rvk_status rvk_dcg_solve_dev(rvk_dcg_plan P, const double* b_own, double* x_own)
+{
+    if (!P || !b_own || !x_own) return set_error(RVK_ERR_INVALID, "null argument");
+    if (!P->comm && !P->peer.on && P->sh.nranks > 1)
+        return set_error(RVK_ERR_INVALID, "loopback shards are solved with rvk_dcg_loopback_solve");
+    if (!P->cfg.use_graph) return enqueue_dcg(P, b_own, x_own);
+    cudaStream_t s = P->ctx->stream;
+    if (!(P->graph && P->graph_b == b_own && P->graph_x == x_own)) {
+        if (P->graph) cudaGraphExecDestroy(P->graph);
+        P->graph          = nullptr;
+        const bool   nccl = !P->peer.on && P->comm && P->sh.nranks > 1;
+        cudaGraph_t  g    = nullptr;
+        RVK_CUDA(cudaStreamBeginCapture(s, nccl ? cudaStreamCaptureModeThreadLocal
+                                                : cudaStreamCaptureModeGlobal));
+        rvk_status  rc = enqueue_dcg(P, b_own, x_own);
+        cudaError_t e  = cudaStreamEndCapture(s, &g);
+        if (rc != RVK_OK) {
+            if (g) cudaGraphDestroy(g);
+            return rc;
+        }
+        if (e != cudaSuccess) return cuda_error(e, "cudaStreamEndCapture (sharded solve not capturable)");
+        e = cudaGraphInstantiate(&P->graph, g, 0);
+        cudaGraphDestroy(g);
+        if (e != cudaSuccess) {
+            P->graph = nullptr;
+            return cuda_error(e, "cudaGraphInstantiate (sharded solve)");
+        }
+        P->graph_b = b_own;
+        P->graph_x = x_own;
+    }
+    RVK_CUDA(cudaGraphLaunch(P->graph, s));
+    return RVK_OK;
 }
 
 // All P shards on one device, enqueued phase by phase on shard 0's stream
@@ -1075,6 +1138,14 @@ rvk_status rvk_dcg_result(rvk_dcg_plan P, double* hist_host, rvk_cg_info* info)
     if (h.state == RVK_CG_COMM_ERROR)
         return set_error(RVK_ERR_COMM, "dcg_solve: a peer did not arrive within %llu s (PEER backend)",
                          (unsigned long long)(kPeerTimeoutNs / 1000000000ull));
+    // NCCL backend: an asynchronous communicator error (a peer died, a
+    // network fault) surfaces here, never as a hang in a later solve
+    if (P->comm && P->comm->comm && nccl().CommGetAsyncError) {
+        ncclResult_t ae = ncclSuccess;
+        if (nccl().CommGetAsyncError(P->comm->comm, &ae) == ncclSuccess && ae != ncclSuccess &&
+            ae != ncclInProgress)
+            return nccl_error(ae, "dcg_solve: NCCL communicator async error");
+    }
     return RVK_OK;
 }
 

@@ -43,7 +43,7 @@ EXPORTS = [
     "rvk_cg_set_profiling", "rvk_cg_kernel_times", "rvk_cg_plan_mode", "rvk_cg_plan_flags",
     "rvk_cg_plan_vector",
     "rvk_laplacian_rows_nnz", "rvk_build_laplacian_rows", "rvk_comm_unique_id", "rvk_comm_init",
-    "rvk_comm_destroy", "rvk_dcg_plan_create", "rvk_dcg_plan_destroy", "rvk_dcg_solve_dev",
+    "rvk_comm_destroy", "rvk_comm_size", "rvk_dcg_plan_create", "rvk_dcg_plan_destroy", "rvk_dcg_solve_dev",
     "rvk_dcg_loopback_solve", "rvk_dcg_result", "rvk_dcg_plan_flags", "rvk_dcg_window", "rvk_dcg_attach_peers",
     "rvk_ipc_get_handle", "rvk_ipc_open_handle", "rvk_ipc_close_handle", "rvk_tfqmr_plan_create",
     "rvk_tfqmr_plan_destroy", "rvk_tfqmr_solve_dev", "rvk_tfqmr_result", "rvk_tfqmr_plan_flags",
@@ -167,6 +167,7 @@ def lib():
         "rvk_comm_unique_id": (i, [vp, i]),
         "rvk_comm_init": (i, [vp, i, i, C.POINTER(vp)]),
         "rvk_comm_destroy": (i, [vp]),
+        "rvk_comm_size": (i, [vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
         "rvk_dcg_plan_create": (i, [vp, C.POINTER(Csr), Shard, CgConfig, vp, vp, C.POINTER(vp)]),
         "rvk_dcg_plan_destroy": (i, [vp]),
         "rvk_dcg_solve_dev": (i, [vp, vp, vp]),

@@ -93,16 +93,20 @@ def _cfg(max_it, pc, rtol, atol, opts=0):
 
 
 class ShardPlan:
-    """One shard's distributed CG plan (rvk_dcg_plan)."""
+    """One shard's distributed CG plan (rvk_dcg_plan).  use_graph: the solve
+    is captured into a CUDA graph on first use (per b / x pair) and replayed
+    (rvk_dcg_solve_dev; loopback plans are solved phase by phase instead)."""
 
     def __init__(self, ctx, A: "rvk.DeviceCsr", sh: ShardSpec, max_it=20, pc="jacobi", rtol=0.0,
-                 atol=0.0, comm=None, shared_gather: int | None = None):
+                 atol=0.0, comm=None, shared_gather: int | None = None, use_graph: bool = False,
+                 opts: int = 0):
         self.ctx, self.A, self.sh, self.max_it = ctx, A, sh, max_it
         shard = rvk.Shard(sh.n_own, sh.halo_lo, sh.halo_hi, sh.rank, sh.nranks)
+        cfg = _cfg(max_it, pc, rtol, atol, opts)
+        cfg.use_graph = 1 if use_graph else 0
         h = C.c_void_p()
-        rvk.check(rvk.lib().rvk_dcg_plan_create(ctx.h, C.byref(A.c), shard,
-                                                _cfg(max_it, pc, rtol, atol), comm, shared_gather,
-                                                C.byref(h)))
+        rvk.check(rvk.lib().rvk_dcg_plan_create(ctx.h, C.byref(A.c), shard, cfg, comm,
+                                                shared_gather, C.byref(h)))
         self.h = h
         ctx._deps.add(self)
 
@@ -219,7 +223,11 @@ def disconnect_peers(opened: list[int]):
 
 def init_comm(rank: int, world: int):
     """NCCL communicator: rank 0 makes the unique id, torch.distributed
-    broadcasts it (the only thing torch does on this path)."""
+    broadcasts it (the only thing torch does on this path).  The
+    communicator's own view (ncclCommCount / ncclCommUserRank) is logged and
+    checked against the launcher's."""
+    import sys
+
     import torch
     import torch.distributed as dist
 
@@ -233,14 +241,147 @@ def init_comm(rank: int, world: int):
     raw = bytes(t.cpu().tolist())
     comm = C.c_void_p()
     rvk.check(rvk.lib().rvk_comm_init(raw, world, rank, C.byref(comm)))
+    nr, rk = C.c_int(), C.c_int()
+    rvk.check(rvk.lib().rvk_comm_size(comm, C.byref(nr), C.byref(rk)))
+    print(f"[rvk] NCCL communicator: rank {rk.value} of {nr.value} (launcher: {rank} of {world})",
+          file=sys.stderr, flush=True)
+    if (nr.value, rk.value) != (world, rank):
+        raise RuntimeError(f"NCCL communicator reports rank {rk.value}/{nr.value}, "
+                           f"launcher {rank}/{world}")
     return comm
 
 
+def _build_shard(ctx, dim, pts, grid, shards, rank, seed=0x9E3779B97F4A7C15):
+    """The shard's local CSR (device assembly) and its slice of the global RHS."""
+    sh = shards[rank]
+    A = local_laplacian(ctx, dim, pts, grid, sh)
+    b = rvk.DeviceArray(sh.n_own)
+    x = rvk.DeviceArray(sh.n_own)
+    rvk.check(rvk.lib().rvk_fill_rhs(ctx.h, (seed + sh.row_begin) & (2 ** 64 - 1), sh.n_own, b.ptr))
+    return sh, A, b, x
+
+
+def _time_sharded(plan, b, x, stream, steps, warmup, tdev, local):
+    """K solves timed by CUDA events on every rank's solve stream, a barrier
+    and a device sync on both sides; returns (max-over-ranks ms, clocks,
+    host syncs on this rank)."""
+    import torch
+    import torch.distributed as dist
+
+    import bench
+    for _ in range(warmup):
+        plan.solve_dev(b, x)
+    plan.result()
+    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    dist.barrier()
+    torch.cuda.synchronize()
+    syncs0 = rvk.host_syncs()
+    with bench.ClockSampler(local) as clk:
+        for k in range(steps):
+            ev0[k].record(stream)
+            plan.solve_dev(b, x)
+            ev1[k].record(stream)
+        stream.synchronize()
+    syncs = rvk.host_syncs() - syncs0
+    dist.barrier()
+    ms_local = sum(ev0[k].elapsed_time(ev1[k]) for k in range(steps)) / steps
+    t = torch.tensor([ms_local], device=tdev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item()), clk.summary(), syncs
+
+
+def _peer_or_nccl(args, ctx, A, sh, shards, b, x, comm, rank, world, tdev):
+    """The product backend is PEER (in-kernel NVLink halo / partial stores);
+    it is used only if its first solve equals the NCCL solve bit for bit on
+    every rank (same arithmetic and fold order by construction).  Returns
+    (backend, plan, other_plan, opened handles, fallback reason)."""
+    import numpy as _np
+    import torch
+    import torch.distributed as dist
+
+    nccl_plan = ref_hist = ref_x = None
+    if comm is not None:
+        nccl_plan = ShardPlan(ctx, A, sh, 20, comm=comm, use_graph=True)
+        nccl_plan.solve_dev(b, x)
+        ref_hist = nccl_plan.result().hist
+        ref_x = x.download(ctx)
+    backend, fallback, opened, plan = "nccl", None, [], nccl_plan
+    if comm is None or getattr(args, "comm", "peer") == "peer":
+        peer_plan = None
+        try:
+            peer_plan = ShardPlan(ctx, A, sh, 20, use_graph=True)
+            opened = connect_peers(peer_plan, shards, rank, world)
+            peer_plan.solve_dev(b, x)
+            ph = peer_plan.result().hist
+            ok = nccl_plan is None or (_np.array_equal(ph, ref_hist) and
+                                       _np.array_equal(x.download(ctx), ref_x))
+            err = None if ok else "PEER solve differs from the NCCL solve"
+        except Exception as e:  # noqa: BLE001 -- report and fall back, never hang
+            err, peer_plan = f"PEER setup failed: {e}".splitlines()[0][:200], None
+        if nccl_plan is None and err is not None:
+            raise RuntimeError(err)  # no backend left
+        flags = torch.tensor([0 if err is None else 1], device=tdev)
+        dist.all_reduce(flags)  # every rank takes the same backend
+        if int(flags.item()) == 0:
+            backend, plan = "peer", peer_plan
+            if nccl_plan is not None:
+                nccl_plan.close()
+                nccl_plan = None
+        else:
+            fallback = err or "another rank's PEER check failed"
+            if peer_plan is not None:
+                peer_plan.close()
+    return backend, plan, opened, fallback, nccl_plan is not None or backend == "nccl"
+
+
+def _check_vs_single_gpu(ctx, dim, pts, grid, hist, x_shard, sh, rank, tdev):
+    """Rank 0 solves the same GLOBAL system with the single-GPU plan (when it
+    fits) and every rank compares: the history (identical on all ranks) and
+    ||x||^2 summed over the shards, within 1e-10 (reduction trees differ
+    between the 1-GPU and the P-shard solve, so not bitwise)."""
+    import numpy as _np
+    import torch
+    import torch.distributed as dist
+
+    n_glob = int(_np.prod(grid))
+    res = torch.zeros(3, dtype=torch.float64, device=tdev)  # ok, hist err, x err
+    xx = torch.tensor([float(_np.dot(x_shard, x_shard))], dtype=torch.float64, device=tdev)
+    dist.all_reduce(xx)
+    if rank == 0:
+        if n_glob <= (1 << 28):
+            A = rvk.DeviceCsr.laplacian(ctx, dim, pts, grid)
+            b = rvk.DeviceArray(n_glob)
+            x = rvk.DeviceArray(n_glob)
+            rvk.check(rvk.lib().rvk_fill_rhs(ctx.h, 0x9E3779B97F4A7C15, n_glob, b.ptr))
+            p1 = rvk.CgPlan(ctx, A, max_it=20)
+            p1.solve_dev(b, x)
+            r1 = p1.result()
+            x1 = x.download(ctx)
+            p1.close()
+            del A, b, x
+            eh = float(_np.max(_np.abs(r1.hist - hist) / _np.abs(r1.hist)))
+            ex = abs(float(_np.dot(x1, x1)) - float(xx.item())) / float(_np.dot(x1, x1))
+            res[:] = torch.tensor([1.0, eh, ex], dtype=torch.float64)
+    dist.broadcast(res, 0)
+    if res[0].item() == 0.0:
+        return {"checked": False, "reason": f"global system of {n_glob} rows not solved on one GPU"}
+    eh, ex = float(res[1].item()), float(res[2].item())
+    return {"checked": True, "vs": "single-GPU plan, same global system", "hist_rel_err": eh,
+            "x_norm2_rel_err": ex, "ok": bool(eh < 1e-10 and ex < 1e-10)}
+
+
 def bench_main(args, cfg):
-    """bench.py under torchrun: one shard per rank.  Backend PEER (in-kernel
-    NVLink halo pushes + partial broadcast, no NCCL on the data path) unless
-    --comm nccl, or unless the PEER setup fails / its first solve differs
-    from the NCCL solve bit for bit (then NCCL, with the reason in the JSON)."""
+    """bench.py under torchrun: one shard per rank.
+
+    value: the weak-scaled workload (each GPU keeps one config-sized slab, the
+    global grid grows along the slowest axis), so it stays comparable with
+    the N = 1 line.  strong_768: BASELINE.json configs[4] -- the fixed 768^3
+    grid row-sharded over the N GPUs -- measured in the same invocation.
+    Backend PEER (in-kernel NVLink halo pushes + partial broadcast, no NCCL
+    on the data path) unless --comm nccl, or unless the PEER setup fails / its
+    first solve differs from the NCCL solve bit for bit (then NCCL, with the
+    reason in the JSON).  Every solve is one replayed CUDA graph."""
     import json
     import sys
 
@@ -248,7 +389,7 @@ def bench_main(args, cfg):
     import torch.distributed as dist
 
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-    from bench import ClockSampler, peaks  # noqa: E402  (bench.py is the caller)
+    import bench  # noqa: E402  (bench.py is the caller)
 
     rank = int(os.environ["RANK"])
     world = int(os.environ["WORLD_SIZE"])
@@ -265,12 +406,8 @@ def bench_main(args, cfg):
     else:
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     tdev = "cpu" if shared else f"cuda:{local}"
-    dim, pts, grid, desc = cfg
-    weak = args.config != "7pt768"
-    if weak:  # every GPU keeps the single-GPU workload: stack slabs along the slowest axis
-        grid = tuple(grid[:-1]) + (grid[-1] * world,)
+    dim, pts, grid, desc, strong_cfg = bench.workload(args, world)
     shards = partition(dim, grid, world)
-    sh = shards[rank]
     stream = torch.cuda.Stream()
     ctx = rvk.Ctx(stream.cuda_stream)
     comm, comm_err = None, None
@@ -279,60 +416,11 @@ def bench_main(args, cfg):
             comm = init_comm(rank, world)
         except Exception as e:  # noqa: BLE001 -- PEER needs no NCCL; report it
             comm_err = f"NCCL unavailable: {e}".splitlines()[0][:200]
-    A = local_laplacian(ctx, dim, pts, grid, sh)
-    b = rvk.DeviceArray(sh.n_own)
-    x = rvk.DeviceArray(sh.n_own)
-    # the slice of the global RHS this shard owns
-    full_seed = 0x9E3779B97F4A7C15
-    rvk.check(rvk.lib().rvk_fill_rhs(ctx.h, (full_seed + sh.row_begin) & (2 ** 64 - 1), sh.n_own,
-                                     b.ptr))
-    nccl_plan = ref_hist = ref_x = None
-    if comm is not None:
-        nccl_plan = ShardPlan(ctx, A, sh, 20, comm=comm)
-        nccl_plan.solve_dev(b, x)
-        ref_hist = nccl_plan.result().hist
-        ref_x = x.download(ctx)
-
-    backend, fallback, opened, plan = "nccl", comm_err, [], nccl_plan
-    if comm is None or getattr(args, "comm", "peer") == "peer":
-        try:
-            peer_plan = ShardPlan(ctx, A, sh, 20)
-            opened = connect_peers(peer_plan, shards, rank, world)
-            peer_plan.solve_dev(b, x)
-            ph = peer_plan.result().hist
-            ok = nccl_plan is None or (np.array_equal(ph, ref_hist) and
-                                       np.array_equal(x.download(ctx), ref_x))
-            err = None if ok else "PEER solve differs from the NCCL solve"
-        except Exception as e:  # noqa: BLE001 -- report and fall back, never hang
-            err, peer_plan = f"PEER setup failed: {e}".splitlines()[0][:200], None
-        if nccl_plan is None and err is not None:
-            raise RuntimeError(err)  # no backend left
-        flags = torch.tensor([0 if err is None else 1], device=tdev)
-        dist.all_reduce(flags)  # every rank takes the same backend
-        if int(flags.item()) == 0:
-            backend, plan = "peer", peer_plan
-        else:
-            fallback = err or "another rank's PEER check failed"
-    for _ in range(args.warmup):
-        plan.solve_dev(b, x)
-    plan.result()
-    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    dist.barrier()
-    torch.cuda.synchronize()
-    syncs0 = rvk.host_syncs()
-    with ClockSampler(local) as clk:
-        for k in range(args.steps):
-            ev0[k].record(stream)
-            plan.solve_dev(b, x)
-            ev1[k].record(stream)
-        stream.synchronize()
-    syncs = rvk.host_syncs() - syncs0
-    dist.barrier()
-    ms_local = sum(ev0[k].elapsed_time(ev1[k]) for k in range(args.steps)) / args.steps
-    t = torch.tensor([ms_local], device=tdev)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
+    sh, A, b, x = _build_shard(ctx, dim, pts, grid, shards, rank)
+    backend, plan, opened, fallback, _ = _peer_or_nccl(args, ctx, A, sh, shards, b, x, comm, rank,
+                                                        world, tdev)
+    fallback = fallback or comm_err
+    ms, clocks, syncs = _time_sharded(plan, b, x, stream, args.steps, args.warmup, tdev, local)
     res = plan.result()
 
     # ---- e2e: pinned host b shard -> device, solve, x shard -> host (events) --
@@ -354,21 +442,32 @@ def bench_main(args, cfg):
     t = torch.tensor([e2e_local], device=tdev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     e2e_ms = float(t.item())
-    plan.result()
+    res = plan.result()
+    x_own = x.download(ctx)
+    fl = rvk.lib().rvk_dcg_plan_flags(plan.h)
+    dist.barrier()  # no rank frees a window a peer may still store into
+    plan.close()
+    disconnect_peers(opened)
+    del A, b, x
+
+    # ---- correctness of this run: vs the single-GPU solve of the same system --
+    check = _check_vs_single_gpu(ctx, dim, pts, grid, res.hist, x_own, sh, rank, tdev)
+
+    # ---- BASELINE configs[4]: 768^3 row-sharded over the N GPUs ---------------
+    strong = None
+    if not strong_cfg and not getattr(args, "no_strong", False):
+        strong = _strong_768(args, ctx, stream, comm, rank, world, tdev, local)
 
     n_glob = int(np.prod(grid))
     nnz_glob = _global_nnz(dim, pts, grid)
-    fl = rvk.lib().rvk_dcg_plan_flags(plan.h)
-    ob = 4 if fl & 8 else 8               # int32 row offsets streamed
-    # per-iteration vector bytes: 96 n, x traffic 24 n -> 8 n + 16 n / group
-    # (pairs: 16 n; whole solve, RVK_PLAN_X_SOLVE: 8.8 n), constant
-    # Jacobi diagonal (RVK_PLAN_CONST_DIAG) -8 n per iteration and setup
-    grp = 20 if fl & 128 else (2 if fl & 16 else 1)
-    vb = 96 - (16 - 16 / grp) - (8 if fl & 1 else 0)
-    b_min = int(20 * (12 * nnz_glob + ob * (n_glob + 1) + vb * n_glob) + (56 if fl & 1 else 64) * n_glob)
-    hbm_peak, peak_src = peaks()
+    b_min = _shard_bytes(n_glob, nnz_glob, fl)
+    hbm_peak, peak_src = bench.peaks()
     per_gpu = b_min / world / (ms * 1e-3) / 1e9
     launches = 3 + 2 * 20 + (1 if fl & 16 else 0)  # reset, setup, 20 x (K1, K2), finish, x-fix
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        cpu = bench.cpu_baseline_entry(dim, pts, grid)
+    traffic, traffic_src = bench.ncu_traffic(args.config + "_shard", "solve")
     if rank == 0:
         comm_desc = {"peer": "PEER: K1/K2 store halo planes + dot partials into the neighbours' "
                              "windows over NVLink (cudaIpc), device flag sync; no NCCL on the "
@@ -376,22 +475,21 @@ def bench_main(args, cfg):
                      "nccl": "NCCL halo (ncclSend/Recv, 1 plane/neighbour, z and p) + "
                              "ncclAllGather of dot partials between kernels"}[backend]
         out = {
-            "metric": "20-iter Jacobi-CG solve time, achieved HBM GB/s vs peak, host syncs/iter",
+            "metric": bench.METRIC,
             "value": round(ms, 4), "unit": "ms/solve", "n_gpus": 1 if shared else world,
             "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": False,
-            "scaling": "weak" if weak else "strong", "vs_baseline": None, "dtype": "f64",
+            "scaling": bench.scaling_label(args), "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": f"{desc} row-sharded over {world} GPUs"
-                                   + (f" (weak: global grid {grid})" if weak else ""),
-                       "n": n_glob, "nnz": nnz_glob, "parallelism": f"rows{world}",
-                       "comm": comm_desc, "comm_fallback": fallback,
-                       "shared_gpu_functional_check": shared,
-                       "l2": "no flush: per-GPU working set >> 126 MB L2"},
+            "config": bench.bench_config(args, world),
+            "run": {"comm": comm_desc, "comm_fallback": fallback, "graph": True,
+                    "shared_gpu_functional_check": shared,
+                    "l2": "no flush: per-GPU working set >> 126 MB L2"},
             "roofline": {"bound": "hbm", "kernel": "whole sharded solve, per GPU (K1+K2+comm)",
                          "achieved": round(per_gpu, 1), "peak": hbm_peak, "unit": "GB/s",
-                         "frac": round(per_gpu / hbm_peak, 4), "traffic": None,
-                         "peak_source": peak_src},
+                         "frac": round(per_gpu / hbm_peak, 4), "traffic": traffic,
+                         "traffic_source": traffic_src, "peak_source": peak_src,
+                         "alg_bytes_per_solve_per_gpu": b_min // world},
             "solve_roofline": {"alg_bytes_per_solve": b_min,
                                "achieved_aggregate_gbs": round(b_min / (ms * 1e-3) / 1e9, 1)},
             "host_syncs_per_iter": syncs / (args.steps * 20),
@@ -400,20 +498,59 @@ def bench_main(args, cfg):
             "e2e": {"value": round(e2e_ms, 4), "unit": "ms/solve",
                     "h2d_bytes_per_step": 8 * n_glob, "d2h_bytes_per_step": 8 * n_glob},
             "gpu_launches": launches * args.steps * world,
-            "cpu_baseline": None,
-            "clocks": clk.summary(),
+            "check": check,
+            "strong_768": strong,
+            "cpu_baseline": cpu,
+            "clocks": clocks,
         }
         print(json.dumps(out), flush=True)
-    dist.barrier()  # no rank frees a window a peer may still store into
-    plan.close()
-    if nccl_plan is not None and plan is not nccl_plan:
-        nccl_plan.close()
-    disconnect_peers(opened)
+    dist.barrier()
     if comm is not None:
         rvk.lib().rvk_comm_destroy(comm)
     dist.destroy_process_group()
 
 
+def _shard_bytes(n_glob, nnz_glob, fl):
+    """Algorithmic bytes of one sharded solve (all ranks): per iteration
+    12 nnz + 8 (n+1) + 96 n with the x traffic cut by the x group (whole
+    solve, RVK_PLAN_X_SOLVE: 8.4 n; pairs: 16 n) and the constant Jacobi
+    diagonal (RVK_PLAN_CONST_DIAG: -8 n per iteration and in the setup)."""
+    grp = 20 if fl & 128 else (2 if fl & 16 else 1)
+    vb = 96 - (16 - 16 / grp) - (8 if fl & 1 else 0)
+    return int(20 * (12 * nnz_glob + 8 * (n_glob + 1) + vb * n_glob) + (56 if fl & 1 else 64) * n_glob)
+
+
+def _strong_768(args, ctx, stream, comm, rank, world, tdev, local):
+    """768^3 7-point row-sharded over the N GPUs, same backend selection as
+    the main run; ms/solve max over ranks, iterations/s, per-GPU GB/s."""
+    import bench
+    g = bench.CONFIGS["7pt768"][2]
+    shards = partition(3, g, world)
+    sh, A, b, x = _build_shard(ctx, 3, 7, g, shards, rank)
+    backend, plan, opened, fallback, _ = _peer_or_nccl(args, ctx, A, sh, shards, b, x, comm, rank,
+                                                        world, tdev)
+    steps = max(3, min(args.steps, 10))
+    ms, clocks, syncs = _time_sharded(plan, b, x, stream, steps, 3, tdev, local)
+    res = plan.result()
+    fl = rvk.lib().rvk_dcg_plan_flags(plan.h)
+    import torch.distributed as dist
+    dist.barrier()
+    plan.close()
+    disconnect_peers(opened)
+    n, nnz = bench._laplacian_size(3, 7, g)
+    b_min = _shard_bytes(n, nnz, fl)
+    hbm_peak, _ = bench.peaks()
+    per_gpu = b_min / world / (ms * 1e-3) / 1e9
+    if rank == 0:
+        print(f"strong_768 N={world}: {ms:.2f} ms/solve ({backend}), {per_gpu:.0f} GB/s per GPU",
+              file=__import__("sys").stderr, flush=True)
+    return {"workload": "3D 7-point Laplacian 768^3, Jacobi-CG 20 iterations (BASELINE configs[4])",
+            "n_gpus": world, "backend": backend, "comm_fallback": fallback,
+            "ms_per_solve": round(ms, 3), "steps": steps,
+            "iters_per_s": round(res.iterations / (ms * 1e-3), 1),
+            "per_gpu_gbs": round(per_gpu, 1), "frac": round(per_gpu / hbm_peak, 4),
+            "alg_bytes_per_solve": b_min, "host_syncs_per_iter": syncs / (steps * 20),
+            "clocks": clocks}
 def _global_nnz(dim, pts, grid):
     nx, ny, nz = (list(grid) + [1, 1])[:3]
     n = C.c_int64()

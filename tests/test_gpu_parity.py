@@ -828,3 +828,29 @@ def test_whole_solve_x_written_on_every_exit(ctx, graph, op):
         else:
             assert np.linalg.norm(x - ref.x) <= 1e-10 * np.linalg.norm(ref.x)
         plan.close()
+
+
+@pytest.mark.parametrize("graph", [True, False])
+def test_fused_solve_with_misaligned_b_and_x(ctx, graph):
+    """b / x only 8-byte aligned (ptr + 8) on a FUSED plan above
+    the small-system sizes.  The setup is then NOT folded into K1(0) (whose
+    gathers and L2 bulk prefetches of b need 16-B alignment) and x falls back
+    to the scalar update path; the result matches the oracle and the aligned
+    solve."""
+    dim, pts, g = 3, 7, (96, 90, 80)  # 691,200 rows > 512 K
+    Ah = O.build_laplacian(dim, pts, g)
+    n = Ah.n_rows
+    b = O.rhs(n)
+    ref = O.cg_solve(Ah, b, max_it=20)
+    A = rvk.DeviceCsr.laplacian(ctx, dim, pts, g)
+    plan = rvk.CgPlan(ctx, A, max_it=20, use_graph=graph, mode="fused")
+    assert plan.flags() & 512  # the plan folds for aligned right-hand sides
+    big_b = up(ctx, np.concatenate([[0.0], b, [0.0]]))
+    big_x = up(ctx, np.full(n + 2, np.nan))
+    rvk.check(rvk.lib().rvk_cg_solve_dev(plan.h, big_b.ptr + 8, big_x.ptr + 8))
+    res = plan.result()
+    x = big_x.download(ctx)
+    assert np.isnan(x[0]) and np.isnan(x[-1])  # nothing written outside x
+    check_cg(res, x[1:-1], ref)
+    xa, ra = plan.solve_host(b)  # aligned (plan staging buffers): folded path
+    check_cg(ra, xa, ref)
