@@ -50,8 +50,15 @@ typedef enum {
 /* Thread-local description of the last failure on this thread. */
 const char* rvk_last_error(void);
 int         rvk_abi_version(void);
-/* Number of SMs / name of device 0 as seen by the library (setup helper). */
+/* Number of SMs / name of the calling thread's current device (setup helper). */
 int         rvk_device_info(int* sm_count, char* name, int name_len);
+/* Device selection for the calling thread (cudaGetDeviceCount /
+ * cudaSetDevice): contexts, vectors and plans created afterwards on this
+ * thread live on that device.  One process may drive several GPUs (e.g. one
+ * host thread per device); kernel attributes and per-device caches are kept
+ * per device. */
+int         rvk_device_count(void);
+rvk_status  rvk_set_device(int device);
 
 /* ---- context: a CUDA stream + reduction scratch (PetscDeviceContext) -----
  * Replaces rivulet::Context's agent-thread queue (context.hpp:75-114;
@@ -367,8 +374,8 @@ rvk_status rvk_dcg_plan_destroy(rvk_dcg_plan plan);
 /* One shard per process: halo exchange (ncclSend/Recv) + partial-sum
  * allgather, or the PEER kernels, all stream-ordered -- zero host syncs.
  * cfg.use_graph != 0: the solve is captured once per (b, x) into a CUDA
- * graph (global capture mode for PEER / single-rank plans: any synchronous
- * call invalidates the capture) and replayed.  rvk_dcg_result also reports a
+ * graph (thread-local capture mode: any synchronous call made by the
+ * enqueuing thread invalidates the capture) and replayed.  rvk_dcg_result also reports a
  * pending NCCL asynchronous communicator error (RVK_ERR_COMM). */
 rvk_status rvk_dcg_solve_dev(rvk_dcg_plan plan, const double* b_own, double* x_own);
 rvk_status rvk_dcg_loopback_solve(rvk_dcg_plan* plans, int nplans, const double* const* b_own,

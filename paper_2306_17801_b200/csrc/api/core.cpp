@@ -1,6 +1,9 @@
 // core.cpp -- contexts, dependency tracking, launches, storage, counters.
 #include "internal.hpp"
 
+#include <memory>
+#include <mutex>
+
 #include <algorithm>
 #include <atomic>
 #include <cstring>
@@ -65,10 +68,18 @@ ContextImpl::~ContextImpl()
     if (h) rvk_ctx_destroy(h); // drains first
 }
 
+// One per device (the calling thread's current device): a process may drive
+// several GPUs, e.g. one host thread per device.
 const Context& global_sync_context()
 {
-    static Context ctx(StreamType::GloballyBlocking, "global_sync");
-    return ctx;
+    static std::mutex                              m;
+    static std::unique_ptr<Context>                per_dev[64];
+    int                                            dev = 0;
+    check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
+    std::lock_guard<std::mutex> lk(m);
+    auto&                       c = per_dev[dev & 63];
+    if (!c) c = std::make_unique<Context>(StreamType::GloballyBlocking, "global_sync");
+    return *c;
 }
 
 // ---- tracker -------------------------------------------------------------------
@@ -189,14 +200,30 @@ EvPtr Launch::end()
 
 // ---- storage ----------------------------------------------------------------------
 namespace {
-cudaStream_t mem_stream()
+// The allocation stream of a device (created on first use, with that device
+// current).  Storage lives on the device that was current when it was
+// allocated; its release goes to the same device's stream.
+cudaStream_t mem_stream(int dev)
 {
-    static cudaStream_t s = [] {
-        cudaStream_t st = nullptr;
-        check_cuda(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "cudaStreamCreate");
-        return st;
-    }();
+    static std::mutex   m;
+    static cudaStream_t per_dev[64] = {};
+    std::lock_guard<std::mutex> lk(m);
+    cudaStream_t& s = per_dev[dev & 63];
+    if (!s) {
+        int prev = 0;
+        check_cuda(cudaGetDevice(&prev), "cudaGetDevice");
+        if (prev != dev) check_cuda(cudaSetDevice(dev), "cudaSetDevice");
+        const cudaError_t e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+        if (prev != dev) cudaSetDevice(prev);
+        check_cuda(e, "cudaStreamCreate");
+    }
     return s;
+}
+int current_device()
+{
+    int dev = 0;
+    check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
+    return dev;
 }
 } // namespace
 
@@ -204,9 +231,10 @@ void* device_alloc(std::size_t bytes)
 {
     void* p = nullptr;
     if (bytes == 0) bytes = 16;
-    check_cuda(cudaMallocAsync(&p, bytes, mem_stream()), "cudaMallocAsync");
+    const cudaStream_t s = mem_stream(current_device());
+    check_cuda(cudaMallocAsync(&p, bytes, s), "cudaMallocAsync");
     // allocation is setup, not data: make it usable from any stream now
-    check_cuda(cudaStreamSynchronize(mem_stream()), "cudaStreamSynchronize(alloc)");
+    check_cuda(cudaStreamSynchronize(s), "cudaStreamSynchronize(alloc)");
     return p;
 }
 
@@ -214,8 +242,19 @@ void device_release(void* p, ObjectId id)
 {
     // Deferred release (managed_state.hpp:13-15): the free is
     // stream-ordered after every outstanding access, the host never waits.
-    Tracker::get().release_on(id, mem_stream());
-    if (p) cudaFreeAsync(p, mem_stream());
+    // The owning device's stream (the handle may die on another thread).
+    int                   dev = current_device();
+    cudaPointerAttributes a{};
+    if (p && cudaPointerGetAttributes(&a, p) == cudaSuccess && a.type == cudaMemoryTypeDevice)
+        dev = a.device;
+    else
+        cudaGetLastError();
+    const cudaStream_t s    = mem_stream(dev);
+    const int          prev = current_device();
+    if (prev != dev) cudaSetDevice(dev); // events and the free on the owning device
+    Tracker::get().release_on(id, s);
+    if (p) cudaFreeAsync(p, s);
+    if (prev != dev) cudaSetDevice(prev);
 }
 
 void check_no_write_view(const VecState& v, const char* api)
@@ -246,10 +285,16 @@ MatState::MatState(std::string name_) : id(next_object_id()), name(std::move(nam
 MatState::~MatState()
 {
     plans.reset();
-    Tracker::get().release_on(id, mem_stream());
-    if (off) cudaFreeAsync(off, mem_stream());
-    if (cols) cudaFreeAsync(cols, mem_stream());
-    if (vals) cudaFreeAsync(vals, mem_stream());
+    // the three arrays live on one device: release them there (device_release
+    // finds it from the pointer); the tracker entry of the matrix goes with
+    // the first non-null array
+    bool released = false;
+    for (void* p : {static_cast<void*>(off), static_cast<void*>(cols), static_cast<void*>(vals)})
+        if (p) {
+            device_release(p, released ? kUnknownId : id);
+            released = true;
+        }
+    if (!released) Tracker::get().release_on(id, mem_stream(current_device()));
 }
 
 } // namespace detail

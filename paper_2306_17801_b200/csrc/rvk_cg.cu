@@ -898,7 +898,7 @@ rvk_status build_while_graph(rvk_cg_plan P, const double* b, double* x, cudaGrap
         return rc;
     };
     // prologue
-    RVK_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeGlobal));
+    RVK_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
     rvk_status rc = vec ? launch_setup<true>(P, pcm, b, x) : launch_setup<false>(P, pcm, b, x);
     if (rc == RVK_OK) rc = launch_k1(P, 0, true, P->p[0], P->p[1]);
     const bool defer = x_defer(P, vec);
@@ -923,7 +923,7 @@ rvk_status build_while_graph(rvk_cg_plan P, const double* b, double* x, cudaGrap
     cudaGraph_t body = prm.conditional.phGraph_out[0];
     // body: odd iteration (p_old = p[1]) then even iteration (p_old = p[0])
     if ((e = cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0,
-                                           cudaStreamCaptureModeGlobal)) != cudaSuccess)
+                                           cudaStreamCaptureModeThreadLocal)) != cudaSuccess)
         return fail(cuda_error(e, "cudaStreamBeginCaptureToGraph"));
     // body: npb iterations (residues 1, 2, ..., 0 mod npb), so every p buffer
     // index is static; a group ending mid-body is flushed by the epilogue
@@ -940,7 +940,7 @@ rvk_status build_while_graph(rvk_cg_plan P, const double* b, double* x, cudaGrap
     if (e != cudaSuccess) return fail(cuda_error(e, "capture (while body)"));
     if (defer) { // epilogue after the loop: apply an update left pending
         cudaGraph_t epi = nullptr;
-        RVK_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeGlobal));
+        RVK_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
         rc = launch_xfix(P, x, wr);
         e  = cudaStreamEndCapture(s, &epi);
         if (rc != RVK_OK) return fail(rc);
@@ -1524,10 +1524,13 @@ rvk_status rvk_cg_solve_dev(rvk_cg_plan P, const double* b, double* x)
         P->launches = -1; // data-dependent: 3 + 4 per body pass
     } else {
         cudaGraph_t g = nullptr;
-        // Global capture mode: ANY synchronous CUDA call made while the solve
-        // is being enqueued invalidates the capture -- a structural proof
-        // that the solve performs zero host synchronisations.
-        RVK_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeGlobal));
+        // Thread-local capture mode: ANY synchronous CUDA call this thread
+        // makes while the solve is being enqueued invalidates the capture --
+        // a structural proof that the solve performs zero host
+        // synchronisations.  (Thread-local, not global: a global capture is
+        // invalidated by other host threads' allocations, which breaks one
+        // process driving several GPUs from several threads.)
+        RVK_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
         rvk_status rc = enqueue_solve(P, b, x);
         cudaError_t e = cudaStreamEndCapture(s, &g);
         if (rc != RVK_OK) {

@@ -1053,10 +1053,10 @@ rvk_status enqueue_dcg(rvk_dcg_plan P, const double* b_own, double* x_own)
 // PEER: 2 kernels per iteration carry all communication; NCCL: halo
 // send/recv + 2 allgathers per iteration between the kernels.  With
 // cfg.use_graph the solve is captured once per (b, x) into a CUDA graph and
-// replayed: PEER / single-rank plans in GLOBAL capture mode, which fails on
-// any synchronous CUDA call made while the solve is enqueued (the structural
-// proof of zero host syncs, as in rvk_cg_solve_dev); NCCL plans in
-// thread-local mode (NCCL's own proxy thread keeps running during capture).
+// replayed, in thread-local capture mode: any synchronous CUDA call this
+// thread makes while the solve is enqueued fails the capture (the structural
+// proof of zero host syncs, as in rvk_cg_solve_dev), while other host threads
+// -- NCCL's proxy thread, other devices' threads -- are not affected.
 rvk_status rvk_dcg_solve_dev(rvk_dcg_plan P, const double* b_own, double* x_own)
 {
     if (!P || !b_own || !x_own) return set_error(RVK_ERR_INVALID, "null argument");
@@ -1067,10 +1067,8 @@ rvk_status rvk_dcg_solve_dev(rvk_dcg_plan P, const double* b_own, double* x_own)
     if (!(P->graph && P->graph_b == b_own && P->graph_x == x_own)) {
         if (P->graph) cudaGraphExecDestroy(P->graph);
         P->graph          = nullptr;
-        const bool   nccl = !P->peer.on && P->comm && P->sh.nranks > 1;
         cudaGraph_t  g    = nullptr;
-        RVK_CUDA(cudaStreamBeginCapture(s, nccl ? cudaStreamCaptureModeThreadLocal
-                                                : cudaStreamCaptureModeGlobal));
+        RVK_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
         rvk_status  rc = enqueue_dcg(P, b_own, x_own);
         cudaError_t e  = cudaStreamEndCapture(s, &g);
         if (rc != RVK_OK) {

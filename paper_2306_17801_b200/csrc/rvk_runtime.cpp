@@ -83,6 +83,19 @@ int rvk_device_info(int* sms, char* name, int name_len)
     return RVK_OK;
 }
 
+int rvk_device_count(void)
+{
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+    return n;
+}
+
+rvk_status rvk_set_device(int device)
+{
+    RVK_CUDA(cudaSetDevice(device));
+    return RVK_OK;
+}
+
 uint64_t rvk_host_sync_count(void) { return g_host_syncs.load(); }
 void     rvk_host_sync_reset(void) { g_host_syncs.store(0); }
 

@@ -663,7 +663,7 @@ rvk_status rvk_tfqmr_solve_dev(rvk_tfqmr_plan P, const double* b, double* x)
         if (P->graph) cudaGraphExecDestroy(P->graph);
         P->graph      = nullptr;
         cudaGraph_t g = nullptr;
-        RVK_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeGlobal)); // proves 0 host syncs
+        RVK_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal)); // proves 0 host syncs
         rvk_status  rc = enqueue_tfqmr(P, b, x);
         cudaError_t e  = cudaStreamEndCapture(s, &g);
         if (rc != RVK_OK) {

@@ -29,7 +29,7 @@ CG_RUNNING, CG_CONVERGED, CG_BREAKDOWN, CG_COMM_ERROR = 0, 1, 2, 3
 
 # every symbol include/rvk.h declares (checked by tests/test_abi.py)
 EXPORTS = [
-    "rvk_last_error", "rvk_abi_version", "rvk_device_info",
+    "rvk_last_error", "rvk_abi_version", "rvk_device_info", "rvk_device_count", "rvk_set_device",
     "rvk_ctx_create", "rvk_ctx_destroy", "rvk_ctx_stream", "rvk_ctx_synchronize",
     "rvk_ctx_query_idle", "rvk_ctx_wait_for", "rvk_host_sync_count", "rvk_host_sync_reset",
     "rvk_malloc", "rvk_free", "rvk_malloc_async", "rvk_free_async", "rvk_host_alloc", "rvk_host_free", "rvk_memcpy_h2d",
@@ -110,6 +110,8 @@ def lib():
     sig = {
         "rvk_last_error": (C.c_char_p, []),
         "rvk_abi_version": (i, []),
+        "rvk_device_count": (i, []),
+        "rvk_set_device": (i, [i]),
         "rvk_device_info": (i, [C.POINTER(C.c_int), C.c_char_p, i]),
         "rvk_ctx_create": (i, [vp, C.POINTER(vp)]),
         "rvk_ctx_destroy": (i, [vp]),

@@ -1,6 +1,7 @@
 // test_api.cpp -- the C++ drop-in API (include/rivulet/) against SPEC.md's
 // examples and the CPU oracle (oracle/rvk_oracle.h, test infrastructure).
 // Run by tests/test_gpu_api.py on a B200; prints PASS/FAIL per case.
+#include "rvk.h"
 #include "rivulet/context.hpp"
 #include "rivulet/csr.hpp"
 #include "rivulet/expr.hpp"
@@ -21,6 +22,7 @@ extern "C" {
 #include <cstring>
 #include <functional>
 #include <string>
+#include <thread>
 #include <vector>
 
 using namespace rivulet;
@@ -298,6 +300,55 @@ int main()
         std::printf("  syncs: async(5)=%llu async(20)=%llu fused=%llu\n", (unsigned long long)syncs[0],
                     (unsigned long long)syncs[1], (unsigned long long)(runtime::host_syncs() - s0));
         EXPECT(runtime::host_syncs() - s0 == 1);
+    });
+    run("one process, one host thread per device: concurrent cg_solve on every GPU (2+ threads)", [] {
+        // per-device kernel attributes / SM counts / sync contexts / memory
+        // streams: each thread selects its device and runs the whole API there.
+        // With one GPU both threads share device 0 (the concurrency part).
+        const int ndev = rvk_device_count();
+        EXPECT(ndev >= 1);
+        const int nthr = ndev >= 2 ? ndev : 2;
+        auto h = oracle_laplacian(3, 7, 40, 36, 32);
+        std::vector<double> bh(h.n), xo(h.n), hist(21), work(5 * h.n);
+        ro_rhs(0x9E3779B97F4A7C15ull, (int64_t)h.n, bh.data());
+        ro_cg_config cfg{20, RO_PC_JACOBI, 0.0, 0.0};
+        ro_cg_solve((int64_t)h.n, h.off.data(), h.cols.data(), h.vals.data(), bh.data(), xo.data(),
+                    hist.data(), cfg, work.data());
+        std::vector<int>         ok(nthr, 0);
+        std::vector<std::string> err(nthr);
+        std::vector<std::thread> th;
+        for (int t = 0; t < nthr; ++t)
+            th.emplace_back([&, t] {
+                try {
+                    if (rvk_set_device(t % ndev) != RVK_OK) throw std::runtime_error(rvk_last_error());
+                    CsrMatrix    A(h.n, h.n, h.off, h.cols, h.vals);
+                    DenseVector  b(bh), x(h.n);
+                    SolverConfig c;
+                    for (int rep = 0; rep < 3; ++rep) {
+                        auto res = cg_solve(A, b, x, c);
+                        if (res.iterations != 20) throw std::runtime_error("iterations");
+                        for (int k = 0; k <= 20; ++k)
+                            if (!(rel(res.history[k], hist[k]) < 1e-10)) throw std::runtime_error("history");
+                        auto   xh = x.to_host();
+                        double num = 0, den = 0;
+                        for (std::size_t i = 0; i < h.n; ++i) {
+                            num += (xh[i] - xo[i]) * (xh[i] - xo[i]);
+                            den += xo[i] * xo[i];
+                        }
+                        if (!(std::sqrt(num / den) < 1e-10)) throw std::runtime_error("x");
+                    }
+                    ok[t] = 1;
+                } catch (const std::exception& e) {
+                    err[t] = e.what();
+                }
+            });
+        for (auto& t : th) t.join();
+        rvk_set_device(0);
+        for (int t = 0; t < nthr; ++t) {
+            if (!ok[t]) std::printf("  thread %d (device %d): %s\n", t, t % ndev, err[t].c_str());
+            EXPECT(ok[t]);
+        }
+        std::printf("  %d threads on %d device(s)\n", nthr, ndev);
     });
     run("cg breakdown reported with iteration (all modes)", [] {
         CsrMatrix   A(2, 2, {0, 1, 2}, {0, 1}, {1.0, -1.0});

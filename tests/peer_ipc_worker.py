@@ -29,6 +29,7 @@ def main():
     grid = tuple(int(v) for v in sys.argv[3].split("x"))
     max_it, rtol, repeats = int(sys.argv[4]), float(sys.argv[5]), int(sys.argv[6])
     one_gpu = len(sys.argv) > 7 and sys.argv[7] == "shared"
+    use_graph = len(sys.argv) > 8 and sys.argv[8] == "graph"  # the solve as one replayed CUDA graph
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     dev = 0 if one_gpu else int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(dev)
@@ -37,7 +38,7 @@ def main():
     shards = partition(dim, grid, world)
     sh = shards[rank]
     A = local_laplacian(ctx, dim, pts, grid, sh)
-    plan = ShardPlan(ctx, A, sh, max_it, rtol=rtol)
+    plan = ShardPlan(ctx, A, sh, max_it, rtol=rtol, use_graph=use_graph)
     opened = connect_peers(plan, shards, rank, world)
     b = rvk.DeviceArray(sh.n_own)
     x = rvk.DeviceArray(sh.n_own)

@@ -27,28 +27,35 @@ def free_port():
         return s.getsockname()[1]
 
 
-def run(world, dim, pts, grid, max_it=20, rtol=0.0, repeats=2):
+def run(world, dim, pts, grid, max_it=20, rtol=0.0, repeats=2, graph=False):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={world}", "--master-addr=127.0.0.1", f"--master-port={free_port()}",
            os.path.join(ROOT, "tests", "peer_ipc_worker.py"), str(dim), str(pts),
-           "x".join(map(str, grid)), str(max_it), repr(rtol), str(repeats), "shared"]
+           "x".join(map(str, grid)), str(max_it), repr(rtol), str(repeats), "shared",
+           "graph" if graph else "stream"]
     p = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert p.returncode == 0, p.stderr[-3000:]
     line = [ln for ln in p.stdout.splitlines() if ln.startswith("{")][-1]
     return json.loads(line)
 
 
-@pytest.mark.parametrize("world,dim,pts,grid", [(2, 3, 7, (24, 20, 18)), (3, 2, 9, (40, 45)),
-                                                (2, 3, 27, (12, 12, 16))])
-def test_peer_ipc_processes_vs_oracle(world, dim, pts, grid):
-    r = run(world, dim, pts, grid)
+@pytest.mark.parametrize("world,dim,pts,grid,graph", [(2, 3, 7, (24, 20, 18), False),
+                                                      (3, 2, 9, (40, 45), False),
+                                                      (2, 3, 27, (12, 12, 16), False),
+                                                      (2, 3, 7, (24, 20, 18), True),
+                                                      (3, 2, 5, (64, 61), True)])
+def test_peer_ipc_processes_vs_oracle(world, dim, pts, grid, graph):
+    """graph: every rank's solve is captured (thread-local capture mode: no
+    synchronous call anywhere in the enqueue) and replayed `repeats` times."""
+    r = run(world, dim, pts, grid, repeats=3 if graph else 2, graph=graph)
     assert r["states"] == [0] * world and r["iterations"] == [20] * world
     assert r["all_ranks_and_repeats_identical"]
     assert r["hist_rel"] < 1e-10 and r["x_rel"] < 1e-10
 
 
-def test_peer_ipc_processes_early_exit():
-    r = run(2, 2, 5, (32, 30), max_it=300, rtol=1e-6)
+@pytest.mark.parametrize("graph", [False, True])
+def test_peer_ipc_processes_early_exit(graph):
+    r = run(2, 2, 5, (32, 30), max_it=300, rtol=1e-6, graph=graph)
     assert r["states"] == [1, 1] and r["iterations"][0] == r["ref_iterations"]
     assert r["x_rel"] < 1e-10
 
@@ -61,15 +68,20 @@ def test_bench_two_ranks_shared_gpu():
     env = dict(os.environ, RVK_SHARED_GPU="1")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr=127.0.0.1", f"--master-port={free_port()}", "bench.py", "--gpus", "2",
-           "--steps", "2", "--warmup", "3", "--config", "7pt256"]
+           "--steps", "2", "--warmup", "3", "--config", "7pt256", "--no-cpu-baseline"]
     p = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
     assert p.returncode == 0, p.stderr[-3000:]
     lines = [ln for ln in p.stdout.splitlines() if ln.startswith("{")]
     assert len(lines) == 1, p.stdout[-2000:]
     out = json.loads(lines[0])
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "e2e",
-              "gpu_launches", "roofline", "clocks", "host_syncs_per_iter"):
+              "gpu_launches", "roofline", "clocks", "host_syncs_per_iter", "strong_768", "check"):
         assert k in out, k
-    assert out["config"]["shared_gpu_functional_check"] is True
+    assert out["run"]["shared_gpu_functional_check"] is True
     assert out["iterations"] == 20 and out["host_syncs_per_iter"] == 0
-    assert out["config"]["comm"].startswith("PEER")
+    assert out["run"]["comm"].startswith("PEER")
+    # the sharded run agrees with the single-GPU plan on the same global system
+    assert out["check"]["checked"] and out["check"]["ok"], out["check"]
+    # BASELINE configs[4] measured in the same invocation, sharded over both ranks
+    s = out["strong_768"]
+    assert s["n_gpus"] == 2 and s["backend"] == "peer" and s["host_syncs_per_iter"] == 0
