@@ -238,7 +238,7 @@ def sample_grid(dim, grid):
     return ((nx, ny, k) if dim == 3 else (nx, k)) if k < nplanes else tuple(grid)
 
 
-def time_reference(dim, pts, grid, steps: int, warmup: int) -> dict:
+def time_reference(dim, pts, grid, steps: int, warmup: int, solver: str = "cg") -> dict:
     """The reference's own kernels (oracle/_ref, kernels_{scalar,avx2}.cpp)
     driving the PETSc-order PCG on this host, 1 thread (the reference's
     kernels are single-threaded), on a bounded sample of the workload, each
@@ -257,10 +257,12 @@ def time_reference(dim, pts, grid, steps: int, warmup: int) -> dict:
         backends = {"scalar": 0}
         if O.ref_lib().ref_avx2_supported():
             backends["avx2"] = 1
-        solvers = {k: (lambda be=be: O.ref_cg_solve(A, b, max_it=MAX_IT, backend=be))
+        ref = O.ref_tfqmr_solve if solver == "tfqmr" else O.ref_cg_solve
+        solvers = {k: (lambda be=be: ref(A, b, max_it=MAX_IT, backend=be))
                    for k, be in backends.items()}
     else:
-        solvers = {"port": lambda: O.cg_solve(A, b, max_it=MAX_IT)}
+        port = O.tfqmr_solve if solver == "tfqmr" else O.cg_solve
+        solvers = {"port": lambda: port(A, b, max_it=MAX_IT)}
     solvers[next(iter(solvers))]()  # first touch of the work arrays (page faults), untimed
     per = {}
     for name, f in solvers.items():
@@ -321,10 +323,10 @@ def run_reference(args, cfg):
     print(json.dumps(out), flush=True)
 
 
-def cpu_baseline_entry(dim, pts, grid) -> dict:
+def cpu_baseline_entry(dim, pts, grid, solver: str = "cg") -> dict:
     """cpu_baseline of a GPU line: one sample solve per reference backend, the
     fastest reported (time_reference)."""
-    ref = time_reference(dim, pts, grid, steps=0, warmup=0)
+    ref = time_reference(dim, pts, grid, steps=0, warmup=0, solver=solver)
     return {"value": round(ref["per_backend_ms"][ref["best"]], 1), "unit": "ms/solve",
             "cores": ref["cores"], "kind": ref["kind"],
             "sample": "1 " + ref["sample"] + f" on the GPU box host per backend; value = the "
@@ -440,17 +442,9 @@ def run_tfqmr(args, cfg):
         e2e_once()
         e2e.append((time.perf_counter() - t0) * 1e3)
     e2e_ms = statistics.mean(e2e)
-    cpu = None
-    if not args.no_cpu_baseline:
-        import oracle as O
-        Ah = O.build_laplacian(dim, pts, grid)
-        bb = O.rhs(Ah.n_rows)
-        t0 = time.perf_counter()
-        O.tfqmr_solve(Ah, bb, max_it=MAX_IT)
-        cpu = {"value": round((time.perf_counter() - t0) * 1e3, 1), "unit": "ms/solve", "cores": 1,
-               "kind": "port",
-               "sample": f"1 full {MAX_IT}-iteration TFQMR solve of {desc} (oracle restatement; "
-                         "the reference ships no TFQMR source)"}
+    # the TFQMR loop over the reference's own kernels (oracle/ref_shim.cpp:
+    # ref_tfqmr_solve; the reference ships no TFQMR driver), fastest backend
+    cpu = None if args.no_cpu_baseline else cpu_baseline_entry(dim, pts, grid, solver="tfqmr")
     out = {
         "metric": f"20-iter Jacobi-TFQMR solve time, achieved HBM GB/s vs peak, host syncs/iter",
         "value": round(ms, 4), "unit": "ms/solve", "n_gpus": 1, "steps": args.steps,

@@ -16,7 +16,7 @@ __all__ = [
     "build", "lib", "ref_lib", "ref_available", "Csr", "build_laplacian", "laplacian_nnz",
     "rhs", "diagonal", "cg_solve", "ref_cg_solve", "spmv", "ref_spmv", "dot", "nrm2",
     "CgResult", "DEFAULT_SEED", "tfqmr_solve", "build_laplacian_rows", "stencil_spmv",
-    "cg_solve_stencil",
+    "cg_solve_stencil", "ref_tfqmr_solve",
 ]
 
 DEFAULT_SEED = 0x9E3779B97F4A7C15
@@ -113,6 +113,9 @@ def ref_lib():
         L.ref_pointwise_mult.argtypes = [C.c_int, C.c_int64, _f64p, _f64p, _f64p]
         L.ref_csr_spmv.argtypes = [C.c_int, C.c_int64, C.c_int64, _i64p, _i32p, _f64p,
                                    C.c_int64, _f64p, _f64p]
+        L.ref_tfqmr_solve.argtypes = [C.c_int, C.c_int64, C.c_int64, _i64p, _i32p, _f64p, _f64p,
+                                      _f64p, _f64p, C.c_int, C.c_int, C.c_double, C.c_double,
+                                      _f64p, np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS")]
         L.ref_cg_solve.argtypes = [C.c_int, C.c_int64, C.c_int64, _i64p, _i32p, _f64p, _f64p,
                                    _f64p, _f64p, C.c_int, C.c_int, C.c_double, C.c_double,
                                    _f64p, np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS")]
@@ -224,6 +227,21 @@ def ref_cg_solve(A: Csr, b: np.ndarray, max_it: int = 20, pc: str = "jacobi",
     ref_lib().ref_cg_solve(backend, n, A.nnz, A.off, A.cols, A.vals, b, x, hist, max_it,
                            1 if pc == "jacobi" else 0, rtol, atol, work, out)
     return CgResult(x, hist[: out[1] + 1].copy(), int(out[0]), int(out[1]), int(out[2]))
+
+
+def ref_tfqmr_solve(A: Csr, b: np.ndarray, max_it: int = 20, pc: str = "jacobi",
+                    rtol: float = 0.0, atol: float = 0.0, backend: int = 0) -> CgResult:
+    """tfqmr_solve's loop over the reference's own kernels (oracle/_ref,
+    ref_shim.cpp:ref_tfqmr_solve)."""
+    n = A.n_rows
+    b = np.ascontiguousarray(b, np.float64)
+    x = np.empty(n, np.float64)
+    hist = np.full(2 * max_it + 1, np.nan)
+    work = np.empty(11 * n, np.float64)
+    out = np.zeros(4, np.int32)
+    ref_lib().ref_tfqmr_solve(backend, n, A.nnz, A.off, A.cols, A.vals, b, x, hist, max_it,
+                              1 if pc == "jacobi" else 0, rtol, atol, work, out)
+    return CgResult(x, hist[: out[3]].copy(), int(out[0]), int(out[1]), int(out[2]))
 
 
 def tfqmr_solve(A: Csr, b: np.ndarray, max_it: int = 20, pc: str = "jacobi",

@@ -27,6 +27,7 @@ struct Ops {
     double (*nrm2)(std::span<const double>);
     void (*axpy)(double, std::span<const double>, std::span<double>);
     void (*aypx)(double, std::span<const double>, std::span<double>);
+    void (*waxpy)(double, std::span<const double>, std::span<const double>, std::span<double>);
     void (*pointwise_mult)(std::span<const double>, std::span<const double>, std::span<double>);
     void (*csr_spmv)(std::span<const std::int64_t>, std::span<const std::int32_t>,
                      std::span<const double>, std::span<const double>, std::span<double>);
@@ -37,14 +38,14 @@ struct Ops {
 Ops ops_for(int backend)
 {
     if (backend == 0)
-        return {rk::scalar::dot, rk::scalar::nrm2, rk::scalar::axpy, rk::scalar::aypx,
+        return {rk::scalar::dot, rk::scalar::nrm2, rk::scalar::axpy, rk::scalar::aypx, rk::scalar::waxpy,
                 rk::scalar::pointwise_mult, rk::scalar::csr_spmv};
 #if RIVULET_X86_64
     if (backend == 1)
-        return {rk::avx2::dot, rk::avx2::nrm2, rk::avx2::axpy, rk::avx2::aypx,
+        return {rk::avx2::dot, rk::avx2::nrm2, rk::avx2::axpy, rk::avx2::aypx, rk::avx2::waxpy,
                 rk::avx2::pointwise_mult, rk::avx2::csr_spmv};
 #endif
-    return {rk::dot, rk::nrm2, rk::axpy, rk::aypx, rk::pointwise_mult, rk::csr_spmv};
+    return {rk::dot, rk::nrm2, rk::axpy, rk::aypx, rk::waxpy, rk::pointwise_mult, rk::csr_spmv};
 }
 
 template <typename T>
@@ -149,6 +150,93 @@ void ref_cg_solve(int backend, std::int64_t n, std::int64_t nnz, const std::int6
         if (conv(dp)) { out3[0] = 1; return; }
         beta = o.dot(csp(z, n), csp(r, n));
     }
+}
+
+// Left-Jacobi TFQMR (Freund's single-loop formulation, two
+// half-iterations per outer iteration) in PETSc KSPSolve_TFQMR operation
+// order -- the same loop as rvk_oracle.c:ro_tfqmr_solve, every vector and
+// matrix operation through the reference's own kernels (the reference ships
+// no TFQMR source: solvers.cpp is absent).  B = D^-1 applied on the left:
+// each operator application is T1 = A v, out = dinv .* T1.  hist: ||B r0||
+// then the residual bound sqrt(2i+m+2) tau of every half step.
+// out4 = {status, iterations, breakdown_iter, n_hist}.
+void ref_tfqmr_solve(int backend, std::int64_t n, std::int64_t nnz, const std::int64_t* off,
+                     const std::int32_t* cols, const double* vals, const double* b, double* x,
+                     double* hist, int max_it, int pc, double rtol, double atol, double* work,
+                     int* out4)
+{
+    const Ops o = ops_for(backend);
+    double *R = work, *RP = work + n, *U = work + 2 * n, *P = work + 3 * n, *V = work + 4 * n;
+    double *D = work + 5 * n, *Q = work + 6 * n, *T = work + 7 * n, *AUQ = work + 8 * n;
+    double *T1 = work + 9 * n, *dinv = work + 10 * n;
+    const auto bytes = static_cast<std::size_t>(n) * sizeof(double);
+    int        nh    = 0;
+    out4[0] = 0; out4[1] = 0; out4[2] = -1; out4[3] = 0;
+    auto apply_BA = [&](const double* v, double* out) {
+        o.csr_spmv(csp(off, n + 1), csp(cols, nnz), csp(vals, nnz), csp(v, n), sp(T1, n));
+        if (pc == 1) o.pointwise_mult(csp(dinv, n), csp(T1, n), sp(out, n));
+        else std::memcpy(out, T1, bytes);
+    };
+    std::memset(x, 0, bytes);
+    if (pc == 1) {
+        for (std::int64_t row = 0; row < n; ++row) {
+            double d = 0.0;
+            for (auto k = off[row]; k < off[row + 1]; ++k)
+                if (cols[k] == row) d = vals[k];
+            dinv[row] = 1.0 / d;
+        }
+        o.pointwise_mult(csp(dinv, n), csp(b, n), sp(R, n)); // R = B (b - A x0), x0 = 0
+    } else {
+        std::memcpy(R, b, bytes);
+    }
+    double dp = o.nrm2(csp(R, n));
+    hist[nh++] = dp;
+    const double dp0 = dp;
+    auto conv = [&](double v) { return v <= std::fmax(rtol * dp0, atol); };
+    if (conv(dp)) { out4[0] = 1; out4[3] = nh; return; }
+    std::memcpy(RP, R, bytes);
+    double etaold = 0.0, psiold = 0.0, tau = dp, dpold = dp;
+    double rhoold = o.dot(csp(R, n), csp(RP, n));
+    std::memcpy(U, R, bytes);
+    std::memcpy(P, R, bytes);
+    apply_BA(P, V);
+    std::memset(D, 0, bytes);
+    for (int i = 0; i < max_it; ++i) {
+        const double s = o.dot(csp(V, n), csp(RP, n));
+        if (s == 0.0) { out4[0] = 2; out4[2] = i; out4[3] = nh; return; }
+        const double a = rhoold / s;
+        o.waxpy(-a, csp(V, n), csp(U, n), sp(Q, n));  // q = u - a v
+        o.waxpy(1.0, csp(U, n), csp(Q, n), sp(T, n)); // t = u + q
+        apply_BA(T, AUQ);
+        o.axpy(-a, csp(AUQ, n), sp(R, n));            // r = r - a B A (u + q)
+        dp = o.nrm2(csp(R, n));
+        for (int m = 0; m < 2; ++m) {
+            const double w   = m == 0 ? std::sqrt(dp * dpold) : dp;
+            const double psi = w / tau;
+            const double cm  = 1.0 / std::sqrt(1.0 + psi * psi);
+            tau              = tau * psi * cm;
+            const double eta = cm * cm * a;
+            const double cf  = psiold * psiold * etaold / a;
+            o.aypx(cf, csp(m == 0 ? U : Q, n), sp(D, n)); // d = (u|q) + cf d
+            o.axpy(eta, csp(D, n), sp(x, n));             // x = x + eta d
+            const double dpest = std::sqrt(2.0 * i + m + 2.0) * tau;
+            hist[nh++]         = dpest;
+            if (conv(dpest)) { out4[0] = 1; out4[1] = i + 1; out4[3] = nh; return; }
+            etaold = eta;
+            psiold = psi;
+        }
+        out4[1] = i + 1;
+        const double rho = o.dot(csp(R, n), csp(RP, n));
+        if (rhoold == 0.0) { out4[0] = 2; out4[2] = i; out4[3] = nh; return; }
+        const double bb = rho / rhoold;
+        o.waxpy(bb, csp(Q, n), csp(R, n), sp(U, n)); // u = r + b q
+        o.axpy(bb, csp(P, n), sp(Q, n));             // q = q + b p
+        o.waxpy(bb, csp(Q, n), csp(U, n), sp(P, n)); // p = u + b q
+        apply_BA(P, V);
+        rhoold = rho;
+        dpold  = dp;
+    }
+    out4[3] = nh;
 }
 
 } // extern "C"

@@ -1,4 +1,5 @@
-"""Generate tests/golden/cg_golden.json from the REFERENCE's own kernels.
+"""Generate tests/golden/cg_golden.json and tfqmr_golden.json from the
+REFERENCE's own kernels.
 
 Run here (needs oracle/_ref, i.e. /root/reference at build time):
     python tests/golden/make_golden.py
@@ -63,6 +64,41 @@ def main():
             "spmv_b": hexs(O.ref_spmv(A, b, backend=0)),
         })
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "cg_golden.json")
+    with open(path, "w") as f:
+        json.dump(out, f, indent=0)
+    print("wrote", path, os.path.getsize(path), "bytes")
+    tfqmr()
+
+
+TFQMR_CASES = [
+    # (name, dim, points, grid, pc, max_it, rtol)  -- SPEC.md:467-475 left-Jacobi TFQMR
+    ("5pt_16x16", 2, 5, (16, 16), "jacobi", 20, 0.0),
+    ("5pt_32x32", 2, 5, (32, 32), "jacobi", 20, 0.0),
+    ("9pt_32x32", 2, 9, (32, 32), "jacobi", 20, 0.0),
+    ("7pt_8x8x8", 3, 7, (8, 8, 8), "jacobi", 20, 0.0),
+    ("27pt_8x8x8", 3, 27, (8, 8, 8), "jacobi", 20, 0.0),
+    ("7pt_5x4x3", 3, 7, (5, 4, 3), "jacobi", 20, 0.0),
+    ("9pt_16x16_nopc", 2, 9, (16, 16), "none", 20, 0.0),
+    # device-side exit inside an outer iteration (rtol on the residual bound)
+    ("5pt_24x20_rtol", 2, 5, (24, 20), "jacobi", 200, 1e-6),
+]
+
+
+def tfqmr():
+    """The TFQMR loop of oracle/ref_shim.cpp:ref_tfqmr_solve: every vector and
+    matrix operation through kernels_scalar.cpp (backend 0)."""
+    out = {"generator": "oracle/_ref (reference kernels_scalar.cpp) via ref_tfqmr_solve, "
+                        "tests/golden/make_golden.py",
+           "seed": hex(O.DEFAULT_SEED), "cases": []}
+    for name, dim, pts, grid, pc, max_it, rtol in TFQMR_CASES:
+        A = O.build_laplacian(dim, pts, grid)
+        b = O.rhs(A.n_rows)
+        r = O.ref_tfqmr_solve(A, b, max_it=max_it, pc=pc, rtol=rtol, backend=0)
+        out["cases"].append({
+            "name": name, "dim": dim, "points": pts, "grid": list(grid), "pc": pc,
+            "max_it": max_it, "rtol": rtol, "n": A.n_rows, "sha_b": sha(b),
+            "status": r.status, "iterations": r.iterations, "hist": hexs(r.hist), "x": hexs(r.x)})
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "tfqmr_golden.json")
     with open(path, "w") as f:
         json.dump(out, f, indent=0)
     print("wrote", path, os.path.getsize(path), "bytes")

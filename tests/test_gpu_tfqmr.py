@@ -9,6 +9,9 @@ where the true residual stalls -- tests/test_oracle_tfqmr.py) are compared
 absolutely at 1e-14 ||B r0|| (a few dozen ulp of the initial residual).  Elementwise updates are bit-identical to the
 oracle's; only the three reductions per iteration differ in tree order.
 """
+import json
+import os
+
 import numpy as np
 import pytest
 
@@ -204,6 +207,30 @@ def test_tfqmr_constant_diagonal_bitexact(ctx, spec):
     assert np.array_equal(x1, x0)
     assert np.array_equal(r1.hist, r0.hist)
     check(r1, x1, O.tfqmr_solve(Ah, b, max_it=20))
+
+
+def _tfqmr_golden():
+    p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "tfqmr_golden.json")
+    with open(p) as f:
+        return json.load(f)["cases"]
+
+
+@pytest.mark.parametrize("case", _tfqmr_golden(), ids=lambda c: c["name"])
+@pytest.mark.parametrize("mode", ["fused", "unfused"])
+def test_tfqmr_vs_reference_golden(ctx, case, mode):
+    """Committed fixtures from the TFQMR loop over the reference's own kernels
+    (oracle/ref_shim.cpp:ref_tfqmr_solve, kernels_scalar.cpp); SPEC.md:474
+    tolerance 1e-8 on the history and x."""
+    A = rvk.DeviceCsr.laplacian(ctx, case["dim"], case["points"], tuple(case["grid"]))
+    b = O.rhs(A.n_rows)
+    plan, x, res = solve(ctx, A, b, max_it=case["max_it"], pc=case["pc"], rtol=case["rtol"],
+                         mode=mode)
+    hist = np.array([float.fromhex(v) for v in case["hist"]])
+    xref = np.array([float.fromhex(v) for v in case["x"]])
+    assert res.iterations == case["iterations"] and res.state == case["status"]
+    assert res.hist.size == hist.size
+    assert np.max(np.abs(res.hist - hist) / hist) < 1e-8
+    assert np.linalg.norm(x - xref) / np.linalg.norm(xref) < 1e-8
 
 
 @pytest.mark.parametrize("seed,n,nonsym", [(0, 4000, False), (1, 60000, False), (2, 30000, True)])

@@ -3,20 +3,66 @@
 The reference ships no TFQMR source (SPEC.md:467-475,
 :501 fix only "the standard Freund single-loop formulation with two
 half-iterations fused per outer iteration").  So the restatement is pinned
-by (1) an independent pure-Python transcription of the same recurrence,
+by (0) the same loop run over the REFERENCE's own kernels
+(oracle/ref_shim.cpp:ref_tfqmr_solve, kernels_{scalar,avx2}.cpp compiled
+into oracle/_ref) -- bit for bit on the scalar backend -- and the golden
+vectors it generated (tests/golden/tfqmr_golden.json, make_golden.py);
+(1) an independent pure-Python transcription of the same recurrence,
 element-for-element, on small systems; (2) the SPEC known answers (A = I
 exact in the first iteration, breakdown with iteration index); (3) the
 method's defining properties: the history is a residual BOUND
 (||B(b - A x_k)|| <= sqrt(k+1) tau_k) and the solve converges on a
 non-symmetric system, TFQMR's raison d'etre.
-Parity vs the reference itself stays unpinned for TFQMR.
 """
+import json
 import math
+import os
 
 import numpy as np
 import pytest
 
 import oracle as O
+
+TFQMR_GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "tfqmr_golden.json")
+needs_ref = pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
+
+
+def _tfqmr_golden_cases():
+    with open(TFQMR_GOLDEN) as f:
+        return json.load(f)["cases"]
+
+
+@pytest.mark.parametrize("case", _tfqmr_golden_cases(), ids=lambda c: c["name"])
+def test_tfqmr_restatement_reproduces_reference_golden(case):
+    """The C restatement == the reference-kernel loop's committed vectors,
+    bit for bit (history, x, status, iterations)."""
+    A = O.build_laplacian(case["dim"], case["points"], tuple(case["grid"]))
+    b = O.rhs(A.n_rows)
+    r = O.tfqmr_solve(A, b, max_it=case["max_it"], pc=case["pc"], rtol=case["rtol"])
+    assert r.status == case["status"] and r.iterations == case["iterations"]
+    assert [float(v).hex() for v in r.hist] == case["hist"]
+    assert [float(v).hex() for v in r.x] == case["x"]
+
+
+@needs_ref
+@pytest.mark.parametrize("spec", [(2, 5, (23, 19)), (2, 9, (16, 21)), (3, 7, (9, 8, 7)),
+                                  (3, 27, (7, 6, 5))])
+@pytest.mark.parametrize("pc", ["jacobi", "none"])
+def test_tfqmr_restatement_bitexact_vs_reference_kernels(spec, pc):
+    """Live: the restatement vs ref_tfqmr_solve over kernels_scalar.cpp (bit
+    for bit), and over the AVX2 kernels (their reductions use 4 lanes, so
+    within SPEC.md:474's 1e-8 while the history is above rounding level --
+    tiny systems reach it within 20 iterations)."""
+    dim, pts, g = spec
+    A = O.build_laplacian(dim, pts, g)
+    b = O.rhs(A.n_rows)
+    mine = O.tfqmr_solve(A, b, max_it=20, pc=pc)
+    ref = O.ref_tfqmr_solve(A, b, max_it=20, pc=pc, backend=0)
+    assert np.array_equal(mine.hist, ref.hist) and np.array_equal(mine.x, ref.x)
+    if O.ref_lib().ref_avx2_supported():
+        av = O.ref_tfqmr_solve(A, b, max_it=20, pc=pc, backend=1)
+        keep = ref.hist > 1e-6 * ref.hist[0]
+        assert np.max(np.abs(av.hist[keep] - ref.hist[keep]) / ref.hist[keep]) < 1e-8
 
 
 def _dense(A):
