@@ -7,6 +7,7 @@
 
 #include <array>
 #include <cstdint>
+#include <string>
 
 namespace rivulet::runtime {
 
@@ -37,6 +38,13 @@ void log_kernel(KernelKind kind, std::uint64_t flops, std::uint64_t kernel_count
 
 // Host synchronisations performed by the library (trace::host_sync analogue).
 std::uint64_t host_syncs();
+
+// The counters above as one JSON object: {"census": {kind: {kernels, flops}},
+// "total_flops", "reductions", "copies": {h2d, d2h, h2d_bytes, d2h_bytes},
+// "host_syncs", "dependency_edges"} (the metrics export; the event timeline
+// is rivulet::trace).
+std::string to_json();
+void        write_json(const std::string& path);
 
 void reset_all();
 

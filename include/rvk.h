@@ -73,10 +73,37 @@ rvk_status rvk_ctx_query_idle(rvk_ctx ctx, int* idle);   /* context.hpp:92; no b
 /* wait_for (context.hpp:88-90): future work on `waiter` starts after all
  * work enqueued on `waitee` so far.  Self-wait is a no-op. */
 rvk_status rvk_ctx_wait_for(rvk_ctx waiter, rvk_ctx waitee);
+/* Process-unique id and a display name (context.hpp:80-86 id()/name()): the
+ * trace's context rows. */
+uint64_t   rvk_ctx_id(rvk_ctx ctx);
+rvk_status rvk_ctx_set_name(rvk_ctx ctx, const char* name);
 
 /* ---- host-sync accounting (trace.hpp:40-41 HostSync events) ------------- */
 uint64_t rvk_host_sync_count(void);
 void     rvk_host_sync_reset(void);
+
+/* ---- tracing (trace.hpp:11-46, trace.cpp:48-104) ------------------------
+ * Task events: every solve / vector op / SpMV / assembly enqueued through
+ * this ABI and every C++-API kernel launch, timed ON THE DEVICE (two timing
+ * events on the context's stream, mapped onto the host steady clock when the
+ * trace is read; inside a stream capture the host enqueue time is logged
+ * instead).  HostSync events: every counted host wait, with its duration.
+ * Wait events: cross-context ordering edges.  Marker: user annotations.
+ * Every task and host wait is also an NVTX range (names as in the trace).
+ * Reading the trace (count / write) waits for the traced device work; it is
+ * not counted as a host sync.  Off by default; recording costs nothing then
+ * beyond the NVTX push/pop. */
+void       rvk_trace_enable(int on);        /* trace::set_enabled */
+int        rvk_trace_enabled(void);
+void       rvk_trace_clear(void);
+void       rvk_trace_marker(const char* label);
+size_t     rvk_trace_count(void);           /* events recorded so far */
+/* One JSON object per line, the reference's keys (trace.cpp:90-100):
+ * task, enqueue_seq, ctx, ctx_name, label, kind, blocked, start, end (ns),
+ * plus device_timed. */
+rvk_status rvk_trace_write_jsonl(const char* path);
+/* Chrome trace-event JSON (chrome://tracing / Perfetto timeline). */
+rvk_status rvk_trace_write_chrome(const char* path);
 
 /* ---- device memory (plumbing) -------------------------------------------- */
 rvk_status rvk_malloc(void** dev, size_t bytes);

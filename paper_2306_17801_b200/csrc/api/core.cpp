@@ -1,11 +1,13 @@
 // core.cpp -- contexts, dependency tracking, launches, storage, counters.
 #include "internal.hpp"
+#include "rvk_context.hpp"
 
 #include <memory>
 #include <mutex>
 
 #include <algorithm>
 #include <atomic>
+#include <cstdio>
 #include <cstring>
 
 namespace rivulet {
@@ -99,6 +101,7 @@ void Tracker::begin(const Context& ctx, ObjectId id, Mode mode)
     auto wait = [&](const Access& a) {
         if (a.ctx == ctx.id() || !a.ev) return; // FIFO on the same stream covers it
         check_cuda(cudaStreamWaitEvent(s, a.ev->e, 0), "cudaStreamWaitEvent");
+        rvk::trace::wait_edge(ctx.id(), a.ctx, "wait_for ctx");
         ++edges_;
     };
     if (r.last_write) wait(*r.last_write);
@@ -134,18 +137,16 @@ bool Tracker::await_host(ObjectId id, Mode mode)
         if (mode != Mode::Read)
             for (auto& a : it->second.readers) evs.push_back(a.ev);
     }
-    bool blocked = false;
+    std::vector<EvPtr> busy;
     for (auto& e : evs) {
         if (!e) continue;
-        if (cudaEventQuery(e->e) == cudaErrorNotReady) {
-            blocked = true;
-            check_cuda(cudaEventSynchronize(e->e), "cudaEventSynchronize");
-        } else {
-            (void)cudaGetLastError();
-        }
+        if (cudaEventQuery(e->e) == cudaErrorNotReady) busy.push_back(e);
+        else (void)cudaGetLastError();
     }
-    if (blocked) rvk::note_host_sync();
-    return blocked;
+    if (busy.empty()) return false;
+    rvk::trace::HostSyncScope hs("await_host", 0, true); // counted + traced
+    for (auto& e : busy) check_cuda(cudaEventSynchronize(e->e), "cudaEventSynchronize");
+    return true;
 }
 
 void Tracker::release_on(ObjectId id, cudaStream_t stream)
@@ -185,10 +186,13 @@ void Launch::begin()
     if (ctx_.stream_type() == StreamType::GloballyBlocking) drain_all();
     auto& t = Tracker::get();
     for (auto& [id, m] : acc_) t.begin(ctx_, id, m);
+    task_ = std::make_unique<rvk::trace::TaskScope>(
+        reinterpret_cast<cudaStream_t>(ctx_.cuda_stream()), label_.c_str(), ctx_.id(), ctx_.name().c_str());
 }
 
 EvPtr Launch::end()
 {
+    task_.reset(); // the task ends after its kernel(s)
     auto         ev = make_event();
     cudaStream_t s  = reinterpret_cast<cudaStream_t>(ctx_.cuda_stream());
     check_cuda(cudaEventRecord(ev->e, s), "cudaEventRecord");
@@ -311,6 +315,8 @@ Context::Context(StreamType type, std::string name) : impl_(std::make_shared<det
     impl_->type = type;
     impl_->name = std::move(name);
     detail::check(rvk_ctx_create(nullptr, &impl_->h), "Context");
+    impl_->h->id = impl_->id; // one id in the trace for the C++ and C views
+    detail::check(rvk_ctx_set_name(impl_->h, impl_->name.c_str()), "Context");
     std::lock_guard lk(detail::g_ctx_mu);
     detail::g_contexts.push_back(impl_);
 }
@@ -421,6 +427,35 @@ void log_d2h(std::uint64_t bytes)
 }
 
 std::uint64_t host_syncs() { return rvk_host_sync_count(); }
+
+std::string to_json()
+{
+    const Census     c = census();
+    const CopyCounts k = copy_counts();
+    std::string      j = "{\"census\":{";
+    for (int i = 0; i < static_cast<int>(KernelKind::kCount); ++i) {
+        j += (i ? ",\"" : "\"") + std::string(to_string(static_cast<KernelKind>(i))) +
+             "\":{\"kernels\":" + std::to_string(c.kernels[i]) +
+             ",\"flops\":" + std::to_string(c.flops[i]) + "}";
+    }
+    j += "},\"total_flops\":" + std::to_string(c.total_flops());
+    j += ",\"reductions\":" + std::to_string(c.reductions());
+    j += ",\"copies\":{\"h2d\":" + std::to_string(k.h2d) + ",\"d2h\":" + std::to_string(k.d2h) +
+         ",\"h2d_bytes\":" + std::to_string(k.h2d_bytes) +
+         ",\"d2h_bytes\":" + std::to_string(k.d2h_bytes) + "}";
+    j += ",\"host_syncs\":" + std::to_string(host_syncs());
+    j += ",\"dependency_edges\":" + std::to_string(detail::Tracker::get().edges()) + "}";
+    return j;
+}
+
+void write_json(const std::string& path)
+{
+    std::FILE* f = std::fopen(path.c_str(), "w");
+    if (!f) throw Error("runtime: cannot open '" + path + "' for writing");
+    const std::string j = to_json() + "\n";
+    const bool        ok = std::fwrite(j.data(), 1, j.size(), f) == j.size();
+    if (std::fclose(f) != 0 || !ok) throw Error("runtime: cannot write '" + path + "'");
+}
 
 void reset_all()
 {

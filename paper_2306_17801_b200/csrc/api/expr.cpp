@@ -360,11 +360,13 @@ double Managed::at(std::size_t i)
     if (!state_->host_valid) {
         // implicit synchronisation with the pending producer (managed.cpp:74-91)
         detail::Tracker::get().await_host(id(), detail::Mode::Read);
-        detail::check_cuda(cudaMemcpy(state_->host.data(), state_->dev, size() * sizeof(double),
-                                      cudaMemcpyDeviceToHost),
-                           "Managed::front");
+        {
+            rvk::trace::HostSyncScope hs("Managed::front", 0, true); // counted + traced
+            detail::check_cuda(cudaMemcpy(state_->host.data(), state_->dev, size() * sizeof(double),
+                                          cudaMemcpyDeviceToHost),
+                               "Managed::front");
+        }
         runtime::log_d2h(size() * sizeof(double));
-        rvk::note_host_sync();
         state_->host_valid  = true;
         state_->pending.reset();
         state_->pending_ctx = 0;

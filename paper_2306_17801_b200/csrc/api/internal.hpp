@@ -17,6 +17,7 @@
 #include "rivulet/runtime.hpp"
 #include "rivulet/vector.hpp"
 #include "rvk.h"
+#include "rvk_trace.hpp"
 
 #include <cuda_runtime.h>
 
@@ -110,6 +111,7 @@ private:
     Context                                 ctx_;
     std::string                             label_;
     std::vector<std::pair<ObjectId, Mode>>  acc_;
+    std::unique_ptr<rvk::trace::TaskScope>  task_; // begin() .. end(): NVTX range + trace Task
 };
 
 // ---- storage ---------------------------------------------------------------------

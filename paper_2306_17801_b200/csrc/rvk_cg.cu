@@ -546,8 +546,10 @@ rvk_status csr_bands(cudaStream_t s, const rvk_csr& A, SpmvBands* out)
     std::vector<unsigned long long> h(kDiagTable + 2);
     RVK_CUDA(cudaMemcpyAsync(h.data(), table, kDiagTable * 8 + 16, cudaMemcpyDeviceToHost, s));
     RVK_CUDA(cudaFreeAsync(table, s));
-    note_host_sync();
-    RVK_CUDA(cudaStreamSynchronize(s));
+    {
+        trace::HostSyncScope hs_("cg_plan.diagonal_scan");
+        RVK_CUDA(cudaStreamSynchronize(s));
+    }
     if (reinterpret_cast<int*>(&h[kDiagTable])[0]) return RVK_OK; // > 128 diagonals: general CSR
     std::vector<int64_t> d;
     for (int i = 0; i < kDiagTable; ++i)
@@ -599,8 +601,10 @@ rvk_status vector_is_constant(cudaStream_t s, int64_t n, const double* v, bool* 
     RVK_CUDA(cudaMemcpyAsync(&h, d, sizeof(int), cudaMemcpyDeviceToHost, s));
     RVK_CUDA(cudaMemcpyAsync(value, v, sizeof(double), cudaMemcpyDeviceToHost, s));
     RVK_CUDA(cudaFreeAsync(d, s));
-    note_host_sync();
-    RVK_CUDA(cudaStreamSynchronize(s));
+    {
+        trace::HostSyncScope hs_("cg_plan.const_diag_check");
+        RVK_CUDA(cudaStreamSynchronize(s));
+    }
     *is_const = h == 0;
     return RVK_OK;
 }
@@ -1117,8 +1121,10 @@ rvk_status solve_hostsync(rvk_cg_plan P, const double* b, double* x)
     double*       d   = P->tmp; // device scalar slot
     auto          read = [&](double* out) -> rvk_status {
         RVK_CUDA(cudaMemcpyAsync(out, d, sizeof(double), cudaMemcpyDeviceToHost, s));
-        note_host_sync();
-        RVK_CUDA(cudaStreamSynchronize(s));
+        {
+            trace::HostSyncScope hs_("cg_hostsync.read_scalar");
+            RVK_CUDA(cudaStreamSynchronize(s));
+        }
         return RVK_OK;
     };
     std::vector<double> hist(P->cfg.max_it + 1, 0.0);
@@ -1234,8 +1240,10 @@ rvk_status rvk_csr_validate(rvk_ctx ctx, const rvk_csr* A, int64_t* max_row_len)
     unsigned long long host[2] = {0, 0};
     RVK_CUDA(cudaMemcpyAsync(host, err, 16, cudaMemcpyDeviceToHost, ctx->stream));
     RVK_CUDA(cudaFreeAsync(err, ctx->stream));
-    note_host_sync();
-    RVK_CUDA(cudaStreamSynchronize(ctx->stream));
+    {
+        trace::HostSyncScope hs_("csr_validate");
+        RVK_CUDA(cudaStreamSynchronize(ctx->stream));
+    }
     const unsigned int e = (unsigned int)host[0];
     if (max_row_len) *max_row_len = (int64_t)host[1];
     if (A->n_rows == 0 && A->nnz != 0) return set_error(RVK_ERR_INVALID, "CsrMatrix: nnz != 0 with no rows");
@@ -1253,6 +1261,7 @@ rvk_status rvk_csr_spmv(rvk_ctx ctx, const rvk_csr* A, const double* x, double* 
     if (!ctx || !A) return set_error(RVK_ERR_INVALID, "csr_spmv: null argument");
     if (A->n_rows == 0) return RVK_OK;
     if (!x || !y) return set_error(RVK_ERR_INVALID, "csr_spmv: null vector");
+    RVK_TRACE_TASK(ctx, "rvk_csr_spmv");
     if (A->nnz == 0) return rvk_set(ctx, A->n_rows, 0.0, y); // every row empty: y = 0
     // Tile height from the mean row length (no host sync on this path);
     // tiles that overflow a stage fall back to direct global reads.
@@ -1268,6 +1277,7 @@ rvk_status rvk_csr_diagonal(rvk_ctx ctx, const rvk_csr* A, double* diag)
 {
     if (!ctx || !A || (A->n_rows > 0 && !diag)) return set_error(RVK_ERR_INVALID, "null argument");
     if (A->n_rows == 0) return RVK_OK;
+    RVK_TRACE_TASK(ctx, "rvk_csr_diagonal");
     k_diagonal<false><<<update_grid(2 * A->n_rows), kUpdThreads, 0, ctx->stream>>>(
         A->n_rows, A->row_offsets, A->col_indices, A->values, diag, 0);
     RVK_CHECK_LAUNCH("k_diagonal");
@@ -1278,6 +1288,7 @@ rvk_status rvk_csr_diagonal_inverse(rvk_ctx ctx, const rvk_csr* A, double* dinv)
 {
     if (!ctx || !A || (A->n_rows > 0 && !dinv)) return set_error(RVK_ERR_INVALID, "null argument");
     if (A->n_rows == 0) return RVK_OK;
+    RVK_TRACE_TASK(ctx, "rvk_csr_diagonal_inverse");
     k_diagonal<true><<<update_grid(2 * A->n_rows), kUpdThreads, 0, ctx->stream>>>(
         A->n_rows, A->row_offsets, A->col_indices, A->values, dinv, 0);
     RVK_CHECK_LAUNCH("k_diagonal");
@@ -1288,6 +1299,7 @@ rvk_status rvk_cg_plan_create(rvk_ctx ctx, const rvk_csr* A, rvk_cg_config cfg, 
 {
     if (!ctx || !A || !out) return set_error(RVK_ERR_INVALID, "cg_plan_create: null argument");
     *out = nullptr;
+    RVK_TRACE_TASK(ctx, "cg.plan_create");
     if (A->n_rows != A->n_cols) return set_error(RVK_ERR_DIM, "cg_solve: matrix is not square");
     if (A->n_rows < 1) return set_error(RVK_ERR_DIM, "cg_solve: empty system");
     if (cfg.max_it < 1) return set_error(RVK_ERR_INVALID, "cg_solve: max_it must be >= 1");
@@ -1410,6 +1422,7 @@ rvk_status rvk_cg_plan_create_stencil(rvk_ctx ctx, int dim, int points, int64_t 
                                       int64_t nz, rvk_cg_config cfg, rvk_cg_plan* out)
 {
     if (!ctx || !out) return set_error(RVK_ERR_INVALID, "cg_plan_create_stencil: null argument");
+    RVK_TRACE_TASK(ctx, "cg.plan_create_stencil");
     *out = nullptr;
     if (dim == 2) nz = 1;
     int64_t n = 0, nnz = 0;
@@ -1504,6 +1517,7 @@ rvk_status rvk_cg_solve_dev(rvk_cg_plan P, const double* b, double* x)
     if (!P) return set_error(RVK_ERR_INVALID, "null plan");
     if (!b || !x) return set_error(RVK_ERR_INVALID, "cg_solve: null vector");
     if (b == x) return set_error(RVK_ERR_INVALID, "cg_solve: b and x must not alias");
+    RVK_TRACE_TASK(P->ctx, "cg.solve");
     cudaStream_t s = P->ctx->stream;
     if (P->mode == RVK_CG_MODE_HOSTSYNC) return solve_hostsync(P, b, x);
     // one cooperative launch needs no graph
@@ -1567,8 +1581,10 @@ rvk_status rvk_cg_result(rvk_cg_plan P, double* hist_host, rvk_cg_info* info)
     if (hist_host)
         RVK_CUDA(cudaMemcpyAsync(hist_host, P->hist, sizeof(double) * (P->cfg.max_it + 1),
                                  cudaMemcpyDeviceToHost, s));
-    note_host_sync();
-    RVK_CUDA(cudaStreamSynchronize(s));
+    {
+        trace::HostSyncScope hs_("rvk_cg_result");
+        RVK_CUDA(cudaStreamSynchronize(s));
+    }
     if (info) {
         info->state          = h.state;
         info->iterations     = h.iterations;
@@ -1584,6 +1600,7 @@ rvk_status rvk_cg_solve_host(rvk_cg_plan P, const double* b_host, double* x_host
                              double* hist_host, rvk_cg_info* info)
 {
     if (!P || !b_host || !x_host) return set_error(RVK_ERR_INVALID, "null argument");
+    RVK_TRACE_TASK(P->ctx, "cg.solve_host");
     const size_t vb = (size_t)P->A.n_rows * sizeof(double);
     if (!P->b_buf) RVK_CUDA(cudaMalloc(&P->b_buf, vb));
     if (!P->x_buf) RVK_CUDA(cudaMalloc(&P->x_buf, vb));
@@ -1607,6 +1624,7 @@ rvk_status rvk_cg_solve_host_many(rvk_cg_plan P, int nrhs, const double* const* 
     if (!P || nrhs < 0 || (nrhs && (!b_host || !x_host)))
         return set_error(RVK_ERR_INVALID, "null argument");
     if (nrhs == 0) return RVK_OK;
+    RVK_TRACE_TASK(P->ctx, "cg.solve_host_many");
     const size_t vb = (size_t)P->A.n_rows * sizeof(double);
     const int    H  = P->cfg.max_it + 1;
     cudaStream_t s  = P->ctx->stream;
@@ -1662,8 +1680,10 @@ rvk_status rvk_cg_solve_host_many(rvk_cg_plan P, int nrhs, const double* const* 
         RVK_CUDA(cudaMemcpyAsync(hist_host, P->hist_all, (size_t)nrhs * H * sizeof(double),
                                  cudaMemcpyDeviceToHost, s));
     RVK_CUDA(cudaMemcpyAsync(st.data(), P->st_all, nrhs * sizeof(CgState), cudaMemcpyDeviceToHost, s));
-    note_host_sync();
-    RVK_CUDA(cudaStreamSynchronize(s));
+    {
+        trace::HostSyncScope hs_("rvk_cg_solve_host_many");
+        RVK_CUDA(cudaStreamSynchronize(s));
+    }
     int broke = -1;
     for (int k = 0; k < nrhs; ++k) {
         if (infos) {

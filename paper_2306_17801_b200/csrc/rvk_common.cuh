@@ -6,6 +6,7 @@
 #include <cstdint>
 
 #include "rvk.h"
+#include "rvk_trace.hpp"
 
 namespace rvk {
 
@@ -228,6 +229,9 @@ cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
     return cudaPeekAtLastError();
 }
 } // namespace rvk
+
+// Device task of an ABI entry point: NVTX range + trace Task event (rvk_trace.hpp).
+#define RVK_TRACE_TASK(ctx, label) ::rvk::trace::TaskScope rvk_task_((ctx)->stream, (label), (ctx)->id, (ctx)->name)
 
 #define RVK_CUDA(call)                                                   \
     do {                                                                 \

@@ -24,6 +24,8 @@ struct rvk_ctx_s {
     bool          owns_stream = false;
     rvk::Scratch  scratch{};
     cudaEvent_t   wait_event  = nullptr; // reused by rvk_ctx_wait_for
+    uint64_t      id          = 0;       // process-unique (trace rows)
+    char          name[48]    = "";      // rvk_ctx_set_name (trace rows)
 };
 
 namespace rvk {

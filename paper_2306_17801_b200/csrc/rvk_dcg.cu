@@ -851,6 +851,7 @@ rvk_status phase_finish(rvk_dcg_plan P)
 rvk_status nccl_allgather(rvk_dcg_plan P)
 {
     double* mine = P->gather + P->sh.rank * 4;
+    RVK_TRACE_TASK(P->ctx, "dcg.nccl_allgather");
     RVK_NCCL(nccl().AllGather(mine, P->gather, 4, ncclDouble, P->comm->comm, P->ctx->stream));
     return RVK_OK;
 }
@@ -864,6 +865,7 @@ rvk_status nccl_halo(rvk_dcg_plan P, bool with_p, int it)
     const int   nv      = with_p ? 2 : 1;
     auto&       api     = nccl();
     cudaStream_t s      = P->ctx->stream;
+    RVK_TRACE_TASK(P->ctx, "dcg.nccl_halo");
     RVK_NCCL(api.GroupStart());
     for (int v = 0; v < nv; ++v) {
         double* base = vecs[v];
@@ -970,6 +972,7 @@ rvk_status rvk_dcg_plan_create(rvk_ctx ctx, const rvk_csr* A, rvk_shard sh, rvk_
                                rvk_comm comm, double* shared_gather, rvk_dcg_plan* out)
 {
     if (!ctx || !A || !out) return set_error(RVK_ERR_INVALID, "dcg_plan_create: null argument");
+    RVK_TRACE_TASK(ctx, "dcg.plan_create");
     *out = nullptr;
     if (sh.nranks < 1 || sh.nranks > kMaxRanks || sh.rank < 0 || sh.rank >= sh.nranks)
         return set_error(RVK_ERR_INVALID, "dcg_plan_create: bad shard rank/nranks");
@@ -1062,6 +1065,7 @@ rvk_status rvk_dcg_solve_dev(rvk_dcg_plan P, const double* b_own, double* x_own)
     if (!P || !b_own || !x_own) return set_error(RVK_ERR_INVALID, "null argument");
     if (!P->comm && !P->peer.on && P->sh.nranks > 1)
         return set_error(RVK_ERR_INVALID, "loopback shards are solved with rvk_dcg_loopback_solve");
+    RVK_TRACE_TASK(P->ctx, "dcg.solve");
     if (!P->cfg.use_graph) return enqueue_dcg(P, b_own, x_own);
     cudaStream_t s = P->ctx->stream;
     if (!(P->graph && P->graph_b == b_own && P->graph_x == x_own)) {
@@ -1103,6 +1107,7 @@ rvk_status rvk_dcg_loopback_solve(rvk_dcg_plan* Ps, int np, const double* const*
         if (!peer && np > 1 && (Ps[r]->owns_gather || Ps[r]->gather != Ps[0]->gather))
             return set_error(RVK_ERR_INVALID, "loopback shards need one shared gather buffer");
     }
+    RVK_TRACE_TASK(Ps[0]->ctx, "dcg.loopback_solve");
     // phase-major order: every flag a PEER kernel waits for was released by
     // a kernel enqueued before it on this stream (no spin ever blocks)
     for (int r = 0; r < np; ++r) RVK_TRY(phase_setup(Ps[r], b[r], x[r]));
@@ -1124,8 +1129,10 @@ rvk_status rvk_dcg_result(rvk_dcg_plan P, double* hist_host, rvk_cg_info* info)
     RVK_CUDA(cudaMemcpyAsync(&h, P->st, sizeof h, cudaMemcpyDeviceToHost, s));
     if (hist_host)
         RVK_CUDA(cudaMemcpyAsync(hist_host, P->hist, (P->cfg.max_it + 1) * 8, cudaMemcpyDeviceToHost, s));
-    note_host_sync();
-    RVK_CUDA(cudaStreamSynchronize(s));
+    {
+        trace::HostSyncScope hs_("rvk_dcg_result");
+        RVK_CUDA(cudaStreamSynchronize(s));
+    }
     if (info) {
         info->state          = h.state;
         info->iterations     = h.iterations;

@@ -103,7 +103,9 @@ rvk_status rvk_ctx_create(void* cuda_stream, rvk_ctx* out)
 {
     if (!out) return set_error(RVK_ERR_INVALID, "ctx_create: null out");
     *out   = nullptr;
+    static std::atomic<uint64_t> next_id{0};
     auto c = new rvk_ctx_s();
+    c->id  = ++next_id;
     if (cuda_stream) {
         c->stream = static_cast<cudaStream_t>(cuda_stream);
     } else {
@@ -142,12 +144,22 @@ rvk_status rvk_ctx_destroy(rvk_ctx c)
 }
 
 void* rvk_ctx_stream(rvk_ctx c) { return c ? static_cast<void*>(c->stream) : nullptr; }
+uint64_t rvk_ctx_id(rvk_ctx c) { return c ? c->id : 0; }
+
+rvk_status rvk_ctx_set_name(rvk_ctx c, const char* name)
+{
+    if (!c) return set_error(RVK_ERR_INVALID, "null context");
+    std::snprintf(c->name, sizeof c->name, "%s", name ? name : "");
+    return RVK_OK;
+}
 
 rvk_status rvk_ctx_synchronize(rvk_ctx c)
 {
     if (!c) return set_error(RVK_ERR_INVALID, "null context");
-    note_host_sync();
-    RVK_CUDA(cudaStreamSynchronize(c->stream));
+    {
+        trace::HostSyncScope hs_("rvk_ctx_synchronize", c->id);
+        RVK_CUDA(cudaStreamSynchronize(c->stream));
+    }
     return RVK_OK;
 }
 
@@ -169,6 +181,7 @@ rvk_status rvk_ctx_wait_for(rvk_ctx waiter, rvk_ctx waitee)
     if (waiter == waitee || waiter->stream == waitee->stream) return RVK_OK; // no-op
     RVK_CUDA(cudaEventRecord(waitee->wait_event, waitee->stream));
     RVK_CUDA(cudaStreamWaitEvent(waiter->stream, waitee->wait_event, 0));
+    trace::wait_edge(waiter->id, waitee->id, "wait_for ctx");
     return RVK_OK;
 }
 
@@ -248,8 +261,10 @@ rvk_status rvk_scalar_read(rvk_ctx c, const double* s_dev, double* out_host)
 {
     if (!c || !s_dev || !out_host) return set_error(RVK_ERR_INVALID, "null argument");
     RVK_CUDA(cudaMemcpyAsync(out_host, s_dev, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-    note_host_sync();
-    RVK_CUDA(cudaStreamSynchronize(c->stream));
+    {
+        trace::HostSyncScope hs_("rvk_scalar_read");
+        RVK_CUDA(cudaStreamSynchronize(c->stream));
+    }
     return RVK_OK;
 }
 

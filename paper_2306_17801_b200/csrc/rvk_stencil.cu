@@ -152,6 +152,7 @@ rvk_status rvk_build_laplacian(rvk_ctx ctx, int dim, int points, int64_t nx, int
     int64_t n = 0, nnz = 0;
     rvk_status rc = rvk_laplacian_size(dim, points, nx, ny, nz, &n, &nnz);
     if (rc != RVK_OK) return rc;
+    RVK_TRACE_TASK(ctx, "rvk_build_laplacian");
     Grid3 g{nx, ny, nz, (points == 9 || points == 27) ? 1 : 0, dim == 3 ? 1 : 0,
             (double)(points - 1)};
     k_build_laplacian<<<grid_for(n), 256, 0, ctx->stream>>>(g, 0, n, 0, off, cols, vals);
@@ -184,6 +185,7 @@ rvk_status rvk_build_laplacian_rows(rvk_ctx ctx, int dim, int points, int64_t nx
     int64_t    nnz = 0;
     rvk_status rc  = rvk_laplacian_rows_nnz(dim, points, nx, ny, nz, row_begin, row_end, &nnz);
     if (rc != RVK_OK) return rc;
+    RVK_TRACE_TASK(ctx, "rvk_build_laplacian_rows");
     Grid3 g{nx, ny, nz, (points == 9 || points == 27) ? 1 : 0, dim == 3 ? 1 : 0,
             (double)(points - 1)};
     k_build_laplacian<<<grid_for(row_end - row_begin), 256, 0, ctx->stream>>>(
@@ -196,6 +198,7 @@ rvk_status rvk_fill_rhs(rvk_ctx ctx, uint64_t seed, int64_t n, double* b)
 {
     if (!ctx || (n > 0 && !b)) return set_error(RVK_ERR_INVALID, "null argument");
     if (n <= 0) return RVK_OK;
+    RVK_TRACE_TASK(ctx, "rvk_fill_rhs");
     k_fill_rhs<<<grid_for(n), 256, 0, ctx->stream>>>(seed, n, b);
     RVK_CHECK_LAUNCH("k_fill_rhs");
     return RVK_OK;

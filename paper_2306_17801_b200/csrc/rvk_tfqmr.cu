@@ -589,6 +589,7 @@ rvk_status rvk_tfqmr_plan_create(rvk_ctx ctx, const rvk_csr* A, rvk_cg_config cf
                                  rvk_tfqmr_plan* out)
 {
     if (!ctx || !A || !out) return set_error(RVK_ERR_INVALID, "tfqmr_plan_create: null argument");
+    RVK_TRACE_TASK(ctx, "tfqmr.plan_create");
     *out = nullptr;
     if (A->n_rows != A->n_cols) return set_error(RVK_ERR_DIM, "tfqmr_solve: matrix is not square");
     if (A->n_rows < 1) return set_error(RVK_ERR_DIM, "tfqmr_solve: empty system");
@@ -657,6 +658,7 @@ rvk_status rvk_tfqmr_solve_dev(rvk_tfqmr_plan P, const double* b, double* x)
 {
     if (!P || !b || !x) return set_error(RVK_ERR_INVALID, "tfqmr_solve: null argument");
     if (b == x) return set_error(RVK_ERR_INVALID, "tfqmr_solve: b and x must not alias");
+    RVK_TRACE_TASK(P->ctx, "tfqmr.solve");
     cudaStream_t s = P->ctx->stream;
     if (!P->cfg.use_graph) return enqueue_tfqmr(P, b, x);
     if (!P->graph || P->g_b != b || P->g_x != x) {
@@ -696,8 +698,10 @@ rvk_status rvk_tfqmr_result(rvk_tfqmr_plan P, double* hist_host, int* n_hist, rv
     if (hist_host)
         RVK_CUDA(cudaMemcpyAsync(hist_host, P->hist, 8 * (2 * (size_t)P->cfg.max_it + 1),
                                  cudaMemcpyDeviceToHost, s));
-    note_host_sync();
-    RVK_CUDA(cudaStreamSynchronize(s));
+    {
+        trace::HostSyncScope hs_("rvk_tfqmr_result");
+        RVK_CUDA(cudaStreamSynchronize(s));
+    }
     if (n_hist) *n_hist = h.nhist;
     if (info) {
         info->state          = h.state;

@@ -237,12 +237,14 @@ extern "C" {
 rvk_status rvk_dot(rvk_ctx ctx, int64_t n, const double* x, const double* y, double* out_dev)
 {
     if (!ctx) return set_error(RVK_ERR_INVALID, "null context");
+    RVK_TRACE_TASK(ctx, "rvk_dot");
     return launch_reduce<0>(ctx->stream, ctx->scratch, n, x, y, out_dev, nullptr, nullptr);
 }
 
 rvk_status rvk_nrm2(rvk_ctx ctx, int64_t n, const double* x, double* out_dev)
 {
     if (!ctx) return set_error(RVK_ERR_INVALID, "null context");
+    RVK_TRACE_TASK(ctx, "rvk_nrm2");
     return launch_reduce<1>(ctx->stream, ctx->scratch, n, x, nullptr, out_dev, nullptr, nullptr);
 }
 
@@ -250,6 +252,7 @@ rvk_status rvk_dot2(rvk_ctx ctx, int64_t n, const double* z, const double* r, do
                     double* zr_dev)
 {
     if (!ctx) return set_error(RVK_ERR_INVALID, "null context");
+    RVK_TRACE_TASK(ctx, "rvk_dot2");
     return launch_reduce<2>(ctx->stream, ctx->scratch, n, z, r, zz_dev, zr_dev, nullptr);
 }
 
@@ -257,6 +260,7 @@ rvk_status rvk_axpy(rvk_ctx ctx, int64_t n, rvk_scalar a, const double* x, doubl
 {
     if (n > 0 && (!x || !y)) return set_error(RVK_ERR_INVALID, "axpy: null vector");
     if (!ctx) return set_error(RVK_ERR_INVALID, "null context");
+    RVK_TRACE_TASK(ctx, "rvk_axpy");
     return launch_ew<EW_AXPY>(ctx->stream, n, a, x, y, y, nullptr);
 }
 
@@ -264,6 +268,7 @@ rvk_status rvk_aypx(rvk_ctx ctx, int64_t n, rvk_scalar b, const double* x, doubl
 {
     if (n > 0 && (!x || !y)) return set_error(RVK_ERR_INVALID, "aypx: null vector");
     if (!ctx) return set_error(RVK_ERR_INVALID, "null context");
+    RVK_TRACE_TASK(ctx, "rvk_aypx");
     return launch_ew<EW_AYPX>(ctx->stream, n, b, x, y, y, nullptr);
 }
 
@@ -272,12 +277,14 @@ rvk_status rvk_waxpy(rvk_ctx ctx, int64_t n, rvk_scalar a, const double* x, cons
 {
     if (n > 0 && (!x || !y)) return set_error(RVK_ERR_INVALID, "waxpy: null vector");
     if (!ctx) return set_error(RVK_ERR_INVALID, "null context");
+    RVK_TRACE_TASK(ctx, "rvk_waxpy");
     return launch_ew<EW_WAXPY>(ctx->stream, n, a, x, y, w, nullptr);
 }
 
 rvk_status rvk_scale(rvk_ctx ctx, int64_t n, rvk_scalar a, double* x)
 {
     if (!ctx) return set_error(RVK_ERR_INVALID, "null context");
+    RVK_TRACE_TASK(ctx, "rvk_scale");
     return launch_ew<EW_SCALE>(ctx->stream, n, a, nullptr, x, x, nullptr);
 }
 
@@ -286,12 +293,14 @@ rvk_status rvk_pointwise_mult(rvk_ctx ctx, int64_t n, const double* a, const dou
 {
     if (n > 0 && (!a || !b)) return set_error(RVK_ERR_INVALID, "pointwise_mult: null vector");
     if (!ctx) return set_error(RVK_ERR_INVALID, "null context");
+    RVK_TRACE_TASK(ctx, "rvk_pointwise_mult");
     return launch_ew<EW_PMULT>(ctx->stream, n, const_scalar(0.0), a, b, out, nullptr);
 }
 
 rvk_status rvk_set(rvk_ctx ctx, int64_t n, double value, double* x)
 {
     if (!ctx) return set_error(RVK_ERR_INVALID, "null context");
+    RVK_TRACE_TASK(ctx, "rvk_set");
     return launch_ew<EW_SET>(ctx->stream, n, const_scalar(value), nullptr, nullptr, x, nullptr);
 }
 
@@ -300,6 +309,7 @@ rvk_status rvk_copy(rvk_ctx ctx, int64_t n, const double* src, double* dst)
     if (!ctx) return set_error(RVK_ERR_INVALID, "null context");
     if (n < 0) return set_error(RVK_ERR_INVALID, "negative length");
     if (n == 0 || src == dst) return RVK_OK;
+    RVK_TRACE_TASK(ctx, "rvk_copy");
     RVK_CUDA(cudaMemcpyAsync(dst, src, (size_t)n * sizeof(double), cudaMemcpyDeviceToDevice,
                              ctx->stream));
     return RVK_OK;
@@ -313,6 +323,7 @@ rvk_status rvk_scalar_eval(rvk_ctx ctx, rvk_scalar s, double* out_dev)
     if (s.kind != RVK_SCALAR_CONST && !s.p0) return set_error(RVK_ERR_INVALID, "null scalar ptr");
     if (s.kind == RVK_SCALAR_DIV_PTR_PTR && !s.p1)
         return set_error(RVK_ERR_INVALID, "null scalar divisor ptr");
+    RVK_TRACE_TASK(ctx, "rvk_scalar_eval");
     k_scalar_eval<<<1, 1, 0, ctx->stream>>>(s, out_dev);
     RVK_CHECK_LAUNCH("k_scalar_eval");
     return RVK_OK;

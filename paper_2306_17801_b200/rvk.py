@@ -31,7 +31,10 @@ CG_RUNNING, CG_CONVERGED, CG_BREAKDOWN, CG_COMM_ERROR = 0, 1, 2, 3
 EXPORTS = [
     "rvk_last_error", "rvk_abi_version", "rvk_device_info", "rvk_device_count", "rvk_set_device",
     "rvk_ctx_create", "rvk_ctx_destroy", "rvk_ctx_stream", "rvk_ctx_synchronize",
-    "rvk_ctx_query_idle", "rvk_ctx_wait_for", "rvk_host_sync_count", "rvk_host_sync_reset",
+    "rvk_ctx_query_idle", "rvk_ctx_wait_for", "rvk_ctx_id", "rvk_ctx_set_name",
+    "rvk_host_sync_count", "rvk_host_sync_reset",
+    "rvk_trace_enable", "rvk_trace_enabled", "rvk_trace_clear", "rvk_trace_marker", "rvk_trace_count",
+    "rvk_trace_write_jsonl", "rvk_trace_write_chrome",
     "rvk_malloc", "rvk_free", "rvk_malloc_async", "rvk_free_async", "rvk_host_alloc", "rvk_host_free", "rvk_memcpy_h2d",
     "rvk_memcpy_d2h", "rvk_memcpy_d2d", "rvk_scalar_eval", "rvk_scalar_read",
     "rvk_dot", "rvk_nrm2", "rvk_dot2", "rvk_axpy", "rvk_aypx", "rvk_waxpy", "rvk_scale",
@@ -119,7 +122,16 @@ def lib():
         "rvk_ctx_synchronize": (i, [vp]),
         "rvk_ctx_query_idle": (i, [vp, C.POINTER(C.c_int)]),
         "rvk_ctx_wait_for": (i, [vp, vp]),
+        "rvk_ctx_id": (C.c_uint64, [vp]),
+        "rvk_ctx_set_name": (i, [vp, C.c_char_p]),
         "rvk_host_sync_count": (C.c_uint64, []),
+        "rvk_trace_enable": (None, [i]),
+        "rvk_trace_enabled": (i, []),
+        "rvk_trace_clear": (None, []),
+        "rvk_trace_marker": (None, [C.c_char_p]),
+        "rvk_trace_count": (C.c_size_t, []),
+        "rvk_trace_write_jsonl": (i, [C.c_char_p]),
+        "rvk_trace_write_chrome": (i, [C.c_char_p]),
         "rvk_host_sync_reset": (None, []),
         "rvk_malloc": (i, [C.POINTER(vp), C.c_size_t]),
         "rvk_free": (i, [vp]),
@@ -205,6 +217,46 @@ def host_syncs() -> int:
     return int(lib().rvk_host_sync_count())
 
 
+class trace:
+    """rvk_trace_* (reference trace.hpp:11-46): Task / Wait / HostSync /
+    Marker events, device-timed tasks, JSONL and Chrome-trace export."""
+
+    @staticmethod
+    def enable(on: bool = True):
+        lib().rvk_trace_enable(1 if on else 0)
+
+    @staticmethod
+    def enabled() -> bool:
+        return bool(lib().rvk_trace_enabled())
+
+    @staticmethod
+    def clear():
+        lib().rvk_trace_clear()
+
+    @staticmethod
+    def marker(label: str):
+        lib().rvk_trace_marker(label.encode())
+
+    @staticmethod
+    def count() -> int:
+        return int(lib().rvk_trace_count())
+
+    @staticmethod
+    def write_jsonl(path: str):
+        check(lib().rvk_trace_write_jsonl(os.fsencode(path)))
+
+    @staticmethod
+    def write_chrome(path: str):
+        check(lib().rvk_trace_write_chrome(os.fsencode(path)))
+
+    @staticmethod
+    def events(tmp_path: str) -> list:
+        import json
+        trace.write_jsonl(tmp_path)
+        with open(tmp_path) as f:
+            return [json.loads(line) for line in f if line.strip()]
+
+
 def device_info():
     n = C.c_int(0)
     name = C.create_string_buffer(128)
@@ -253,6 +305,13 @@ class Ctx:
 
     def wait_for(self, other: "Ctx"):
         check(lib().rvk_ctx_wait_for(self.h, other.h))
+
+    @property
+    def id(self) -> int:
+        return int(lib().rvk_ctx_id(self.h))
+
+    def set_name(self, name: str):
+        check(lib().rvk_ctx_set_name(self.h, name.encode()))
 
 
 class DeviceArray:

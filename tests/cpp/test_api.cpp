@@ -11,6 +11,7 @@
 #include "rivulet/runtime.hpp"
 #include "rivulet/solvers.hpp"
 #include "rivulet/stencil.hpp"
+#include "rivulet/trace.hpp"
 #include "rivulet/vector.hpp"
 
 extern "C" {
@@ -20,6 +21,7 @@ extern "C" {
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <fstream>
 #include <functional>
 #include <string>
 #include <thread>
@@ -686,6 +688,68 @@ int main()
             ++programs;
         }
         std::printf("  %d programs\n", programs);
+    });
+    run("trace: device-timed tasks, Wait edges, HostSync events, JSONL + census export (trace.hpp:11-46)", [] {
+        Context a(StreamType::DefaultBlocking, "producer"), b(StreamType::DefaultBlocking, "consumer");
+        const std::size_t n = 1 << 22;
+        DenseVector v(n);
+        Managed d;
+        a.synchronize();
+        trace::clear();
+        trace::set_enabled(true);
+        vec_set_async(v, 2.0, a);
+        vec_scale_async(v, 3.0, a);
+        vec_norm_async(v, NormType::Norm2, d, b); // RAW across contexts: one Wait edge
+        trace::marker("before front");
+        const double nv = d.front();              // host sync (traced)
+        EXPECT(rel(nv, 6.0 * std::sqrt((double)n)) < 1e-13);
+        auto evs = trace::snapshot();
+        int tasks = 0, waits = 0, syncs = 0, marks = 0;
+        std::uint64_t last_seq = 0;
+        for (const auto& e : evs) {
+            if (e.kind == trace::EventKind::Task) {
+                ++tasks;
+                EXPECT(e.enqueue_seq > last_seq); // tasks in enqueue order
+                last_seq = e.enqueue_seq;
+                EXPECT(e.device_timed);
+                EXPECT(e.t_end_ns >= e.t_start_ns);
+                EXPECT(e.context_id == a.id() || e.context_id == b.id());
+                EXPECT(e.context_name == (e.context_id == a.id() ? "producer" : "consumer"));
+            }
+            if (e.kind == trace::EventKind::Wait) {
+                ++waits;
+                EXPECT(e.context_id == b.id());
+            }
+            if (e.kind == trace::EventKind::HostSync) ++syncs;
+            if (e.kind == trace::EventKind::Marker) ++marks;
+        }
+        std::printf("  tasks=%d waits=%d host_syncs=%d markers=%d\n", tasks, waits, syncs, marks);
+        EXPECT(tasks == 3 && waits == 1 && marks == 1 && syncs >= 1);
+        // the scale on `a` ran after the set on `a`, the norm on `b` after both
+        const trace::TraceEvent* t[3];
+        int k = 0;
+        for (const auto& e : evs)
+            if (e.kind == trace::EventKind::Task) t[k++] = &e;
+        EXPECT(t[1]->t_start_ns >= t[0]->t_end_ns - 2000 && t[2]->t_start_ns >= t[1]->t_end_ns - 2000);
+        const std::string path = "/tmp/rvk_trace_test.jsonl";
+        trace::write_jsonl(path);
+        std::ifstream in(path);
+        std::string line;
+        int lines = 0;
+        while (std::getline(in, line)) {
+            EXPECT(line.front() == '{' && line.back() == '}');
+            EXPECT(line.find("\"kind\":") != std::string::npos);
+            ++lines;
+        }
+        EXPECT(lines == (int)evs.size());
+        trace::write_chrome("/tmp/rvk_trace_test.json");
+        const std::string j = runtime::to_json();
+        EXPECT(j.find("\"host_syncs\":") != std::string::npos && j.find("\"norm\":{\"kernels\":") != std::string::npos);
+        trace::set_enabled(false);
+        trace::clear();
+        vec_set_async(v, 1.0, a);
+        a.synchronize();
+        EXPECT(trace::snapshot().empty()); // off: nothing recorded
     });
     std::printf("%s: %d failure(s)\n", g_fail ? "FAILED" : "OK", g_fail);
     return g_fail ? 1 : 0;
