@@ -508,7 +508,7 @@ def strong768_single(args, stream, ctx) -> dict:
     n, nnz = A.n_rows, A.nnz
     b, x = rvk.DeviceArray(n), rvk.DeviceArray(n)
     rvk.check(rvk.lib().rvk_fill_rhs(ctx.h, 0x9E3779B97F4A7C15, n, b.ptr))
-    plan = rvk.CgPlan(ctx, A, max_it=MAX_IT, mode="fused")
+    plan = rvk.CgPlan(ctx, A, max_it=MAX_IT, mode="fused", opts=args.opts)
     fl = plan.flags()
     bm = bytes_model(n, nnz, "fused", bool(fl & 1), bool(fl & 16), bool(fl & 32),
                      MAX_IT if fl & 128 else (4 if fl & 64 else 2), bool(fl & 512))
@@ -552,7 +552,8 @@ def run_gpu(args, cfg):
     b = rvk.DeviceArray(n)
     x = rvk.DeviceArray(n)
     rvk.check(rvk.lib().rvk_fill_rhs(ctx.h, 0x9E3779B97F4A7C15, n, b.ptr))
-    plan = rvk.CgPlan(ctx, A, max_it=MAX_IT, mode=args.mode, use_graph=not args.no_graph)
+    plan = rvk.CgPlan(ctx, A, max_it=MAX_IT, mode=args.mode, use_graph=not args.no_graph,
+                      opts=args.opts)
     fl = plan.flags()
     const_diag, x_defer, z_virtual = bool(fl & 1), bool(fl & 16), bool(fl & 32)
     x_group = MAX_IT if fl & 128 else (4 if fl & 64 else 2)
@@ -714,6 +715,8 @@ def main():
     ap.add_argument("--operator", choices=["csr", "stencil"], default="csr",
                     help="csr: the AIJ/CSR operator (headline); stencil: matrix-free (SURVEY 8f)")
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--opts", type=int, default=0,
+                    help="rvk_cg_config.opts bits (include/rvk.h RVK_OPT_*), for A/B runs")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-strong", action="store_true",
                     help="skip the 768^3 strong-scaling section (BASELINE configs[4])")

@@ -251,7 +251,10 @@ typedef struct {
  *                        setup kernel (no RVK_PLAN_FOLD_SETUP)
  *   RVK_OPT_X_GROUP4     fused solve: x updated per group of 4 iterations
  *                        instead of once per solve (RVK_PLAN_X_SOLVE)
- *   RVK_OPT_X_EACH       fused solve: x updated in every iteration's K2    */
+ *   RVK_OPT_X_EACH       fused solve: x updated in every iteration's K2
+ *   RVK_OPT_MARCH        CSR plans with a plane structure: the plane-marching
+ *                        K1 (RVK_PLAN_MARCH) even for small planes
+ *   RVK_OPT_NO_MARCH     never the plane-marching K1                       */
 #define RVK_OPT_KEEP_WORK   1
 #define RVK_OPT_DINV_VECTOR 2
 #define RVK_OPT_Z_STORED    4
@@ -262,6 +265,8 @@ typedef struct {
 #define RVK_OPT_NO_FOLD     128
 #define RVK_OPT_X_GROUP4    256
 #define RVK_OPT_X_EACH      512
+#define RVK_OPT_MARCH       1024
+#define RVK_OPT_NO_MARCH    2048
 
 typedef struct {
     int state;          /* rvk_cg_state: RUNNING here means "ran max_it"     */
@@ -322,6 +327,11 @@ rvk_status rvk_cg_solve_host_many(rvk_cg_plan plan, int nrhs, const double* cons
                                    rows <= 9 entries; RVK_OPT_NO_CLUSTER disables)              */
 #define RVK_PLAN_X_SOLVE    128 /* ... one group = the whole fixed-iteration solve: x is written
                                    once, at the end (5 <= max_it <= 32, p buffers fit)          */
+#define RVK_PLAN_MARCH      1024 /* fused CSR K1 (iterations >= 1) is the plane-marching SpMV:
+                                    each SM owns an in-plane row range and walks it through
+                                    the planes, the formed gathered operand of planes k-1,
+                                    k, k+1 cached in shared memory (large 3D planes, or
+                                    RVK_OPT_MARCH; RVK_OPT_NO_MARCH disables)            */
 #define RVK_PLAN_Z_VIRTUAL  32  /* fused solve never stores z = d r (constant diagonal / no PC):
                                    the SpMV gathers r and forms d r (bit-identical;
                                    RVK_OPT_Z_STORED / RVK_OPT_Z_VIRTUAL override)               */

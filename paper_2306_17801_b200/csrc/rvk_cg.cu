@@ -30,6 +30,7 @@
 // the whole solve is one CUDA graph replayed with no host involvement.
 #include "rvk_common.cuh"
 #include "rvk_context.hpp"
+#include "rvk_spmv_march.cuh"
 #include "rvk_internal.hpp"
 #include "rvk_cg.cuh"
 #include "rvk_spmv.cuh"
@@ -564,8 +565,38 @@ rvk_status csr_bands(cudaStream_t s, const rvk_csr& A, SpmvBands* out)
         out->has_lead = true;
         out->lead_lo  = lo;
         out->lead_hi  = d.back();
+        // plane stride: the highest band's middle diagonal Q, mirrored by -Q,
+        // every other diagonal within the in-plane width of 0 or +-Q (3D
+        // stencils: Q = nx ny; the plane-marching K1's cache geometry)
+        const int64_t q = lo + (d.back() - lo) / 2;
+        const bool    has_q  = std::binary_search(d.begin(), d.end(), q);
+        const bool    has_mq = std::binary_search(d.begin(), d.end(), -q);
+        int64_t       w = 0; // in-plane half width
+        for (int64_t v : d)
+            if (v > -lo && v < lo) w = std::max<int64_t>(w, v < 0 ? -v : v);
+        if (has_q && has_mq && q % 32 == 0 && q > 2 * (w + (d.back() - lo))) out->plane_q = q;
     }
     return RVK_OK;
+}
+
+bool make_spmv_march(const rvk_csr& A, int64_t max_row_len, int64_t Q, int grid, SpmvArgs* a,
+                     SpmvMarch* M)
+{
+    if (Q <= 0 || Q % 32 != 0 || Q / 32 < grid || A.n_rows < 3 * Q) return false;
+    SpmvMarch m;
+    m.Q    = Q;
+    m.K    = (A.n_rows + Q - 1) / Q;
+    m.grid = grid;
+    m.Lmax = (int)(((Q / 32 + grid - 1) / grid) * 32);
+    const int64_t budget =
+        (int64_t)kSpmvMarchSmem - (int64_t)kSpmvHeaderBytes - (int64_t)3 * m.Lmax * 8;
+    if (budget <= 0) return false;
+    SpmvArgs s = make_spmv_args(A, max_row_len, nullptr, budget);
+    if (s.stages < 2 || s.smem_bytes() - kSpmvHeaderBytes > (size_t)budget) return false;
+    if ((int64_t)s.R * s.cap <= 0) return false;
+    *a = s;
+    *M = m;
+    return true;
 }
 
 rvk_status diag_inverse(cudaStream_t s, const rvk_csr& A, int64_t col_off, double* dinv)
@@ -618,6 +649,9 @@ struct rvk_cg_plan_s {
     rvk_csr       A{};
     rvk_cg_config cfg{};
     SpmvArgs      sa{};
+    bool          march = false;            // K1 (it >= 1) is k_spmv_march (RVK_PLAN_MARCH)
+    SpmvArgs      sa_m{};                   // ... its ring geometry
+    SpmvMarch     mg{};                     // ... and plane ranges
     int           spmv_grid = 0, upd_grid = 0, setup_grid = 0, persist_grid = 0;
     int           mode = RVK_CG_MODE_FUSED; // resolved (AUTO -> FUSED | PERSISTENT)
     int           cluster = 0;              // PERSISTENT: CTAs of the one-cluster DSMEM solve (0: grid barriers)
@@ -856,6 +890,7 @@ rvk_status launch_k1(rvk_cg_plan P, int it, bool first, const double* p_old, dou
             return launch_spmv(s, P->sa, op, ta, P->spmv_grid);
         }
         CgSpmvOp<false, true> op{P->r, p_old, p_new, P->w, P->st, n, it, 0.0, zs};
+        if (P->march) return launch_spmv_march(s, P->sa_m, P->mg, op, ta);
         return launch_spmv(s, P->sa, op, ta, P->spmv_grid);
     }
     if (first) {
@@ -863,6 +898,7 @@ rvk_status launch_k1(rvk_cg_plan P, int it, bool first, const double* p_old, dou
         return launch_spmv(s, P->sa, op, ta, P->spmv_grid);
     }
     CgSpmvOp<false> op{P->z, p_old, p_new, P->w, P->st, n, it, 0.0};
+    if (P->march) return launch_spmv_march(s, P->sa_m, P->mg, op, ta);
     return launch_spmv(s, P->sa, op, ta, P->spmv_grid);
 }
 
@@ -1320,6 +1356,11 @@ rvk_status rvk_cg_plan_create(rvk_ctx ctx, const rvk_csr* A, rvk_cg_config cfg, 
     P->sa            = make_spmv_args(*A, maxlen, &bands);
     P->sa.small_rows = (cfg.opts & RVK_OPT_SMALL_K1) ? 512 * 1024 : 0;
     P->spmv_grid = sm_count();
+    // plane-marching K1 for large 3D planes (>= 512^2 rows per plane: there
+    // the row-order sweep re-reads the -plane gathers from DRAM)
+    if (!(cfg.opts & RVK_OPT_NO_MARCH) && bands.plane_q > 0 &&
+        (bands.plane_q >= (int64_t)512 * 512 || (cfg.opts & RVK_OPT_MARCH)))
+        P->march = make_spmv_march(*A, maxlen, bands.plane_q, P->spmv_grid, &P->sa_m, &P->mg);
     // one resident wave each (the vectorised loops take 2 elements per thread)
     P->upd_grid   = resident_grid(k_cg_update<true, 1>, kUpdThreads, (A->n_rows + 1) / 2);
     P->setup_grid = resident_grid(k_cg_setup<true, 1>, kUpdThreads, (A->n_rows + 1) / 2);
@@ -1402,7 +1443,8 @@ int rvk_cg_plan_flags(rvk_cg_plan P)
            ((P->mode == RVK_CG_MODE_FUSED && x_defer(P, true) && P->xq > 4) ? RVK_PLAN_X_SOLVE : 0) |
            ((P->mode == RVK_CG_MODE_PERSISTENT && P->cluster) ? RVK_PLAN_CLUSTER : 0) |
            (fold_setup(P, nullptr) ? RVK_PLAN_FOLD_SETUP : 0) |
-           (P->zv ? RVK_PLAN_Z_VIRTUAL : 0);
+           (P->zv ? RVK_PLAN_Z_VIRTUAL : 0) |
+           ((P->march && !P->stencil && P->mode != RVK_CG_MODE_PERSISTENT) ? RVK_PLAN_MARCH : 0);
 }
 
 const double* rvk_cg_plan_vector(rvk_cg_plan P, int which)

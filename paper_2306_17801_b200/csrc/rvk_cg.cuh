@@ -106,6 +106,16 @@ struct CgSpmvOp {
         w[i]           = sum;
         return add(acc, mul(p, sum));
     }
+    // k_spmv_march: a cached (already formed) gathered value rides in a Fetch
+    static __device__ __forceinline__ Fetch  from_formed(double p) { return Fetch{p, 0.0}; }
+    static __device__ __forceinline__ double formed(const Fetch& f) { return f.z; }
+    // the same epilogue with p_new[i] already formed (k_spmv_march's cache)
+    __device__ __forceinline__ double row_p(int64_t i, double sum, double acc, double p) const
+    {
+        p_new[i] = p;
+        w[i]     = sum;
+        return add(acc, mul(p, sum));
+    }
     __device__ __forceinline__ void tail(double pAp) const
     {
         const double a = st->beta / pAp;

@@ -54,6 +54,7 @@ constexpr int    kSpmvUnroll        = 8;                   // default nonzeros p
 #endif
 constexpr size_t kSpmvHeaderBytes   = 2048;                // barriers, meta, reduction scratch
 constexpr size_t kSpmvStageBudget   = 200 * 1024;          // dynamic smem for the ring
+constexpr size_t kSpmvMarchSmem     = 227 * 1024;          // k_spmv_march: cache + ring (sm_100 max)
 
 struct SpmvStageMeta {
     int64_t kv0;    // first value index held in the stage (16-B aligned)
@@ -69,6 +70,7 @@ static_assert(kSpmvMaxStages * sizeof(SpmvStageMeta) <= 512 - 128, "meta must fi
 struct SpmvBands {
     bool    has_lead = false;
     int64_t lead_lo = 0, lead_hi = 0;
+    int64_t plane_q = 0; // > 0: diagonals +-Q bound two plane bands (3D stencil), Q % 32 == 0
 };
 
 struct SpmvArgs {
@@ -105,7 +107,8 @@ __host__ __device__ inline int align16(int64_t b) { return (int)((b + 15) & ~int
 // (CSR rows of max_row_len) fits a stage with >= 3 stages in the ring (else
 // 2).  Rows too long for any stage still work (direct tiles).  B: the
 // leading diagonal band to L2-prefetch (null: none).
-inline SpmvArgs make_spmv_args(const rvk_csr& A, int64_t max_row_len, const SpmvBands* B = nullptr)
+inline SpmvArgs make_spmv_args(const rvk_csr& A, int64_t max_row_len, const SpmvBands* B = nullptr,
+                               int64_t stage_budget = (int64_t)kSpmvStageBudget)
 {
     if (max_row_len < 1) max_row_len = 1;
     SpmvArgs a{};
@@ -121,7 +124,7 @@ inline SpmvArgs make_spmv_args(const rvk_csr& A, int64_t max_row_len, const Spmv
         // values of a batch overrun into the column region)
         const int64_t ob = align16((int64_t)(R + 2) * 8), vb = cap * 8, cb = align16(cap * 4 + 48);
         const int64_t sb = ob + vb + cb;
-        const int64_t st = std::min<int64_t>(kSpmvMaxStages, (int64_t)kSpmvStageBudget / sb);
+        const int64_t st = std::min<int64_t>(kSpmvMaxStages, stage_budget / sb);
         if (st < min_stages) return false;
         a.R = R;
         a.stages = (int)st;

@@ -1,0 +1,309 @@
+// rvk_spmv_march.cuh -- plane-marching CSR SpMV for large 3D stencil grids.
+//
+// Same row sums as k_spmv_tma (kernels_scalar.cpp:53-63 order, each product
+// rounded before it is added: bit-identical), different tile order and a
+// shared-memory cache of the gathered operand.
+//
+// Why: in row order the grid sweeps z-planes with the whole chip, so a
+// gathered value is used three times one plane of streamed bytes apart (as
+// the +plane neighbour, as the row's own plane, as the -plane neighbour).
+// At 768^3 two planes of streamed CSR (146 MB) exceed the 126 MB L2 and the
+// -plane gathers come back from DRAM: +13% traffic (profiles/
+// r01_plane_study.md), and every gathered nonzero is an L2 request.
+//
+// Here CTA g owns the in-plane row range [a_g, a_g + L_g) (Q rows per plane,
+// split into 148 contiguous ranges) and marches it through the planes
+// k = 0 .. K-1 (tiles of <= R rows of plane k, TMA-staged exactly like
+// k_spmv_tma).  The CTA keeps the FORMED gathered value p_j (for the CG K1:
+// p = z + b p_old, the same single rounding every gather would compute) of
+// its range for planes k-1, k and k+1 in a 3-slot shared-memory ring:
+//   * the thread of row i = kQ + a + o loads z/p_old at i + Q (the +plane
+//     element at its own offset, a coalesced first-touch DRAM read that the
+//     producer L2-prefetched one tile ahead), forms p and stores it in slot
+//     (k+1) % 3 -- every slot entry is written by exactly one thread;
+//   * a gathered column inside the CTA's range of plane k or k-1 is read from
+//     its slot (LDS), the row's own +plane column from the register, anything
+//     else (range halos, far columns of a general CSR) from global memory;
+//   * one consumer barrier per plane step orders the slot writes of step k
+//     before the reads of steps k+1 and k+2.
+// Correctness needs no stencil structure (a miss is a global gather); the
+// structure only decides the hit rate.  DRAM sees every gathered value once.
+#pragma once
+
+#include "rvk_spmv.cuh"
+
+namespace rvk {
+
+struct SpmvMarch {
+    int64_t Q;     // rows per plane (a multiple of 32)
+    int64_t K;     // planes (ceil(n / Q))
+    int     Lmax;  // largest CTA range (rows; multiple of 32)
+    int     grid;  // CTAs (ranges)
+    size_t  smem_bytes(const SpmvArgs& a) const
+    {
+        return kSpmvHeaderBytes + (size_t)3 * Lmax * 8 + (size_t)a.stages * a.stage_bytes;
+    }
+};
+
+// CTA g's range of in-plane rows: [a, a + L), 32-row aligned.
+__host__ __device__ inline void march_range(const SpmvMarch& M, int g, int64_t* a, int* L)
+{
+    const int64_t q32 = M.Q / 32;
+    const int64_t b0 = q32 * g / M.grid, b1 = q32 * (g + 1) / M.grid;
+    *a = b0 * 32;
+    *L = (int)((b1 - b0) * 32);
+}
+
+// Row tile t of plane k for a CTA with range [a, a + L): rows [r0, r1).
+__device__ __forceinline__ void march_tile(const SpmvArgs& A, const SpmvMarch& M, int64_t a, int L,
+                                           int64_t k, int t, int64_t* r0, int64_t* r1)
+{
+    const int64_t base = k * M.Q + a;
+    *r0                = base + (int64_t)t * A.R;
+    *r1                = min(min(*r0 + A.R, base + L), A.n_rows);
+    if (*r0 > A.n_rows) *r0 = A.n_rows;
+}
+
+// One row of plane k: gathers classified against the slot ring.
+//   Ck / Cm : slots of planes k and k-1 (index = column - (kQ + a) [+ Q])
+//   Cn      : slot of plane k+1 (this row stores its own +plane value there)
+// Row and column indices fit 32 bits (int32 columns), so the classification
+// runs in 32-bit arithmetic.  A cache hit is carried in the op's Fetch slot
+// (Op::from_formed / Op::formed) so hits and misses share registers: the
+// LDS of a hit and the LDG of a miss are predicated alternatives.
+template <int U, class Op, class Acc, class ColF, class ValF>
+__device__ __forceinline__ Acc march_row(const Op& op, Acc acc, int i, int base, int L, int Q, int n,
+                                         const double* Ck, const double* Cm, double* Cn, int kb,
+                                         int ke, ColF col, ValF val)
+{
+    const int o = i - base; // offset in the range, 0 <= o < L
+    // own +plane element (first touch in DRAM): formed once, cached for the
+    // next two steps, and used directly if this row gathers it
+    double pq = 0.0;
+    if (i < n - Q) {
+        pq    = op.value(op.fetch(i + Q));
+        Cn[o] = pq;
+    }
+    double sum = 0.0;
+    for (int k = kb; k < ke; k += U) {
+        typename Op::Fetch f[U];
+        unsigned           miss = 0;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int c   = k + u < ke ? col(k + u) : i; // past the row's end: a harmless slot
+            const int rel = c - base;
+            if ((unsigned)rel < (unsigned)L) f[u] = Op::from_formed(Ck[rel]);
+            else if ((unsigned)(rel + Q) < (unsigned)L) f[u] = Op::from_formed(Cm[rel + Q]);
+            else if (rel - Q == o) f[u] = Op::from_formed(pq);
+            else {
+                f[u] = op.fetch(c);
+                miss |= 1u << u;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const double v = (miss >> u) & 1u ? op.value(f[u]) : Op::formed(f[u]);
+            const double t = add(sum, mul(val(k + u), v));
+            sum            = k + u < ke ? t : sum;
+        }
+    }
+    return op.row_p(i, sum, acc, Ck[o]);
+}
+
+template <class Op, int U>
+__global__ void __launch_bounds__(kSpmvThreads, 1)
+    k_spmv_march(SpmvArgs A, SpmvMarch M, Op op_in, TailArgs tail)
+{
+    const int64_t* __restrict__ OFF = A.off;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    uint64_t*      full   = reinterpret_cast<uint64_t*>(smem_raw);
+    uint64_t*      empty  = full + kSpmvMaxStages;
+    SpmvStageMeta* meta   = reinterpret_cast<SpmvStageMeta*>(smem_raw + 128);
+    double*        red    = reinterpret_cast<double*>(smem_raw + 512);
+    int*           flag   = reinterpret_cast<int*>(smem_raw + 512 + 1024);
+    double*        cache  = reinterpret_cast<double*>(smem_raw + kSpmvHeaderBytes);
+    unsigned char* stage0 = smem_raw + kSpmvHeaderBytes + (size_t)3 * M.Lmax * 8;
+
+    Op op = op_in;
+    if (!op.init()) return;
+
+    int64_t a;
+    int     L;
+    march_range(M, blockIdx.x, &a, &L);
+    const int T = (L + A.R - 1) / A.R; // tiles per plane step
+
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        for (int s = 0; s < A.stages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], (A.consumers / 32) / A.groups);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    if (tid < 32) {
+        // ===================== producer warp =====================
+        if (tid == 0) {
+            const uint64_t pol_stream = policy_evict_first();
+            int            j          = 0;
+            for (int64_t k = 0; k < M.K; ++k) {
+                for (int t = 0; t < T; ++t, ++j) {
+                    const int s = j % A.stages;
+                    if (j >= A.stages) mbar_wait(&empty[s], ((j / A.stages) - 1) & 1);
+                    int64_t r0, r1;
+                    march_tile(A, M, a, L, k, t, &r0, &r1);
+                    SpmvStageMeta& m = meta[s];
+                    // offsets of R + 2 rows (16-B multiple) must stay inside
+                    // off[0..n]; the matrix's last tile is direct (rounded
+                    // value / column ranges could pass nnz)
+                    const bool direct = r1 >= A.n_rows || r0 + A.R + 2 > A.n_rows + 1;
+                    int64_t    ck0 = 0, ck1 = 0;
+                    if (!direct) {
+                        ck0 = (int64_t)__ldg(OFF + r0);
+                        ck1 = (int64_t)__ldg(OFF + r1);
+                    }
+                    const int64_t kv0 = ck0 & ~int64_t(1), kv1 = (ck1 + 1) & ~int64_t(1);
+                    const int64_t kc0 = ck0 & ~int64_t(3), kc1 = (ck1 + 3) & ~int64_t(3);
+                    const bool    dir = direct || (kv1 - kv0) > A.cap || (kc1 - kc0) > A.cap;
+                    m.kv0             = kv0;
+                    m.kc0             = kc0;
+                    m.direct          = dir ? 1 : 0;
+                    if (dir) {
+                        mbar_arrive(&full[s]);
+                    } else {
+                        unsigned char* st = stage0 + (size_t)s * A.stage_bytes;
+                        const uint32_t ob = (uint32_t)((A.R + 2) * 8);
+                        const uint32_t vb = (uint32_t)((kv1 - kv0) * 8);
+                        const uint32_t cb = (uint32_t)((kc1 - kc0) * 4);
+                        mbar_arrive_expect_tx(&full[s], ob + vb + cb);
+                        bulk_g2s(st, OFF + r0, ob, &full[s], pol_stream);
+                        if (vb) bulk_g2s(st + A.off_bytes, A.vals + kv0, vb, &full[s], pol_stream);
+                        if (cb) bulk_g2s(st + A.off_bytes + A.val_bytes, A.cols + kc0, cb, &full[s], pol_stream);
+                    }
+                    // the NEXT tile's +plane elements (first-touch DRAM reads of
+                    // its rows' own-offset loads): L2 prefetch
+                    int64_t q0, q1;
+                    if (t + 1 < T) march_tile(A, M, a, L, k, t + 1, &q0, &q1);
+                    else march_tile(A, M, a, L, k + 1, 0, &q0, &q1);
+                    int64_t lo = (q0 + M.Q) & ~int64_t(1), hi = min(q1 + M.Q, A.n_cols) & ~int64_t(1);
+                    if (hi > lo) {
+                        const int nps = op.num_src();
+                        for (int p = 0; p < nps; ++p)
+                            bulk_prefetch_l2(op.src_ptr(p) + lo, (uint32_t)(hi - lo) * 8);
+                    }
+                }
+            }
+        }
+        return;
+    }
+
+    // ===================== consumer warps =====================
+    const int ctid  = tid - 32;
+    const int gs    = A.consumers / A.groups;
+    const int group = ctid / gs, gtid = ctid % gs;
+    constexpr int NS = spmv_sums<Op>::value;
+    spmv_acc_t<Op> acc{};
+
+    // prologue: plane 0 of the range into slot 0
+    for (int o = ctid; o < L; o += A.consumers) {
+        const int64_t i = a + o;
+        if (i < A.n_rows) cache[o] = op.value(op.fetch((int32_t)i));
+    }
+    asm volatile("bar.sync 2, %0;" ::"r"(A.consumers) : "memory");
+
+    int j = 0;
+    for (int64_t k = 0; k < M.K; ++k) {
+        const double* Ck   = cache + (size_t)(k % 3) * M.Lmax;
+        const double* Cm   = cache + (size_t)((k + 2) % 3) * M.Lmax;
+        double*       Cn   = cache + (size_t)((k + 1) % 3) * M.Lmax;
+        const int64_t base = k * M.Q + a;
+        for (int t = 0; t < T; ++t, ++j) {
+            if (j % A.groups != group) continue;
+            const int s = j % A.stages;
+            mbar_wait(&full[s], (j / A.stages) & 1);
+            int64_t r0, r1;
+            march_tile(A, M, a, L, k, t, &r0, &r1);
+            const int            rows = (int)(r1 - r0);
+            const SpmvStageMeta& m    = meta[s];
+            if (m.direct) {
+                const int32_t* __restrict__ Cg = A.cols;
+                const double* __restrict__ Vg  = A.vals;
+                for (int lr = gtid; lr < rows; lr += gs) {
+                    const int64_t kb = OFF[r0 + lr], ke = OFF[r0 + lr + 1];
+                    acc = march_row<U>(op, acc, (int)(r0 + lr), (int)base, L, (int)M.Q, (int)A.n_rows, Ck,
+                                       Cm, Cn, 0, (int)(ke - kb),
+                                       [&](int q) { return __ldg(Cg + kb + q); },
+                                       [&](int q) { return __ldg(Vg + kb + q); });
+                }
+            } else {
+                unsigned char* st  = stage0 + (size_t)s * A.stage_bytes;
+                const int64_t  kv0 = m.kv0;
+                const int32_t* Cc  = reinterpret_cast<const int32_t*>(st + A.off_bytes + A.val_bytes) +
+                                    (kv0 - m.kc0);
+                const int64_t* O   = reinterpret_cast<const int64_t*>(st);
+                const double*  V   = reinterpret_cast<const double*>(st + A.off_bytes);
+                for (int lr = gtid; lr < rows; lr += gs) {
+                    const int kb = (int)(O[lr] - kv0), ke = (int)(O[lr + 1] - kv0);
+                    acc = march_row<U>(op, acc, (int)(r0 + lr), (int)base, L, (int)M.Q, (int)A.n_rows, Ck,
+                                       Cm, Cn, kb, ke, [&](int q) { return Cc[q]; },
+                                       [&](int q) { return V[q]; });
+                }
+            }
+            __syncwarp();
+            if ((ctid & 31) == 0) mbar_arrive(&empty[s]);
+        }
+        // slot (k+1) complete before step k+1 reads it; slot (k-1) free
+        asm volatile("bar.sync 2, %0;" ::"r"(A.consumers) : "memory");
+    }
+
+    if constexpr (Op::kHasTail) {
+        double v[NS];
+        if constexpr (NS == 1) v[0] = acc;
+        else {
+#pragma unroll
+            for (int q = 0; q < NS; ++q) v[q] = acc.v[q];
+        }
+        block_sum<NS>(v, red, ctid, A.consumers, 1);
+        if (ctid == 0) {
+#pragma unroll
+            for (int q = 0; q < NS; ++q) tail.partials[(size_t)blockIdx.x * NS + q] = v[q];
+        }
+        if (!last_block<spmv_sys_fence<Op>::value>(tail.ticket, ctid, flag, A.consumers, 1)) return;
+        fold_partials<NS>(tail.partials, gridDim.x, v, red, ctid, A.consumers, 1);
+        if (ctid == 0) {
+            if constexpr (NS == 1) op.tail(v[0]);
+            else op.tail(v);
+            *tail.ticket = 0u;
+        }
+    }
+}
+
+// Plan-time geometry: Q = the plane stride (from the CSR's diagonals), one
+// range per SM.  Returns false when the matrix has no plane structure or the
+// cache + a ring of >= 2 stages does not fit the shared memory.
+bool make_spmv_march(const rvk_csr& A, int64_t max_row_len, int64_t Q, int grid, SpmvArgs* a,
+                     SpmvMarch* M);
+
+template <class Op>
+rvk_status launch_spmv_march(cudaStream_t stream, const SpmvArgs& a, const SpmvMarch& M,
+                             const Op& op, TailArgs tail)
+{
+    static std::atomic<uint64_t> configured{0};
+    if (device_first_use(configured)) {
+        const int smax = (int)kSpmvMarchSmem;
+        RVK_CUDA(cudaFuncSetAttribute(k_spmv_march<Op, 7>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax));
+        RVK_CUDA(cudaFuncSetAttribute(k_spmv_march<Op, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax));
+        RVK_CUDA(cudaFuncSetAttribute(k_spmv_march<Op, 9>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax));
+        device_mark_done(configured);
+    }
+    const int    th = 32 + a.consumers;
+    const size_t sm = M.smem_bytes(a);
+    if (a.unroll == 7) k_spmv_march<Op, 7><<<M.grid, th, sm, stream>>>(a, M, op, tail);
+    else if (a.unroll == 9) k_spmv_march<Op, 9><<<M.grid, th, sm, stream>>>(a, M, op, tail);
+    else k_spmv_march<Op, 8><<<M.grid, th, sm, stream>>>(a, M, op, tail);
+    RVK_CHECK_LAUNCH("k_spmv_march");
+    return RVK_OK;
+}
+
+} // namespace rvk

@@ -214,7 +214,8 @@ bool write_chrome(const std::string& path)
     for (const auto& e : ev) {
         const bool          host = e.kind == HostSync || e.kind == Marker;
         const std::uint64_t tid  = host ? 0 : e.ctx_id + 1;
-        if (!rows.count(tid))
+        // a context's row is named from any of its events that carries the name
+        if (!rows.count(tid) || (!host && !e.ctx_name.empty() && rows[tid].find('(') == std::string::npos))
             rows[tid] = host ? std::string("host")
                              : "ctx " + std::to_string(e.ctx_id) +
                                    (e.ctx_name.empty() ? "" : " (" + e.ctx_name + ")");
