@@ -663,7 +663,10 @@ def run_gpu(args, cfg):
         "roofline": {"bound": "hbm",
                      "kernel": {"fused": ("k_mf_tma (matrix-free stencil + on-the-fly AYPX + p.w)"
                                           if args.operator == "stencil" else
-                                          "k_spmv_tma<CgSpmvOp> (SpMV + on-the-fly AYPX + p.w)"),
+                                          ("k_spmv_march<CgSpmvOp> (plane-marching SpMV, smem plane "
+                                           "cache + on-the-fly AYPX + p.w; K1(0): k_spmv_tma)"
+                                           if fl & 1024 else
+                                           "k_spmv_tma<CgSpmvOp> (SpMV + on-the-fly AYPX + p.w)")),
                                 "unfused": "k_spmv_tma<SpmvGuardedOp> (SpMV)",
                                 "persistent": "k_cg_persistent / k_cg_cluster (whole solve, one launch)",
                                 "hostsync": "whole solve (host-sync baseline)"}[mode],

@@ -254,7 +254,9 @@ typedef struct {
  *   RVK_OPT_X_EACH       fused solve: x updated in every iteration's K2
  *   RVK_OPT_MARCH        CSR plans with a plane structure: the plane-marching
  *                        K1 (RVK_PLAN_MARCH) even for small planes
- *   RVK_OPT_NO_MARCH     never the plane-marching K1                       */
+ *   RVK_OPT_NO_MARCH     never the plane-marching K1
+ *   RVK_OPT_NO_GRID      PERSISTENT mode: no one-launch grid solve for mid-size
+ *                        systems (the generic grid-barrier kernel instead)   */
 #define RVK_OPT_KEEP_WORK   1
 #define RVK_OPT_DINV_VECTOR 2
 #define RVK_OPT_Z_STORED    4
@@ -267,6 +269,7 @@ typedef struct {
 #define RVK_OPT_X_EACH      512
 #define RVK_OPT_MARCH       1024
 #define RVK_OPT_NO_MARCH    2048
+#define RVK_OPT_NO_GRID     4096
 
 typedef struct {
     int state;          /* rvk_cg_state: RUNNING here means "ran max_it"     */
@@ -332,6 +335,10 @@ rvk_status rvk_cg_solve_host_many(rvk_cg_plan plan, int nrhs, const double* cons
                                     the planes, the formed gathered operand of planes k-1,
                                     k, k+1 cached in shared memory (large 3D planes, or
                                     RVK_OPT_MARCH; RVK_OPT_NO_MARCH disables)            */
+#define RVK_PLAN_GRID       2048 /* PERSISTENT / AUTO plan runs the one-launch grid solve (16 K < n <=
+                                    ~450 K rows, rows <= 9 entries): CSR in shared memory, row
+                                    vectors in registers, 2 grid barriers per iteration
+                                    (RVK_OPT_NO_GRID disables)                                  */
 #define RVK_PLAN_Z_VIRTUAL  32  /* fused solve never stores z = d r (constant diagonal / no PC):
                                    the SpMV gathers r and forms d r (bit-identical;
                                    RVK_OPT_Z_STORED / RVK_OPT_Z_VIRTUAL override)               */

@@ -565,16 +565,30 @@ rvk_status csr_bands(cudaStream_t s, const rvk_csr& A, SpmvBands* out)
         out->has_lead = true;
         out->lead_lo  = lo;
         out->lead_hi  = d.back();
-        // plane stride: the highest band's middle diagonal Q, mirrored by -Q,
-        // every other diagonal within the in-plane width of 0 or +-Q (3D
-        // stencils: Q = nx ny; the plane-marching K1's cache geometry)
-        const int64_t q = lo + (d.back() - lo) / 2;
-        const bool    has_q  = std::binary_search(d.begin(), d.end(), q);
-        const bool    has_mq = std::binary_search(d.begin(), d.end(), -q);
-        int64_t       w = 0; // in-plane half width
-        for (int64_t v : d)
-            if (v > -lo && v < lo) w = std::max<int64_t>(w, v < 0 ? -v : v);
-        if (has_q && has_mq && q % 32 == 0 && q > 2 * (w + (d.back() - lo))) out->plane_q = q;
+    }
+    // plane stride (3D stencils): split the positive diagonals at their
+    // largest gap; the upper cluster is the +plane band, Q its middle
+    // diagonal, which must be mirrored by -Q and exceed twice the widths of
+    // the in-plane and plane bands (the plane-marching K1's cache geometry)
+    std::vector<int64_t> pos;
+    for (int64_t v : d)
+        if (v > 0) pos.push_back(v);
+    if (pos.size() >= 2) {
+        size_t  cut = 0;
+        int64_t gap = pos[0];
+        for (size_t i = 1; i < pos.size(); ++i)
+            if (pos[i] - pos[i - 1] > gap) {
+                gap = pos[i] - pos[i - 1];
+                cut = i;
+            }
+        if (cut > 0) {
+            const int64_t q    = pos[cut + (pos.size() - cut) / 2];
+            const int64_t band = std::max(q - pos[cut], pos.back() - q);
+            const int64_t w    = pos[cut - 1];
+            if (std::binary_search(d.begin(), d.end(), -q) && q % 32 == 0 && q > 2 * (w + band) &&
+                pos[cut] - w > w + band)
+                out->plane_q = q;
+        }
     }
     return RVK_OK;
 }
@@ -583,20 +597,40 @@ bool make_spmv_march(const rvk_csr& A, int64_t max_row_len, int64_t Q, int grid,
                      SpmvMarch* M)
 {
     if (Q <= 0 || Q % 32 != 0 || Q / 32 < grid || A.n_rows < 3 * Q) return false;
-    SpmvMarch m;
-    m.Q    = Q;
-    m.K    = (A.n_rows + Q - 1) / Q;
-    m.grid = grid;
-    m.Lmax = (int)(((Q / 32 + grid - 1) / grid) * 32);
-    const int64_t budget =
-        (int64_t)kSpmvMarchSmem - (int64_t)kSpmvHeaderBytes - (int64_t)3 * m.Lmax * 8;
-    if (budget <= 0) return false;
-    SpmvArgs s = make_spmv_args(A, max_row_len, nullptr, budget);
-    if (s.stages < 2 || s.smem_bytes() - kSpmvHeaderBytes > (size_t)budget) return false;
-    if ((int64_t)s.R * s.cap <= 0) return false;
-    *a = s;
-    *M = m;
-    return true;
+    // the fewest ranges per CTA (passes: a smaller cache) that leave a TMA
+    // ring of >= 3 stages; else the fewest with 2
+    bool found = false;
+    for (int passes = 1; passes <= 16 && Q / 32 >= (int64_t)grid * passes; ++passes) {
+        SpmvMarch m;
+        m.Q      = Q;
+        m.K      = (A.n_rows + Q - 1) / Q;
+        m.grid   = grid;
+        m.passes = passes;
+        m.Lmax   = (int)(((Q / 32 + (int64_t)grid * passes - 1) / ((int64_t)grid * passes)) * 32);
+        const int64_t budget =
+            (int64_t)kSpmvMarchSmem - (int64_t)kSpmvHeaderBytes - (int64_t)3 * m.Lmax * 8;
+        if (budget <= 0) continue;
+        // the stage also holds the tile's +plane z / p_old (16 B per row)
+        SpmvArgs s{};
+        for (int64_t b = budget; b > 0; b -= 4096) {
+            s = make_spmv_args(A, max_row_len, nullptr, b);
+            const int64_t sb = s.stage_bytes + (int64_t)s.R * 16;
+            if (s.stages >= 2 && (int64_t)s.stages * sb <= budget) break;
+        }
+        m.stage_bytes = s.stage_bytes + s.R * 16;
+        if (s.stages < 2 || (int64_t)s.stages * m.stage_bytes > budget) continue;
+        if (!found) {
+            *a    = s;
+            *M    = m;
+            found = true;
+        }
+        if (s.stages >= 3) {
+            *a = s;
+            *M = m;
+            return true;
+        }
+    }
+    return found;
 }
 
 rvk_status diag_inverse(cudaStream_t s, const rvk_csr& A, int64_t col_off, double* dinv)
@@ -655,6 +689,8 @@ struct rvk_cg_plan_s {
     int           spmv_grid = 0, upd_grid = 0, setup_grid = 0, persist_grid = 0;
     int           mode = RVK_CG_MODE_FUSED; // resolved (AUTO -> FUSED | PERSISTENT)
     int           cluster = 0;              // PERSISTENT: CTAs of the one-cluster DSMEM solve (0: grid barriers)
+    int           grid_rpc = 0, grid_ctas = 0; // PERSISTENT: the one-launch grid solve (k_cg_grid), rows per CTA
+    unsigned*     gbar = nullptr;            // ... its arrival counter
     int           maxlen  = 0;              // longest row
     bool          k2_last = false;          // enqueue_fused: the K2 being launched is the solve's last
     bool          stencil = false;          // matrix-free operator (rvk_cg_plan_create_stencil)
@@ -1141,6 +1177,9 @@ rvk_status enqueue_persistent(rvk_cg_plan P, const double* b, double* x)
     P->launches = 1;
     if (P->cluster)
         return launch_cluster(P->ctx->stream, a, P->cfg.pc == RVK_PC_JACOBI, P->cluster, P->maxlen);
+    if (P->grid_rpc)
+        return launch_grid_solve(P->ctx->stream, a, P->gbar, P->cfg.pc == RVK_PC_JACOBI, P->grid_rpc,
+                                 P->grid_ctas, P->maxlen);
     return launch_persistent(P->ctx->stream, a, P->cfg.pc == RVK_PC_JACOBI, P->persist_grid);
 }
 
@@ -1367,12 +1406,16 @@ rvk_status rvk_cg_plan_create(rvk_ctx ctx, const rvk_csr* A, rvk_cg_config cfg, 
     P->persist_grid = persistent_grid(A->n_rows);
     P->mode         = cfg.mode;
     P->maxlen = (int)std::min<int64_t>(maxlen, 1 << 30);
-    if (cfg.mode == RVK_CG_MODE_AUTO || cfg.mode == RVK_CG_MODE_PERSISTENT)
+    if (cfg.mode == RVK_CG_MODE_AUTO || cfg.mode == RVK_CG_MODE_PERSISTENT) {
         P->cluster = (cfg.opts & RVK_OPT_NO_CLUSTER) ? 0 : cluster_ctas(A->n_rows, maxlen);
+        if (!P->cluster && !(cfg.opts & RVK_OPT_NO_GRID))
+            P->grid_rpc = grid_solve_rows(A->n_rows, maxlen, &P->grid_ctas);
+    }
     if (cfg.mode == RVK_CG_MODE_AUTO) {
         // up to 16 K rows: the one-cluster DSMEM solve (one launch, cluster
-        // barriers); above, the HBM-streaming fused graph
-        P->mode = P->cluster ? RVK_CG_MODE_PERSISTENT : RVK_CG_MODE_FUSED;
+        // barriers); up to ~450 K rows the one-launch grid solve (grid
+        // barriers, CSR in shared memory); above, the HBM-streaming fused graph
+        P->mode = (P->cluster || P->grid_rpc) ? RVK_CG_MODE_PERSISTENT : RVK_CG_MODE_FUSED;
         // and up to 512 K rows the plain-block K1 (k_spmv_small: 256^2 5-point
         // solve 0.229 -> 0.211 ms; explicit FUSED keeps the TMA kernel unless
         // RVK_OPT_SMALL_K1 asks)
@@ -1398,6 +1441,7 @@ rvk_status rvk_cg_plan_create(rvk_ctx ctx, const rvk_csr* A, rvk_cg_config cfg, 
     alloc(reinterpret_cast<void**>(&P->partials), sizeof(double) * 4 * kMaxReduceBlocks);
     alloc(reinterpret_cast<void**>(&P->tickets), 16 * sizeof(unsigned int));
     alloc(reinterpret_cast<void**>(&P->tmp), 16 * sizeof(double));
+    alloc(reinterpret_cast<void**>(&P->gbar), 16 * sizeof(unsigned));
     if (e != cudaSuccess) {
         rvk_cg_plan_destroy(P);
         return cuda_error(e, "rvk_cg_plan_create: allocation");
@@ -1442,6 +1486,7 @@ int rvk_cg_plan_flags(rvk_cg_plan P)
            ((P->mode == RVK_CG_MODE_FUSED && x_defer(P, true) && P->xq == 4) ? RVK_PLAN_X_GROUP4 : 0) |
            ((P->mode == RVK_CG_MODE_FUSED && x_defer(P, true) && P->xq > 4) ? RVK_PLAN_X_SOLVE : 0) |
            ((P->mode == RVK_CG_MODE_PERSISTENT && P->cluster) ? RVK_PLAN_CLUSTER : 0) |
+           ((P->mode == RVK_CG_MODE_PERSISTENT && P->grid_rpc) ? RVK_PLAN_GRID : 0) |
            (fold_setup(P, nullptr) ? RVK_PLAN_FOLD_SETUP : 0) |
            (P->zv ? RVK_PLAN_Z_VIRTUAL : 0) |
            ((P->march && !P->stencil && P->mode != RVK_CG_MODE_PERSISTENT) ? RVK_PLAN_MARCH : 0);
@@ -1534,7 +1579,7 @@ rvk_status rvk_cg_plan_destroy(rvk_cg_plan P)
     if (P->s_out) cudaStreamDestroy(P->s_out);
     void* bufs[] = {P->dinv, P->r, P->z, P->w, P->hist, P->st,
                     P->partials, P->tickets, P->tmp, P->b_buf, P->x_buf, P->b_buf2,
-                    P->x_buf2, P->hist_all, P->st_all};
+                    P->x_buf2, P->hist_all, P->st_all, P->gbar};
     for (void* b : bufs)
         if (b) cudaFree(b);
     for (double* b : P->p)

@@ -108,6 +108,7 @@ struct CgSpmvOp {
     }
     // k_spmv_march: a cached (already formed) gathered value rides in a Fetch
     static __device__ __forceinline__ Fetch  from_formed(double p) { return Fetch{p, 0.0}; }
+    static __device__ __forceinline__ Fetch  raw(double z, double p) { return Fetch{z, p}; }
     static __device__ __forceinline__ double formed(const Fetch& f) { return f.z; }
     // the same epilogue with p_new[i] already formed (k_spmv_march's cache)
     __device__ __forceinline__ double row_p(int64_t i, double sum, double acc, double p) const
@@ -180,6 +181,11 @@ rvk_status launch_persistent(cudaStream_t s, const PersistArgs& args, bool jacob
 // one-cluster DSMEM solve (rvk_cg_small.cu): cluster size or 0 (not eligible)
 int        cluster_ctas(int64_t n, int64_t max_row_len);
 rvk_status launch_cluster(cudaStream_t s, const PersistArgs& args, bool jacobi, int ctas, int max_row_len);
+// one-launch grid solve for mid-size grids (rvk_cg_small.cu): rows per CTA or
+// 0 (not eligible); bar = a plan-owned arrival counter (zeroed per launch)
+int        grid_solve_rows(int64_t n, int64_t max_row_len, int* ctas);
+rvk_status launch_grid_solve(cudaStream_t s, const PersistArgs& args, unsigned* bar, bool jacobi,
+                             int rpc, int ctas, int max_row_len);
 
 // After the last iteration (or an early exit): apply the updates DEFER K2s
 // left pending, in iteration order: x = ((x + a_0 p_0) + a_1 p_1) + ... .

@@ -362,6 +362,214 @@ __global__ void __launch_bounds__(kCRows, 1) k_cg_cluster(PersistArgs a)
     cl.sync(); // no CTA leaves while a neighbour may still address its shared memory
 }
 
+
+// ---------------------------------------------------------------------------
+// Grid solve for mid-size L2-resident grids (16 K < n <= ~450 K rows): the
+// whole solve in ONE cooperative launch of <= 148 CTAs x 1024 threads, R
+// rows per thread.  Each CTA keeps its rows' CSR in shared memory (ELL
+// layout, loaded once), and x, r, z, p and the Jacobi diagonal of its rows in
+// registers for the whole solve; only the gathered operands z and p travel
+// through global memory (L2).  Two grid barriers per iteration, each fused
+// with its reduction: a CTA stores its block partial, releases a monotonic
+// arrival counter and spins on it; then EVERY CTA folds the G partials in
+// the same fixed order (lane l sums blocks l, l+32, ... ascending, then a
+// shuffle tree), so all CTAs derive bit-identical scalars and exit together.
+// Element arithmetic is the reference's (mul-then-add, same operand order),
+// p is formed per gathered entry as in the fused K1.  Replaces the 41
+// launches of the fused graph, whose ~5 us per launch floor bounds 256^2 -
+// 512^2 solves.
+constexpr int kGThreads = 1024;
+constexpr int kGMaxR    = 3;   // rows per thread
+constexpr int kGMaxCta  = 148;
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p)
+{
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Block-sum v, publish, grid barrier #`index`, fold every CTA's partials.
+template <int NV>
+__device__ __forceinline__ void grid_reduce(double (&v)[NV], double* partials, unsigned* bar,
+                                            unsigned target, double* red, double* out_sh)
+{
+    const int tid = threadIdx.x;
+    block_sum<NV>(v, red, tid, kGThreads, 1);
+    if (tid == 0) {
+#pragma unroll
+        for (int j = 0; j < NV; ++j) partials[blockIdx.x * 4 + j] = v[j];
+        __threadfence();
+        atomicAdd(bar, 1u);
+        while (ld_acquire_u32(bar) < target) {
+        }
+    }
+    __syncthreads();
+    if (tid < 32) {
+        double f[NV];
+#pragma unroll
+        for (int j = 0; j < NV; ++j) f[j] = 0.0;
+        for (int blk = tid; blk < (int)gridDim.x; blk += 32) {
+#pragma unroll
+            for (int j = 0; j < NV; ++j) f[j] = add(f[j], __ldcg(partials + blk * 4 + j));
+        }
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+            f[j] = warp_sum(f[j]);
+            if (tid == 0) out_sh[j] = f[j];
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < NV; ++j) v[j] = out_sh[j];
+    __syncthreads(); // out_sh reusable
+}
+
+template <bool JACOBI, int NZ, int R>
+__global__ void __launch_bounds__(kGThreads, 1)
+    k_cg_grid(PersistArgs a, unsigned* bar, int rpc)
+{
+    extern __shared__ __align__(16) unsigned char gsm[];
+    double*  ev   = reinterpret_cast<double*>(gsm);                   // [rpc][NZ] values
+    int32_t* ec   = reinterpret_cast<int32_t*>(ev + (size_t)rpc * NZ); // [rpc][NZ] columns
+    uint8_t* ecnt = reinterpret_cast<uint8_t*>(ec + (size_t)rpc * NZ); // [rpc] row lengths
+    __shared__ double red[128], out_sh[4];
+    const int     tid  = threadIdx.x;
+    const bool    lead = blockIdx.x == 0 && tid == 0;
+    const int64_t r0   = (int64_t)blockIdx.x * rpc;
+    unsigned      nbar = 0; // barriers passed
+    const unsigned G   = gridDim.x;
+
+    // this CTA's rows into shared memory (ELL, row order kept)
+    for (int j = tid; j < rpc; j += kGThreads) {
+        const int64_t i = r0 + j;
+        int           c = 0;
+        if (i < a.n) {
+            const int64_t kb = a.off[i], ke = a.off[i + 1];
+            c                = (int)(ke - kb);
+            for (int k = 0; k < c; ++k) {
+                ev[(size_t)j * NZ + k] = a.vals[kb + k];
+                ec[(size_t)j * NZ + k] = a.cols[kb + k];
+            }
+        }
+        ecnt[j] = (uint8_t)c;
+    }
+
+    // ---- setup: r = b, x = 0, z = B r; z.z, z.r ------------------------------
+    double x[R], r[R], z[R], pv[R], d[R];
+    bool   own[R];
+    double acc[2] = {0.0, 0.0};
+#pragma unroll
+    for (int m = 0; m < R; ++m) {
+        const int     j = tid + m * kGThreads;
+        const int64_t i = r0 + j;
+        own[m]          = j < rpc && i < a.n;
+        d[m]            = (own[m] && JACOBI) ? a.dinv[i] : 1.0;
+        r[m]            = own[m] ? a.b[i] : 0.0;
+        z[m]            = JACOBI ? mul(d[m], r[m]) : r[m];
+        x[m]            = 0.0;
+        pv[m]           = 0.0;
+        if (own[m]) {
+            a.z[i] = z[m];
+            acc[0] = add(acc[0], mul(z[m], z[m]));
+            acc[1] = add(acc[1], mul(z[m], r[m]));
+        }
+    }
+    grid_reduce<2>(acc, a.partials, bar, ++nbar * G, red, out_sh); // (also publishes the smem CSR)
+    double       beta = acc[1];
+    const double dp0  = sqrt(acc[0]);
+    int          state = RVK_CG_RUNNING, iters = 0, bk = -1;
+    double       alpha = 0.0, pAp = 0.0, betaold = 0.0, dp = dp0;
+    if (cg_converged(dp0, dp0, a.rtol, a.atol)) state = RVK_CG_CONVERGED;
+
+    for (int it = 0; it < a.max_it && state == RVK_CG_RUNNING; ++it) {
+        // ---- w = A p, p = z + b p_old formed per gathered entry ---------------
+        double bb = 0.0;
+        if (it > 0) {
+            if (betaold == 0.0) {
+                state = RVK_CG_BREAKDOWN;
+                bk    = it;
+                break;
+            }
+            bb = beta / betaold;
+        }
+        const double* po = (it & 1) ? a.p1 : a.p0;
+        double*       pn = (it & 1) ? a.p0 : a.p1;
+        double        w[R];
+        double        pw = 0.0;
+#pragma unroll
+        for (int m = 0; m < R; ++m) {
+            w[m] = 0.0;
+            if (!own[m]) continue;
+            const int j   = tid + m * kGThreads;
+            const int cnt = ecnt[j];
+            double    zj[NZ], pj[NZ];
+#pragma unroll
+            for (int k = 0; k < NZ; ++k) {
+                const int32_t c = k < cnt ? ec[(size_t)j * NZ + k] : 0;
+                zj[k]           = __ldcg(a.z + c);
+                pj[k]           = it == 0 ? 0.0 : __ldcg(po + c);
+            }
+#pragma unroll
+            for (int k = 0; k < NZ; ++k)
+                if (k < cnt)
+                    w[m] = add(w[m], mul(ev[(size_t)j * NZ + k], it == 0 ? zj[k] : aypx1(bb, zj[k], pj[k])));
+            pv[m] = it == 0 ? z[m] : aypx1(bb, z[m], pv[m]);
+            pn[r0 + j] = pv[m];
+            pw = add(pw, mul(pv[m], w[m]));
+        }
+        double v1[1] = {pw};
+        grid_reduce<1>(v1, a.partials, bar, ++nbar * G, red, out_sh);
+        pAp             = v1[0];
+        const double al = beta / pAp;
+        if (pAp == 0.0 || !isfinite(al)) {
+            state = RVK_CG_BREAKDOWN;
+            bk    = it;
+            break;
+        }
+        alpha   = al;
+        betaold = beta;
+        // ---- x += a p, r += (-a) w, z = B r; z.z, z.r ------------------------
+        acc[0] = acc[1] = 0.0;
+#pragma unroll
+        for (int m = 0; m < R; ++m) {
+            if (!own[m]) continue;
+            x[m] = axpy1(al, pv[m], x[m]);
+            r[m] = axpy1(-al, w[m], r[m]);
+            z[m] = JACOBI ? mul(d[m], r[m]) : r[m];
+            a.z[r0 + tid + m * kGThreads] = z[m];
+            acc[0] = add(acc[0], mul(z[m], z[m]));
+            acc[1] = add(acc[1], mul(z[m], r[m]));
+        }
+        grid_reduce<2>(acc, a.partials, bar, ++nbar * G, red, out_sh);
+        dp    = sqrt(acc[0]);
+        iters = it + 1;
+        if (lead) a.hist[it + 1] = dp;
+        if (cg_converged(dp, dp0, a.rtol, a.atol)) state = RVK_CG_CONVERGED;
+        beta = acc[1];
+    }
+#pragma unroll
+    for (int m = 0; m < R; ++m)
+        if (own[m]) {
+            const int64_t i = r0 + tid + m * kGThreads;
+            a.x[i]          = x[m];
+            a.r[i]          = r[m];
+        }
+    if (lead) {
+        a.hist[0]            = dp0;
+        a.st->dp0            = dp0;
+        a.st->dp             = dp;
+        a.st->alpha          = alpha;
+        a.st->pAp            = pAp;
+        a.st->beta           = beta;
+        a.st->betaold        = betaold;
+        a.st->iterations     = iters;
+        a.st->breakdown_iter = bk;
+        a.st->state          = state;
+        a.st->done           = 1;
+    }
+}
+
 } // namespace
 
 int persistent_grid(int64_t n)
@@ -432,6 +640,51 @@ rvk_status launch_persistent(cudaStream_t s, const PersistArgs& args, bool jacob
     const void* fn = jacobi ? (const void*)k_cg_persistent<true> : (const void*)k_cg_persistent<false>;
     RVK_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kPThreads), kargs, 0, s));
     return RVK_OK;
+}
+
+} // namespace rvk
+
+namespace rvk {
+
+// Grid-solve geometry: rows per CTA (32-aligned) and CTAs, or 0 when the
+// system does not qualify (rows > 9 entries, more than 148 x 3 x 1024 rows,
+// or the ELL rows do not fit the shared memory).
+int grid_solve_rows(int64_t n, int64_t max_row_len, int* ctas)
+{
+    if (n < 1 || max_row_len > kCMaxNnz) return 0;
+    const int     nz  = max_row_len <= 5 ? 5 : (max_row_len <= 7 ? 7 : 9);
+    const int64_t rpc = ((n + kGMaxCta - 1) / kGMaxCta + 31) / 32 * 32;
+    if (rpc > (int64_t)kGMaxR * kGThreads) return 0;
+    const size_t smem = (size_t)rpc * nz * 12 + rpc;
+    if (smem > 220 * 1024) return 0;
+    *ctas = (int)((n + rpc - 1) / rpc);
+    return (int)rpc;
+}
+
+rvk_status launch_grid_solve(cudaStream_t s, const PersistArgs& args, unsigned* bar, bool jacobi,
+                             int rpc, int ctas, int max_row_len)
+{
+    const int    nz   = max_row_len <= 5 ? 5 : (max_row_len <= 7 ? 7 : 9);
+    const int    R    = (rpc + kGThreads - 1) / kGThreads;
+    const size_t smem = (size_t)rpc * nz * 12 + rpc;
+    RVK_CUDA(cudaMemsetAsync(bar, 0, sizeof(unsigned), s));
+    void* kargs[] = {const_cast<PersistArgs*>(&args), &bar, &rpc};
+    auto go = [&](auto fn) -> rvk_status {
+        // > 48 KB dynamic shared memory: per device and instantiation (idempotent)
+        RVK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+        RVK_CUDA(cudaLaunchCooperativeKernel((const void*)fn, dim3(ctas), dim3(kGThreads), kargs, smem, s));
+        return RVK_OK;
+    };
+#define RVK_GRID_CASE(J, NZ, RR)                                                   \
+    if (jacobi == J && nz == NZ && R == RR) return go(k_cg_grid<J, NZ, RR>);
+    RVK_GRID_CASE(true, 5, 1) RVK_GRID_CASE(true, 5, 2) RVK_GRID_CASE(true, 5, 3)
+    RVK_GRID_CASE(true, 7, 1) RVK_GRID_CASE(true, 7, 2) RVK_GRID_CASE(true, 7, 3)
+    RVK_GRID_CASE(true, 9, 1) RVK_GRID_CASE(true, 9, 2) RVK_GRID_CASE(true, 9, 3)
+    RVK_GRID_CASE(false, 5, 1) RVK_GRID_CASE(false, 5, 2) RVK_GRID_CASE(false, 5, 3)
+    RVK_GRID_CASE(false, 7, 1) RVK_GRID_CASE(false, 7, 2) RVK_GRID_CASE(false, 7, 3)
+    RVK_GRID_CASE(false, 9, 1) RVK_GRID_CASE(false, 9, 2) RVK_GRID_CASE(false, 9, 3)
+#undef RVK_GRID_CASE
+    return set_error(RVK_ERR_INVALID, "grid solve: unsupported geometry (R %d, nz %d)", R, nz);
 }
 
 } // namespace rvk

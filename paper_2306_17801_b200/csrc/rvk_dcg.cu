@@ -57,6 +57,7 @@
 #include "rvk_cg.cuh"
 #include "rvk_common.cuh"
 #include "rvk_context.hpp"
+#include "rvk_spmv_march.cuh"
 #include "rvk_internal.hpp"
 #include "rvk_spmv.cuh"
 
@@ -392,10 +393,17 @@ struct DcgSpmvOp {
     }
     __device__ __forceinline__ double row(int64_t i, double sum, double acc, const Fetch& o) const
     {
-        const double p     = value(o);
-        pnew_own[i]        = p;
+        return row_p(i, sum, acc, value(o));
+    }
+    // k_spmv_march: cached (formed) gathered values ride in a Fetch
+    static __device__ __forceinline__ Fetch  from_formed(double p) { return Fetch{p, 0.0}; }
+    static __device__ __forceinline__ Fetch  raw(double z, double p) { return Fetch{z, p}; }
+    static __device__ __forceinline__ double formed(const Fetch& f) { return f.z; }
+    __device__ __forceinline__ double row_p(int64_t i, double sum, double acc, double p) const
+    {
+        pnew_own[i] = p;
         if constexpr (PEER) peer_push(lo_pn, hi_pn, pr.plane, pr.n_own, i, p);
-        w[i]               = sum;
+        w[i] = sum;
         return add(acc, mul(p, sum));
     }
     __device__ __forceinline__ void tail(double pAp_local) const
@@ -614,6 +622,9 @@ struct rvk_dcg_plan_s {
     rvk_shard     sh{};
     rvk_cg_config cfg{};
     SpmvArgs      sa{};
+    bool          march = false; // K1 (it >= 1) is k_spmv_march (RVK_PLAN_MARCH)
+    SpmvArgs      sa_m{};
+    SpmvMarch     mg{};
     int           upd_grid = 0;
     int64_t       n_ext = 0;
     unsigned char* win = nullptr;  // [z | p0 | p1 | flags | gather], the exported PEER window
@@ -762,6 +773,8 @@ rvk_status launch_k1(rvk_dcg_plan P, int it)
     const int64_t          ho = P->sh.halo_lo;
     DcgSpmvOp<FIRST, PEER> op{P->z, po, pn, P->w, scalars(P), ho, go, it, 0.0, P->peer,
                               P->peer.lo_p[k], P->peer.hi_p[k], 0u, P->z + ho, po + ho, pn + ho};
+    if constexpr (!FIRST)
+        if (P->march) return launch_spmv_march(P->ctx->stream, P->sa_m, P->mg, op, ta);
     return launch_spmv(P->ctx->stream, P->sa, op, ta, sm_count());
 }
 
@@ -998,6 +1011,14 @@ rvk_status rvk_dcg_plan_create(rvk_ctx ctx, const rvk_csr* A, rvk_shard sh, rvk_
     SpmvBands bands; // leading-edge L2 prefetch (see rvk_cg.cu)
     if (csr_bands(ctx->stream, *A, &bands) != RVK_OK) bands = SpmvBands{};
     P->sa          = make_spmv_args(*A, maxlen, &bands);
+    {
+        // plane stride: one halo = one plane (z-slab shards); a single shard
+        // has no halo, its CSR diagonals give it (rvk_cg.cu csr_bands)
+        const int64_t q = sh.halo_lo ? sh.halo_lo : (sh.halo_hi ? sh.halo_hi : bands.plane_q);
+        if (!(cfg.opts & RVK_OPT_NO_MARCH) && q > 0 &&
+            (q >= (int64_t)512 * 512 || (cfg.opts & RVK_OPT_MARCH)))
+            P->march = make_spmv_march(*A, maxlen, q, sm_count(), &P->sa_m, &P->mg);
+    }
     P->upd_grid    = resident_grid(k_dcg_update<1, true, 2, true>, kUpdThreads, (sh.n_own + 1) / 2);
     P->owns_gather = shared_gather == nullptr;
     P->gather      = shared_gather;
@@ -1158,7 +1179,8 @@ int rvk_dcg_plan_flags(rvk_dcg_plan P)
 {
     if (!P) return -1;
     return (P->const_diag ? RVK_PLAN_CONST_DIAG : 0) |
-           (x_defer(P) ? RVK_PLAN_X_DEFER : 0) | (x_solve(P) ? RVK_PLAN_X_SOLVE : 0);
+           (x_defer(P) ? RVK_PLAN_X_DEFER : 0) | (x_solve(P) ? RVK_PLAN_X_SOLVE : 0) |
+           (P->march ? RVK_PLAN_MARCH : 0);
 }
 
 // ---- PEER backend ----------------------------------------------------------

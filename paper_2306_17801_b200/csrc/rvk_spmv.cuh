@@ -54,7 +54,8 @@ constexpr int    kSpmvUnroll        = 8;                   // default nonzeros p
 #endif
 constexpr size_t kSpmvHeaderBytes   = 2048;                // barriers, meta, reduction scratch
 constexpr size_t kSpmvStageBudget   = 200 * 1024;          // dynamic smem for the ring
-constexpr size_t kSpmvMarchSmem     = 227 * 1024;          // k_spmv_march: cache + ring (sm_100 max)
+constexpr size_t kSpmvMarchSmemMax  = 227 * 1024;          // sm_100 opt-in shared memory per block
+constexpr size_t kSpmvMarchSmem     = 223 * 1024;          // k_spmv_march: cache + ring (4 KB for op statics)
 
 struct SpmvStageMeta {
     int64_t kv0;    // first value index held in the stage (16-B aligned)

@@ -35,21 +35,25 @@
 namespace rvk {
 
 struct SpmvMarch {
-    int64_t Q;     // rows per plane (a multiple of 32)
-    int64_t K;     // planes (ceil(n / Q))
-    int     Lmax;  // largest CTA range (rows; multiple of 32)
-    int     grid;  // CTAs (ranges)
+    int64_t Q;      // rows per plane (a multiple of 32)
+    int64_t K;      // planes (ceil(n / Q))
+    int     Lmax;   // largest range (rows; multiple of 32)
+    int     grid;   // CTAs
+    int     stage_bytes; // SpmvArgs::stage_bytes + the staged +plane z / p_old (16 B per row)
+    int     passes; // ranges per CTA: the plane is split into grid x passes ranges, CTA g
+                    // marches ranges g, g + grid, ... one after the other (a smaller cache
+                    // leaves room for a deeper TMA ring)
     size_t  smem_bytes(const SpmvArgs& a) const
     {
-        return kSpmvHeaderBytes + (size_t)3 * Lmax * 8 + (size_t)a.stages * a.stage_bytes;
+        return kSpmvHeaderBytes + (size_t)3 * Lmax * 8 + (size_t)a.stages * stage_bytes;
     }
 };
 
-// CTA g's range of in-plane rows: [a, a + L), 32-row aligned.
-__host__ __device__ inline void march_range(const SpmvMarch& M, int g, int64_t* a, int* L)
+// Range r's in-plane rows: [a, a + L), 32-row aligned.
+__host__ __device__ inline void march_range(const SpmvMarch& M, int r, int64_t* a, int* L)
 {
-    const int64_t q32 = M.Q / 32;
-    const int64_t b0 = q32 * g / M.grid, b1 = q32 * (g + 1) / M.grid;
+    const int64_t q32 = M.Q / 32, nr = (int64_t)M.grid * M.passes;
+    const int64_t b0 = q32 * r / nr, b1 = q32 * (r + 1) / nr;
     *a = b0 * 32;
     *L = (int)((b1 - b0) * 32);
 }
@@ -71,17 +75,25 @@ __device__ __forceinline__ void march_tile(const SpmvArgs& A, const SpmvMarch& M
 // runs in 32-bit arithmetic.  A cache hit is carried in the op's Fetch slot
 // (Op::from_formed / Op::formed) so hits and misses share registers: the
 // LDS of a hit and the LDG of a miss are predicated alternatives.
+//   cs      : column of row 0 (0; a row-sharded plan's local columns start
+//             after the lower halo plane)
+//   zq / pq : this row's +plane z / p_old, TMA-staged with the tile (null:
+//             the tile has none staged -- fetch from global memory if the
+//             +plane exists)
 template <int U, class Op, class Acc, class ColF, class ValF>
-__device__ __forceinline__ Acc march_row(const Op& op, Acc acc, int i, int base, int L, int Q, int n,
-                                         const double* Ck, const double* Cm, double* Cn, int kb,
+__device__ __forceinline__ Acc march_row(const Op& op, Acc acc, int i, int base, int L, int Q,
+                                         int ncols, int cs, const double* Ck, const double* Cm,
+                                         double* Cn, const double* zq, const double* pqr, int kb,
                                          int ke, ColF col, ValF val)
 {
-    const int o = i - base; // offset in the range, 0 <= o < L
-    // own +plane element (first touch in DRAM): formed once, cached for the
-    // next two steps, and used directly if this row gathers it
+    const int  o     = i - base; // offset in the range, 0 <= o < L
+    const bool has_q = i + cs < ncols - Q;
+    base += cs;                  // from here on: column space
+    // the row's own +plane value: formed once from the staged raw operands,
+    // cached for steps k+1 (own plane) and k+2 (-plane)
     double pq = 0.0;
-    if (i < n - Q) {
-        pq    = op.value(op.fetch(i + Q));
+    if (has_q) {
+        pq    = zq ? op.value(Op::raw(zq[0], pqr[0])) : op.value(op.fetch(base + o + Q));
         Cn[o] = pq;
     }
     double sum = 0.0;
@@ -90,7 +102,7 @@ __device__ __forceinline__ Acc march_row(const Op& op, Acc acc, int i, int base,
         unsigned           miss = 0;
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const int c   = k + u < ke ? col(k + u) : i; // past the row's end: a harmless slot
+            const int c   = k + u < ke ? col(k + u) : base + o; // past the row's end: a harmless slot
             const int rel = c - base;
             if ((unsigned)rel < (unsigned)L) f[u] = Op::from_formed(Ck[rel]);
             else if ((unsigned)(rel + Q) < (unsigned)L) f[u] = Op::from_formed(Cm[rel + Q]);
@@ -103,7 +115,9 @@ __device__ __forceinline__ Acc march_row(const Op& op, Acc acc, int i, int base,
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const double v = (miss >> u) & 1u ? op.value(f[u]) : Op::formed(f[u]);
-            const double t = add(sum, mul(val(k + u), v));
+            // slots past the row's end re-read the batch's first value (in
+            // bounds for the direct path's global arrays) and are not summed
+            const double t = add(sum, mul(val(k + u < ke ? k + u : k), v));
             sum            = k + u < ke ? t : sum;
         }
     }
@@ -127,11 +141,6 @@ __global__ void __launch_bounds__(kSpmvThreads, 1)
     Op op = op_in;
     if (!op.init()) return;
 
-    int64_t a;
-    int     L;
-    march_range(M, blockIdx.x, &a, &L);
-    const int T = (L + A.R - 1) / A.R; // tiles per plane step
-
     const int tid = threadIdx.x;
     if (tid == 0) {
         for (int s = 0; s < A.stages; ++s) {
@@ -147,6 +156,11 @@ __global__ void __launch_bounds__(kSpmvThreads, 1)
         if (tid == 0) {
             const uint64_t pol_stream = policy_evict_first();
             int            j          = 0;
+            for (int pass = 0; pass < M.passes; ++pass) {
+            int64_t a;
+            int     L;
+            march_range(M, blockIdx.x + pass * M.grid, &a, &L);
+            const int T = (L + A.R - 1) / A.R; // tiles per plane step
             for (int64_t k = 0; k < M.K; ++k) {
                 for (int t = 0; t < T; ++t, ++j) {
                     const int s = j % A.stages;
@@ -169,30 +183,33 @@ __global__ void __launch_bounds__(kSpmvThreads, 1)
                     m.kv0             = kv0;
                     m.kc0             = kc0;
                     m.direct          = dir ? 1 : 0;
+                    // +plane segment of the tile (z, p_old at rows + cs + Q):
+                    // contiguous, so TMA-staged with the CSR -- the rows' only
+                    // first-touch gathers leave the consumers' critical path
+                    const int64_t cs   = op.own_col(0);
+                    const bool    plus = !dir && r1 + cs + M.Q <= A.n_cols && op.num_src() == 2;
+                    m.pad              = plus ? 1 : 0;
                     if (dir) {
                         mbar_arrive(&full[s]);
                     } else {
-                        unsigned char* st = stage0 + (size_t)s * A.stage_bytes;
+                        unsigned char* st = stage0 + (size_t)s * M.stage_bytes;
                         const uint32_t ob = (uint32_t)((A.R + 2) * 8);
                         const uint32_t vb = (uint32_t)((kv1 - kv0) * 8);
                         const uint32_t cb = (uint32_t)((kc1 - kc0) * 4);
-                        mbar_arrive_expect_tx(&full[s], ob + vb + cb);
+                        const uint32_t qb = plus ? (uint32_t)((r1 - r0) * 8) : 0u;
+                        mbar_arrive_expect_tx(&full[s], ob + vb + cb + 2 * qb);
                         bulk_g2s(st, OFF + r0, ob, &full[s], pol_stream);
                         if (vb) bulk_g2s(st + A.off_bytes, A.vals + kv0, vb, &full[s], pol_stream);
                         if (cb) bulk_g2s(st + A.off_bytes + A.val_bytes, A.cols + kc0, cb, &full[s], pol_stream);
-                    }
-                    // the NEXT tile's +plane elements (first-touch DRAM reads of
-                    // its rows' own-offset loads): L2 prefetch
-                    int64_t q0, q1;
-                    if (t + 1 < T) march_tile(A, M, a, L, k, t + 1, &q0, &q1);
-                    else march_tile(A, M, a, L, k + 1, 0, &q0, &q1);
-                    int64_t lo = (q0 + M.Q) & ~int64_t(1), hi = min(q1 + M.Q, A.n_cols) & ~int64_t(1);
-                    if (hi > lo) {
-                        const int nps = op.num_src();
-                        for (int p = 0; p < nps; ++p)
-                            bulk_prefetch_l2(op.src_ptr(p) + lo, (uint32_t)(hi - lo) * 8);
+                        if (qb) {
+                            unsigned char* q = st + A.stage_bytes;
+                            bulk_g2s(q, op.src_ptr(0) + r0 + cs + M.Q, qb, &full[s], pol_stream);
+                            bulk_g2s(q + (size_t)A.R * 8, op.src_ptr(1) + r0 + cs + M.Q, qb, &full[s],
+                                     pol_stream);
+                        }
                     }
                 }
+            }
             }
         }
         return;
@@ -205,14 +222,20 @@ __global__ void __launch_bounds__(kSpmvThreads, 1)
     constexpr int NS = spmv_sums<Op>::value;
     spmv_acc_t<Op> acc{};
 
+    const int cs = (int)op.own_col(0);
+    int       j  = 0;
+    for (int pass = 0; pass < M.passes; ++pass) {
+    int64_t a;
+    int     L;
+    march_range(M, blockIdx.x + pass * M.grid, &a, &L);
+    const int T = (L + A.R - 1) / A.R; // tiles per plane step
     // prologue: plane 0 of the range into slot 0
     for (int o = ctid; o < L; o += A.consumers) {
         const int64_t i = a + o;
-        if (i < A.n_rows) cache[o] = op.value(op.fetch((int32_t)i));
+        if (i < A.n_rows) cache[o] = op.value(op.fetch((int32_t)(i + cs)));
     }
     asm volatile("bar.sync 2, %0;" ::"r"(A.consumers) : "memory");
 
-    int j = 0;
     for (int64_t k = 0; k < M.K; ++k) {
         const double* Ck   = cache + (size_t)(k % 3) * M.Lmax;
         const double* Cm   = cache + (size_t)((k + 2) % 3) * M.Lmax;
@@ -231,22 +254,25 @@ __global__ void __launch_bounds__(kSpmvThreads, 1)
                 const double* __restrict__ Vg  = A.vals;
                 for (int lr = gtid; lr < rows; lr += gs) {
                     const int64_t kb = OFF[r0 + lr], ke = OFF[r0 + lr + 1];
-                    acc = march_row<U>(op, acc, (int)(r0 + lr), (int)base, L, (int)M.Q, (int)A.n_rows, Ck,
-                                       Cm, Cn, 0, (int)(ke - kb),
+                    acc = march_row<U>(op, acc, (int)(r0 + lr), (int)base, L, (int)M.Q, (int)A.n_cols, cs,
+                                       Ck, Cm, Cn, nullptr, nullptr, 0, (int)(ke - kb),
                                        [&](int q) { return __ldg(Cg + kb + q); },
                                        [&](int q) { return __ldg(Vg + kb + q); });
                 }
             } else {
-                unsigned char* st  = stage0 + (size_t)s * A.stage_bytes;
+                unsigned char* st  = stage0 + (size_t)s * M.stage_bytes;
                 const int64_t  kv0 = m.kv0;
+                const double*  Zq  = m.pad ? reinterpret_cast<const double*>(st + A.stage_bytes) : nullptr;
+                const double*  Pq  = Zq ? Zq + A.R : nullptr;
                 const int32_t* Cc  = reinterpret_cast<const int32_t*>(st + A.off_bytes + A.val_bytes) +
                                     (kv0 - m.kc0);
                 const int64_t* O   = reinterpret_cast<const int64_t*>(st);
                 const double*  V   = reinterpret_cast<const double*>(st + A.off_bytes);
                 for (int lr = gtid; lr < rows; lr += gs) {
                     const int kb = (int)(O[lr] - kv0), ke = (int)(O[lr + 1] - kv0);
-                    acc = march_row<U>(op, acc, (int)(r0 + lr), (int)base, L, (int)M.Q, (int)A.n_rows, Ck,
-                                       Cm, Cn, kb, ke, [&](int q) { return Cc[q]; },
+                    acc = march_row<U>(op, acc, (int)(r0 + lr), (int)base, L, (int)M.Q, (int)A.n_cols, cs,
+                                       Ck, Cm, Cn, Zq ? Zq + lr : nullptr, Pq ? Pq + lr : nullptr,
+                                       kb, ke, [&](int q) { return Cc[q]; },
                                        [&](int q) { return V[q]; });
                 }
             }
@@ -256,6 +282,7 @@ __global__ void __launch_bounds__(kSpmvThreads, 1)
         // slot (k+1) complete before step k+1 reads it; slot (k-1) free
         asm volatile("bar.sync 2, %0;" ::"r"(A.consumers) : "memory");
     }
+    } // pass
 
     if constexpr (Op::kHasTail) {
         double v[NS];
@@ -291,10 +318,18 @@ rvk_status launch_spmv_march(cudaStream_t stream, const SpmvArgs& a, const SpmvM
 {
     static std::atomic<uint64_t> configured{0};
     if (device_first_use(configured)) {
-        const int smax = (int)kSpmvMarchSmem;
-        RVK_CUDA(cudaFuncSetAttribute(k_spmv_march<Op, 7>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax));
-        RVK_CUDA(cudaFuncSetAttribute(k_spmv_march<Op, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax));
-        RVK_CUDA(cudaFuncSetAttribute(k_spmv_march<Op, 9>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax));
+        // dynamic + static shared memory <= the opt-in maximum (an op may
+        // bring static shared memory of its own)
+        auto set = [](auto fn) -> rvk_status {
+            cudaFuncAttributes fa{};
+            RVK_CUDA(cudaFuncGetAttributes(&fa, fn));
+            const int smax = (int)(kSpmvMarchSmemMax - fa.sharedSizeBytes);
+            RVK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smax));
+            return RVK_OK;
+        };
+        if (rvk_status st = set(k_spmv_march<Op, 7>); st != RVK_OK) return st;
+        if (rvk_status st = set(k_spmv_march<Op, 8>); st != RVK_OK) return st;
+        if (rvk_status st = set(k_spmv_march<Op, 9>); st != RVK_OK) return st;
         device_mark_done(configured);
     }
     const int    th = 32 + a.consumers;

@@ -152,7 +152,7 @@ class ShardPlan:
 
 
 def loopback_solve(ctx, dim, points, grid, nranks, b_host: np.ndarray, max_it=20, pc="jacobi",
-                   rtol=0.0, atol=0.0, backend="gather", repeats=1):
+                   rtol=0.0, atol=0.0, backend="gather", repeats=1, opts=0, flags_out=None):
     """All shards on one device (test path): returns (x, CgResult of shard 0,
     per-shard results).  backend "gather": D2D halo copies + one shared
     gather buffer between kernels; "peer": the PEER kernels (in-kernel halo
@@ -167,8 +167,10 @@ def loopback_solve(ctx, dim, points, grid, nranks, b_host: np.ndarray, max_it=20
         rvk.check(rvk.lib().rvk_set(ctx.h, 4 * nranks, 0.0, gather.ptr))
     mats = [local_laplacian(ctx, dim, points, grid, s) for s in shards]
     plans = [ShardPlan(ctx, mats[i], s, max_it, pc, rtol, atol, None,
-                       gather.ptr if (gather is not None and nranks > 1) else None)
+                       gather.ptr if (gather is not None and nranks > 1) else None, opts=opts)
              for i, s in enumerate(shards)]
+    if flags_out is not None:
+        flags_out.extend(int(rvk.lib().rvk_dcg_plan_flags(p.h)) for p in plans)
     if peer:
         windows = [p.window()[0] for p in plans]
         for p in plans:

@@ -89,3 +89,30 @@ def test_march_selection_rules(ctx):
         plan = rvk.CgPlan(ctx, A, max_it=2, opts=opts)
         assert bool(plan.flags() & rvk.PLAN_MARCH) == want, (g, opts)
         plan.close()
+
+
+@pytest.mark.parametrize("nranks,backend", [(1, "gather"), (2, "peer"), (3, "peer"), (2, "gather"),
+                                            (3, "gather"), (4, "peer")])
+@pytest.mark.parametrize("pts", [7, 27])
+def test_march_row_sharded(ctx, nranks, backend, pts):
+    """Row-sharded plans (z-slabs with one halo plane): the march K1 on the
+    local CSR (columns shifted by the lower halo), the lower halo plane read
+    as global gathers, the boundary planes' p pushed to the neighbours."""
+    from paper_2306_17801_b200.sharded import loopback_solve
+    g = (96, 64, 3 * nranks + 6)
+    Ah = O.build_laplacian(3, pts, g)
+    b = O.rhs(Ah.n_rows)
+    ref = O.cg_solve(Ah, b, max_it=20)
+    flags = []
+    x, res, per = loopback_solve(ctx, 3, pts, g, nranks, b, max_it=20, backend=backend,
+                                 opts=rvk.OPT_MARCH, flags_out=flags)
+    assert all(f & rvk.PLAN_MARCH for f in flags), flags
+    x0, res0, _ = loopback_solve(ctx, 3, pts, g, nranks, b, max_it=20, backend=backend,
+                                 opts=rvk.OPT_NO_MARCH)
+    assert res.iterations == 20
+    eh = np.abs(res.hist - ref.hist) / ref.hist
+    ex = np.linalg.norm(x - ref.x) / np.linalg.norm(ref.x)
+    assert eh.max() < 1e-10 and ex < 1e-10, (np.argmax(eh > 1e-10), eh.max(), ex,
+                                             [np.linalg.norm(x[s] - ref.x[s]) for s in
+                                              np.array_split(np.arange(x.size), nranks)])
+    assert np.max(np.abs(res.hist - res0.hist) / res0.hist) < 1e-12

@@ -694,7 +694,7 @@ def test_cluster_solve(ctx, spec, pc):
         x2, res2 = plan.solve_host(b)  # repeatable
         assert np.array_equal(x, x2) and np.array_equal(res.hist, res2.hist)
         grid = rvk.CgPlan(ctx, A, max_it=max_it, rtol=rtol, pc=pc, mode="persistent",
-                          opts=rvk.OPT_NO_CLUSTER)
+                          opts=rvk.OPT_NO_CLUSTER | rvk.OPT_NO_GRID)
         assert not grid.flags() & 256
         xg, resg = grid.solve_host(b)
         check_cg_floor(resg, xg, ref)
