@@ -600,7 +600,11 @@ bool make_spmv_march(const rvk_csr& A, int64_t max_row_len, int64_t Q, int grid,
     // the fewest ranges per CTA (passes: a smaller cache) that leave a TMA
     // ring of >= 3 stages; else the fewest with 2
     bool found = false;
+#ifdef RVK_MARCH_PASSES
+    for (int passes = RVK_MARCH_PASSES; passes <= RVK_MARCH_PASSES; ++passes) {
+#else
     for (int passes = 1; passes <= 16 && Q / 32 >= (int64_t)grid * passes; ++passes) {
+#endif
         SpmvMarch m;
         m.Q      = Q;
         m.K      = (A.n_rows + Q - 1) / Q;

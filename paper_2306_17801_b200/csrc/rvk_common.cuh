@@ -168,6 +168,15 @@ __device__ __forceinline__ uint64_t policy_evict_first()
     return p;
 }
 
+// ... default priority (an explicit policy for bulk copies that must not be
+// demoted, e.g. operands other CTAs gather again soon).
+__device__ __forceinline__ uint64_t policy_evict_normal()
+{
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+
 // ... and for data several CTAs will re-read soon (the x-windows).
 __device__ __forceinline__ uint64_t policy_evict_last()
 {

@@ -155,6 +155,7 @@ __global__ void __launch_bounds__(kSpmvThreads, 1)
         // ===================== producer warp =====================
         if (tid == 0) {
             const uint64_t pol_stream = policy_evict_first();
+            const uint64_t pol_keep   = policy_evict_normal();
             int            j          = 0;
             for (int pass = 0; pass < M.passes; ++pass) {
             int64_t a;
@@ -203,9 +204,11 @@ __global__ void __launch_bounds__(kSpmvThreads, 1)
                         if (cb) bulk_g2s(st + A.off_bytes + A.val_bytes, A.cols + kc0, cb, &full[s], pol_stream);
                         if (qb) {
                             unsigned char* q = st + A.stage_bytes;
-                            bulk_g2s(q, op.src_ptr(0) + r0 + cs + M.Q, qb, &full[s], pol_stream);
+                            // normal L2 priority: the neighbouring ranges read
+                            // these lines again as their halo gathers
+                            bulk_g2s(q, op.src_ptr(0) + r0 + cs + M.Q, qb, &full[s], pol_keep);
                             bulk_g2s(q + (size_t)A.R * 8, op.src_ptr(1) + r0 + cs + M.Q, qb, &full[s],
-                                     pol_stream);
+                                     pol_keep);
                         }
                     }
                 }
@@ -229,10 +232,12 @@ __global__ void __launch_bounds__(kSpmvThreads, 1)
     int     L;
     march_range(M, blockIdx.x + pass * M.grid, &a, &L);
     const int T = (L + A.R - 1) / A.R; // tiles per plane step
-    // prologue: plane 0 of the range into slot 0
+    // prologue: plane 0 of the range into slot 0, and the plane below it into
+    // slot 2 when the column space has one (a row shard's lower halo plane)
     for (int o = ctid; o < L; o += A.consumers) {
         const int64_t i = a + o;
         if (i < A.n_rows) cache[o] = op.value(op.fetch((int32_t)(i + cs)));
+        if (i + cs - M.Q >= 0) cache[(size_t)2 * M.Lmax + o] = op.value(op.fetch((int32_t)(i + cs - M.Q)));
     }
     asm volatile("bar.sync 2, %0;" ::"r"(A.consumers) : "memory");
 

@@ -30,10 +30,20 @@ def kernel_entry(path):
             "l2_hit_pct": float(d["lts__t_sector_hit_rate.pct"][0])}
 
 
-def main(tag="r01"):
+def lib_sha16():
+    import hashlib
+    with open(os.path.join(ROOT, "paper_2306_17801_b200", "lib", "librvk.so"), "rb") as f:
+        return hashlib.sha256(f.read()).hexdigest()[:16]
+
+
+def main(tag="r02"):
+    # the captures in gpurun_out/ must come from the library now in the tree
+    # (scripts/gpu_profiles.sh runs on the snapshot of this tree)
     out = {"_note": f"{tag}: ncu --set full --clock-control none, one launch each "
-                    "(serialised, after 4 warm launches); per-launch DRAM bytes = traffic"}
+                    "(serialised, after 4 warm launches); per-launch DRAM bytes = traffic",
+           "lib_sha16": lib_sha16()}
     for cfg, files in {"7pt256": {"k1": "prof_k1", "k2": "prof_k2"},
+                       "7pt768": {"k1": "prof_march768"},
                        "27pt256": {"k1": "prof_k1_27pt"}, "9pt4096": {"k1": "prof_k1_9pt"},
                        "7pt256_matrix_free": {"k1": "prof_mf"},
                        "27pt256_matrix_free": {"k1": "prof_mf_27pt"}}.items():
@@ -53,7 +63,7 @@ def main(tag="r01"):
         cnt[name] += 1
     T = sum(tot.values())
     with open(os.path.join(P, f"{tag}_launch_shares_7pt256.txt"), "w") as fh:
-        fh.write(f"ncu --metrics gpu__time_duration.sum launch list, 2 solves of 3D 7-pt 256^3\n")
+        fh.write("ncu --metrics gpu__time_duration.sum launch list, 2 solves of 3D 7-pt 256^3\n")
         for k in sorted(tot, key=lambda k: -tot[k]):
             fh.write(f"{k:45s} n={cnt[k]:3d} total={tot[k]:9.1f} us avg={tot[k]/cnt[k]:8.1f} us "
                      f"share={tot[k]/T:6.1%}\n")
