@@ -253,7 +253,7 @@ typedef struct {
  *                        instead of once per solve (RVK_PLAN_X_SOLVE)
  *   RVK_OPT_X_EACH       fused solve: x updated in every iteration's K2
  *   RVK_OPT_MARCH        CSR plans with a plane structure: the plane-marching
- *                        K1 (RVK_PLAN_MARCH) even for small planes
+ *                        K1 (RVK_PLAN_MARCH; opt-in)
  *   RVK_OPT_NO_MARCH     never the plane-marching K1
  *   RVK_OPT_NO_GRID      PERSISTENT mode: no one-launch grid solve for mid-size
  *                        systems (the generic grid-barrier kernel instead)   */
@@ -333,8 +333,7 @@ rvk_status rvk_cg_solve_host_many(rvk_cg_plan plan, int nrhs, const double* cons
 #define RVK_PLAN_MARCH      1024 /* fused CSR K1 (iterations >= 1) is the plane-marching SpMV:
                                     each SM owns an in-plane row range and walks it through
                                     the planes, the formed gathered operand of planes k-1,
-                                    k, k+1 cached in shared memory (large 3D planes, or
-                                    RVK_OPT_MARCH; RVK_OPT_NO_MARCH disables)            */
+                                    k, k+1 cached in shared memory (RVK_OPT_MARCH)       */
 #define RVK_PLAN_GRID       2048 /* PERSISTENT / AUTO plan runs the one-launch grid solve (16 K < n <=
                                     ~450 K rows, rows <= 9 entries): CSR in shared memory, row
                                     vectors in registers, 2 grid barriers per iteration

@@ -600,11 +600,7 @@ bool make_spmv_march(const rvk_csr& A, int64_t max_row_len, int64_t Q, int grid,
     // the fewest ranges per CTA (passes: a smaller cache) that leave a TMA
     // ring of >= 3 stages; else the fewest with 2
     bool found = false;
-#ifdef RVK_MARCH_PASSES
-    for (int passes = RVK_MARCH_PASSES; passes <= RVK_MARCH_PASSES; ++passes) {
-#else
     for (int passes = 1; passes <= 16 && Q / 32 >= (int64_t)grid * passes; ++passes) {
-#endif
         SpmvMarch m;
         m.Q      = Q;
         m.K      = (A.n_rows + Q - 1) / Q;
@@ -1399,10 +1395,11 @@ rvk_status rvk_cg_plan_create(rvk_ctx ctx, const rvk_csr* A, rvk_cg_config cfg, 
     P->sa            = make_spmv_args(*A, maxlen, &bands);
     P->sa.small_rows = (cfg.opts & RVK_OPT_SMALL_K1) ? 512 * 1024 : 0;
     P->spmv_grid = sm_count();
-    // plane-marching K1 for large 3D planes (>= 512^2 rows per plane: there
-    // the row-order sweep re-reads the -plane gathers from DRAM)
-    if (!(cfg.opts & RVK_OPT_NO_MARCH) && bands.plane_q > 0 &&
-        (bands.plane_q >= (int64_t)512 * 512 || (cfg.opts & RVK_OPT_MARCH)))
+    // plane-marching K1 (opt-in): DRAM reads at the algorithmic minimum for
+    // large 3D planes, but measured slower than the row-order kernel on B200
+    // (768^3: 12.4-13.9 vs 10.3 ms per K1, profiles/r02/march_768.md), so
+    // only RVK_OPT_MARCH selects it
+    if ((cfg.opts & RVK_OPT_MARCH) && !(cfg.opts & RVK_OPT_NO_MARCH) && bands.plane_q > 0)
         P->march = make_spmv_march(*A, maxlen, bands.plane_q, P->spmv_grid, &P->sa_m, &P->mg);
     // one resident wave each (the vectorised loops take 2 elements per thread)
     P->upd_grid   = resident_grid(k_cg_update<true, 1>, kUpdThreads, (A->n_rows + 1) / 2);

@@ -77,8 +77,9 @@ def test_march_early_exit_and_graph_modes(ctx, use_graph):
 
 
 def test_march_selection_rules(ctx):
-    # auto: only planes >= 512^2 rows; 2D grids and small planes never
+    # opt-in only; 2D grids, small planes, < 3 planes never
     for dim, pts, g, opts, want in [(3, 7, (96, 64, 12), 0, False),
+                                    (3, 7, (768, 768, 3), 0, False),
                                     (3, 7, (96, 64, 12), rvk.OPT_MARCH, True),
                                     (2, 5, (4096, 64), rvk.OPT_MARCH, False),   # Q = 4096 < 148 x 32
                                     (3, 7, (90, 64, 12), rvk.OPT_MARCH, True),  # Q = 5760
