@@ -308,6 +308,7 @@ template <bool FIRST, bool PEER>
 struct DcgSpmvOp {
     static constexpr bool kHasTail  = true;
     static constexpr bool kSysFence = PEER;
+    static constexpr bool kNoSmall  = true; // shard plans never take the small-system K1
     const double* __restrict__ z;     // extended (halo) layout
     const double* __restrict__ p_old; // extended
     double* __restrict__ p_new;       // extended

@@ -371,6 +371,12 @@ struct spmv_sys_fence : std::false_type {};
 template <class Op>
 struct spmv_sys_fence<Op, std::void_t<decltype(Op::kSysFence)>>
     : std::integral_constant<bool, Op::kSysFence> {};
+// Op::kNoSmall: the op is never launched on a small_rows plan (row-sharded
+// and TFQMR plans), so k_spmv_small is not instantiated for it.
+template <class Op, class = void>
+struct spmv_no_small : std::false_type {};
+template <class Op>
+struct spmv_no_small<Op, std::void_t<decltype(Op::kNoSmall)>> : std::integral_constant<bool, Op::kNoSmall> {};
 template <class Op>
 using spmv_acc_t = std::conditional_t<spmv_sums<Op>::value == 1, double, SumVec<spmv_sums<Op>::value>>;
 
@@ -594,6 +600,7 @@ rvk_status launch_spmv(cudaStream_t stream, const SpmvArgs& a, const Op& op, Tai
                        int grid)
 {
     // (the tail's partial slots: the plans reserve 2 x kMaxReduceBlocks doubles)
+    if constexpr (!spmv_no_small<Op>::value)
     if (a.small_rows && a.n_rows <= a.small_rows &&
         ((a.n_rows + kSpmvSmallThreads - 1) / kSpmvSmallThreads) * spmv_sums<Op>::value <=
             2 * (int64_t)kMaxReduceBlocks) {

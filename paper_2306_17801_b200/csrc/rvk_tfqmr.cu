@@ -241,6 +241,7 @@ __global__ void __launch_bounds__(kTfqThreads)
 template <int PC>
 struct TfqAOp {
     static constexpr bool kHasTail = true;
+    static constexpr bool kNoSmall = true; // TFQMR plans never take the small-system K1
     static constexpr int  kSums    = 2;
     const double* __restrict__ u;
     const double* __restrict__ v;
@@ -322,6 +323,7 @@ struct TfqAOp {
 template <int PC>
 struct TfqBOp {
     static constexpr bool kHasTail = true;
+    static constexpr bool kNoSmall = true;
     const double* __restrict__ p;
     const double* __restrict__ rp;
     const double* __restrict__ dinv;
