@@ -566,6 +566,13 @@ rvk_status csr_bands(cudaStream_t s, const rvk_csr& A, SpmvBands* out)
         out->lead_lo  = lo;
         out->lead_hi  = d.back();
     }
+    int64_t hi = d.front(); // the lowest band, mirrored
+    for (size_t i = 0; i + 1 < d.size() && d[i + 1] - hi <= kGap; ++i) hi = d[i + 1];
+    if (hi - d.front() <= kMaxBand && hi < lo) {
+        out->has_trail = true;
+        out->trail_lo  = d.front();
+        out->trail_hi  = hi;
+    }
     // plane stride (3D stencils): split the positive diagonals at their
     // largest gap; the upper cluster is the +plane band, Q its middle
     // diagonal, which must be mirrored by -Q and exceed twice the widths of
