@@ -566,13 +566,6 @@ rvk_status csr_bands(cudaStream_t s, const rvk_csr& A, SpmvBands* out)
         out->lead_lo  = lo;
         out->lead_hi  = d.back();
     }
-    int64_t hi = d.front(); // the lowest band, mirrored
-    for (size_t i = 0; i + 1 < d.size() && d[i + 1] - hi <= kGap; ++i) hi = d[i + 1];
-    if (hi - d.front() <= kMaxBand && hi < lo) {
-        out->has_trail = true;
-        out->trail_lo  = d.front();
-        out->trail_hi  = hi;
-    }
     // plane stride (3D stencils): split the positive diagonals at their
     // largest gap; the upper cluster is the +plane band, Q its middle
     // diagonal, which must be mirrored by -Q and exceed twice the widths of
@@ -1436,8 +1429,8 @@ rvk_status rvk_cg_plan_create(rvk_ctx ctx, const rvk_csr* A, rvk_cg_config cfg, 
     };
     // every vector a K1 may gather (dinv, r with a virtual z, z, p) padded by
     // 4 doubles
-    alloc(reinterpret_cast<void**>(&P->dinv), vb);
-    alloc(reinterpret_cast<void**>(&P->r), vb);
+    alloc(reinterpret_cast<void**>(&P->dinv), vb + 32);
+    alloc(reinterpret_cast<void**>(&P->r), vb + 32);
     alloc(reinterpret_cast<void**>(&P->z), vb + 32);
     alloc(reinterpret_cast<void**>(&P->p[0]), vb + 32);
     alloc(reinterpret_cast<void**>(&P->p[1]), vb + 32);
@@ -1546,7 +1539,7 @@ rvk_status rvk_cg_plan_create_stencil(rvk_ctx ctx, int dim, int points, int64_t 
         if (e == cudaSuccess) e = cudaMalloc(q, bytes);
     };
     alloc(reinterpret_cast<void**>(&P->dinv), 64); // unused: the diagonal is constant
-    alloc(reinterpret_cast<void**>(&P->r), vb);
+    alloc(reinterpret_cast<void**>(&P->r), vb + 32);
     alloc(reinterpret_cast<void**>(&P->z), vb + 32);
     alloc(reinterpret_cast<void**>(&P->p[0]), vb + 32);
     alloc(reinterpret_cast<void**>(&P->p[1]), vb + 32);

@@ -72,8 +72,6 @@ struct SpmvBands {
     bool    has_lead = false;
     int64_t lead_lo = 0, lead_hi = 0;
     int64_t plane_q = 0; // > 0: diagonals +-Q bound two plane bands (3D stencil), Q % 32 == 0
-    bool    has_trail = false; // the lowest band [trail_lo, trail_hi] of (col - row)
-    int64_t trail_lo = 0, trail_hi = 0;
 };
 
 struct SpmvArgs {
@@ -90,8 +88,6 @@ struct SpmvArgs {
     int            off_bytes, val_bytes, col_bytes, stage_bytes; // [off | vals | cols]
     int            pf;                    // 1: L2-prefetch the next tile's leading-edge columns
     int64_t        pf_lo, pf_hi;          // ... the band [pf_lo, pf_hi] of (col - row)
-    int            pft;                   // 1: also L2-prefetch the next tile's trailing band
-    int64_t        pft_lo, pft_hi;        //    (large planes: the -plane gathers miss L2)
     const int64_t* off;
     const int32_t* cols;
     const double*  vals;
@@ -158,15 +154,6 @@ inline SpmvArgs make_spmv_args(const rvk_csr& A, int64_t max_row_len, const Spmv
     a.pf      = (B && B->has_lead && B->lead_lo > 0) ? 1 : 0;
     a.pf_lo   = a.pf ? B->lead_lo : 0;
     a.pf_hi   = a.pf ? B->lead_hi : 0;
-    // trailing band: when it lies further back than ~2 x 64 MB of streamed
-    // CSR (L2 reuse distance), the -plane lines were evicted since their
-    // last use -- prefetch them too (DRAM re-read, but off the critical path)
-#ifndef RVK_TRAIL_ROWS
-#define RVK_TRAIL_ROWS (int64_t)(256 * 1024)
-#endif
-    a.pft    = (a.pf && B->has_trail && B->lead_lo - B->trail_hi >= 2 * RVK_TRAIL_ROWS) ? 1 : 0;
-    a.pft_lo = a.pft ? B->trail_lo : 0;
-    a.pft_hi = a.pft ? B->trail_hi : 0;
     // enough groups that every consumer thread owns a row of some tile
     a.consumers = kSpmvConsumers;
     a.groups    = 1;
@@ -466,16 +453,6 @@ __global__ void __launch_bounds__(kSpmvThreads, 1) k_spmv_tma(SpmvArgs A, Op op_
                 // leading edge of this CTA's NEXT tile: its highest-diagonal
                 // columns are first-touch DRAM misses for the gathers; start
                 // them now (L2 prefetch, no smem, no barrier)
-                if (A.pft && tn < A.n_tiles) {
-                    const int64_t q0 = tn * A.R, q1 = min(q0 + A.R, A.n_rows);
-                    int64_t       lo = max(q0 + A.pft_lo, (int64_t)0) & ~int64_t(1);
-                    int64_t       hi = max(min(q1 + A.pft_hi, A.n_cols), (int64_t)0) & ~int64_t(1);
-                    if (hi > lo) {
-                        const int nps = op.num_src();
-                        for (int k = 0; k < nps; ++k)
-                            bulk_prefetch_l2(op.src_ptr(k) + lo, (uint32_t)(hi - lo) * 8);
-                    }
-                }
                 if (A.pf && tn < A.n_tiles) {
                     const int64_t q0 = tn * A.R, q1 = min(q0 + A.R, A.n_rows);
                     int64_t       lo = max(q0 + A.pf_lo, (int64_t)0) & ~int64_t(1);

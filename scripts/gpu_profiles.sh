@@ -14,5 +14,7 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_sp
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_cg_update -s 4 -c 1 -o gpurun_out/prof_k2 -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline > /dev/null 2>&1; echo ncu k2 rc $?
 timeout 600 ncu --set full --clock-control none -k regex:k_spmv_tma -s 4 -c 1 -o gpurun_out/prof_k1_27pt -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline --config 27pt256 > /dev/null 2>&1; echo ncu k1 27pt rc $?
 timeout 600 ncu --set full --clock-control none -k regex:k_spmv_tma -s 4 -c 1 -o gpurun_out/prof_k1_9pt -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline --config 9pt4096 > /dev/null 2>&1; echo ncu k1 9pt rc $?
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_spmv_tma -s 4 -c 1 -o gpurun_out/prof_k1_768 -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-strong --config 7pt768 > /dev/null 2>&1; echo ncu k1 768 rc $?
+timeout 600 ncu --nvtx --nvtx-include "dcg.loopback_solve/" --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 44 --csv python scripts/shard_k1_probe.py > gpurun_out/shard_solve_dram.csv 2>&1; echo ncu shard solve rc $?
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_mf_tma -s 4 -c 1 -o gpurun_out/prof_mf -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline --operator stencil > /dev/null 2>&1; echo ncu mf rc $?
 timeout 600 ncu --set full --clock-control none -k regex:k_mf_tma -s 4 -c 1 -o gpurun_out/prof_mf_27pt -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline --operator stencil --config 27pt256 > /dev/null 2>&1; echo ncu mf 27pt rc $?

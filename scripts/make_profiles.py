@@ -43,7 +43,7 @@ def main(tag="r02"):
                     "(serialised, after 4 warm launches); per-launch DRAM bytes = traffic",
            "lib_sha16": lib_sha16()}
     for cfg, files in {"7pt256": {"k1": "prof_k1", "k2": "prof_k2"},
-                       "7pt768": {"k1": "prof_march768"},
+                       "7pt768": {"k1": "prof_k1_768"},
                        "27pt256": {"k1": "prof_k1_27pt"}, "9pt4096": {"k1": "prof_k1_9pt"},
                        "7pt256_matrix_free": {"k1": "prof_mf"},
                        "27pt256_matrix_free": {"k1": "prof_mf_27pt"}}.items():
@@ -51,6 +51,25 @@ def main(tag="r02"):
             path = os.path.join(G, f + ".ncu-rep")
             if os.path.exists(path):
                 out.setdefault(cfg, {})[k] = kernel_entry(path)
+    # one whole P = 1 row-shard solve (the N > 1 bench line's per-GPU traffic):
+    # every kernel inside the NVTX range dcg.loopback_solve
+    sp = os.path.join(G, "shard_solve_dram.csv")
+    if os.path.exists(sp):
+        txt = open(sp).read().splitlines()
+        hdr = next((r for r in csv.reader(txt) if r and r[0] == "ID"), None)
+        if hdr:
+            im, iv = hdr.index("Metric Name"), hdr.index("Metric Value")
+            tot = collections.defaultdict(float)
+            ids = set()
+            for r in csv.reader(txt):
+                if len(r) > iv and r[0].isdigit():
+                    tot[r[im]] += float(r[iv])
+                    ids.add(r[0])
+            rd, wr = tot["dram__bytes_read.sum"], tot["dram__bytes_write.sum"]
+            out["7pt256_shard"] = {"solve": {
+                "kernels": len(ids), "dram_bytes": int(rd + wr), "dram_read": int(rd),
+                "dram_write": int(wr), "kernel_time_us_ncu": round(tot["gpu__time_duration.sum"] / 1e3, 1),
+                "capture": "ncu --nvtx --nvtx-include dcg.loopback_solve/ (P = 1 shard, 256^3 7-point)"}}
     with open(os.path.join(P, "ncu_summary.json"), "w") as fh:
         json.dump(out, fh, indent=1)
     # launch list shares
