@@ -10,7 +10,9 @@ from ncu_summary import summary  # noqa: E402
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 G = os.path.join(ROOT, "gpurun_out")
-P = os.path.join(ROOT, "profiles")
+# on the GPU box: PROFILES_OUT=gpurun_out/profiles_out (merged back), then copied
+P = os.environ.get("PROFILES_OUT", os.path.join(ROOT, "profiles"))
+os.makedirs(P, exist_ok=True)
 UNIT = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1, "us": 1e-6, "ms": 1e-3, "ns": 1e-9}
 
 
