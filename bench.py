@@ -186,11 +186,14 @@ def ncu_traffic(config: str, kernel: str = "k1"):
     k = d.get(config, {}).get(kernel)
     if not k:
         return None, None
+    from paper_2306_17801_b200 import rvk
     lib = os.path.join(ROOT, "paper_2306_17801_b200", "lib", "librvk.so")
     src = {"file": "profiles/ncu_summary.json", "capture": d.get("_note"),
+           "captured_build_id": d.get("build_id"), "loaded_build_id": rvk.lib().rvk_build_id().decode(),
            "captured_lib_sha16": d.get("lib_sha16"), "loaded_lib_sha16": _file_sha16(lib)}
-    src["build_match"] = bool(src["captured_lib_sha16"]) and \
-        src["captured_lib_sha16"] == src["loaded_lib_sha16"]
+    # build ids hash the library's sources (stable across rebuilds)
+    src["build_match"] = bool(src["captured_build_id"]) and \
+        src["captured_build_id"] == src["loaded_build_id"]
     return k.get("dram_bytes"), src
 
 

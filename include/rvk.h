@@ -50,6 +50,9 @@ typedef enum {
 /* Thread-local description of the last failure on this thread. */
 const char* rvk_last_error(void);
 int         rvk_abi_version(void);
+/* sha256 (16 hex digits) of the library's sources: profiles record it, so a
+ * bench run can tell whether committed ncu numbers came from this code. */
+const char* rvk_build_id(void);
 /* Number of SMs / name of the calling thread's current device (setup helper). */
 int         rvk_device_info(int* sm_count, char* name, int name_len);
 /* Device selection for the calling thread (cudaGetDeviceCount /

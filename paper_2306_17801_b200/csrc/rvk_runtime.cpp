@@ -67,6 +67,10 @@ using namespace rvk;
 extern "C" {
 
 const char* rvk_last_error(void) { return g_err; }
+#ifndef RVK_BUILD_ID
+#define RVK_BUILD_ID "unknown"
+#endif
+const char* rvk_build_id(void) { return RVK_BUILD_ID; }
 int         rvk_abi_version(void) { return RVK_ABI_VERSION; }
 
 int rvk_device_info(int* sms, char* name, int name_len)

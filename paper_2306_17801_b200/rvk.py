@@ -29,7 +29,7 @@ CG_RUNNING, CG_CONVERGED, CG_BREAKDOWN, CG_COMM_ERROR = 0, 1, 2, 3
 
 # every symbol include/rvk.h declares (checked by tests/test_abi.py)
 EXPORTS = [
-    "rvk_last_error", "rvk_abi_version", "rvk_device_info", "rvk_device_count", "rvk_set_device",
+    "rvk_last_error", "rvk_abi_version", "rvk_build_id", "rvk_device_info", "rvk_device_count", "rvk_set_device",
     "rvk_ctx_create", "rvk_ctx_destroy", "rvk_ctx_stream", "rvk_ctx_synchronize",
     "rvk_ctx_query_idle", "rvk_ctx_wait_for", "rvk_ctx_id", "rvk_ctx_set_name",
     "rvk_host_sync_count", "rvk_host_sync_reset",
@@ -115,6 +115,7 @@ def lib():
     sig = {
         "rvk_last_error": (C.c_char_p, []),
         "rvk_abi_version": (i, []),
+        "rvk_build_id": (C.c_char_p, []),
         "rvk_device_count": (i, []),
         "rvk_set_device": (i, [i]),
         "rvk_device_info": (i, [C.POINTER(C.c_int), C.c_char_p, i]),

@@ -38,12 +38,18 @@ def lib_sha16():
         return hashlib.sha256(f.read()).hexdigest()[:16]
 
 
+def build_id():
+    sys.path.insert(0, ROOT)
+    from paper_2306_17801_b200 import rvk
+    return rvk.lib().rvk_build_id().decode()
+
+
 def main(tag="r02"):
     # the captures in gpurun_out/ must come from the library now in the tree
     # (scripts/gpu_profiles.sh runs on the snapshot of this tree)
     out = {"_note": f"{tag}: ncu --set full --clock-control none, one launch each "
                     "(serialised, after 4 warm launches); per-launch DRAM bytes = traffic",
-           "lib_sha16": lib_sha16()}
+           "lib_sha16": lib_sha16(), "build_id": build_id()}
     for cfg, files in {"7pt256": {"k1": "prof_k1", "k2": "prof_k2"},
                        "7pt768": {"k1": "prof_k1_768"},
                        "27pt256": {"k1": "prof_k1_27pt"}, "9pt4096": {"k1": "prof_k1_9pt"},
