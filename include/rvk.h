@@ -257,7 +257,6 @@ typedef struct {
  *   RVK_OPT_X_EACH       fused solve: x updated in every iteration's K2
  *   RVK_OPT_MARCH        CSR plans with a plane structure: the plane-marching
  *                        K1 (RVK_PLAN_MARCH; opt-in)
- *   RVK_OPT_NO_MARCH     never the plane-marching K1
  *   RVK_OPT_NO_GRID      PERSISTENT mode: no one-launch grid solve for mid-size
  *                        systems (the generic grid-barrier kernel instead)   */
 #define RVK_OPT_KEEP_WORK   1
@@ -271,7 +270,6 @@ typedef struct {
 #define RVK_OPT_X_GROUP4    256
 #define RVK_OPT_X_EACH      512
 #define RVK_OPT_MARCH       1024
-#define RVK_OPT_NO_MARCH    2048
 #define RVK_OPT_NO_GRID     4096
 
 typedef struct {

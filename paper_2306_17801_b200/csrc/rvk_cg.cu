@@ -1394,12 +1394,21 @@ rvk_status rvk_cg_plan_create(rvk_ctx ctx, const rvk_csr* A, rvk_cg_config cfg, 
     if (csr_bands(ctx->stream, *A, &bands) != RVK_OK) bands = SpmvBands{};
     P->sa            = make_spmv_args(*A, maxlen, &bands);
     P->sa.small_rows = (cfg.opts & RVK_OPT_SMALL_K1) ? 512 * 1024 : 0;
+    {
+        // the matrix keeps normal L2 priority when it and the five vectors
+        // one iteration touches fit in 100 MB of the 126 MB L2 (re-read from
+        // L2 by every K1).  Measured, fused 5-point: 512^2 (47 MB) 0.336 ->
+        // 0.317 ms per solve; 1024^2 (111 MB, not kept) 0.618 ms either way,
+        // 0.685 ms if kept (L2 thrash).
+        const int64_t ws = A->nnz * 12 + (A->n_rows + 1) * 8 + A->n_rows * 40;
+        P->sa.csr_keep   = ws <= (int64_t)100 * 1024 * 1024 ? 1 : 0;
+    }
     P->spmv_grid = sm_count();
     // plane-marching K1 (opt-in): DRAM reads at the algorithmic minimum for
     // large 3D planes, but measured slower than the row-order kernel on B200
     // (768^3: 12.4-13.9 vs 10.3 ms per K1, profiles/r02/march_768.md), so
     // only RVK_OPT_MARCH selects it
-    if ((cfg.opts & RVK_OPT_MARCH) && !(cfg.opts & RVK_OPT_NO_MARCH) && bands.plane_q > 0)
+    if ((cfg.opts & RVK_OPT_MARCH) && bands.plane_q > 0)
         P->march = make_spmv_march(*A, maxlen, bands.plane_q, P->spmv_grid, &P->sa_m, &P->mg);
     // one resident wave each (the vectorised loops take 2 elements per thread)
     P->upd_grid   = resident_grid(k_cg_update<true, 1>, kUpdThreads, (A->n_rows + 1) / 2);

@@ -1016,7 +1016,7 @@ rvk_status rvk_dcg_plan_create(rvk_ctx ctx, const rvk_csr* A, rvk_shard sh, rvk_
         // plane stride: one halo = one plane (z-slab shards); a single shard
         // has no halo, its CSR diagonals give it (rvk_cg.cu csr_bands)
         const int64_t q = sh.halo_lo ? sh.halo_lo : (sh.halo_hi ? sh.halo_hi : bands.plane_q);
-        if ((cfg.opts & RVK_OPT_MARCH) && !(cfg.opts & RVK_OPT_NO_MARCH) && q > 0)
+        if ((cfg.opts & RVK_OPT_MARCH) && q > 0)
             P->march = make_spmv_march(*A, maxlen, q, sm_count(), &P->sa_m, &P->mg);
     }
     P->upd_grid    = resident_grid(k_dcg_update<1, true, 2, true>, kUpdThreads, (sh.n_own + 1) / 2);

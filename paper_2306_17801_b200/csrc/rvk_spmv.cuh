@@ -92,6 +92,8 @@ struct SpmvArgs {
     const int32_t* cols;
     const double*  vals;
     int64_t        small_rows; // > 0: systems up to this many rows use k_spmv_small (plan's choice)
+    int            csr_keep;   // 1: the CSR stream keeps normal L2 priority (it fits the L2 with
+                               //    the vectors and is re-read every iteration)
 
     size_t smem_bytes() const { return kSpmvHeaderBytes + (size_t)stages * stage_bytes; }
 };
@@ -409,7 +411,9 @@ __global__ void __launch_bounds__(kSpmvThreads, 1) k_spmv_tma(SpmvArgs A, Op op_
     if (tid < 32) {
         // ===================== producer warp =====================
         if (tid == 0) {
-            const uint64_t pol_stream = policy_evict_first(); // CSR: read once
+            // CSR: read once per launch -- evict first, unless the whole
+            // matrix stays L2-resident across the solve's launches
+            const uint64_t pol_stream = A.csr_keep ? policy_evict_normal() : policy_evict_first();
             int64_t        v   = blockIdx.x;
             int64_t        k0 = 0, k1 = 0; // slab bounds, prefetched one tile ahead
             if (v < A.n_tiles) {

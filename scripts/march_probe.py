@@ -14,7 +14,7 @@ b = O.rhs(A.n_rows)
 p1 = rvk.CgPlan(ctx, A, max_it=4, opts=opts)
 print("flags", p1.flags(), "march", bool(p1.flags() & rvk.PLAN_MARCH))
 x1, r1 = p1.solve_host(b)
-p0 = rvk.CgPlan(ctx, A, max_it=4, opts=rvk.OPT_NO_MARCH)
+p0 = rvk.CgPlan(ctx, A, max_it=4, opts=0)
 x0, r0 = p0.solve_host(b)
 print("hist rel", np.max(np.abs(r1.hist - r0.hist) / r0.hist), "x rel",
       np.linalg.norm(x1 - x0) / np.linalg.norm(x0))

@@ -29,7 +29,7 @@ def test_march_w_p_bitexact_vs_row_order(ctx, spec, zv):
     b = O.rhs(A.n_rows)
     zopt = rvk.OPT_Z_VIRTUAL if zv else rvk.OPT_Z_STORED
     out = {}
-    for name, opt in (("march", rvk.OPT_MARCH), ("rows", rvk.OPT_NO_MARCH)):
+    for name, opt in (("march", rvk.OPT_MARCH), ("rows", 0)):
         plan = rvk.CgPlan(ctx, A, max_it=2, opts=opt | zopt | rvk.OPT_KEEP_WORK)
         assert bool(plan.flags() & rvk.PLAN_MARCH) == (name == "march"), plan.flags()
         plan.solve_host(b)
@@ -109,7 +109,7 @@ def test_march_row_sharded(ctx, nranks, backend, pts):
                                  opts=rvk.OPT_MARCH, flags_out=flags)
     assert all(f & rvk.PLAN_MARCH for f in flags), flags
     x0, res0, _ = loopback_solve(ctx, 3, pts, g, nranks, b, max_it=20, backend=backend,
-                                 opts=rvk.OPT_NO_MARCH)
+                                 opts=0)
     assert res.iterations == 20
     eh = np.abs(res.hist - ref.hist) / ref.hist
     ex = np.linalg.norm(x - ref.x) / np.linalg.norm(ref.x)
