@@ -33,8 +33,19 @@ __device__ __forceinline__ double fold_slot(const double* partials, int j, doubl
 {
     const int tid = threadIdx.x;
     if (tid < 32) {
+        // all of a lane's loads first (grid <= 2 x 148 blocks: <= 10 per
+        // lane), then the adds in ascending block order
+        constexpr int kPer = (2 * 148 + 31) / 32;
+        double        pv[kPer];
+#pragma unroll
+        for (int q = 0; q < kPer; ++q) {
+            const int blk = tid + 32 * q;
+            pv[q]         = blk < (int)gridDim.x ? __ldcg(partials + blk * 4 + j) : 0.0;
+        }
         double v = 0.0;
-        for (int blk = tid; blk < (int)gridDim.x; blk += 32) v += __ldcg(partials + blk * 4 + j);
+#pragma unroll
+        for (int q = 0; q < kPer; ++q)
+            if (tid + 32 * q < (int)gridDim.x) v += pv[q];
         v = warp_sum(v);
         if (tid == 0) *sh = v;
     }
@@ -378,8 +389,11 @@ __global__ void __launch_bounds__(kCRows, 1) k_cg_cluster(PersistArgs a)
 // p is formed per gathered entry as in the fused K1.  Replaces the 41
 // launches of the fused graph, whose ~5 us per launch floor bounds 256^2 -
 // 512^2 solves.
-constexpr int kGThreads = 1024;
-constexpr int kGMaxR    = 3;   // rows per thread
+#ifndef RVK_GRID_THREADS
+#define RVK_GRID_THREADS 1024
+#endif
+constexpr int kGThreads = RVK_GRID_THREADS;
+constexpr int kGMaxR    = 3 * 1024 / kGThreads; // rows per thread (capacity 148 x 3072 rows)
 constexpr int kGMaxCta  = 148;
 
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p)
@@ -406,12 +420,27 @@ __device__ __forceinline__ void grid_reduce(double (&v)[NV], double* partials, u
     }
     __syncthreads();
     if (tid < 32) {
+        // every lane issues all its loads (<= 5 blocks x NV) before the first
+        // add: one L2 round trip instead of one per block; the adds keep the
+        // ascending block order
+        constexpr int kPer = (kGMaxCta + 31) / 32;
+        double        pv[kPer][NV];
+#pragma unroll
+        for (int q = 0; q < kPer; ++q) {
+            const int blk = tid + 32 * q;
+#pragma unroll
+            for (int j = 0; j < NV; ++j)
+                pv[q][j] = blk < (int)gridDim.x ? __ldcg(partials + blk * 4 + j) : 0.0;
+        }
         double f[NV];
 #pragma unroll
         for (int j = 0; j < NV; ++j) f[j] = 0.0;
-        for (int blk = tid; blk < (int)gridDim.x; blk += 32) {
 #pragma unroll
-            for (int j = 0; j < NV; ++j) f[j] = add(f[j], __ldcg(partials + blk * 4 + j));
+        for (int q = 0; q < kPer; ++q) {
+            if (tid + 32 * q < (int)gridDim.x) {
+#pragma unroll
+                for (int j = 0; j < NV; ++j) f[j] = add(f[j], pv[q][j]);
+            }
         }
 #pragma unroll
         for (int j = 0; j < NV; ++j) {
@@ -680,9 +709,10 @@ rvk_status launch_grid_solve(cudaStream_t s, const PersistArgs& args, unsigned* 
     };
 #define RVK_GRID_CASE(NZ, RR)                                                      \
     if (nz == NZ && R == RR) return go(k_cg_grid<NZ, RR>);
-    RVK_GRID_CASE(5, 1) RVK_GRID_CASE(5, 2) RVK_GRID_CASE(5, 3)
-    RVK_GRID_CASE(7, 1) RVK_GRID_CASE(7, 2) RVK_GRID_CASE(7, 3)
-    RVK_GRID_CASE(9, 1) RVK_GRID_CASE(9, 2) RVK_GRID_CASE(9, 3)
+#define RVK_GRID_NZ(NZ) RVK_GRID_CASE(NZ, 1) RVK_GRID_CASE(NZ, 2) RVK_GRID_CASE(NZ, 3) \
+    if constexpr (kGMaxR > 3) { RVK_GRID_CASE(NZ, 4) RVK_GRID_CASE(NZ, 5) RVK_GRID_CASE(NZ, 6) }
+    RVK_GRID_NZ(5) RVK_GRID_NZ(7) RVK_GRID_NZ(9)
+#undef RVK_GRID_NZ
 #undef RVK_GRID_CASE
     return set_error(RVK_ERR_INVALID, "grid solve: unsupported geometry (R %d, nz %d)", R, nz);
 }
