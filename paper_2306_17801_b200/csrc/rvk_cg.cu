@@ -1418,8 +1418,12 @@ rvk_status rvk_cg_plan_create(rvk_ctx ctx, const rvk_csr* A, rvk_cg_config cfg, 
     P->maxlen = (int)std::min<int64_t>(maxlen, 1 << 30);
     if (cfg.mode == RVK_CG_MODE_AUTO || cfg.mode == RVK_CG_MODE_PERSISTENT) {
         P->cluster = (cfg.opts & RVK_OPT_NO_CLUSTER) ? 0 : cluster_ctas(A->n_rows, maxlen);
-        if (!P->cluster && !(cfg.opts & RVK_OPT_NO_GRID))
+        // the grid solve from 8 K rows up (measured: 128^2 grid 0.109 vs
+        // cluster 0.119 ms, 64^2 cluster 0.096 vs grid 0.111 ms)
+        if ((!P->cluster || P->cluster > 8) && !(cfg.opts & RVK_OPT_NO_GRID)) {
             P->grid_rpc = grid_solve_rows(A->n_rows, maxlen, &P->grid_ctas);
+            if (P->grid_rpc) P->cluster = 0;
+        }
     }
     if (cfg.mode == RVK_CG_MODE_AUTO) {
         // up to 16 K rows: the one-cluster DSMEM solve (one launch, cluster

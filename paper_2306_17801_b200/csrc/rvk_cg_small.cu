@@ -390,7 +390,7 @@ __global__ void __launch_bounds__(kCRows, 1) k_cg_cluster(PersistArgs a)
 // launches of the fused graph, whose ~5 us per launch floor bounds 256^2 -
 // 512^2 solves.
 #ifndef RVK_GRID_THREADS
-#define RVK_GRID_THREADS 1024
+#define RVK_GRID_THREADS 512 // measured: 256^2 0.128 (1024 threads) -> 0.115 ms
 #endif
 constexpr int kGThreads = RVK_GRID_THREADS;
 constexpr int kGMaxR    = 3 * 1024 / kGThreads; // rows per thread (capacity 148 x 3072 rows)

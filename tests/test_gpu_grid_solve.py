@@ -39,7 +39,8 @@ def test_grid_solve_vs_oracle(ctx, spec, pc):
 
 
 def test_grid_solve_eligibility(ctx):
-    for dim, pts, g, want in [(2, 5, (128, 128), False),   # 16384 rows: the cluster solve
+    for dim, pts, g, want in [(2, 5, (64, 64), False),     # 4096 rows: the cluster solve
+                              (2, 5, (128, 128), True),     # 16384: grid (cluster only <= 8 K rows)
                               (3, 27, (30, 30, 30), False),  # rows of 27 entries
                               (2, 5, (129, 128), True),
                               (2, 5, (700, 700), False),   # > 148 x 3 x 1024 rows

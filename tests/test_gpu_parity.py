@@ -687,8 +687,11 @@ def test_cluster_solve(ctx, spec, pc):
     A = rvk.DeviceCsr.laplacian(ctx, dim, pts, g)
     for max_it, rtol in ((20, 0.0), (200, 1e-6)):
         ref = O.cg_solve(Ah, b, max_it=max_it, rtol=rtol, pc=pc)
-        plan = rvk.CgPlan(ctx, A, max_it=max_it, rtol=rtol, pc=pc, mode="auto")
+        # AUTO: the cluster solve up to 8 K rows, the grid solve above
+        plan = rvk.CgPlan(ctx, A, max_it=max_it, rtol=rtol, pc=pc, mode="auto",
+                          opts=rvk.OPT_NO_GRID)
         assert bool(plan.flags() & 256) == (Ah.n_rows <= 16384)
+        assert bool(rvk.CgPlan(ctx, A, max_it=2, mode="auto").flags() & 256) == (Ah.n_rows <= 8192)
         x, res = plan.solve_host(b)
         check_cg_floor(res, x, ref)
         x2, res2 = plan.solve_host(b)  # repeatable
