@@ -58,6 +58,33 @@ def test_cg_baseline_config_vs_serial_oracle(ctx, spec):
         assert eh < RTOL and ex < RTOL, (name, eh, ex)
 
 
+@pytest.mark.parametrize("spec", [(2, 9, (4096, 4096)), (3, 27, (256, 256, 256))],
+                         ids=["9pt4096", "27pt256"])
+def test_tfqmr_baseline_config_vs_serial_oracle(ctx, spec):
+    """Left-Jacobi TFQMR at the BASELINE sizes vs the
+    serial oracle (ro_tfqmr_solve, pinned to the reference kernels):
+    SPEC.md:474's 1e-8 on the history (entries at the recurrence's rounding
+    floor compared at 1e-14 of ||B r0||) and x."""
+    dim, pts, g = spec
+    Ah = O.build_laplacian(dim, pts, g)
+    b = O.rhs(Ah.n_rows)
+    ref = O.tfqmr_solve(Ah, b, max_it=20)
+    del Ah
+    gc.collect()
+    A = rvk.DeviceCsr.laplacian(ctx, dim, pts, g)
+    plan = rvk.TfqmrPlan(ctx, A, max_it=20)
+    db, dx = rvk.DeviceArray.from_host(ctx, b), rvk.DeviceArray(b.size)
+    plan.solve_dev(db, dx)
+    res = plan.result()
+    x = dx.download(ctx)
+    plan.close()
+    assert res.iterations == ref.iterations and res.state == ref.status
+    tol = 1e-8 * np.abs(ref.hist) + 1e-14 * ref.hist[0]
+    err = np.abs(res.hist - ref.hist)
+    print(f"TFQMR {dim}D {pts}-pt {g}: max hist err / tol {np.max(err / tol):.2e}, x {rel_x(x, ref.x):.2e}")
+    assert np.all(err <= tol) and rel_x(x, ref.x) < 1e-8
+
+
 G768 = (768, 768, 768)
 
 
