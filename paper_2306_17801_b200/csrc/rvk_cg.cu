@@ -687,6 +687,7 @@ struct rvk_cg_plan_s {
     SpmvArgs      sa_m{};                   // ... its ring geometry
     SpmvMarch     mg{};                     // ... and plane ranges
     int           spmv_grid = 0, upd_grid = 0, setup_grid = 0, persist_grid = 0;
+    int           xfix_grid = 0;             // k_cg_xfix: its own resident wave (46 registers)
     int           mode = RVK_CG_MODE_FUSED; // resolved (AUTO -> FUSED | PERSISTENT)
     int           cluster = 0;              // PERSISTENT: CTAs of the one-cluster DSMEM solve (0: grid barriers)
     int           grid_rpc = 0, grid_ctas = 0; // PERSISTENT: the one-launch grid solve (k_cg_grid), rows per CTA
@@ -843,7 +844,7 @@ rvk_status launch_xfix(rvk_cg_plan P, double* x, int npb, bool xzero = false)
     for (int k = 0; k < npb; ++k) pb.p[k] = P->p[k];
     // 4 p streams in flight per thread (measured 7-point 256^3, 20 p's:
     // 2 / 4 / 8 per batch = 500 / 475 / 492 us)
-    launch_k(k_cg_xfix<4>, P->upd_grid, kUpdThreads, 0, P->ctx->stream, P->A.n_rows, x, pb, npb,
+    launch_k(k_cg_xfix<4>, P->xfix_grid, kUpdThreads, 0, P->ctx->stream, P->A.n_rows, x, pb, npb,
                (const CgState*)P->st, xzero ? 1 : 0);
     RVK_CHECK_LAUNCH("k_cg_xfix");
     return RVK_OK;
@@ -1412,6 +1413,7 @@ rvk_status rvk_cg_plan_create(rvk_ctx ctx, const rvk_csr* A, rvk_cg_config cfg, 
         P->march = make_spmv_march(*A, maxlen, bands.plane_q, P->spmv_grid, &P->sa_m, &P->mg);
     // one resident wave each (the vectorised loops take 2 elements per thread)
     P->upd_grid   = resident_grid(k_cg_update<true, 1>, kUpdThreads, (A->n_rows + 1) / 2);
+    P->xfix_grid  = resident_grid(k_cg_xfix<4>, kUpdThreads, (A->n_rows + 1) / 2);
     P->setup_grid = resident_grid(k_cg_setup<true, 1>, kUpdThreads, (A->n_rows + 1) / 2);
     P->persist_grid = persistent_grid(A->n_rows);
     P->mode         = cfg.mode;
@@ -1545,6 +1547,7 @@ rvk_status rvk_cg_plan_create_stencil(rvk_ctx ctx, int dim, int points, int64_t 
     P->mf_grid    = mf_grid(P->geom);
     P->spmv_grid  = sm_count();
     P->upd_grid   = resident_grid(k_cg_update<true, 2>, kUpdThreads, (n + 1) / 2);
+    P->xfix_grid  = resident_grid(k_cg_xfix<4>, kUpdThreads, (n + 1) / 2);
     P->setup_grid = resident_grid(k_cg_setup<true, 2>, kUpdThreads, (n + 1) / 2);
     const size_t vb = (size_t)n * sizeof(double);
     cudaError_t  e  = cudaSuccess;

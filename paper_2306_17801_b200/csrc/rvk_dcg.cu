@@ -419,7 +419,9 @@ struct DcgSpmvOp {
 // pend_a[slot] -- the next iteration's pair flush, or with the whole-solve
 // ring the final k_cg_xfix; 2 x = (x + a' p_prev) + a p) -- bit-identical x.
 template <int PC, bool PEER, int XM = 0, bool VEC = false>
-__global__ void __launch_bounds__(kUpdThreads)
+// (3 blocks per SM: the register cap keeps the update's resident wave as
+// wide as the single-GPU k_cg_update's)
+__global__ void __launch_bounds__(kUpdThreads, 3)
     k_dcg_update(int64_t n, const double* __restrict__ p, const double* __restrict__ w,
                  const double* __restrict__ dinv, double dconst, double* __restrict__ x,
                  double* __restrict__ r,
@@ -626,7 +628,7 @@ struct rvk_dcg_plan_s {
     bool          march = false; // K1 (it >= 1) is k_spmv_march (RVK_PLAN_MARCH)
     SpmvArgs      sa_m{};
     SpmvMarch     mg{};
-    int           upd_grid = 0;
+    int           upd_grid = 0, xfix_grid = 0;
     int64_t       n_ext = 0;
     unsigned char* win = nullptr;  // [z | p0 | p1 | flags | gather], the exported PEER window
     size_t        win_bytes = 0;
@@ -847,7 +849,7 @@ rvk_status phase_xfix(rvk_dcg_plan P, double* x)
     if (!x_defer(P)) return RVK_OK;
     XBufs pb{};
     for (int k = 0; k < P->npb; ++k) pb.p[k] = P->p[k] + P->sh.halo_lo;
-    k_cg_xfix<4><<<P->upd_grid, kUpdThreads, 0, P->ctx->stream>>>(P->sh.n_own, x, pb, P->npb,
+    k_cg_xfix<4><<<P->xfix_grid, kUpdThreads, 0, P->ctx->stream>>>(P->sh.n_own, x, pb, P->npb,
                                                                    P->st, x_solve(P) ? 1 : 0);
     RVK_CHECK_LAUNCH("k_cg_xfix");
     return RVK_OK;
@@ -1020,6 +1022,7 @@ rvk_status rvk_dcg_plan_create(rvk_ctx ctx, const rvk_csr* A, rvk_shard sh, rvk_
             P->march = make_spmv_march(*A, maxlen, q, sm_count(), &P->sa_m, &P->mg);
     }
     P->upd_grid    = resident_grid(k_dcg_update<1, true, 2, true>, kUpdThreads, (sh.n_own + 1) / 2);
+    P->xfix_grid   = resident_grid(k_cg_xfix<4>, kUpdThreads, (sh.n_own + 1) / 2);
     P->owns_gather = shared_gather == nullptr;
     P->gather      = shared_gather;
     rvk_status rc  = alloc_plan_buffers(P);
