@@ -421,9 +421,11 @@ __global__ void __launch_bounds__(kSpmvThreads, 1) k_spmv_tma(SpmvArgs A, Op op_
                 k0 = (int64_t)__ldg(OFF + t * A.R);
                 k1 = (int64_t)__ldg(OFF + min(t * A.R + A.R, A.n_rows));
             }
+            // stage / phase counters kept incrementally: a run-time division
+            // per tile costs more than the tile's address arithmetic
+            int s = 0, ph = 0;
             for (int j = 0; v < A.n_tiles; ++j, v += gridDim.x) {
-                const int s = j % A.stages;
-                if (j >= A.stages) mbar_wait(&empty[s], ((j / A.stages) - 1) & 1);
+                if (j >= A.stages) mbar_wait(&empty[s], ph ^ 1);
                 const int64_t t  = v;
                 const int64_t r0 = t * A.R;
                 const int64_t r1 = min(r0 + A.R, A.n_rows);
@@ -441,19 +443,24 @@ __global__ void __launch_bounds__(kSpmvThreads, 1) k_spmv_tma(SpmvArgs A, Op op_
                 m.kv0                = kv0;
                 m.kc0                = kc0;
                 m.direct             = direct ? 1 : 0;
+                const int cur        = s;
+                if (++s == A.stages) {
+                    s  = 0;
+                    ph ^= 1;
+                }
                 if (direct) {
-                    mbar_arrive(&full[s]);
+                    mbar_arrive(&full[cur]);
                     continue;
                 }
-                unsigned char* st = stage0 + (size_t)s * A.stage_bytes;
+                unsigned char* st = stage0 + (size_t)cur * A.stage_bytes;
                 // R+2 offsets (a 16-B multiple; the last tile is direct)
                 const uint32_t ob = (uint32_t)((A.R + 2) * 8);
                 const uint32_t vb = (uint32_t)((kv1 - kv0) * 8);
                 const uint32_t cb = (uint32_t)((kc1 - kc0) * 4);
-                mbar_arrive_expect_tx(&full[s], ob + vb + cb);
-                bulk_g2s(st, OFF + r0, ob, &full[s], pol_stream);
-                if (vb) bulk_g2s(st + A.off_bytes, A.vals + kv0, vb, &full[s], pol_stream);
-                if (cb) bulk_g2s(st + A.off_bytes + A.val_bytes, A.cols + kc0, cb, &full[s], pol_stream);
+                mbar_arrive_expect_tx(&full[cur], ob + vb + cb);
+                bulk_g2s(st, OFF + r0, ob, &full[cur], pol_stream);
+                if (vb) bulk_g2s(st + A.off_bytes, A.vals + kv0, vb, &full[cur], pol_stream);
+                if (cb) bulk_g2s(st + A.off_bytes + A.val_bytes, A.cols + kc0, cb, &full[cur], pol_stream);
                 // leading edge of this CTA's NEXT tile: its highest-diagonal
                 // columns are first-touch DRAM misses for the gathers; start
                 // them now (L2 prefetch, no smem, no barrier)
@@ -482,13 +489,13 @@ __global__ void __launch_bounds__(kSpmvThreads, 1) k_spmv_tma(SpmvArgs A, Op op_
     static_assert(NS >= 1 && NS <= 4, "at most 4 fused reductions");
     spmv_acc_t<Op> acc{};
     int64_t   v     = blockIdx.x + (int64_t)group * gridDim.x;
-    for (int j = group; v < A.n_tiles; j += A.groups, v += (int64_t)A.groups * gridDim.x) {
-        const int s = j % A.stages;
-        const int64_t t = v;
-        mbar_wait(&full[s], (j / A.stages) & 1);
+    int       s     = group, ph = 0; // stage / phase, advanced by the group count (it divides the ring)
+    for (; v < A.n_tiles; v += (int64_t)A.groups * gridDim.x) {
+        mbar_wait(&full[s], ph);
+        const SpmvStageMeta& m = meta[s];
+        const int64_t t    = v;
         const int64_t r0   = t * A.R;
         const int     rows = (int)min((int64_t)A.R, A.n_rows - r0);
-        const SpmvStageMeta& m = meta[s];
         if (m.direct) {
             acc = spmv_rows_direct<U>(op, acc, gtid, gs, rows, r0, OFF + r0, A.cols, A.vals);
         } else {
@@ -503,6 +510,10 @@ __global__ void __launch_bounds__(kSpmvThreads, 1) k_spmv_tma(SpmvArgs A, Op op_
         }
         __syncwarp();
         if ((ctid & 31) == 0) mbar_arrive(&empty[s]);
+        if ((s += A.groups) >= A.stages) {
+            s -= A.stages;
+            ph ^= 1;
+        }
     }
 
     if constexpr (Op::kHasTail) {
