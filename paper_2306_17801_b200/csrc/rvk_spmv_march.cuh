@@ -157,6 +157,7 @@ __global__ void __launch_bounds__(kSpmvThreads, 1)
             const uint64_t pol_stream = policy_evict_first();
             const uint64_t pol_keep   = policy_evict_normal();
             int            j          = 0;
+            int            s = 0, ph = 0; // ring slot / phase of tile j (no per-tile division)
             for (int pass = 0; pass < M.passes; ++pass) {
             int64_t a;
             int     L;
@@ -164,8 +165,7 @@ __global__ void __launch_bounds__(kSpmvThreads, 1)
             const int T = (L + A.R - 1) / A.R; // tiles per plane step
             for (int64_t k = 0; k < M.K; ++k) {
                 for (int t = 0; t < T; ++t, ++j) {
-                    const int s = j % A.stages;
-                    if (j >= A.stages) mbar_wait(&empty[s], ((j / A.stages) - 1) & 1);
+                    if (j >= A.stages) mbar_wait(&empty[s], ph ^ 1);
                     int64_t r0, r1;
                     march_tile(A, M, a, L, k, t, &r0, &r1);
                     SpmvStageMeta& m = meta[s];
@@ -211,6 +211,10 @@ __global__ void __launch_bounds__(kSpmvThreads, 1)
                                      pol_keep);
                         }
                     }
+                    if (++s == A.stages) {
+                        s  = 0;
+                        ph ^= 1;
+                    }
                 }
             }
             }
@@ -227,6 +231,7 @@ __global__ void __launch_bounds__(kSpmvThreads, 1)
 
     const int cs = (int)op.own_col(0);
     int       j  = 0;
+    int       rs = 0, rph = 0, rg = 0; // ring slot, phase and owning group of tile j
     for (int pass = 0; pass < M.passes; ++pass) {
     int64_t a;
     int     L;
@@ -247,9 +252,15 @@ __global__ void __launch_bounds__(kSpmvThreads, 1)
         double*       Cn   = cache + (size_t)((k + 1) % 3) * M.Lmax;
         const int64_t base = k * M.Q + a;
         for (int t = 0; t < T; ++t, ++j) {
-            if (j % A.groups != group) continue;
-            const int s = j % A.stages;
-            mbar_wait(&full[s], (j / A.stages) & 1);
+            const int s = rs, mine = rg == group;
+            const int phs = rph;
+            if (++rs == A.stages) {
+                rs  = 0;
+                rph ^= 1;
+            }
+            if (++rg == A.groups) rg = 0;
+            if (!mine) continue;
+            mbar_wait(&full[s], phs);
             int64_t r0, r1;
             march_tile(A, M, a, L, k, t, &r0, &r1);
             const int            rows = (int)(r1 - r0);
