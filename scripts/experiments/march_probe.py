@@ -1,7 +1,7 @@
 """One plane-marching CG solve on a 3D 7-point grid (argv: nx ny nz [opts]),
 checked against the row-order plan: used under compute-sanitizer."""
 import sys, os
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np
 from paper_2306_17801_b200 import rvk
 import oracle as O
