@@ -40,6 +40,9 @@ CONFIGS = {
     "5pt128": (2, 5, (128, 128), "2D 5-point Laplacian 128x128 (latency sweep)"),
     "5pt256": (2, 5, (256, 256), "2D 5-point Laplacian 256x256 (latency sweep)"),
     "5pt512": (2, 5, (512, 512), "2D 5-point Laplacian 512x512 (latency sweep)"),
+    "5pt768": (2, 5, (768, 768), "2D 5-point Laplacian 768x768 (latency sweep)"),
+    "9pt1024": (2, 9, (1024, 1024), "2D 9-point Laplacian 1024x1024 (grid-solve study)"),
+    "7pt100": (3, 7, (100, 100, 100), "3D 7-point Laplacian 100^3 (grid-solve study)"),
 }
 METRIC = "20-iter Jacobi-CG solve time, achieved HBM GB/s vs peak, host syncs/iter"
 MAX_IT = 20
@@ -716,8 +719,9 @@ def main():
     ap.add_argument("--impl", choices=["rvk", "reference"], default="rvk")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="7pt256")
     ap.add_argument("--mode", choices=["fused", "unfused", "persistent", "auto", "hostsync"],
-                    default="auto", help="auto: the one-cluster solve for <= 16 K rows, "
-                                         "else the fused 2-kernel/iteration graph")
+                    default="auto", help="auto: the one-cluster solve for <= 8 K rows, the one-launch "
+                                         "grid solve up to 148 x 8 K rows, else the fused "
+                                         "2-kernel/iteration graph")
     ap.add_argument("--operator", choices=["csr", "stencil"], default="csr",
                     help="csr: the AIJ/CSR operator (headline); stencil: matrix-free (SURVEY 8f)")
     ap.add_argument("--no-graph", action="store_true")

@@ -258,7 +258,9 @@ typedef struct {
  *   RVK_OPT_MARCH        CSR plans with a plane structure: the plane-marching
  *                        K1 (RVK_PLAN_MARCH; opt-in)
  *   RVK_OPT_NO_GRID      PERSISTENT mode: no one-launch grid solve for mid-size
- *                        systems (the generic grid-barrier kernel instead)   */
+ *                        systems (the generic grid-barrier kernel instead)
+ *   RVK_OPT_NO_GRID_L2   no grid solve over the global ELL copy (RVK_PLAN_GRID_L2):
+ *                        AUTO runs those systems as the fused graph          */
 #define RVK_OPT_KEEP_WORK   1
 #define RVK_OPT_DINV_VECTOR 2
 #define RVK_OPT_Z_STORED    4
@@ -271,6 +273,7 @@ typedef struct {
 #define RVK_OPT_X_EACH      512
 #define RVK_OPT_MARCH       1024
 #define RVK_OPT_NO_GRID     4096
+#define RVK_OPT_NO_GRID_L2  8192
 
 typedef struct {
     int state;          /* rvk_cg_state: RUNNING here means "ran max_it"     */
@@ -339,6 +342,10 @@ rvk_status rvk_cg_solve_host_many(rvk_cg_plan plan, int nrhs, const double* cons
                                     ~450 K rows, rows <= 9 entries): CSR in shared memory, row
                                     vectors in registers, 2 grid barriers per iteration
                                     (RVK_OPT_NO_GRID disables)                                  */
+#define RVK_PLAN_GRID_L2    4096 /* ... for 3 K - 8 K rows per CTA (up to 148 x 8 K rows; 1024^2):
+                                    the matrix from a plan-owned k-major ELL copy in global
+                                    memory (L2-resident), x / r / p in shared memory
+                                    (RVK_OPT_NO_GRID_L2 disables)                               */
 #define RVK_PLAN_Z_VIRTUAL  32  /* fused solve never stores z = d r (constant diagonal / no PC):
                                    the SpMV gathers r and forms d r (bit-identical;
                                    RVK_OPT_Z_STORED / RVK_OPT_Z_VIRTUAL override)               */

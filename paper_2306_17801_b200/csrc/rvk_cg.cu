@@ -692,6 +692,9 @@ struct rvk_cg_plan_s {
     int           cluster = 0;              // PERSISTENT: CTAs of the one-cluster DSMEM solve (0: grid barriers)
     int           grid_rpc = 0, grid_ctas = 0; // PERSISTENT: the one-launch grid solve (k_cg_grid), rows per CTA
     unsigned*     gbar = nullptr;            // ... its arrival counter
+    bool          grid_l2 = false;           // ... past the shared-memory ELL: k_cg_grid_l2 over ell
+    GridEll       ell{};
+    void*         ell_buf = nullptr;
     int           maxlen  = 0;              // longest row
     bool          k2_last = false;          // enqueue_fused: the K2 being launched is the solve's last
     bool          stencil = false;          // matrix-free operator (rvk_cg_plan_create_stencil)
@@ -1180,7 +1183,7 @@ rvk_status enqueue_persistent(rvk_cg_plan P, const double* b, double* x)
         return launch_cluster(P->ctx->stream, a, P->cfg.pc == RVK_PC_JACOBI, P->cluster, P->maxlen);
     if (P->grid_rpc)
         return launch_grid_solve(P->ctx->stream, a, P->gbar, P->cfg.pc == RVK_PC_JACOBI, P->grid_rpc,
-                                 P->grid_ctas, P->maxlen);
+                                 P->grid_ctas, P->maxlen, P->grid_l2 ? &P->ell : nullptr);
     return launch_persistent(P->ctx->stream, a, P->cfg.pc == RVK_PC_JACOBI, P->persist_grid);
 }
 
@@ -1423,7 +1426,15 @@ rvk_status rvk_cg_plan_create(rvk_ctx ctx, const rvk_csr* A, rvk_cg_config cfg, 
         // the grid solve from 8 K rows up (measured: 128^2 grid 0.109 vs
         // cluster 0.119 ms, 64^2 cluster 0.096 vs grid 0.111 ms)
         if ((!P->cluster || P->cluster > 8) && !(cfg.opts & RVK_OPT_NO_GRID)) {
-            P->grid_rpc = grid_solve_rows(A->n_rows, maxlen, &P->grid_ctas);
+            int l2      = 0;
+            P->grid_rpc = grid_solve_rows(A->n_rows, maxlen, &P->grid_ctas, &l2);
+            if (l2 && (cfg.opts & RVK_OPT_NO_GRID_L2)) P->grid_rpc = 0;
+            // AUTO takes the L2 grid solve up to 4 K rows per CTA (8 rows per
+            // thread): measured 5-point 768^2 0.315 vs fused 0.421 ms; at
+            // 1024^2 (7 K rows per CTA, 97 MB of ELL + vectors, L2 hit 70%)
+            // 0.700 vs fused 0.589 ms -- explicit PERSISTENT still runs it
+            if (l2 && cfg.mode == RVK_CG_MODE_AUTO && P->grid_rpc > 4096) P->grid_rpc = 0;
+            P->grid_l2 = P->grid_rpc && l2;
             if (P->grid_rpc) P->cluster = 0;
         }
     }
@@ -1458,11 +1469,31 @@ rvk_status rvk_cg_plan_create(rvk_ctx ctx, const rvk_csr* A, rvk_cg_config cfg, 
     alloc(reinterpret_cast<void**>(&P->tickets), 16 * sizeof(unsigned int));
     alloc(reinterpret_cast<void**>(&P->tmp), 16 * sizeof(double));
     alloc(reinterpret_cast<void**>(&P->gbar), 16 * sizeof(unsigned));
+    size_t ell_c_at = 0, ell_n_at = 0;
+    if (P->grid_l2) {
+        // k-major ELL of the matrix for k_cg_grid_l2 (values, columns, lengths)
+        const size_t nz = P->maxlen <= 5 ? 5 : (P->maxlen <= 7 ? 7 : 9);
+        ell_c_at        = (nz * vb + 255) / 256 * 256;
+        ell_n_at        = ell_c_at + (nz * (size_t)A->n_rows * 4 + 255) / 256 * 256;
+        alloc(&P->ell_buf, ell_n_at + (size_t)A->n_rows);
+    }
     if (e != cudaSuccess) {
         rvk_cg_plan_destroy(P);
         return cuda_error(e, "rvk_cg_plan_create: allocation");
     }
     cudaStream_t s = ctx->stream;
+    if (P->grid_l2) {
+        unsigned char* base = static_cast<unsigned char*>(P->ell_buf);
+        P->ell.v            = reinterpret_cast<double*>(base);
+        P->ell.c            = reinterpret_cast<int32_t*>(base + ell_c_at);
+        P->ell.n            = base + ell_n_at;
+        const rvk_status bs = build_grid_ell(s, A->n_rows, A->row_offsets, A->col_indices, A->values, P->maxlen,
+                                             P->ell.v, P->ell.c, P->ell.n);
+        if (bs != RVK_OK) {
+            rvk_cg_plan_destroy(P);
+            return bs;
+        }
+    }
     e              = cudaMemsetAsync(P->tickets, 0, 16 * sizeof(unsigned int), s);
     if (e == cudaSuccess) e = cudaMemsetAsync(P->p[0], 0, vb, s);
     if (e == cudaSuccess) e = cudaMemsetAsync(P->p[1], 0, vb, s);
@@ -1503,6 +1534,7 @@ int rvk_cg_plan_flags(rvk_cg_plan P)
            ((P->mode == RVK_CG_MODE_FUSED && x_defer(P, true) && P->xq > 4) ? RVK_PLAN_X_SOLVE : 0) |
            ((P->mode == RVK_CG_MODE_PERSISTENT && P->cluster) ? RVK_PLAN_CLUSTER : 0) |
            ((P->mode == RVK_CG_MODE_PERSISTENT && P->grid_rpc) ? RVK_PLAN_GRID : 0) |
+           ((P->mode == RVK_CG_MODE_PERSISTENT && P->grid_rpc && P->grid_l2) ? RVK_PLAN_GRID_L2 : 0) |
            (fold_setup(P, nullptr) ? RVK_PLAN_FOLD_SETUP : 0) |
            (P->zv ? RVK_PLAN_Z_VIRTUAL : 0) |
            ((P->march && !P->stencil && P->mode != RVK_CG_MODE_PERSISTENT) ? RVK_PLAN_MARCH : 0);
@@ -1596,7 +1628,7 @@ rvk_status rvk_cg_plan_destroy(rvk_cg_plan P)
     if (P->s_out) cudaStreamDestroy(P->s_out);
     void* bufs[] = {P->dinv, P->r, P->z, P->w, P->hist, P->st,
                     P->partials, P->tickets, P->tmp, P->b_buf, P->x_buf, P->b_buf2,
-                    P->x_buf2, P->hist_all, P->st_all, P->gbar};
+                    P->x_buf2, P->hist_all, P->st_all, P->gbar, P->ell_buf};
     for (void* b : bufs)
         if (b) cudaFree(b);
     for (double* b : P->p)

@@ -183,9 +183,18 @@ int        cluster_ctas(int64_t n, int64_t max_row_len);
 rvk_status launch_cluster(cudaStream_t s, const PersistArgs& args, bool jacobi, int ctas, int max_row_len);
 // one-launch grid solve for mid-size grids (rvk_cg_small.cu): rows per CTA or
 // 0 (not eligible); bar = a plan-owned arrival counter (zeroed per launch)
-int        grid_solve_rows(int64_t n, int64_t max_row_len, int* ctas);
+// (*l2 = 1: the rows' ELL exceeds the shared memory -> k_cg_grid_l2 over
+// a plan-owned k-major ELL copy built by build_grid_ell, passed as ell)
+struct GridEll {
+    double*  v = nullptr; // [nz][n] values
+    int32_t* c = nullptr; // [nz][n] columns
+    uint8_t* n = nullptr; // [n] row lengths
+};
+int        grid_solve_rows(int64_t n, int64_t max_row_len, int* ctas, int* l2);
+rvk_status build_grid_ell(cudaStream_t s, int64_t n, const int64_t* off, const int32_t* cols,
+                          const double* vals, int max_row_len, double* ev, int32_t* ec, uint8_t* en);
 rvk_status launch_grid_solve(cudaStream_t s, const PersistArgs& args, unsigned* bar, bool jacobi,
-                             int rpc, int ctas, int max_row_len);
+                             int rpc, int ctas, int max_row_len, const GridEll* ell);
 
 // After the last iteration (or an early exit): apply the updates DEFER K2s
 // left pending, in iteration order: x = ((x + a_0 p_0) + a_1 p_1) + ... .

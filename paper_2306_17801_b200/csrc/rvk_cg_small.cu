@@ -395,6 +395,7 @@ __global__ void __launch_bounds__(kCRows, 1) k_cg_cluster(PersistArgs a)
 constexpr int kGThreads = RVK_GRID_THREADS;
 constexpr int kGMaxR    = 3 * 1024 / kGThreads; // rows per thread (capacity 148 x 3072 rows)
 constexpr int kGMaxCta  = 148;
+constexpr int kG2MaxRpc = 8192; // k_cg_grid_l2: x, r, p in shared memory (8 K rows: 200 KB)
 
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p)
 {
@@ -601,6 +602,167 @@ __global__ void __launch_bounds__(kGThreads, 1)
     }
 }
 
+// Plan-time ELL copy for the L2 grid solve: k-major (entry k of row i at
+// k * n + i, so a warp's 32 rows read 32 consecutive words per k), row
+// lengths in bytes.  Entries past a row's length are never read.
+__global__ void k_ell_build(int64_t n, const int64_t* __restrict__ off, const int32_t* __restrict__ cols,
+                            const double* __restrict__ vals, int nz, double* ev, int32_t* ec, uint8_t* en)
+{
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t kb = off[i];
+        const int     c  = (int)(off[i + 1] - kb);
+        for (int k = 0; k < c; ++k) {
+            ev[k * n + i] = vals[kb + k];
+            ec[k * n + i] = cols[kb + k];
+        }
+        en[i] = (uint8_t)c;
+    }
+}
+
+// The grid solve past the shared-memory ELL's reach (3 K .. 8 K rows per CTA:
+// 1024^2 5-point = 7104).  The matrix comes from the plan's k-major ELL copy
+// in global memory (63 MB at 1024^2 5-point: with z and the two p's, 88 MB,
+// L2-resident across iterations); x, r and p of the CTA's rows live in
+// shared memory, w in registers (R rows per thread).  Same barriers, same
+// fold order and element arithmetic as k_cg_grid; the own row's z is formed
+// from r (z = d r, the value K2 stores) instead of being kept.
+template <int NZ, int R>
+__global__ void __launch_bounds__(kGThreads, 1)
+    k_cg_grid_l2(PersistArgs a, unsigned* bar, int rpc, const double* __restrict__ ev,
+                 const int32_t* __restrict__ ec, const uint8_t* __restrict__ en)
+{
+    extern __shared__ __align__(16) unsigned char gsm[];
+    double*  xs  = reinterpret_cast<double*>(gsm);
+    double*  rs  = xs + rpc;
+    double*  ps  = rs + rpc;
+    uint8_t* cs  = reinterpret_cast<uint8_t*>(ps + rpc);
+    __shared__ double red[128], out_sh[4];
+    const int      tid  = threadIdx.x;
+    const bool     lead = blockIdx.x == 0 && tid == 0;
+    const int64_t  n    = a.n;
+    const int64_t  r0   = (int64_t)blockIdx.x * rpc;
+    const int      nown = (int)(n - r0 < rpc ? n - r0 : rpc); // rows of this CTA
+    unsigned       nbar = 0;
+    const unsigned G    = gridDim.x;
+
+    // ---- setup: r = b, x = 0, z = B r; z.z, z.r ------------------------------
+    double acc[2] = {0.0, 0.0};
+#pragma unroll
+    for (int m = 0; m < R; ++m) {
+        const int j = tid + m * kGThreads;
+        if (j >= nown) continue;
+        const int64_t i  = r0 + j;
+        const double  ri = a.b[i];
+        const double  zi = mul(a.dinv[i], ri);
+        xs[j] = 0.0;
+        rs[j] = ri;
+        ps[j] = 0.0;
+        cs[j] = en[i];
+        a.z[i] = zi;
+        acc[0] = add(acc[0], mul(zi, zi));
+        acc[1] = add(acc[1], mul(zi, ri));
+    }
+    grid_reduce<2>(acc, a.partials, bar, ++nbar * G, red, out_sh);
+    double       beta = acc[1];
+    const double dp0  = sqrt(acc[0]);
+    int          state = RVK_CG_RUNNING, iters = 0, bk = -1;
+    double       alpha = 0.0, pAp = 0.0, betaold = 0.0, dp = dp0;
+    if (cg_converged(dp0, dp0, a.rtol, a.atol)) state = RVK_CG_CONVERGED;
+
+    for (int it = 0; it < a.max_it && state == RVK_CG_RUNNING; ++it) {
+        double bb = 0.0;
+        if (it > 0) {
+            if (betaold == 0.0) {
+                state = RVK_CG_BREAKDOWN;
+                bk    = it;
+                break;
+            }
+            bb = beta / betaold;
+        }
+        const double* po = (it & 1) ? a.p1 : a.p0;
+        double*       pn = (it & 1) ? a.p0 : a.p1;
+        double w[R];
+        double pw = 0.0;
+#pragma unroll
+        for (int m = 0; m < R; ++m) {
+            w[m]        = 0.0;
+            const int j = tid + m * kGThreads;
+            if (j >= nown) continue;
+            const int64_t i   = r0 + j;
+            const int     cnt = cs[j];
+            int32_t       c[NZ];
+            double        v[NZ], zj[NZ], pj[NZ];
+#pragma unroll
+            for (int k = 0; k < NZ; ++k) {
+                c[k] = k < cnt ? __ldg(ec + k * n + i) : 0;
+                v[k] = k < cnt ? __ldg(ev + k * n + i) : 0.0;
+            }
+#pragma unroll
+            for (int k = 0; k < NZ; ++k) {
+                zj[k] = __ldcg(a.z + c[k]);
+                pj[k] = it == 0 ? 0.0 : __ldcg(po + c[k]);
+            }
+#pragma unroll
+            for (int k = 0; k < NZ; ++k)
+                if (k < cnt) w[m] = add(w[m], mul(v[k], it == 0 ? zj[k] : aypx1(bb, zj[k], pj[k])));
+            const double zi = mul(__ldg(a.dinv + i), rs[j]);
+            const double pv = it == 0 ? zi : aypx1(bb, zi, ps[j]);
+            ps[j] = pv;
+            pn[i] = pv;
+            pw    = add(pw, mul(pv, w[m]));
+        }
+        double v1[1] = {pw};
+        grid_reduce<1>(v1, a.partials, bar, ++nbar * G, red, out_sh);
+        pAp             = v1[0];
+        const double al = beta / pAp;
+        if (pAp == 0.0 || !isfinite(al)) {
+            state = RVK_CG_BREAKDOWN;
+            bk    = it;
+            break;
+        }
+        alpha   = al;
+        betaold = beta;
+        // ---- x += a p, r += (-a) w, z = B r; z.z, z.r ------------------------
+        acc[0] = acc[1] = 0.0;
+#pragma unroll
+        for (int m = 0; m < R; ++m) {
+            const int j = tid + m * kGThreads;
+            if (j >= nown) continue;
+            const int64_t i  = r0 + j;
+            xs[j]            = axpy1(al, ps[j], xs[j]);
+            const double ri  = axpy1(-al, w[m], rs[j]);
+            const double zi  = mul(__ldg(a.dinv + i), ri);
+            rs[j]            = ri;
+            a.z[i]           = zi;
+            acc[0]           = add(acc[0], mul(zi, zi));
+            acc[1]           = add(acc[1], mul(zi, ri));
+        }
+        grid_reduce<2>(acc, a.partials, bar, ++nbar * G, red, out_sh);
+        dp    = sqrt(acc[0]);
+        iters = it + 1;
+        if (lead) a.hist[it + 1] = dp;
+        if (cg_converged(dp, dp0, a.rtol, a.atol)) state = RVK_CG_CONVERGED;
+        beta = acc[1];
+    }
+    for (int j = tid; j < nown; j += kGThreads) {
+        a.x[r0 + j] = xs[j];
+        a.r[r0 + j] = rs[j];
+    }
+    if (lead) {
+        a.hist[0]            = dp0;
+        a.st->dp0            = dp0;
+        a.st->dp             = dp;
+        a.st->alpha          = alpha;
+        a.st->pAp            = pAp;
+        a.st->beta           = beta;
+        a.st->betaold        = betaold;
+        a.st->iterations     = iters;
+        a.st->breakdown_iter = bk;
+        a.st->state          = state;
+        a.st->done           = 1;
+    }
+}
+
 } // namespace
 
 int persistent_grid(int64_t n)
@@ -678,28 +840,58 @@ rvk_status launch_persistent(cudaStream_t s, const PersistArgs& args, bool jacob
 namespace rvk {
 
 // Grid-solve geometry: rows per CTA (32-aligned) and CTAs, or 0 when the
-// system does not qualify (rows > 9 entries, more than 148 x 3 x 1024 rows,
-// or the ELL rows do not fit the shared memory).
-int grid_solve_rows(int64_t n, int64_t max_row_len, int* ctas)
+// system does not qualify (rows > 9 entries or more than 148 x 8 K rows).
+// *l2 = 1: the rows' ELL does not fit the shared memory (more than 3 K rows
+// per CTA, or the ELL bytes), so the solve reads the plan's global ELL copy
+// (k_cg_grid_l2, x / r / p in shared memory).
+int grid_solve_rows(int64_t n, int64_t max_row_len, int* ctas, int* l2)
 {
     if (n < 1 || max_row_len > kCMaxNnz) return 0;
     const int     nz  = max_row_len <= 5 ? 5 : (max_row_len <= 7 ? 7 : 9);
     const int64_t rpc = ((n + kGMaxCta - 1) / kGMaxCta + 31) / 32 * 32;
-    if (rpc > (int64_t)kGMaxR * kGThreads) return 0;
+    if (rpc > kG2MaxRpc) return 0;
     const size_t smem = (size_t)rpc * nz * 12 + rpc;
-    if (smem > 220 * 1024) return 0;
-    *ctas = (int)((n + rpc - 1) / rpc);
+    *l2               = (rpc > (int64_t)kGMaxR * kGThreads || smem > 220 * 1024) ? 1 : 0;
+    *ctas             = (int)((n + rpc - 1) / rpc);
     return (int)rpc;
 }
 
+rvk_status build_grid_ell(cudaStream_t s, int64_t n, const int64_t* off, const int32_t* cols,
+                          const double* vals, int max_row_len, double* ev, int32_t* ec, uint8_t* en)
+{
+    const int nz = max_row_len <= 5 ? 5 : (max_row_len <= 7 ? 7 : 9);
+    k_ell_build<<<(int)std::min<int64_t>((n + 255) / 256, 4 * 148 * 8), 256, 0, s>>>(n, off, cols, vals, nz, ev,
+                                                                                     ec, en);
+    RVK_CHECK_LAUNCH("k_ell_build");
+    return RVK_OK;
+}
+
 rvk_status launch_grid_solve(cudaStream_t s, const PersistArgs& args, unsigned* bar, bool jacobi,
-                             int rpc, int ctas, int max_row_len)
+                             int rpc, int ctas, int max_row_len, const GridEll* ell)
 {
     (void)jacobi; // the plan's dinv is 1.0 without a preconditioner
     const int    nz   = max_row_len <= 5 ? 5 : (max_row_len <= 7 ? 7 : 9);
     const int    R    = (rpc + kGThreads - 1) / kGThreads;
-    const size_t smem = (size_t)rpc * nz * 12 + rpc;
     RVK_CUDA(cudaMemsetAsync(bar, 0, sizeof(unsigned), s));
+    if (ell) {
+        const size_t smem    = (size_t)rpc * 24 + rpc;
+        void*        kargs[] = {const_cast<PersistArgs*>(&args), &bar, &rpc, const_cast<double**>(&ell->v),
+                                const_cast<int32_t**>(&ell->c), const_cast<uint8_t**>(&ell->n)};
+        auto go = [&](auto fn) -> rvk_status {
+            RVK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+            RVK_CUDA(cudaLaunchCooperativeKernel((const void*)fn, dim3(ctas), dim3(kGThreads), kargs, smem, s));
+            return RVK_OK;
+        };
+        const int Ri = R <= 8 ? 8 : (R <= 12 ? 12 : 16);
+#define RVK_GRID2_CASE(NZ, RR)                                                        \
+        if (nz == NZ && Ri == RR) return go(k_cg_grid_l2<NZ, RR>);
+        RVK_GRID2_CASE(5, 8) RVK_GRID2_CASE(5, 12) RVK_GRID2_CASE(5, 16)
+        RVK_GRID2_CASE(7, 8) RVK_GRID2_CASE(7, 12) RVK_GRID2_CASE(7, 16)
+        RVK_GRID2_CASE(9, 8) RVK_GRID2_CASE(9, 12) RVK_GRID2_CASE(9, 16)
+#undef RVK_GRID2_CASE
+        return set_error(RVK_ERR_INVALID, "grid solve (L2): unsupported geometry (R %d, nz %d)", R, nz);
+    }
+    const size_t smem = (size_t)rpc * nz * 12 + rpc;
     void* kargs[] = {const_cast<PersistArgs*>(&args), &bar, &rpc};
     auto go = [&](auto fn) -> rvk_status {
         // > 48 KB dynamic shared memory: per device and instantiation (idempotent)

@@ -43,12 +43,27 @@ def test_grid_solve_eligibility(ctx):
                               (2, 5, (128, 128), True),     # 16384: grid (cluster only <= 8 K rows)
                               (3, 27, (30, 30, 30), False),  # rows of 27 entries
                               (2, 5, (129, 128), True),
-                              (2, 5, (700, 700), False),   # > 148 x 3 x 1024 rows
+                              (2, 5, (660, 660), True),
+                              (2, 5, (700, 700), True),    # > 148 x 3 x 1024 rows: the L2 variant
+                              (2, 5, (778, 778), True),    # 4096 rows per CTA
+                              (2, 5, (780, 780), False),   # AUTO: fused above 4 K rows per CTA
                               (2, 5, (1024, 1024), False)]:
         A = rvk.DeviceCsr.laplacian(ctx, dim, pts, g)
         plan = rvk.CgPlan(ctx, A, max_it=2, mode="auto")
         assert bool(plan.flags() & rvk.PLAN_GRID) == want, g
+        l2 = g[0] * g[1] > 148 * 3072
+        assert bool(plan.flags() & rvk.PLAN_GRID_L2) == (want and l2), g
         plan.close()
+    # explicit PERSISTENT: the L2 grid solve up to 148 x 8 K rows
+    for g, want in [((780, 780), True), ((1024, 1024), True), ((1110, 1100), False)]:
+        A = rvk.DeviceCsr.laplacian(ctx, 2, 5, g)
+        plan = rvk.CgPlan(ctx, A, max_it=2, mode="persistent")
+        assert bool(plan.flags() & rvk.PLAN_GRID_L2) == want, g
+        plan.close()
+    A = rvk.DeviceCsr.laplacian(ctx, 2, 5, (700, 700))
+    plan = rvk.CgPlan(ctx, A, max_it=2, mode="auto", opts=rvk.OPT_NO_GRID_L2)
+    assert not plan.flags() & (rvk.PLAN_GRID | rvk.PLAN_GRID_L2)
+    plan.close()
     A = rvk.DeviceCsr.laplacian(ctx, 2, 5, (256, 256))
     plan = rvk.CgPlan(ctx, A, max_it=2, mode="persistent", opts=rvk.OPT_NO_GRID)
     assert not plan.flags() & rvk.PLAN_GRID
@@ -75,7 +90,30 @@ def permuted_spd(rng, grid):
     return O.Csr(n, n, np.cumsum(off), jj.astype(np.int32), vv)
 
 
-@pytest.mark.parametrize("seed,grid", [(0, (200, 200)), (1, (450, 440))])
+@pytest.mark.parametrize("spec", [(2, 5, (700, 700)), (2, 5, (1024, 1024)), (2, 9, (1024, 1000)),
+                                  (3, 7, (100, 100, 100)), (3, 7, (80, 80, 80)), (3, 27, (40, 40, 40))],
+                         ids=["5pt700", "5pt1024", "9pt1024x1000", "7pt100", "7pt80", "27pt40"])
+def test_grid_solve_l2_vs_oracle(ctx, spec):
+    """k_cg_grid_l2 (RVK_PLAN_GRID_L2): the matrix from the plan's global
+    k-major ELL copy, x / r / p in shared memory -- 3 K .. 8 K rows per CTA
+    (27-point rows exceed 9 entries: not eligible, the fused graph runs)."""
+    dim, pts, g = spec
+    Ah = O.build_laplacian(dim, pts, g)
+    b = O.rhs(Ah.n_rows)
+    A = rvk.DeviceCsr.laplacian(ctx, dim, pts, g)
+    for pc in ("jacobi", "none"):
+        for max_it, rtol in ((20, 0.0), (400, 1e-5)):
+            ref = O.cg_solve(Ah, b, max_it=max_it, rtol=rtol, pc=pc)
+            plan = rvk.CgPlan(ctx, A, max_it=max_it, rtol=rtol, pc=pc, mode="persistent")
+            assert bool(plan.flags() & rvk.PLAN_GRID_L2) == (pts != 27), plan.flags()
+            x, res = plan.solve_host(b)
+            check_cg_floor(res, x, ref)
+            x2, res2 = plan.solve_host(b)
+            assert np.array_equal(x, x2) and np.array_equal(res.hist, res2.hist)
+            plan.close()
+
+
+@pytest.mark.parametrize("seed,grid", [(0, (200, 200)), (1, (450, 440)), (2, (800, 790))])
 def test_grid_solve_irregular(ctx, seed, grid):
     rng = np.random.default_rng(seed)
     Ah = permuted_spd(rng, grid)
@@ -83,15 +121,18 @@ def test_grid_solve_irregular(ctx, seed, grid):
     A = rvk.DeviceCsr.from_host(ctx, n, n, Ah.off, Ah.cols, Ah.vals)
     b = O.rhs(n)
     ref = O.cg_solve(Ah, b, max_it=20)
-    plan = rvk.CgPlan(ctx, A, max_it=20, mode="auto")
+    plan = rvk.CgPlan(ctx, A, max_it=20, mode="persistent")
     assert plan.flags() & rvk.PLAN_GRID
+    assert bool(plan.flags() & rvk.PLAN_GRID_L2) == (n > 148 * 3072)
     x, res = plan.solve_host(b)
     check_cg_floor(res, x, ref)
 
 
-def test_grid_solve_zero_rhs_and_host_syncs(ctx):
-    A = rvk.DeviceCsr.laplacian(ctx, 2, 5, (256, 256))
-    plan = rvk.CgPlan(ctx, A, max_it=20, mode="auto")
+@pytest.mark.parametrize("g", [(256, 256), (1024, 1024)])
+def test_grid_solve_zero_rhs_and_host_syncs(ctx, g):
+    A = rvk.DeviceCsr.laplacian(ctx, 2, 5, g)
+    plan = rvk.CgPlan(ctx, A, max_it=20, mode="persistent")
+    assert plan.flags() & rvk.PLAN_GRID
     x0, r0 = plan.solve_host(np.zeros(A.n_rows))
     assert r0.iterations == 0 and not np.any(x0)
     b = rvk.DeviceArray.from_host(ctx, O.rhs(A.n_rows))
