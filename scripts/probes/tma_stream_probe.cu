@@ -94,11 +94,11 @@ __global__ void __launch_bounds__(544, 1)
     if (acc == 123456789) *sink = acc;
 }
 
-int main()
+int main(int argc, char** argv)
 {
     int sms;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    const long bytes = 24L << 30; // 24 GiB
+    const long bytes = (argc > 1 ? atol(argv[1]) : 24L) << 30; // GiB (default 24)
     char* buf;
     int*  sink;
     if (cudaMalloc(&buf, bytes) != cudaSuccess) { printf("alloc failed\n"); return 1; }
