@@ -43,6 +43,9 @@ CONFIGS = {
     "5pt768": (2, 5, (768, 768), "2D 5-point Laplacian 768x768 (latency sweep)"),
     "9pt1024": (2, 9, (1024, 1024), "2D 9-point Laplacian 1024x1024 (grid-solve study)"),
     "7pt100": (3, 7, (100, 100, 100), "3D 7-point Laplacian 100^3 (grid-solve study)"),
+    "7pt128": (3, 7, (128, 128, 128), "3D 7-point Laplacian 128^3 (fused persistent study)"),
+    "9pt2048": (2, 9, (2048, 2048), "2D 9-point Laplacian 2048x2048 (fused persistent study)"),
+    "5pt2048": (2, 5, (2048, 2048), "2D 5-point Laplacian 2048x2048 (fused persistent study)"),
 }
 METRIC = "20-iter Jacobi-CG solve time, achieved HBM GB/s vs peak, host syncs/iter"
 MAX_IT = 20

@@ -260,7 +260,11 @@ typedef struct {
  *   RVK_OPT_NO_GRID      PERSISTENT mode: no one-launch grid solve for mid-size
  *                        systems (the generic grid-barrier kernel instead)
  *   RVK_OPT_NO_GRID_L2   no grid solve over the global ELL copy (RVK_PLAN_GRID_L2):
- *                        AUTO runs those systems as the fused graph          */
+ *                        AUTO runs those systems as the fused graph
+ *   RVK_OPT_FPERSIST     AUTO: the fused persistent solve (RVK_PLAN_FPERSIST) for
+ *                        fixed-iteration solves past the grid solves (opt-in:
+ *                        measured level with / slower than the fused graph)
+ *   RVK_OPT_NO_FPERSIST  never the fused persistent solve                      */
 #define RVK_OPT_KEEP_WORK   1
 #define RVK_OPT_DINV_VECTOR 2
 #define RVK_OPT_Z_STORED    4
@@ -274,6 +278,8 @@ typedef struct {
 #define RVK_OPT_MARCH       1024
 #define RVK_OPT_NO_GRID     4096
 #define RVK_OPT_NO_GRID_L2  8192
+#define RVK_OPT_FPERSIST    16384
+#define RVK_OPT_NO_FPERSIST 32768
 
 typedef struct {
     int state;          /* rvk_cg_state: RUNNING here means "ran max_it"     */
@@ -346,6 +352,12 @@ rvk_status rvk_cg_solve_host_many(rvk_cg_plan plan, int nrhs, const double* cons
                                     the matrix from a plan-owned k-major ELL copy in global
                                     memory (L2-resident), x / r / p in shared memory
                                     (RVK_OPT_NO_GRID_L2 disables)                               */
+#define RVK_PLAN_FPERSIST   8192 /* PERSISTENT / AUTO plan runs the fused persistent solve: each
+                                    iteration's SpMV (the TMA ring of the fused K1, kept
+                                    across iterations) and update phases in ONE cooperative
+                                    launch, grid barriers fused with the reductions (explicit
+                                    PERSISTENT past the grid solves, or RVK_OPT_FPERSIST for
+                                    fixed-iteration AUTO solves; rows <= 9 entries)             */
 #define RVK_PLAN_Z_VIRTUAL  32  /* fused solve never stores z = d r (constant diagonal / no PC):
                                    the SpMV gathers r and forms d r (bit-identical;
                                    RVK_OPT_Z_STORED / RVK_OPT_Z_VIRTUAL override)               */

@@ -500,6 +500,14 @@ int update_grid(int64_t n)
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 // ---- stencil structure (plan time) -------------------------------------------
+// AUTO: fixed-iteration solves up to this many rows (past the grid solves)
+// would run as the fused persistent kernel (k_cg_fp).  0: measured slower
+// than (or level with) the fused graph almost everywhere -- 5-point 1024^2
+// 0.695 vs 0.588 ms, 9-point 1024^2 0.699 vs 0.696, 7-point 100^3 0.606 vs
+// 0.635, 128^3 1.24 vs 1.15, 9-point 2048^2 2.92 vs 2.35 --
+// so it is opt-in (RVK_OPT_FPERSIST) and the explicit PERSISTENT mode's
+// kernel past the grid solves
+constexpr int64_t            kFpAutoRows = 0;
 constexpr int                kDiagTable = 128;
 constexpr unsigned long long kDiagEmpty = ~0ull;
 
@@ -693,6 +701,7 @@ struct rvk_cg_plan_s {
     int           grid_rpc = 0, grid_ctas = 0; // PERSISTENT: the one-launch grid solve (k_cg_grid), rows per CTA
     unsigned*     gbar = nullptr;            // ... its arrival counter
     bool          grid_l2 = false;           // ... past the shared-memory ELL: k_cg_grid_l2 over ell
+    bool          fp      = false;           // PERSISTENT: the fused persistent solve (k_cg_fp)
     GridEll       ell{};
     void*         ell_buf = nullptr;
     int           maxlen  = 0;              // longest row
@@ -1179,6 +1188,12 @@ rvk_status enqueue_persistent(rvk_cg_plan P, const double* b, double* x)
                   P->z, P->p[0], P->p[1], P->w, P->hist, P->st, P->partials, P->cfg.max_it,
                   P->cfg.rtol, P->cfg.atol};
     P->launches = 1;
+    if (P->fp) {
+        const FpArgs f{P->A.n_rows, b, P->dinv, P->dconst, P->const_diag ? 0 : 1, x, P->r, P->z, P->p[0],
+                       P->p[1], P->w, P->hist, P->st, P->partials, P->gbar, P->cfg.max_it, P->cfg.rtol,
+                       P->cfg.atol};
+        return launch_fp(P->ctx->stream, P->sa, f);
+    }
     if (P->cluster)
         return launch_cluster(P->ctx->stream, a, P->cfg.pc == RVK_PC_JACOBI, P->cluster, P->maxlen);
     if (P->grid_rpc)
@@ -1438,11 +1453,22 @@ rvk_status rvk_cg_plan_create(rvk_ctx ctx, const rvk_csr* A, rvk_cg_config cfg, 
             if (P->grid_rpc) P->cluster = 0;
         }
     }
+    if ((cfg.mode == RVK_CG_MODE_AUTO || cfg.mode == RVK_CG_MODE_PERSISTENT) && !P->cluster && !P->grid_rpc &&
+        fp_eligible(P->sa) && !(cfg.opts & RVK_OPT_NO_FPERSIST)) {
+        // the fused persistent solve (k_cg_fp): explicit PERSISTENT always;
+        // AUTO for fixed-iteration solves up to kFpAutoRows (launch / tail
+        // latency bound there) or when RVK_OPT_FPERSIST asks
+        const bool fixed = cfg.rtol == 0.0 && cfg.atol == 0.0 && cfg.use_graph != 2;
+        P->fp = cfg.mode == RVK_CG_MODE_PERSISTENT ||
+                (fixed && (A->n_rows <= kFpAutoRows || (cfg.opts & RVK_OPT_FPERSIST)));
+    }
     if (cfg.mode == RVK_CG_MODE_AUTO) {
         // up to 16 K rows: the one-cluster DSMEM solve (one launch, cluster
         // barriers); up to ~450 K rows the one-launch grid solve (grid
-        // barriers, CSR in shared memory); above, the HBM-streaming fused graph
-        P->mode = (P->cluster || P->grid_rpc) ? RVK_CG_MODE_PERSISTENT : RVK_CG_MODE_FUSED;
+        // barriers, CSR in shared memory; ~606 K over a global ELL copy);
+        // fixed-iteration solves up to kFpAutoRows the fused persistent
+        // solve; above, the HBM-streaming fused graph
+        P->mode = (P->cluster || P->grid_rpc || P->fp) ? RVK_CG_MODE_PERSISTENT : RVK_CG_MODE_FUSED;
         // and up to 512 K rows the plain-block K1 (k_spmv_small: 256^2 5-point
         // solve 0.229 -> 0.211 ms; explicit FUSED keeps the TMA kernel unless
         // RVK_OPT_SMALL_K1 asks)
@@ -1535,6 +1561,7 @@ int rvk_cg_plan_flags(rvk_cg_plan P)
            ((P->mode == RVK_CG_MODE_PERSISTENT && P->cluster) ? RVK_PLAN_CLUSTER : 0) |
            ((P->mode == RVK_CG_MODE_PERSISTENT && P->grid_rpc) ? RVK_PLAN_GRID : 0) |
            ((P->mode == RVK_CG_MODE_PERSISTENT && P->grid_rpc && P->grid_l2) ? RVK_PLAN_GRID_L2 : 0) |
+           ((P->mode == RVK_CG_MODE_PERSISTENT && P->fp) ? RVK_PLAN_FPERSIST : 0) |
            (fold_setup(P, nullptr) ? RVK_PLAN_FOLD_SETUP : 0) |
            (P->zv ? RVK_PLAN_Z_VIRTUAL : 0) |
            ((P->march && !P->stencil && P->mode != RVK_CG_MODE_PERSISTENT) ? RVK_PLAN_MARCH : 0);

@@ -196,6 +196,31 @@ rvk_status build_grid_ell(cudaStream_t s, int64_t n, const int64_t* off, const i
 rvk_status launch_grid_solve(cudaStream_t s, const PersistArgs& args, unsigned* bar, bool jacobi,
                              int rpc, int ctas, int max_row_len, const GridEll* ell);
 
+// Fused persistent solve (rvk_cg_fp.cu): K1 / K2 phases of every iteration in
+// one cooperative launch that keeps the TMA SpMV ring across iterations.
+struct FpArgs {
+    int64_t       n;
+    const double* b;
+    const double* dinv;
+    double        dconst; // the constant Jacobi diagonal when dvec == 0
+    int           dvec;
+    double*       x;
+    double*       r;
+    double*       z;
+    double*       p0;
+    double*       p1;
+    double*       w;
+    double*       hist;
+    CgState*      st;
+    double*       partials; // 4 doubles per block
+    unsigned*     bar;      // arrival counter (zeroed per launch)
+    int           max_it;
+    double        rtol, atol;
+};
+struct SpmvArgs;
+bool       fp_eligible(const SpmvArgs& a);
+rvk_status launch_fp(cudaStream_t s, const SpmvArgs& a, const FpArgs& f);
+
 // After the last iteration (or an early exit): apply the updates DEFER K2s
 // left pending, in iteration order: x = ((x + a_0 p_0) + a_1 p_1) + ... .
 // pb: the q rotating p buffers; iteration j wrote pb[(j + 1) % q].  With the

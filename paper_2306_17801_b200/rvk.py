@@ -86,8 +86,8 @@ class CgConfig(C.Structure):
 OPT_KEEP_WORK, OPT_DINV_VECTOR, OPT_Z_STORED, OPT_Z_VIRTUAL = 1, 2, 4, 8
 OPT_NO_CLUSTER, OPT_SMALL_K1, OPT_MF_SIMPLE, OPT_NO_FOLD = 16, 32, 64, 128
 OPT_X_GROUP4, OPT_X_EACH = 256, 512
-OPT_MARCH, OPT_NO_GRID, OPT_NO_GRID_L2 = 1024, 4096, 8192
-PLAN_MARCH, PLAN_GRID, PLAN_GRID_L2 = 1024, 2048, 4096
+OPT_MARCH, OPT_NO_GRID, OPT_NO_GRID_L2, OPT_FPERSIST, OPT_NO_FPERSIST = 1024, 4096, 8192, 16384, 32768
+PLAN_MARCH, PLAN_GRID, PLAN_GRID_L2, PLAN_FPERSIST = 1024, 2048, 4096, 8192
 
 
 class Shard(C.Structure):
