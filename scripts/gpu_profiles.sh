@@ -18,6 +18,7 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_sp
 timeout 600 ncu --nvtx --nvtx-include "dcg.loopback_solve/" --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 44 --csv python scripts/shard_k1_probe.py > gpurun_out/shard_solve_dram.csv 2>&1; echo ncu shard solve rc $?
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_mf_tma -s 4 -c 1 -o gpurun_out/prof_mf -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline --operator stencil > /dev/null 2>&1; echo ncu mf rc $?
 timeout 600 ncu --set full --clock-control none -k regex:k_mf_tma -s 4 -c 1 -o gpurun_out/prof_mf_27pt -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline --operator stencil --config 27pt256 > /dev/null 2>&1; echo ncu mf 27pt rc $?
+timeout 600 ncu --set full --clock-control none -k regex:k_cg_grid_l2 -s 3 -c 1 -o gpurun_out/prof_gridl2_768 -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-strong --config 5pt768 > /dev/null 2>&1; echo ncu grid_l2 rc $?
 # summarise on the box (ncu CLI there), keep only the headline K1 report
 PROFILES_OUT=gpurun_out/profiles_out python scripts/make_profiles.py r02 > gpurun_out/make_profiles.log 2>&1; echo "make_profiles rc $?"
 for f in gpurun_out/prof_*.ncu-rep; do [ "$f" = gpurun_out/prof_k1.ncu-rep ] || rm -f "$f"; done

@@ -54,7 +54,8 @@ def main(tag="r02"):
                        "7pt768": {"k1": "prof_k1_768"},
                        "27pt256": {"k1": "prof_k1_27pt"}, "9pt4096": {"k1": "prof_k1_9pt"},
                        "7pt256_matrix_free": {"k1": "prof_mf"},
-                       "27pt256_matrix_free": {"k1": "prof_mf_27pt"}}.items():
+                       "27pt256_matrix_free": {"k1": "prof_mf_27pt"},
+                       "5pt768_grid_l2": {"solve": "prof_gridl2_768"}}.items():
         for k, f in files.items():
             path = os.path.join(G, f + ".ncu-rep")
             if os.path.exists(path):
