@@ -53,6 +53,7 @@ constexpr int    kSpmvUnroll        = 8;                   // default nonzeros p
 #define SPMV_FULL_FAST 1                                   // warp-uniform unmasked full batches
 #endif
 constexpr size_t kSpmvHeaderBytes   = 2048;                // barriers, meta, reduction scratch
+constexpr int64_t kSpmvBigTileRows  = 256ll * 1024 * 1024;  // make_spmv_args: 1024-row tiles above
 constexpr size_t kSpmvStageBudget   = 200 * 1024;          // dynamic smem for the ring
 constexpr size_t kSpmvMarchSmemMax  = 227 * 1024;          // sm_100 opt-in shared memory per block
 constexpr size_t kSpmvMarchSmem     = 223 * 1024;          // k_spmv_march: cache + ring (4 KB for op statics)
@@ -139,6 +140,12 @@ inline SpmvArgs make_spmv_args(const rvk_csr& A, int64_t max_row_len, const Spmv
         return true;
     };
     bool ok = false;
+    // very large systems (768^3: 453 M rows): 1024-row tiles in a 2-stage
+    // ring where they fit (5- / 7-point rows).  Measured, 7-point K1: 768^3
+    // 9.81 -> 9.56 ms (solve 254.4 -> 249.1 ms); 512^3 +0.3% and 256^3
+    // -0.4% (so only above 256 M rows); 256-row tiles were slower at 768^3
+    // and 256^3 (scripts/experiments/README.md, tile-geometry A/B)
+    if (A.n_rows > kSpmvBigTileRows) ok = fit(1024, 2);
     for (int need = 3; need >= 2 && !ok; --need)
         for (int R = 1024; R >= 32 && !ok; R /= 2) ok = fit(R, need);
     if (!ok) { // rows longer than a stage: every tile direct, small ring
