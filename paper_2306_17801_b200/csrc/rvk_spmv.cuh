@@ -53,7 +53,11 @@ constexpr int    kSpmvUnroll        = 8;                   // default nonzeros p
 #define SPMV_FULL_FAST 1                                   // warp-uniform unmasked full batches
 #endif
 constexpr size_t kSpmvHeaderBytes   = 2048;                // barriers, meta, reduction scratch
-constexpr int64_t kSpmvBigTileRows  = 256ll * 1024 * 1024;  // make_spmv_args: 1024-row tiles above
+#ifndef RVK_SPMV_BIG_TILE_ROWS
+#define RVK_SPMV_BIG_TILE_ROWS (256ll * 1024 * 1024)
+#endif
+constexpr int64_t kSpmvBigTileRows  = RVK_SPMV_BIG_TILE_ROWS;  // make_spmv_args: 1024-row tiles above
+constexpr int64_t kSpmvPrefetchMaxLead = 128 * 1024;         // ... leading-band L2 prefetch up to
 constexpr size_t kSpmvStageBudget   = 200 * 1024;          // dynamic smem for the ring
 constexpr size_t kSpmvMarchSmemMax  = 227 * 1024;          // sm_100 opt-in shared memory per block
 constexpr size_t kSpmvMarchSmem     = 223 * 1024;          // k_spmv_march: cache + ring (4 KB for op statics)
@@ -160,7 +164,12 @@ inline SpmvArgs make_spmv_args(const rvk_csr& A, int64_t max_row_len, const Spmv
     // (the ring must fit the dynamic shared memory launch_spmv configures)
     assert(a.smem_bytes() <= kSpmvHeaderBytes + kSpmvStageBudget);
     a.n_tiles = (A.n_rows + a.R - 1) / a.R;
-    a.pf      = (B && B->has_lead && B->lead_lo > 0) ? 1 : 0;
+    // the leading-edge L2 prefetch pays while the +plane band is near
+    // (2D grids, 3D planes <= 128 K rows: 256^3 7-point K1 318.9 -> 316.5 us,
+    // 27-point 960.8 -> 930.4 us); for larger planes it costs DRAM bandwidth
+    // (7-point K1 without it: 384^3 1074 -> 1062 us, 512^3 2735 -> 2541 us,
+    // 768^3 9554 -> 8566 us; scripts/experiments/README.md)
+    a.pf = (B && B->has_lead && B->lead_lo > 0 && B->lead_lo <= kSpmvPrefetchMaxLead) ? 1 : 0;
     a.pf_lo   = a.pf ? B->lead_lo : 0;
     a.pf_hi   = a.pf ? B->lead_hi : 0;
     // enough groups that every consumer thread owns a row of some tile
