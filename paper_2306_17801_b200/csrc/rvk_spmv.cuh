@@ -54,7 +54,7 @@ constexpr int    kSpmvUnroll        = 8;                   // default nonzeros p
 #endif
 constexpr size_t kSpmvHeaderBytes   = 2048;                // barriers, meta, reduction scratch
 #ifndef RVK_SPMV_BIG_TILE_ROWS
-#define RVK_SPMV_BIG_TILE_ROWS (256ll * 1024 * 1024)
+#define RVK_SPMV_BIG_TILE_ROWS (32ll * 1024 * 1024)
 #endif
 constexpr int64_t kSpmvBigTileRows  = RVK_SPMV_BIG_TILE_ROWS;  // make_spmv_args: 1024-row tiles above
 constexpr int64_t kSpmvPrefetchMaxLead = 128 * 1024;         // ... leading-band L2 prefetch up to
@@ -144,11 +144,11 @@ inline SpmvArgs make_spmv_args(const rvk_csr& A, int64_t max_row_len, const Spmv
         return true;
     };
     bool ok = false;
-    // very large systems (768^3: 453 M rows): 1024-row tiles in a 2-stage
-    // ring where they fit (5- / 7-point rows).  Measured, 7-point K1: 768^3
-    // 9.81 -> 9.56 ms (solve 254.4 -> 249.1 ms); 512^3 +0.3% and 256^3
-    // -0.4% (so only above 256 M rows); 256-row tiles were slower at 768^3
-    // and 256^3 (scripts/experiments/README.md, tile-geometry A/B)
+    // large systems (> 32 M rows, i.e. 3D planes past the leading-band
+    // prefetch's reach): 1024-row tiles in a 2-stage ring where they fit
+    // (5- / 7-point rows).  Measured, 7-point K1 without the prefetch:
+    // 384^3 1057 -> 1030 us, 512^3 2537 -> 2470 us, 768^3 8868 -> 8554 us;
+    // 256-row tiles were slower (scripts/experiments/README.md)
     if (A.n_rows > kSpmvBigTileRows) ok = fit(1024, 2);
     for (int need = 3; need >= 2 && !ok; --need)
         for (int R = 1024; R >= 32 && !ok; R /= 2) ok = fit(R, need);
